@@ -1,0 +1,176 @@
+"""Pin the CPU oracle before trusting it (CPU-only, no GPU).
+
+1. The C restatement (oracle/spct_oracle.c) reproduces every known answer the
+   reference's own tests assert (tests/golden/known_answers.json).
+2. It reproduces the committed outputs of the unmodified reference
+   (tests/golden/ref_vectors.npz) bit for bit.
+3. When oracle/_ref is built (always in the build container), it agrees with the
+   live reference on fresh seeded inputs, including every schedule kind.
+"""
+import numpy as np
+import pytest
+
+import oracle
+
+
+def test_known_ih_2x2(golden):
+    k = golden[0]["ih_2x2"]
+    t = oracle.build_ih(np.array(k["binmap"], np.uint16), k["bins"])
+    for kk, y, x, v in k["expect_at"]:
+        assert t[kk, y, x] == v
+    assert not t[:, 0, :].any() and not t[:, :, 0].any()
+
+
+def test_known_ih_1x1(golden):
+    k = golden[0]["ih_1x1"]
+    t = oracle.build_ih(np.array(k["binmap"], np.uint16), k["bins"])
+    nz = np.argwhere(t)
+    assert nz.tolist() == [e[:3] for e in k["nonzero"]]
+    assert t[5, 1, 1] == 1
+
+
+def test_known_quantize_and_gray(golden):
+    kn = golden[0]
+    q = kn["quantize_32"]
+    img = np.array([q["pixels"]], np.uint8)
+    assert oracle.quantize(img, q["bins"], q["lo"], q["hi"]).tolist() == [q["expect"]]
+    c = kn["quantize_clamp"]
+    out = oracle.quantize(img, c["bins"], c["lo"], c["hi"])
+    assert out[0, 0] == c["expect_first"] and out[0, -1] == c["expect_last"]
+    for bins, lo, hi in kn["quantize_contract"]["bad"]:
+        with pytest.raises(oracle.ContractError):
+            oracle.quantize(img, bins, lo, hi)
+    g = kn["grayscale"]
+    rgb = np.array(g["rgb"], np.uint8)
+    gray = oracle.to_grayscale(rgb[None, :, 0], rgb[None, :, 1], rgb[None, :, 2])
+    assert gray.tolist() == [g["expect"]]
+
+
+def test_known_hist_fixture(golden):
+    k = golden[0]["hist_fixture_0p7"]
+    img = np.array(k["image"], np.uint8)
+    t = oracle.build_ih(oracle.quantize(img, k["bins"]), k["bins"])
+    m = oracle.hist_distance_map(t, k["template"], k["kw"], k["kh"], k["p"])
+    x, y = k["at"]
+    assert abs(m[y, x] - k["expect"]) <= k["eps"] * max(1.0, k["expect"])
+
+
+def test_known_stats_and_memory(golden):
+    kn = golden[0]
+    for c in kn["schedule_stats"]["cases"]:
+        s = oracle.schedule_stats(*c["args"])
+        assert s.wavefront_iterations == c["iters"] and s.tile_count == c["tiles"]
+        if "eff_lo" in c:
+            assert c["eff_lo"] < s.scan_efficiency < c["eff_hi"]
+    for bad in kn["schedule_stats"]["bad"]:
+        with pytest.raises(oracle.ContractError):
+            oracle.schedule_stats(*bad)
+    for c in kn["estimate_memory"]["cases"]:
+        pad, raw, deg = oracle.estimate_memory(*c["args"])
+        if "raw" in c:
+            assert raw == c["raw"]
+        if "padded" in c:
+            assert pad == c["padded"]
+        assert deg == c["degenerate"] if "degenerate" in c else True
+    for bad in kn["estimate_memory"]["bad"]:
+        with pytest.raises(oracle.ContractError):
+            oracle.estimate_memory(*bad)
+
+
+def test_known_budget_reject(golden):
+    k = golden[0]["budget_reject"]
+    bm = oracle.random_binmap(k["w"], k["h"], k["bins"], 3)
+    with pytest.raises(oracle.ContractError):
+        oracle.validate_build(bm, k["bins"], budget=k["budget"])
+    oracle.validate_build(bm, k["bins"])
+    bad = bm.copy()
+    bad[0, 7] = k["bins"]
+    with pytest.raises(oracle.ContractError):
+        oracle.validate_build(bad, k["bins"])
+
+
+def test_oracle_matches_reference_vectors(golden):
+    vec = golden[1]
+    for key in [k for k in vec if k.endswith("_tensor")]:
+        bm = vec[key.replace("_tensor", "_bins")]
+        t = oracle.build_ih(bm, 16)
+        assert np.array_equal(t, vec[key]), key
+        t32 = oracle.build_ih(bm, 16, dtype=np.uint32)
+        assert np.array_equal(t32.astype(np.uint64), vec[key]), key
+    t = oracle.build_ih(vec["region_bins"], 32)
+    for r, want in zip(vec["region_rects"], vec["region_hists"]):
+        assert np.array_equal(oracle.region_histogram(t, *map(int, r)), want)
+    qb = oracle.quantize(vec["lmap_noise_img"], 8)
+    t = oracle.build_ih(qb, 8)
+    tmpl = np.full(8, 1.0 / 8)
+    # same operation order as likelihood.cpp:211-221 -> bit-identical maps
+    assert np.array_equal(oracle.hist_distance_map(t, tmpl, 7, 5, 2.0), vec["lmap_noise_p2"])
+    assert np.array_equal(oracle.hist_distance_map(t, tmpl, 7, 5, 1.0), vec["lmap_noise_p1"])
+    qb = oracle.quantize(vec["lmap_smooth_img"], 16)
+    t = oracle.build_ih(qb, 16)
+    th = vec["lmap_smooth_tmpl"]
+    assert np.array_equal(oracle.hist_distance_map(t, th, 20, 16, 1.0), vec["lmap_smooth_p1"])
+    assert np.array_equal(oracle.hist_distance_map(t, th, 20, 16, 3.0), vec["lmap_smooth_p3"])
+    # the tensor-free sliding-window map is the same arithmetic per window
+    assert np.array_equal(oracle.hist_match_map_direct(qb, 16, th, 20, 16, 1.0), vec["lmap_smooth_p1"])
+    gray = oracle.to_grayscale(vec["color_r"], vec["color_g"], vec["color_b"])
+    assert np.array_equal(gray, vec["color_gray"])
+    assert np.array_equal(oracle.quantize(gray, 32), vec["color_q32"])
+    assert np.array_equal(oracle.quantize(gray, 7, 30.0, 200.0), vec["color_q7_lohi"])
+
+
+def test_grayscale_quantize_integer_shortcuts():
+    """(r+g+b+1)//3 and (v*b)>>8 are exact restatements."""
+    s = np.arange(0, 766)
+    r = np.minimum(s, 255)
+    g = np.minimum(np.maximum(s - 255, 0), 255)
+    b = np.maximum(s - 510, 0)
+    gray = oracle.to_grayscale(r[None].astype(np.uint8), g[None].astype(np.uint8), b[None].astype(np.uint8))
+    assert np.array_equal(gray[0], ((s + 1) // 3).astype(np.uint8))
+    v = np.arange(256, dtype=np.uint8)[None]
+    for bins in [1, 2, 3, 7, 16, 32, 100, 128, 255, 256, 257, 1000, 1024, 65536]:
+        assert np.array_equal(oracle.quantize(v, bins)[0], ((v[0].astype(np.int64) * bins) >> 8).astype(np.uint16))
+
+
+def test_slab_partial_sums_recompose():
+    """Bin-slab sharding: per-slab partial p-sums add up to the full map."""
+    img = oracle.smooth_image(40, 30, 5)
+    qb = oracle.quantize(img, 12)
+    crop = qb[5:14, 8:19]
+    th = np.bincount(crop.reshape(-1), minlength=12).astype(np.float64) / crop.size
+    for p in (1.0, 2.0):
+        full = oracle.hist_match_map_direct(qb, 12, th, 11, 9, p)
+        parts = [oracle.hist_partial(qb, 12, th, 11, 9, p, k0, k0 + 4) for k0 in (0, 4, 8)]
+        got = oracle.hist_finalize(parts[0] + parts[1] + parts[2], 40, 30, 11, 9, p)
+        assert np.allclose(got, full, rtol=1e-12, atol=1e-12)
+
+
+ref = pytest.mark.skipif(not oracle.have_ref(), reason="oracle/_ref not built")
+
+
+@ref
+@pytest.mark.parametrize("w,h,bins", [(1, 1, 4), (5, 3, 16), (33, 31, 16), (70, 129, 16), (97, 61, 37)])
+def test_oracle_vs_live_reference_all_schedules(w, h, bins):
+    bm = oracle.random_binmap(w, h, bins, 4242 + w)
+    mine = oracle.build_ih(bm, bins)
+    for kind in (oracle.SEQUENTIAL, oracle.STS, oracle.CW_TIS, oracle.WF_TIS):
+        for tile, threads in ((32, 1), (64, 4)):
+            assert np.array_equal(oracle.RefTensor(bm, bins, kind, tile, threads).array(), mine)
+
+
+@ref
+def test_oracle_vs_live_reference_maps():
+    img = oracle.noise_image(57, 43, 3)
+    qb = oracle.ref_quantize(img, 9)
+    t = oracle.RefTensor(qb, 9)
+    crop = qb[10:21, 5:18]
+    th = np.bincount(crop.reshape(-1), minlength=9).astype(np.float64) / crop.size
+    mine_t = oracle.build_ih(qb, 9)
+    for p in (1.0, 1.5, 2.0):
+        want = t.hist_distance_map(th, 13, 11, p)
+        assert np.array_equal(oracle.hist_distance_map(mine_t, th, 13, 11, p), want)
+        assert np.array_equal(oracle.hist_match_map_direct(qb, 9, th, 13, 11, p), want)
+    with pytest.raises(oracle.ContractError):
+        t.hist_distance_map(th * 2, 13, 11, 1.0)
+    with pytest.raises(oracle.ContractError):
+        t.hist_distance_map(th, 13, 11, 0.5)
