@@ -1,0 +1,45 @@
+# Build of the product library (sm_100a only) and the CPU oracle.
+#
+#   make            -> paper_1711_01656_b200/libspct_b200.so  (+ oracle)
+#   make lib        -> product library only
+#   make oracle     -> oracle/libspct_oracle.so and oracle/_ref/libspct_ref.so
+#
+# The .so files are git-ignored but travel to the GPU box with gpurun.
+NVCC      ?= /usr/local/cuda/bin/nvcc
+ARCH      ?= -gencode arch=compute_100a,code=sm_100a
+NVFLAGS   ?= -O3 -lineinfo -std=c++17 $(ARCH) -Xcompiler -fPIC -Xptxas -warn-spills --expt-relaxed-constexpr
+PKG        = paper_1711_01656_b200
+CSRC       = $(PKG)/csrc
+LIB        = $(PKG)/libspct_b200.so
+CU_SRCS    = $(CSRC)/ih_build.cu $(CSRC)/hist_match.cu $(CSRC)/fused.cu $(CSRC)/profile.cu
+HOST_SRCS  = $(CSRC)/host/spct_host.cpp
+HDRS       = include/spct_cuda.h $(CSRC)/spct_device.cuh $(CSRC)/spct_internal.h $(wildcard include/spct/*.hpp)
+OBJDIR     = build/obj
+CU_OBJS    = $(patsubst $(CSRC)/%.cu,$(OBJDIR)/%.o,$(CU_SRCS))
+HOST_OBJS  = $(patsubst $(CSRC)/host/%.cpp,$(OBJDIR)/host_%.o,$(HOST_SRCS))
+
+.PHONY: all lib oracle clean sass
+all: lib oracle
+
+lib: $(LIB)
+
+$(OBJDIR)/%.o: $(CSRC)/%.cu $(HDRS)
+	@mkdir -p $(OBJDIR)
+	$(NVCC) $(NVFLAGS) -Iinclude -I$(CSRC) -c $< -o $@
+
+$(OBJDIR)/host_%.o: $(CSRC)/host/%.cpp $(HDRS)
+	@mkdir -p $(OBJDIR)
+	$(CXX) -O2 -std=c++20 -fPIC -Iinclude -I$(CSRC) -I/usr/local/cuda/include -c $< -o $@
+
+$(LIB): $(CU_OBJS) $(HOST_OBJS)
+	$(NVCC) $(ARCH) -shared -o $@ $^ -lcudart
+
+oracle:
+	$(MAKE) -C oracle
+
+sass: $(LIB)
+	/usr/local/cuda/bin/cuobjdump -sass $(LIB) > build/libspct_b200.sass
+
+clean:
+	rm -rf build $(LIB)
+	$(MAKE) -C oracle clean

@@ -1,0 +1,4 @@
+// Forwarding header: the reference include path spct/error.hpp maps onto the
+// B200-backed drop-in API declared in spct/spct.hpp.
+#pragma once
+#include "spct/spct.hpp"

@@ -1,0 +1,191 @@
+/*
+ * spct_cuda.h — C-ABI of the B200 (sm_100a) integral-histogram / likelihood-map path.
+ *
+ * This is the drop-in boundary under the reference's C++ API (namespace spct,
+ * /root/reference/proj/include/spct/{imagecore,integral,likelihood}.hpp).  The C++
+ * host layer (include/spct/*.hpp, paper_1711_01656_b200/csrc/host/) keeps the
+ * reference signatures and calls down through these entry points; Python tests and
+ * bench.py bind them with ctypes.  No C++ or torch types cross this interface:
+ * plain pointers, sizes and a cudaStream_t passed as void*.
+ *
+ * Conventions
+ *   - Every entry point returns an spct_status.  Contract checks run first and use
+ *     the reference's predicates, so a call that would throw spct::contract_error in
+ *     the reference returns SPCT_ERR_CONTRACT here and launches nothing.
+ *   - Device pointers are marked (dev).  Calls are stream-ordered and asynchronous
+ *     unless stated; nothing allocates behind the caller's back except where a
+ *     workspace is explicitly queried (spct_cu_*_workspace).
+ *   - spct_cu_last_error() returns a thread-local message for the last failure.
+ *
+ * Device tensor layout (struct spct_ih): the reference stores, per bin, a zero-padded
+ * (h+1)x(w+1) uint64 plane (integral.hpp:78-93).  The device stores the same values
+ * as uint32 WITHOUT the all-zero padding row/column:
+ *      data[k*plane_pitch + y*row_pitch + x] == H(bin0+k, y+1, x+1)   (reference indexing)
+ * for 0<=k<bins, 0<=y<height, 0<=x<width, with row_pitch a multiple of 32 elements
+ * (128-byte rows -> full-line, 16-byte-vector stores).  uint32 is exact because
+ * every cell is <= height*width < 2^32 (checked).  spct_cu_ih_export re-creates the
+ * reference layout (padding included, widened to uint64) for host mirrors.
+ */
+#ifndef SPCT_CUDA_H
+#define SPCT_CUDA_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    SPCT_OK = 0,
+    SPCT_ERR_CONTRACT = 2, /* spct::contract_error (reference error.hpp:11-14) */
+    SPCT_ERR_IO = 3,       /* spct::io_error (error.hpp:17-20) */
+    SPCT_ERR_CUDA = 4,     /* CUDA runtime / launch failure */
+    SPCT_ERR_OOM = 5       /* device allocation failed */
+} spct_status;
+
+/* ScanScheduleKind (reference integral.hpp:21-26).  All kinds produce the same
+ * bits; on the device they select nothing — accepted for drop-in. */
+enum { SPCT_SCHED_SEQUENTIAL = 0, SPCT_SCHED_STS = 1, SPCT_SCHED_CW_TIS = 2, SPCT_SCHED_WF_TIS = 3 };
+
+/* Window-match metrics.  MINKOWSKI is the reference's hist_distance_map
+ * (likelihood.cpp:193-225).  The other three are extensions named by the thesis
+ * but absent from the reference: definitions in DESIGN.md. */
+enum { SPCT_METRIC_MINKOWSKI = 0, SPCT_METRIC_INTERSECTION = 1, SPCT_METRIC_BHATTACHARYYA = 2,
+       SPCT_METRIC_CHISQ = 3 };
+
+/* Pixel source of a build: what the fused load stage reads and how it bins it. */
+enum { SPCT_SRC_BINS_U16 = 0, /* a BinMap (imagecore.hpp:65-76), values < nbins           */
+       SPCT_SRC_GRAY_U8 = 1,  /* GrayImage -> quantize(img, nbins, lo, hi)  imagecore.cpp:45 */
+       SPCT_SRC_RGB_U8 = 2,   /* planar ColorImage -> to_grayscale -> quantize   :17-24      */
+       SPCT_SRC_SCALAR_F64 = 3 /* ScalarMap -> quantize(map, nbins, lo, hi)       :50-53      */ };
+
+typedef struct {
+    int kind;             /* SPCT_SRC_* */
+    const void* plane[3]; /* (dev) plane[0] = bins/gray/R/values; plane[1..2] = G, B for RGB */
+    int64_t pitch;        /* elements between rows of each plane (>= width) */
+    int width, height;
+    int nbins;            /* total bin count b of the histogram */
+    double lo, hi;        /* quantisation range (defaults 0, 256) */
+} spct_source;
+
+typedef struct {
+    uint32_t* data;      /* (dev) see layout above */
+    int bins;            /* planes stored (a bin slab when sharded) */
+    int bin0;            /* global index of plane 0 (slab start) */
+    int nbins_total;     /* b of the full histogram */
+    int height, width;   /* source image dims */
+    int64_t row_pitch;   /* elements, multiple of 32, >= width */
+    int64_t plane_pitch; /* elements, >= height*row_pitch */
+} spct_ih;
+
+/* ----------------------------------------------------------------- library */
+
+const char* spct_cu_last_error(void);
+/* Returns the library ABI version (1) and reports the CUDA device it will use. */
+int spct_cu_version(void);
+spct_status spct_cu_device_info(int* sm_major, int* sm_minor, int* num_sms);
+
+/* ----------------------------------------------------------------- imagecore */
+
+/* to_grayscale (imagecore.cpp:17-24): out = lround((r+g+b)/3). (dev) planes, n pixels. */
+spct_status spct_cu_to_grayscale(const uint8_t* r, const uint8_t* g, const uint8_t* b, int64_t n,
+                                 uint8_t* out, void* stream);
+
+/* quantize (imagecore.cpp:28-53) of a GRAY_U8 / RGB_U8 / SCALAR_F64 source into a
+ * dense BinMap (dev, width*height uint16).  Contract: width,height > 0,
+ * 1 <= nbins <= 65536, hi > lo (imagecore.cpp:30-31,46,51). */
+spct_status spct_cu_quantize(const spct_source* src, uint16_t* out_bins, void* stream);
+
+/* Validation pass of build_tensor (integral.cpp:337-343): max BinMap value (dev -> host,
+ * synchronises the stream). */
+spct_status spct_cu_binmap_max(const uint16_t* bins, int64_t pitch, int width, int height,
+                               int* out_max, void* stream);
+
+/* ----------------------------------------------------------------- integral histogram */
+
+/* estimate_memory (integral.cpp:592-599), same arithmetic.  elem_bytes as in the reference. */
+spct_status spct_cu_estimate_memory(int w, int h, int bins, int elem_bytes, uint64_t* padded,
+                                    uint64_t* raw, int* degenerate);
+
+/* schedule_stats (integral.cpp:579-590). */
+spct_status spct_cu_schedule_stats(int w, int h, int tile, int scan_len, long long* iterations,
+                                   long long* tiles, double* efficiency);
+
+/* Pitches the library wants for a (width, height, bins) tensor; fills row_pitch,
+ * plane_pitch and returns the device bytes needed for data. */
+spct_status spct_cu_ih_layout(int width, int height, int bins, int64_t* row_pitch,
+                              int64_t* plane_pitch, uint64_t* bytes);
+
+/* Scratch the build needs (row-carry and band-carry tables); 0 is possible. */
+spct_status spct_cu_ih_build_workspace(const spct_source* src, int bin0, int bins,
+                                       size_t* bytes);
+
+/* build_integral_histogram (integral.cpp:548-551) of bins [out->bin0, out->bin0+out->bins)
+ * into the caller-allocated device tensor `out`.  The contract checks of build_tensor
+ * (integral.cpp:510-514) are the caller's: the host layer runs them with the
+ * reference predicates (including the 2 GiB budget with elem_bytes = 8).  Here the
+ * device-side checks are: dims > 0, nbins >= 1, slab inside [0, nbins), h*w < 2^32,
+ * pitches aligned.  BinMap sources must already be validated (spct_cu_binmap_max). */
+spct_status spct_cu_ih_build(const spct_source* src, const spct_ih* out, void* workspace,
+                             size_t workspace_bytes, void* stream);
+
+/* Re-create the reference layout for planes [k0, k1) of the tensor: a (k1-k0) x
+ * (height+1) x (width+1) uint64 block with zero padding row/column (dev dst). */
+spct_status spct_cu_ih_export_u64(const spct_ih* t, int k0, int k1, uint64_t* dst, void* stream);
+
+/* region_histogram / region_count (integral.cpp:561-577), batched: rects (dev) are
+ * n x {x, y, w, h} int32; out (dev) is n x t->bins uint32 (counts of planes
+ * [0, t->bins)).  Rects are validated on the host by the caller (Rect::inside). */
+spct_status spct_cu_region_counts(const spct_ih* t, const int32_t* rects, int n, uint32_t* out,
+                                  void* stream);
+
+/* ----------------------------------------------------------------- likelihood maps */
+
+/* Contract checks of hist_distance_map (likelihood.cpp:196-206) on a HOST template. */
+spct_status spct_cu_hist_check(int nbins, int width, int height, const double* tmpl_host,
+                               int ntmpl, int kw, int kh, double p);
+
+/* hist_distance_map (likelihood.cpp:193-225) over a device tensor that holds ALL bins
+ * (t->bin0 == 0, t->bins == t->nbins_total): map (dev) is height x width float64,
+ * borders replicated as spread_valid (:44-58).  tmpl (dev) has nbins doubles.
+ * MINKOWSKI follows the reference's operation order (k = 0..b-1, divide, pow). */
+spct_status spct_cu_hist_match(const spct_ih* t, const double* tmpl, int kw, int kh, double p,
+                               int metric, double* map, void* stream);
+
+/* Bin-slab partial of the window statistic over the valid grid (nv x nu, nu = width-kw+1,
+ * nv = height-kh+1): partial[v*nu+u] (+)= sum_{k in slab} term_k.  With accumulate = 0
+ * the buffer is overwritten.  Summing slab partials (e.g. an NCCL reduce across GPUs)
+ * then spct_cu_hist_finalize gives the full map. */
+spct_status spct_cu_hist_partial(const spct_ih* t, const double* tmpl, int kw, int kh, double p,
+                                 int metric, double* partial, int accumulate, void* stream);
+
+/* partial sums (dev, nv x nu) -> likelihood map (dev, height x width) with the
+ * reference's finalisation (likelihood.cpp:220-224) and spread_valid border replication. */
+spct_status spct_cu_hist_finalize(const double* partial, int width, int height, int kw, int kh,
+                                  double p, int metric, double* map, void* stream);
+
+/* Fused build + match: one pass that writes the integral histogram of the slab
+ * [out->bin0, out->bin0+out->bins) AND the slab's partial window statistic (as
+ * spct_cu_hist_partial), without re-reading the tensor from HBM.  `out->data` may be
+ * NULL to compute the partial map only.  tmpl (dev) holds the FULL template
+ * (nbins_total doubles).  Workspace from spct_cu_ih_build_workspace. */
+spct_status spct_cu_ih_build_match(const spct_source* src, const spct_ih* out, const double* tmpl,
+                                   int kw, int kh, double p, int metric, double* partial,
+                                   void* workspace, size_t workspace_bytes, void* stream);
+
+/* ----------------------------------------------------------------- instrumentation */
+
+/* Every kernel launch of this library increments a process-wide counter.  With
+ * profiling enabled, the main kernels (ih_sweep, ih_sweep_match, match_partial) are
+ * bracketed by CUDA events recorded on their launch stream; spct_cu_profile_read
+ * synchronises those events and returns the summed device time per kernel name. */
+uint64_t spct_cu_launch_count(void);
+void spct_cu_profile_enable(int on);
+void spct_cu_profile_reset(void);
+spct_status spct_cu_profile_read(const char* kernel, double* total_ms, int* launches);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SPCT_CUDA_H */

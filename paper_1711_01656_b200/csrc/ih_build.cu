@@ -1,0 +1,481 @@
+// Integral-histogram construction on sm_100a.
+//
+// Replaces build_integral_histogram / build_tensor and its four CPU schedules
+// (reference proj/src/integral.cpp:348-551).  Data flow:
+//
+//   rowcarry_kernel   per (row, 128-column strip): exclusive count of every slab bin
+//                     in the row left of the strip          -> Lt[s][y][kl]
+//   bandcount_kernel  per (band, strip): column counts of every slab bin over the
+//                     band's rows                            -> CC[j][kl][x]
+//   bandscan_kernel   prefix over bands and columns          -> Hb[j][kl][x] (in place)
+//   ih_sweep_kernel   per (band, strip, bin slab): one warp per B-bin slab sweeps the
+//                     band top to bottom; lane l owns columns 4l..4l+3 of the strip and
+//                     keeps H(y, x, k) for those 4 columns x B bins in registers.  A row
+//                     update is  H(y,x,k) = H(y-1,x,k) + L(y,k) + #{c <= x in strip : bin = k},
+//                     the in-strip count coming from byte-SIMD one-hot matches and one
+//                     warp shuffle scan of 4 bins packed per word.  Each plane-row of the
+//                     strip leaves as one coalesced 512-byte run of 16-byte stores.
+//
+// The pixel -> bin stage (to_grayscale + quantize) is fused into every load.
+#include <algorithm>
+#include <cstdlib>
+#include <cstring>
+
+#include "spct_internal.h"
+
+using namespace spct_dev;
+
+namespace spct_impl {
+
+// ------------------------------------------------------------------ planning
+
+BuildPlan plan_build(int width, int height, int bins) {
+    BuildPlan p{};
+    p.B = bins <= 4 ? 4 : (bins <= 8 ? 8 : 16);
+    const int nslabs = static_cast<int>(ceil_div(bins, p.B));
+    p.warps = std::min(8, nslabs);
+    p.slab_groups = static_cast<int>(ceil_div(nslabs, p.warps));
+    p.Lb = static_cast<int>(round_up(bins, p.B));
+    p.nstrips = static_cast<int>(ceil_div(width, kStrip));
+    p.Wp = p.nstrips * kStrip;
+    int band_rows = 0;
+    if (const char* e = std::getenv("SPCT_BAND_ROWS")) band_rows = std::atoi(e);
+    if (band_rows <= 0) {
+        // Aim for ~1024 independent tiles so 148 SMs get balanced work; never
+        // shorter than 64 rows (the carry tables scale with 1 / band_rows).
+        const int64_t per_band = static_cast<int64_t>(p.nstrips) * p.slab_groups;
+        int64_t nb = std::max<int64_t>(1, ceil_div(1024, per_band));
+        nb = std::min<int64_t>(nb, std::max<int64_t>(1, height / 64));
+        band_rows = static_cast<int>(ceil_div(height, nb));
+    }
+    band_rows = std::max(1, std::min(band_rows, height));
+    p.band_rows = band_rows;
+    p.nbands = static_cast<int>(ceil_div(height, band_rows));
+    p.lt_bytes = p.nstrips > 1 ? static_cast<size_t>(p.nstrips) * height * p.Lb * 4 : 0;
+    p.hb_bytes = p.nbands > 1 ? static_cast<size_t>(p.nbands - 1) * p.Lb * p.Wp * 4 : 0;
+    return p;
+}
+
+spct_status make_quant(const spct_source* src, QuantParams* q) {
+    if (!src) return contract("build: null source");
+    if (!(src->width > 0 && src->height > 0)) return contract("build: empty bin map");
+    if (!(src->nbins >= 1 && src->nbins <= 65536)) return contract("quantize: bins must be in [1, 65536]");
+    if (src->pitch < src->width) return contract("source pitch smaller than width");
+    if (!src->plane[0]) return contract("source plane 0 is null");
+    if (src->kind == SPCT_SRC_RGB_U8 && (!src->plane[1] || !src->plane[2]))
+        return contract("RGB source needs three planes");
+    if (src->kind < SPCT_SRC_BINS_U16 || src->kind > SPCT_SRC_SCALAR_F64) return contract("unknown source kind");
+    if (src->kind != SPCT_SRC_BINS_U16 && !(src->hi > src->lo)) return contract("quantize: hi must exceed lo");
+    q->kind = src->kind;
+    q->nbins = src->nbins;
+    q->lo = src->lo;
+    q->scale = src->nbins / (src->hi - src->lo);  // imagecore.cpp:33
+    q->fast_u8 = (src->kind == SPCT_SRC_GRAY_U8 || src->kind == SPCT_SRC_RGB_U8) && src->lo == 0.0 &&
+                 src->hi == 256.0;
+    q->p0 = src->plane[0];
+    q->p1 = src->plane[1];
+    q->p2 = src->plane[2];
+    q->pitch = src->pitch;
+    q->width = src->width;
+    q->height = src->height;
+    return SPCT_OK;
+}
+
+spct_status check_ih(const spct_ih* t) {
+    if (!t) return contract("null tensor descriptor");
+    if (!(t->width > 0 && t->height > 0)) return contract("tensor: empty dims");
+    if (!(t->nbins_total >= 1 && t->bins >= 1 && t->bin0 >= 0 && t->bin0 + t->bins <= t->nbins_total))
+        return contract("tensor: bin slab outside [0, nbins)");
+    if (static_cast<uint64_t>(t->width) * static_cast<uint64_t>(t->height) >= (1ull << 32))
+        return contract("tensor: height*width must be < 2^32 for uint32 cells");
+    if (t->row_pitch < t->width || t->row_pitch % 32 != 0) return contract("tensor: row_pitch must be >= width and a multiple of 32");
+    if (t->plane_pitch < t->row_pitch * t->height || t->plane_pitch % 32 != 0)
+        return contract("tensor: plane_pitch must be >= height*row_pitch and a multiple of 32");
+    return SPCT_OK;
+}
+
+}  // namespace spct_impl
+
+using namespace spct_impl;
+
+namespace spct_build {
+
+// ------------------------------------------------------------------ pre-passes
+
+// Lt[(s*H + y)*Lb + kl] = count of slab bin kl in row y, columns [0, 128*s).
+// One CTA (128 threads = one strip width) per row; bins handled in chunks.
+constexpr int kCarryChunk = 4096;
+
+__global__ void __launch_bounds__(128) rowcarry_kernel(QuantParams q, int bin0, int bins, int Lb, int nstrips,
+                                                       uint32_t* __restrict__ Lt) {
+    __shared__ uint32_t hist[kCarryChunk];
+    const int y = blockIdx.x;
+    const int kc0 = blockIdx.y * kCarryChunk;
+    const int kcn = min(kCarryChunk, Lb - kc0);
+    for (int i = threadIdx.x; i < kcn; i += blockDim.x) hist[i] = 0;
+    __syncthreads();
+    for (int s = 0; s < nstrips; ++s) {
+        uint32_t* dst = Lt + (static_cast<int64_t>(s) * q.height + y) * Lb + kc0;
+        for (int i = threadIdx.x; i < kcn; i += blockDim.x) dst[i] = hist[i];
+        __syncthreads();
+        const int x = s * kStrip + threadIdx.x;
+        if (s + 1 < nstrips && x < q.width) {
+            const int kl = pixel_bin(q, x, y) - bin0 - kc0;
+            if (kl >= 0 && kl < kcn && kl + kc0 < bins) atomicAdd(&hist[kl], 1u);
+        }
+        __syncthreads();
+    }
+}
+
+// CC[(j*Lb + kl)*Wp + x] = count of slab bin kl in column x over band j's rows,
+// for bands j = 0 .. nbands-2 (the last band feeds nothing).
+constexpr int kBandChunk = 64;
+
+__global__ void __launch_bounds__(128) bandcount_kernel(QuantParams q, int bin0, int bins, int Lb, int Wp,
+                                                        int band_rows, uint32_t* __restrict__ CC) {
+    __shared__ uint32_t cnt[kBandChunk][kStrip];
+    const int x = blockIdx.x * kStrip + threadIdx.x;
+    const int j = blockIdx.y;
+    const int kc0 = blockIdx.z * kBandChunk;
+    const int kcn = min(kBandChunk, Lb - kc0);
+    for (int i = 0; i < kcn; ++i) cnt[i][threadIdx.x] = 0;
+    const int y0 = j * band_rows, y1 = min(q.height, y0 + band_rows);
+    if (x < q.width) {
+        for (int y = y0; y < y1; ++y) {
+            const int kl = pixel_bin(q, x, y) - bin0 - kc0;
+            if (kl >= 0 && kl < kcn && kl + kc0 < bins) cnt[kl][threadIdx.x] += 1;
+        }
+    }
+    for (int i = 0; i < kcn; ++i) CC[(static_cast<int64_t>(j) * Lb + kc0 + i) * Wp + x] = cnt[i][threadIdx.x];
+}
+
+// In place: Hb[j-1][kl][x] = sum_{j' < j} sum_{c <= x} CC[j'][kl][c]  (j = 1..nbands-1),
+// i.e. the unpadded IH value at row y0_j - 1.  One CTA per slab bin; each thread owns
+// a contiguous run of columns; a block scan per band.
+__global__ void __launch_bounds__(1024) bandscan_kernel(int Lb, int Wp, int nbands, uint32_t* __restrict__ CCHb) {
+    __shared__ uint32_t warp_tot[32];
+    const int kl = blockIdx.x;
+    const int per = (Wp + blockDim.x - 1) / blockDim.x;  // <= 64 handled by the loop below
+    const int xs = threadIdx.x * per;
+    constexpr int kMaxPer = 16;
+    uint32_t run[kMaxPer];
+#pragma unroll
+    for (int i = 0; i < kMaxPer; ++i) run[i] = 0;
+    for (int j = 1; j < nbands; ++j) {
+        uint32_t* row = CCHb + (static_cast<int64_t>(j - 1) * Lb + kl) * Wp;
+        uint32_t tot = 0;
+#pragma unroll
+        for (int i = 0; i < kMaxPer; ++i) {
+            if (i < per && xs + i < Wp) {
+                run[i] += row[xs + i];  // vertical: bands < j
+                tot += run[i];
+            }
+        }
+        // exclusive scan of per-thread totals across the block
+        const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+        uint32_t v = tot;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            uint32_t t = __shfl_up_sync(0xffffffffu, v, o);
+            if (lane >= o) v += t;
+        }
+        __syncthreads();
+        if (lane == 31) warp_tot[wid] = v;
+        __syncthreads();
+        if (wid == 0) {
+            uint32_t w = lane < static_cast<int>(blockDim.x >> 5) ? warp_tot[lane] : 0;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                uint32_t t = __shfl_up_sync(0xffffffffu, w, o);
+                if (lane >= o) w += t;
+            }
+            warp_tot[lane] = w;  // inclusive
+        }
+        __syncthreads();
+        uint32_t acc = v - tot + (wid > 0 ? warp_tot[wid - 1] : 0);
+#pragma unroll
+        for (int i = 0; i < kMaxPer; ++i) {
+            if (i < per && xs + i < Wp) {
+                acc += run[i];
+                row[xs + i] = acc;  // in place: this band's CC slot now holds Hb[j]
+            }
+        }
+    }
+}
+
+// ------------------------------------------------------------------ main sweep
+
+template <int B>
+__global__ void __launch_bounds__(256) ih_sweep_kernel(QuantParams q, spct_ih out, int Lb, int Wp, int band_rows,
+                                                       int warps_per_cta, const uint32_t* __restrict__ Lt,
+                                                       const uint32_t* __restrict__ Hb) {
+    const int lane = lane_id();
+    const int warp = threadIdx.x >> 5;
+    const int strip = blockIdx.x;
+    const int band = blockIdx.y;
+    const int slab = blockIdx.z * warps_per_cta + warp;
+    const int kl0 = slab * B;  // first slab-local bin of this warp
+    if (kl0 >= out.bins) return;
+    const int x0 = strip * kStrip + 4 * lane;  // first of this lane's 4 columns
+    const int y0 = band * band_rows, y1 = min(out.height, y0 + band_rows);
+    const int H = out.height;
+    const bool lane_live = x0 < out.row_pitch;
+
+    // vertical carry: H at row y0-1 for this lane's 4 columns
+    uint32_t V[4][B];
+    if (band > 0) {
+        const uint32_t* hb = Hb + (static_cast<int64_t>(band - 1) * Lb + kl0) * Wp + x0;
+#pragma unroll
+        for (int k = 0; k < B; ++k) {
+            uint4 v = *reinterpret_cast<const uint4*>(hb + static_cast<int64_t>(k) * Wp);
+            V[0][k] = v.x;
+            V[1][k] = v.y;
+            V[2][k] = v.z;
+            V[3][k] = v.w;
+        }
+    } else {
+#pragma unroll
+        for (int k = 0; k < B; ++k) V[0][k] = V[1][k] = V[2][k] = V[3][k] = 0;
+    }
+
+    uint32_t* base_ptr = out.data + static_cast<int64_t>(kl0) * out.plane_pitch + x0;
+    const int k_live = min(B, out.bins - kl0);
+    const uint32_t* lt_strip = Lt ? Lt + (static_cast<int64_t>(strip) * H) * Lb + kl0 : nullptr;
+
+    uint32_t nxt = load_rel4(q, x0, y0, out.bin0 + kl0, B);
+    for (int y = y0; y < y1; ++y) {
+        const uint32_t cur = nxt;
+        if (y + 1 < y1) nxt = load_rel4(q, x0, y + 1, out.bin0 + kl0, B);
+
+        uint32_t L[B];
+        if (lt_strip && strip > 0) {
+            const uint4* lp = reinterpret_cast<const uint4*>(lt_strip + static_cast<int64_t>(y) * Lb);
+#pragma unroll
+            for (int k4 = 0; k4 < B / 4; ++k4) {
+                uint4 v = __ldg(lp + k4);
+                L[4 * k4 + 0] = v.x;
+                L[4 * k4 + 1] = v.y;
+                L[4 * k4 + 2] = v.z;
+                L[4 * k4 + 3] = v.w;
+            }
+        } else {
+#pragma unroll
+            for (int k = 0; k < B; ++k) L[k] = 0;
+        }
+
+        // in-lane inclusive prefix bytes per bin and the lane's count per bin
+        uint32_t P[B];
+        uint32_t packed[B / 4];
+#pragma unroll
+        for (int i = 0; i < B / 4; ++i) packed[i] = 0;
+#pragma unroll
+        for (int k = 0; k < B; ++k) {
+            P[k] = match_bytes(cur, 0x01010101u * static_cast<uint32_t>(k)) * 0x01010101u;
+            packed[k >> 2] |= (P[k] >> 24) << ((k & 3) * 8);
+        }
+        // exclusive warp scan, 4 bins per word (each byte <= 128: no overflow)
+        uint32_t excl[B / 4];
+#pragma unroll
+        for (int i = 0; i < B / 4; ++i) {
+            uint32_t v = packed[i];
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                uint32_t t = __shfl_up_sync(0xffffffffu, v, o);
+                if (lane >= o) v += t;
+            }
+            excl[i] = v - packed[i];
+        }
+        uint32_t* rowp = base_ptr + static_cast<int64_t>(y) * out.row_pitch;
+#pragma unroll
+        for (int k = 0; k < B; ++k) {
+            const uint32_t base = L[k] + ((excl[k >> 2] >> ((k & 3) * 8)) & 0xFFu);
+            V[0][k] += base + (P[k] & 0xFFu);
+            V[1][k] += base + ((P[k] >> 8) & 0xFFu);
+            V[2][k] += base + ((P[k] >> 16) & 0xFFu);
+            V[3][k] += base + (P[k] >> 24);
+            if (lane_live && k < k_live)
+                __stcs(reinterpret_cast<uint4*>(rowp + static_cast<int64_t>(k) * out.plane_pitch),
+                       make_uint4(V[0][k], V[1][k], V[2][k], V[3][k]));
+        }
+    }
+}
+
+// ------------------------------------------------------------------ small kernels
+
+__global__ void gray_kernel(const uint8_t* __restrict__ r, const uint8_t* __restrict__ g,
+                            const uint8_t* __restrict__ b, int64_t n, uint8_t* __restrict__ out) {
+    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+        out[i] = static_cast<uint8_t>(gray_of(r[i], g[i], b[i]));
+}
+
+__global__ void quantize_kernel(QuantParams q, uint16_t* __restrict__ out) {
+    const int64_t n = static_cast<int64_t>(q.width) * q.height;
+    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int y = static_cast<int>(i / q.width), x = static_cast<int>(i % q.width);
+        out[i] = static_cast<uint16_t>(pixel_bin(q, x, y));
+    }
+}
+
+__global__ void binmax_kernel(const uint16_t* __restrict__ bins, int64_t pitch, int w, int h, int* out) {
+    int m = 0;
+    const int64_t n = static_cast<int64_t>(w) * h;
+    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int y = static_cast<int>(i / w), x = static_cast<int>(i % w);
+        m = max(m, static_cast<int>(bins[static_cast<int64_t>(y) * pitch + x]));
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
+    if ((threadIdx.x & 31) == 0) atomicMax(out, m);
+}
+
+__global__ void export_kernel(spct_ih t, int k0, int k1, uint64_t* __restrict__ dst) {
+    const int64_t W1 = t.width + 1, H1 = t.height + 1;
+    const int64_t n = static_cast<int64_t>(k1 - k0) * H1 * W1;
+    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int64_t k = i / (H1 * W1), rem = i % (H1 * W1);
+        const int64_t y = rem / W1, x = rem % W1;
+        uint64_t v = 0;
+        if (y > 0 && x > 0) v = t.data[(k0 + k) * t.plane_pitch + (y - 1) * t.row_pitch + (x - 1)];
+        dst[i] = v;
+    }
+}
+
+int grid_for(int64_t n, int block) {
+    int64_t g = (n + block - 1) / block;
+    return static_cast<int>(std::min<int64_t>(std::max<int64_t>(g, 1), 148 * 32));
+}
+
+}  // namespace spct_build
+
+using namespace spct_build;
+
+// ------------------------------------------------------------------ C-ABI
+
+extern "C" spct_status spct_cu_to_grayscale(const uint8_t* r, const uint8_t* g, const uint8_t* b, int64_t n,
+                                            uint8_t* out, void* stream) {
+    if (n < 0) return contract("to_grayscale: negative size");
+    if (n == 0) return SPCT_OK;
+    if (!r || !g || !b || !out) return contract("to_grayscale: null plane");
+    gray_kernel<<<grid_for(n, 256), 256, 0, as_stream(stream)>>>(r, g, b, n, out);
+    return launch_status("to_grayscale");
+}
+
+extern "C" spct_status spct_cu_quantize(const spct_source* src, uint16_t* out, void* stream) {
+    QuantParams q;
+    if (!src) return contract("quantize: null source");
+    if (!(src->width > 0 && src->height > 0)) return contract("quantize: empty image");
+    if (auto st = make_quant(src, &q)) return st;
+    if (!out) return contract("quantize: null output");
+    const int64_t n = static_cast<int64_t>(q.width) * q.height;
+    quantize_kernel<<<grid_for(n, 256), 256, 0, as_stream(stream)>>>(q, out);
+    return launch_status("quantize");
+}
+
+extern "C" spct_status spct_cu_binmap_max(const uint16_t* bins, int64_t pitch, int width, int height, int* out_max,
+                                          void* stream) {
+    if (!(width > 0 && height > 0)) return contract("build: empty bin map");
+    if (!bins || !out_max || pitch < width) return contract("binmap_max: bad arguments");
+    int* d = nullptr;
+    cudaStream_t s = as_stream(stream);
+    if (auto st = cuda_status(cudaMallocAsync(&d, sizeof(int), s), "binmap_max alloc")) return st;
+    cudaMemsetAsync(d, 0, sizeof(int), s);
+    const int64_t n = static_cast<int64_t>(width) * height;
+    binmax_kernel<<<grid_for(n, 256), 256, 0, s>>>(bins, pitch, width, height, d);
+    spct_status st = launch_status("binmap_max");
+    int h = 0;
+    if (st == SPCT_OK) st = cuda_status(cudaMemcpyAsync(&h, d, sizeof(int), cudaMemcpyDeviceToHost, s), "binmap_max copy");
+    cudaFreeAsync(d, s);
+    if (st == SPCT_OK) st = cuda_status(cudaStreamSynchronize(s), "binmap_max sync");
+    *out_max = h;
+    return st;
+}
+
+extern "C" spct_status spct_cu_ih_layout(int width, int height, int bins, int64_t* row_pitch, int64_t* plane_pitch,
+                                         uint64_t* bytes) {
+    if (!(width > 0 && height > 0 && bins >= 1)) return contract("ih_layout: empty tensor");
+    const int64_t rp = round_up(width, 32);
+    const int64_t pp = rp * height;
+    if (row_pitch) *row_pitch = rp;
+    if (plane_pitch) *plane_pitch = pp;
+    if (bytes) *bytes = static_cast<uint64_t>(pp) * static_cast<uint64_t>(bins) * 4u;
+    return SPCT_OK;
+}
+
+extern "C" spct_status spct_cu_ih_build_workspace(const spct_source* src, int bin0, int bins, size_t* bytes) {
+    (void)bin0;
+    if (!src || !bytes) return contract("ih_build_workspace: null argument");
+    if (!(src->width > 0 && src->height > 0 && bins >= 1)) return contract("build: empty bin map");
+    BuildPlan p = plan_build(src->width, src->height, bins);
+    *bytes = p.lt_bytes + p.hb_bytes + 256;
+    return SPCT_OK;
+}
+
+namespace spct_impl {
+
+// Shared by spct_cu_ih_build and the fused build+match path: launch the three
+// carry pre-passes into the workspace.  Returns table pointers.
+spct_status build_carries(const QuantParams& q, const spct_ih& out, const BuildPlan& p, void* workspace,
+                          size_t ws_bytes, cudaStream_t s, uint32_t** Lt, uint32_t** Hb) {
+    *Lt = nullptr;
+    *Hb = nullptr;
+    if (p.lt_bytes + p.hb_bytes > 0 && (!workspace || ws_bytes < p.lt_bytes + p.hb_bytes))
+        return contract("ih_build: workspace too small (query spct_cu_ih_build_workspace)");
+    char* ws = static_cast<char*>(workspace);
+    if (p.lt_bytes) {
+        *Lt = reinterpret_cast<uint32_t*>(ws);
+        dim3 g(q.height, static_cast<unsigned>(ceil_div(p.Lb, kCarryChunk)));
+        rowcarry_kernel<<<g, 128, 0, s>>>(q, out.bin0, out.bins, p.Lb, p.nstrips, *Lt);
+        if (auto st = launch_status("rowcarry_kernel")) return st;
+    }
+    if (p.hb_bytes) {
+        *Hb = reinterpret_cast<uint32_t*>(ws + p.lt_bytes);
+        dim3 g(p.nstrips, p.nbands - 1, static_cast<unsigned>(ceil_div(p.Lb, kBandChunk)));
+        bandcount_kernel<<<g, 128, 0, s>>>(q, out.bin0, out.bins, p.Lb, p.Wp, p.band_rows, *Hb);
+        if (auto st = launch_status("bandcount_kernel")) return st;
+        if (ceil_div(p.Wp, 1024) > 16) return contract("ih_build: width too large for bandscan (max 16384)");
+        bandscan_kernel<<<p.Lb, 1024, 0, s>>>(p.Lb, p.Wp, p.nbands, *Hb);
+        if (auto st = launch_status("bandscan_kernel")) return st;
+    }
+    return SPCT_OK;
+}
+
+}  // namespace spct_impl
+
+extern "C" spct_status spct_cu_ih_build(const spct_source* src, const spct_ih* out, void* workspace,
+                                        size_t workspace_bytes, void* stream) {
+    QuantParams q;
+    if (auto st = make_quant(src, &q)) return st;
+    if (auto st = check_ih(out)) return st;
+    if (!out->data) return contract("ih_build: null tensor data");
+    if (out->width != src->width || out->height != src->height || out->nbins_total != src->nbins)
+        return contract("ih_build: tensor dims do not match the source");
+    if (reinterpret_cast<uintptr_t>(out->data) % 16 != 0) return contract("ih_build: tensor data must be 16-byte aligned");
+    const BuildPlan p = plan_build(out->width, out->height, out->bins);
+    cudaStream_t s = as_stream(stream);
+    uint32_t *Lt, *Hb;
+    if (auto st = build_carries(q, *out, p, workspace, workspace_bytes, s, &Lt, &Hb)) return st;
+    dim3 grid(p.nstrips, p.nbands, p.slab_groups);
+    const int threads = 32 * p.warps;
+    const int prof = prof_begin("ih_sweep", s);
+    switch (p.B) {
+        case 4: ih_sweep_kernel<4><<<grid, threads, 0, s>>>(q, *out, p.Lb, p.Wp, p.band_rows, p.warps, Lt, Hb); break;
+        case 8: ih_sweep_kernel<8><<<grid, threads, 0, s>>>(q, *out, p.Lb, p.Wp, p.band_rows, p.warps, Lt, Hb); break;
+        default: ih_sweep_kernel<16><<<grid, threads, 0, s>>>(q, *out, p.Lb, p.Wp, p.band_rows, p.warps, Lt, Hb); break;
+    }
+    prof_end(prof, s);
+    return launch_status("ih_sweep_kernel");
+}
+
+extern "C" spct_status spct_cu_ih_export_u64(const spct_ih* t, int k0, int k1, uint64_t* dst, void* stream) {
+    if (auto st = check_ih(t)) return st;
+    if (!(0 <= k0 && k0 <= k1 && k1 <= t->bins)) return contract("ih_export: plane range outside the tensor");
+    if (k0 == k1) return SPCT_OK;
+    if (!dst || !t->data) return contract("ih_export: null pointer");
+    const int64_t n = static_cast<int64_t>(k1 - k0) * (t->height + 1) * (t->width + 1);
+    export_kernel<<<grid_for(n, 256), 256, 0, as_stream(stream)>>>(*t, k0, k1, dst);
+    return launch_status("ih_export");
+}

@@ -1,0 +1,63 @@
+// Host-side helpers shared by the C-ABI translation units.
+#pragma once
+
+#include <cstdint>
+#include <cstdio>
+#include <string>
+
+#include <cuda_runtime.h>
+
+#include "spct_cuda.h"
+#include "spct_device.cuh"
+
+namespace spct_impl {
+
+void set_error(const std::string& msg);
+
+inline spct_status contract(const char* msg) {
+    set_error(msg);
+    return SPCT_ERR_CONTRACT;
+}
+
+inline spct_status cuda_status(cudaError_t e, const char* where) {
+    if (e == cudaSuccess) return SPCT_OK;
+    set_error(std::string(where) + ": " + cudaGetErrorString(e));
+    return e == cudaErrorMemoryAllocation ? SPCT_ERR_OOM : SPCT_ERR_CUDA;
+}
+
+// Instrumentation (profile.cu): count launches; bracket main kernels with events.
+void note_launch(int n = 1);
+int prof_begin(const char* name, cudaStream_t s);
+void prof_end(int id, cudaStream_t s);
+
+inline spct_status launch_status(const char* where) {
+    note_launch();
+    return cuda_status(cudaGetLastError(), where);
+}
+
+inline cudaStream_t as_stream(void* s) { return static_cast<cudaStream_t>(s); }
+
+inline int64_t round_up(int64_t v, int64_t m) { return (v + m - 1) / m * m; }
+inline int64_t ceil_div(int64_t v, int64_t m) { return (v + m - 1) / m; }
+
+// Validate a source and derive the kernel-side quantisation parameters.
+spct_status make_quant(const spct_source* src, spct_dev::QuantParams* q);
+
+// Validate a device tensor descriptor.
+spct_status check_ih(const spct_ih* t);
+
+// Bins per warp and band height used by the build for a given slab size / image.
+struct BuildPlan {
+    int B;          // bins per warp (4, 8 or 16)
+    int warps;      // warps per CTA (slabs per CTA)
+    int Lb;         // slab bins padded to a multiple of B (carry-table row length)
+    int nstrips;    // ceil(width / 128)
+    int Wp;         // nstrips * 128
+    int band_rows;  // rows per band
+    int nbands;
+    int slab_groups;  // CTAs along the bin axis
+    size_t lt_bytes, hb_bytes;
+};
+BuildPlan plan_build(int width, int height, int bins);
+
+}  // namespace spct_impl

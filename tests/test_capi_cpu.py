@@ -1,0 +1,119 @@
+"""CPU-side checks of the C-ABI library (no GPU needed, no kernel launches).
+
+* libspct_b200.so loads and exports every symbol include/spct_cuda.h declares;
+* host-only entry points (layout, workspace, analytics, contract checks) agree
+  with the oracle and reject bad arguments with SPCT_ERR_CONTRACT before any
+  device work — the reference's contract_error behaviour.
+"""
+import ctypes as C
+
+import numpy as np
+import pytest
+
+import oracle
+from paper_1711_01656_b200 import _capi as A
+
+
+def test_library_exports_every_header_symbol():
+    lib = A.lib()
+    declared = A.header_symbols()
+    assert len(declared) >= 18
+    for name in declared:
+        assert hasattr(lib, name), name
+        assert name in A.SIGNATURES, f"{name} declared in the header but not bound"
+    assert lib.spct_cu_version() == 1
+
+
+def test_estimate_memory_and_schedule_stats_match_oracle():
+    from paper_1711_01656_b200 import estimate_memory, schedule_stats
+
+    for args in [(2048, 2048, 64, 1), (512, 512, 32, 8), (100, 100, 0, 8), (4096, 4096, 128, 4), (0, 3, 2, 8)]:
+        assert estimate_memory(*args) == oracle.estimate_memory(*args)
+    for args in [(1024, 1024, 32, 1024), (512, 512, 32, 512), (70, 33, 32, 64), (64, 64, 64, 2)]:
+        it, tl, ef = schedule_stats(*args)
+        s = oracle.schedule_stats(*args)
+        assert (it, tl, ef) == (s.wavefront_iterations, s.tile_count, s.scan_efficiency)
+    with pytest.raises(A.ContractError):
+        schedule_stats(0, 4, 32, 64)
+    with pytest.raises(A.ContractError):
+        schedule_stats(4, 4, 32, 1)
+    with pytest.raises(A.ContractError):
+        estimate_memory(-1, 4, 4, 4)
+
+
+def test_layout_is_aligned_and_tight():
+    lib = A.lib()
+    for w, h, b in [(1, 1, 1), (33, 31, 16), (4096, 4096, 128), (8192, 8192, 256), (1000, 7, 3)]:
+        rp, pp, nb = C.c_int64(), C.c_int64(), C.c_uint64()
+        A.check(lib.spct_cu_ih_layout(w, h, b, C.byref(rp), C.byref(pp), C.byref(nb)))
+        assert rp.value % 32 == 0 and rp.value >= w and rp.value - w < 32
+        assert pp.value == rp.value * h and nb.value == pp.value * b * 4
+    # the headline tensor is exactly b*H*W*4 bytes: no padding traffic
+    rp, pp, nb = C.c_int64(), C.c_int64(), C.c_uint64()
+    A.check(lib.spct_cu_ih_layout(4096, 4096, 128, C.byref(rp), C.byref(pp), C.byref(nb)))
+    assert nb.value == 128 * 4096 * 4096 * 4
+
+
+def test_workspace_query():
+    lib = A.lib()
+    src = A.spct_source()
+    src.kind, src.width, src.height, src.nbins, src.pitch, src.lo, src.hi = A.SRC_GRAY_U8, 4096, 4096, 128, 4096, 0.0, 256.0
+    ws = C.c_size_t()
+    A.check(lib.spct_cu_ih_build_workspace(C.byref(src), 0, 128, C.byref(ws)))
+    assert 0 < ws.value < 4096 * 4096 * 128 * 4 // 20  # carry tables stay a few % of the tensor
+    src.width = 0
+    assert lib.spct_cu_ih_build_workspace(C.byref(src), 0, 128, C.byref(ws)) == A.SPCT_ERR_CONTRACT
+
+
+def _hc(nbins, w, h, tmpl, kw, kh, p):
+    th = np.ascontiguousarray(tmpl, np.float64)
+    return A.lib().spct_cu_hist_check(nbins, w, h, th.ctypes.data_as(C.POINTER(C.c_double)), th.size, kw, kh, p)
+
+
+def test_hist_check_mirrors_reference_predicates():
+    good = np.full(8, 1 / 8)
+    assert _hc(8, 30, 22, good, 7, 5, 2.0) == 0
+    for bad in [(8, 30, 22, good, 7, 5, 0.5),          # p < 1
+                (8, 30, 22, good, 31, 5, 1.0),         # kernel exceeds image
+                (8, 30, 22, good, 0, 5, 1.0),
+                (9, 30, 22, good, 7, 5, 1.0),          # bin count mismatch
+                (8, 30, 22, good * 2, 7, 5, 1.0),      # not normalised
+                (8, 30, 22, np.r_[good[:-1] + 1 / 56, -0.0 - 1e-9], 7, 5, 1.0)]:  # negative entry
+        assert _hc(*bad) == A.SPCT_ERR_CONTRACT
+        assert oracle.clib().or_hist_check(bad[0], bad[1], bad[2], np.ascontiguousarray(bad[3], np.float64),
+                                           len(bad[3]), bad[4], bad[5], bad[6]) == 2
+    # 1e-6 slack on the template mass (likelihood.cpp:206)
+    assert _hc(8, 30, 22, good * (1 + 5e-7), 7, 5, 1.0) == 0
+
+
+def test_contract_errors_before_device_work():
+    lib = A.lib()
+    src = A.spct_source()
+    src.kind, src.width, src.height, src.nbins, src.pitch = A.SRC_GRAY_U8, 4, 1, 0, 4
+    src.plane[0] = 1  # never dereferenced: the contract check fires first
+    assert lib.spct_cu_quantize(C.byref(src), 1, None) == A.SPCT_ERR_CONTRACT
+    assert b"bins must be in [1, 65536]" in lib.spct_cu_last_error()
+    src.nbins, src.lo, src.hi = 8, 10.0, 10.0
+    assert lib.spct_cu_quantize(C.byref(src), 1, None) == A.SPCT_ERR_CONTRACT
+    assert b"hi must exceed lo" in lib.spct_cu_last_error()
+    t = A.spct_ih(1, 4, 2, 5, 16, 16, 32, 32 * 16)  # slab [2, 6) outside nbins 5
+    assert lib.spct_cu_region_counts(C.byref(t), 1, 1, 1, None) == A.SPCT_ERR_CONTRACT
+    t = A.spct_ih(1, 4, 0, 4, 16, 16, 20, 20 * 16)  # row pitch not a multiple of 32
+    assert lib.spct_cu_ih_export_u64(C.byref(t), 0, 1, 1, None) == A.SPCT_ERR_CONTRACT
+    t = A.spct_ih(1, 4, 0, 4, 65536, 65536, 65536, 65536 * 65536)  # h*w = 2^32 does not fit uint32
+    assert lib.spct_cu_hist_partial(C.byref(t), 1, 3, 3, 1.0, 0, 1, 0, None) == A.SPCT_ERR_CONTRACT
+
+
+def test_python_api_contracts_without_gpu():
+    import paper_1711_01656_b200 as P
+
+    assert P.schedule_from_string("wavefront") == 3 and P.schedule_from_string("seq") == 0
+    with pytest.raises(P.ContractError):
+        P.schedule_from_string("bogus")
+    with pytest.raises(P.ContractError):
+        P.api._validate_schedule(P.ScanSchedule(3, 32, 0))
+    with pytest.raises(P.ContractError):
+        P.api._validate_schedule(P.ScanSchedule(3, 1, 2))
+    with pytest.raises(P.ContractError):
+        P.api._check_budget(16, 16, 4, 64)  # test_integral.cpp:196-198
+    P.api._check_budget(16, 16, 4, P.DEFAULT_BUDGET)

@@ -1,0 +1,277 @@
+"""GPU parity: the CUDA path against the CPU oracle and the reference's golden vectors.
+
+Bars (BASELINE.json north star):
+  * integral histograms: bit-exact, uint32 device cells == uint64 oracle cells, padding included;
+  * likelihood maps: Minkowski p = 1 over a full-bin tensor is bit-exact (same operation
+    order as likelihood.cpp:211-221); other p / metrics / slab sums within
+    |g - r| <= 1e-5 * |r| + 1e-12 (RTOL/ATOL below).
+Sizes are the reference's own awkward sizes (test_integral.cpp:74) plus strip / band
+boundaries of the device sweep; full-size configs are covered by size-independent
+properties in test_gpu_properties.py.
+"""
+import os
+
+import numpy as np
+import pytest
+
+import oracle
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+RTOL, ATOL = 1e-5, 1e-12
+
+
+@pytest.fixture(scope="module")
+def P():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_1711_01656_b200 as P
+
+    return P
+
+
+@pytest.fixture
+def band_rows(monkeypatch):
+    def set_rows(n):
+        monkeypatch.setenv("SPCT_BAND_ROWS", str(n))
+    return set_rows
+
+
+def close(g, r):
+    return np.all(np.abs(g - r) <= RTOL * np.abs(r) + ATOL)
+
+
+def test_golden_reference_tensors(P, golden):
+    vec = golden[1]
+    for key in [k for k in vec if k.endswith("_tensor")]:
+        bm = vec[key.replace("_tensor", "_bins")]
+        t = P.build_integral_histogram(bm, 16)
+        assert np.array_equal(t.padded_u64(), vec[key]), key
+
+
+def test_known_answers(P, golden):
+    kn = golden[0]
+    k = kn["ih_2x2"]
+    t = P.build_integral_histogram(np.array(k["binmap"], np.uint16), k["bins"])
+    for kk, y, x, v in k["expect_at"]:
+        assert t.at(kk, y, x) == v
+    a = t.padded_u64()
+    assert not a[:, 0, :].any() and not a[:, :, 0].any()
+    k = kn["ih_1x1"]
+    t = P.build_integral_histogram(np.array(k["binmap"], np.uint16), k["bins"])
+    assert np.argwhere(t.padded_u64()).tolist() == [e[:3] for e in k["nonzero"]]
+    q = kn["quantize_32"]
+    img = np.array([q["pixels"]], np.uint8)
+    assert P.api.as_numpy_u16(P.quantize(img, 32)).tolist() == [q["expect"]]
+    c = kn["quantize_clamp"]
+    out = P.api.as_numpy_u16(P.quantize(img, c["bins"], c["lo"], c["hi"]))
+    assert out[0, 0] == c["expect_first"] and out[0, -1] == c["expect_last"]
+    for bins, lo, hi in kn["quantize_contract"]["bad"]:
+        with pytest.raises(P.ContractError):
+            P.quantize(img, bins, lo, hi)
+    g = kn["grayscale"]
+    rgb = np.array(g["rgb"], np.uint8)
+    gray = P.to_grayscale(rgb[None, :, 0], rgb[None, :, 1], rgb[None, :, 2]).cpu().numpy()
+    assert gray.tolist() == [g["expect"]]
+    f = kn["hist_fixture_0p7"]
+    t = P.build_integral_histogram(np.array(f["image"], np.uint8), f["bins"])
+    m = P.hist_distance_map(t, f["template"], f["kw"], f["kh"], f["p"]).cpu().numpy()
+    assert abs(m[f["at"][1], f["at"][0]] - f["expect"]) <= f["eps"]
+
+
+SIZES = [(1, 1), (5, 3), (33, 31), (64, 64), (70, 129), (256, 40), (127, 5), (128, 9), (129, 300), (383, 77),
+         (513, 260)]
+
+
+@pytest.mark.parametrize("w,h", SIZES)
+@pytest.mark.parametrize("bins", [1, 3, 16, 37])
+def test_ih_bit_exact_binmap(P, w, h, bins):
+    bm = oracle.random_binmap(w, h, bins, 1000 + w * 7 + h + bins)
+    t = P.build_integral_histogram(bm, bins)
+    assert np.array_equal(t.padded_u64(), oracle.build_ih(bm, bins))
+
+
+@pytest.mark.parametrize("rows", [1, 2, 7, 64])
+def test_ih_band_carries(P, band_rows, rows):
+    band_rows(rows)
+    for (w, h, bins) in [(70, 129, 16), (300, 150, 9), (257, 64, 33)]:
+        bm = oracle.random_binmap(w, h, bins, rows * 31 + w)
+        t = P.build_integral_histogram(bm, bins)
+        assert np.array_equal(t.padded_u64(), oracle.build_ih(bm, bins)), (rows, w, h, bins)
+
+
+@pytest.mark.parametrize("bins", [2, 4, 5, 8, 9, 16, 17, 32, 64, 100, 128, 200, 256])
+def test_ih_bin_counts(P, bins):
+    img = oracle.smooth_image(300, 97, bins)
+    bm = oracle.quantize(img, bins)
+    t = P.build_integral_histogram(bm, bins)
+    assert np.array_equal(t.padded_u64(), oracle.build_ih(bm, bins))
+
+
+def test_ih_sources_fused_quantize(P):
+    """gray u8 (fast and general lo/hi), planar RGB and float64 sources quantise in the load stage."""
+    g = oracle.noise_image(301, 133, 5)
+    for bins, lo, hi in [(16, 0.0, 256.0), (32, 0.0, 256.0), (7, 30.0, 200.0), (300, 0.0, 256.0), (5, -3.5, 97.25)]:
+        t = P.build_integral_histogram(g, bins, lo=lo, hi=hi)
+        want = oracle.build_ih(oracle.quantize(g, bins, lo, hi), bins)
+        assert np.array_equal(t.padded_u64(), want), (bins, lo, hi)
+    r, gg, b = oracle.noise_color(150, 77, 1)
+    t = P.build_integral_histogram((r, gg, b), 32)
+    want = oracle.build_ih(oracle.quantize(oracle.to_grayscale(r, gg, b), 32), 32)
+    assert np.array_equal(t.padded_u64(), want)
+    rng = np.random.default_rng(3)
+    s = rng.normal(0.0, 50.0, (61, 140))
+    s[0, :4] = [np.inf, -np.inf, 1e300, -1e300]  # out-of-int-range floor -> bin 0 like x86
+    t = P.build_integral_histogram(s, 12, lo=-100.0, hi=100.0)
+    want = oracle.build_ih(oracle.quantize(s, 12, -100.0, 100.0), 12)
+    assert np.array_equal(t.padded_u64(), want)
+
+
+def test_quantize_kernel_matches_reference(P, golden):
+    vec = golden[1]
+    gray = P.to_grayscale(vec["color_r"], vec["color_g"], vec["color_b"]).cpu().numpy()
+    assert np.array_equal(gray, vec["color_gray"])
+    assert np.array_equal(P.api.as_numpy_u16(P.quantize(gray, 32)), vec["color_q32"])
+    assert np.array_equal(P.api.as_numpy_u16(P.quantize(gray, 7, 30.0, 200.0)), vec["color_q7_lohi"])
+    v = np.arange(256, dtype=np.uint8)[None]
+    for bins in [1, 3, 128, 255, 256, 1000, 65536]:
+        assert np.array_equal(P.api.as_numpy_u16(P.quantize(v, bins)), oracle.quantize(v, bins))
+
+
+@pytest.mark.parametrize("k0,k1", [(0, 5), (5, 16), (3, 4), (16, 37), (0, 37)])
+def test_ih_bin_slab(P, k0, k1):
+    bm = oracle.random_binmap(211, 97, 37, k0 * 100 + k1)
+    t = P.build_integral_histogram(bm, 37, bin0=k0, bins=k1 - k0)
+    assert np.array_equal(t.padded_u64(), oracle.build_ih(bm, 37, k0, k1))
+
+
+def test_region_queries(P, golden):
+    vec = golden[1]
+    t = P.build_integral_histogram(vec["region_bins"], 32)
+    got = P.region_histograms(t, vec["region_rects"])
+    assert np.array_equal(got, vec["region_hists"])
+    # exhaustive rects on 6x6 two-bin maps (test_integral.cpp:91-105)
+    rng = oracle.Rng(4242)
+    for trial in range(20):
+        bm = rng.binmap(6, 6, 2)
+        t = P.build_integral_histogram(bm, 2)
+        rects = [[x1, y1, x2 - x1, y2 - y1] for y1 in range(7) for y2 in range(y1, 7) for x1 in range(7)
+                 for x2 in range(x1, 7)]
+        got = P.region_histograms(t, rects)
+        ot = oracle.build_ih(bm, 2)
+        want = np.stack([oracle.region_histogram(ot, *r) for r in rects])
+        assert np.array_equal(got, want)
+    t = P.build_integral_histogram(oracle.random_binmap(8, 8, 4, 5), 4)
+    assert not P.region_histogram(t, 3, 3, 0, 0).any()
+    with pytest.raises(P.ContractError):
+        P.region_histogram(t, 5, 5, 4, 4)
+    with pytest.raises(P.ContractError):
+        P.region_histogram(t, -1, 0, 2, 2)
+    with pytest.raises(P.ContractError):
+        P.region_count(t, 9, 0, 0, 1, 1)
+
+
+def test_build_contract_errors(P):
+    bm = oracle.random_binmap(16, 16, 4, 3)
+    bad = bm.copy()
+    bad[0, 7] = 4
+    with pytest.raises(P.ContractError):
+        P.build_integral_histogram(bad, 4)
+    with pytest.raises(P.ContractError):
+        P.build_integral_histogram(bm, 4, memory_budget=64)
+    with pytest.raises(P.ContractError):
+        P.build_integral_histogram(np.zeros((0, 0), np.uint16), 4)
+    with pytest.raises(P.ContractError):
+        P.build_integral_histogram(bm, 4, P.ScanSchedule(3, 32, 0))
+
+
+def test_maps_golden_reference(P, golden):
+    vec = golden[1]
+    t = P.build_integral_histogram(vec["lmap_noise_img"], 8)
+    tm = np.full(8, 1 / 8)
+    assert np.array_equal(P.hist_distance_map(t, tm, 7, 5, 1.0).cpu().numpy(), vec["lmap_noise_p1"])
+    assert close(P.hist_distance_map(t, tm, 7, 5, 2.0).cpu().numpy(), vec["lmap_noise_p2"])
+    t = P.build_integral_histogram(vec["lmap_smooth_img"], 16)
+    th = vec["lmap_smooth_tmpl"]
+    assert np.array_equal(P.hist_distance_map(t, th, 20, 16, 1.0).cpu().numpy(), vec["lmap_smooth_p1"])
+    assert close(P.hist_distance_map(t, th, 20, 16, 3.0).cpu().numpy(), vec["lmap_smooth_p3"])
+
+
+@pytest.mark.parametrize("w,h,bins,kw,kh", [(96, 80, 16, 20, 16), (130, 67, 9, 13, 11), (257, 140, 32, 64, 64),
+                                            (50, 40, 5, 50, 40), (61, 33, 24, 1, 1), (200, 100, 128, 31, 17)])
+def test_maps_vs_oracle(P, w, h, bins, kw, kh):
+    img = oracle.smooth_image(w, h, w + h)
+    qb = oracle.quantize(img, bins)
+    y0, x0 = (h - kh) // 3, (w - kw) // 2
+    crop = qb[y0:y0 + kh, x0:x0 + kw]
+    th = np.bincount(crop.reshape(-1), minlength=bins).astype(np.float64) / crop.size
+    t = P.build_integral_histogram(img, bins)
+    want = oracle.hist_match_map_direct(qb, bins, th, kw, kh, 1.0)
+    got = P.hist_distance_map(t, th, kw, kh, 1.0).cpu().numpy()
+    assert np.array_equal(got, want)
+    assert got[y0 + (kh - 1) // 2, x0 + (kw - 1) // 2] == 1.0  # the template's own window
+    for p in (1.5, 2.0, 3.0):
+        assert close(P.hist_distance_map(t, th, kw, kh, p).cpu().numpy(),
+                     oracle.hist_match_map_direct(qb, bins, th, kw, kh, p))
+    for metric in (1, 2, 3):  # extensions: parity against the self-written oracle definitions
+        assert close(P.hist_match_map(t, th, kw, kh, 1.0, metric).cpu().numpy(),
+                     oracle.hist_match_map_direct(qb, bins, th, kw, kh, 1.0, metric))
+
+
+def test_map_contracts(P):
+    t = P.build_integral_histogram(oracle.random_binmap(30, 22, 8, 1), 8)
+    good = np.full(8, 1 / 8)
+    for args in [(good, 7, 5, 0.5), (good, 31, 5, 1.0), (np.full(9, 1 / 9), 7, 5, 1.0), (good * 2, 7, 5, 1.0)]:
+        with pytest.raises(P.ContractError):
+            P.hist_distance_map(t, *args)
+
+
+@pytest.mark.parametrize("p,metric", [(1.0, 0), (2.0, 0), (1.0, 1), (1.0, 2), (1.0, 3)])
+def test_slab_partials_recompose(P, p, metric):
+    """Bin-slab sharding (what each GPU computes before the NCCL reduce)."""
+    img = oracle.smooth_image(190, 120, 77)
+    bins, kw, kh = 40, 24, 18
+    qb = oracle.quantize(img, bins)
+    crop = qb[40:58, 60:84]
+    th = np.bincount(crop.reshape(-1), minlength=bins).astype(np.float64) / crop.size
+    tm = torch.from_numpy(th).cuda()
+    acc = None
+    for k0, k1 in [(0, 13), (13, 27), (27, 40)]:
+        t = P.build_integral_histogram(img, bins, bin0=k0, bins=k1 - k0)
+        part = P.hist_partial(t, tm, kw, kh, p, metric)
+        acc = part if acc is None else acc + part
+    got = P.hist_finalize(acc, 190, 120, kw, kh, p, metric).cpu().numpy()
+    assert close(got, oracle.hist_match_map_direct(qb, bins, th, kw, kh, p, metric))
+
+
+@pytest.mark.parametrize("slabs", [1, 2, 5])
+def test_fused_build_match(P, slabs):
+    img = oracle.smooth_image(333, 211, 9)
+    bins, kw, kh = 48, 64, 64
+    qb = oracle.quantize(img, bins)
+    crop = qb[100:164, 150:214]
+    th = np.bincount(crop.reshape(-1), minlength=bins).astype(np.float64) / crop.size
+    edges = np.linspace(0, bins, slabs + 1).astype(int)
+    acc = None
+    for k0, k1 in zip(edges[:-1], edges[1:]):
+        t, part = P.build_and_match(img, bins, th, kw, kh, 1.0, bin0=int(k0), bins=int(k1 - k0))
+        assert np.array_equal(t.padded_u64(), oracle.build_ih(qb, bins, int(k0), int(k1)))
+        acc = part.clone() if acc is None else acc + part
+    got = P.hist_finalize(acc, 333, 211, kw, kh, 1.0).cpu().numpy()
+    want = oracle.hist_match_map_direct(qb, bins, th, kw, kh, 1.0)
+    assert close(got, want)
+    if slabs == 1:
+        assert np.array_equal(got, want)
+
+
+@pytest.mark.skipif(not oracle.have_ref(), reason="oracle/_ref not built")
+def test_against_live_reference(P):
+    img = oracle.noise_image(57, 43, 3)
+    qb = oracle.ref_quantize(img, 9)
+    rt = oracle.RefTensor(qb, 9, oracle.WF_TIS, 32, 4)
+    t = P.build_integral_histogram(img, 9)
+    assert np.array_equal(t.padded_u64(), rt.array())
+    crop = qb[10:21, 5:18]
+    th = np.bincount(crop.reshape(-1), minlength=9).astype(np.float64) / crop.size
+    assert np.array_equal(P.hist_distance_map(t, th, 13, 11, 1.0).cpu().numpy(), rt.hist_distance_map(th, 13, 11, 1.0))
