@@ -1,13 +1,372 @@
-// Fused build + match entry point (placeholder schedule: build, then match on the
-// freshly written slab).  The single-pass kernel replaces this in DESIGN.md §4.
-#include "spct_internal.h"
+// Fused integral histogram + sliding-window matcher (one pass over the frame).
+//
+// Replaces build_integral_histogram followed by hist_distance_map (reference
+// integral.cpp:548-551, likelihood.cpp:193-225) without re-reading the tensor: the
+// window counts come from a vertical running histogram kept in shared memory.
+//
+// CTA = (128-column strip, band of rows, group of <= 128 bins); 8 warps x 16 bins.
+//   * V part (optional, `STORE`): the build sweep of sweep_common.cuh writes the
+//     integral-histogram rows of the strip (same bits as spct_cu_ih_build).
+//   * vc: for each of the CTA's bins and each of 256 "extended" columns
+//     [x0-128, x0+128) the count of that bin in the column over the last kh rows
+//     (u16 cells, two per 32-bit word, 64 KB).  Every row, thread t adds the entering
+//     pixel of column t and removes the pixel that left the window: two shared
+//     atomics per column, independent of the bin count.
+//   * G: per bin, the inclusive prefix of vc along the 256 columns (u16 pairs, lane l
+//     owns columns 4l..4l+3 of each half; in-lane IMAD prefix + one 16-bit-packed warp
+//     scan).  The count of the kw x kh window whose bottom-right pixel is (e, y) is
+//     G(e) - G(e - kw), read back through a per-warp staging row.
+//   * distance: Minkowski p = 1 / intersection with an integral template
+//     (s_k = T t_k in Z, the template-crop case) is exact integer arithmetic:
+//     sum_k |c_k - s_k| = C + S - 2 sum_k min(c_k, s_k), with min.u16x2 on packed
+//     pairs.  Every other metric / p evaluates likelihood.cpp's per-bin term in FP64.
+//   * the 8 warps' per-window partials are combined in a fixed order through shared
+//     memory and written as one partial-map row (float64) per CTA row.
+#include <algorithm>
+#include <cmath>
 
+#include "spct_internal.h"
+#include "sweep_common.cuh"
+
+using namespace spct_dev;
 using namespace spct_impl;
+
+namespace spct_fused {
+
+constexpr int kWarps = 8;
+constexpr int kB = 16;
+constexpr int kGroupBins = kWarps * kB;  // 128 bins per CTA
+constexpr int kExt = 256;                // extended columns per CTA (128 halo + 128 strip)
+constexpr int kVcWords = kExt / 2;       // u16 pairs per bin row
+
+struct FusedParams {
+    int kw, kh, nu, nv;
+    int metric, p_kind, T_pow2, accumulate;
+    double p, T, invT;
+    int group0;                  // first slab-local bin of this launch's bin group
+    const double* tmpl;          // full template, indexed by global bin
+    const uint32_t* prep;        // [0] fast flag, [1..] srep (slab-local), then S per group (int64)
+    const long long* S_group;    // sum of integral s_k per 128-bin group
+    double* partial;
+};
+
+__device__ __forceinline__ uint32_t min_u16x2(uint32_t a, uint32_t b) {
+    uint32_t r;
+    asm("min.u16x2 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(b));
+    return r;
+}
+
+// Per-bin term of the general path (same arithmetic as hist_match.cu bin_term).
+__device__ __forceinline__ double general_term(uint32_t c, double t, const FusedParams& f) {
+    const double cd = static_cast<double>(c);
+    const double q = f.T_pow2 ? __dmul_rn(cd, f.invT) : __ddiv_rn(cd, f.T);
+    switch (f.metric) {
+        case SPCT_METRIC_MINKOWSKI: {
+            const double a = fabs(__dsub_rn(q, t));
+            if (f.p_kind == 1) return a;
+            if (f.p_kind == 2) return __dmul_rn(a, a);
+            return pow(a, f.p);
+        }
+        case SPCT_METRIC_INTERSECTION:
+            return fmin(q, t);
+        case SPCT_METRIC_BHATTACHARYYA:
+            return sqrt(__dmul_rn(q, t));
+        default: {
+            const double den = __dadd_rn(q, t);
+            if (!(den > 0.0)) return 0.0;
+            const double df = __dsub_rn(q, t);
+            return __ddiv_rn(__dmul_rn(df, df), den);
+        }
+    }
+}
+
+// Template prep: s_k = T t_k; fast path iff every s_k of the slab is an integer up to
+// FP noise (then the integer formula is exact to ~1e-15) and the metric allows it.
+__global__ void prep_kernel(const double* __restrict__ tmpl, int bin0, int bins, double T, int fast_metric,
+                            uint32_t* __restrict__ prep, long long* __restrict__ S_group, int ngroups) {
+    __shared__ int ok;
+    if (threadIdx.x == 0) ok = fast_metric;
+    __syncthreads();
+    for (int k = threadIdx.x; k < bins; k += blockDim.x) {
+        const double s = T * tmpl[bin0 + k];
+        const double n = rint(s);
+        const bool integral = fabs(s - n) <= 8.0 * 2.220446049250313e-16 * fmax(1.0, fabs(s)) && n >= 0.0 && n <= T;
+        if (!integral) ok = 0;
+        const uint32_t ni = integral ? static_cast<uint32_t>(n) : 0u;
+        prep[1 + k] = ni | (ni << 16);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) prep[0] = ok;
+    for (int g = threadIdx.x; g < ngroups; g += blockDim.x) {
+        long long acc = 0;
+        for (int k = g * kGroupBins; k < min(bins, (g + 1) * kGroupBins); ++k) acc += prep[1 + k] & 0xFFFFu;
+        S_group[g] = acc;
+    }
+}
+
+template <bool STORE>
+__global__ void __launch_bounds__(256, 1) sweep_match_kernel(QuantParams q, spct_ih out, int Lb, int Wp,
+                                                             int band_rows, const uint32_t* __restrict__ Lt,
+                                                             const uint32_t* __restrict__ Hb, FusedParams f) {
+    extern __shared__ uint4 smem_raw[];
+    uint32_t* vc = reinterpret_cast<uint32_t*>(smem_raw);       // [128 bins][128 words]
+    uint32_t* gbuf = vc + kGroupBins * kVcWords;                   // [8 warps][128 words]
+    double* red = reinterpret_cast<double*>(gbuf + kWarps * kVcWords);  // [2][8][128]
+    __shared__ int s_fast;
+
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int strip = blockIdx.x, band = blockIdx.y;
+    const int g0 = f.group0;                               // slab-local first bin of the CTA
+    const int nb_cta = min(kGroupBins, out.bins - g0);
+    const int nwarps_live = (nb_cta + kB - 1) / kB;
+    const int kl0 = g0 + warp * kB;                        // warp's first slab-local bin
+    const bool warp_live = warp < nwarps_live;
+    const int k_live = min(kB, out.bins - kl0);
+    const int xs = strip * kStrip;                         // strip's first column
+    const int xl = xs + 4 * lane;                          // lane's first strip column
+    const int H = out.height, W = out.width;
+    const int y0 = band * band_rows, y1 = min(H, y0 + band_rows);
+    const int ystart = max(0, y0 - f.kh + 1);
+
+    if (tid == 0) s_fast = f.prep[0];
+    for (int i = tid; i < kGroupBins * kVcWords; i += blockDim.x) vc[i] = 0;
+
+    uint32_t V[4][kB];
+    if (STORE) {
+        if (warp_live) vpart_init<kB>(V, Hb, band, Lb, kl0, Wp, xl);
+    }
+    uint32_t* base_ptr = STORE ? out.data + static_cast<int64_t>(kl0) * out.plane_pitch + xl : nullptr;
+    const uint32_t* lt_strip = (Lt && strip > 0) ? Lt + static_cast<int64_t>(strip) * H * Lb + kl0 : nullptr;
+    const bool lane_live = xl < out.row_pitch;
+    __syncthreads();
+    const bool fast = s_fast != 0;
+    const double S = fast ? static_cast<double>(f.S_group[g0 / kGroupBins]) : 0.0;
+
+    // pending row for the deferred cross-warp combine
+    int pend_y = -1;
+    auto combine = [&](int yy) {
+        // thread t < 128: window with right edge at strip column t, bottom row yy
+        if (tid < kStrip) {
+            const int e = xs + tid;
+            const int u = e - f.kw + 1, v = yy - f.kh + 1;
+            if (u >= 0 && e < W) {
+                const double* rb = red + (yy & 1) * (kWarps * kStrip);
+                double term;
+                if (fast) {
+                    long long I = 0, C = 0;
+                    for (int w = 0; w < nwarps_live; ++w) {
+                        const uint32_t x = reinterpret_cast<const uint32_t*>(rb + w * kStrip)[2 * tid];
+                        I += x & 0xFFFFu;
+                        C += x >> 16;
+                    }
+                    term = f.metric == SPCT_METRIC_INTERSECTION
+                               ? static_cast<double>(I) * f.invT
+                               : static_cast<double>(C + static_cast<long long>(S) - 2 * I) * f.invT;
+                } else {
+                    term = 0.0;
+                    for (int w = 0; w < nwarps_live; ++w) term = __dadd_rn(term, rb[w * kStrip + tid]);
+                }
+                double* dst = f.partial + static_cast<int64_t>(v) * f.nu + u;
+                *dst = f.accumulate ? __dadd_rn(*dst, term) : term;
+            }
+        }
+    };
+
+    for (int y = ystart; y < y1; ++y) {
+        __syncthreads();  // A: previous row's vc / red reads are done
+        if (pend_y >= 0) {
+            combine(pend_y);
+            pend_y = -1;
+        }
+        {   // vertical running histogram: add row y, remove row y - kh
+            const int x = xs - kStrip + tid;
+            if (x >= 0 && x < W) {
+                const uint32_t inc = 1u << (16 * (tid & 1));
+                const int bn = pixel_bin(q, x, y) - out.bin0 - g0;
+                if (static_cast<unsigned>(bn) < static_cast<unsigned>(nb_cta)) atomicAdd(&vc[bn * kVcWords + (tid >> 1)], inc);
+                const int yo = y - f.kh;
+                if (yo >= 0) {
+                    const int bo = pixel_bin(q, x, yo) - out.bin0 - g0;
+                    if (static_cast<unsigned>(bo) < static_cast<unsigned>(nb_cta)) atomicSub(&vc[bo * kVcWords + (tid >> 1)], inc);
+                }
+            }
+        }
+        __syncthreads();  // B: vc holds rows (y - kh, y]
+        if (y < y0) continue;  // pre-roll rows only feed vc
+
+        if (STORE && warp_live) {
+            const uint32_t cur = load_rel4(q, xl, y, out.bin0 + kl0, kB);
+            vpart_row<kB>(V, cur, lt_strip ? lt_strip + static_cast<int64_t>(y) * Lb : nullptr, lane,
+                          base_ptr + static_cast<int64_t>(y) * out.row_pitch, out.plane_pitch, lane_live, k_live);
+        }
+        if (y < f.kh - 1) continue;  // no window ends on this row yet
+
+        double* rb = red + (y & 1) * (kWarps * kStrip) + warp * kStrip;
+        if (warp_live) {
+            uint32_t* gb = gbuf + warp * kVcWords;
+            uint32_t I0 = 0, I1 = 0, C0 = 0, C1 = 0;
+            double acc[4] = {0.0, 0.0, 0.0, 0.0};
+            const int idx = kStrip + 4 * lane - f.kw;  // first ext cell of G(e - kw)
+            for (int k = 0; k < kB; ++k) {
+                if (k >= k_live) break;
+                const uint32_t* vrow = vc + (warp * kB + k) * kVcWords;
+                const uint2 wa = *reinterpret_cast<const uint2*>(vrow + 2 * lane);
+                const uint2 wb = *reinterpret_cast<const uint2*>(vrow + 64 + 2 * lane);
+                uint32_t a0 = wa.x * 0x10001u;
+                uint32_t a1 = wa.y * 0x10001u + __byte_perm(a0, 0, 0x3232);
+                uint32_t b0 = wb.x * 0x10001u;
+                uint32_t b1 = wb.y * 0x10001u + __byte_perm(b0, 0, 0x3232);
+                const uint32_t tot = __byte_perm(a1, b1, 0x7632);  // {sum(a), sum(b)} as u16 fields
+                uint32_t inc = tot;
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    const uint32_t t = __shfl_up_sync(0xffffffffu, inc, o);
+                    if (lane >= o) inc += t;
+                }
+                const uint32_t ex = inc - tot;
+                const uint32_t T1 = __shfl_sync(0xffffffffu, inc, 31) & 0xFFFFu;
+                const uint32_t ba = __byte_perm(ex, 0, 0x1010);
+                const uint32_t bb = __byte_perm(ex, 0, 0x3232) + T1 * 0x10001u;
+                a0 += ba;
+                a1 += ba;
+                b0 += bb;
+                b1 += bb;
+                *reinterpret_cast<uint2*>(gb + 2 * lane) = make_uint2(a0, a1);
+                *reinterpret_cast<uint2*>(gb + 64 + 2 * lane) = make_uint2(b0, b1);
+                __syncwarp();
+                uint32_t p0, p1;
+                if ((idx & 1) == 0) {
+                    p0 = gb[idx >> 1];
+                    p1 = gb[(idx >> 1) + 1];
+                } else {
+                    const uint32_t q0 = gb[idx >> 1], q1 = gb[(idx >> 1) + 1], q2 = gb[(idx >> 1) + 2];
+                    p0 = __byte_perm(q0, q1, 0x5432);
+                    p1 = __byte_perm(q1, q2, 0x5432);
+                }
+                __syncwarp();
+                const uint32_t c0 = b0 - p0, c1 = b1 - p1;  // window counts {j=0, j=1}, {j=2, j=3}
+                if (fast) {
+                    const uint32_t s = f.prep[1 + kl0 + k];
+                    I0 += min_u16x2(c0, s);
+                    I1 += min_u16x2(c1, s);
+                    C0 += c0;
+                    C1 += c1;
+                } else {
+                    const double t = __ldg(f.tmpl + out.bin0 + kl0 + k);
+                    acc[0] = __dadd_rn(acc[0], general_term(c0 & 0xFFFFu, t, f));
+                    acc[1] = __dadd_rn(acc[1], general_term(c0 >> 16, t, f));
+                    acc[2] = __dadd_rn(acc[2], general_term(c1 & 0xFFFFu, t, f));
+                    acc[3] = __dadd_rn(acc[3], general_term(c1 >> 16, t, f));
+                }
+            }
+            if (fast) {
+                // per window: I | C << 16 in the low word of the slot
+                uint32_t* rw = reinterpret_cast<uint32_t*>(rb);
+                rw[2 * (4 * lane + 0)] = (I0 & 0xFFFFu) | (C0 << 16);
+                rw[2 * (4 * lane + 1)] = (I0 >> 16) | (C0 & 0xFFFF0000u);
+                rw[2 * (4 * lane + 2)] = (I1 & 0xFFFFu) | (C1 << 16);
+                rw[2 * (4 * lane + 3)] = (I1 >> 16) | (C1 & 0xFFFF0000u);
+            } else {
+                rb[4 * lane + 0] = acc[0];
+                rb[4 * lane + 1] = acc[1];
+                rb[4 * lane + 2] = acc[2];
+                rb[4 * lane + 3] = acc[3];
+            }
+        }
+        pend_y = y;
+    }
+    __syncthreads();
+    if (pend_y >= 0) combine(pend_y);
+}
+
+constexpr size_t kSmemBytes = (size_t(kGroupBins) * kVcWords + size_t(kWarps) * kVcWords) * 4 +
+                              size_t(2) * kWarps * kStrip * 8;
+
+}  // namespace spct_fused
+
+using namespace spct_fused;
+
+namespace spct_impl {
+size_t fused_prep_bytes(int bins) { return (static_cast<size_t>(bins) + 1) * 4 + 256 + ((bins + 127) / 128 + 1) * 8; }
+}  // namespace spct_impl
 
 extern "C" spct_status spct_cu_ih_build_match(const spct_source* src, const spct_ih* out, const double* tmpl, int kw,
                                               int kh, double p, int metric, double* partial, void* workspace,
                                               size_t workspace_bytes, void* stream) {
-    if (!out || !out->data) return contract("ih_build_match: this schedule needs tensor storage");
-    if (auto st = spct_cu_ih_build(src, out, workspace, workspace_bytes, stream)) return st;
-    return spct_cu_hist_partial(out, tmpl, kw, kh, p, metric, partial, 0, stream);
+    QuantParams q;
+    if (auto st = make_quant(src, &q)) return st;
+    if (auto st = check_ih(out)) return st;
+    if (out->width != src->width || out->height != src->height || out->nbins_total != src->nbins)
+        return contract("ih_build_match: tensor dims do not match the source");
+    if (out->data && reinterpret_cast<uintptr_t>(out->data) % 16 != 0)
+        return contract("ih_build_match: tensor data must be 16-byte aligned");
+    if (!(p >= 1.0)) return contract("hist_distance_map: Minkowski order must be >= 1");
+    if (!(kw >= 1 && kh >= 1 && kw <= src->width && kh <= src->height))
+        return contract("hist_distance_map: kernel exceeds image");
+    if (metric < SPCT_METRIC_MINKOWSKI || metric > SPCT_METRIC_CHISQ) return contract("hist_match: unknown metric");
+    if (!tmpl || !partial) return contract("ih_build_match: null template or partial");
+    cudaStream_t s = as_stream(stream);
+    const int64_t T = static_cast<int64_t>(kw) * kh;
+    const bool fusable = kw <= 128 && kh <= 255 && T <= 65535;
+    if (!fusable) {
+        // window too large for the 16-bit running-histogram cells: two passes
+        if (!out->data) return contract("ih_build_match: window too large for the fused path; pass tensor storage");
+        if (auto st = spct_cu_ih_build(src, out, workspace, workspace_bytes, stream)) return st;
+        return spct_cu_hist_partial(out, tmpl, kw, kh, p, metric, partial, 0, stream);
+    }
+    const BuildPlan bp = plan_build(out->width, out->height, out->bins, kB);
+    const size_t need = (out->data ? bp.lt_bytes + bp.hb_bytes : 0) + fused_prep_bytes(out->bins);
+    if (!workspace || workspace_bytes < need) return contract("ih_build_match: workspace too small");
+    uint32_t *Lt = nullptr, *Hb = nullptr;
+    char* ws = static_cast<char*>(workspace);
+    if (out->data) {
+        if (auto st = build_carries(q, *out, bp, workspace, workspace_bytes, s, &Lt, &Hb)) return st;
+        ws += bp.lt_bytes + bp.hb_bytes;
+    }
+    const int ngroups = static_cast<int>(ceil_div(out->bins, kGroupBins));
+    uint32_t* prep = reinterpret_cast<uint32_t*>(ws);
+    long long* Sg = reinterpret_cast<long long*>(ws + round_up((static_cast<int64_t>(out->bins) + 1) * 4, 256));
+    const int fast_metric = (metric == SPCT_METRIC_MINKOWSKI && p == 1.0) || metric == SPCT_METRIC_INTERSECTION;
+    prep_kernel<<<1, 256, 0, s>>>(tmpl, out->bin0, out->bins, static_cast<double>(T), fast_metric, prep, Sg, ngroups);
+    if (auto st = launch_status("prep_kernel")) return st;
+
+    FusedParams f{};
+    f.kw = kw;
+    f.kh = kh;
+    f.nu = out->width - kw + 1;
+    f.nv = out->height - kh + 1;
+    f.metric = metric;
+    f.p = p;
+    f.p_kind = p == 1.0 ? 1 : (p == 2.0 ? 2 : 0);
+    f.T = static_cast<double>(T);
+    f.invT = 1.0 / f.T;
+    f.T_pow2 = (T & (T - 1)) == 0;
+    f.tmpl = tmpl;
+    f.prep = prep;
+    f.S_group = Sg;
+    f.partial = partial;
+    static bool attr_set[2] = {false, false};
+    for (int g = 0; g < ngroups; ++g) {
+        f.group0 = g * kGroupBins;
+        f.accumulate = g > 0;
+        dim3 grid(bp.nstrips, bp.nbands, 1);
+        const int prof = prof_begin(out->data ? "ih_sweep_match" : "sweep_match_nostore", s);
+        if (out->data) {
+            if (!attr_set[1]) {
+                cudaFuncSetAttribute(sweep_match_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBytes);
+                attr_set[1] = true;
+            }
+            sweep_match_kernel<true><<<grid, 256, kSmemBytes, s>>>(q, *out, bp.Lb, bp.Wp, bp.band_rows, Lt, Hb, f);
+        } else {
+            if (!attr_set[0]) {
+                cudaFuncSetAttribute(sweep_match_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBytes);
+                attr_set[0] = true;
+            }
+            sweep_match_kernel<false><<<grid, 256, kSmemBytes, s>>>(q, *out, bp.Lb, bp.Wp, bp.band_rows, nullptr,
+                                                                    nullptr, f);
+        }
+        prof_end(prof, s);
+        if (auto st = launch_status("sweep_match_kernel")) return st;
+    }
+    return SPCT_OK;
 }

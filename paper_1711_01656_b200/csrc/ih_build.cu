@@ -22,6 +22,7 @@
 #include <cstring>
 
 #include "spct_internal.h"
+#include "sweep_common.cuh"
 
 using namespace spct_dev;
 
@@ -29,9 +30,9 @@ namespace spct_impl {
 
 // ------------------------------------------------------------------ planning
 
-BuildPlan plan_build(int width, int height, int bins) {
+BuildPlan plan_build(int width, int height, int bins, int force_B) {
     BuildPlan p{};
-    p.B = bins <= 4 ? 4 : (bins <= 8 ? 8 : 16);
+    p.B = force_B ? force_B : (bins <= 4 ? 4 : (bins <= 8 ? 8 : 16));
     const int nslabs = static_cast<int>(ceil_div(bins, p.B));
     p.warps = std::min(8, nslabs);
     p.slab_groups = static_cast<int>(ceil_div(nslabs, p.warps));
@@ -218,85 +219,21 @@ __global__ void __launch_bounds__(256) ih_sweep_kernel(QuantParams q, spct_ih ou
     if (kl0 >= out.bins) return;
     const int x0 = strip * kStrip + 4 * lane;  // first of this lane's 4 columns
     const int y0 = band * band_rows, y1 = min(out.height, y0 + band_rows);
-    const int H = out.height;
     const bool lane_live = x0 < out.row_pitch;
-
-    // vertical carry: H at row y0-1 for this lane's 4 columns
-    uint32_t V[4][B];
-    if (band > 0) {
-        const uint32_t* hb = Hb + (static_cast<int64_t>(band - 1) * Lb + kl0) * Wp + x0;
-#pragma unroll
-        for (int k = 0; k < B; ++k) {
-            uint4 v = *reinterpret_cast<const uint4*>(hb + static_cast<int64_t>(k) * Wp);
-            V[0][k] = v.x;
-            V[1][k] = v.y;
-            V[2][k] = v.z;
-            V[3][k] = v.w;
-        }
-    } else {
-#pragma unroll
-        for (int k = 0; k < B; ++k) V[0][k] = V[1][k] = V[2][k] = V[3][k] = 0;
-    }
-
-    uint32_t* base_ptr = out.data + static_cast<int64_t>(kl0) * out.plane_pitch + x0;
     const int k_live = min(B, out.bins - kl0);
-    const uint32_t* lt_strip = Lt ? Lt + (static_cast<int64_t>(strip) * H) * Lb + kl0 : nullptr;
+
+    uint32_t V[4][B];
+    vpart_init<B>(V, Hb, band, Lb, kl0, Wp, x0);
+    uint32_t* base_ptr = out.data + static_cast<int64_t>(kl0) * out.plane_pitch + x0;
+    const uint32_t* lt_strip =
+        (Lt && strip > 0) ? Lt + static_cast<int64_t>(strip) * out.height * Lb + kl0 : nullptr;
 
     uint32_t nxt = load_rel4(q, x0, y0, out.bin0 + kl0, B);
     for (int y = y0; y < y1; ++y) {
         const uint32_t cur = nxt;
         if (y + 1 < y1) nxt = load_rel4(q, x0, y + 1, out.bin0 + kl0, B);
-
-        uint32_t L[B];
-        if (lt_strip && strip > 0) {
-            const uint4* lp = reinterpret_cast<const uint4*>(lt_strip + static_cast<int64_t>(y) * Lb);
-#pragma unroll
-            for (int k4 = 0; k4 < B / 4; ++k4) {
-                uint4 v = __ldg(lp + k4);
-                L[4 * k4 + 0] = v.x;
-                L[4 * k4 + 1] = v.y;
-                L[4 * k4 + 2] = v.z;
-                L[4 * k4 + 3] = v.w;
-            }
-        } else {
-#pragma unroll
-            for (int k = 0; k < B; ++k) L[k] = 0;
-        }
-
-        // in-lane inclusive prefix bytes per bin and the lane's count per bin
-        uint32_t P[B];
-        uint32_t packed[B / 4];
-#pragma unroll
-        for (int i = 0; i < B / 4; ++i) packed[i] = 0;
-#pragma unroll
-        for (int k = 0; k < B; ++k) {
-            P[k] = match_bytes(cur, 0x01010101u * static_cast<uint32_t>(k)) * 0x01010101u;
-            packed[k >> 2] |= (P[k] >> 24) << ((k & 3) * 8);
-        }
-        // exclusive warp scan, 4 bins per word (each byte <= 128: no overflow)
-        uint32_t excl[B / 4];
-#pragma unroll
-        for (int i = 0; i < B / 4; ++i) {
-            uint32_t v = packed[i];
-#pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                uint32_t t = __shfl_up_sync(0xffffffffu, v, o);
-                if (lane >= o) v += t;
-            }
-            excl[i] = v - packed[i];
-        }
-        uint32_t* rowp = base_ptr + static_cast<int64_t>(y) * out.row_pitch;
-#pragma unroll
-        for (int k = 0; k < B; ++k) {
-            const uint32_t base = L[k] + ((excl[k >> 2] >> ((k & 3) * 8)) & 0xFFu);
-            V[0][k] += base + (P[k] & 0xFFu);
-            V[1][k] += base + ((P[k] >> 8) & 0xFFu);
-            V[2][k] += base + ((P[k] >> 16) & 0xFFu);
-            V[3][k] += base + (P[k] >> 24);
-            if (lane_live && k < k_live)
-                __stcs(reinterpret_cast<uint4*>(rowp + static_cast<int64_t>(k) * out.plane_pitch),
-                       make_uint4(V[0][k], V[1][k], V[2][k], V[3][k]));
-        }
+        vpart_row<B>(V, cur, lt_strip ? lt_strip + static_cast<int64_t>(y) * Lb : nullptr, lane,
+                     base_ptr + static_cast<int64_t>(y) * out.row_pitch, out.plane_pitch, lane_live, k_live);
     }
 }
 
@@ -409,8 +346,9 @@ extern "C" spct_status spct_cu_ih_build_workspace(const spct_source* src, int bi
     (void)bin0;
     if (!src || !bytes) return contract("ih_build_workspace: null argument");
     if (!(src->width > 0 && src->height > 0 && bins >= 1)) return contract("build: empty bin map");
-    BuildPlan p = plan_build(src->width, src->height, bins);
-    *bytes = p.lt_bytes + p.hb_bytes + 256;
+    const BuildPlan p = plan_build(src->width, src->height, bins);
+    const BuildPlan pf = plan_build(src->width, src->height, bins, 16);  // fused sweep: 16 bins per warp
+    *bytes = std::max(p.lt_bytes + p.hb_bytes, pf.lt_bytes + pf.hb_bytes) + fused_prep_bytes(bins) + 256;
     return SPCT_OK;
 }
 

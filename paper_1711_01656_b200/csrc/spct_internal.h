@@ -58,6 +58,14 @@ struct BuildPlan {
     int slab_groups;  // CTAs along the bin axis
     size_t lt_bytes, hb_bytes;
 };
-BuildPlan plan_build(int width, int height, int bins);
+BuildPlan plan_build(int width, int height, int bins, int force_B = 0);
+
+// Workspace of the fused path's template prep (fused.cu).
+size_t fused_prep_bytes(int bins);
+
+// Carry pre-passes of a build (ih_build.cu); fills the row-carry (Lt) and band-carry
+// (Hb) tables inside `workspace`.
+spct_status build_carries(const spct_dev::QuantParams& q, const spct_ih& out, const BuildPlan& p, void* workspace,
+                          size_t ws_bytes, cudaStream_t s, uint32_t** Lt, uint32_t** Hb);
 
 }  // namespace spct_impl

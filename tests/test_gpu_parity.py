@@ -261,8 +261,90 @@ def test_fused_build_match(P, slabs):
     got = P.hist_finalize(acc, 333, 211, kw, kh, 1.0).cpu().numpy()
     want = oracle.hist_match_map_direct(qb, bins, th, kw, kh, 1.0)
     assert close(got, want)
-    if slabs == 1:
-        assert np.array_equal(got, want)
+
+
+def _crop_template(qb, bins, x0, y0, kw, kh):
+    crop = qb[y0:y0 + kh, x0:x0 + kw]
+    return np.bincount(crop.reshape(-1), minlength=bins).astype(np.float64) / crop.size
+
+
+FUSED_CASES = [  # w, h, bins, kw, kh
+    (333, 211, 48, 64, 64), (130, 67, 9, 13, 11), (257, 140, 130, 64, 64), (300, 200, 128, 128, 100),
+    (97, 301, 20, 1, 1), (128, 128, 16, 127, 5), (45, 33, 7, 45, 33), (700, 90, 256, 31, 17), (520, 260, 33, 65, 3)]
+
+
+@pytest.mark.parametrize("w,h,bins,kw,kh", FUSED_CASES)
+@pytest.mark.parametrize("store", [True, False])
+def test_fused_integral_template(P, w, h, bins, kw, kh, store):
+    """Template = histogram of a kw x kh crop (integral s_k): the exact integer path."""
+    img = oracle.smooth_image(w, h, w * 3 + h)
+    qb = oracle.quantize(img, bins)
+    th = _crop_template(qb, bins, (w - kw) // 3, (h - kh) // 2, kw, kh)
+    want = oracle.hist_match_map_direct(qb, bins, th, kw, kh, 1.0)
+    if store:
+        t, part = P.build_and_match(img, bins, th, kw, kh, 1.0)
+        assert np.array_equal(t.padded_u64(), oracle.build_ih(qb, bins))
+    else:
+        t = P.IntegralHistogramTensor(w, h, bins)
+        t.desc.data = None
+        _, part = P.build_and_match(img, bins, th, kw, kh, 1.0, out=t)
+    got = P.hist_finalize(part, w, h, kw, kh, 1.0).cpu().numpy()
+    assert close(got, want)
+    inter = oracle.hist_match_map_direct(qb, bins, th, kw, kh, 1.0, oracle.INTERSECTION)
+    _, part = P.build_and_match(img, bins, th, kw, kh, 1.0, 1)
+    assert close(P.hist_finalize(part, w, h, kw, kh, 1.0, 1).cpu().numpy(), inter)
+
+
+@pytest.mark.parametrize("w,h,bins,kw,kh", FUSED_CASES[:6])
+@pytest.mark.parametrize("p,metric", [(1.0, 0), (2.0, 0), (1.7, 0), (1.0, 1), (1.0, 2), (1.0, 3)])
+def test_fused_general_template(P, w, h, bins, kw, kh, p, metric):
+    """Non-integral template (random weights): the FP64 per-bin path."""
+    img = oracle.noise_image(w, h, w + 7 * h)
+    qb = oracle.quantize(img, bins)
+    rng = np.random.default_rng(w * h)
+    th = rng.random(bins)
+    th /= th.sum()
+    t, part = P.build_and_match(img, bins, th, kw, kh, p, metric)
+    got = P.hist_finalize(part, w, h, kw, kh, p, metric).cpu().numpy()
+    assert close(got, oracle.hist_match_map_direct(qb, bins, th, kw, kh, p, metric))
+
+
+@pytest.mark.parametrize("rows", [1, 5, 64, 100])
+def test_fused_bands(P, band_rows, rows):
+    band_rows(rows)
+    w, h, bins, kw, kh = 290, 173, 40, 64, 37
+    img = oracle.smooth_image(w, h, rows)
+    qb = oracle.quantize(img, bins)
+    th = _crop_template(qb, bins, 100, 60, kw, kh)
+    t, part = P.build_and_match(img, bins, th, kw, kh, 1.0)
+    assert np.array_equal(t.padded_u64(), oracle.build_ih(qb, bins))
+    assert close(P.hist_finalize(part, w, h, kw, kh, 1.0).cpu().numpy(),
+                 oracle.hist_match_map_direct(qb, bins, th, kw, kh, 1.0))
+
+
+def test_fused_sources_and_slabs(P):
+    r, g, b = oracle.noise_color(403, 150, 2)
+    gray = oracle.to_grayscale(r, g, b)
+    bins, kw, kh = 200, 64, 64
+    qb = oracle.quantize(gray, bins)
+    th = _crop_template(qb, bins, 200, 40, kw, kh)
+    acc = None
+    for k0, k1 in [(0, 77), (77, 200)]:
+        t, part = P.build_and_match((r, g, b), bins, th, kw, kh, 1.0, bin0=k0, bins=k1 - k0)
+        assert np.array_equal(t.padded_u64(), oracle.build_ih(qb, bins, k0, k1))
+        acc = part.clone() if acc is None else acc + part
+    assert close(P.hist_finalize(acc, 403, 150, kw, kh, 1.0).cpu().numpy(),
+                 oracle.hist_match_map_direct(qb, bins, th, kw, kh, 1.0))
+
+
+def test_fused_large_window_falls_back(P):
+    w, h, bins, kw, kh = 300, 280, 12, 200, 150
+    img = oracle.smooth_image(w, h, 4)
+    qb = oracle.quantize(img, bins)
+    th = _crop_template(qb, bins, 50, 60, kw, kh)
+    t, part = P.build_and_match(img, bins, th, kw, kh, 1.0)
+    assert np.array_equal(P.hist_finalize(part, w, h, kw, kh, 1.0).cpu().numpy(),
+                          oracle.hist_match_map_direct(qb, bins, th, kw, kh, 1.0))
 
 
 @pytest.mark.skipif(not oracle.have_ref(), reason="oracle/_ref not built")
