@@ -104,15 +104,14 @@ __global__ void prep_kernel(const double* __restrict__ tmpl, int bin0, int bins,
     }
 }
 
-template <bool STORE>
-__global__ void __launch_bounds__(256, 1) sweep_match_kernel(QuantParams q, spct_ih out, int Lb, int Wp,
+template <bool STORE, bool FAST>
+__global__ void __launch_bounds__(256, 2) sweep_match_kernel(QuantParams q, spct_ih out, int Lb, int Wp,
                                                              int band_rows, const uint32_t* __restrict__ Lt,
                                                              const uint32_t* __restrict__ Hb, FusedParams f) {
     extern __shared__ uint4 smem_raw[];
     uint32_t* vc = reinterpret_cast<uint32_t*>(smem_raw);       // [128 bins][128 words]
     uint32_t* gbuf = vc + kGroupBins * kVcWords;                   // [8 warps][128 words]
     double* red = reinterpret_cast<double*>(gbuf + kWarps * kVcWords);  // [2][8][128]
-    __shared__ int s_fast;
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int strip = blockIdx.x, band = blockIdx.y;
@@ -128,7 +127,8 @@ __global__ void __launch_bounds__(256, 1) sweep_match_kernel(QuantParams q, spct
     const int y0 = band * band_rows, y1 = min(H, y0 + band_rows);
     const int ystart = max(0, y0 - f.kh + 1);
 
-    if (tid == 0) s_fast = f.prep[0];
+    // Both variants are launched; the one that does not match the template prep exits.
+    if ((__ldg(f.prep) != 0) != FAST) return;
     for (int i = tid; i < kGroupBins * kVcWords; i += blockDim.x) vc[i] = 0;
 
     uint32_t V[4][kB];
@@ -139,7 +139,7 @@ __global__ void __launch_bounds__(256, 1) sweep_match_kernel(QuantParams q, spct
     const uint32_t* lt_strip = (Lt && strip > 0) ? Lt + static_cast<int64_t>(strip) * H * Lb + kl0 : nullptr;
     const bool lane_live = xl < out.row_pitch;
     __syncthreads();
-    const bool fast = s_fast != 0;
+    constexpr bool fast = FAST;
     const double S = fast ? static_cast<double>(f.S_group[g0 / kGroupBins]) : 0.0;
 
     // pending row for the deferred cross-warp combine
@@ -185,7 +185,7 @@ __global__ void __launch_bounds__(256, 1) sweep_match_kernel(QuantParams q, spct
                 const int bn = pixel_bin(q, x, y) - out.bin0 - g0;
                 if (static_cast<unsigned>(bn) < static_cast<unsigned>(nb_cta)) atomicAdd(&vc[bn * kVcWords + (tid >> 1)], inc);
                 const int yo = y - f.kh;
-                if (yo >= 0) {
+                if (yo >= ystart) {  // rows before ystart were never added
                     const int bo = pixel_bin(q, x, yo) - out.bin0 - g0;
                     if (static_cast<unsigned>(bo) < static_cast<unsigned>(nb_cta)) atomicSub(&vc[bo * kVcWords + (tid >> 1)], inc);
                 }
@@ -207,6 +207,7 @@ __global__ void __launch_bounds__(256, 1) sweep_match_kernel(QuantParams q, spct
             uint32_t I0 = 0, I1 = 0, C0 = 0, C1 = 0;
             double acc[4] = {0.0, 0.0, 0.0, 0.0};
             const int idx = kStrip + 4 * lane - f.kw;  // first ext cell of G(e - kw)
+#pragma unroll 1
             for (int k = 0; k < kB; ++k) {
                 if (k >= k_live) break;
                 const uint32_t* vrow = vc + (warp * kB + k) * kVcWords;
@@ -345,27 +346,32 @@ extern "C" spct_status spct_cu_ih_build_match(const spct_source* src, const spct
     f.prep = prep;
     f.S_group = Sg;
     f.partial = partial;
-    static bool attr_set[2] = {false, false};
+    static bool attr_set = false;
+    if (!attr_set) {
+        cudaFuncSetAttribute(sweep_match_kernel<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBytes);
+        cudaFuncSetAttribute(sweep_match_kernel<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBytes);
+        cudaFuncSetAttribute(sweep_match_kernel<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBytes);
+        cudaFuncSetAttribute(sweep_match_kernel<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBytes);
+        attr_set = true;
+    }
     for (int g = 0; g < ngroups; ++g) {
         f.group0 = g * kGroupBins;
         f.accumulate = g > 0;
         dim3 grid(bp.nstrips, bp.nbands, 1);
+        // integer (template-crop) variant and FP64 variant: the one not selected by the
+        // device-side template prep exits on entry
         const int prof = prof_begin(out->data ? "ih_sweep_match" : "sweep_match_nostore", s);
         if (out->data) {
-            if (!attr_set[1]) {
-                cudaFuncSetAttribute(sweep_match_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBytes);
-                attr_set[1] = true;
-            }
-            sweep_match_kernel<true><<<grid, 256, kSmemBytes, s>>>(q, *out, bp.Lb, bp.Wp, bp.band_rows, Lt, Hb, f);
+            sweep_match_kernel<true, true><<<grid, 256, kSmemBytes, s>>>(q, *out, bp.Lb, bp.Wp, bp.band_rows, Lt, Hb, f);
+            sweep_match_kernel<true, false><<<grid, 256, kSmemBytes, s>>>(q, *out, bp.Lb, bp.Wp, bp.band_rows, Lt, Hb, f);
         } else {
-            if (!attr_set[0]) {
-                cudaFuncSetAttribute(sweep_match_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBytes);
-                attr_set[0] = true;
-            }
-            sweep_match_kernel<false><<<grid, 256, kSmemBytes, s>>>(q, *out, bp.Lb, bp.Wp, bp.band_rows, nullptr,
-                                                                    nullptr, f);
+            sweep_match_kernel<false, true><<<grid, 256, kSmemBytes, s>>>(q, *out, bp.Lb, bp.Wp, bp.band_rows, nullptr,
+                                                                          nullptr, f);
+            sweep_match_kernel<false, false><<<grid, 256, kSmemBytes, s>>>(q, *out, bp.Lb, bp.Wp, bp.band_rows, nullptr,
+                                                                           nullptr, f);
         }
         prof_end(prof, s);
+        note_launch();
         if (auto st = launch_status("sweep_match_kernel")) return st;
     }
     return SPCT_OK;
