@@ -105,13 +105,17 @@ __global__ void prep_kernel(const double* __restrict__ tmpl, int bin0, int bins,
 }
 
 template <bool STORE, bool FAST>
-__global__ void __launch_bounds__(256, 2) sweep_match_kernel(QuantParams q, spct_ih out, int Lb, int Wp,
+__global__ void __launch_bounds__(256, 2) sweep_match_kernel(QuantParams q, PixelMode pm, spct_ih out, int Lb, int Wp,
                                                              int band_rows, const uint32_t* __restrict__ Lt,
                                                              const uint32_t* __restrict__ Hb, FusedParams f) {
     extern __shared__ uint4 smem_raw[];
-    uint32_t* vc = reinterpret_cast<uint32_t*>(smem_raw);       // [128 bins][128 words]
-    uint32_t* gbuf = vc + kGroupBins * kVcWords;                   // [8 warps][128 words]
-    double* red = reinterpret_cast<double*>(gbuf + kWarps * kVcWords);  // [2][8][128]
+    uint32_t* vc = reinterpret_cast<uint32_t*>(smem_raw);            // [128 bins][128 words]
+    uint32_t* gbuf = vc + kGroupBins * kVcWords;                       // [8 warps][2][128 words]
+    double* red = reinterpret_cast<double*>(gbuf + kWarps * 2 * kVcWords);  // [2 rows][8 warps][128]
+    uint32_t* srep_s = reinterpret_cast<uint32_t*>(red + 2 * kWarps * kStrip);  // [128]
+
+    // Both variants are launched; the one that does not match the template prep exits.
+    if ((__ldg(f.prep) != 0) != FAST) return;
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int strip = blockIdx.x, band = blockIdx.y;
@@ -126,42 +130,42 @@ __global__ void __launch_bounds__(256, 2) sweep_match_kernel(QuantParams q, spct
     const int H = out.height, W = out.width;
     const int y0 = band * band_rows, y1 = min(H, y0 + band_rows);
     const int ystart = max(0, y0 - f.kh + 1);
+    const int k0 = out.bin0 + kl0;                         // global bin of the warp's first plane
+    const uint32_t kpat0 = pm.byte_mode ? 0x01010101u * static_cast<uint32_t>(k0) : 0u;
 
-    // Both variants are launched; the one that does not match the template prep exits.
-    if ((__ldg(f.prep) != 0) != FAST) return;
     for (int i = tid; i < kGroupBins * kVcWords; i += blockDim.x) vc[i] = 0;
+    if (FAST && tid < kGroupBins) srep_s[tid] = tid < nb_cta ? __ldg(f.prep + 1 + g0 + tid) : 0u;
 
     uint32_t V[4][kB];
-    if (STORE) {
-        if (warp_live) vpart_init<kB>(V, Hb, band, Lb, kl0, Wp, xl);
-    }
+    if (STORE && warp_live) vpart_init<kB>(V, Hb, band, Lb, kl0, Wp, xl);
     uint32_t* base_ptr = STORE ? out.data + static_cast<int64_t>(kl0) * out.plane_pitch + xl : nullptr;
     const uint32_t* lt_strip = (Lt && strip > 0) ? Lt + static_cast<int64_t>(strip) * H * Lb + kl0 : nullptr;
     const bool lane_live = xl < out.row_pitch;
+    const long long S = FAST ? f.S_group[g0 / kGroupBins] : 0;
+    // G(e - kw): first extended cell of this lane's four windows, as a word and a bit shift
+    const int idx = kStrip + 4 * lane - f.kw;
+    const int pw = idx >> 1, psh = (idx & 1) * 16;
+    uint32_t* gb = gbuf + warp * 2 * kVcWords;
+    const uint32_t* vbase = vc + warp * kB * kVcWords + 2 * lane;
     __syncthreads();
-    constexpr bool fast = FAST;
-    const double S = fast ? static_cast<double>(f.S_group[g0 / kGroupBins]) : 0.0;
 
-    // pending row for the deferred cross-warp combine
-    int pend_y = -1;
+    // deferred cross-warp combine of row yy (thread t < 128: window ending at strip column t)
     auto combine = [&](int yy) {
-        // thread t < 128: window with right edge at strip column t, bottom row yy
         if (tid < kStrip) {
             const int e = xs + tid;
             const int u = e - f.kw + 1, v = yy - f.kh + 1;
             if (u >= 0 && e < W) {
                 const double* rb = red + (yy & 1) * (kWarps * kStrip);
                 double term;
-                if (fast) {
+                if (FAST) {
                     long long I = 0, C = 0;
                     for (int w = 0; w < nwarps_live; ++w) {
                         const uint32_t x = reinterpret_cast<const uint32_t*>(rb + w * kStrip)[2 * tid];
                         I += x & 0xFFFFu;
                         C += x >> 16;
                     }
-                    term = f.metric == SPCT_METRIC_INTERSECTION
-                               ? static_cast<double>(I) * f.invT
-                               : static_cast<double>(C + static_cast<long long>(S) - 2 * I) * f.invT;
+                    term = f.metric == SPCT_METRIC_INTERSECTION ? static_cast<double>(I) * f.invT
+                                                                : static_cast<double>(C + S - 2 * I) * f.invT;
                 } else {
                     term = 0.0;
                     for (int w = 0; w < nwarps_live; ++w) term = __dadd_rn(term, rb[w * kStrip + tid]);
@@ -172,6 +176,7 @@ __global__ void __launch_bounds__(256, 2) sweep_match_kernel(QuantParams q, spct
         }
     };
 
+    int pend_y = -1;
     for (int y = ystart; y < y1; ++y) {
         __syncthreads();  // A: previous row's vc / red reads are done
         if (pend_y >= 0) {
@@ -183,11 +188,13 @@ __global__ void __launch_bounds__(256, 2) sweep_match_kernel(QuantParams q, spct
             if (x >= 0 && x < W) {
                 const uint32_t inc = 1u << (16 * (tid & 1));
                 const int bn = pixel_bin(q, x, y) - out.bin0 - g0;
-                if (static_cast<unsigned>(bn) < static_cast<unsigned>(nb_cta)) atomicAdd(&vc[bn * kVcWords + (tid >> 1)], inc);
+                if (static_cast<unsigned>(bn) < static_cast<unsigned>(nb_cta))
+                    atomicAdd(&vc[bn * kVcWords + (tid >> 1)], inc);
                 const int yo = y - f.kh;
                 if (yo >= ystart) {  // rows before ystart were never added
                     const int bo = pixel_bin(q, x, yo) - out.bin0 - g0;
-                    if (static_cast<unsigned>(bo) < static_cast<unsigned>(nb_cta)) atomicSub(&vc[bo * kVcWords + (tid >> 1)], inc);
+                    if (static_cast<unsigned>(bo) < static_cast<unsigned>(nb_cta))
+                        atomicSub(&vc[bo * kVcWords + (tid >> 1)], inc);
                 }
             }
         }
@@ -195,35 +202,28 @@ __global__ void __launch_bounds__(256, 2) sweep_match_kernel(QuantParams q, spct
         if (y < y0) continue;  // pre-roll rows only feed vc
 
         if (STORE && warp_live) {
-            const uint32_t cur = load_rel4(q, xl, y, out.bin0 + kl0, kB);
-            vpart_row<kB>(V, cur, lt_strip ? lt_strip + static_cast<int64_t>(y) * Lb : nullptr, lane,
-                          base_ptr + static_cast<int64_t>(y) * out.row_pitch, out.plane_pitch, lane_live, k_live);
+            const uint32_t cur = load_bins4(q, pm, xl, y, k0, kB);
+            vpart_row<kB, true>(V, cur, kpat0, lt_strip ? lt_strip + static_cast<int64_t>(y) * Lb : nullptr,
+                                base_ptr + static_cast<int64_t>(y) * out.row_pitch, out.plane_pitch, lane_live,
+                                k_live);
         }
         if (y < f.kh - 1) continue;  // no window ends on this row yet
 
-        double* rb = red + (y & 1) * (kWarps * kStrip) + warp * kStrip;
         if (warp_live) {
-            uint32_t* gb = gbuf + warp * kVcWords;
             uint32_t I0 = 0, I1 = 0, C0 = 0, C1 = 0;
             double acc[4] = {0.0, 0.0, 0.0, 0.0};
-            const int idx = kStrip + 4 * lane - f.kw;  // first ext cell of G(e - kw)
-#pragma unroll 1
+#pragma unroll 4
             for (int k = 0; k < kB; ++k) {
-                if (k >= k_live) break;
-                const uint32_t* vrow = vc + (warp * kB + k) * kVcWords;
-                const uint2 wa = *reinterpret_cast<const uint2*>(vrow + 2 * lane);
-                const uint2 wb = *reinterpret_cast<const uint2*>(vrow + 64 + 2 * lane);
+                const uint32_t* vw = vbase + k * kVcWords;
+                const uint2 wa = *reinterpret_cast<const uint2*>(vw);
+                const uint2 wb = *reinterpret_cast<const uint2*>(vw + 64);
+                // in-lane inclusive prefix of the 4 columns of each half (u16 pairs)
                 uint32_t a0 = wa.x * 0x10001u;
                 uint32_t a1 = wa.y * 0x10001u + __byte_perm(a0, 0, 0x3232);
                 uint32_t b0 = wb.x * 0x10001u;
                 uint32_t b1 = wb.y * 0x10001u + __byte_perm(b0, 0, 0x3232);
-                const uint32_t tot = __byte_perm(a1, b1, 0x7632);  // {sum(a), sum(b)} as u16 fields
-                uint32_t inc = tot;
-#pragma unroll
-                for (int o = 1; o < 32; o <<= 1) {
-                    const uint32_t t = __shfl_up_sync(0xffffffffu, inc, o);
-                    if (lane >= o) inc += t;
-                }
+                const uint32_t tot = __byte_perm(a1, b1, 0x7632);  // {sum a, sum b}
+                const uint32_t inc = warp_incl_scan(tot);
                 const uint32_t ex = inc - tot;
                 const uint32_t T1 = __shfl_sync(0xffffffffu, inc, 31) & 0xFFFFu;
                 const uint32_t ba = __byte_perm(ex, 0, 0x1010);
@@ -232,35 +232,29 @@ __global__ void __launch_bounds__(256, 2) sweep_match_kernel(QuantParams q, spct
                 a1 += ba;
                 b0 += bb;
                 b1 += bb;
-                *reinterpret_cast<uint2*>(gb + 2 * lane) = make_uint2(a0, a1);
-                *reinterpret_cast<uint2*>(gb + 64 + 2 * lane) = make_uint2(b0, b1);
+                uint32_t* g = gb + (k & 1) * kVcWords;
+                *reinterpret_cast<uint2*>(g + 2 * lane) = make_uint2(a0, a1);
+                *reinterpret_cast<uint2*>(g + 64 + 2 * lane) = make_uint2(b0, b1);
                 __syncwarp();
-                uint32_t p0, p1;
-                if ((idx & 1) == 0) {
-                    p0 = gb[idx >> 1];
-                    p1 = gb[(idx >> 1) + 1];
-                } else {
-                    const uint32_t q0 = gb[idx >> 1], q1 = gb[(idx >> 1) + 1], q2 = gb[(idx >> 1) + 2];
-                    p0 = __byte_perm(q0, q1, 0x5432);
-                    p1 = __byte_perm(q1, q2, 0x5432);
-                }
-                __syncwarp();
+                const uint32_t q0 = g[pw], q1 = g[pw + 1], q2 = g[pw + 2];
+                const uint32_t p0 = __funnelshift_r(q0, q1, psh), p1 = __funnelshift_r(q1, q2, psh);
                 const uint32_t c0 = b0 - p0, c1 = b1 - p1;  // window counts {j=0, j=1}, {j=2, j=3}
-                if (fast) {
-                    const uint32_t s = f.prep[1 + kl0 + k];
-                    I0 += min_u16x2(c0, s);
-                    I1 += min_u16x2(c1, s);
+                if (FAST) {
+                    const uint32_t sk = srep_s[warp * kB + k];
+                    I0 += min_u16x2(c0, sk);
+                    I1 += min_u16x2(c1, sk);
                     C0 += c0;
                     C1 += c1;
-                } else {
-                    const double t = __ldg(f.tmpl + out.bin0 + kl0 + k);
+                } else if (k < k_live) {
+                    const double t = __ldg(f.tmpl + k0 + k);
                     acc[0] = __dadd_rn(acc[0], general_term(c0 & 0xFFFFu, t, f));
                     acc[1] = __dadd_rn(acc[1], general_term(c0 >> 16, t, f));
                     acc[2] = __dadd_rn(acc[2], general_term(c1 & 0xFFFFu, t, f));
                     acc[3] = __dadd_rn(acc[3], general_term(c1 >> 16, t, f));
                 }
             }
-            if (fast) {
+            double* rb = red + (y & 1) * (kWarps * kStrip) + warp * kStrip;
+            if (FAST) {
                 // per window: I | C << 16 in the low word of the slot
                 uint32_t* rw = reinterpret_cast<uint32_t*>(rb);
                 rw[2 * (4 * lane + 0)] = (I0 & 0xFFFFu) | (C0 << 16);
@@ -280,8 +274,8 @@ __global__ void __launch_bounds__(256, 2) sweep_match_kernel(QuantParams q, spct
     if (pend_y >= 0) combine(pend_y);
 }
 
-constexpr size_t kSmemBytes = (size_t(kGroupBins) * kVcWords + size_t(kWarps) * kVcWords) * 4 +
-                              size_t(2) * kWarps * kStrip * 8;
+constexpr size_t kSmemBytes = (size_t(kGroupBins) * kVcWords + size_t(kWarps) * 2 * kVcWords) * 4 +
+                              size_t(2) * kWarps * kStrip * 8 + size_t(kGroupBins) * 4;
 
 }  // namespace spct_fused
 
@@ -346,6 +340,7 @@ extern "C" spct_status spct_cu_ih_build_match(const spct_source* src, const spct
     f.prep = prep;
     f.S_group = Sg;
     f.partial = partial;
+    const PixelMode pm = make_pixel_mode(q);
     static bool attr_set = false;
     if (!attr_set) {
         cudaFuncSetAttribute(sweep_match_kernel<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBytes);
@@ -362,12 +357,12 @@ extern "C" spct_status spct_cu_ih_build_match(const spct_source* src, const spct
         // device-side template prep exits on entry
         const int prof = prof_begin(out->data ? "ih_sweep_match" : "sweep_match_nostore", s);
         if (out->data) {
-            sweep_match_kernel<true, true><<<grid, 256, kSmemBytes, s>>>(q, *out, bp.Lb, bp.Wp, bp.band_rows, Lt, Hb, f);
-            sweep_match_kernel<true, false><<<grid, 256, kSmemBytes, s>>>(q, *out, bp.Lb, bp.Wp, bp.band_rows, Lt, Hb, f);
+            sweep_match_kernel<true, true><<<grid, 256, kSmemBytes, s>>>(q, pm, *out, bp.Lb, bp.Wp, bp.band_rows, Lt, Hb, f);
+            sweep_match_kernel<true, false><<<grid, 256, kSmemBytes, s>>>(q, pm, *out, bp.Lb, bp.Wp, bp.band_rows, Lt, Hb, f);
         } else {
-            sweep_match_kernel<false, true><<<grid, 256, kSmemBytes, s>>>(q, *out, bp.Lb, bp.Wp, bp.band_rows, nullptr,
+            sweep_match_kernel<false, true><<<grid, 256, kSmemBytes, s>>>(q, pm, *out, bp.Lb, bp.Wp, bp.band_rows, nullptr,
                                                                           nullptr, f);
-            sweep_match_kernel<false, false><<<grid, 256, kSmemBytes, s>>>(q, *out, bp.Lb, bp.Wp, bp.band_rows, nullptr,
+            sweep_match_kernel<false, false><<<grid, 256, kSmemBytes, s>>>(q, pm, *out, bp.Lb, bp.Wp, bp.band_rows, nullptr,
                                                                            nullptr, f);
         }
         prof_end(prof, s);

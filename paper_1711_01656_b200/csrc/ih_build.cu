@@ -206,9 +206,9 @@ __global__ void __launch_bounds__(1024) bandscan_kernel(int Lb, int Wp, int nban
 
 // ------------------------------------------------------------------ main sweep
 
-template <int B>
-__global__ void __launch_bounds__(256) ih_sweep_kernel(QuantParams q, spct_ih out, int Lb, int Wp, int band_rows,
-                                                       int warps_per_cta, const uint32_t* __restrict__ Lt,
+template <int B, bool GUARD>
+__global__ void __launch_bounds__(256) ih_sweep_kernel(QuantParams q, PixelMode pm, spct_ih out, int Lb, int Wp,
+                                                       int band_rows, int warps_per_cta, const uint32_t* __restrict__ Lt,
                                                        const uint32_t* __restrict__ Hb) {
     const int lane = lane_id();
     const int warp = threadIdx.x >> 5;
@@ -217,10 +217,13 @@ __global__ void __launch_bounds__(256) ih_sweep_kernel(QuantParams q, spct_ih ou
     const int slab = blockIdx.z * warps_per_cta + warp;
     const int kl0 = slab * B;  // first slab-local bin of this warp
     if (kl0 >= out.bins) return;
+    const int k_live = min(B, out.bins - kl0);
+    if ((k_live < B) != GUARD) return;  // full slabs run the unguarded variant
     const int x0 = strip * kStrip + 4 * lane;  // first of this lane's 4 columns
     const int y0 = band * band_rows, y1 = min(out.height, y0 + band_rows);
     const bool lane_live = x0 < out.row_pitch;
-    const int k_live = min(B, out.bins - kl0);
+    const int k0 = out.bin0 + kl0;
+    const uint32_t kpat0 = pm.byte_mode ? 0x01010101u * static_cast<uint32_t>(k0) : 0u;
 
     uint32_t V[4][B];
     vpart_init<B>(V, Hb, band, Lb, kl0, Wp, x0);
@@ -228,12 +231,12 @@ __global__ void __launch_bounds__(256) ih_sweep_kernel(QuantParams q, spct_ih ou
     const uint32_t* lt_strip =
         (Lt && strip > 0) ? Lt + static_cast<int64_t>(strip) * out.height * Lb + kl0 : nullptr;
 
-    uint32_t nxt = load_rel4(q, x0, y0, out.bin0 + kl0, B);
+    uint32_t nxt = load_bins4(q, pm, x0, y0, k0, B);
     for (int y = y0; y < y1; ++y) {
         const uint32_t cur = nxt;
-        if (y + 1 < y1) nxt = load_rel4(q, x0, y + 1, out.bin0 + kl0, B);
-        vpart_row<B>(V, cur, lt_strip ? lt_strip + static_cast<int64_t>(y) * Lb : nullptr, lane,
-                     base_ptr + static_cast<int64_t>(y) * out.row_pitch, out.plane_pitch, lane_live, k_live);
+        if (y + 1 < y1) nxt = load_bins4(q, pm, x0, y + 1, k0, B);
+        vpart_row<B, GUARD>(V, cur, kpat0, lt_strip ? lt_strip + static_cast<int64_t>(y) * Lb : nullptr,
+                            base_ptr + static_cast<int64_t>(y) * out.row_pitch, out.plane_pitch, lane_live, k_live);
     }
 }
 
@@ -399,10 +402,15 @@ extern "C" spct_status spct_cu_ih_build(const spct_source* src, const spct_ih* o
     dim3 grid(p.nstrips, p.nbands, p.slab_groups);
     const int threads = 32 * p.warps;
     const int prof = prof_begin("ih_sweep", s);
+    const PixelMode pm = make_pixel_mode(q);
     switch (p.B) {
-        case 4: ih_sweep_kernel<4><<<grid, threads, 0, s>>>(q, *out, p.Lb, p.Wp, p.band_rows, p.warps, Lt, Hb); break;
-        case 8: ih_sweep_kernel<8><<<grid, threads, 0, s>>>(q, *out, p.Lb, p.Wp, p.band_rows, p.warps, Lt, Hb); break;
-        default: ih_sweep_kernel<16><<<grid, threads, 0, s>>>(q, *out, p.Lb, p.Wp, p.band_rows, p.warps, Lt, Hb); break;
+#define SPCT_SWEEP(BB)                                                                                          \
+    ih_sweep_kernel<BB, false><<<grid, threads, 0, s>>>(q, pm, *out, p.Lb, p.Wp, p.band_rows, p.warps, Lt, Hb); \
+    if (out->bins % BB) ih_sweep_kernel<BB, true><<<grid, threads, 0, s>>>(q, pm, *out, p.Lb, p.Wp, p.band_rows, p.warps, Lt, Hb);
+        case 4: SPCT_SWEEP(4) break;
+        case 8: SPCT_SWEEP(8) break;
+        default: SPCT_SWEEP(16) break;
+#undef SPCT_SWEEP
     }
     prof_end(prof, s);
     return launch_status("ih_sweep_kernel");

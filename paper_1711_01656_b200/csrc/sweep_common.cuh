@@ -2,8 +2,8 @@
 // build+match sweep.
 //
 // A warp owns a 128-column strip (lane l: columns 4l..4l+3) and a slab of B bins.
-// For every row it receives the row's four relative bins per lane packed in bytes
-// (0xFF = not in the slab) and updates, per bin k and column j,
+// For every row it receives the four pixel bins of the lane packed in bytes and
+// updates, per bin k and column j,
 //     V[j][k] += L(y, k) + E_k(l) + P_k(j)
 // where L is the count of k in the row left of the strip (carry table), E_k the count
 // of k in lanes < l (one warp shuffle scan over four bins packed per word) and P_k(j)
@@ -15,6 +15,81 @@
 #include "spct_device.cuh"
 
 namespace spct_dev {
+
+// How the packed bins of a lane are formed (host-chosen, warp-uniform).
+//   byte_mode: nbins <= 256, bytes hold the absolute bin; bin k matches byte value k.
+//              Columns past the image edge hold garbage: they only influence columns
+//              further right, which are never stored.
+//   otherwise: bytes hold bin - k0 for bins of the warp's slab and 0xFF elsewhere.
+//   shift >= 0: gray uint8 with lo = 0, hi = 256 and nbins = 2^(8-shift): bin = v >> shift.
+struct PixelMode {
+    int byte_mode;
+    int shift;
+};
+
+__host__ inline PixelMode make_pixel_mode(const QuantParams& q) {
+    PixelMode m{q.nbins <= 256, -1};
+    if (q.kind == SPCT_SRC_GRAY_U8 && q.fast_u8 && q.nbins <= 256 && (q.nbins & (q.nbins - 1)) == 0) {
+        int s = 8;
+        while ((1 << (8 - s)) != q.nbins) --s;
+        m.shift = s;
+    }
+    return m;
+}
+
+// Packed bins of pixels (x .. x+3, y).  x is a multiple of 4.
+__device__ __forceinline__ uint32_t load_bins4(const QuantParams& q, const PixelMode& m, int x, int y, int k0, int nb) {
+    if (m.shift >= 0) {
+        const int64_t off = static_cast<int64_t>(y) * q.pitch + x;
+        const uint8_t* p = static_cast<const uint8_t*>(q.p0) + off;
+        uint32_t w;
+        if (x + 3 < q.width && (reinterpret_cast<uintptr_t>(p) & 3) == 0) {
+            w = __ldg(reinterpret_cast<const uint32_t*>(p));
+        } else {
+            w = 0;
+#pragma unroll
+            for (int j = 0; j < 4; ++j)
+                if (x + j < q.width) w |= static_cast<uint32_t>(__ldg(p + j)) << (8 * j);
+        }
+        return (w >> m.shift) & (0x01010101u * (0xFFu >> m.shift));
+    }
+    if (m.byte_mode) {
+        uint32_t w = 0;
+        const bool full = x + 3 < q.width;
+        if (full && q.kind == SPCT_SRC_GRAY_U8 &&
+            ((reinterpret_cast<uintptr_t>(q.p0) + static_cast<int64_t>(y) * q.pitch + x) & 3) == 0) {
+            const uint32_t v = __ldg(reinterpret_cast<const uint32_t*>(static_cast<const uint8_t*>(q.p0) +
+                                                                        static_cast<int64_t>(y) * q.pitch + x));
+#pragma unroll
+            for (int j = 0; j < 4; ++j) w |= static_cast<uint32_t>(bin_of_u8((v >> (8 * j)) & 0xFFu, q)) << (8 * j);
+        } else {
+#pragma unroll
+            for (int j = 0; j < 4; ++j)
+                if (x + j < q.width) w |= static_cast<uint32_t>(pixel_bin(q, x + j, y)) << (8 * j);
+        }
+        return w;
+    }
+    return load_rel4(q, x, y, k0, nb);
+}
+
+// Inclusive warp scan step with the shuffle's in-range predicate (no select).
+__device__ __forceinline__ uint32_t scan_add(uint32_t v, int o) {
+    uint32_t r;
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t.reg .u32 t;\n\t"
+        "shfl.sync.up.b32 t|p, %1, %2, 0, 0xffffffff;\n\t"
+        "@p add.u32 %1, %1, t;\n\t"
+        "mov.u32 %0, %1;\n\t}"
+        : "=r"(r), "+r"(v)
+        : "r"(o));
+    return r;
+}
+
+__device__ __forceinline__ uint32_t warp_incl_scan(uint32_t v) {
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) v = scan_add(v, o);
+    return v;
+}
 
 template <int B>
 __device__ __forceinline__ void vpart_init(uint32_t (&V)[4][B], const uint32_t* __restrict__ Hb, int band, int Lb,
@@ -35,43 +110,37 @@ __device__ __forceinline__ void vpart_init(uint32_t (&V)[4][B], const uint32_t* 
     }
 }
 
-// One row of the sweep.  `lt_row` points at L(y, kl0 .. kl0+B) (16-byte aligned) or is
-// null for the first strip; `rowp` at column x0 of plane kl0, row y; stores go to
-// rowp + k*plane_pitch when `store` and k < k_live.
-template <int B>
-__device__ __forceinline__ void vpart_row(uint32_t (&V)[4][B], uint32_t cur, const uint32_t* __restrict__ lt_row,
-                                          int lane, uint32_t* rowp, int64_t plane_pitch, bool store, int k_live) {
+// One row of the sweep.  `kpat0` = k0 * 0x01010101 in byte mode (k0 = global bin of
+// the warp's first plane), 0 in relative mode.  `lt_row` points at L(y, kl0 ..) or is
+// null for the first strip; `p` at column x0 of the warp's first plane in row y.
+// GUARD: the slab has fewer than B live planes (k_live); `store`: lane inside the pitch.
+template <int B, bool GUARD>
+__device__ __forceinline__ void vpart_row(uint32_t (&V)[4][B], uint32_t bins4, uint32_t kpat0,
+                                          const uint32_t* __restrict__ lt_row, uint32_t* p, int64_t plane_pitch,
+                                          bool store, int k_live) {
 #pragma unroll
     for (int g = 0; g < B / 4; ++g) {
         uint4 L = make_uint4(0, 0, 0, 0);
         if (lt_row) L = __ldg(reinterpret_cast<const uint4*>(lt_row) + g);
         uint32_t P[4];
-        uint32_t packed = 0;
 #pragma unroll
-        for (int i = 0; i < 4; ++i) {
-            const uint32_t k = 4 * g + i;
-            P[i] = match_bytes(cur, 0x01010101u * k) * 0x01010101u;
-            packed |= (P[i] >> 24) << (8 * i);
-        }
-        uint32_t v = packed;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const uint32_t t = __shfl_up_sync(0xffffffffu, v, o);
-            if (lane >= o) v += t;
-        }
-        const uint32_t excl = v - packed;
+        for (int i = 0; i < 4; ++i)
+            P[i] = match_bytes(bins4, kpat0 + 0x01010101u * static_cast<uint32_t>(4 * g + i)) * 0x01010101u;
+        // lane totals (byte 3 of each prefix) -> one word, four bins
+        const uint32_t packed = __byte_perm(__byte_perm(P[0], P[1], 0x0073), __byte_perm(P[2], P[3], 0x0073), 0x5410);
+        const uint32_t excl = warp_incl_scan(packed) - packed;
         const uint32_t Lk[4] = {L.x, L.y, L.z, L.w};
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
             const int k = 4 * g + i;
-            const uint32_t base = Lk[i] + ((excl >> (8 * i)) & 0xFFu);
-            V[0][k] += base + (P[i] & 0xFFu);
-            V[1][k] += base + ((P[i] >> 8) & 0xFFu);
-            V[2][k] += base + ((P[i] >> 16) & 0xFFu);
+            const uint32_t base = Lk[i] + __byte_perm(excl, 0, 0x4440 + i);
+            V[0][k] += base + __byte_perm(P[i], 0, 0x4440);
+            V[1][k] += base + __byte_perm(P[i], 0, 0x4441);
+            V[2][k] += base + __byte_perm(P[i], 0, 0x4442);
             V[3][k] += base + (P[i] >> 24);
-            if (store && k < k_live)
-                __stcs(reinterpret_cast<uint4*>(rowp + static_cast<int64_t>(k) * plane_pitch),
-                       make_uint4(V[0][k], V[1][k], V[2][k], V[3][k]));
+            if (store && (!GUARD || k < k_live))
+                __stcs(reinterpret_cast<uint4*>(p), make_uint4(V[0][k], V[1][k], V[2][k], V[3][k]));
+            p += plane_pitch;
         }
     }
 }
