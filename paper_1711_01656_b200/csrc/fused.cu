@@ -104,15 +104,47 @@ __global__ void prep_kernel(const double* __restrict__ tmpl, int bin0, int bins,
     }
 }
 
+// Window counts of bin k for the lane's four windows (right edges at strip columns
+// 4l..4l+3), returned as two u16 pairs.  `vw` = vc row of bin k at word 2*lane, `g` the
+// warp's staging row for this bin (double-buffered by bin parity).
+__device__ __forceinline__ void window_counts(const uint32_t* vw, uint32_t* g, int lane, int pw, int psh,
+                                              uint32_t& c0, uint32_t& c1) {
+    const uint2 wa = *reinterpret_cast<const uint2*>(vw);
+    const uint2 wb = *reinterpret_cast<const uint2*>(vw + 64);
+    // in-lane inclusive prefix of the 4 columns of each half (u16 pairs)
+    uint32_t a0 = wa.x * 0x10001u;
+    uint32_t a1 = wa.y * 0x10001u + __byte_perm(a0, 0, 0x3232);
+    uint32_t b0 = wb.x * 0x10001u;
+    uint32_t b1 = wb.y * 0x10001u + __byte_perm(b0, 0, 0x3232);
+    const uint32_t tot = __byte_perm(a1, b1, 0x7632);  // {sum a, sum b}
+    const uint32_t inc = warp_incl_scan(tot);
+    const uint32_t ex = inc - tot;
+    const uint32_t T1 = __shfl_sync(0xffffffffu, inc, 31) & 0xFFFFu;
+    const uint32_t ba = __byte_perm(ex, 0, 0x1010);
+    const uint32_t bb = __byte_perm(ex, 0, 0x3232) + T1 * 0x10001u;
+    a0 += ba;
+    a1 += ba;
+    b0 += bb;
+    b1 += bb;
+    *reinterpret_cast<uint2*>(g + 2 * lane) = make_uint2(a0, a1);
+    *reinterpret_cast<uint2*>(g + 64 + 2 * lane) = make_uint2(b0, b1);
+    __syncwarp();
+    const uint32_t q0 = g[pw], q1 = g[pw + 1], q2 = g[pw + 2];
+    c0 = b0 - __funnelshift_r(q0, q1, psh);
+    c1 = b1 - __funnelshift_r(q1, q2, psh);
+}
+
 template <bool STORE, bool FAST>
 __global__ void __launch_bounds__(256, 2) sweep_match_kernel(QuantParams q, PixelMode pm, spct_ih out, int Lb, int Wp,
                                                              int band_rows, const uint32_t* __restrict__ Lt,
                                                              const uint32_t* __restrict__ Hb, FusedParams f) {
     extern __shared__ uint4 smem_raw[];
-    uint32_t* vc = reinterpret_cast<uint32_t*>(smem_raw);            // [128 bins][128 words]
-    uint32_t* gbuf = vc + kGroupBins * kVcWords;                       // [8 warps][2][128 words]
+    uint32_t* vc = reinterpret_cast<uint32_t*>(smem_raw);                 // [128 bins][128 words]
+    uint32_t* gbuf = vc + kGroupBins * kVcWords;                            // [8 warps][2][128 words]
     double* red = reinterpret_cast<double*>(gbuf + kWarps * 2 * kVcWords);  // [2 rows][8 warps][128]
     uint32_t* srep_s = reinterpret_cast<uint32_t*>(red + 2 * kWarps * kStrip);  // [128]
+    uint32_t* lrow = srep_s + kGroupBins;                                   // [2 rows][128] row carries
+    uint16_t* rowbins = reinterpret_cast<uint16_t*>(lrow + 2 * kGroupBins);  // [2 rows][128] strip bins
 
     // Both variants are launched; the one that does not match the template prep exits.
     if ((__ldg(f.prep) != 0) != FAST) return;
@@ -134,12 +166,11 @@ __global__ void __launch_bounds__(256, 2) sweep_match_kernel(QuantParams q, Pixe
     const uint32_t kpat0 = pm.byte_mode ? 0x01010101u * static_cast<uint32_t>(k0) : 0u;
 
     for (int i = tid; i < kGroupBins * kVcWords; i += blockDim.x) vc[i] = 0;
-    if (FAST && tid < kGroupBins) srep_s[tid] = tid < nb_cta ? __ldg(f.prep + 1 + g0 + tid) : 0u;
+    if (tid < kGroupBins) srep_s[tid] = (FAST && tid < nb_cta) ? __ldg(f.prep + 1 + g0 + tid) : 0u;
 
     uint32_t V[4][kB];
     if (STORE && warp_live) vpart_init<kB>(V, Hb, band, Lb, kl0, Wp, xl);
     uint32_t* base_ptr = STORE ? out.data + static_cast<int64_t>(kl0) * out.plane_pitch + xl : nullptr;
-    const uint32_t* lt_strip = (Lt && strip > 0) ? Lt + static_cast<int64_t>(strip) * H * Lb + kl0 : nullptr;
     const bool lane_live = xl < out.row_pitch;
     const long long S = FAST ? f.S_group[g0 / kGroupBins] : 0;
     // G(e - kw): first extended cell of this lane's four windows, as a word and a bit shift
@@ -147,6 +178,16 @@ __global__ void __launch_bounds__(256, 2) sweep_match_kernel(QuantParams q, Pixe
     const int pw = idx >> 1, psh = (idx & 1) * 16;
     uint32_t* gb = gbuf + warp * 2 * kVcWords;
     const uint32_t* vbase = vc + warp * kB * kVcWords + 2 * lane;
+
+    // staging thread: extended column tid; prefetch one row ahead
+    const int xt = xs - kStrip + tid;
+    const bool xt_live = xt >= 0 && xt < W;
+    const uint32_t* lt_cta = (STORE && Lt && strip > 0 && tid < kGroupBins && g0 + tid < Lb)
+                                 ? Lt + static_cast<int64_t>(strip) * H * Lb + g0 + tid
+                                 : nullptr;
+    int pn = (xt_live) ? pixel_bin(q, xt, ystart) : 0xFFFF;
+    int po = -1;  // ystart - kh < ystart: nothing to remove on the first row
+    uint32_t lpre = lt_cta ? __ldg(lt_cta + static_cast<int64_t>(ystart) * Lb) : 0u;
     __syncthreads();
 
     // deferred cross-warp combine of row yy (thread t < 128: window ending at strip column t)
@@ -178,81 +219,86 @@ __global__ void __launch_bounds__(256, 2) sweep_match_kernel(QuantParams q, Pixe
 
     int pend_y = -1;
     for (int y = ystart; y < y1; ++y) {
-        __syncthreads();  // A: previous row's vc / red reads are done
+        __syncthreads();  // A: previous row's vc / red / staging reads are done
         if (pend_y >= 0) {
             combine(pend_y);
             pend_y = -1;
         }
-        {   // vertical running histogram: add row y, remove row y - kh
-            const int x = xs - kStrip + tid;
-            if (x >= 0 && x < W) {
+        {   // stage row y: vertical running histogram (add row y, remove row y - kh),
+            // the strip's bins and row carries for the sweep, then prefetch row y + 1
+            if (xt_live) {
                 const uint32_t inc = 1u << (16 * (tid & 1));
-                const int bn = pixel_bin(q, x, y) - out.bin0 - g0;
+                const int bn = pn - out.bin0 - g0;
                 if (static_cast<unsigned>(bn) < static_cast<unsigned>(nb_cta))
                     atomicAdd(&vc[bn * kVcWords + (tid >> 1)], inc);
-                const int yo = y - f.kh;
-                if (yo >= ystart) {  // rows before ystart were never added
-                    const int bo = pixel_bin(q, x, yo) - out.bin0 - g0;
-                    if (static_cast<unsigned>(bo) < static_cast<unsigned>(nb_cta))
-                        atomicSub(&vc[bo * kVcWords + (tid >> 1)], inc);
-                }
+                const int bo = po - out.bin0 - g0;
+                if (po >= 0 && static_cast<unsigned>(bo) < static_cast<unsigned>(nb_cta))
+                    atomicSub(&vc[bo * kVcWords + (tid >> 1)], inc);
+            }
+            if (tid >= kStrip) rowbins[(y & 1) * kStrip + tid - kStrip] = static_cast<uint16_t>(pn);
+            else lrow[(y & 1) * kGroupBins + tid] = lpre;
+            if (y + 1 < y1) {
+                pn = xt_live ? pixel_bin(q, xt, y + 1) : 0xFFFF;
+                const int yo = y + 1 - f.kh;
+                po = (xt_live && yo >= ystart) ? pixel_bin(q, xt, yo) : -1;
+                if (lt_cta) lpre = __ldg(lt_cta + static_cast<int64_t>(y + 1) * Lb);
             }
         }
-        __syncthreads();  // B: vc holds rows (y - kh, y]
+        __syncthreads();  // B: vc holds rows (y - kh, y]; staging rows ready
         if (y < y0) continue;  // pre-roll rows only feed vc
-
-        if (STORE && warp_live) {
-            const uint32_t cur = load_bins4(q, pm, xl, y, k0, kB);
-            vpart_row<kB, true>(V, cur, kpat0, lt_strip ? lt_strip + static_cast<int64_t>(y) * Lb : nullptr,
-                                base_ptr + static_cast<int64_t>(y) * out.row_pitch, out.plane_pitch, lane_live,
-                                k_live);
+        const bool match_row = y >= f.kh - 1;
+        if (!warp_live || (!STORE && !match_row)) {
+            pend_y = match_row ? y : pend_y;
+            continue;
         }
-        if (y < f.kh - 1) continue;  // no window ends on this row yet
 
-        if (warp_live) {
-            uint32_t I0 = 0, I1 = 0, C0 = 0, C1 = 0;
-            double acc[4] = {0.0, 0.0, 0.0, 0.0};
-#pragma unroll 4
-            for (int k = 0; k < kB; ++k) {
-                const uint32_t* vw = vbase + k * kVcWords;
-                const uint2 wa = *reinterpret_cast<const uint2*>(vw);
-                const uint2 wb = *reinterpret_cast<const uint2*>(vw + 64);
-                // in-lane inclusive prefix of the 4 columns of each half (u16 pairs)
-                uint32_t a0 = wa.x * 0x10001u;
-                uint32_t a1 = wa.y * 0x10001u + __byte_perm(a0, 0, 0x3232);
-                uint32_t b0 = wb.x * 0x10001u;
-                uint32_t b1 = wb.y * 0x10001u + __byte_perm(b0, 0, 0x3232);
-                const uint32_t tot = __byte_perm(a1, b1, 0x7632);  // {sum a, sum b}
-                const uint32_t inc = warp_incl_scan(tot);
-                const uint32_t ex = inc - tot;
-                const uint32_t T1 = __shfl_sync(0xffffffffu, inc, 31) & 0xFFFFu;
-                const uint32_t ba = __byte_perm(ex, 0, 0x1010);
-                const uint32_t bb = __byte_perm(ex, 0, 0x3232) + T1 * 0x10001u;
-                a0 += ba;
-                a1 += ba;
-                b0 += bb;
-                b1 += bb;
-                uint32_t* g = gb + (k & 1) * kVcWords;
-                *reinterpret_cast<uint2*>(g + 2 * lane) = make_uint2(a0, a1);
-                *reinterpret_cast<uint2*>(g + 64 + 2 * lane) = make_uint2(b0, b1);
-                __syncwarp();
-                const uint32_t q0 = g[pw], q1 = g[pw + 1], q2 = g[pw + 2];
-                const uint32_t p0 = __funnelshift_r(q0, q1, psh), p1 = __funnelshift_r(q1, q2, psh);
-                const uint32_t c0 = b0 - p0, c1 = b1 - p1;  // window counts {j=0, j=1}, {j=2, j=3}
-                if (FAST) {
-                    const uint32_t sk = srep_s[warp * kB + k];
-                    I0 += min_u16x2(c0, sk);
-                    I1 += min_u16x2(c1, sk);
-                    C0 += c0;
-                    C1 += c1;
-                } else if (k < k_live) {
-                    const double t = __ldg(f.tmpl + k0 + k);
-                    acc[0] = __dadd_rn(acc[0], general_term(c0 & 0xFFFFu, t, f));
-                    acc[1] = __dadd_rn(acc[1], general_term(c0 >> 16, t, f));
-                    acc[2] = __dadd_rn(acc[2], general_term(c1 & 0xFFFFu, t, f));
-                    acc[3] = __dadd_rn(acc[3], general_term(c1 >> 16, t, f));
+        uint32_t bins4 = 0;
+        if (STORE) {
+            const uint2 rb2 = *reinterpret_cast<const uint2*>(rowbins + (y & 1) * kStrip + 4 * lane);
+            if (pm.byte_mode) {
+                bins4 = __byte_perm(rb2.x, rb2.y, 0x6420);
+            } else {
+                const uint32_t b4[4] = {rb2.x & 0xFFFFu, rb2.x >> 16, rb2.y & 0xFFFFu, rb2.y >> 16};
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    const uint32_t r = b4[j] - static_cast<uint32_t>(k0);
+                    bins4 |= (r < static_cast<uint32_t>(kB) ? r : 0xFFu) << (8 * j);
                 }
             }
+        }
+        const uint4* lr = reinterpret_cast<const uint4*>(lrow + (y & 1) * kGroupBins + warp * kB);
+        uint32_t* prow = STORE ? base_ptr + static_cast<int64_t>(y) * out.row_pitch : nullptr;
+
+        uint32_t I0 = 0, I1 = 0, C0 = 0, C1 = 0;
+        double acc[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+        for (int g = 0; g < kB / 4; ++g) {
+            if (STORE)
+                vpart_group<kB, true>(V, g, bins4, kpat0, lr[g], prow + static_cast<int64_t>(4 * g) * out.plane_pitch,
+                                      out.plane_pitch, lane_live, k_live);
+            if (match_row) {
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                    const int k = 4 * g + i;
+                    uint32_t c0, c1;
+                    window_counts(vbase + k * kVcWords, gb + (k & 1) * kVcWords, lane, pw, psh, c0, c1);
+                    if (FAST) {
+                        const uint32_t sk = srep_s[warp * kB + k];
+                        I0 += min_u16x2(c0, sk);
+                        I1 += min_u16x2(c1, sk);
+                        C0 += c0;
+                        C1 += c1;
+                    } else if (k < k_live) {
+                        const double t = __ldg(f.tmpl + k0 + k);
+                        acc[0] = __dadd_rn(acc[0], general_term(c0 & 0xFFFFu, t, f));
+                        acc[1] = __dadd_rn(acc[1], general_term(c0 >> 16, t, f));
+                        acc[2] = __dadd_rn(acc[2], general_term(c1 & 0xFFFFu, t, f));
+                        acc[3] = __dadd_rn(acc[3], general_term(c1 >> 16, t, f));
+                    }
+                }
+            }
+        }
+        if (match_row) {
             double* rb = red + (y & 1) * (kWarps * kStrip) + warp * kStrip;
             if (FAST) {
                 // per window: I | C << 16 in the low word of the slot
@@ -267,15 +313,15 @@ __global__ void __launch_bounds__(256, 2) sweep_match_kernel(QuantParams q, Pixe
                 rb[4 * lane + 2] = acc[2];
                 rb[4 * lane + 3] = acc[3];
             }
+            pend_y = y;
         }
-        pend_y = y;
     }
     __syncthreads();
     if (pend_y >= 0) combine(pend_y);
 }
 
 constexpr size_t kSmemBytes = (size_t(kGroupBins) * kVcWords + size_t(kWarps) * 2 * kVcWords) * 4 +
-                              size_t(2) * kWarps * kStrip * 8 + size_t(kGroupBins) * 4;
+                              size_t(2) * kWarps * kStrip * 8 + size_t(kGroupBins) * 4 * 3 + size_t(2) * kStrip * 2;
 
 }  // namespace spct_fused
 

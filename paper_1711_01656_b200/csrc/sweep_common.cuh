@@ -146,3 +146,33 @@ __device__ __forceinline__ void vpart_row(uint32_t (&V)[4][B], uint32_t bins4, u
 }
 
 }  // namespace spct_dev
+
+namespace spct_dev {
+
+// One group of four planes (4g .. 4g+3) of vpart_row, for callers that interleave
+// the row update with other work.  `p` points at plane 4g of the row.
+template <int B, bool GUARD>
+__device__ __forceinline__ void vpart_group(uint32_t (&V)[4][B], int g, uint32_t bins4, uint32_t kpat0, uint4 L,
+                                            uint32_t* p, int64_t plane_pitch, bool store, int k_live) {
+    uint32_t P[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+        P[i] = match_bytes(bins4, kpat0 + 0x01010101u * static_cast<uint32_t>(4 * g + i)) * 0x01010101u;
+    const uint32_t packed = __byte_perm(__byte_perm(P[0], P[1], 0x0073), __byte_perm(P[2], P[3], 0x0073), 0x5410);
+    const uint32_t excl = warp_incl_scan(packed) - packed;
+    const uint32_t Lk[4] = {L.x, L.y, L.z, L.w};
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        const int k = 4 * g + i;
+        const uint32_t base = Lk[i] + __byte_perm(excl, 0, 0x4440 + i);
+        V[0][k] += base + __byte_perm(P[i], 0, 0x4440);
+        V[1][k] += base + __byte_perm(P[i], 0, 0x4441);
+        V[2][k] += base + __byte_perm(P[i], 0, 0x4442);
+        V[3][k] += base + (P[i] >> 24);
+        if (store && (!GUARD || k < k_live))
+            __stcs(reinterpret_cast<uint4*>(p), make_uint4(V[0][k], V[1][k], V[2][k], V[3][k]));
+        p += plane_pitch;
+    }
+}
+
+}  // namespace spct_dev
