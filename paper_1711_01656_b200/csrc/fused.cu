@@ -185,8 +185,9 @@ __global__ void __launch_bounds__(256, 2) sweep_match_kernel(QuantParams q, Pixe
     const uint32_t* lt_cta = (STORE && Lt && strip > 0 && tid < kGroupBins && g0 + tid < Lb)
                                  ? Lt + static_cast<int64_t>(strip) * H * Lb + g0 + tid
                                  : nullptr;
-    int pn = (xt_live) ? pixel_bin(q, xt, ystart) : 0xFFFF;
-    int po = -1;  // ystart - kh < ystart: nothing to remove on the first row
+    // raw pixel values of the staging column, quantised one row after the load
+    uint64_t rn = xt_live ? pixel_raw(q, xt, ystart) : 0, ro = 0;
+    bool have_o = false;  // ystart - kh < ystart: nothing to remove on the first row
     uint32_t lpre = lt_cta ? __ldg(lt_cta + static_cast<int64_t>(ystart) * Lb) : 0u;
     __syncthreads();
 
@@ -226,6 +227,8 @@ __global__ void __launch_bounds__(256, 2) sweep_match_kernel(QuantParams q, Pixe
         }
         {   // stage row y: vertical running histogram (add row y, remove row y - kh),
             // the strip's bins and row carries for the sweep, then prefetch row y + 1
+            const int pn = xt_live ? bin_of_raw(rn, q) : 0xFFFF;
+            const int po = (xt_live && have_o) ? bin_of_raw(ro, q) : -1;
             if (xt_live) {
                 const uint32_t inc = 1u << (16 * (tid & 1));
                 const int bn = pn - out.bin0 - g0;
@@ -238,9 +241,12 @@ __global__ void __launch_bounds__(256, 2) sweep_match_kernel(QuantParams q, Pixe
             if (tid >= kStrip) rowbins[(y & 1) * kStrip + tid - kStrip] = static_cast<uint16_t>(pn);
             else lrow[(y & 1) * kGroupBins + tid] = lpre;
             if (y + 1 < y1) {
-                pn = xt_live ? pixel_bin(q, xt, y + 1) : 0xFFFF;
                 const int yo = y + 1 - f.kh;
-                po = (xt_live && yo >= ystart) ? pixel_bin(q, xt, yo) : -1;
+                have_o = yo >= ystart;
+                if (xt_live) {
+                    rn = pixel_raw(q, xt, y + 1);
+                    if (have_o) ro = pixel_raw(q, xt, yo);
+                }
                 if (lt_cta) lpre = __ldg(lt_cta + static_cast<int64_t>(y + 1) * Lb);
             }
         }

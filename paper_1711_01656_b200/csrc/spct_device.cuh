@@ -72,6 +72,38 @@ __device__ __forceinline__ int pixel_bin(const QuantParams& q, int x, int y) {
     }
 }
 
+// Split form of pixel_bin for software pipelining: pixel_raw issues the load(s) and
+// returns the raw value (u8 / u16 / packed RGB / f64 bits); bin_of_raw quantises it
+// later, so the load latency overlaps a whole row of work.
+__device__ __forceinline__ uint64_t pixel_raw(const QuantParams& q, int x, int y) {
+    const int64_t i = static_cast<int64_t>(y) * q.pitch + x;
+    switch (q.kind) {
+        case SPCT_SRC_BINS_U16:
+            return __ldg(static_cast<const uint16_t*>(q.p0) + i);
+        case SPCT_SRC_GRAY_U8:
+            return __ldg(static_cast<const uint8_t*>(q.p0) + i);
+        case SPCT_SRC_RGB_U8:
+            return static_cast<uint64_t>(__ldg(static_cast<const uint8_t*>(q.p0) + i)) |
+                   (static_cast<uint64_t>(__ldg(static_cast<const uint8_t*>(q.p1) + i)) << 8) |
+                   (static_cast<uint64_t>(__ldg(static_cast<const uint8_t*>(q.p2) + i)) << 16);
+        default:
+            return static_cast<uint64_t>(__double_as_longlong(__ldg(static_cast<const double*>(q.p0) + i)));
+    }
+}
+
+__device__ __forceinline__ int bin_of_raw(uint64_t raw, const QuantParams& q) {
+    switch (q.kind) {
+        case SPCT_SRC_BINS_U16:
+            return static_cast<int>(raw);
+        case SPCT_SRC_GRAY_U8:
+            return bin_of_u8(static_cast<uint32_t>(raw), q);
+        case SPCT_SRC_RGB_U8:
+            return bin_of_u8(gray_of(raw & 0xFF, (raw >> 8) & 0xFF, (raw >> 16) & 0xFF), q);
+        default:
+            return quantize_value(__longlong_as_double(static_cast<long long>(raw)), q);
+    }
+}
+
 // Four consecutive pixels (x .. x+3) of row y as relative bins packed in bytes:
 // byte j = bin(x+j) - k0 when it lies in [0, nb), else 0xFF (never matches).
 // Columns >= width are 0xFF as well.  The aligned gray/bins fast paths issue one
