@@ -18,8 +18,8 @@ OBJDIR     = build/obj
 CU_OBJS    = $(patsubst $(CSRC)/%.cu,$(OBJDIR)/%.o,$(CU_SRCS))
 HOST_OBJS  = $(patsubst $(CSRC)/host/%.cpp,$(OBJDIR)/host_%.o,$(HOST_SRCS))
 
-.PHONY: all lib oracle clean sass
-all: lib oracle
+.PHONY: all lib oracle clean sass dropin
+all: lib oracle dropin
 
 lib: $(LIB)
 
@@ -43,3 +43,11 @@ sass: $(LIB)
 clean:
 	rm -rf build $(LIB)
 	$(MAKE) -C oracle clean
+
+# C++ drop-in test: reference-style cases against include/spct/*.hpp, linked with the
+# product library (run on a GPU box by tests/test_dropin_cpp.py).
+DROPIN = build/dropin_test
+dropin: $(DROPIN)
+$(DROPIN): tests/cpp/dropin_test.cpp $(LIB) $(wildcard include/spct/*.hpp)
+	@mkdir -p build
+	$(CXX) -O2 -std=c++20 -Iinclude -o $@ tests/cpp/dropin_test.cpp -L$(PKG) -lspct_b200 -Wl,-rpath,'$$ORIGIN/../$(PKG)'

@@ -216,9 +216,10 @@ def run_ours(args) -> None:
 
     import paper_1711_01656_b200 as P
     from paper_1711_01656_b200 import profiling
+    from paper_1711_01656_b200.sharding import max_over_ranks, reduce_partials, slab_bounds
 
     nbins = BINS_PER_GPU * world
-    bin0 = BINS_PER_GPU * rank
+    bin0, bin1 = slab_bounds(nbins, world, rank)
     frame_h = make_frame(W_IMG, H_IMG)
     tmpl = template_hist(frame_h, nbins, KW, KH)
     dev = torch.device("cuda", local)
@@ -235,7 +236,7 @@ def run_ours(args) -> None:
         P.build_and_match(src, nbins, None, KW, KH, P_ORDER, bin0=bin0, bins=BINS_PER_GPU, out=t, partial=part,
                           tmpl_dev=tm)
         if world > 1:
-            dist.reduce(part, dst=0, op=dist.ReduceOp.SUM)
+            reduce_partials(part, dst=0)
         if rank == 0:
             P.hist_finalize(part, W_IMG, H_IMG, KW, KH, P_ORDER, out=lmap)
 
@@ -255,11 +256,7 @@ def run_ours(args) -> None:
             b.record(stream)
         barrier()
         ms = sum(a.elapsed_time(b) for a, b in ev)
-        if world > 1:
-            x = torch.tensor([ms], dtype=torch.float64, device=dev)
-            dist.all_reduce(x, op=dist.ReduceOp.MAX)
-            ms = float(x.item())
-        return ms / k
+        return max_over_ranks(ms, dev) / k
 
     for _ in range(args.warmup):
         step(frame)

@@ -1,0 +1,188 @@
+// Drop-in check of the C++ API: reference-style test cases written against the
+// unchanged spct:: signatures (cf. proj/tests/test_integral.cpp, test_likelihood.cpp,
+// test_imagecore.cpp), compiled against include/spct/*.hpp and linked with
+// libspct_b200.so instead of the reference library.  Run by tests/test_dropin_cpp.py
+// on a GPU box; exits non-zero on the first failed check.
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <random>
+#include <string>
+#include <vector>
+
+#include "spct/imagecore.hpp"
+#include "spct/integral.hpp"
+#include "spct/likelihood.hpp"
+
+using namespace spct;
+
+static int g_checks = 0;
+#define CHECK(cond)                                                                  \
+    do {                                                                             \
+        ++g_checks;                                                                  \
+        if (!(cond)) {                                                               \
+            std::fprintf(stderr, "%s:%d: CHECK failed: %s\n", __FILE__, __LINE__, #cond); \
+            std::exit(1);                                                            \
+        }                                                                            \
+    } while (0)
+#define CHECK_THROWS_AS(expr, E)      \
+    do {                              \
+        bool thrown = false;          \
+        try {                         \
+            (void)(expr);             \
+        } catch (const E&) {          \
+            thrown = true;            \
+        }                             \
+        CHECK(thrown);                \
+    } while (0)
+
+static BinMap random_binmap(int w, int h, int bins, unsigned seed) {
+    std::mt19937 rng(seed);
+    std::uniform_int_distribution<int> d(0, bins - 1);
+    BinMap bm(w, h, bins);
+    for (auto& v : bm.data) v = static_cast<std::uint16_t>(d(rng));
+    return bm;
+}
+
+// Plain sequential recurrence (integral.cpp:348-361) as the in-test oracle.
+static std::vector<std::uint64_t> seq_tensor(const BinMap& bm) {
+    const std::size_t rs = bm.width + 1, ps = rs * (bm.height + 1);
+    std::vector<std::uint64_t> t(ps * bm.bins, 0);
+    for (int k = 0; k < bm.bins; ++k)
+        for (int y = 1; y <= bm.height; ++y)
+            for (int x = 1; x <= bm.width; ++x)
+                t[k * ps + y * rs + x] = t[k * ps + y * rs + x - 1] + t[k * ps + (y - 1) * rs + x] -
+                                         t[k * ps + (y - 1) * rs + x - 1] + (bm.at(x - 1, y - 1) == k);
+    return t;
+}
+
+int main() {
+    {  // hand-computed 2x2 prefix planes (test_integral.cpp:40-57)
+        BinMap bm(2, 2, 2);
+        bm.at(0, 0) = 0;
+        bm.at(1, 0) = 1;
+        bm.at(0, 1) = 1;
+        bm.at(1, 1) = 0;
+        auto t = build_integral_histogram(bm);
+        CHECK(t.at(0, 2, 2) == 2);
+        CHECK(t.at(1, 2, 2) == 2);
+        CHECK(t.at(0, 1, 1) == 1);
+        CHECK(t.at(1, 1, 1) == 0);
+        for (int k = 0; k < 2; ++k)
+            for (int i = 0; i < 3; ++i) {
+                CHECK(t.at(k, 0, i) == 0);
+                CHECK(t.at(k, i, 0) == 0);
+            }
+    }
+    {  // all schedules produce identical tensors, equal to the recurrence (test_integral.cpp:72-87)
+        const int sizes[][2] = {{1, 1}, {5, 3}, {33, 31}, {64, 64}, {70, 129}, {256, 40}};
+        unsigned seed = 1000;
+        for (auto& s : sizes) {
+            BinMap bm = random_binmap(s[0], s[1], 16, seed++);
+            auto want = seq_tensor(bm);
+            for (auto kind : {ScanScheduleKind::Sequential, ScanScheduleKind::ScanTransposeScan,
+                              ScanScheduleKind::CrossWeaveTiled, ScanScheduleKind::WavefrontTiled}) {
+                auto t = build_integral_histogram(bm, {kind, 64, 4});
+                CHECK(t.data == want);
+                CHECK(t.data.size() == want.size());
+            }
+        }
+    }
+    {  // region histogram vs brute force, degenerate and out-of-range rects (test_integral.cpp:89-132)
+        BinMap bm = random_binmap(200, 150, 32, 7);
+        auto t = build_integral_histogram(bm, {ScanScheduleKind::WavefrontTiled, 32, 4});
+        std::mt19937 rng(8);
+        for (int i = 0; i < 50; ++i) {
+            int x1 = rng() % 200, y1 = rng() % 150;
+            Rect r{x1, y1, static_cast<int>(rng() % (200 - x1 + 1)), static_cast<int>(rng() % (150 - y1 + 1))};
+            auto hist = region_histogram(t, r);
+            std::uint64_t total = 0;
+            for (int k = 0; k < 32; ++k) {
+                std::uint64_t n = 0;
+                for (int y = r.y; y < r.bottom(); ++y)
+                    for (int x = r.x; x < r.right(); ++x) n += bm.at(x, y) == k;
+                CHECK(hist[k] == n);
+                CHECK(region_count(t, k, r) == n);
+                total += hist[k];
+            }
+            CHECK(total == static_cast<std::uint64_t>(r.area()));
+        }
+        auto z = region_histogram(t, Rect{3, 3, 0, 0});
+        for (auto v : z) CHECK(v == 0);
+        CHECK_THROWS_AS(region_histogram(t, Rect{195, 145, 8, 8}), contract_error);
+        CHECK_THROWS_AS(region_histogram(t, Rect{-1, 0, 2, 2}), contract_error);
+        CHECK_THROWS_AS(region_count(t, 40, Rect{0, 0, 1, 1}), contract_error);
+    }
+    {  // build contract violations (test_integral.cpp:190-206)
+        BinMap bm = random_binmap(16, 16, 4, 3);
+        BinMap bad = bm;
+        bad.data[7] = 4;
+        CHECK_THROWS_AS(build_integral_histogram(bad), contract_error);
+        CHECK_THROWS_AS(build_integral_histogram(bm, {}, 64), contract_error);
+        CHECK_THROWS_AS(build_integral_histogram(BinMap{}), contract_error);
+        CHECK_THROWS_AS(build_integral_histogram(bm, {ScanScheduleKind::WavefrontTiled, 32, 0}), contract_error);
+        CHECK(schedule_from_string("wavefront") == ScanScheduleKind::WavefrontTiled);
+        CHECK_THROWS_AS(schedule_from_string("bogus"), contract_error);
+    }
+    {  // quantize / grayscale (test_imagecore.cpp:48-50, 88-106)
+        GrayImage img(4, 1);
+        img.data = {0, 64, 128, 255};
+        BinMap bm = quantize(img, 32, 0.0, 256.0);
+        CHECK(bm.at(0, 0) == 0 && bm.at(1, 0) == 8 && bm.at(2, 0) == 16 && bm.at(3, 0) == 31);
+        BinMap c = quantize(img, 4, 100.0, 200.0);
+        CHECK(c.at(0, 0) == 0 && c.at(3, 0) == 3);
+        CHECK_THROWS_AS(quantize(img, 0), contract_error);
+        CHECK_THROWS_AS(quantize(img, 70000), contract_error);
+        CHECK_THROWS_AS(quantize(img, 8, 10.0, 10.0), contract_error);
+        ColorImage col(2, 1);
+        col.r = {10, 255};
+        col.g = {20, 255};
+        col.b = {40, 255};
+        GrayImage g = to_grayscale(col);
+        CHECK(g.data[0] == 23 && g.data[1] == 255);
+    }
+    {  // hist distance: identity, disjoint, hand fixture (test_likelihood.cpp:156-194)
+        GrayImage img(12, 10);
+        std::mt19937 rng(3);
+        std::uniform_int_distribution<int> d(0, 255);
+        for (auto& p : img.data) p = static_cast<std::uint8_t>(d(rng));
+        BinMap bm = quantize(img, 8);
+        auto t = build_integral_histogram(bm);
+        Rect win{4, 3, 5, 4};
+        std::vector<double> th(8, 0.0);
+        for (int y = win.y; y < win.bottom(); ++y)
+            for (int x = win.x; x < win.right(); ++x) th[bm.at(x, y)] += 1.0;
+        for (double& v : th) v /= win.area();
+        LikelihoodMap map = hist_distance_map(t, th, win.w, win.h, 1.0);
+        CHECK(std::abs(map.at(win.x + 2, win.y + 1) - 1.0) <= 1e-12);
+        GrayImage dark(9, 9, 10);
+        auto td = build_integral_histogram(quantize(dark, 4));
+        std::vector<double> bright(4, 0.0);
+        bright[3] = 1.0;
+        for (double v : hist_distance_map(td, bright, 3, 3, 1.0).values) CHECK(std::abs(v) <= 1e-12);
+        GrayImage six(2, 3);
+        six.data = {0, 100, 100, 200, 200, 200};
+        auto t6 = build_integral_histogram(quantize(six, 3));
+        LikelihoodMap h6 = hist_distance_map(t6, {0.4, 0.4, 0.2}, 2, 3, 1.0);
+        CHECK(std::abs(h6.at(0, 1) - 0.7) <= 1e-12);
+        CHECK_THROWS_AS(hist_distance_map(t6, {0.4, 0.4, 0.2}, 2, 3, 0.5), contract_error);
+        CHECK_THROWS_AS(hist_distance_map(t6, {0.5, 0.5}, 2, 3, 1.0), contract_error);
+        // the fused frame path agrees with build + hist_distance_map
+        IntegralHistogramTensor tf;
+        LikelihoodMap mf = likelihood_from_frame(img, 8, th, win.w, win.h, 1.0, &tf);
+        CHECK(tf.data == t.data);
+        for (std::size_t i = 0; i < mf.values.size(); ++i)
+            CHECK(std::abs(mf.values[i] - map.values[i]) <= 1e-5 * std::abs(map.values[i]) + 1e-12);
+    }
+    {  // analytics (test_integral.cpp:155-188)
+        auto s = schedule_stats(1024, 1024, 32, 1024);
+        CHECK(s.wavefront_iterations == 63 && s.tile_count == 1024);
+        CHECK(s.scan_efficiency > 0.29 && s.scan_efficiency < 0.31);
+        auto e = estimate_memory(512, 512, 32, 8);
+        CHECK(e.padded_bytes == 32ull * 513 * 513 * 8 && e.raw_bytes == 64ull * 1024 * 1024);
+        CHECK(estimate_memory(100, 100, 0, 8).degenerate);
+        CHECK_THROWS_AS(estimate_memory(-1, 4, 4, 4), contract_error);
+    }
+    std::printf("dropin_test: %d checks passed\n", g_checks);
+    return 0;
+}
