@@ -104,31 +104,35 @@ __global__ void prep_kernel(const double* __restrict__ tmpl, int bin0, int bins,
     }
 }
 
-// Window counts of bin k for the lane's four windows (right edges at strip columns
-// 4l..4l+3), returned as two u16 pairs.  `vw` = vc row of bin k at word 2*lane, `g` the
-// warp's staging row for this bin (double-buffered by bin parity).
-__device__ __forceinline__ void window_counts(const uint32_t* vw, uint32_t* g, int lane, int pw, int psh,
-                                              uint32_t& c0, uint32_t& c1) {
+// Window counts, phase 1: for bin row `vw` (vc of the bin at word 2*lane), the inclusive
+// prefix G of the 256 extended columns for the lane's 8 columns (u16 pairs): stages the
+// pairs in `g` (the warp's staging row for this bin) and returns the strip half b0, b1.
+__device__ __forceinline__ void window_prefix(const uint32_t* vw, uint32_t* g, int lane, uint32_t& b0,
+                                              uint32_t& b1) {
     const uint2 wa = *reinterpret_cast<const uint2*>(vw);
     const uint2 wb = *reinterpret_cast<const uint2*>(vw + 64);
-    // in-lane inclusive prefix of the 4 columns of each half (u16 pairs)
     uint32_t a0 = wa.x * 0x10001u;
     uint32_t a1 = wa.y * 0x10001u + __byte_perm(a0, 0, 0x3232);
-    uint32_t b0 = wb.x * 0x10001u;
-    uint32_t b1 = wb.y * 0x10001u + __byte_perm(b0, 0, 0x3232);
+    b0 = wb.x * 0x10001u;
+    b1 = wb.y * 0x10001u + __byte_perm(b0, 0, 0x3232);
     const uint32_t tot = __byte_perm(a1, b1, 0x7632);  // {sum a, sum b}
     const uint32_t inc = warp_incl_scan(tot);
     const uint32_t ex = inc - tot;
-    const uint32_t T1 = __shfl_sync(0xffffffffu, inc, 31) & 0xFFFFu;
+    const uint32_t T1 = __byte_perm(__shfl_sync(0xffffffffu, inc, 31), 0, 0x1010);  // total of the halo half
     const uint32_t ba = __byte_perm(ex, 0, 0x1010);
-    const uint32_t bb = __byte_perm(ex, 0, 0x3232) + T1 * 0x10001u;
+    const uint32_t bb = __byte_perm(ex, 0, 0x3232) + T1;
     a0 += ba;
     a1 += ba;
     b0 += bb;
     b1 += bb;
     *reinterpret_cast<uint2*>(g + 2 * lane) = make_uint2(a0, a1);
     *reinterpret_cast<uint2*>(g + 64 + 2 * lane) = make_uint2(b0, b1);
-    __syncwarp();
+}
+
+// Window counts, phase 2 (after a __syncwarp): c = G(e) - G(e - kw) for the lane's four
+// windows, as two u16 pairs {j=0, j=1}, {j=2, j=3}.
+__device__ __forceinline__ void window_diff(const uint32_t* g, int pw, int psh, uint32_t b0, uint32_t b1,
+                                            uint32_t& c0, uint32_t& c1) {
     const uint32_t q0 = g[pw], q1 = g[pw + 1], q2 = g[pw + 2];
     c0 = b0 - __funnelshift_r(q0, q1, psh);
     c1 = b1 - __funnelshift_r(q1, q2, psh);
@@ -140,8 +144,8 @@ __global__ void __launch_bounds__(256, 2) sweep_match_kernel(QuantParams q, Pixe
                                                              const uint32_t* __restrict__ Hb, FusedParams f) {
     extern __shared__ uint4 smem_raw[];
     uint32_t* vc = reinterpret_cast<uint32_t*>(smem_raw);                 // [128 bins][128 words]
-    uint32_t* gbuf = vc + kGroupBins * kVcWords;                            // [8 warps][2][128 words]
-    double* red = reinterpret_cast<double*>(gbuf + kWarps * 2 * kVcWords);  // [2 rows][8 warps][128]
+    uint32_t* gbuf = vc + kGroupBins * kVcWords;                            // [8 warps][4][128 words]
+    double* red = reinterpret_cast<double*>(gbuf + kWarps * 4 * kVcWords);  // [2 rows][8 warps][128]
     uint32_t* srep_s = reinterpret_cast<uint32_t*>(red + 2 * kWarps * kStrip);  // [128]
     uint32_t* lrow = srep_s + kGroupBins;                                   // [2 rows][128] row carries
     uint16_t* rowbins = reinterpret_cast<uint16_t*>(lrow + 2 * kGroupBins);  // [2 rows][128] strip bins
@@ -172,11 +176,12 @@ __global__ void __launch_bounds__(256, 2) sweep_match_kernel(QuantParams q, Pixe
     if (STORE && warp_live) vpart_init<kB>(V, Hb, band, Lb, kl0, Wp, xl);
     uint32_t* base_ptr = STORE ? out.data + static_cast<int64_t>(kl0) * out.plane_pitch + xl : nullptr;
     const bool lane_live = xl < out.row_pitch;
+    const uint32_t store_mask = lane_live ? (k_live >= 32 ? 0xFFFFFFFFu : (1u << max(k_live, 0)) - 1u) : 0u;
     const long long S = FAST ? f.S_group[g0 / kGroupBins] : 0;
     // G(e - kw): first extended cell of this lane's four windows, as a word and a bit shift
     const int idx = kStrip + 4 * lane - f.kw;
     const int pw = idx >> 1, psh = (idx & 1) * 16;
-    uint32_t* gb = gbuf + warp * 2 * kVcWords;
+    uint32_t* gb = gbuf + warp * 4 * kVcWords;
     const uint32_t* vbase = vc + warp * kB * kVcWords + 2 * lane;
 
     // staging thread: extended column tid; prefetch one row ahead
@@ -280,14 +285,19 @@ __global__ void __launch_bounds__(256, 2) sweep_match_kernel(QuantParams q, Pixe
 #pragma unroll
         for (int g = 0; g < kB / 4; ++g) {
             if (STORE)
-                vpart_group<kB, true>(V, g, bins4, kpat0, lr[g], prow + static_cast<int64_t>(4 * g) * out.plane_pitch,
-                                      out.plane_pitch, lane_live, k_live);
+                vpart_group<kB>(V, g, bins4 ^ kpat0, lr[g], prow + static_cast<int64_t>(4 * g) * out.plane_pitch,
+                                out.plane_pitch, store_mask);
             if (match_row) {
+                uint32_t bw[4][2];
+#pragma unroll
+                for (int i = 0; i < 4; ++i)
+                    window_prefix(vbase + (4 * g + i) * kVcWords, gb + i * kVcWords, lane, bw[i][0], bw[i][1]);
+                __syncwarp();
 #pragma unroll
                 for (int i = 0; i < 4; ++i) {
                     const int k = 4 * g + i;
                     uint32_t c0, c1;
-                    window_counts(vbase + k * kVcWords, gb + (k & 1) * kVcWords, lane, pw, psh, c0, c1);
+                    window_diff(gb + i * kVcWords, pw, psh, bw[i][0], bw[i][1], c0, c1);
                     if (FAST) {
                         const uint32_t sk = srep_s[warp * kB + k];
                         I0 += min_u16x2(c0, sk);
@@ -302,6 +312,7 @@ __global__ void __launch_bounds__(256, 2) sweep_match_kernel(QuantParams q, Pixe
                         acc[3] = __dadd_rn(acc[3], general_term(c1 >> 16, t, f));
                     }
                 }
+                __syncwarp();
             }
         }
         if (match_row) {
@@ -326,7 +337,7 @@ __global__ void __launch_bounds__(256, 2) sweep_match_kernel(QuantParams q, Pixe
     if (pend_y >= 0) combine(pend_y);
 }
 
-constexpr size_t kSmemBytes = (size_t(kGroupBins) * kVcWords + size_t(kWarps) * 2 * kVcWords) * 4 +
+constexpr size_t kSmemBytes = (size_t(kGroupBins) * kVcWords + size_t(kWarps) * 4 * kVcWords) * 4 +
                               size_t(2) * kWarps * kStrip * 8 + size_t(kGroupBins) * 4 * 3 + size_t(2) * kStrip * 2;
 
 }  // namespace spct_fused
@@ -392,7 +403,7 @@ extern "C" spct_status spct_cu_ih_build_match(const spct_source* src, const spct
     f.prep = prep;
     f.S_group = Sg;
     f.partial = partial;
-    const PixelMode pm = make_pixel_mode(q);
+    const PixelMode pm = make_pixel_mode(q, out->bin0);
     static bool attr_set = false;
     if (!attr_set) {
         cudaFuncSetAttribute(sweep_match_kernel<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBytes);

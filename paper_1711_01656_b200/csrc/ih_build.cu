@@ -402,7 +402,7 @@ extern "C" spct_status spct_cu_ih_build(const spct_source* src, const spct_ih* o
     dim3 grid(p.nstrips, p.nbands, p.slab_groups);
     const int threads = 32 * p.warps;
     const int prof = prof_begin("ih_sweep", s);
-    const PixelMode pm = make_pixel_mode(q);
+    const PixelMode pm = make_pixel_mode(q, out->bin0);
     switch (p.B) {
 #define SPCT_SWEEP(BB)                                                                                          \
     ih_sweep_kernel<BB, false><<<grid, threads, 0, s>>>(q, pm, *out, p.Lb, p.Wp, p.band_rows, p.warps, Lt, Hb); \

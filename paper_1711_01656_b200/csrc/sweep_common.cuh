@@ -17,7 +17,9 @@
 namespace spct_dev {
 
 // How the packed bins of a lane are formed (host-chosen, warp-uniform).
-//   byte_mode: nbins <= 256, bytes hold the absolute bin; bin k matches byte value k.
+//   byte_mode: nbins <= 256 and the slab start is a multiple of 16; bytes hold the
+//              absolute bin, and bin k0 + k (k0 % 16 == 0, k < 16) is matched as
+//              (byte ^ k0) == k.
 //              Columns past the image edge hold garbage: they only influence columns
 //              further right, which are never stored.
 //   otherwise: bytes hold bin - k0 for bins of the warp's slab and 0xFF elsewhere.
@@ -27,9 +29,9 @@ struct PixelMode {
     int shift;
 };
 
-__host__ inline PixelMode make_pixel_mode(const QuantParams& q) {
-    PixelMode m{q.nbins <= 256, -1};
-    if (q.kind == SPCT_SRC_GRAY_U8 && q.fast_u8 && q.nbins <= 256 && (q.nbins & (q.nbins - 1)) == 0) {
+__host__ inline PixelMode make_pixel_mode(const QuantParams& q, int bin0) {
+    PixelMode m{q.nbins <= 256 && bin0 % 16 == 0, -1};
+    if (m.byte_mode && q.kind == SPCT_SRC_GRAY_U8 && q.fast_u8 && (q.nbins & (q.nbins - 1)) == 0) {
         int s = 8;
         while ((1 << (8 - s)) != q.nbins) --s;
         m.shift = s;
@@ -75,8 +77,7 @@ __device__ __forceinline__ uint32_t load_bins4(const QuantParams& q, const Pixel
 // Inclusive warp scan step with the shuffle's in-range predicate (no select).
 __device__ __forceinline__ uint32_t scan_add(uint32_t v, int o) {
     uint32_t r;
-    asm volatile(
-        "{\n\t.reg .pred p;\n\t.reg .u32 t;\n\t"
+    asm("{\n\t.reg .pred p;\n\t.reg .u32 t;\n\t"
         "shfl.sync.up.b32 t|p, %1, %2, 0, 0xffffffff;\n\t"
         "@p add.u32 %1, %1, t;\n\t"
         "mov.u32 %0, %1;\n\t}"
@@ -125,7 +126,7 @@ __device__ __forceinline__ void vpart_row(uint32_t (&V)[4][B], uint32_t bins4, u
         uint32_t P[4];
 #pragma unroll
         for (int i = 0; i < 4; ++i)
-            P[i] = match_bytes(bins4, kpat0 + 0x01010101u * static_cast<uint32_t>(4 * g + i)) * 0x01010101u;
+            P[i] = match_bytes(bins4 ^ kpat0, 0x01010101u * static_cast<uint32_t>(4 * g + i)) * 0x01010101u;
         // lane totals (byte 3 of each prefix) -> one word, four bins
         const uint32_t packed = __byte_perm(__byte_perm(P[0], P[1], 0x0073), __byte_perm(P[2], P[3], 0x0073), 0x5410);
         const uint32_t excl = warp_incl_scan(packed) - packed;
@@ -151,13 +152,13 @@ namespace spct_dev {
 
 // One group of four planes (4g .. 4g+3) of vpart_row, for callers that interleave
 // the row update with other work.  `p` points at plane 4g of the row.
-template <int B, bool GUARD>
-__device__ __forceinline__ void vpart_group(uint32_t (&V)[4][B], int g, uint32_t bins4, uint32_t kpat0, uint4 L,
-                                            uint32_t* p, int64_t plane_pitch, bool store, int k_live) {
+template <int B>
+__device__ __forceinline__ void vpart_group(uint32_t (&V)[4][B], int g, uint32_t dbins, uint4 L, uint32_t* p,
+                                            int64_t plane_pitch, uint32_t store_mask) {
+    // dbins = bins4 ^ kpat0; store_mask bit k: plane k is live and the lane is inside the pitch
     uint32_t P[4];
 #pragma unroll
-    for (int i = 0; i < 4; ++i)
-        P[i] = match_bytes(bins4, kpat0 + 0x01010101u * static_cast<uint32_t>(4 * g + i)) * 0x01010101u;
+    for (int i = 0; i < 4; ++i) P[i] = match_bytes(dbins, 0x01010101u * static_cast<uint32_t>(4 * g + i)) * 0x01010101u;
     const uint32_t packed = __byte_perm(__byte_perm(P[0], P[1], 0x0073), __byte_perm(P[2], P[3], 0x0073), 0x5410);
     const uint32_t excl = warp_incl_scan(packed) - packed;
     const uint32_t Lk[4] = {L.x, L.y, L.z, L.w};
@@ -169,8 +170,7 @@ __device__ __forceinline__ void vpart_group(uint32_t (&V)[4][B], int g, uint32_t
         V[1][k] += base + __byte_perm(P[i], 0, 0x4441);
         V[2][k] += base + __byte_perm(P[i], 0, 0x4442);
         V[3][k] += base + (P[i] >> 24);
-        if (store && (!GUARD || k < k_live))
-            __stcs(reinterpret_cast<uint4*>(p), make_uint4(V[0][k], V[1][k], V[2][k], V[3][k]));
+        if (store_mask & (1u << k)) __stcs(reinterpret_cast<uint4*>(p), make_uint4(V[0][k], V[1][k], V[2][k], V[3][k]));
         p += plane_pitch;
     }
 }
