@@ -282,22 +282,61 @@ __global__ void __launch_bounds__(256, 2) sweep_match_kernel(QuantParams q, Pixe
 
         uint32_t I0 = 0, I1 = 0, C0 = 0, C1 = 0;
         double acc[4] = {0.0, 0.0, 0.0, 0.0};
+        const uint32_t dbins = bins4 ^ kpat0;
 #pragma unroll
         for (int g = 0; g < kB / 4; ++g) {
+            // (1) per-lane counts: one-hot prefixes of the sweep, in-lane vc prefixes of 4 bins
+            uint32_t P[4], sc[5], tot[4];
+            uint32_t a0[4], a1[4], b0[4], b1[4];
+            sc[4] = STORE ? vpart_counts(g, dbins, P) : 0u;
+            const uint32_t vpacked = sc[4];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                if (match_row) {
+                    const uint32_t* vw = vbase + (4 * g + i) * kVcWords;
+                    const uint2 wa = *reinterpret_cast<const uint2*>(vw);
+                    const uint2 wb = *reinterpret_cast<const uint2*>(vw + 64);
+                    a0[i] = wa.x * 0x10001u;
+                    a1[i] = wa.y * 0x10001u + __byte_perm(a0[i], 0, 0x3232);
+                    b0[i] = wb.x * 0x10001u;
+                    b1[i] = wb.y * 0x10001u + __byte_perm(b0[i], 0, 0x3232);
+                    tot[i] = __byte_perm(a1[i], b1[i], 0x7632);  // {sum a, sum b}
+                } else {
+                    a0[i] = a1[i] = b0[i] = b1[i] = tot[i] = 0u;
+                }
+                sc[i] = tot[i];
+            }
+            // (2) five independent warp scans, interleaved
+            if (STORE) warp_incl_scan_n<5>(sc);
+            else {
+                uint32_t (&s4)[4] = reinterpret_cast<uint32_t (&)[4]>(sc);
+                warp_incl_scan_n<4>(s4);
+            }
+            // (3) sweep: register update + stores
             if (STORE)
-                vpart_group<kB>(V, g, bins4 ^ kpat0, lr[g], prow + static_cast<int64_t>(4 * g) * out.plane_pitch,
+                vpart_apply<kB>(V, g, P, sc[4] - vpacked, lr[g], prow + static_cast<int64_t>(4 * g) * out.plane_pitch,
                                 out.plane_pitch, store_mask);
             if (match_row) {
-                uint32_t bw[4][2];
+                // (4) G of the 8 columns (halo half + strip half), staged for the partner reads
 #pragma unroll
-                for (int i = 0; i < 4; ++i)
-                    window_prefix(vbase + (4 * g + i) * kVcWords, gb + i * kVcWords, lane, bw[i][0], bw[i][1]);
+                for (int i = 0; i < 4; ++i) {
+                    const uint32_t ex = sc[i] - tot[i];
+                    const uint32_t T1 = __byte_perm(__shfl_sync(0xffffffffu, sc[i], 31), 0, 0x1010);
+                    const uint32_t ba = __byte_perm(ex, 0, 0x1010);
+                    const uint32_t bb = __byte_perm(ex, 0, 0x3232) + T1;
+                    uint32_t* gi = gb + i * kVcWords;
+                    *reinterpret_cast<uint2*>(gi + 2 * lane) = make_uint2(a0[i] + ba, a1[i] + ba);
+                    b0[i] += bb;
+                    b1[i] += bb;
+                    *reinterpret_cast<uint2*>(gi + 64 + 2 * lane) = make_uint2(b0[i], b1[i]);
+                }
                 __syncwarp();
+                // (5) window counts c = G(e) - G(e - kw) and the distance accumulation
 #pragma unroll
                 for (int i = 0; i < 4; ++i) {
                     const int k = 4 * g + i;
                     uint32_t c0, c1;
-                    window_diff(gb + i * kVcWords, pw, psh, bw[i][0], bw[i][1], c0, c1);
+                    window_diff(gb + i * kVcWords, pw, psh, b0[i], b1[i], c0, c1);
                     if (FAST) {
                         const uint32_t sk = srep_s[warp * kB + k];
                         I0 += min_u16x2(c0, sk);

@@ -176,3 +176,44 @@ __device__ __forceinline__ void vpart_group(uint32_t (&V)[4][B], int g, uint32_t
 }
 
 }  // namespace spct_dev
+
+namespace spct_dev {
+
+// N independent inclusive warp scans, interleaved step by step so the shuffle latencies
+// overlap (the compiler does not interleave separate scan chains on its own).
+template <int N>
+__device__ __forceinline__ void warp_incl_scan_n(uint32_t (&v)[N]) {
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+#pragma unroll
+        for (int i = 0; i < N; ++i) v[i] = scan_add(v[i], o);
+    }
+}
+
+// vpart_group split in two halves around a shared scan: the one-hot prefix words of
+// group g (returns the packed per-lane counts to scan) ...
+__device__ __forceinline__ uint32_t vpart_counts(int g, uint32_t dbins, uint32_t (&P)[4]) {
+#pragma unroll
+    for (int i = 0; i < 4; ++i) P[i] = match_bytes(dbins, 0x01010101u * static_cast<uint32_t>(4 * g + i)) * 0x01010101u;
+    return __byte_perm(__byte_perm(P[0], P[1], 0x0073), __byte_perm(P[2], P[3], 0x0073), 0x5410);
+}
+
+// ... and the register update + stores once the scan result (`excl`) is known.
+template <int B>
+__device__ __forceinline__ void vpart_apply(uint32_t (&V)[4][B], int g, const uint32_t (&P)[4], uint32_t excl, uint4 L,
+                                            uint32_t* p, int64_t plane_pitch, uint32_t store_mask) {
+    const uint32_t Lk[4] = {L.x, L.y, L.z, L.w};
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        const int k = 4 * g + i;
+        const uint32_t base = Lk[i] + __byte_perm(excl, 0, 0x4440 + i);
+        V[0][k] += base + __byte_perm(P[i], 0, 0x4440);
+        V[1][k] += base + __byte_perm(P[i], 0, 0x4441);
+        V[2][k] += base + __byte_perm(P[i], 0, 0x4442);
+        V[3][k] += base + (P[i] >> 24);
+        if (store_mask & (1u << k)) __stcs(reinterpret_cast<uint4*>(p), make_uint4(V[0][k], V[1][k], V[2][k], V[3][k]));
+        p += plane_pitch;
+    }
+}
+
+}  // namespace spct_dev
