@@ -233,10 +233,13 @@ def run_ours(args) -> None:
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
 
     def step(src):
-        P.build_and_match(src, nbins, None, KW, KH, P_ORDER, bin0=bin0, bins=BINS_PER_GPU, out=t, partial=part,
+        if world == 1:
+            # every bin on this GPU: the sweep writes the finished map itself
+            P.build_and_match_map(src, nbins, None, KW, KH, P_ORDER, out=t, lmap=lmap, tmpl_dev=tm)
+            return
+        P.build_and_match(src, nbins, None, KW, KH, P_ORDER, bin0=bin0, bins=bin1 - bin0, out=t, partial=part,
                           tmpl_dev=tm)
-        if world > 1:
-            reduce_partials(part, dst=0)
+        reduce_partials(part, dst=0)
         if rank == 0:
             P.hist_finalize(part, W_IMG, H_IMG, KW, KH, P_ORDER, out=lmap)
 
@@ -308,7 +311,8 @@ def run_ours(args) -> None:
         if name == "match_partial":
             alg = binpx * 4 + nu * nv * 8  # standalone matcher: IH read once + partial write
         elif name == "ih_sweep_match":
-            alg = binpx * 4 + W_IMG * H_IMG + nu * nv * 8  # IH write + frame read + partial write
+            # IH write + frame read + map write (N = 1: finished W x H map; N > 1: partial nu x nv)
+            alg = binpx * 4 + W_IMG * H_IMG + (W_IMG * H_IMG * 8 if world == 1 else nu * nv * 8)
         else:
             alg = binpx * 4 + W_IMG * H_IMG  # IH write + frame read
         achieved = alg / (kms * 1e-3) / 1e9

@@ -174,6 +174,14 @@ spct_status spct_cu_ih_build_match(const spct_source* src, const spct_ih* out, c
                                    int kw, int kh, double p, int metric, double* partial,
                                    void* workspace, size_t workspace_bytes, void* stream);
 
+/* Fused build + match producing the finished likelihood map (dev, height x width,
+ * spread_valid borders) in the same pass: build_integral_histogram followed by
+ * hist_distance_map (tools/spct_main.cpp:332-333) for a tensor that holds every bin
+ * (out->bin0 == 0, out->bins == out->nbins_total).  `out->data` may be NULL. */
+spct_status spct_cu_ih_build_match_map(const spct_source* src, const spct_ih* out, const double* tmpl,
+                                       int kw, int kh, double p, int metric, double* map,
+                                       void* workspace, size_t workspace_bytes, void* stream);
+
 /* ----------------------------------------------------------------- instrumentation */
 
 /* Every kernel launch of this library increments a process-wide counter.  With

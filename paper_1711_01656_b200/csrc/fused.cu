@@ -48,7 +48,24 @@ struct FusedParams {
     const uint32_t* prep;        // [0] fast flag, [1..] srep (slab-local), then S per group (int64)
     const long long* S_group;    // sum of integral s_k per 128-bin group
     double* partial;
+    double* map;                 // non-null: write the finished likelihood map (one group = every bin)
+    double inv_p, dmax;
+    int W, H;
 };
+
+// likelihood.cpp:220-221 (and the extension metrics), as in hist_match.cu finalize_kernel.
+__device__ __forceinline__ double finalize_L(double s, const FusedParams& f) {
+    double L;
+    if (f.metric == SPCT_METRIC_MINKOWSKI) {
+        const double d = f.p_kind == 1 ? s : pow(s, f.inv_p);
+        L = __dsub_rn(1.0, __ddiv_rn(d, f.dmax));
+    } else if (f.metric == SPCT_METRIC_CHISQ) {
+        L = __dsub_rn(1.0, __ddiv_rn(s, 2.0));
+    } else {
+        L = s;
+    }
+    return L < 0.0 ? 0.0 : (L > 1.0 ? 1.0 : L);
+}
 
 __device__ __forceinline__ uint32_t min_u16x2(uint32_t a, uint32_t b) {
     uint32_t r;
@@ -105,14 +122,16 @@ __global__ void prep_kernel(const double* __restrict__ tmpl, int bin0, int bins,
 }
 
 // Window counts, phase 1: for bin row `vw` (vc of the bin at word 2*lane), the inclusive
-// prefix G of the 256 extended columns for the lane's 8 columns (u16 pairs): stages the
-// pairs in `g` (the warp's staging row for this bin) and returns the strip half b0, b1.
-__device__ __forceinline__ void window_prefix(const uint32_t* vw, uint32_t* g, int lane, uint32_t& b0,
-                                              uint32_t& b1) {
+// prefix G of the 256 extended columns for the lane's 8 columns (u16 pairs): the halo
+// half (a0, a1) and the strip half (b0, b1); with STAGE they are also written to `g`
+// (the warp's staging row for this bin) for the general-kw partner reads.
+template <bool STAGE>
+__device__ __forceinline__ void window_prefix(const uint32_t* vw, uint32_t* g, int lane, uint32_t& a0, uint32_t& a1,
+                                              uint32_t& b0, uint32_t& b1) {
     const uint2 wa = *reinterpret_cast<const uint2*>(vw);
     const uint2 wb = *reinterpret_cast<const uint2*>(vw + 64);
-    uint32_t a0 = wa.x * 0x10001u;
-    uint32_t a1 = wa.y * 0x10001u + __byte_perm(a0, 0, 0x3232);
+    a0 = wa.x * 0x10001u;
+    a1 = wa.y * 0x10001u + __byte_perm(a0, 0, 0x3232);
     b0 = wb.x * 0x10001u;
     b1 = wb.y * 0x10001u + __byte_perm(b0, 0, 0x3232);
     const uint32_t tot = __byte_perm(a1, b1, 0x7632);  // {sum a, sum b}
@@ -125,8 +144,10 @@ __device__ __forceinline__ void window_prefix(const uint32_t* vw, uint32_t* g, i
     a1 += ba;
     b0 += bb;
     b1 += bb;
-    *reinterpret_cast<uint2*>(g + 2 * lane) = make_uint2(a0, a1);
-    *reinterpret_cast<uint2*>(g + 64 + 2 * lane) = make_uint2(b0, b1);
+    if (STAGE) {
+        *reinterpret_cast<uint2*>(g + 2 * lane) = make_uint2(a0, a1);
+        *reinterpret_cast<uint2*>(g + 64 + 2 * lane) = make_uint2(b0, b1);
+    }
 }
 
 // Window counts, phase 2 (after a __syncwarp): c = G(e) - G(e - kw) for the lane's four
@@ -138,7 +159,7 @@ __device__ __forceinline__ void window_diff(const uint32_t* g, int pw, int psh, 
     c1 = b1 - __funnelshift_r(q1, q2, psh);
 }
 
-template <bool STORE, bool FAST>
+template <bool STORE, bool FAST, int KWM>
 __global__ void __launch_bounds__(256, 2) sweep_match_kernel(QuantParams q, PixelMode pm, spct_ih out, int Lb, int Wp,
                                                              int band_rows, const uint32_t* __restrict__ Lt,
                                                              const uint32_t* __restrict__ Hb, FusedParams f) {
@@ -217,8 +238,18 @@ __global__ void __launch_bounds__(256, 2) sweep_match_kernel(QuantParams q, Pixe
                     term = 0.0;
                     for (int w = 0; w < nwarps_live; ++w) term = __dadd_rn(term, rb[w * kStrip + tid]);
                 }
-                double* dst = f.partial + static_cast<int64_t>(v) * f.nu + u;
-                *dst = f.accumulate ? __dadd_rn(*dst, term) : term;
+                if (f.map) {
+                    // finished map with spread_valid's border replication (likelihood.cpp:44-58)
+                    const double L = finalize_L(term, f);
+                    const int x = u + (f.kw - 1) / 2, yc = v + (f.kh - 1) / 2;
+                    const int xa = u == 0 ? 0 : x, xb = u == f.nu - 1 ? f.W - 1 : x;
+                    const int ya = v == 0 ? 0 : yc, yb = v == f.nv - 1 ? f.H - 1 : yc;
+                    for (int yy = ya; yy <= yb; ++yy)
+                        for (int xx = xa; xx <= xb; ++xx) f.map[static_cast<int64_t>(yy) * f.W + xx] = L;
+                } else {
+                    double* dst = f.partial + static_cast<int64_t>(v) * f.nu + u;
+                    *dst = f.accumulate ? __dadd_rn(*dst, term) : term;
+                }
             }
         }
     };
@@ -282,61 +313,34 @@ __global__ void __launch_bounds__(256, 2) sweep_match_kernel(QuantParams q, Pixe
 
         uint32_t I0 = 0, I1 = 0, C0 = 0, C1 = 0;
         double acc[4] = {0.0, 0.0, 0.0, 0.0};
-        const uint32_t dbins = bins4 ^ kpat0;
 #pragma unroll
         for (int g = 0; g < kB / 4; ++g) {
-            // (1) per-lane counts: one-hot prefixes of the sweep, in-lane vc prefixes of 4 bins
-            uint32_t P[4], sc[5], tot[4];
-            uint32_t a0[4], a1[4], b0[4], b1[4];
-            sc[4] = STORE ? vpart_counts(g, dbins, P) : 0u;
-            const uint32_t vpacked = sc[4];
-#pragma unroll
-            for (int i = 0; i < 4; ++i) {
-                if (match_row) {
-                    const uint32_t* vw = vbase + (4 * g + i) * kVcWords;
-                    const uint2 wa = *reinterpret_cast<const uint2*>(vw);
-                    const uint2 wb = *reinterpret_cast<const uint2*>(vw + 64);
-                    a0[i] = wa.x * 0x10001u;
-                    a1[i] = wa.y * 0x10001u + __byte_perm(a0[i], 0, 0x3232);
-                    b0[i] = wb.x * 0x10001u;
-                    b1[i] = wb.y * 0x10001u + __byte_perm(b0[i], 0, 0x3232);
-                    tot[i] = __byte_perm(a1[i], b1[i], 0x7632);  // {sum a, sum b}
-                } else {
-                    a0[i] = a1[i] = b0[i] = b1[i] = tot[i] = 0u;
-                }
-                sc[i] = tot[i];
-            }
-            // (2) five independent warp scans, interleaved
-            if (STORE) warp_incl_scan_n<5>(sc);
-            else {
-                uint32_t (&s4)[4] = reinterpret_cast<uint32_t (&)[4]>(sc);
-                warp_incl_scan_n<4>(s4);
-            }
-            // (3) sweep: register update + stores
             if (STORE)
-                vpart_apply<kB>(V, g, P, sc[4] - vpacked, lr[g], prow + static_cast<int64_t>(4 * g) * out.plane_pitch,
+                vpart_group<kB>(V, g, bins4 ^ kpat0, lr[g], prow + static_cast<int64_t>(4 * g) * out.plane_pitch,
                                 out.plane_pitch, store_mask);
             if (match_row) {
-                // (4) G of the 8 columns (halo half + strip half), staged for the partner reads
+                uint32_t aw[4][2], bw[4][2];
 #pragma unroll
-                for (int i = 0; i < 4; ++i) {
-                    const uint32_t ex = sc[i] - tot[i];
-                    const uint32_t T1 = __byte_perm(__shfl_sync(0xffffffffu, sc[i], 31), 0, 0x1010);
-                    const uint32_t ba = __byte_perm(ex, 0, 0x1010);
-                    const uint32_t bb = __byte_perm(ex, 0, 0x3232) + T1;
-                    uint32_t* gi = gb + i * kVcWords;
-                    *reinterpret_cast<uint2*>(gi + 2 * lane) = make_uint2(a0[i] + ba, a1[i] + ba);
-                    b0[i] += bb;
-                    b1[i] += bb;
-                    *reinterpret_cast<uint2*>(gi + 64 + 2 * lane) = make_uint2(b0[i], b1[i]);
-                }
-                __syncwarp();
-                // (5) window counts c = G(e) - G(e - kw) and the distance accumulation
+                for (int i = 0; i < 4; ++i)
+                    window_prefix<KWM == 0>(vbase + (4 * g + i) * kVcWords, gb + i * kVcWords, lane, aw[i][0], aw[i][1],
+                                            bw[i][0], bw[i][1]);
+                if (KWM == 0) __syncwarp();
 #pragma unroll
                 for (int i = 0; i < 4; ++i) {
                     const int k = 4 * g + i;
                     uint32_t c0, c1;
-                    window_diff(gb + i * kVcWords, pw, psh, b0[i], b1[i], c0, c1);
+                    if (KWM == 64) {
+                        // G(e - 64): the partner lane^16's halo half (lanes < 16) or strip half (>= 16)
+                        const uint32_t r0 = __shfl_xor_sync(0xffffffffu, lane >= 16 ? aw[i][0] : bw[i][0], 16);
+                        const uint32_t r1 = __shfl_xor_sync(0xffffffffu, lane >= 16 ? aw[i][1] : bw[i][1], 16);
+                        c0 = bw[i][0] - r0;
+                        c1 = bw[i][1] - r1;
+                    } else if (KWM == 128) {
+                        c0 = bw[i][0] - aw[i][0];  // G(e - 128) is the lane's own halo half
+                        c1 = bw[i][1] - aw[i][1];
+                    } else {
+                        window_diff(gb + i * kVcWords, pw, psh, bw[i][0], bw[i][1], c0, c1);
+                    }
                     if (FAST) {
                         const uint32_t sk = srep_s[warp * kB + k];
                         I0 += min_u16x2(c0, sk);
@@ -351,7 +355,7 @@ __global__ void __launch_bounds__(256, 2) sweep_match_kernel(QuantParams q, Pixe
                         acc[3] = __dadd_rn(acc[3], general_term(c1 >> 16, t, f));
                     }
                 }
-                __syncwarp();
+                if (KWM == 0) __syncwarp();
             }
         }
         if (match_row) {
@@ -387,9 +391,34 @@ namespace spct_impl {
 size_t fused_prep_bytes(int bins) { return (static_cast<size_t>(bins) + 1) * 4 + 256 + ((bins + 127) / 128 + 1) * 8; }
 }  // namespace spct_impl
 
-extern "C" spct_status spct_cu_ih_build_match(const spct_source* src, const spct_ih* out, const double* tmpl, int kw,
-                                              int kh, double p, int metric, double* partial, void* workspace,
-                                              size_t workspace_bytes, void* stream) {
+namespace spct_fused {
+
+template <int KWM>
+void launch_variants(dim3 grid, cudaStream_t s, const QuantParams& q, const PixelMode& pm, const spct_ih& out,
+                     const BuildPlan& bp, const uint32_t* Lt, const uint32_t* Hb, const FusedParams& f) {
+    static bool attr_set = false;
+    if (!attr_set) {
+        cudaFuncSetAttribute(sweep_match_kernel<true, true, KWM>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBytes);
+        cudaFuncSetAttribute(sweep_match_kernel<true, false, KWM>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBytes);
+        cudaFuncSetAttribute(sweep_match_kernel<false, true, KWM>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBytes);
+        cudaFuncSetAttribute(sweep_match_kernel<false, false, KWM>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBytes);
+        attr_set = true;
+    }
+    // integer (template-crop) variant and FP64 variant: the one not selected by the
+    // device-side template prep exits on entry
+    if (out.data) {
+        sweep_match_kernel<true, true, KWM><<<grid, 256, kSmemBytes, s>>>(q, pm, out, bp.Lb, bp.Wp, bp.band_rows, Lt, Hb, f);
+        sweep_match_kernel<true, false, KWM><<<grid, 256, kSmemBytes, s>>>(q, pm, out, bp.Lb, bp.Wp, bp.band_rows, Lt, Hb, f);
+    } else {
+        sweep_match_kernel<false, true, KWM><<<grid, 256, kSmemBytes, s>>>(q, pm, out, bp.Lb, bp.Wp, bp.band_rows, nullptr, nullptr, f);
+        sweep_match_kernel<false, false, KWM><<<grid, 256, kSmemBytes, s>>>(q, pm, out, bp.Lb, bp.Wp, bp.band_rows, nullptr, nullptr, f);
+    }
+}
+
+// Shared body of spct_cu_ih_build_match (partial != null) and spct_cu_ih_build_match_map (map != null).
+spct_status build_match(const spct_source* src, const spct_ih* out, const double* tmpl, int kw, int kh, double p,
+                        int metric, double* partial, double* map, void* workspace, size_t workspace_bytes,
+                        void* stream) {
     QuantParams q;
     if (auto st = make_quant(src, &q)) return st;
     if (auto st = check_ih(out)) return st;
@@ -401,14 +430,29 @@ extern "C" spct_status spct_cu_ih_build_match(const spct_source* src, const spct
     if (!(kw >= 1 && kh >= 1 && kw <= src->width && kh <= src->height))
         return contract("hist_distance_map: kernel exceeds image");
     if (metric < SPCT_METRIC_MINKOWSKI || metric > SPCT_METRIC_CHISQ) return contract("hist_match: unknown metric");
-    if (!tmpl || !partial) return contract("ih_build_match: null template or partial");
+    if (!tmpl || !(partial || map)) return contract("ih_build_match: null template or output");
+    if (map && (out->bin0 != 0 || out->bins != out->nbins_total))
+        return contract("ih_build_match_map: the slab must hold every bin (use the partial form for slabs)");
     cudaStream_t s = as_stream(stream);
     const int64_t T = static_cast<int64_t>(kw) * kh;
     const bool fusable = kw <= 128 && kh <= 255 && T <= 65535;
+    const int ngroups = static_cast<int>(ceil_div(out->bins, kGroupBins));
+    if (fusable && map && ngroups > 1) {
+        // more than one 128-bin group: accumulate the groups' partials, then finalise
+        double* part = nullptr;
+        const size_t n = static_cast<size_t>(out->width - kw + 1) * (out->height - kh + 1);
+        if (auto st = cuda_status(cudaMallocAsync(&part, n * sizeof(double), s), "ih_build_match_map alloc")) return st;
+        spct_status st = build_match(src, out, tmpl, kw, kh, p, metric, part, nullptr, workspace, workspace_bytes, stream);
+        if (st == SPCT_OK) st = spct_cu_hist_finalize(part, out->width, out->height, kw, kh, p, metric, map, stream);
+        cudaFreeAsync(part, s);
+        return st;
+    }
     if (!fusable) {
-        // window too large for the 16-bit running-histogram cells: two passes
-        if (!out->data) return contract("ih_build_match: window too large for the fused path; pass tensor storage");
+        // two passes: window too large for the 16-bit running-histogram cells, or a
+        // finished map over more than one 128-bin group
+        if (!out->data) return contract("ih_build_match: this shape needs tensor storage (two-pass schedule)");
         if (auto st = spct_cu_ih_build(src, out, workspace, workspace_bytes, stream)) return st;
+        if (map) return spct_cu_hist_match(out, tmpl, kw, kh, p, metric, map, stream);
         return spct_cu_hist_partial(out, tmpl, kw, kh, p, metric, partial, 0, stream);
     }
     const BuildPlan bp = plan_build(out->width, out->height, out->bins, kB);
@@ -420,7 +464,6 @@ extern "C" spct_status spct_cu_ih_build_match(const spct_source* src, const spct
         if (auto st = build_carries(q, *out, bp, workspace, workspace_bytes, s, &Lt, &Hb)) return st;
         ws += bp.lt_bytes + bp.hb_bytes;
     }
-    const int ngroups = static_cast<int>(ceil_div(out->bins, kGroupBins));
     uint32_t* prep = reinterpret_cast<uint32_t*>(ws);
     long long* Sg = reinterpret_cast<long long*>(ws + round_up((static_cast<int64_t>(out->bins) + 1) * 4, 256));
     const int fast_metric = (metric == SPCT_METRIC_MINKOWSKI && p == 1.0) || metric == SPCT_METRIC_INTERSECTION;
@@ -434,6 +477,8 @@ extern "C" spct_status spct_cu_ih_build_match(const spct_source* src, const spct
     f.nv = out->height - kh + 1;
     f.metric = metric;
     f.p = p;
+    f.inv_p = 1.0 / p;
+    f.dmax = std::pow(2.0, 1.0 / p);  // likelihood.cpp:208
     f.p_kind = p == 1.0 ? 1 : (p == 2.0 ? 2 : 0);
     f.T = static_cast<double>(T);
     f.invT = 1.0 / f.T;
@@ -442,34 +487,38 @@ extern "C" spct_status spct_cu_ih_build_match(const spct_source* src, const spct
     f.prep = prep;
     f.S_group = Sg;
     f.partial = partial;
+    f.map = map;
+    f.W = out->width;
+    f.H = out->height;
     const PixelMode pm = make_pixel_mode(q, out->bin0);
-    static bool attr_set = false;
-    if (!attr_set) {
-        cudaFuncSetAttribute(sweep_match_kernel<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBytes);
-        cudaFuncSetAttribute(sweep_match_kernel<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBytes);
-        cudaFuncSetAttribute(sweep_match_kernel<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBytes);
-        cudaFuncSetAttribute(sweep_match_kernel<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBytes);
-        attr_set = true;
-    }
     for (int g = 0; g < ngroups; ++g) {
         f.group0 = g * kGroupBins;
         f.accumulate = g > 0;
         dim3 grid(bp.nstrips, bp.nbands, 1);
-        // integer (template-crop) variant and FP64 variant: the one not selected by the
-        // device-side template prep exits on entry
         const int prof = prof_begin(out->data ? "ih_sweep_match" : "sweep_match_nostore", s);
-        if (out->data) {
-            sweep_match_kernel<true, true><<<grid, 256, kSmemBytes, s>>>(q, pm, *out, bp.Lb, bp.Wp, bp.band_rows, Lt, Hb, f);
-            sweep_match_kernel<true, false><<<grid, 256, kSmemBytes, s>>>(q, pm, *out, bp.Lb, bp.Wp, bp.band_rows, Lt, Hb, f);
-        } else {
-            sweep_match_kernel<false, true><<<grid, 256, kSmemBytes, s>>>(q, pm, *out, bp.Lb, bp.Wp, bp.band_rows, nullptr,
-                                                                          nullptr, f);
-            sweep_match_kernel<false, false><<<grid, 256, kSmemBytes, s>>>(q, pm, *out, bp.Lb, bp.Wp, bp.band_rows, nullptr,
-                                                                           nullptr, f);
-        }
+        if (kw == 64) launch_variants<64>(grid, s, q, pm, *out, bp, Lt, Hb, f);
+        else if (kw == 128) launch_variants<128>(grid, s, q, pm, *out, bp, Lt, Hb, f);
+        else launch_variants<0>(grid, s, q, pm, *out, bp, Lt, Hb, f);
         prof_end(prof, s);
         note_launch();
         if (auto st = launch_status("sweep_match_kernel")) return st;
     }
     return SPCT_OK;
+}
+
+}  // namespace spct_fused
+
+extern "C" spct_status spct_cu_ih_build_match(const spct_source* src, const spct_ih* out, const double* tmpl, int kw,
+                                              int kh, double p, int metric, double* partial, void* workspace,
+                                              size_t workspace_bytes, void* stream) {
+    if (!partial) return contract("ih_build_match: null partial");
+    return spct_fused::build_match(src, out, tmpl, kw, kh, p, metric, partial, nullptr, workspace, workspace_bytes,
+                                   stream);
+}
+
+extern "C" spct_status spct_cu_ih_build_match_map(const spct_source* src, const spct_ih* out, const double* tmpl, int kw,
+                                                  int kh, double p, int metric, double* map, void* workspace,
+                                                  size_t workspace_bytes, void* stream) {
+    if (!map) return contract("ih_build_match_map: null map");
+    return spct_fused::build_match(src, out, tmpl, kw, kh, p, metric, nullptr, map, workspace, workspace_bytes, stream);
 }

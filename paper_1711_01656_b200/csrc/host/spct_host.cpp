@@ -336,12 +336,9 @@ LikelihoodMap likelihood_from_frame(const GrayImage& img, int bins, const std::v
     std::size_t ws = 0;
     check(spct_cu_ih_build_workspace(&s, 0, bins, &ws));
     DevBuf work(ws);
-    const std::size_t nvalid = std::size_t(img.width - kw + 1) * (img.height - kh + 1);
-    DevBuf part(nvalid * 8), map(std::size_t(img.width) * img.height * 8);
-    check(spct_cu_ih_build_match(&s, &d, tm.as<double>(), kw, kh, p, SPCT_METRIC_MINKOWSKI, part.as<double>(), work.p,
-                                 ws, nullptr));
-    check(spct_cu_hist_finalize(part.as<double>(), img.width, img.height, kw, kh, p, SPCT_METRIC_MINKOWSKI,
-                                map.as<double>(), nullptr));
+    DevBuf map(std::size_t(img.width) * img.height * 8);
+    check(spct_cu_ih_build_match_map(&s, &d, tm.as<double>(), kw, kh, p, SPCT_METRIC_MINKOWSKI, map.as<double>(),
+                                     work.p, ws, nullptr));
     LikelihoodMap out;
     out.width = img.width;
     out.height = img.height;

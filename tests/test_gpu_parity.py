@@ -295,6 +295,35 @@ def test_fused_integral_template(P, w, h, bins, kw, kh, store):
     assert close(P.hist_finalize(part, w, h, kw, kh, 1.0, 1).cpu().numpy(), inter)
 
 
+@pytest.mark.parametrize("w,h,bins,kw,kh", FUSED_CASES + [(300, 290, 100, 64, 50), (260, 140, 64, 128, 128)])
+@pytest.mark.parametrize("store", [True, False])
+def test_fused_map_direct(P, w, h, bins, kw, kh, store):
+    """spct_cu_ih_build_match_map: finished map (incl. spread_valid borders) in the sweep."""
+    img = oracle.smooth_image(w, h, w + 5 * h)
+    qb = oracle.quantize(img, bins)
+    th = _crop_template(qb, bins, (w - kw) // 2, (h - kh) // 3, kw, kh)
+    t = P.IntegralHistogramTensor(w, h, bins)
+    if not store:
+        t.desc.data = None
+    _, lmap = P.build_and_match_map(img, bins, th, kw, kh, 1.0, out=t)
+    assert close(lmap.cpu().numpy(), oracle.hist_match_map_direct(qb, bins, th, kw, kh, 1.0))
+    if store:
+        assert np.array_equal(t.padded_u64(), oracle.build_ih(qb, bins))
+    rng = np.random.default_rng(w)
+    tg = rng.random(bins)
+    tg /= tg.sum()
+    for p, metric in [(1.0, 0), (2.0, 0), (1.0, 1), (1.0, 3)]:
+        _, lmap = P.build_and_match_map(img, bins, tg, kw, kh, p, metric, out=t)
+        assert close(lmap.cpu().numpy(), oracle.hist_match_map_direct(qb, bins, tg, kw, kh, p, metric)), (p, metric)
+
+
+def test_fused_map_rejects_slabs(P):
+    img = oracle.smooth_image(100, 80, 1)
+    t = P.IntegralHistogramTensor(100, 80, 32, bin0=16, bins=16)
+    with pytest.raises(P.ContractError):
+        P.build_and_match_map(img, 32, np.full(32, 1 / 32), 16, 16, 1.0, out=t)
+
+
 @pytest.mark.parametrize("w,h,bins,kw,kh", FUSED_CASES[:6])
 @pytest.mark.parametrize("p,metric", [(1.0, 0), (2.0, 0), (1.7, 0), (1.0, 1), (1.0, 2), (1.0, 3)])
 def test_fused_general_template(P, w, h, bins, kw, kh, p, metric):
