@@ -3,11 +3,8 @@
 // Replaces build_integral_histogram / build_tensor and its four CPU schedules
 // (reference proj/src/integral.cpp:348-551).  Data flow:
 //
-//   rowcarry_kernel   per (row, 128-column strip): exclusive count of every slab bin
-//                     in the row left of the strip          -> Lt[s][y][kl]
-//   bandcount_kernel  per (band, strip): column counts of every slab bin over the
-//                     band's rows                            -> CC[j][kl][x]
-//   bandscan_kernel   prefix over bands and columns          -> Hb[j][kl][x] (in place)
+//   carries.cu        row carries Lt[s][y][kl] (count of each slab bin left of strip s)
+//                     and band carries Hb[j][kl][x] (IH row at the top of band j)
 //   ih_sweep_kernel   per (band, strip, bin slab): one warp per B-bin slab sweeps the
 //                     band top to bottom; lane l owns columns 4l..4l+3 of the strip and
 //                     keeps H(y, x, k) for those 4 columns x B bins in registers.  A row
@@ -100,109 +97,6 @@ spct_status check_ih(const spct_ih* t) {
 using namespace spct_impl;
 
 namespace spct_build {
-
-// ------------------------------------------------------------------ pre-passes
-
-// Lt[(s*H + y)*Lb + kl] = count of slab bin kl in row y, columns [0, 128*s).
-// One CTA (128 threads = one strip width) per row; bins handled in chunks.
-constexpr int kCarryChunk = 4096;
-
-__global__ void __launch_bounds__(128) rowcarry_kernel(QuantParams q, int bin0, int bins, int Lb, int nstrips,
-                                                       uint32_t* __restrict__ Lt) {
-    __shared__ uint32_t hist[kCarryChunk];
-    const int y = blockIdx.x;
-    const int kc0 = blockIdx.y * kCarryChunk;
-    const int kcn = min(kCarryChunk, Lb - kc0);
-    for (int i = threadIdx.x; i < kcn; i += blockDim.x) hist[i] = 0;
-    __syncthreads();
-    for (int s = 0; s < nstrips; ++s) {
-        uint32_t* dst = Lt + (static_cast<int64_t>(s) * q.height + y) * Lb + kc0;
-        for (int i = threadIdx.x; i < kcn; i += blockDim.x) dst[i] = hist[i];
-        __syncthreads();
-        const int x = s * kStrip + threadIdx.x;
-        if (s + 1 < nstrips && x < q.width) {
-            const int kl = pixel_bin(q, x, y) - bin0 - kc0;
-            if (kl >= 0 && kl < kcn && kl + kc0 < bins) atomicAdd(&hist[kl], 1u);
-        }
-        __syncthreads();
-    }
-}
-
-// CC[(j*Lb + kl)*Wp + x] = count of slab bin kl in column x over band j's rows,
-// for bands j = 0 .. nbands-2 (the last band feeds nothing).
-constexpr int kBandChunk = 64;
-
-__global__ void __launch_bounds__(128) bandcount_kernel(QuantParams q, int bin0, int bins, int Lb, int Wp,
-                                                        int band_rows, uint32_t* __restrict__ CC) {
-    __shared__ uint32_t cnt[kBandChunk][kStrip];
-    const int x = blockIdx.x * kStrip + threadIdx.x;
-    const int j = blockIdx.y;
-    const int kc0 = blockIdx.z * kBandChunk;
-    const int kcn = min(kBandChunk, Lb - kc0);
-    for (int i = 0; i < kcn; ++i) cnt[i][threadIdx.x] = 0;
-    const int y0 = j * band_rows, y1 = min(q.height, y0 + band_rows);
-    if (x < q.width) {
-        for (int y = y0; y < y1; ++y) {
-            const int kl = pixel_bin(q, x, y) - bin0 - kc0;
-            if (kl >= 0 && kl < kcn && kl + kc0 < bins) cnt[kl][threadIdx.x] += 1;
-        }
-    }
-    for (int i = 0; i < kcn; ++i) CC[(static_cast<int64_t>(j) * Lb + kc0 + i) * Wp + x] = cnt[i][threadIdx.x];
-}
-
-// In place: Hb[j-1][kl][x] = sum_{j' < j} sum_{c <= x} CC[j'][kl][c]  (j = 1..nbands-1),
-// i.e. the unpadded IH value at row y0_j - 1.  One CTA per slab bin; each thread owns
-// a contiguous run of columns; a block scan per band.
-__global__ void __launch_bounds__(1024) bandscan_kernel(int Lb, int Wp, int nbands, uint32_t* __restrict__ CCHb) {
-    __shared__ uint32_t warp_tot[32];
-    const int kl = blockIdx.x;
-    const int per = (Wp + blockDim.x - 1) / blockDim.x;  // <= 64 handled by the loop below
-    const int xs = threadIdx.x * per;
-    constexpr int kMaxPer = 16;
-    uint32_t run[kMaxPer];
-#pragma unroll
-    for (int i = 0; i < kMaxPer; ++i) run[i] = 0;
-    for (int j = 1; j < nbands; ++j) {
-        uint32_t* row = CCHb + (static_cast<int64_t>(j - 1) * Lb + kl) * Wp;
-        uint32_t tot = 0;
-#pragma unroll
-        for (int i = 0; i < kMaxPer; ++i) {
-            if (i < per && xs + i < Wp) {
-                run[i] += row[xs + i];  // vertical: bands < j
-                tot += run[i];
-            }
-        }
-        // exclusive scan of per-thread totals across the block
-        const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-        uint32_t v = tot;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            uint32_t t = __shfl_up_sync(0xffffffffu, v, o);
-            if (lane >= o) v += t;
-        }
-        __syncthreads();
-        if (lane == 31) warp_tot[wid] = v;
-        __syncthreads();
-        if (wid == 0) {
-            uint32_t w = lane < static_cast<int>(blockDim.x >> 5) ? warp_tot[lane] : 0;
-#pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                uint32_t t = __shfl_up_sync(0xffffffffu, w, o);
-                if (lane >= o) w += t;
-            }
-            warp_tot[lane] = w;  // inclusive
-        }
-        __syncthreads();
-        uint32_t acc = v - tot + (wid > 0 ? warp_tot[wid - 1] : 0);
-#pragma unroll
-        for (int i = 0; i < kMaxPer; ++i) {
-            if (i < per && xs + i < Wp) {
-                acc += run[i];
-                row[xs + i] = acc;  // in place: this band's CC slot now holds Hb[j]
-            }
-        }
-    }
-}
 
 // ------------------------------------------------------------------ main sweep
 
@@ -355,36 +249,6 @@ extern "C" spct_status spct_cu_ih_build_workspace(const spct_source* src, int bi
     return SPCT_OK;
 }
 
-namespace spct_impl {
-
-// Shared by spct_cu_ih_build and the fused build+match path: launch the three
-// carry pre-passes into the workspace.  Returns table pointers.
-spct_status build_carries(const QuantParams& q, const spct_ih& out, const BuildPlan& p, void* workspace,
-                          size_t ws_bytes, cudaStream_t s, uint32_t** Lt, uint32_t** Hb) {
-    *Lt = nullptr;
-    *Hb = nullptr;
-    if (p.lt_bytes + p.hb_bytes > 0 && (!workspace || ws_bytes < p.lt_bytes + p.hb_bytes))
-        return contract("ih_build: workspace too small (query spct_cu_ih_build_workspace)");
-    char* ws = static_cast<char*>(workspace);
-    if (p.lt_bytes) {
-        *Lt = reinterpret_cast<uint32_t*>(ws);
-        dim3 g(q.height, static_cast<unsigned>(ceil_div(p.Lb, kCarryChunk)));
-        rowcarry_kernel<<<g, 128, 0, s>>>(q, out.bin0, out.bins, p.Lb, p.nstrips, *Lt);
-        if (auto st = launch_status("rowcarry_kernel")) return st;
-    }
-    if (p.hb_bytes) {
-        *Hb = reinterpret_cast<uint32_t*>(ws + p.lt_bytes);
-        dim3 g(p.nstrips, p.nbands - 1, static_cast<unsigned>(ceil_div(p.Lb, kBandChunk)));
-        bandcount_kernel<<<g, 128, 0, s>>>(q, out.bin0, out.bins, p.Lb, p.Wp, p.band_rows, *Hb);
-        if (auto st = launch_status("bandcount_kernel")) return st;
-        if (ceil_div(p.Wp, 1024) > 16) return contract("ih_build: width too large for bandscan (max 16384)");
-        bandscan_kernel<<<p.Lb, 1024, 0, s>>>(p.Lb, p.Wp, p.nbands, *Hb);
-        if (auto st = launch_status("bandscan_kernel")) return st;
-    }
-    return SPCT_OK;
-}
-
-}  // namespace spct_impl
 
 extern "C" spct_status spct_cu_ih_build(const spct_source* src, const spct_ih* out, void* workspace,
                                         size_t workspace_bytes, void* stream) {
