@@ -144,6 +144,23 @@ __device__ __forceinline__ uint32_t match_bytes(uint32_t packed, uint32_t kpat) 
     return (~t & 0x80808080u) >> 7;
 }
 
+// In-lane inclusive prefix of the one-hot matches in bytes: byte j = #{i <= j : byte_i == k}.
+// Uses (j+1) - #non-matches: one IMAD folds the complement and the prefix multiply.
+__device__ __forceinline__ uint32_t match_prefix(uint32_t packed, uint32_t kpat) {
+    const uint32_t x = packed ^ kpat;
+    const uint32_t nz = (((x & 0x7F7F7F7Fu) + 0x7F7F7F7Fu) | x) & 0x80808080u;  // 0x80 where byte != k
+    return 0x04030201u - (nz >> 7) * 0x01010101u;
+}
+
+// 16-byte streaming store under a predicate, without a branch.
+__device__ __forceinline__ void st_cs_v4_if(bool pred, uint32_t* p, uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
+    asm volatile(
+        "{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %5, 0;\n\t"
+        "@q st.global.cs.v4.u32 [%0], {%1, %2, %3, %4};\n\t}"
+        :
+        : "l"(p), "r"(a), "r"(b), "r"(c), "r"(d), "r"(static_cast<uint32_t>(pred)));
+}
+
 __device__ __forceinline__ int lane_id() { return threadIdx.x & 31; }
 
 }  // namespace spct_dev

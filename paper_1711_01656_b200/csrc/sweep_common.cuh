@@ -126,7 +126,7 @@ __device__ __forceinline__ void vpart_row(uint32_t (&V)[4][B], uint32_t bins4, u
         uint32_t P[4];
 #pragma unroll
         for (int i = 0; i < 4; ++i)
-            P[i] = match_bytes(bins4 ^ kpat0, 0x01010101u * static_cast<uint32_t>(4 * g + i)) * 0x01010101u;
+            P[i] = match_prefix(bins4 ^ kpat0, 0x01010101u * static_cast<uint32_t>(4 * g + i));
         // lane totals (byte 3 of each prefix) -> one word, four bins
         const uint32_t packed = __byte_perm(__byte_perm(P[0], P[1], 0x0073), __byte_perm(P[2], P[3], 0x0073), 0x5410);
         const uint32_t excl = warp_incl_scan(packed) - packed;
@@ -139,8 +139,7 @@ __device__ __forceinline__ void vpart_row(uint32_t (&V)[4][B], uint32_t bins4, u
             V[1][k] += base + __byte_perm(P[i], 0, 0x4441);
             V[2][k] += base + __byte_perm(P[i], 0, 0x4442);
             V[3][k] += base + (P[i] >> 24);
-            if (store && (!GUARD || k < k_live))
-                __stcs(reinterpret_cast<uint4*>(p), make_uint4(V[0][k], V[1][k], V[2][k], V[3][k]));
+            st_cs_v4_if(store && (!GUARD || k < k_live), p, V[0][k], V[1][k], V[2][k], V[3][k]);
             p += plane_pitch;
         }
     }
@@ -158,7 +157,7 @@ __device__ __forceinline__ void vpart_group(uint32_t (&V)[4][B], int g, uint32_t
     // dbins = bins4 ^ kpat0; store_mask bit k: plane k is live and the lane is inside the pitch
     uint32_t P[4];
 #pragma unroll
-    for (int i = 0; i < 4; ++i) P[i] = match_bytes(dbins, 0x01010101u * static_cast<uint32_t>(4 * g + i)) * 0x01010101u;
+    for (int i = 0; i < 4; ++i) P[i] = match_prefix(dbins, 0x01010101u * static_cast<uint32_t>(4 * g + i));
     const uint32_t packed = __byte_perm(__byte_perm(P[0], P[1], 0x0073), __byte_perm(P[2], P[3], 0x0073), 0x5410);
     const uint32_t excl = warp_incl_scan(packed) - packed;
     const uint32_t Lk[4] = {L.x, L.y, L.z, L.w};
@@ -170,7 +169,7 @@ __device__ __forceinline__ void vpart_group(uint32_t (&V)[4][B], int g, uint32_t
         V[1][k] += base + __byte_perm(P[i], 0, 0x4441);
         V[2][k] += base + __byte_perm(P[i], 0, 0x4442);
         V[3][k] += base + (P[i] >> 24);
-        if (store_mask & (1u << k)) __stcs(reinterpret_cast<uint4*>(p), make_uint4(V[0][k], V[1][k], V[2][k], V[3][k]));
+        st_cs_v4_if((store_mask >> k) & 1u, p, V[0][k], V[1][k], V[2][k], V[3][k]);
         p += plane_pitch;
     }
 }
@@ -194,7 +193,7 @@ __device__ __forceinline__ void warp_incl_scan_n(uint32_t (&v)[N]) {
 // group g (returns the packed per-lane counts to scan) ...
 __device__ __forceinline__ uint32_t vpart_counts(int g, uint32_t dbins, uint32_t (&P)[4]) {
 #pragma unroll
-    for (int i = 0; i < 4; ++i) P[i] = match_bytes(dbins, 0x01010101u * static_cast<uint32_t>(4 * g + i)) * 0x01010101u;
+    for (int i = 0; i < 4; ++i) P[i] = match_prefix(dbins, 0x01010101u * static_cast<uint32_t>(4 * g + i));
     return __byte_perm(__byte_perm(P[0], P[1], 0x0073), __byte_perm(P[2], P[3], 0x0073), 0x5410);
 }
 
@@ -211,7 +210,7 @@ __device__ __forceinline__ void vpart_apply(uint32_t (&V)[4][B], int g, const ui
         V[1][k] += base + __byte_perm(P[i], 0, 0x4441);
         V[2][k] += base + __byte_perm(P[i], 0, 0x4442);
         V[3][k] += base + (P[i] >> 24);
-        if (store_mask & (1u << k)) __stcs(reinterpret_cast<uint4*>(p), make_uint4(V[0][k], V[1][k], V[2][k], V[3][k]));
+        st_cs_v4_if((store_mask >> k) & 1u, p, V[0][k], V[1][k], V[2][k], V[3][k]);
         p += plane_pitch;
     }
 }
