@@ -152,13 +152,10 @@ __device__ __forceinline__ uint32_t match_prefix(uint32_t packed, uint32_t kpat)
     return 0x04030201u - (nz >> 7) * 0x01010101u;
 }
 
-// 16-byte streaming store under a predicate, without a branch.
+// 16-byte streaming store under a predicate (the address is computed unconditionally by
+// the caller so the compiler emits a predicated STG rather than a branch).
 __device__ __forceinline__ void st_cs_v4_if(bool pred, uint32_t* p, uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
-    asm volatile(
-        "{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %5, 0;\n\t"
-        "@q st.global.cs.v4.u32 [%0], {%1, %2, %3, %4};\n\t}"
-        :
-        : "l"(p), "r"(a), "r"(b), "r"(c), "r"(d), "r"(static_cast<uint32_t>(pred)));
+    if (pred) __stcs(reinterpret_cast<uint4*>(p), make_uint4(a, b, c, d));
 }
 
 __device__ __forceinline__ int lane_id() { return threadIdx.x & 31; }
