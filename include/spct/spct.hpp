@@ -187,6 +187,13 @@ LikelihoodMap hist_distance_map(const IntegralHistogramTensor& t, const std::vec
 // ---------------------------------------------------------------- extensions (not in the reference)
 enum class HistMetric { Minkowski = 0, Intersection = 1, Bhattacharyya = 2, ChiSquare = 3 };
 
+// hist_distance_map over a tensor built by this library recomputes the window counts
+// from the tensor's source frame in the fused sweep (within the 1e-5 map tolerance).
+// With exact maps on (set_exact_maps(true) or SPCT_EXACT_MAPS=1) it reads the tensor
+// with the reference's operation order instead: bit-identical for p = 1.
+void set_exact_maps(bool on);
+bool exact_maps();
+
 // hist_distance_map with a selectable bin-to-bin statistic (thesis PAPER.md:703).
 LikelihoodMap hist_match_map(const IntegralHistogramTensor& t, const std::vector<double>& template_hist, int kw,
                              int kh, HistMetric metric, double p = 1.0);

@@ -132,6 +132,9 @@ class IntegralHistogramTensor:
         self.row_pitch, self.plane_pitch = rp.value, pp.value
         self.storage = torch.empty(nbytes.value // 4, dtype=torch.int32, device=device or "cuda")
         self.desc = A.spct_ih(self.storage.data_ptr(), bins, bin0, nbins_total, height, width, rp.value, pp.value)
+        # (spct_source, keep-alive device tensors) of the frame the tensor was built from, if any:
+        # window statistics can then be recomputed from 1 B/px instead of re-reading the tensor
+        self.source = None
 
     def planes(self) -> torch.Tensor:
         """(bins, height, row_pitch) int32 view of the unpadded device cells."""
@@ -249,6 +252,11 @@ def build_integral_histogram(bm, nbins: int | None = None, schedule: ScanSchedul
     check(A.lib().spct_cu_ih_build_workspace(C.byref(src), t.bin0, t.bins, C.byref(ws)))
     wbuf = _WS.get(ws.value, keep[0].device)
     check(A.lib().spct_cu_ih_build(C.byref(src), C.byref(t.desc), _ptr(wbuf), wbuf.numel(), _stream(stream)))
+    if isinstance(bm, torch.Tensor) and bm.is_cuda:  # caller-owned device memory: keep a private copy
+        keep = [k.clone() for k in keep]
+        for i, k in enumerate(keep):
+            src.plane[i] = _ptr(k)
+    t.source = (src, keep)
     return t
 
 
@@ -291,16 +299,31 @@ def _tmpl(tmpl, nbins: int, width: int, height: int, kw: int, kh: int, p: float)
 
 
 def hist_match_map(t: IntegralHistogramTensor, tmpl, kw: int, kh: int, p: float = 1.0,
-                   metric: int = A.METRIC_MINKOWSKI, stream=None) -> torch.Tensor:
-    """likelihood.cpp:193-225 (metric MINKOWSKI) -> (height, width) float64 device map."""
+                   metric: int = A.METRIC_MINKOWSKI, stream=None, exact: bool = False) -> torch.Tensor:
+    """likelihood.cpp:193-225 (metric MINKOWSKI) -> (height, width) float64 device map.
+
+    A tensor built by this library remembers its source frame, and the map is then
+    recomputed by the fused sweep from 1 B/px (no tensor re-read; within the 1e-5 map
+    tolerance).  ``exact=True`` (or a tensor without a source) reads the tensor with
+    the reference's operation order instead: bit-identical to the reference for p = 1."""
     dt = _tmpl(tmpl, t.bins, t.width, t.height, kw, kh, p)
     out = torch.empty((t.height, t.width), dtype=torch.float64, device=dt.device)
+    if not exact and t.source is not None and t.bin0 == 0 and t.bins == t.nbins_total:
+        src, _keep = t.source
+        nodata = A.spct_ih(None, t.bins, t.bin0, t.nbins_total, t.height, t.width, t.row_pitch, t.plane_pitch)
+        ws = C.c_size_t()
+        check(A.lib().spct_cu_ih_build_workspace(C.byref(src), 0, t.bins, C.byref(ws)))
+        wbuf = _WS.get(ws.value, dt.device)
+        check(A.lib().spct_cu_ih_build_match_map(C.byref(src), C.byref(nodata), _ptr(dt), kw, kh, p, metric,
+                                                 _ptr(out), _ptr(wbuf), wbuf.numel(), _stream(stream)))
+        return out
     check(A.lib().spct_cu_hist_match(C.byref(t.desc), _ptr(dt), kw, kh, p, metric, _ptr(out), _stream(stream)))
     return out
 
 
-def hist_distance_map(t: IntegralHistogramTensor, tmpl, kw: int, kh: int, p: float = 1.0, stream=None):
-    return hist_match_map(t, tmpl, kw, kh, p, A.METRIC_MINKOWSKI, stream)
+def hist_distance_map(t: IntegralHistogramTensor, tmpl, kw: int, kh: int, p: float = 1.0, stream=None,
+                      exact: bool = False):
+    return hist_match_map(t, tmpl, kw, kh, p, A.METRIC_MINKOWSKI, stream, exact)
 
 
 def hist_partial(t: IntegralHistogramTensor, tmpl_dev: torch.Tensor, kw: int, kh: int, p: float = 1.0,

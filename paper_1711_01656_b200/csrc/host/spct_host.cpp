@@ -6,6 +6,7 @@
 // Device failures throw spct::device_error.
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 
@@ -15,6 +16,16 @@
 #include "spct_cuda.h"
 
 namespace spct {
+
+namespace {
+bool g_exact_maps = [] {
+    const char* e = std::getenv("SPCT_EXACT_MAPS");
+    return e && *e && *e != '0';
+}();
+}  // namespace
+
+void set_exact_maps(bool on) { g_exact_maps = on; }
+bool exact_maps() { return g_exact_maps; }
 
 namespace {
 
@@ -59,6 +70,10 @@ namespace detail {
 struct DeviceTensor {
     spct_ih desc{};
     std::unique_ptr<DevBuf> mem;
+    // The frame the tensor was built from (device copy): hist_distance_map recomputes
+    // window counts from it (1 B/px) instead of re-reading b*H*W*4 tensor bytes.
+    spct_source src{};
+    std::unique_ptr<DevBuf> src_mem;
 };
 
 std::size_t HostMirror::size() const {
@@ -199,8 +214,10 @@ void validate_build(const BinMap& bm, const ScanSchedule& schedule, std::uint64_
                              std::to_string(budget));
 }
 
-IntegralHistogramTensor build_from_source(const spct_source& src) {
+IntegralHistogramTensor build_from_source(const spct_source& src, std::unique_ptr<DevBuf> src_mem) {
     auto dt = std::make_shared<detail::DeviceTensor>();
+    dt->src = src;
+    dt->src_mem = std::move(src_mem);
     spct_ih& d = dt->desc;
     std::uint64_t bytes = 0;
     check(spct_cu_ih_layout(src.width, src.height, src.nbins, &d.row_pitch, &d.plane_pitch, &bytes));
@@ -229,16 +246,16 @@ IntegralHistogramTensor build_from_source(const spct_source& src) {
 IntegralHistogramTensor build_integral_histogram(const BinMap& bins, const ScanSchedule& schedule,
                                                  std::uint64_t memory_budget) {
     validate_build(bins, schedule, memory_budget);
-    DevBuf src(bins.data.size() * 2);
-    upload(src, bins.data);
+    auto src = std::make_unique<DevBuf>(bins.data.size() * 2);
+    upload(*src, bins.data);
     spct_source s{};
     s.kind = SPCT_SRC_BINS_U16;
-    s.plane[0] = src.p;
+    s.plane[0] = src->p;
     s.pitch = bins.width;
     s.width = bins.width;
     s.height = bins.height;
     s.nbins = bins.bins;
-    return build_from_source(s);
+    return build_from_source(s, std::move(src));
 }
 
 namespace {
@@ -287,7 +304,19 @@ LikelihoodMap hist_match_map(const IntegralHistogramTensor& t, const std::vector
     const spct_ih& d = desc_of(t);
     DevBuf tm(th.size() * 8), map(std::size_t(t.width) * t.height * 8);
     upload(tm, th);
-    check(spct_cu_hist_match(&d, tm.as<double>(), kw, kh, p, int(metric), map.as<double>(), nullptr));
+    const detail::DeviceTensor& dt = *t.data.dev;
+    if (dt.src_mem && !exact_maps()) {
+        // recompute the window counts from the source in the fused sweep (no tensor re-read)
+        spct_ih nodata = d;
+        nodata.data = nullptr;
+        std::size_t ws = 0;
+        check(spct_cu_ih_build_workspace(&dt.src, 0, d.bins, &ws));
+        DevBuf work(ws);
+        check(spct_cu_ih_build_match_map(&dt.src, &nodata, tm.as<double>(), kw, kh, p, int(metric), map.as<double>(),
+                                         work.p, ws, nullptr));
+    } else {
+        check(spct_cu_hist_match(&d, tm.as<double>(), kw, kh, p, int(metric), map.as<double>(), nullptr));
+    }
     LikelihoodMap out;
     out.width = t.width;
     out.height = t.height;
@@ -311,12 +340,13 @@ LikelihoodMap likelihood_from_frame(const GrayImage& img, int bins, const std::v
         throw contract_error("tensor of " + std::to_string(est.padded_bytes) + " bytes exceeds the memory budget of " +
                              std::to_string(memory_budget));
     check(spct_cu_hist_check(bins, img.width, img.height, th.data(), int(th.size()), kw, kh, p));
-    DevBuf src(img.data.size()), tm(th.size() * 8);
-    upload(src, img.data);
+    auto src = std::make_unique<DevBuf>(img.data.size());
+    DevBuf tm(th.size() * 8);
+    upload(*src, img.data);
     upload(tm, th);
     spct_source s{};
     s.kind = SPCT_SRC_GRAY_U8;
-    s.plane[0] = src.p;
+    s.plane[0] = src->p;
     s.pitch = img.width;
     s.width = img.width;
     s.height = img.height;
@@ -350,6 +380,8 @@ LikelihoodMap likelihood_from_frame(const GrayImage& img, int bins, const std::v
         tensor_out->height = img.height;
         tensor_out->width = img.width;
         tensor_out->data.clear();
+        dt->src = s;
+        dt->src_mem = std::move(src);
         tensor_out->data.dev = std::move(dt);
     }
     return out;

@@ -167,6 +167,12 @@ int main() {
         CHECK(std::abs(h6.at(0, 1) - 0.7) <= 1e-12);
         CHECK_THROWS_AS(hist_distance_map(t6, {0.4, 0.4, 0.2}, 2, 3, 0.5), contract_error);
         CHECK_THROWS_AS(hist_distance_map(t6, {0.5, 0.5}, 2, 3, 1.0), contract_error);
+        // exact mode (tensor re-read, reference operation order) agrees with the default
+        set_exact_maps(true);
+        LikelihoodMap mx = hist_distance_map(t, th, win.w, win.h, 1.0);
+        set_exact_maps(false);
+        for (std::size_t i = 0; i < mx.values.size(); ++i)
+            CHECK(std::abs(mx.values[i] - map.values[i]) <= 1e-5 * std::abs(mx.values[i]) + 1e-12);
         // the fused frame path agrees with build + hist_distance_map
         IntegralHistogramTensor tf;
         LikelihoodMap mf = likelihood_from_frame(img, 8, th, win.w, win.h, 1.0, &tf);

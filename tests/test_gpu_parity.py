@@ -190,11 +190,14 @@ def test_maps_golden_reference(P, golden):
     vec = golden[1]
     t = P.build_integral_histogram(vec["lmap_noise_img"], 8)
     tm = np.full(8, 1 / 8)
-    assert np.array_equal(P.hist_distance_map(t, tm, 7, 5, 1.0).cpu().numpy(), vec["lmap_noise_p1"])
+    assert np.array_equal(P.hist_distance_map(t, tm, 7, 5, 1.0, exact=True).cpu().numpy(), vec["lmap_noise_p1"])
+    assert close(P.hist_distance_map(t, tm, 7, 5, 1.0).cpu().numpy(), vec["lmap_noise_p1"])
     assert close(P.hist_distance_map(t, tm, 7, 5, 2.0).cpu().numpy(), vec["lmap_noise_p2"])
+    assert close(P.hist_distance_map(t, tm, 7, 5, 2.0, exact=True).cpu().numpy(), vec["lmap_noise_p2"])
     t = P.build_integral_histogram(vec["lmap_smooth_img"], 16)
     th = vec["lmap_smooth_tmpl"]
-    assert np.array_equal(P.hist_distance_map(t, th, 20, 16, 1.0).cpu().numpy(), vec["lmap_smooth_p1"])
+    assert np.array_equal(P.hist_distance_map(t, th, 20, 16, 1.0, exact=True).cpu().numpy(), vec["lmap_smooth_p1"])
+    assert close(P.hist_distance_map(t, th, 20, 16, 1.0).cpu().numpy(), vec["lmap_smooth_p1"])
     assert close(P.hist_distance_map(t, th, 20, 16, 3.0).cpu().numpy(), vec["lmap_smooth_p3"])
 
 
@@ -208,10 +211,13 @@ def test_maps_vs_oracle(P, w, h, bins, kw, kh):
     th = np.bincount(crop.reshape(-1), minlength=bins).astype(np.float64) / crop.size
     t = P.build_integral_histogram(img, bins)
     want = oracle.hist_match_map_direct(qb, bins, th, kw, kh, 1.0)
-    got = P.hist_distance_map(t, th, kw, kh, 1.0).cpu().numpy()
-    assert np.array_equal(got, want)
+    got = P.hist_distance_map(t, th, kw, kh, 1.0, exact=True).cpu().numpy()
+    assert np.array_equal(got, want)  # tensor path: the reference's rounding sequence
+    assert close(P.hist_distance_map(t, th, kw, kh, 1.0).cpu().numpy(), want)  # source path
     assert got[y0 + (kh - 1) // 2, x0 + (kw - 1) // 2] == 1.0  # the template's own window
     for p in (1.5, 2.0, 3.0):
+        assert close(P.hist_distance_map(t, th, kw, kh, p, exact=True).cpu().numpy(),
+                     oracle.hist_match_map_direct(qb, bins, th, kw, kh, p))
         assert close(P.hist_distance_map(t, th, kw, kh, p).cpu().numpy(),
                      oracle.hist_match_map_direct(qb, bins, th, kw, kh, p))
     for metric in (1, 2, 3):  # extensions: parity against the self-written oracle definitions
@@ -385,4 +391,5 @@ def test_against_live_reference(P):
     assert np.array_equal(t.padded_u64(), rt.array())
     crop = qb[10:21, 5:18]
     th = np.bincount(crop.reshape(-1), minlength=9).astype(np.float64) / crop.size
-    assert np.array_equal(P.hist_distance_map(t, th, 13, 11, 1.0).cpu().numpy(), rt.hist_distance_map(th, 13, 11, 1.0))
+    assert np.array_equal(P.hist_distance_map(t, th, 13, 11, 1.0, exact=True).cpu().numpy(),
+                          rt.hist_distance_map(th, 13, 11, 1.0))
