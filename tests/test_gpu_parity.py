@@ -323,6 +323,24 @@ def test_fused_map_direct(P, w, h, bins, kw, kh, store):
         assert close(lmap.cpu().numpy(), oracle.hist_match_map_direct(qb, bins, tg, kw, kh, p, metric)), (p, metric)
 
 
+def test_frame_pipeline_matches_single_frames(P):
+    from paper_1711_01656_b200.pipeline import FramePipeline
+
+    w, h, bins, kw, kh = 300, 220, 64, 64, 48
+    frames = [oracle.smooth_image(w, h, 500 + i) for i in range(5)]
+    qb0 = oracle.quantize(frames[0], bins)
+    th = _crop_template(qb0, bins, 100, 80, kw, kh)
+    pipe = FramePipeline(w, h, bins, th, kw, kh, 1.0)
+    hf = FramePipeline.pinned_frames(frames)
+    hm = pipe.pinned_maps(len(frames))
+    pipe.run(hf, hm)
+    for f, m in zip(frames, hm):
+        qb = oracle.quantize(f, bins)
+        assert close(m.numpy(), oracle.hist_match_map_direct(qb, bins, th, kw, kh, 1.0))
+    # the tensor of the last frame stays resident
+    assert np.array_equal(pipe.tensor.padded_u64(), oracle.build_ih(oracle.quantize(frames[-1], bins), bins))
+
+
 def test_fused_map_rejects_slabs(P):
     img = oracle.smooth_image(100, 80, 1)
     t = P.IntegralHistogramTensor(100, 80, 32, bin0=16, bins=16)
