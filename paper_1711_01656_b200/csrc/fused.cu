@@ -391,6 +391,22 @@ namespace spct_impl {
 size_t fused_prep_bytes(int bins) { return (static_cast<size_t>(bins) + 1) * 4 + 256 + ((bins + 127) / 128 + 1) * 8; }
 }  // namespace spct_impl
 
+namespace spct_impl {
+int fused_ctas_per_sm() {
+    static int n = 0;
+    if (n) return n;
+    int v = 0;
+    cudaFuncSetAttribute(spct_fused::sweep_match_kernel<true, true, 64>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)spct_fused::kSmemBytes);
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&v, spct_fused::sweep_match_kernel<true, true, 64>, 256,
+                                                      spct_fused::kSmemBytes) != cudaSuccess || v <= 0) {
+        cudaGetLastError();
+        v = 2;
+    }
+    return n = v;
+}
+}  // namespace spct_impl
+
 namespace spct_fused {
 
 template <int KWM>
@@ -455,7 +471,7 @@ spct_status build_match(const spct_source* src, const spct_ih* out, const double
         if (map) return spct_cu_hist_match(out, tmpl, kw, kh, p, metric, map, stream);
         return spct_cu_hist_partial(out, tmpl, kw, kh, p, metric, partial, 0, stream);
     }
-    const BuildPlan bp = plan_build(out->width, out->height, out->bins, kB);
+    const BuildPlan bp = plan_fused_sweep(out->width, out->height, out->bins);
     const size_t need = (out->data ? bp.lt_bytes + bp.hb_bytes : 0) + fused_prep_bytes(out->bins);
     if (!workspace || workspace_bytes < need) return contract("ih_build_match: workspace too small");
     uint32_t *Lt = nullptr, *Hb = nullptr;

@@ -27,7 +27,20 @@ namespace spct_impl {
 
 // ------------------------------------------------------------------ planning
 
-BuildPlan plan_build(int width, int height, int bins, int force_B) {
+int device_sms() {
+    static int sms = [] {
+        int dev = 0, n = 0;
+        if (cudaGetDevice(&dev) != cudaSuccess ||
+            cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || n <= 0) {
+            cudaGetLastError();
+            return 148;  // B200
+        }
+        return n;
+    }();
+    return sms;
+}
+
+BuildPlan plan_build(int width, int height, int bins, int force_B, int ctas_per_sm, int min_band_rows) {
     BuildPlan p{};
     p.B = force_B ? force_B : (bins <= 4 ? 4 : (bins <= 8 ? 8 : 16));
     const int nslabs = static_cast<int>(ceil_div(bins, p.B));
@@ -39,12 +52,30 @@ BuildPlan plan_build(int width, int height, int bins, int force_B) {
     int band_rows = 0;
     if (const char* e = std::getenv("SPCT_BAND_ROWS")) band_rows = std::atoi(e);
     if (band_rows <= 0) {
-        // Aim for ~1024 independent tiles so 148 SMs get balanced work; never
-        // shorter than 64 rows (the carry tables scale with 1 / band_rows).
+        // Each (strip, band, slab group) tile is one long-lived CTA.  Pick the band count so
+        // the tiles fill whole waves of the resident CTA slots (SMs x CTAs per SM): a
+        // partial last wave runs at partial occupancy for a full tile time.  Bands are
+        // kept >= min_band_rows (carry tables and the matcher's pre-roll scale with
+        // 1 / band_rows).
         const int64_t per_band = static_cast<int64_t>(p.nstrips) * p.slab_groups;
-        int64_t nb = std::max<int64_t>(1, ceil_div(1024, per_band));
-        nb = std::min<int64_t>(nb, std::max<int64_t>(1, height / 64));
-        band_rows = static_cast<int>(ceil_div(height, nb));
+        const int64_t slots = static_cast<int64_t>(device_sms()) * std::max(1, ctas_per_sm);
+        const int64_t nb_max = std::max<int64_t>(1, height / std::max(1, min_band_rows));
+        int64_t best_nb = 1;
+        double best_eff = -1.0;
+        for (int64_t nb = 1; nb <= nb_max; ++nb) {
+            const int br = static_cast<int>(ceil_div(height, nb));
+            const int64_t tiles = per_band * ceil_div(height, br);
+            const int64_t waves = ceil_div(tiles, slots);
+            if (waves > 8) break;  // finer than 8 waves buys nothing
+            // load balance x a mild preference for >= 2 waves (tail hiding across tiles)
+            const double eff = static_cast<double>(tiles) / static_cast<double>(waves * slots) *
+                               (waves >= 2 ? 1.0 : 0.97);
+            if (eff > best_eff + 1e-9) {
+                best_eff = eff;
+                best_nb = nb;
+            }
+        }
+        band_rows = static_cast<int>(ceil_div(height, best_nb));
     }
     band_rows = std::max(1, std::min(band_rows, height));
     p.band_rows = band_rows;
@@ -187,6 +218,35 @@ int grid_for(int64_t n, int block) {
 
 using namespace spct_build;
 
+namespace spct_impl {
+
+int build_ctas_per_sm(int B, int threads) {
+    static int cache[3][9] = {};
+    const int bi = B == 4 ? 0 : (B == 8 ? 1 : 2), wi = std::min(8, std::max(1, threads / 32));
+    if (cache[bi][wi]) return cache[bi][wi];
+    int n = 0;
+    cudaError_t e;
+    if (B == 4) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, ih_sweep_kernel<4, false>, threads, 0);
+    else if (B == 8) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, ih_sweep_kernel<8, false>, threads, 0);
+    else e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, ih_sweep_kernel<16, false>, threads, 0);
+    if (e != cudaSuccess || n <= 0) {
+        cudaGetLastError();
+        n = 2;
+    }
+    return cache[bi][wi] = n;
+}
+
+BuildPlan plan_build_sweep(int width, int height, int bins) {
+    const BuildPlan probe = plan_build(width, height, bins, 0, 2, 32);
+    return plan_build(width, height, bins, 0, build_ctas_per_sm(probe.B, 32 * probe.warps), 32);
+}
+
+BuildPlan plan_fused_sweep(int width, int height, int bins) {
+    return plan_build(width, height, bins, 16, fused_ctas_per_sm(), 64);
+}
+
+}  // namespace spct_impl
+
 // ------------------------------------------------------------------ C-ABI
 
 extern "C" spct_status spct_cu_to_grayscale(const uint8_t* r, const uint8_t* g, const uint8_t* b, int64_t n,
@@ -243,8 +303,8 @@ extern "C" spct_status spct_cu_ih_build_workspace(const spct_source* src, int bi
     (void)bin0;
     if (!src || !bytes) return contract("ih_build_workspace: null argument");
     if (!(src->width > 0 && src->height > 0 && bins >= 1)) return contract("build: empty bin map");
-    const BuildPlan p = plan_build(src->width, src->height, bins);
-    const BuildPlan pf = plan_build(src->width, src->height, bins, 16);  // fused sweep: 16 bins per warp
+    const BuildPlan p = plan_build_sweep(src->width, src->height, bins);
+    const BuildPlan pf = plan_fused_sweep(src->width, src->height, bins);  // fused sweep: 16 bins per warp
     *bytes = std::max(p.lt_bytes + p.hb_bytes, pf.lt_bytes + pf.hb_bytes) + fused_prep_bytes(bins) + 256;
     return SPCT_OK;
 }
@@ -259,7 +319,7 @@ extern "C" spct_status spct_cu_ih_build(const spct_source* src, const spct_ih* o
     if (out->width != src->width || out->height != src->height || out->nbins_total != src->nbins)
         return contract("ih_build: tensor dims do not match the source");
     if (reinterpret_cast<uintptr_t>(out->data) % 16 != 0) return contract("ih_build: tensor data must be 16-byte aligned");
-    const BuildPlan p = plan_build(out->width, out->height, out->bins);
+    const BuildPlan p = plan_build_sweep(out->width, out->height, out->bins);
     cudaStream_t s = as_stream(stream);
     uint32_t *Lt, *Hb;
     if (auto st = build_carries(q, *out, p, workspace, workspace_bytes, s, &Lt, &Hb)) return st;

@@ -58,7 +58,16 @@ struct BuildPlan {
     int slab_groups;  // CTAs along the bin axis
     size_t lt_bytes, hb_bytes;
 };
-BuildPlan plan_build(int width, int height, int bins, int force_B = 0);
+BuildPlan plan_build(int width, int height, int bins, int force_B = 0, int ctas_per_sm = 2, int min_band_rows = 32);
+
+// Resident CTAs per SM of the build sweep (B bins per warp, `threads` per CTA) and of the
+// fused sweep; used to size bands in whole waves.  Fall back to 2 without a device.
+int build_ctas_per_sm(int B, int threads);
+int fused_ctas_per_sm();
+int device_sms();
+// The two plans every caller (workspace query included) must agree on.
+BuildPlan plan_build_sweep(int width, int height, int bins);
+BuildPlan plan_fused_sweep(int width, int height, int bins);
 
 // Workspace of the fused path's template prep (fused.cu).
 size_t fused_prep_bytes(int bins);
