@@ -10,7 +10,8 @@ import ctypes as C
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libspct_b200.so")
+# SPCT_LIB_PATH: development hook for A/B runs of alternative builds of the same library
+LIB_PATH = os.environ.get("SPCT_LIB_PATH") or os.path.join(HERE, "libspct_b200.so")
 
 SPCT_OK, SPCT_ERR_CONTRACT, SPCT_ERR_IO, SPCT_ERR_CUDA, SPCT_ERR_OOM = 0, 2, 3, 4, 5
 SRC_BINS_U16, SRC_GRAY_U8, SRC_RGB_U8, SRC_SCALAR_F64 = 0, 1, 2, 3

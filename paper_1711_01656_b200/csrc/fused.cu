@@ -49,7 +49,7 @@ struct FusedParams {
     const long long* S_group;    // sum of integral s_k per 128-bin group
     double* partial;
     double* map;                 // non-null: write the finished likelihood map (one group = every bin)
-    double inv_p, dmax;
+    double inv_p, dmax, inv_dmax;  // inv_dmax != 0 iff dmax is a power of two (exact product)
     int W, H;
 };
 
@@ -58,9 +58,9 @@ __device__ __forceinline__ double finalize_L(double s, const FusedParams& f) {
     double L;
     if (f.metric == SPCT_METRIC_MINKOWSKI) {
         const double d = f.p_kind == 1 ? s : pow(s, f.inv_p);
-        L = __dsub_rn(1.0, __ddiv_rn(d, f.dmax));
+        L = __dsub_rn(1.0, f.inv_dmax != 0.0 ? __dmul_rn(d, f.inv_dmax) : __ddiv_rn(d, f.dmax));
     } else if (f.metric == SPCT_METRIC_CHISQ) {
-        L = __dsub_rn(1.0, __ddiv_rn(s, 2.0));
+        L = __dsub_rn(1.0, __dmul_rn(s, 0.5));  // == s / 2 exactly
     } else {
         L = s;
     }
@@ -212,32 +212,56 @@ __global__ void __launch_bounds__(256, 2) sweep_match_kernel(QuantParams q, Pixe
                                  ? Lt + static_cast<int64_t>(strip) * H * Lb + g0 + tid
                                  : nullptr;
     // raw pixel values of the staging column, quantised one row after the load
-    uint64_t rn = xt_live ? pixel_raw(q, xt, ystart) : 0, ro = 0;
-    bool have_o = false;  // ystart - kh < ystart: nothing to remove on the first row
-    uint32_t lpre = lt_cta ? __ldg(lt_cta + static_cast<int64_t>(ystart) * Lb) : 0u;
-    __syncthreads();
+    uint64_t rn = xt_live ? pixel_raw(q, xt, y0) : 0, ro = 0;
+    bool have_o = false;  // y0 - kh < ystart: nothing to remove on the first row
+    uint32_t lpre = lt_cta ? __ldg(lt_cta + static_cast<int64_t>(y0) * Lb) : 0u;
+    __syncthreads();  // vc zeroed
 
-    // deferred cross-warp combine of row yy (thread t < 128: window ending at strip column t)
+    // Pre-roll rows [ystart, y0) only feed vc, and nothing leaves the window there: one
+    // barrier-free pass with several loads in flight (a per-row loop would pay the full
+    // DRAM latency on every row).
+    if (xt_live) {
+        const int nb_lo = out.bin0 + g0;
+        const uint32_t inc = 1u << (16 * (tid & 1));
+        uint32_t* vcol = vc + (tid >> 1);
+        for (int y = ystart; y < y0; y += 8) {
+            uint64_t r[8];
+#pragma unroll
+            for (int i = 0; i < 8; ++i) r[i] = y + i < y0 ? pixel_raw(q, xt, y + i) : 0;
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+                const int bn = bin_of_raw(r[i], q) - nb_lo;
+                if (y + i < y0 && static_cast<unsigned>(bn) < static_cast<unsigned>(nb_cta))
+                    atomicAdd(vcol + bn * kVcWords, inc);
+            }
+        }
+    }
+
+    // Cross-warp combine of row yy: thread t < 128 sums the 8 warps' partials of the
+    // window ending at strip column t in a fixed order.  (Spreading it over all 8 warps
+    // was measured slower: every warp then carries the combine's latency.)
     auto combine = [&](int yy) {
         if (tid < kStrip) {
-            const int e = xs + tid;
+            const int t = tid;
+            const double* rb = red + (yy & 1) * (kWarps * kStrip);
+            double term = 0.0;
+            if (FAST) {
+                // I | C << 16 per warp; both sums stay below 2^16 (at most kw * kh <= 32640)
+                uint32_t x = 0;
+#pragma unroll
+                for (int w = 0; w < kWarps; ++w)
+                    if (w < nwarps_live) x += reinterpret_cast<const uint32_t*>(rb + w * kStrip)[2 * t];
+                const long long I = x & 0xFFFFu, C = x >> 16;
+                term = f.metric == SPCT_METRIC_INTERSECTION ? static_cast<double>(I) * f.invT
+                                                            : static_cast<double>(C + S - 2 * I) * f.invT;
+            } else {
+#pragma unroll
+                for (int w = 0; w < kWarps; ++w)
+                    if (w < nwarps_live) term = __dadd_rn(term, rb[w * kStrip + t]);
+            }
+            const int e = xs + t;
             const int u = e - f.kw + 1, v = yy - f.kh + 1;
             if (u >= 0 && e < W) {
-                const double* rb = red + (yy & 1) * (kWarps * kStrip);
-                double term;
-                if (FAST) {
-                    long long I = 0, C = 0;
-                    for (int w = 0; w < nwarps_live; ++w) {
-                        const uint32_t x = reinterpret_cast<const uint32_t*>(rb + w * kStrip)[2 * tid];
-                        I += x & 0xFFFFu;
-                        C += x >> 16;
-                    }
-                    term = f.metric == SPCT_METRIC_INTERSECTION ? static_cast<double>(I) * f.invT
-                                                                : static_cast<double>(C + S - 2 * I) * f.invT;
-                } else {
-                    term = 0.0;
-                    for (int w = 0; w < nwarps_live; ++w) term = __dadd_rn(term, rb[w * kStrip + tid]);
-                }
                 if (f.map) {
                     // finished map with spread_valid's border replication (likelihood.cpp:44-58)
                     const double L = finalize_L(term, f);
@@ -254,13 +278,13 @@ __global__ void __launch_bounds__(256, 2) sweep_match_kernel(QuantParams q, Pixe
         }
     };
 
-    int pend_y = -1;
-    for (int y = ystart; y < y1; ++y) {
-        __syncthreads();  // A: previous row's vc / red / staging reads are done
-        if (pend_y >= 0) {
-            combine(pend_y);
-            pend_y = -1;
-        }
+    // row yy's partials are in `red` (and must be combined) iff it is a match row
+    auto pending = [&](int yy) { return yy >= y0 && yy >= f.kh - 1; };
+    for (int y = y0; y < y1; ++y) {
+        __syncthreads();  // A: previous row's vc / staging reads are done, its partials written
+        // row y - 1's partials were written before A; its buffer is rewritten only after
+        // the next B.  Warps 0-3 combine while warps 4-7 start staging.
+        if (pending(y - 1)) combine(y - 1);
         {   // stage row y: vertical running histogram (add row y, remove row y - kh),
             // the strip's bins and row carries for the sweep, then prefetch row y + 1
             const int pn = xt_live ? bin_of_raw(rn, q) : 0xFFFF;
@@ -287,12 +311,8 @@ __global__ void __launch_bounds__(256, 2) sweep_match_kernel(QuantParams q, Pixe
             }
         }
         __syncthreads();  // B: vc holds rows (y - kh, y]; staging rows ready
-        if (y < y0) continue;  // pre-roll rows only feed vc
         const bool match_row = y >= f.kh - 1;
-        if (!warp_live || (!STORE && !match_row)) {
-            pend_y = match_row ? y : pend_y;
-            continue;
-        }
+        if (!warp_live || (!STORE && !match_row)) continue;
 
         uint32_t bins4 = 0;
         if (STORE) {
@@ -373,11 +393,10 @@ __global__ void __launch_bounds__(256, 2) sweep_match_kernel(QuantParams q, Pixe
                 rb[4 * lane + 2] = acc[2];
                 rb[4 * lane + 3] = acc[3];
             }
-            pend_y = y;
         }
     }
     __syncthreads();
-    if (pend_y >= 0) combine(pend_y);
+    if (y1 > y0 && pending(y1 - 1)) combine(y1 - 1);
 }
 
 constexpr size_t kSmemBytes = (size_t(kGroupBins) * kVcWords + size_t(kWarps) * 4 * kVcWords) * 4 +
@@ -495,6 +514,10 @@ spct_status build_match(const spct_source* src, const spct_ih* out, const double
     f.p = p;
     f.inv_p = 1.0 / p;
     f.dmax = std::pow(2.0, 1.0 / p);  // likelihood.cpp:208
+    {   // d / dmax == d * (1 / dmax) bit for bit when dmax is a power of two (p = 1: dmax = 2)
+        int e = 0;
+        f.inv_dmax = std::frexp(f.dmax, &e) == 0.5 ? 1.0 / f.dmax : 0.0;
+    }
     f.p_kind = p == 1.0 ? 1 : (p == 2.0 ? 2 : 0);
     f.T = static_cast<double>(T);
     f.invT = 1.0 / f.T;

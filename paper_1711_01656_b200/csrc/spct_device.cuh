@@ -158,6 +158,17 @@ __device__ __forceinline__ void st_cs_v4_if(bool pred, uint32_t* p, uint32_t a, 
     if (pred) __stcs(reinterpret_cast<uint4*>(p), make_uint4(a, b, c, d));
 }
 
+// Same store, predicated in PTX so it never becomes a branch.  No "memory" clobber:
+// nothing in the sweeps reads the integral histogram back, and a clobber would pin
+// every shared-memory access around the store.
+__device__ __forceinline__ void st_cs_v4_pred(uint32_t pred, uint32_t* p, uint32_t a, uint32_t b, uint32_t c,
+                                              uint32_t d) {
+    asm volatile(
+        "{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %5, 0;\n\t"
+        "@q st.global.cs.v4.u32 [%0], {%1, %2, %3, %4};\n\t}" ::"l"(p),
+        "r"(a), "r"(b), "r"(c), "r"(d), "r"(pred));
+}
+
 __device__ __forceinline__ int lane_id() { return threadIdx.x & 31; }
 
 }  // namespace spct_dev

@@ -139,7 +139,7 @@ __device__ __forceinline__ void vpart_row(uint32_t (&V)[4][B], uint32_t bins4, u
             V[1][k] += base + __byte_perm(P[i], 0, 0x4441);
             V[2][k] += base + __byte_perm(P[i], 0, 0x4442);
             V[3][k] += base + (P[i] >> 24);
-            st_cs_v4_if(store && (!GUARD || k < k_live), p, V[0][k], V[1][k], V[2][k], V[3][k]);
+            st_cs_v4_pred(store && (!GUARD || k < k_live), p, V[0][k], V[1][k], V[2][k], V[3][k]);
             p += plane_pitch;
         }
     }
@@ -169,7 +169,7 @@ __device__ __forceinline__ void vpart_group(uint32_t (&V)[4][B], int g, uint32_t
         V[1][k] += base + __byte_perm(P[i], 0, 0x4441);
         V[2][k] += base + __byte_perm(P[i], 0, 0x4442);
         V[3][k] += base + (P[i] >> 24);
-        st_cs_v4_if((store_mask >> k) & 1u, p, V[0][k], V[1][k], V[2][k], V[3][k]);
+        st_cs_v4_pred((store_mask >> k) & 1u, p, V[0][k], V[1][k], V[2][k], V[3][k]);
         p += plane_pitch;
     }
 }
@@ -210,7 +210,7 @@ __device__ __forceinline__ void vpart_apply(uint32_t (&V)[4][B], int g, const ui
         V[1][k] += base + __byte_perm(P[i], 0, 0x4441);
         V[2][k] += base + __byte_perm(P[i], 0, 0x4442);
         V[3][k] += base + (P[i] >> 24);
-        st_cs_v4_if((store_mask >> k) & 1u, p, V[0][k], V[1][k], V[2][k], V[3][k]);
+        st_cs_v4_pred((store_mask >> k) & 1u, p, V[0][k], V[1][k], V[2][k], V[3][k]);
         p += plane_pitch;
     }
 }
