@@ -150,6 +150,53 @@ __device__ __forceinline__ void window_prefix(const uint32_t* vw, uint32_t* g, i
     }
 }
 
+// Half-warp variant (integer path): half h of the warp handles one bin, lane m = lane & 15
+// owns the 8 halo columns 8m..8m+7 and the 8 strip columns 128+8m.. of the extended row,
+// as four u16-pair words each (a: halo, b: strip).  One 16-lane scan then serves one
+// bin per half, i.e. two bins per warp scan (4 shuffle steps instead of 2 x 5).
+__device__ __forceinline__ uint32_t scan_add16(uint32_t v, int o) {
+    uint32_t r;
+    asm("{\n\t.reg .pred p;\n\t.reg .u32 t;\n\t"
+        "shfl.sync.up.b32 t|p, %1, %2, 0x1000, 0xffffffff;\n\t"
+        "@p add.u32 %1, %1, t;\n\t"
+        "mov.u32 %0, %1;\n\t}"
+        : "=r"(r), "+r"(v)
+        : "r"(o));
+    return r;
+}
+
+template <bool STAGE>
+__device__ __forceinline__ void window_prefix16(const uint32_t* vrow, uint32_t* g, int m, uint32_t (&a)[4],
+                                                uint32_t (&b)[4]) {
+    const uint4 wa = *reinterpret_cast<const uint4*>(vrow + 4 * m);
+    const uint4 wb = *reinterpret_cast<const uint4*>(vrow + 64 + 4 * m);
+    a[0] = wa.x * 0x10001u;
+    a[1] = wa.y * 0x10001u + __byte_perm(a[0], 0, 0x3232);
+    a[2] = wa.z * 0x10001u + __byte_perm(a[1], 0, 0x3232);
+    a[3] = wa.w * 0x10001u + __byte_perm(a[2], 0, 0x3232);
+    b[0] = wb.x * 0x10001u;
+    b[1] = wb.y * 0x10001u + __byte_perm(b[0], 0, 0x3232);
+    b[2] = wb.z * 0x10001u + __byte_perm(b[1], 0, 0x3232);
+    b[3] = wb.w * 0x10001u + __byte_perm(b[2], 0, 0x3232);
+    const uint32_t tot = __byte_perm(a[3], b[3], 0x7632);  // {sum a, sum b}
+    uint32_t inc = tot;
+#pragma unroll
+    for (int o = 1; o < 16; o <<= 1) inc = scan_add16(inc, o);
+    const uint32_t ex = inc - tot;
+    const uint32_t T1 = __byte_perm(__shfl_sync(0xffffffffu, inc, 15, 16), 0, 0x1010);  // halo total
+    const uint32_t ba = __byte_perm(ex, 0, 0x1010);
+    const uint32_t bb = __byte_perm(ex, 0, 0x3232) + T1;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        a[i] += ba;
+        b[i] += bb;
+    }
+    if (STAGE) {
+        *reinterpret_cast<uint4*>(g + 4 * m) = make_uint4(a[0], a[1], a[2], a[3]);
+        *reinterpret_cast<uint4*>(g + 64 + 4 * m) = make_uint4(b[0], b[1], b[2], b[3]);
+    }
+}
+
 // Window counts, phase 2 (after a __syncwarp): c = G(e) - G(e - kw) for the lane's four
 // windows, as two u16 pairs {j=0, j=1}, {j=2, j=3}.
 __device__ __forceinline__ void window_diff(const uint32_t* g, int pw, int psh, uint32_t b0, uint32_t b1,
@@ -204,6 +251,11 @@ __global__ void __launch_bounds__(256, 2) sweep_match_kernel(QuantParams q, Pixe
     const int pw = idx >> 1, psh = (idx & 1) * 16;
     uint32_t* gb = gbuf + warp * 4 * kVcWords;
     const uint32_t* vbase = vc + warp * kB * kVcWords + 2 * lane;
+    // integer path (half-warp layout): half hh, lane mm owns windows 8mm .. 8mm+7
+    const int hh = lane >> 4, mm = lane & 15;
+    const uint32_t* vwarp = vc + warp * kB * kVcWords;
+    const int idx16 = kStrip + 8 * mm - f.kw;
+    const int pw16 = idx16 >> 1, psh16 = (idx16 & 1) * 16;
 
     // staging thread: extended column tid; prefetch one row ahead
     const int xt = xs - kStrip + tid;
@@ -247,10 +299,11 @@ __global__ void __launch_bounds__(256, 2) sweep_match_kernel(QuantParams q, Pixe
             double term = 0.0;
             if (FAST) {
                 // I | C << 16 per warp; both sums stay below 2^16 (at most kw * kh <= 32640)
+                const uint32_t* rw = reinterpret_cast<const uint32_t*>(red) + (yy & 1) * (kWarps * kStrip) + t;
                 uint32_t x = 0;
 #pragma unroll
                 for (int w = 0; w < kWarps; ++w)
-                    if (w < nwarps_live) x += reinterpret_cast<const uint32_t*>(rb + w * kStrip)[2 * t];
+                    if (w < nwarps_live) x += rw[w * kStrip];
                 const long long I = x & 0xFFFFu, C = x >> 16;
                 term = f.metric == SPCT_METRIC_INTERSECTION ? static_cast<double>(I) * f.invT
                                                             : static_cast<double>(C + S - 2 * I) * f.invT;
@@ -332,13 +385,42 @@ __global__ void __launch_bounds__(256, 2) sweep_match_kernel(QuantParams q, Pixe
         uint32_t* prow = STORE ? base_ptr + static_cast<int64_t>(y) * out.row_pitch : nullptr;
 
         uint32_t I0 = 0, I1 = 0, C0 = 0, C1 = 0;
+        uint32_t Iw[4] = {0, 0, 0, 0}, Cw[4] = {0, 0, 0, 0};
         double acc[4] = {0.0, 0.0, 0.0, 0.0};
 #pragma unroll
         for (int g = 0; g < kB / 4; ++g) {
             if (STORE)
                 vpart_group<kB>(V, g, bins4 ^ kpat0, lr[g], prow + static_cast<int64_t>(4 * g) * out.plane_pitch,
                                 out.plane_pitch, store_mask);
-            if (match_row) {
+            if (FAST && match_row) {
+                // half-warp layout: bins 4g + 2p + hh, p = 0, 1
+                uint32_t a[2][4], b[2][4];
+#pragma unroll
+                for (int p = 0; p < 2; ++p)
+                    window_prefix16<KWM == 0>(vwarp + (4 * g + 2 * p + hh) * kVcWords, gb + (2 * p + hh) * kVcWords, mm,
+                                              a[p], b[p]);
+                if (KWM == 0) __syncwarp();
+#pragma unroll
+                for (int p = 0; p < 2; ++p) {
+                    const uint32_t sk = srep_s[warp * kB + 4 * g + 2 * p + hh];
+#pragma unroll
+                    for (int i = 0; i < 4; ++i) {
+                        uint32_t c;
+                        if (KWM == 64) {
+                            // G(e - 64): partner lane m ^ 8's halo (m < 8) or strip (m >= 8) words
+                            c = b[p][i] - __shfl_xor_sync(0xffffffffu, mm >= 8 ? a[p][i] : b[p][i], 8);
+                        } else if (KWM == 128) {
+                            c = b[p][i] - a[p][i];
+                        } else {
+                            const uint32_t* gg = gb + (2 * p + hh) * kVcWords + pw16 + i;
+                            c = b[p][i] - __funnelshift_r(gg[0], gg[1], psh16);
+                        }
+                        Iw[i] += min_u16x2(c, sk);
+                        Cw[i] += c;
+                    }
+                }
+                if (KWM == 0) __syncwarp();
+            } else if (match_row) {
                 uint32_t aw[4][2], bw[4][2];
 #pragma unroll
                 for (int i = 0; i < 4; ++i)
@@ -381,12 +463,19 @@ __global__ void __launch_bounds__(256, 2) sweep_match_kernel(QuantParams q, Pixe
         if (match_row) {
             double* rb = red + (y & 1) * (kWarps * kStrip) + warp * kStrip;
             if (FAST) {
-                // per window: I | C << 16 in the low word of the slot
-                uint32_t* rw = reinterpret_cast<uint32_t*>(rb);
-                rw[2 * (4 * lane + 0)] = (I0 & 0xFFFFu) | (C0 << 16);
-                rw[2 * (4 * lane + 1)] = (I0 >> 16) | (C0 & 0xFFFF0000u);
-                rw[2 * (4 * lane + 2)] = (I1 & 0xFFFFu) | (C1 << 16);
-                rw[2 * (4 * lane + 3)] = (I1 >> 16) | (C1 & 0xFFFF0000u);
+                // the halves hold the same 8 windows (8m .. 8m+7) for different bins: add
+                // them, then half h writes windows 8m + 4h .. 8m + 4h + 3 as I | C << 16
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                    Iw[i] += __shfl_xor_sync(0xffffffffu, Iw[i], 16);
+                    Cw[i] += __shfl_xor_sync(0xffffffffu, Cw[i], 16);
+                }
+                const uint32_t i0 = hh ? Iw[2] : Iw[0], i1 = hh ? Iw[3] : Iw[1];
+                const uint32_t c0 = hh ? Cw[2] : Cw[0], c1 = hh ? Cw[3] : Cw[1];
+                uint32_t* rw = reinterpret_cast<uint32_t*>(red) + (y & 1) * (kWarps * kStrip) + warp * kStrip;
+                *reinterpret_cast<uint4*>(rw + 8 * mm + 4 * hh) =
+                    make_uint4((i0 & 0xFFFFu) | (c0 << 16), (i0 >> 16) | (c0 & 0xFFFF0000u), (i1 & 0xFFFFu) | (c1 << 16),
+                               (i1 >> 16) | (c1 & 0xFFFF0000u));
             } else {
                 rb[4 * lane + 0] = acc[0];
                 rb[4 * lane + 1] = acc[1];
