@@ -121,15 +121,24 @@ __global__ void prep_kernel(const double* __restrict__ tmpl, int bin0, int bins,
     }
 }
 
-// Window counts, phase 1: for bin row `vw` (vc of the bin at word 2*lane), the inclusive
-// prefix G of the 256 extended columns for the lane's 8 columns (u16 pairs): the halo
-// half (a0, a1) and the strip half (b0, b1); with STAGE they are also written to `g`
-// (the warp's staging row for this bin) for the general-kw partner reads.
+// vc rows are stored swizzled: word w of a bin row lives at w ^ ((w >> 3) & 4), so the
+// quarter-warp reads of 8 consecutive words per lane (two 16-B loads, 8 lanes per phase)
+// hit 8 distinct bank groups.  Pairs / quads stay contiguous under the swizzle.
+__device__ __forceinline__ int swz(int w) { return w ^ ((w >> 3) & 4); }
+
+__device__ __forceinline__ uint4 lds4(const uint32_t* row, int w) {
+    return *reinterpret_cast<const uint4*>(row + swz(w));
+}
+
+// Window counts (general path), phase 1: for bin row `vrow`, the inclusive prefix G of the
+// 256 extended columns for the lane's 8 columns (u16 pairs): the halo half (a0, a1) and
+// the strip half (b0, b1); with STAGE they are also written to `g` (the warp's staging
+// row for this bin) for the general-kw partner reads.
 template <bool STAGE>
-__device__ __forceinline__ void window_prefix(const uint32_t* vw, uint32_t* g, int lane, uint32_t& a0, uint32_t& a1,
+__device__ __forceinline__ void window_prefix(const uint32_t* vrow, uint32_t* g, int lane, uint32_t& a0, uint32_t& a1,
                                               uint32_t& b0, uint32_t& b1) {
-    const uint2 wa = *reinterpret_cast<const uint2*>(vw);
-    const uint2 wb = *reinterpret_cast<const uint2*>(vw + 64);
+    const uint2 wa = *reinterpret_cast<const uint2*>(vrow + swz(2 * lane));
+    const uint2 wb = *reinterpret_cast<const uint2*>(vrow + swz(64 + 2 * lane));
     a0 = wa.x * 0x10001u;
     a1 = wa.y * 0x10001u + __byte_perm(a0, 0, 0x3232);
     b0 = wb.x * 0x10001u;
@@ -150,55 +159,8 @@ __device__ __forceinline__ void window_prefix(const uint32_t* vw, uint32_t* g, i
     }
 }
 
-// Half-warp variant (integer path): half h of the warp handles one bin, lane m = lane & 15
-// owns the 8 halo columns 8m..8m+7 and the 8 strip columns 128+8m.. of the extended row,
-// as four u16-pair words each (a: halo, b: strip).  One 16-lane scan then serves one
-// bin per half, i.e. two bins per warp scan (4 shuffle steps instead of 2 x 5).
-__device__ __forceinline__ uint32_t scan_add16(uint32_t v, int o) {
-    uint32_t r;
-    asm("{\n\t.reg .pred p;\n\t.reg .u32 t;\n\t"
-        "shfl.sync.up.b32 t|p, %1, %2, 0x1000, 0xffffffff;\n\t"
-        "@p add.u32 %1, %1, t;\n\t"
-        "mov.u32 %0, %1;\n\t}"
-        : "=r"(r), "+r"(v)
-        : "r"(o));
-    return r;
-}
-
-template <bool STAGE>
-__device__ __forceinline__ void window_prefix16(const uint32_t* vrow, uint32_t* g, int m, uint32_t (&a)[4],
-                                                uint32_t (&b)[4]) {
-    const uint4 wa = *reinterpret_cast<const uint4*>(vrow + 4 * m);
-    const uint4 wb = *reinterpret_cast<const uint4*>(vrow + 64 + 4 * m);
-    a[0] = wa.x * 0x10001u;
-    a[1] = wa.y * 0x10001u + __byte_perm(a[0], 0, 0x3232);
-    a[2] = wa.z * 0x10001u + __byte_perm(a[1], 0, 0x3232);
-    a[3] = wa.w * 0x10001u + __byte_perm(a[2], 0, 0x3232);
-    b[0] = wb.x * 0x10001u;
-    b[1] = wb.y * 0x10001u + __byte_perm(b[0], 0, 0x3232);
-    b[2] = wb.z * 0x10001u + __byte_perm(b[1], 0, 0x3232);
-    b[3] = wb.w * 0x10001u + __byte_perm(b[2], 0, 0x3232);
-    const uint32_t tot = __byte_perm(a[3], b[3], 0x7632);  // {sum a, sum b}
-    uint32_t inc = tot;
-#pragma unroll
-    for (int o = 1; o < 16; o <<= 1) inc = scan_add16(inc, o);
-    const uint32_t ex = inc - tot;
-    const uint32_t T1 = __byte_perm(__shfl_sync(0xffffffffu, inc, 15, 16), 0, 0x1010);  // halo total
-    const uint32_t ba = __byte_perm(ex, 0, 0x1010);
-    const uint32_t bb = __byte_perm(ex, 0, 0x3232) + T1;
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-        a[i] += ba;
-        b[i] += bb;
-    }
-    if (STAGE) {
-        *reinterpret_cast<uint4*>(g + 4 * m) = make_uint4(a[0], a[1], a[2], a[3]);
-        *reinterpret_cast<uint4*>(g + 64 + 4 * m) = make_uint4(b[0], b[1], b[2], b[3]);
-    }
-}
-
-// Window counts, phase 2 (after a __syncwarp): c = G(e) - G(e - kw) for the lane's four
-// windows, as two u16 pairs {j=0, j=1}, {j=2, j=3}.
+// Window counts (general path), phase 2 (after a __syncwarp): c = G(e) - G(e - kw) for the
+// lane's four windows, as two u16 pairs {j=0, j=1}, {j=2, j=3}.
 __device__ __forceinline__ void window_diff(const uint32_t* g, int pw, int psh, uint32_t b0, uint32_t b1,
                                             uint32_t& c0, uint32_t& c1) {
     const uint32_t q0 = g[pw], q1 = g[pw + 1], q2 = g[pw + 2];
@@ -206,17 +168,109 @@ __device__ __forceinline__ void window_diff(const uint32_t* g, int pw, int psh, 
     c1 = b1 - __funnelshift_r(q1, q2, psh);
 }
 
-template <bool STORE, bool FAST, int KWM>
+// Inclusive scan step over 8-lane segments (shuffle in-range predicate, no select).
+__device__ __forceinline__ uint32_t scan_add8(uint32_t v, int o) {
+    uint32_t r;
+    asm("{\n\t.reg .pred p;\n\t.reg .u32 t;\n\t"
+        "shfl.sync.up.b32 t|p, %1, %2, 0x1800, 0xffffffff;\n\t"
+        "@p add.u32 %1, %1, t;\n\t"
+        "mov.u32 %0, %1;\n\t}"
+        : "=r"(r), "+r"(v)
+        : "r"(o));
+    return r;
+}
+
+// Window counts (integer path), quarter-warp layout: lane m (0..7) of a quarter owns the 16
+// windows ending at strip columns 16m .. 16m+15 (extended columns e = 128 + 16m + i) of one
+// bin.  With vc the bin's running column counts over the last kh rows,
+//     c(e) = c(127) + sum_{x=128..e} delta(x),   delta(x) = vc(x) - vc(x - kw),
+// and the anchor c(127) = sum of vc over [128 - kw, 128), i.e. of the lane's vc(e - kw)
+// values with 16m + i < kw.  delta is biased by +255 (>= kh) so every in-lane prefix and
+// scan partial is a non-negative u16; the bias is removed linearly at the end, where the
+// true counts 0 <= c <= kw*kh < 2^16 make the packed pairs exact.  One 8-lane scan of
+// {anchor partial, lane delta total} per bin: 3 shuffle steps + 1 broadcast.
+// Result: c[j] = {c(16m + 2j), c(16m + 2j + 1)} packed u16 pairs.
+template <int KWM>
+__device__ __forceinline__ void window_counts_q(const uint32_t* vrow, int m, int aw0, int apsh,
+                                                const uint32_t* amask, uint32_t (&c)[8]) {
+    uint32_t b[8], a[8];
+    {
+        const uint4 x = lds4(vrow, 64 + 8 * m), y = lds4(vrow, 68 + 8 * m);
+        b[0] = x.x, b[1] = x.y, b[2] = x.z, b[3] = x.w, b[4] = y.x, b[5] = y.y, b[6] = y.z, b[7] = y.w;
+    }
+    if (KWM == 64 || KWM == 128) {
+        const int wa = KWM == 64 ? 32 + 8 * m : 8 * m;
+        const uint4 x = lds4(vrow, wa), y = lds4(vrow, wa + 4);
+        a[0] = x.x, a[1] = x.y, a[2] = x.z, a[3] = x.w, a[4] = y.x, a[5] = y.y, a[6] = y.z, a[7] = y.w;
+    } else {
+        uint32_t r[9];
+#pragma unroll
+        for (int i = 0; i < 9; ++i) r[i] = vrow[swz(aw0 + i)];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) a[j] = __funnelshift_r(r[j], r[j + 1], apsh);
+    }
+    uint32_t w[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+        const uint32_t d = b[j] - a[j] + 0x00FF00FFu;  // {delta + 255} pair (linear, exact after the bias)
+        w[j] = j ? d * 0x10001u + __byte_perm(w[j - 1], 0, 0x3232) : d * 0x10001u;
+    }
+    uint32_t x;  // anchor partial as a u16 pair sum
+    if (KWM == 64 || KWM == 128) {
+        x = (a[0] + a[1]) + (a[2] + a[3]) + (a[4] + a[5]) + (a[6] + a[7]);
+        if (KWM == 64) x = m < 4 ? x : 0u;
+    } else {
+        const uint4 m0 = *reinterpret_cast<const uint4*>(amask + 8 * m);
+        const uint4 m1 = *reinterpret_cast<const uint4*>(amask + 8 * m + 4);
+        x = ((a[0] & m0.x) + (a[1] & m0.y)) + ((a[2] & m0.z) + (a[3] & m0.w)) + ((a[4] & m1.x) + (a[5] & m1.y)) +
+            ((a[6] & m1.z) + (a[7] & m1.w));
+    }
+    const uint32_t pack = ((x + (x >> 16)) & 0xFFFFu) | (w[7] & 0xFFFF0000u);  // {anchor partial, delta total}
+    uint32_t inc = pack;
+#pragma unroll
+    for (int o = 1; o < 8; o <<= 1) inc = scan_add8(inc, o);
+    const uint32_t tot = __shfl_sync(0xffffffffu, inc, 7, 8);
+    const uint32_t s = (tot & 0xFFFFu) + ((inc - pack) >> 16) - 4080u * static_cast<uint32_t>(m);
+    const uint32_t S2 = s * 0x10001u;
+#pragma unroll
+    for (int j = 0; j < 8; ++j)
+        c[j] = w[j] + S2 - ((static_cast<uint32_t>(2 * j + 1) * 255u) | (static_cast<uint32_t>(2 * j + 2) * 255u << 16));
+}
+
+// Cross-quarter reduce-scatter of 8 packed words: afterwards lane (q, m) holds in v[0..1]
+// the warp's sums of words 4 (q >> 1) + 2 (q & 1) + {0, 1}.
+__device__ __forceinline__ void quarter_reduce(uint32_t (&v)[8], int q) {
+    const bool hi2 = q & 2, hi1 = q & 1;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+        const uint32_t send = hi2 ? v[j] : v[j + 4];
+        const uint32_t keep = hi2 ? v[j + 4] : v[j];
+        v[j] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
+    }
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+        const uint32_t send = hi1 ? v[j] : v[j + 2];
+        const uint32_t keep = hi1 ? v[j + 2] : v[j];
+        v[j] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
+    }
+}
+
+// ALLB (integer path only): the CTA's bin group is the whole histogram, so the window
+// total over the group's bins is kw * kh and need not be accumulated.
+template <bool STORE, bool FAST, int KWM, bool ALLB>
 __global__ void __launch_bounds__(256, 2) sweep_match_kernel(QuantParams q, PixelMode pm, spct_ih out, int Lb, int Wp,
                                                              int band_rows, const uint32_t* __restrict__ Lt,
                                                              const uint32_t* __restrict__ Hb, FusedParams f) {
     extern __shared__ uint4 smem_raw[];
-    uint32_t* vc = reinterpret_cast<uint32_t*>(smem_raw);                 // [128 bins][128 words]
-    uint32_t* gbuf = vc + kGroupBins * kVcWords;                            // [8 warps][4][128 words]
+    uint32_t* vc = reinterpret_cast<uint32_t*>(smem_raw);                 // [128 bins][128 words], swizzled
+    uint32_t* gbuf = vc + kGroupBins * kVcWords;                            // [8 warps][4][128 words] (general path)
     double* red = reinterpret_cast<double*>(gbuf + kWarps * 4 * kVcWords);  // [2 rows][8 warps][128]
     uint32_t* srep_s = reinterpret_cast<uint32_t*>(red + 2 * kWarps * kStrip);  // [128]
     uint32_t* lrow = srep_s + kGroupBins;                                   // [2 rows][128] row carries
     uint16_t* rowbins = reinterpret_cast<uint16_t*>(lrow + 2 * kGroupBins);  // [2 rows][128] strip bins
+    uint32_t* amask = reinterpret_cast<uint32_t*>(rowbins + 2 * kStrip);    // [8 lanes][8 words] anchor masks
+    // integer path: per row parity, warp and window pair, the packed {I, I} sums (and C after them)
+    uint32_t* red32 = reinterpret_cast<uint32_t*>(red);
 
     // Both variants are launched; the one that does not match the template prep exits.
     if ((__ldg(f.prep) != 0) != FAST) return;
@@ -239,27 +293,34 @@ __global__ void __launch_bounds__(256, 2) sweep_match_kernel(QuantParams q, Pixe
 
     for (int i = tid; i < kGroupBins * kVcWords; i += blockDim.x) vc[i] = 0;
     if (tid < kGroupBins) srep_s[tid] = (FAST && tid < nb_cta) ? __ldg(f.prep + 1 + g0 + tid) : 0u;
+    if (FAST && KWM == 0 && tid < 64) {
+        // anchor masks: u16 i of lane m's word j is valid iff 16m + 2j + i < kw
+        const int n = f.kw - 16 * (tid >> 3) - 2 * (tid & 7);
+        amask[tid] = n >= 2 ? 0xFFFFFFFFu : (n == 1 ? 0xFFFFu : 0u);
+    }
 
     uint32_t V[4][kB];
     if (STORE && warp_live) vpart_init<kB>(V, Hb, band, Lb, kl0, Wp, xl);
     uint32_t* base_ptr = STORE ? out.data + static_cast<int64_t>(kl0) * out.plane_pitch + xl : nullptr;
+    const uint32_t ppb = static_cast<uint32_t>(out.plane_pitch * 4);
     const bool lane_live = xl < out.row_pitch;
     const uint32_t store_mask = lane_live ? (k_live >= 32 ? 0xFFFFFFFFu : (1u << max(k_live, 0)) - 1u) : 0u;
     const long long S = FAST ? f.S_group[g0 / kGroupBins] : 0;
-    // G(e - kw): first extended cell of this lane's four windows, as a word and a bit shift
+    // general path: G(e - kw) as a word and a bit shift
     const int idx = kStrip + 4 * lane - f.kw;
     const int pw = idx >> 1, psh = (idx & 1) * 16;
     uint32_t* gb = gbuf + warp * 4 * kVcWords;
-    const uint32_t* vbase = vc + warp * kB * kVcWords + 2 * lane;
-    // integer path (half-warp layout): half hh, lane mm owns windows 8mm .. 8mm+7
-    const int hh = lane >> 4, mm = lane & 15;
     const uint32_t* vwarp = vc + warp * kB * kVcWords;
-    const int idx16 = kStrip + 8 * mm - f.kw;
-    const int pw16 = idx16 >> 1, psh16 = (idx16 & 1) * 16;
+    // integer path: quarter qq of the warp takes bin 4g + qq; lane mq owns windows 16mq ..
+    const int qq = lane >> 3, mq = lane & 7;
+    const int ca0 = kStrip + 16 * mq - f.kw;  // extended column of vc(e - kw) for the lane's first window
+    const int aw0 = ca0 >> 1, apsh = (ca0 & 1) * 16;
 
     // staging thread: extended column tid; prefetch one row ahead
     const int xt = xs - kStrip + tid;
     const bool xt_live = xt >= 0 && xt < W;
+    const int vcw = swz(tid >> 1);           // the staging column's (swizzled) vc word
+    const uint32_t vinc = 1u << (16 * (tid & 1));
     const uint32_t* lt_cta = (STORE && Lt && strip > 0 && tid < kGroupBins && g0 + tid < Lb)
                                  ? Lt + static_cast<int64_t>(strip) * H * Lb + g0 + tid
                                  : nullptr;
@@ -274,8 +335,7 @@ __global__ void __launch_bounds__(256, 2) sweep_match_kernel(QuantParams q, Pixe
     // DRAM latency on every row).
     if (xt_live) {
         const int nb_lo = out.bin0 + g0;
-        const uint32_t inc = 1u << (16 * (tid & 1));
-        uint32_t* vcol = vc + (tid >> 1);
+        uint32_t* vcol = vc + vcw;
         for (int y = ystart; y < y0; y += 8) {
             uint64_t r[8];
 #pragma unroll
@@ -284,7 +344,7 @@ __global__ void __launch_bounds__(256, 2) sweep_match_kernel(QuantParams q, Pixe
             for (int i = 0; i < 8; ++i) {
                 const int bn = bin_of_raw(r[i], q) - nb_lo;
                 if (y + i < y0 && static_cast<unsigned>(bn) < static_cast<unsigned>(nb_cta))
-                    atomicAdd(vcol + bn * kVcWords, inc);
+                    atomicAdd(vcol + bn * kVcWords, vinc);
             }
         }
     }
@@ -295,19 +355,23 @@ __global__ void __launch_bounds__(256, 2) sweep_match_kernel(QuantParams q, Pixe
     auto combine = [&](int yy) {
         if (tid < kStrip) {
             const int t = tid;
-            const double* rb = red + (yy & 1) * (kWarps * kStrip);
             double term = 0.0;
             if (FAST) {
-                // I | C << 16 per warp; both sums stay below 2^16 (at most kw * kh <= 32640)
-                const uint32_t* rw = reinterpret_cast<const uint32_t*>(red) + (yy & 1) * (kWarps * kStrip) + t;
-                uint32_t x = 0;
+                // packed window pairs; every sum stays below 2^16 (at most kw * kh)
+                const uint32_t* rw = red32 + (yy & 1) * (kWarps * 64) + (t >> 1);
+                uint32_t xi = 0, xc = 0;
 #pragma unroll
                 for (int w = 0; w < kWarps; ++w)
-                    if (w < nwarps_live) x += rw[w * kStrip];
-                const long long I = x & 0xFFFFu, C = x >> 16;
+                    if (w < nwarps_live) {
+                        xi += rw[w * 64];
+                        if (!ALLB) xc += rw[2 * kWarps * 64 + w * 64];
+                    }
+                const long long I = (xi >> (16 * (t & 1))) & 0xFFFFu;
+                const long long C = ALLB ? static_cast<long long>(f.kw) * f.kh : (xc >> (16 * (t & 1))) & 0xFFFFu;
                 term = f.metric == SPCT_METRIC_INTERSECTION ? static_cast<double>(I) * f.invT
                                                             : static_cast<double>(C + S - 2 * I) * f.invT;
             } else {
+                const double* rb = red + (yy & 1) * (kWarps * kStrip);
 #pragma unroll
                 for (int w = 0; w < kWarps; ++w)
                     if (w < nwarps_live) term = __dadd_rn(term, rb[w * kStrip + t]);
@@ -343,13 +407,11 @@ __global__ void __launch_bounds__(256, 2) sweep_match_kernel(QuantParams q, Pixe
             const int pn = xt_live ? bin_of_raw(rn, q) : 0xFFFF;
             const int po = (xt_live && have_o) ? bin_of_raw(ro, q) : -1;
             if (xt_live) {
-                const uint32_t inc = 1u << (16 * (tid & 1));
                 const int bn = pn - out.bin0 - g0;
-                if (static_cast<unsigned>(bn) < static_cast<unsigned>(nb_cta))
-                    atomicAdd(&vc[bn * kVcWords + (tid >> 1)], inc);
+                if (static_cast<unsigned>(bn) < static_cast<unsigned>(nb_cta)) atomicAdd(&vc[bn * kVcWords + vcw], vinc);
                 const int bo = po - out.bin0 - g0;
                 if (po >= 0 && static_cast<unsigned>(bo) < static_cast<unsigned>(nb_cta))
-                    atomicSub(&vc[bo * kVcWords + (tid >> 1)], inc);
+                    atomicSub(&vc[bo * kVcWords + vcw], vinc);
             }
             if (tid >= kStrip) rowbins[(y & 1) * kStrip + tid - kStrip] = static_cast<uint16_t>(pn);
             else lrow[(y & 1) * kGroupBins + tid] = lpre;
@@ -367,9 +429,10 @@ __global__ void __launch_bounds__(256, 2) sweep_match_kernel(QuantParams q, Pixe
         const bool match_row = y >= f.kh - 1;
         if (!warp_live || (!STORE && !match_row)) continue;
 
-        uint32_t bins4 = 0;
+        uint32_t t4[4] = {0, 0, 0, 0};
         if (STORE) {
             const uint2 rb2 = *reinterpret_cast<const uint2*>(rowbins + (y & 1) * kStrip + 4 * lane);
+            uint32_t bins4 = 0;
             if (pm.byte_mode) {
                 bins4 = __byte_perm(rb2.x, rb2.y, 0x6420);
             } else {
@@ -380,51 +443,30 @@ __global__ void __launch_bounds__(256, 2) sweep_match_kernel(QuantParams q, Pixe
                     bins4 |= (r < static_cast<uint32_t>(kB) ? r : 0xFFu) << (8 * j);
                 }
             }
+            onehot_shifts(bins4 ^ kpat0, t4);
         }
         const uint4* lr = reinterpret_cast<const uint4*>(lrow + (y & 1) * kGroupBins + warp * kB);
         uint32_t* prow = STORE ? base_ptr + static_cast<int64_t>(y) * out.row_pitch : nullptr;
 
-        uint32_t I0 = 0, I1 = 0, C0 = 0, C1 = 0;
-        uint32_t Iw[4] = {0, 0, 0, 0}, Cw[4] = {0, 0, 0, 0};
+        uint32_t Iw[8] = {0, 0, 0, 0, 0, 0, 0, 0}, Cw[8] = {0, 0, 0, 0, 0, 0, 0, 0};
         double acc[4] = {0.0, 0.0, 0.0, 0.0};
 #pragma unroll
         for (int g = 0; g < kB / 4; ++g) {
-            if (STORE)
-                vpart_group<kB>(V, g, bins4 ^ kpat0, lr[g], prow + static_cast<int64_t>(4 * g) * out.plane_pitch,
-                                out.plane_pitch, store_mask);
+            if (STORE) vpart_group_q<kB>(V, g, t4, lr[g], prow, ppb, store_mask);
             if (FAST && match_row) {
-                // half-warp layout: bins 4g + 2p + hh, p = 0, 1
-                uint32_t a[2][4], b[2][4];
+                uint32_t c[8];
+                window_counts_q<KWM>(vwarp + (4 * g + qq) * kVcWords, mq, aw0, apsh, amask, c);
+                const uint32_t sk = srep_s[warp * kB + 4 * g + qq];
 #pragma unroll
-                for (int p = 0; p < 2; ++p)
-                    window_prefix16<KWM == 0>(vwarp + (4 * g + 2 * p + hh) * kVcWords, gb + (2 * p + hh) * kVcWords, mm,
-                                              a[p], b[p]);
-                if (KWM == 0) __syncwarp();
-#pragma unroll
-                for (int p = 0; p < 2; ++p) {
-                    const uint32_t sk = srep_s[warp * kB + 4 * g + 2 * p + hh];
-#pragma unroll
-                    for (int i = 0; i < 4; ++i) {
-                        uint32_t c;
-                        if (KWM == 64) {
-                            // G(e - 64): partner lane m ^ 8's halo (m < 8) or strip (m >= 8) words
-                            c = b[p][i] - __shfl_xor_sync(0xffffffffu, mm >= 8 ? a[p][i] : b[p][i], 8);
-                        } else if (KWM == 128) {
-                            c = b[p][i] - a[p][i];
-                        } else {
-                            const uint32_t* gg = gb + (2 * p + hh) * kVcWords + pw16 + i;
-                            c = b[p][i] - __funnelshift_r(gg[0], gg[1], psh16);
-                        }
-                        Iw[i] += min_u16x2(c, sk);
-                        Cw[i] += c;
-                    }
+                for (int j = 0; j < 8; ++j) {
+                    Iw[j] += min_u16x2(c[j], sk);
+                    if (!ALLB) Cw[j] += c[j];
                 }
-                if (KWM == 0) __syncwarp();
             } else if (match_row) {
                 uint32_t aw[4][2], bw[4][2];
 #pragma unroll
                 for (int i = 0; i < 4; ++i)
-                    window_prefix<KWM == 0>(vbase + (4 * g + i) * kVcWords, gb + i * kVcWords, lane, aw[i][0], aw[i][1],
+                    window_prefix<KWM == 0>(vwarp + (4 * g + i) * kVcWords, gb + i * kVcWords, lane, aw[i][0], aw[i][1],
                                             bw[i][0], bw[i][1]);
                 if (KWM == 0) __syncwarp();
 #pragma unroll
@@ -443,13 +485,7 @@ __global__ void __launch_bounds__(256, 2) sweep_match_kernel(QuantParams q, Pixe
                     } else {
                         window_diff(gb + i * kVcWords, pw, psh, bw[i][0], bw[i][1], c0, c1);
                     }
-                    if (FAST) {
-                        const uint32_t sk = srep_s[warp * kB + k];
-                        I0 += min_u16x2(c0, sk);
-                        I1 += min_u16x2(c1, sk);
-                        C0 += c0;
-                        C1 += c1;
-                    } else if (k < k_live) {
+                    if (k < k_live) {
                         const double t = __ldg(f.tmpl + k0 + k);
                         acc[0] = __dadd_rn(acc[0], general_term(c0 & 0xFFFFu, t, f));
                         acc[1] = __dadd_rn(acc[1], general_term(c0 >> 16, t, f));
@@ -461,22 +497,18 @@ __global__ void __launch_bounds__(256, 2) sweep_match_kernel(QuantParams q, Pixe
             }
         }
         if (match_row) {
-            double* rb = red + (y & 1) * (kWarps * kStrip) + warp * kStrip;
             if (FAST) {
-                // the halves hold the same 8 windows (8m .. 8m+7) for different bins: add
-                // them, then half h writes windows 8m + 4h .. 8m + 4h + 3 as I | C << 16
-#pragma unroll
-                for (int i = 0; i < 4; ++i) {
-                    Iw[i] += __shfl_xor_sync(0xffffffffu, Iw[i], 16);
-                    Cw[i] += __shfl_xor_sync(0xffffffffu, Cw[i], 16);
+                // the quarters hold the same 16 windows per lane for different bins
+                quarter_reduce(Iw, qq);
+                const int jb = 4 * (qq >> 1) + 2 * (qq & 1);
+                uint32_t* rw = red32 + (y & 1) * (kWarps * 64) + warp * 64 + 8 * mq + jb;
+                *reinterpret_cast<uint2*>(rw) = make_uint2(Iw[0], Iw[1]);
+                if (!ALLB) {
+                    quarter_reduce(Cw, qq);
+                    *reinterpret_cast<uint2*>(rw + 2 * kWarps * 64) = make_uint2(Cw[0], Cw[1]);
                 }
-                const uint32_t i0 = hh ? Iw[2] : Iw[0], i1 = hh ? Iw[3] : Iw[1];
-                const uint32_t c0 = hh ? Cw[2] : Cw[0], c1 = hh ? Cw[3] : Cw[1];
-                uint32_t* rw = reinterpret_cast<uint32_t*>(red) + (y & 1) * (kWarps * kStrip) + warp * kStrip;
-                *reinterpret_cast<uint4*>(rw + 8 * mm + 4 * hh) =
-                    make_uint4((i0 & 0xFFFFu) | (c0 << 16), (i0 >> 16) | (c0 & 0xFFFF0000u), (i1 & 0xFFFFu) | (c1 << 16),
-                               (i1 >> 16) | (c1 & 0xFFFF0000u));
             } else {
+                double* rb = red + (y & 1) * (kWarps * kStrip) + warp * kStrip;
                 rb[4 * lane + 0] = acc[0];
                 rb[4 * lane + 1] = acc[1];
                 rb[4 * lane + 2] = acc[2];
@@ -489,7 +521,8 @@ __global__ void __launch_bounds__(256, 2) sweep_match_kernel(QuantParams q, Pixe
 }
 
 constexpr size_t kSmemBytes = (size_t(kGroupBins) * kVcWords + size_t(kWarps) * 4 * kVcWords) * 4 +
-                              size_t(2) * kWarps * kStrip * 8 + size_t(kGroupBins) * 4 * 3 + size_t(2) * kStrip * 2;
+                              size_t(2) * kWarps * kStrip * 8 + size_t(kGroupBins) * 4 * 3 + size_t(2) * kStrip * 2 +
+                              64 * 4;
 
 }  // namespace spct_fused
 
@@ -504,9 +537,9 @@ int fused_ctas_per_sm() {
     static int n = 0;
     if (n) return n;
     int v = 0;
-    cudaFuncSetAttribute(spct_fused::sweep_match_kernel<true, true, 64>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaFuncSetAttribute(spct_fused::sweep_match_kernel<true, true, 64, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)spct_fused::kSmemBytes);
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&v, spct_fused::sweep_match_kernel<true, true, 64>, 256,
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&v, spct_fused::sweep_match_kernel<true, true, 64, true>, 256,
                                                       spct_fused::kSmemBytes) != cudaSuccess || v <= 0) {
         cudaGetLastError();
         v = 2;
@@ -517,26 +550,33 @@ int fused_ctas_per_sm() {
 
 namespace spct_fused {
 
-template <int KWM>
+template <int KWM, bool ALLB>
 void launch_variants(dim3 grid, cudaStream_t s, const QuantParams& q, const PixelMode& pm, const spct_ih& out,
                      const BuildPlan& bp, const uint32_t* Lt, const uint32_t* Hb, const FusedParams& f) {
     static bool attr_set = false;
     if (!attr_set) {
-        cudaFuncSetAttribute(sweep_match_kernel<true, true, KWM>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBytes);
-        cudaFuncSetAttribute(sweep_match_kernel<true, false, KWM>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBytes);
-        cudaFuncSetAttribute(sweep_match_kernel<false, true, KWM>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBytes);
-        cudaFuncSetAttribute(sweep_match_kernel<false, false, KWM>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBytes);
+        cudaFuncSetAttribute(sweep_match_kernel<true, true, KWM, ALLB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBytes);
+        cudaFuncSetAttribute(sweep_match_kernel<true, false, KWM, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBytes);
+        cudaFuncSetAttribute(sweep_match_kernel<false, true, KWM, ALLB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBytes);
+        cudaFuncSetAttribute(sweep_match_kernel<false, false, KWM, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBytes);
         attr_set = true;
     }
     // integer (template-crop) variant and FP64 variant: the one not selected by the
     // device-side template prep exits on entry
     if (out.data) {
-        sweep_match_kernel<true, true, KWM><<<grid, 256, kSmemBytes, s>>>(q, pm, out, bp.Lb, bp.Wp, bp.band_rows, Lt, Hb, f);
-        sweep_match_kernel<true, false, KWM><<<grid, 256, kSmemBytes, s>>>(q, pm, out, bp.Lb, bp.Wp, bp.band_rows, Lt, Hb, f);
+        sweep_match_kernel<true, true, KWM, ALLB><<<grid, 256, kSmemBytes, s>>>(q, pm, out, bp.Lb, bp.Wp, bp.band_rows, Lt, Hb, f);
+        sweep_match_kernel<true, false, KWM, false><<<grid, 256, kSmemBytes, s>>>(q, pm, out, bp.Lb, bp.Wp, bp.band_rows, Lt, Hb, f);
     } else {
-        sweep_match_kernel<false, true, KWM><<<grid, 256, kSmemBytes, s>>>(q, pm, out, bp.Lb, bp.Wp, bp.band_rows, nullptr, nullptr, f);
-        sweep_match_kernel<false, false, KWM><<<grid, 256, kSmemBytes, s>>>(q, pm, out, bp.Lb, bp.Wp, bp.band_rows, nullptr, nullptr, f);
+        sweep_match_kernel<false, true, KWM, ALLB><<<grid, 256, kSmemBytes, s>>>(q, pm, out, bp.Lb, bp.Wp, bp.band_rows, nullptr, nullptr, f);
+        sweep_match_kernel<false, false, KWM, false><<<grid, 256, kSmemBytes, s>>>(q, pm, out, bp.Lb, bp.Wp, bp.band_rows, nullptr, nullptr, f);
     }
+}
+
+template <int KWM>
+void launch_kw(bool allb, dim3 grid, cudaStream_t s, const QuantParams& q, const PixelMode& pm, const spct_ih& out,
+               const BuildPlan& bp, const uint32_t* Lt, const uint32_t* Hb, const FusedParams& f) {
+    if (allb) launch_variants<KWM, true>(grid, s, q, pm, out, bp, Lt, Hb, f);
+    else launch_variants<KWM, false>(grid, s, q, pm, out, bp, Lt, Hb, f);
 }
 
 // Shared body of spct_cu_ih_build_match (partial != null) and spct_cu_ih_build_match_map (map != null).
@@ -559,7 +599,8 @@ spct_status build_match(const spct_source* src, const spct_ih* out, const double
         return contract("ih_build_match_map: the slab must hold every bin (use the partial form for slabs)");
     cudaStream_t s = as_stream(stream);
     const int64_t T = static_cast<int64_t>(kw) * kh;
-    const bool fusable = kw <= 128 && kh <= 255 && T <= 65535;
+    // 16-bit running-histogram cells, and plane offsets of a warp's 16 planes in 32 bits
+    const bool fusable = kw <= 128 && kh <= 255 && T <= 65535 && (!out->data || out->plane_pitch * 4 * 15 < (int64_t(1) << 32));
     const int ngroups = static_cast<int>(ceil_div(out->bins, kGroupBins));
     if (fusable && map && ngroups > 1) {
         // more than one 128-bin group: accumulate the groups' partials, then finalise
@@ -624,9 +665,11 @@ spct_status build_match(const spct_source* src, const spct_ih* out, const double
         f.accumulate = g > 0;
         dim3 grid(bp.nstrips, bp.nbands, 1);
         const int prof = prof_begin(out->data ? "ih_sweep_match" : "sweep_match_nostore", s);
-        if (kw == 64) launch_variants<64>(grid, s, q, pm, *out, bp, Lt, Hb, f);
-        else if (kw == 128) launch_variants<128>(grid, s, q, pm, *out, bp, Lt, Hb, f);
-        else launch_variants<0>(grid, s, q, pm, *out, bp, Lt, Hb, f);
+        // the group is the whole histogram: window totals over its bins are kw * kh
+        const bool allb = out->bin0 == 0 && out->bins == out->nbins_total && ngroups == 1;
+        if (kw == 64) launch_kw<64>(allb, grid, s, q, pm, *out, bp, Lt, Hb, f);
+        else if (kw == 128) launch_kw<128>(allb, grid, s, q, pm, *out, bp, Lt, Hb, f);
+        else launch_kw<0>(allb, grid, s, q, pm, *out, bp, Lt, Hb, f);
         prof_end(prof, s);
         note_launch();
         if (auto st = launch_status("sweep_match_kernel")) return st;

@@ -178,40 +178,54 @@ __device__ __forceinline__ void vpart_group(uint32_t (&V)[4][B], int g, uint32_t
 
 namespace spct_dev {
 
-// N independent inclusive warp scans, interleaved step by step so the shuffle latencies
-// overlap (the compiler does not interleave separate scan chains on its own).
-template <int N>
-__device__ __forceinline__ void warp_incl_scan_n(uint32_t (&v)[N]) {
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-#pragma unroll
-        for (int i = 0; i < N; ++i) v[i] = scan_add(v[i], o);
-    }
+// Shift with PTX semantics: amounts >= 32 (including "negative" ones as unsigned) give 0.
+__device__ __forceinline__ uint32_t shl_clamp(uint32_t v, uint32_t n) {
+    uint32_t r;
+    asm("shl.b32 %0, %1, %2;" : "=r"(r) : "r"(v), "r"(n));
+    return r;
 }
 
-// vpart_group split in two halves around a shared scan: the one-hot prefix words of
-// group g (returns the packed per-lane counts to scan) ...
-__device__ __forceinline__ uint32_t vpart_counts(int g, uint32_t dbins, uint32_t (&P)[4]) {
-#pragma unroll
-    for (int i = 0; i < 4; ++i) P[i] = match_prefix(dbins, 0x01010101u * static_cast<uint32_t>(4 * g + i));
-    return __byte_perm(__byte_perm(P[0], P[1], 0x0073), __byte_perm(P[2], P[3], 0x0073), 0x5410);
+// Address of plane k of a row: prow + k * ppb bytes in one IMAD.WIDE (k * ppb < 2^32).
+__device__ __forceinline__ uint32_t* plane_addr(uint32_t* prow, uint32_t k, uint32_t ppb) {
+    uint64_t a;
+    asm("mad.wide.u32 %0, %1, %2, %3;" : "=l"(a) : "r"(k), "r"(ppb), "l"(reinterpret_cast<uint64_t>(prow)));
+    return reinterpret_cast<uint32_t*>(a);
 }
 
-// ... and the register update + stores once the scan result (`excl`) is known.
+// 8 x (relative bin) of the lane's four columns, from dbins = bins4 ^ kpat0; a column off
+// the warp's slab yields >= 128, so no group's one-hot shift lands inside a word.
+__device__ __forceinline__ void onehot_shifts(uint32_t dbins, uint32_t (&t)[4]) {
+    t[0] = (dbins & 0xFFu) << 3;
+    t[1] = (dbins >> 5) & 0x7F8u;
+    t[2] = (dbins >> 13) & 0x7F8u;
+    t[3] = (dbins >> 21) & 0x7F8u;
+}
+
+// One group of four planes (4g .. 4g+3) of the row update, bin-major: Q[j] holds, in byte
+// i, the count of bin 4g+i among the lane's columns <= j (the one-hot of column j is
+// 1 << (8 r_j - 32 g)).  Q[3] is then already the packed per-lane total of the four bins
+// that the cross-lane scan needs.  `prow` points at plane 0 of the warp in this row;
+// plane k is prow + k * ppb bytes.
 template <int B>
-__device__ __forceinline__ void vpart_apply(uint32_t (&V)[4][B], int g, const uint32_t (&P)[4], uint32_t excl, uint4 L,
-                                            uint32_t* p, int64_t plane_pitch, uint32_t store_mask) {
+__device__ __forceinline__ void vpart_group_q(uint32_t (&V)[4][B], int g, const uint32_t (&t)[4], uint4 L,
+                                              uint32_t* prow, uint32_t ppb, uint32_t store_mask) {
+    uint32_t Q[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+        const uint32_t m = shl_clamp(1u, t[j] - 32u * g);
+        Q[j] = j ? Q[j - 1] + m : m;
+    }
+    const uint32_t excl = warp_incl_scan(Q[3]) - Q[3];
     const uint32_t Lk[4] = {L.x, L.y, L.z, L.w};
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
         const int k = 4 * g + i;
         const uint32_t base = Lk[i] + __byte_perm(excl, 0, 0x4440 + i);
-        V[0][k] += base + __byte_perm(P[i], 0, 0x4440);
-        V[1][k] += base + __byte_perm(P[i], 0, 0x4441);
-        V[2][k] += base + __byte_perm(P[i], 0, 0x4442);
-        V[3][k] += base + (P[i] >> 24);
-        st_cs_v4_pred((store_mask >> k) & 1u, p, V[0][k], V[1][k], V[2][k], V[3][k]);
-        p += plane_pitch;
+        V[0][k] += base + __byte_perm(Q[0], 0, 0x4440 + i);
+        V[1][k] += base + __byte_perm(Q[1], 0, 0x4440 + i);
+        V[2][k] += base + __byte_perm(Q[2], 0, 0x4440 + i);
+        V[3][k] += base + __byte_perm(Q[3], 0, 0x4440 + i);
+        st_cs_v4_pred((store_mask >> k) & 1u, plane_addr(prow, k, ppb), V[0][k], V[1][k], V[2][k], V[3][k]);
     }
 }
 
