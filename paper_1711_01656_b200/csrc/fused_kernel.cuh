@@ -1,0 +1,573 @@
+// Fused integral histogram + sliding-window matcher (one pass over the frame).
+//
+// Replaces build_integral_histogram followed by hist_distance_map (reference
+// integral.cpp:548-551, likelihood.cpp:193-225) without re-reading the tensor: the
+// window counts come from a vertical running histogram kept in shared memory.
+//
+// CTA = (128-column strip, band of rows, group of <= 128 bins); 8 warps x 16 bins.
+//   * V part (optional, `STORE`): the build sweep of sweep_common.cuh writes the
+//     integral-histogram rows of the strip (same bits as spct_cu_ih_build).
+//   * vc: for each of the CTA's bins and each of 256 "extended" columns
+//     [x0-128, x0+128) the count of that bin in the column over the last kh rows
+//     (u16 cells, two per 32-bit word, 64 KB).  Every row, thread t adds the entering
+//     pixel of column t and removes the pixel that left the window: two shared
+//     atomics per column, independent of the bin count.
+//   * G: per bin, the inclusive prefix of vc along the 256 columns (u16 pairs, lane l
+//     owns columns 4l..4l+3 of each half; in-lane IMAD prefix + one 16-bit-packed warp
+//     scan).  The count of the kw x kh window whose bottom-right pixel is (e, y) is
+//     G(e) - G(e - kw), read back through a per-warp staging row.
+//   * distance: Minkowski p = 1 / intersection with an integral template
+//     (s_k = T t_k in Z, the template-crop case) is exact integer arithmetic:
+//     sum_k |c_k - s_k| = C + S - 2 sum_k min(c_k, s_k), with min.u16x2 on packed
+//     pairs.  Every other metric / p evaluates likelihood.cpp's per-bin term in FP64.
+//   * the 8 warps' per-window partials are combined in a fixed order through shared
+//     memory and written as one partial-map row (float64) per CTA row.
+#pragma once
+
+#include <algorithm>
+#include <cmath>
+
+#include "spct_internal.h"
+#include "sweep_common.cuh"
+
+namespace spct_fused {
+
+using namespace spct_dev;
+using namespace spct_impl;
+
+constexpr int kWarps = 8;
+constexpr int kB = 16;
+constexpr int kGroupBins = kWarps * kB;  // 128 bins per CTA
+constexpr int kExt = 256;                // extended columns per CTA (128 halo + 128 strip)
+constexpr int kVcWords = kExt / 2;       // u16 pairs per bin row
+
+struct FusedParams {
+    int kw, kh, nu, nv;
+    int metric, p_kind, T_pow2, accumulate;
+    double p, T, invT;
+    int group0;                  // first slab-local bin of this launch's bin group
+    const double* tmpl;          // full template, indexed by global bin
+    const uint32_t* prep;        // [0] fast flag, [1..] srep (slab-local), then S per group (int64)
+    const long long* S_group;    // sum of integral s_k per 128-bin group
+    double* partial;
+    double* map;                 // non-null: write the finished likelihood map (one group = every bin)
+    double inv_p, dmax, inv_dmax;  // inv_dmax != 0 iff dmax is a power of two (exact product)
+    int W, H;
+};
+
+// likelihood.cpp:220-221 (and the extension metrics), as in hist_match.cu finalize_kernel.
+__device__ __forceinline__ double finalize_L(double s, const FusedParams& f) {
+    double L;
+    if (f.metric == SPCT_METRIC_MINKOWSKI) {
+        const double d = f.p_kind == 1 ? s : pow(s, f.inv_p);
+        L = __dsub_rn(1.0, f.inv_dmax != 0.0 ? __dmul_rn(d, f.inv_dmax) : __ddiv_rn(d, f.dmax));
+    } else if (f.metric == SPCT_METRIC_CHISQ) {
+        L = __dsub_rn(1.0, __dmul_rn(s, 0.5));  // == s / 2 exactly
+    } else {
+        L = s;
+    }
+    return L < 0.0 ? 0.0 : (L > 1.0 ? 1.0 : L);
+}
+
+__device__ __forceinline__ uint32_t min_u16x2(uint32_t a, uint32_t b) {
+    uint32_t r;
+    asm("min.u16x2 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(b));
+    return r;
+}
+
+// Per-bin term of the general path (same arithmetic as hist_match.cu bin_term).
+__device__ __forceinline__ double general_term(uint32_t c, double t, const FusedParams& f) {
+    const double cd = static_cast<double>(c);
+    const double q = f.T_pow2 ? __dmul_rn(cd, f.invT) : __ddiv_rn(cd, f.T);
+    switch (f.metric) {
+        case SPCT_METRIC_MINKOWSKI: {
+            const double a = fabs(__dsub_rn(q, t));
+            if (f.p_kind == 1) return a;
+            if (f.p_kind == 2) return __dmul_rn(a, a);
+            return pow(a, f.p);
+        }
+        case SPCT_METRIC_INTERSECTION:
+            return fmin(q, t);
+        case SPCT_METRIC_BHATTACHARYYA:
+            return sqrt(__dmul_rn(q, t));
+        default: {
+            const double den = __dadd_rn(q, t);
+            if (!(den > 0.0)) return 0.0;
+            const double df = __dsub_rn(q, t);
+            return __ddiv_rn(__dmul_rn(df, df), den);
+        }
+    }
+}
+
+
+// vc rows are stored swizzled: word w of a bin row lives at w ^ ((w >> 3) & 4), so the
+// quarter-warp reads of 8 consecutive words per lane (two 16-B loads, 8 lanes per phase)
+// hit 8 distinct bank groups.  Pairs / quads stay contiguous under the swizzle.
+__device__ __forceinline__ int swz(int w) { return w ^ ((w >> 3) & 4); }
+
+__device__ __forceinline__ uint4 lds4(const uint32_t* row, int w) {
+    return *reinterpret_cast<const uint4*>(row + swz(w));
+}
+
+// Window counts (general path), phase 1: for bin row `vrow`, the inclusive prefix G of the
+// 256 extended columns for the lane's 8 columns (u16 pairs): the halo half (a0, a1) and
+// the strip half (b0, b1); with STAGE they are also written to `g` (the warp's staging
+// row for this bin) for the general-kw partner reads.
+template <bool STAGE>
+__device__ __forceinline__ void window_prefix(const uint32_t* vrow, uint32_t* g, int lane, uint32_t& a0, uint32_t& a1,
+                                              uint32_t& b0, uint32_t& b1) {
+    const uint2 wa = *reinterpret_cast<const uint2*>(vrow + swz(2 * lane));
+    const uint2 wb = *reinterpret_cast<const uint2*>(vrow + swz(64 + 2 * lane));
+    a0 = wa.x * 0x10001u;
+    a1 = wa.y * 0x10001u + __byte_perm(a0, 0, 0x3232);
+    b0 = wb.x * 0x10001u;
+    b1 = wb.y * 0x10001u + __byte_perm(b0, 0, 0x3232);
+    const uint32_t tot = __byte_perm(a1, b1, 0x7632);  // {sum a, sum b}
+    const uint32_t inc = warp_incl_scan(tot);
+    const uint32_t ex = inc - tot;
+    const uint32_t T1 = __byte_perm(__shfl_sync(0xffffffffu, inc, 31), 0, 0x1010);  // total of the halo half
+    const uint32_t ba = __byte_perm(ex, 0, 0x1010);
+    const uint32_t bb = __byte_perm(ex, 0, 0x3232) + T1;
+    a0 += ba;
+    a1 += ba;
+    b0 += bb;
+    b1 += bb;
+    if (STAGE) {
+        *reinterpret_cast<uint2*>(g + 2 * lane) = make_uint2(a0, a1);
+        *reinterpret_cast<uint2*>(g + 64 + 2 * lane) = make_uint2(b0, b1);
+    }
+}
+
+// Window counts (general path), phase 2 (after a __syncwarp): c = G(e) - G(e - kw) for the
+// lane's four windows, as two u16 pairs {j=0, j=1}, {j=2, j=3}.
+__device__ __forceinline__ void window_diff(const uint32_t* g, int pw, int psh, uint32_t b0, uint32_t b1,
+                                            uint32_t& c0, uint32_t& c1) {
+    const uint32_t q0 = g[pw], q1 = g[pw + 1], q2 = g[pw + 2];
+    c0 = b0 - __funnelshift_r(q0, q1, psh);
+    c1 = b1 - __funnelshift_r(q1, q2, psh);
+}
+
+// Inclusive scan step over 8-lane segments (shuffle in-range predicate, no select).
+__device__ __forceinline__ uint32_t scan_add8(uint32_t v, int o) {
+    uint32_t r;
+    asm("{\n\t.reg .pred p;\n\t.reg .u32 t;\n\t"
+        "shfl.sync.up.b32 t|p, %1, %2, 0x1800, 0xffffffff;\n\t"
+        "@p add.u32 %1, %1, t;\n\t"
+        "mov.u32 %0, %1;\n\t}"
+        : "=r"(r), "+r"(v)
+        : "r"(o));
+    return r;
+}
+
+// Window counts (integer path), quarter-warp layout: lane m (0..7) of a quarter owns the 16
+// windows ending at strip columns 16m .. 16m+15 (extended columns e = 128 + 16m + i) of one
+// bin.  With vc the bin's running column counts over the last kh rows,
+//     c(e) = c(127) + sum_{x=128..e} delta(x),   delta(x) = vc(x) - vc(x - kw),
+// and the anchor c(127) = sum of vc over [128 - kw, 128), i.e. of the lane's vc(e - kw)
+// values with 16m + i < kw.  delta is biased by +255 (>= kh) so every in-lane prefix and
+// scan partial is a non-negative u16; the bias is removed linearly at the end, where the
+// true counts 0 <= c <= kw*kh < 2^16 make the packed pairs exact.  One 8-lane scan of
+// {anchor partial, lane delta total} per bin: 3 shuffle steps + 1 broadcast.
+// Result: c[j] = {c(16m + 2j), c(16m + 2j + 1)} packed u16 pairs.
+template <int KWM>
+__device__ __forceinline__ void window_counts_q(const uint32_t* pb0, const uint32_t* pb1, const uint32_t* pa0,
+                                                const uint32_t* pa1, const uint32_t* vrow, int m, int aw0, int apsh,
+                                                const uint32_t* amask, uint32_t (&c)[8]) {
+    // pb0/pb1: the lane's two strip quads (words 64 + 8m, +4, swizzled), pa0/pa1 the
+    // vc(e - kw) quads for kw = 64 / 128; the general kw reads 9 words from `vrow`.
+    uint32_t b[8], a[8];
+    {
+        const uint4 x = *reinterpret_cast<const uint4*>(pb0), y = *reinterpret_cast<const uint4*>(pb1);
+        b[0] = x.x, b[1] = x.y, b[2] = x.z, b[3] = x.w, b[4] = y.x, b[5] = y.y, b[6] = y.z, b[7] = y.w;
+    }
+    if (KWM == 64 || KWM == 128) {
+        const uint4 x = *reinterpret_cast<const uint4*>(pa0), y = *reinterpret_cast<const uint4*>(pa1);
+        a[0] = x.x, a[1] = x.y, a[2] = x.z, a[3] = x.w, a[4] = y.x, a[5] = y.y, a[6] = y.z, a[7] = y.w;
+    } else {
+        uint32_t r[9];
+#pragma unroll
+        for (int i = 0; i < 9; ++i) r[i] = vrow[swz(aw0 + i)];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) a[j] = __funnelshift_r(r[j], r[j + 1], apsh);
+    }
+    uint32_t w[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+        const uint32_t d = b[j] - a[j] + 0x00FF00FFu;  // {delta + 255} pair (linear, exact after the bias)
+        w[j] = j ? d * 0x10001u + __byte_perm(w[j - 1], 0, 0x3232) : d * 0x10001u;
+    }
+    uint32_t x;  // anchor partial as a u16 pair sum
+    if (KWM == 64 || KWM == 128) {
+        x = (a[0] + a[1]) + (a[2] + a[3]) + (a[4] + a[5]) + (a[6] + a[7]);
+        if (KWM == 64) x = m < 4 ? x : 0u;
+    } else {
+        const uint4 m0 = *reinterpret_cast<const uint4*>(amask + 8 * m);
+        const uint4 m1 = *reinterpret_cast<const uint4*>(amask + 8 * m + 4);
+        x = ((a[0] & m0.x) + (a[1] & m0.y)) + ((a[2] & m0.z) + (a[3] & m0.w)) + ((a[4] & m1.x) + (a[5] & m1.y)) +
+            ((a[6] & m1.z) + (a[7] & m1.w));
+    }
+    const uint32_t pack = ((x + (x >> 16)) & 0xFFFFu) | (w[7] & 0xFFFF0000u);  // {anchor partial, delta total}
+    uint32_t inc = pack;
+#pragma unroll
+    for (int o = 1; o < 8; o <<= 1) inc = scan_add8(inc, o);
+    const uint32_t tot = __shfl_sync(0xffffffffu, inc, 7, 8);
+    const uint32_t s = (tot & 0xFFFFu) + ((inc - pack) >> 16) - 4080u * static_cast<uint32_t>(m);
+    const uint32_t S2 = s * 0x10001u;
+#pragma unroll
+    for (int j = 0; j < 8; ++j)
+        c[j] = w[j] + S2 - ((static_cast<uint32_t>(2 * j + 1) * 255u) | (static_cast<uint32_t>(2 * j + 2) * 255u << 16));
+}
+
+// Cross-quarter reduce-scatter of 8 packed words: afterwards lane (q, m) holds in v[0..1]
+// the warp's sums of words 4 (q >> 1) + 2 (q & 1) + {0, 1}.
+__device__ __forceinline__ void quarter_reduce(uint32_t (&v)[8], int q) {
+    const bool hi2 = q & 2, hi1 = q & 1;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+        const uint32_t send = hi2 ? v[j] : v[j + 4];
+        const uint32_t keep = hi2 ? v[j + 4] : v[j];
+        v[j] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
+    }
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+        const uint32_t send = hi1 ? v[j] : v[j + 2];
+        const uint32_t keep = hi1 ? v[j + 2] : v[j];
+        v[j] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
+    }
+}
+
+// ALLB (integer path only): the CTA's bin group is the whole histogram, so the window
+// total over the group's bins is kw * kh and need not be accumulated.
+// G8: 8-bit gray input with the default range (bin = v * nbins >> 8): the staging loads
+// and quantises without the generic per-kind dispatch.
+template <bool STORE, bool FAST, int KWM, bool ALLB, bool G8>
+__global__ void __launch_bounds__(256, 2) sweep_match_kernel(QuantParams q, PixelMode pm, spct_ih out, int Lb, int Wp,
+                                                             int band_rows, const uint32_t* __restrict__ Lt,
+                                                             const uint32_t* __restrict__ Hb, FusedParams f) {
+    extern __shared__ uint4 smem_raw[];
+    uint32_t* vc = reinterpret_cast<uint32_t*>(smem_raw);                 // [128 bins][128 words], swizzled
+    uint32_t* gbuf = vc + kGroupBins * kVcWords;                            // [8 warps][4][128 words] (general path)
+    double* red = reinterpret_cast<double*>(gbuf + kWarps * 4 * kVcWords);  // [2 rows][8 warps][128]
+    uint32_t* srep_s = reinterpret_cast<uint32_t*>(red + 2 * kWarps * kStrip);  // [128]
+    uint32_t* lrow = srep_s + kGroupBins;                                   // [2 rows][128] row carries
+    uint16_t* rowbins = reinterpret_cast<uint16_t*>(lrow + 2 * kGroupBins);  // [2 rows][128] strip bins
+    uint32_t* amask = reinterpret_cast<uint32_t*>(rowbins + 2 * kStrip);    // [8 lanes][8 words] anchor masks
+    // integer path: per row parity, warp and window pair, the packed {I, I} sums (and C after them)
+    uint32_t* red32 = reinterpret_cast<uint32_t*>(red);
+
+    // Both variants are launched; the one that does not match the template prep exits.
+    if ((__ldg(f.prep) != 0) != FAST) return;
+
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int strip = blockIdx.x, band = blockIdx.y;
+    const int g0 = f.group0;                               // slab-local first bin of the CTA
+    const int nb_cta = min(kGroupBins, out.bins - g0);
+    const int nwarps_live = (nb_cta + kB - 1) / kB;
+    const int kl0 = g0 + warp * kB;                        // warp's first slab-local bin
+    const bool warp_live = warp < nwarps_live;
+    const int k_live = min(kB, out.bins - kl0);
+    const int xs = strip * kStrip;                         // strip's first column
+    const int xl = xs + 4 * lane;                          // lane's first strip column
+    const int H = out.height, W = out.width;
+    const int y0 = band * band_rows, y1 = min(H, y0 + band_rows);
+    const int ystart = max(0, y0 - f.kh + 1);
+    const int k0 = out.bin0 + kl0;                         // global bin of the warp's first plane
+    const uint32_t kpat0 = pm.byte_mode ? 0x01010101u * static_cast<uint32_t>(k0) : 0u;
+    const uint8_t* g8p = static_cast<const uint8_t*>(q.p0);
+    auto raw_at = [&](int x, int y) -> uint64_t {
+        return G8 ? static_cast<uint64_t>(__ldg(g8p + static_cast<int64_t>(y) * q.pitch + x)) : pixel_raw(q, x, y);
+    };
+    auto bin_of = [&](uint64_t r) -> int {
+        return G8 ? static_cast<int>((static_cast<uint32_t>(r) * static_cast<uint32_t>(q.nbins)) >> 8) : bin_of_raw(r, q);
+    };
+
+    for (int i = tid; i < kGroupBins * kVcWords; i += blockDim.x) vc[i] = 0;
+    if (tid < kGroupBins) srep_s[tid] = (FAST && tid < nb_cta) ? __ldg(f.prep + 1 + g0 + tid) : 0u;
+    if (FAST && KWM == 0 && tid < 64) {
+        // anchor masks: u16 i of lane m's word j is valid iff 16m + 2j + i < kw
+        const int n = f.kw - 16 * (tid >> 3) - 2 * (tid & 7);
+        amask[tid] = n >= 2 ? 0xFFFFFFFFu : (n == 1 ? 0xFFFFu : 0u);
+    }
+
+    uint32_t V[4][kB];
+    if (STORE && warp_live) vpart_init<kB>(V, Hb, band, Lb, kl0, Wp, xl);
+    uint32_t* base_ptr = STORE ? out.data + static_cast<int64_t>(kl0) * out.plane_pitch + xl : nullptr;
+    const bool lane_live = xl < out.row_pitch;
+    const uint32_t store_mask = lane_live ? (k_live >= 32 ? 0xFFFFFFFFu : (1u << max(k_live, 0)) - 1u) : 0u;
+    const long long S = FAST ? f.S_group[g0 / kGroupBins] : 0;
+    // general path: G(e - kw) as a word and a bit shift
+    const int idx = kStrip + 4 * lane - f.kw;
+    const int pw = idx >> 1, psh = (idx & 1) * 16;
+    uint32_t* gb = gbuf + warp * 4 * kVcWords;
+    const uint32_t* vwarp = vc + warp * kB * kVcWords;
+    // integer path: quarter qq of the warp takes bin 4g + qq; lane mq owns windows 16mq ..
+    const int qq = lane >> 3, mq = lane & 7;
+    const int ca0 = kStrip + 16 * mq - f.kw;  // extended column of vc(e - kw) for the lane's first window
+    const int aw0 = ca0 >> 1, apsh = (ca0 & 1) * 16;
+    const uint32_t* vq = vwarp + qq * kVcWords;  // the quarter's bin row for g = 0
+    const uint32_t* pb0 = vq + swz(64 + 8 * mq);
+    const uint32_t* pb1 = vq + (swz(64 + 8 * mq) ^ 4);
+    const int wa = KWM == 128 ? 8 * mq : 32 + 8 * mq;
+    const uint32_t* pa0 = vq + swz(wa);
+    const uint32_t* pa1 = vq + (swz(wa) ^ 4);
+
+    // staging thread: extended column tid; prefetch one row ahead
+    const int xt = xs - kStrip + tid;
+    const bool xt_live = xt >= 0 && xt < W;
+    const int vcw = swz(tid >> 1);           // the staging column's (swizzled) vc word
+    const uint32_t vinc = 1u << (16 * (tid & 1));
+    const uint32_t* lt_cta = (STORE && Lt && strip > 0 && tid < kGroupBins && g0 + tid < Lb)
+                                 ? Lt + static_cast<int64_t>(strip) * H * Lb + g0 + tid
+                                 : nullptr;
+    // raw pixel values of the staging column, quantised one row after the load
+    uint64_t rn = xt_live ? raw_at(xt, y0) : 0, ro = 0;
+    bool have_o = false;  // y0 - kh < ystart: nothing to remove on the first row
+    uint32_t lpre = lt_cta ? __ldg(lt_cta + static_cast<int64_t>(y0) * Lb) : 0u;
+    __syncthreads();  // vc zeroed
+
+    // Pre-roll rows [ystart, y0) only feed vc, and nothing leaves the window there: one
+    // barrier-free pass with several loads in flight (a per-row loop would pay the full
+    // DRAM latency on every row).
+    if (xt_live) {
+        const int nb_lo = out.bin0 + g0;
+        uint32_t* vcol = vc + vcw;
+        for (int y = ystart; y < y0; y += 8) {
+            uint64_t r[8];
+#pragma unroll
+            for (int i = 0; i < 8; ++i) r[i] = y + i < y0 ? raw_at(xt, y + i) : 0;
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+                const int bn = bin_of(r[i]) - nb_lo;
+                if (y + i < y0 && static_cast<unsigned>(bn) < static_cast<unsigned>(nb_cta))
+                    atomicAdd(vcol + bn * kVcWords, vinc);
+            }
+        }
+    }
+
+    // Cross-warp combine of row yy: thread t < 128 sums the 8 warps' partials of the
+    // window ending at strip column t in a fixed order.  (Spreading it over all 8 warps
+    // was measured slower: every warp then carries the combine's latency.)
+    auto combine = [&](int yy) {
+        if (tid < kStrip) {
+            const int t = tid;
+            double term = 0.0;
+            if (FAST) {
+                // packed window pairs; every sum stays below 2^16 (at most kw * kh)
+                const uint32_t* rw = red32 + (yy & 1) * (kWarps * 64) + (t >> 1);
+                uint32_t xi = 0, xc = 0;
+#pragma unroll
+                for (int w = 0; w < kWarps; ++w)
+                    if (w < nwarps_live) {
+                        xi += rw[w * 64];
+                        if (!ALLB) xc += rw[2 * kWarps * 64 + w * 64];
+                    }
+                const long long I = (xi >> (16 * (t & 1))) & 0xFFFFu;
+                const long long C = ALLB ? static_cast<long long>(f.kw) * f.kh : (xc >> (16 * (t & 1))) & 0xFFFFu;
+                term = f.metric == SPCT_METRIC_INTERSECTION ? static_cast<double>(I) * f.invT
+                                                            : static_cast<double>(C + S - 2 * I) * f.invT;
+            } else {
+                const double* rb = red + (yy & 1) * (kWarps * kStrip);
+#pragma unroll
+                for (int w = 0; w < kWarps; ++w)
+                    if (w < nwarps_live) term = __dadd_rn(term, rb[w * kStrip + t]);
+            }
+            const int e = xs + t;
+            const int u = e - f.kw + 1, v = yy - f.kh + 1;
+            if (u >= 0 && e < W) {
+                if (f.map) {
+                    // finished map with spread_valid's border replication (likelihood.cpp:44-58)
+                    const double L = finalize_L(term, f);
+                    const int x = u + (f.kw - 1) / 2, yc = v + (f.kh - 1) / 2;
+                    const int xa = u == 0 ? 0 : x, xb = u == f.nu - 1 ? f.W - 1 : x;
+                    const int ya = v == 0 ? 0 : yc, yb = v == f.nv - 1 ? f.H - 1 : yc;
+                    for (int yy = ya; yy <= yb; ++yy)
+                        for (int xx = xa; xx <= xb; ++xx) f.map[static_cast<int64_t>(yy) * f.W + xx] = L;
+                } else {
+                    double* dst = f.partial + static_cast<int64_t>(v) * f.nu + u;
+                    *dst = f.accumulate ? __dadd_rn(*dst, term) : term;
+                }
+            }
+        }
+    };
+
+    // row yy's partials are in `red` (and must be combined) iff it is a match row
+    auto pending = [&](int yy) { return yy >= y0 && yy >= f.kh - 1; };
+    for (int y = y0; y < y1; ++y) {
+        __syncthreads();  // A: previous row's vc / staging reads are done, its partials written
+        // row y - 1's partials were written before A; its buffer is rewritten only after
+        // the next B.  Warps 0-3 combine while warps 4-7 start staging.
+        if (pending(y - 1)) combine(y - 1);
+        {   // stage row y: vertical running histogram (add row y, remove row y - kh),
+            // the strip's bins and row carries for the sweep, then prefetch row y + 1
+            const int pn = xt_live ? bin_of(rn) : 0xFFFF;
+            const int po = (xt_live && have_o) ? bin_of(ro) : -1;
+            if (xt_live) {
+                const int bn = pn - out.bin0 - g0;
+                if (static_cast<unsigned>(bn) < static_cast<unsigned>(nb_cta)) atomicAdd(&vc[bn * kVcWords + vcw], vinc);
+                const int bo = po - out.bin0 - g0;
+                if (po >= 0 && static_cast<unsigned>(bo) < static_cast<unsigned>(nb_cta))
+                    atomicSub(&vc[bo * kVcWords + vcw], vinc);
+            }
+            if (tid >= kStrip) rowbins[(y & 1) * kStrip + tid - kStrip] = static_cast<uint16_t>(pn);
+            else lrow[(y & 1) * kGroupBins + tid] = lpre;
+            if (y + 1 < y1) {
+                const int yo = y + 1 - f.kh;
+                have_o = yo >= ystart;
+                if (xt_live) {
+                    rn = raw_at(xt, y + 1);
+                    if (have_o) ro = raw_at(xt, yo);
+                }
+                if (lt_cta) lpre = __ldg(lt_cta + static_cast<int64_t>(y + 1) * Lb);
+            }
+        }
+        __syncthreads();  // B: vc holds rows (y - kh, y]; staging rows ready
+        const bool match_row = y >= f.kh - 1;
+        if (!warp_live || (!STORE && !match_row)) continue;
+
+        uint32_t t4[4] = {0, 0, 0, 0};
+        if (STORE) {
+            const uint2 rb2 = *reinterpret_cast<const uint2*>(rowbins + (y & 1) * kStrip + 4 * lane);
+            uint32_t bins4 = 0;
+            if (pm.byte_mode) {
+                bins4 = __byte_perm(rb2.x, rb2.y, 0x6420);
+            } else {
+                const uint32_t b4[4] = {rb2.x & 0xFFFFu, rb2.x >> 16, rb2.y & 0xFFFFu, rb2.y >> 16};
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    const uint32_t r = b4[j] - static_cast<uint32_t>(k0);
+                    bins4 |= (r < static_cast<uint32_t>(kB) ? r : 0xFFu) << (8 * j);
+                }
+            }
+            onehot_shifts(bins4 ^ kpat0, t4);
+        }
+        const uint4* lr = reinterpret_cast<const uint4*>(lrow + (y & 1) * kGroupBins + warp * kB);
+        uint32_t* prow = STORE ? base_ptr + static_cast<int64_t>(y) * out.row_pitch : nullptr;
+
+        uint32_t Iw[8] = {0, 0, 0, 0, 0, 0, 0, 0}, Cw[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+        double acc[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+        for (int g = 0; g < kB / 4; ++g) {
+            if (STORE)
+                vpart_group_q<kB>(V, g, t4, lr[g], prow + static_cast<int64_t>(4 * g) * out.plane_pitch, out.plane_pitch,
+                                  store_mask);
+            if (FAST && match_row) {
+                uint32_t c[8];
+                const int go = 4 * g * kVcWords;
+                window_counts_q<KWM>(pb0 + go, pb1 + go, pa0 + go, pa1 + go, vq + go, mq, aw0, apsh, amask, c);
+                const uint32_t sk = srep_s[warp * kB + 4 * g + qq];
+#pragma unroll
+                for (int j = 0; j < 8; ++j) {
+                    Iw[j] += min_u16x2(c[j], sk);
+                    if (!ALLB) Cw[j] += c[j];
+                }
+            } else if (match_row) {
+                uint32_t aw[4][2], bw[4][2];
+#pragma unroll
+                for (int i = 0; i < 4; ++i)
+                    window_prefix<KWM == 0>(vwarp + (4 * g + i) * kVcWords, gb + i * kVcWords, lane, aw[i][0], aw[i][1],
+                                            bw[i][0], bw[i][1]);
+                if (KWM == 0) __syncwarp();
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                    const int k = 4 * g + i;
+                    uint32_t c0, c1;
+                    if (KWM == 64) {
+                        // G(e - 64): the partner lane^16's halo half (lanes < 16) or strip half (>= 16)
+                        const uint32_t r0 = __shfl_xor_sync(0xffffffffu, lane >= 16 ? aw[i][0] : bw[i][0], 16);
+                        const uint32_t r1 = __shfl_xor_sync(0xffffffffu, lane >= 16 ? aw[i][1] : bw[i][1], 16);
+                        c0 = bw[i][0] - r0;
+                        c1 = bw[i][1] - r1;
+                    } else if (KWM == 128) {
+                        c0 = bw[i][0] - aw[i][0];  // G(e - 128) is the lane's own halo half
+                        c1 = bw[i][1] - aw[i][1];
+                    } else {
+                        window_diff(gb + i * kVcWords, pw, psh, bw[i][0], bw[i][1], c0, c1);
+                    }
+                    if (k < k_live) {
+                        const double t = __ldg(f.tmpl + k0 + k);
+                        acc[0] = __dadd_rn(acc[0], general_term(c0 & 0xFFFFu, t, f));
+                        acc[1] = __dadd_rn(acc[1], general_term(c0 >> 16, t, f));
+                        acc[2] = __dadd_rn(acc[2], general_term(c1 & 0xFFFFu, t, f));
+                        acc[3] = __dadd_rn(acc[3], general_term(c1 >> 16, t, f));
+                    }
+                }
+                if (KWM == 0) __syncwarp();
+            }
+        }
+        if (match_row) {
+            if (FAST) {
+                // the quarters hold the same 16 windows per lane for different bins
+                quarter_reduce(Iw, qq);
+                const int jb = 4 * (qq >> 1) + 2 * (qq & 1);
+                uint32_t* rw = red32 + (y & 1) * (kWarps * 64) + warp * 64 + 8 * mq + jb;
+                *reinterpret_cast<uint2*>(rw) = make_uint2(Iw[0], Iw[1]);
+                if (!ALLB) {
+                    quarter_reduce(Cw, qq);
+                    *reinterpret_cast<uint2*>(rw + 2 * kWarps * 64) = make_uint2(Cw[0], Cw[1]);
+                }
+            } else {
+                double* rb = red + (y & 1) * (kWarps * kStrip) + warp * kStrip;
+                rb[4 * lane + 0] = acc[0];
+                rb[4 * lane + 1] = acc[1];
+                rb[4 * lane + 2] = acc[2];
+                rb[4 * lane + 3] = acc[3];
+            }
+        }
+    }
+    __syncthreads();
+    if (y1 > y0 && pending(y1 - 1)) combine(y1 - 1);
+}
+
+constexpr size_t kSmemBytes = (size_t(kGroupBins) * kVcWords + size_t(kWarps) * 4 * kVcWords) * 4 +
+                              size_t(2) * kWarps * kStrip * 8 + size_t(kGroupBins) * 4 * 3 + size_t(2) * kStrip * 2 +
+                              64 * 4;
+
+
+template <int KWM, bool ALLB, bool G8>
+void launch_variants(dim3 grid, cudaStream_t s, const QuantParams& q, const PixelMode& pm, const spct_ih& out,
+                     const BuildPlan& bp, const uint32_t* Lt, const uint32_t* Hb, const FusedParams& f) {
+    static bool attr_set = false;
+    if (!attr_set) {
+        cudaFuncSetAttribute(sweep_match_kernel<true, true, KWM, ALLB, G8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBytes);
+        cudaFuncSetAttribute(sweep_match_kernel<true, false, KWM, false, G8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBytes);
+        cudaFuncSetAttribute(sweep_match_kernel<false, true, KWM, ALLB, G8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBytes);
+        cudaFuncSetAttribute(sweep_match_kernel<false, false, KWM, false, G8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBytes);
+        attr_set = true;
+    }
+    // integer (template-crop) variant and FP64 variant: the one not selected by the
+    // device-side template prep exits on entry
+    if (out.data) {
+        sweep_match_kernel<true, true, KWM, ALLB, G8><<<grid, 256, kSmemBytes, s>>>(q, pm, out, bp.Lb, bp.Wp, bp.band_rows, Lt, Hb, f);
+        sweep_match_kernel<true, false, KWM, false, G8><<<grid, 256, kSmemBytes, s>>>(q, pm, out, bp.Lb, bp.Wp, bp.band_rows, Lt, Hb, f);
+    } else {
+        sweep_match_kernel<false, true, KWM, ALLB, G8><<<grid, 256, kSmemBytes, s>>>(q, pm, out, bp.Lb, bp.Wp, bp.band_rows, nullptr, nullptr, f);
+        sweep_match_kernel<false, false, KWM, false, G8><<<grid, 256, kSmemBytes, s>>>(q, pm, out, bp.Lb, bp.Wp, bp.band_rows, nullptr, nullptr, f);
+    }
+}
+
+template <int KWM>
+void launch_kw_impl(bool allb, bool g8, dim3 grid, cudaStream_t s, const QuantParams& q, const PixelMode& pm,
+                    const spct_ih& out, const BuildPlan& bp, const uint32_t* Lt, const uint32_t* Hb, const FusedParams& f) {
+    if (g8) {
+        if (allb) launch_variants<KWM, true, true>(grid, s, q, pm, out, bp, Lt, Hb, f);
+        else launch_variants<KWM, false, true>(grid, s, q, pm, out, bp, Lt, Hb, f);
+    } else {
+        if (allb) launch_variants<KWM, true, false>(grid, s, q, pm, out, bp, Lt, Hb, f);
+        else launch_variants<KWM, false, false>(grid, s, q, pm, out, bp, Lt, Hb, f);
+    }
+}
+
+}  // namespace spct_fused
+
+namespace spct_fused {
+// One translation unit per window-width specialisation (fused_kw{64,128,0}.cu), so the
+// kernel variants compile in parallel.
+#define SPCT_FUSED_LAUNCHER(NAME)                                                                              \
+    void NAME(bool allb, bool g8, dim3 grid, cudaStream_t s, const QuantParams& q, const PixelMode& pm,       \
+              const spct_ih& out, const BuildPlan& bp, const uint32_t* Lt, const uint32_t* Hb, const FusedParams& f);
+SPCT_FUSED_LAUNCHER(launch_kw64)
+SPCT_FUSED_LAUNCHER(launch_kw128)
+SPCT_FUSED_LAUNCHER(launch_kw_any)
+#undef SPCT_FUSED_LAUNCHER
+size_t smem_bytes();
+}  // namespace spct_fused

@@ -204,11 +204,10 @@ __device__ __forceinline__ void onehot_shifts(uint32_t dbins, uint32_t (&t)[4]) 
 // One group of four planes (4g .. 4g+3) of the row update, bin-major: Q[j] holds, in byte
 // i, the count of bin 4g+i among the lane's columns <= j (the one-hot of column j is
 // 1 << (8 r_j - 32 g)).  Q[3] is then already the packed per-lane total of the four bins
-// that the cross-lane scan needs.  `prow` points at plane 0 of the warp in this row;
-// plane k is prow + k * ppb bytes.
+// that the cross-lane scan needs.  `p` points at plane 4g of the row.
 template <int B>
-__device__ __forceinline__ void vpart_group_q(uint32_t (&V)[4][B], int g, const uint32_t (&t)[4], uint4 L,
-                                              uint32_t* prow, uint32_t ppb, uint32_t store_mask) {
+__device__ __forceinline__ void vpart_group_q(uint32_t (&V)[4][B], int g, const uint32_t (&t)[4], uint4 L, uint32_t* p,
+                                              int64_t plane_pitch, uint32_t store_mask) {
     uint32_t Q[4];
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
@@ -225,7 +224,8 @@ __device__ __forceinline__ void vpart_group_q(uint32_t (&V)[4][B], int g, const 
         V[1][k] += base + __byte_perm(Q[1], 0, 0x4440 + i);
         V[2][k] += base + __byte_perm(Q[2], 0, 0x4440 + i);
         V[3][k] += base + __byte_perm(Q[3], 0, 0x4440 + i);
-        st_cs_v4_pred((store_mask >> k) & 1u, plane_addr(prow, k, ppb), V[0][k], V[1][k], V[2][k], V[3][k]);
+        st_cs_v4_pred(store_mask & (1u << k), p, V[0][k], V[1][k], V[2][k], V[3][k]);
+        p += plane_pitch;
     }
 }
 
