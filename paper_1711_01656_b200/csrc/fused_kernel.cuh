@@ -40,6 +40,7 @@ constexpr int kB = 16;
 constexpr int kGroupBins = kWarps * kB;  // 128 bins per CTA
 constexpr int kExt = 256;                // extended columns per CTA (128 halo + 128 strip)
 constexpr int kVcWords = kExt / 2;       // u16 pairs per bin row
+constexpr int kVcStride = kVcWords + kVcWords / 8;  // row stride: 4 padding words after every 32
 
 struct FusedParams {
     int kw, kh, nu, nv;
@@ -100,14 +101,11 @@ __device__ __forceinline__ double general_term(uint32_t c, double t, const Fused
 }
 
 
-// vc rows are stored swizzled: word w of a bin row lives at w ^ ((w >> 3) & 4), so the
-// quarter-warp reads of 8 consecutive words per lane (two 16-B loads, 8 lanes per phase)
-// hit 8 distinct bank groups.  Pairs / quads stay contiguous under the swizzle.
-__device__ __forceinline__ int swz(int w) { return w ^ ((w >> 3) & 4); }
-
-__device__ __forceinline__ uint4 lds4(const uint32_t* row, int w) {
-    return *reinterpret_cast<const uint4*>(row + swz(w));
-}
+// vc rows are padded: word w of a bin row lives at w + 4 (w >> 5), so the quarter-warp
+// reads of 8 consecutive words per lane (two 16-B loads, 8 lanes per phase) hit 8
+// distinct bank groups, and every quad the integer path reads sits at a fixed offset
+// from the lane's strip quad.
+__device__ __forceinline__ int vcw(int w) { return w + ((w >> 3) & ~3); }
 
 // Window counts (general path), phase 1: for bin row `vrow`, the inclusive prefix G of the
 // 256 extended columns for the lane's 8 columns (u16 pairs): the halo half (a0, a1) and
@@ -116,8 +114,8 @@ __device__ __forceinline__ uint4 lds4(const uint32_t* row, int w) {
 template <bool STAGE>
 __device__ __forceinline__ void window_prefix(const uint32_t* vrow, uint32_t* g, int lane, uint32_t& a0, uint32_t& a1,
                                               uint32_t& b0, uint32_t& b1) {
-    const uint2 wa = *reinterpret_cast<const uint2*>(vrow + swz(2 * lane));
-    const uint2 wb = *reinterpret_cast<const uint2*>(vrow + swz(64 + 2 * lane));
+    const uint2 wa = *reinterpret_cast<const uint2*>(vrow + vcw(2 * lane));
+    const uint2 wb = *reinterpret_cast<const uint2*>(vrow + vcw(64 + 2 * lane));
     a0 = wa.x * 0x10001u;
     a1 = wa.y * 0x10001u + __byte_perm(a0, 0, 0x3232);
     b0 = wb.x * 0x10001u;
@@ -164,37 +162,38 @@ __device__ __forceinline__ uint32_t scan_add8(uint32_t v, int o) {
 // bin.  With vc the bin's running column counts over the last kh rows,
 //     c(e) = c(127) + sum_{x=128..e} delta(x),   delta(x) = vc(x) - vc(x - kw),
 // and the anchor c(127) = sum of vc over [128 - kw, 128), i.e. of the lane's vc(e - kw)
-// values with 16m + i < kw.  delta is biased by +255 (>= kh) so every in-lane prefix and
-// scan partial is a non-negative u16; the bias is removed linearly at the end, where the
-// true counts 0 <= c <= kw*kh < 2^16 make the packed pairs exact.  One 8-lane scan of
-// {anchor partial, lane delta total} per bin: 3 shuffle steps + 1 broadcast.
+// values with 16m + i < kw.  The in-lane prefix starts at +4080 (= 16 * 255 >= any
+// negative partial sum), so every prefix half is a non-negative u16 and the broadcast of
+// a word's high half is exact; the same offset per lane is removed once, with the anchor,
+// where the true counts 0 <= c <= kw*kh < 2^16 make the packed pairs exact.  One 8-lane
+// scan of {anchor partial, lane prefix total} per bin: 3 shuffle steps + 1 broadcast.
 // Result: c[j] = {c(16m + 2j), c(16m + 2j + 1)} packed u16 pairs.
+// pb: the lane's strip quad (word 64 + 8m, padded); the vc(e - kw) quads of kw = 64 / 128
+// are at fixed offsets from it; the general kw reads 9 words from `vrow`.
 template <int KWM>
-__device__ __forceinline__ void window_counts_q(const uint32_t* pb0, const uint32_t* pb1, const uint32_t* pa0,
-                                                const uint32_t* pa1, const uint32_t* vrow, int m, int aw0, int apsh,
+__device__ __forceinline__ void window_counts_q(const uint32_t* pb, const uint32_t* vrow, int m, int aw0, int apsh,
                                                 const uint32_t* amask, uint32_t (&c)[8]) {
-    // pb0/pb1: the lane's two strip quads (words 64 + 8m, +4, swizzled), pa0/pa1 the
-    // vc(e - kw) quads for kw = 64 / 128; the general kw reads 9 words from `vrow`.
     uint32_t b[8], a[8];
     {
-        const uint4 x = *reinterpret_cast<const uint4*>(pb0), y = *reinterpret_cast<const uint4*>(pb1);
+        const uint4 x = *reinterpret_cast<const uint4*>(pb), y = *reinterpret_cast<const uint4*>(pb + 4);
         b[0] = x.x, b[1] = x.y, b[2] = x.z, b[3] = x.w, b[4] = y.x, b[5] = y.y, b[6] = y.z, b[7] = y.w;
     }
     if (KWM == 64 || KWM == 128) {
-        const uint4 x = *reinterpret_cast<const uint4*>(pa0), y = *reinterpret_cast<const uint4*>(pa1);
+        const uint32_t* pa = pb - (KWM == 64 ? 36 : 72);
+        const uint4 x = *reinterpret_cast<const uint4*>(pa), y = *reinterpret_cast<const uint4*>(pa + 4);
         a[0] = x.x, a[1] = x.y, a[2] = x.z, a[3] = x.w, a[4] = y.x, a[5] = y.y, a[6] = y.z, a[7] = y.w;
     } else {
         uint32_t r[9];
 #pragma unroll
-        for (int i = 0; i < 9; ++i) r[i] = vrow[swz(aw0 + i)];
+        for (int i = 0; i < 9; ++i) r[i] = vrow[vcw(aw0 + i)];
 #pragma unroll
         for (int j = 0; j < 8; ++j) a[j] = __funnelshift_r(r[j], r[j + 1], apsh);
     }
     uint32_t w[8];
 #pragma unroll
     for (int j = 0; j < 8; ++j) {
-        const uint32_t d = b[j] - a[j] + 0x00FF00FFu;  // {delta + 255} pair (linear, exact after the bias)
-        w[j] = j ? d * 0x10001u + __byte_perm(w[j - 1], 0, 0x3232) : d * 0x10001u;
+        const uint32_t d = b[j] - a[j];  // {delta, delta} pair, linear encoding
+        w[j] = d * 0x10001u + (j ? __byte_perm(w[j - 1], 0, 0x3232) : 0x0FF00FF0u);
     }
     uint32_t x;  // anchor partial as a u16 pair sum
     if (KWM == 64 || KWM == 128) {
@@ -206,16 +205,15 @@ __device__ __forceinline__ void window_counts_q(const uint32_t* pb0, const uint3
         x = ((a[0] & m0.x) + (a[1] & m0.y)) + ((a[2] & m0.z) + (a[3] & m0.w)) + ((a[4] & m1.x) + (a[5] & m1.y)) +
             ((a[6] & m1.z) + (a[7] & m1.w));
     }
-    const uint32_t pack = ((x + (x >> 16)) & 0xFFFFu) | (w[7] & 0xFFFF0000u);  // {anchor partial, delta total}
+    const uint32_t pack = ((x + (x >> 16)) & 0xFFFFu) | (w[7] & 0xFFFF0000u);  // {anchor partial, prefix total}
     uint32_t inc = pack;
 #pragma unroll
     for (int o = 1; o < 8; o <<= 1) inc = scan_add8(inc, o);
     const uint32_t tot = __shfl_sync(0xffffffffu, inc, 7, 8);
-    const uint32_t s = (tot & 0xFFFFu) + ((inc - pack) >> 16) - 4080u * static_cast<uint32_t>(m);
+    const uint32_t s = (tot & 0xFFFFu) + ((inc - pack) >> 16) - 4080u * static_cast<uint32_t>(m + 1);
     const uint32_t S2 = s * 0x10001u;
 #pragma unroll
-    for (int j = 0; j < 8; ++j)
-        c[j] = w[j] + S2 - ((static_cast<uint32_t>(2 * j + 1) * 255u) | (static_cast<uint32_t>(2 * j + 2) * 255u << 16));
+    for (int j = 0; j < 8; ++j) c[j] = w[j] + S2;
 }
 
 // Cross-quarter reduce-scatter of 8 packed words: afterwards lane (q, m) holds in v[0..1]
@@ -245,8 +243,8 @@ __global__ void __launch_bounds__(256, 2) sweep_match_kernel(QuantParams q, Pixe
                                                              int band_rows, const uint32_t* __restrict__ Lt,
                                                              const uint32_t* __restrict__ Hb, FusedParams f) {
     extern __shared__ uint4 smem_raw[];
-    uint32_t* vc = reinterpret_cast<uint32_t*>(smem_raw);                 // [128 bins][128 words], swizzled
-    uint32_t* gbuf = vc + kGroupBins * kVcWords;                            // [8 warps][4][128 words] (general path)
+    uint32_t* vc = reinterpret_cast<uint32_t*>(smem_raw);                 // [128 bins][144 words], padded
+    uint32_t* gbuf = vc + kGroupBins * kVcStride;                           // [8 warps][4][128 words] (general path)
     double* red = reinterpret_cast<double*>(gbuf + kWarps * 4 * kVcWords);  // [2 rows][8 warps][128]
     uint32_t* srep_s = reinterpret_cast<uint32_t*>(red + 2 * kWarps * kStrip);  // [128]
     uint32_t* lrow = srep_s + kGroupBins;                                   // [2 rows][128] row carries
@@ -281,7 +279,7 @@ __global__ void __launch_bounds__(256, 2) sweep_match_kernel(QuantParams q, Pixe
         return G8 ? static_cast<int>((static_cast<uint32_t>(r) * static_cast<uint32_t>(q.nbins)) >> 8) : bin_of_raw(r, q);
     };
 
-    for (int i = tid; i < kGroupBins * kVcWords; i += blockDim.x) vc[i] = 0;
+    for (int i = tid; i < kGroupBins * kVcStride; i += blockDim.x) vc[i] = 0;
     if (tid < kGroupBins) srep_s[tid] = (FAST && tid < nb_cta) ? __ldg(f.prep + 1 + g0 + tid) : 0u;
     if (FAST && KWM == 0 && tid < 64) {
         // anchor masks: u16 i of lane m's word j is valid iff 16m + 2j + i < kw
@@ -299,22 +297,18 @@ __global__ void __launch_bounds__(256, 2) sweep_match_kernel(QuantParams q, Pixe
     const int idx = kStrip + 4 * lane - f.kw;
     const int pw = idx >> 1, psh = (idx & 1) * 16;
     uint32_t* gb = gbuf + warp * 4 * kVcWords;
-    const uint32_t* vwarp = vc + warp * kB * kVcWords;
+    const uint32_t* vwarp = vc + warp * kB * kVcStride;
     // integer path: quarter qq of the warp takes bin 4g + qq; lane mq owns windows 16mq ..
     const int qq = lane >> 3, mq = lane & 7;
     const int ca0 = kStrip + 16 * mq - f.kw;  // extended column of vc(e - kw) for the lane's first window
     const int aw0 = ca0 >> 1, apsh = (ca0 & 1) * 16;
-    const uint32_t* vq = vwarp + qq * kVcWords;  // the quarter's bin row for g = 0
-    const uint32_t* pb0 = vq + swz(64 + 8 * mq);
-    const uint32_t* pb1 = vq + (swz(64 + 8 * mq) ^ 4);
-    const int wa = KWM == 128 ? 8 * mq : 32 + 8 * mq;
-    const uint32_t* pa0 = vq + swz(wa);
-    const uint32_t* pa1 = vq + (swz(wa) ^ 4);
+    const uint32_t* vq = vwarp + qq * kVcStride;  // the quarter's bin row for g = 0
+    const uint32_t* pb = vq + vcw(64 + 8 * mq);
 
     // staging thread: extended column tid; prefetch one row ahead
     const int xt = xs - kStrip + tid;
     const bool xt_live = xt >= 0 && xt < W;
-    const int vcw = swz(tid >> 1);           // the staging column's (swizzled) vc word
+    const int vcol_w = vcw(tid >> 1);        // the staging column's (padded) vc word
     const uint32_t vinc = 1u << (16 * (tid & 1));
     const uint32_t* lt_cta = (STORE && Lt && strip > 0 && tid < kGroupBins && g0 + tid < Lb)
                                  ? Lt + static_cast<int64_t>(strip) * H * Lb + g0 + tid
@@ -330,7 +324,7 @@ __global__ void __launch_bounds__(256, 2) sweep_match_kernel(QuantParams q, Pixe
     // DRAM latency on every row).
     if (xt_live) {
         const int nb_lo = out.bin0 + g0;
-        uint32_t* vcol = vc + vcw;
+        uint32_t* vcol = vc + vcol_w;
         for (int y = ystart; y < y0; y += 8) {
             uint64_t r[8];
 #pragma unroll
@@ -339,7 +333,7 @@ __global__ void __launch_bounds__(256, 2) sweep_match_kernel(QuantParams q, Pixe
             for (int i = 0; i < 8; ++i) {
                 const int bn = bin_of(r[i]) - nb_lo;
                 if (y + i < y0 && static_cast<unsigned>(bn) < static_cast<unsigned>(nb_cta))
-                    atomicAdd(vcol + bn * kVcWords, vinc);
+                    atomicAdd(vcol + bn * kVcStride, vinc);
             }
         }
     }
@@ -403,10 +397,10 @@ __global__ void __launch_bounds__(256, 2) sweep_match_kernel(QuantParams q, Pixe
             const int po = (xt_live && have_o) ? bin_of(ro) : -1;
             if (xt_live) {
                 const int bn = pn - out.bin0 - g0;
-                if (static_cast<unsigned>(bn) < static_cast<unsigned>(nb_cta)) atomicAdd(&vc[bn * kVcWords + vcw], vinc);
+                if (static_cast<unsigned>(bn) < static_cast<unsigned>(nb_cta)) atomicAdd(&vc[bn * kVcStride + vcol_w], vinc);
                 const int bo = po - out.bin0 - g0;
                 if (po >= 0 && static_cast<unsigned>(bo) < static_cast<unsigned>(nb_cta))
-                    atomicSub(&vc[bo * kVcWords + vcw], vinc);
+                    atomicSub(&vc[bo * kVcStride + vcol_w], vinc);
             }
             if (tid >= kStrip) rowbins[(y & 1) * kStrip + tid - kStrip] = static_cast<uint16_t>(pn);
             else lrow[(y & 1) * kGroupBins + tid] = lpre;
@@ -452,8 +446,8 @@ __global__ void __launch_bounds__(256, 2) sweep_match_kernel(QuantParams q, Pixe
                                   store_mask);
             if (FAST && match_row) {
                 uint32_t c[8];
-                const int go = 4 * g * kVcWords;
-                window_counts_q<KWM>(pb0 + go, pb1 + go, pa0 + go, pa1 + go, vq + go, mq, aw0, apsh, amask, c);
+                const int go = 4 * g * kVcStride;
+                window_counts_q<KWM>(pb + go, vq + go, mq, aw0, apsh, amask, c);
                 const uint32_t sk = srep_s[warp * kB + 4 * g + qq];
 #pragma unroll
                 for (int j = 0; j < 8; ++j) {
@@ -464,7 +458,7 @@ __global__ void __launch_bounds__(256, 2) sweep_match_kernel(QuantParams q, Pixe
                 uint32_t aw[4][2], bw[4][2];
 #pragma unroll
                 for (int i = 0; i < 4; ++i)
-                    window_prefix<KWM == 0>(vwarp + (4 * g + i) * kVcWords, gb + i * kVcWords, lane, aw[i][0], aw[i][1],
+                    window_prefix<KWM == 0>(vwarp + (4 * g + i) * kVcStride, gb + i * kVcWords, lane, aw[i][0], aw[i][1],
                                             bw[i][0], bw[i][1]);
                 if (KWM == 0) __syncwarp();
 #pragma unroll
@@ -518,7 +512,7 @@ __global__ void __launch_bounds__(256, 2) sweep_match_kernel(QuantParams q, Pixe
     if (y1 > y0 && pending(y1 - 1)) combine(y1 - 1);
 }
 
-constexpr size_t kSmemBytes = (size_t(kGroupBins) * kVcWords + size_t(kWarps) * 4 * kVcWords) * 4 +
+constexpr size_t kSmemBytes = (size_t(kGroupBins) * kVcStride + size_t(kWarps) * 4 * kVcWords) * 4 +
                               size_t(2) * kWarps * kStrip * 8 + size_t(kGroupBins) * 4 * 3 + size_t(2) * kStrip * 2 +
                               64 * 4;
 
