@@ -167,3 +167,217 @@ spct_status build_carries(const QuantParams& q, const spct_ih& out, const BuildP
 }
 
 }  // namespace spct_impl
+
+// ------------------------------------------------------------------ fused-sweep carries
+//
+// The fused build+match sweep (fused_kernel.cuh) starts each (strip s, band j) tile from
+//   Lt16[s][y][kl] = count of kl in row y, columns [0, 128 s)                    (u16)
+//   C16[j-1][kl][x] = count of kl in column x, rows < y0_j                       (u16)
+//   A32[kl][j-1][s] = count of kl in rows < y0_j, columns [0, 128 s)             (u32)
+// and rebuilds H(y0_j, x, kl) = A + sum over the strip's columns <= x of C16 itself, so
+// no 32-bit band-carry table is written or read.  Two passes over 1 B/px:
+//   fcarry_tiles_kernel   one CTA per (strip, band, 128-bin chunk): the strip-row
+//                         histograms (u8), the band's column counts and band x strip totals;
+//   fcarry_prefix_kernel  prefix of the strip-row histograms over strips (-> Lt16) and of
+//                         the column counts over bands (in place -> C16);
+//   fcarry_corner_kernel  one CTA per bin: 2-D prefix of the band x strip totals (-> A32).
+
+namespace spct_carry {
+
+constexpr int kTileBins = 128;
+
+template <bool G8>
+__global__ void __launch_bounds__(256) fcarry_tiles_kernel(QuantParams q, int bin0, int bins, int Lb, int nstrips,
+                                                           int nbands, int band_rows, uint8_t* __restrict__ R8,
+                                                           uint16_t* __restrict__ C16, uint32_t* __restrict__ T1) {
+    extern __shared__ uint32_t fsm[];
+    uint32_t* cnt = fsm;                           // [128 bins][128 columns]
+    uint32_t* rh = fsm + kTileBins * kStrip;       // [8 warps][128 bins]
+    const int s = blockIdx.x, j = blockIdx.y, kc0 = blockIdx.z * kTileBins;
+    const int kcn = min(kTileBins, Lb - kc0);
+    const bool need_r = s + 1 < nstrips, need_c = j + 1 < nbands;
+    if (!need_r && !need_c) return;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    if (need_c)
+        for (int i = tid; i < kTileBins * kStrip; i += 256) cnt[i] = 0;
+    for (int i = tid; i < 8 * kTileBins; i += 256) rh[i] = 0;
+    __syncthreads();
+    const int y0 = j * band_rows, y1 = min(q.height, y0 + band_rows);
+    const int x = s * kStrip + 4 * lane;
+    const int klo = bin0 + kc0, khi = min(kcn, bins - kc0);
+    uint32_t* rw = rh + warp * kTileBins;
+    for (int y = y0 + warp; y < y1; y += 8) {
+        int b[4];
+        if (G8 && x + 3 < q.width &&
+            ((reinterpret_cast<uintptr_t>(q.p0) + static_cast<int64_t>(y) * q.pitch + x) & 3) == 0) {
+            const uint32_t w = __ldg(reinterpret_cast<const uint32_t*>(static_cast<const uint8_t*>(q.p0) +
+                                                                        static_cast<int64_t>(y) * q.pitch + x));
+#pragma unroll
+            for (int c = 0; c < 4; ++c) b[c] = static_cast<int>((((w >> (8 * c)) & 0xFFu) * q.nbins) >> 8);
+        } else {
+#pragma unroll
+            for (int c = 0; c < 4; ++c) b[c] = x + c < q.width ? pixel_bin(q, x + c, y) : -1;
+        }
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+            const int k = b[c] - klo;
+            if (b[c] >= 0 && static_cast<unsigned>(k) < static_cast<unsigned>(khi)) {
+                if (need_c) atomicAdd(&cnt[k * kStrip + 4 * lane + c], 1u);
+                if (need_r) atomicAdd(&rw[k], 1u);
+            }
+        }
+        if (need_r) {
+            __syncwarp();
+            if (4 * lane < kcn) {
+                const uint4 h = *reinterpret_cast<const uint4*>(rw + 4 * lane);
+                *reinterpret_cast<uint4*>(rw + 4 * lane) = make_uint4(0, 0, 0, 0);
+                const uint32_t packed = h.x | (h.y << 8) | (h.z << 16) | (h.w << 24);
+                *reinterpret_cast<uint32_t*>(R8 + (static_cast<int64_t>(s) * q.height + y) * Lb + kc0 + 4 * lane) = packed;
+            }
+            __syncwarp();
+        }
+    }
+    if (!need_c) return;
+    __syncthreads();
+    const int Wp = nstrips * kStrip;
+    for (int i = tid; i < kcn * (kStrip / 2); i += 256) {
+        const int k = i / (kStrip / 2), c2 = 2 * (i % (kStrip / 2));
+        const uint32_t v = cnt[k * kStrip + c2] | (cnt[k * kStrip + c2 + 1] << 16);
+        *reinterpret_cast<uint32_t*>(C16 + (static_cast<int64_t>(j) * Lb + kc0 + k) * Wp + s * kStrip + c2) = v;
+    }
+    // band x strip totals, [kl][j][s]
+    for (int k = warp; k < kcn; k += 8) {
+        const uint4 v = *reinterpret_cast<const uint4*>(cnt + k * kStrip + 4 * lane);
+        uint32_t t = v.x + v.y + v.z + v.w;
+#pragma unroll
+        for (int o = 16; o; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+        if (lane == 0) T1[(static_cast<int64_t>(kc0 + k) * (nbands - 1) + j) * nstrips + s] = t;
+    }
+}
+
+// Blocks [0, nb_lt): row carries (thread = (row, 4 bins)); blocks [nb_lt, ...): column
+// counts over bands (thread = (bin, 4 columns)), in place.
+__global__ void __launch_bounds__(256) fcarry_prefix_kernel(int H, int Lb, int Wp, int nstrips, int nbands, int nb_lt,
+                                                            const uint8_t* __restrict__ R8,
+                                                            uint16_t* __restrict__ Lt16, uint16_t* __restrict__ C16) {
+    if (static_cast<int>(blockIdx.x) < nb_lt) {
+        const int64_t i = static_cast<int64_t>(blockIdx.x) * 256 + threadIdx.x;  // (y, quad)
+        const int quads = Lb / 4;
+        if (i >= static_cast<int64_t>(H) * quads) return;
+        const int64_t off = (i / quads) * Lb + 4 * (i % quads);
+        const int64_t sstride = static_cast<int64_t>(H) * Lb;
+        uint32_t a0 = 0, a1 = 0;  // u16 pairs: bins {0,1}, {2,3}
+        for (int s = 0; s + 1 < nstrips; ++s) {
+            const uint32_t v = __ldg(reinterpret_cast<const uint32_t*>(R8 + s * sstride + off));
+            a0 += __byte_perm(v, 0, 0x4140);  // {b0, b1} as u16 pair
+            a1 += __byte_perm(v, 0, 0x4342);
+            *reinterpret_cast<uint2*>(Lt16 + (s + 1) * sstride + off) = make_uint2(a0, a1);
+        }
+    } else {
+        const int64_t i = static_cast<int64_t>(blockIdx.x - nb_lt) * 256 + threadIdx.x;  // (bin, quad)
+        const int64_t plane = static_cast<int64_t>(Lb) * Wp;
+        if (i >= plane / 4) return;
+        uint16_t* p = C16 + 4 * i;
+        uint2 acc = make_uint2(0, 0);
+        for (int j = 0; j + 1 < nbands; ++j) {
+            const uint2 v = *reinterpret_cast<const uint2*>(p + j * plane);
+            acc.x += v.x;  // u16 pairs: column counts stay below 2^16 (H < 65536)
+            acc.y += v.y;
+            *reinterpret_cast<uint2*>(p + j * plane) = acc;
+        }
+    }
+}
+
+// One CTA per bin: A[kl][j][s] = sum_{j' <= j} sum_{s' < s} T1[kl][j'][s'], in place.
+__global__ void __launch_bounds__(256) fcarry_corner_kernel(int nstrips, int nbands, uint32_t* __restrict__ T1) {
+    extern __shared__ uint32_t tsm[];
+    const int J = nbands - 1, S = nstrips;
+    uint32_t* t = T1 + static_cast<int64_t>(blockIdx.x) * J * S;
+    for (int i = threadIdx.x; i < J * S; i += blockDim.x) tsm[i] = t[i];
+    __syncthreads();
+    for (int jj = threadIdx.x; jj < J; jj += blockDim.x) {  // exclusive prefix over strips
+        uint32_t run = 0;
+        for (int s = 0; s < S; ++s) {
+            const uint32_t v = tsm[jj * S + s];
+            tsm[jj * S + s] = run;
+            run += v;
+        }
+    }
+    __syncthreads();
+    for (int s = threadIdx.x; s < S; s += blockDim.x) {  // inclusive prefix over bands
+        uint32_t run = 0;
+        for (int jj = 0; jj < J; ++jj) {
+            run += tsm[jj * S + s];
+            t[jj * S + s] = run;
+        }
+    }
+}
+
+}  // namespace spct_carry
+
+namespace spct_impl {
+
+FusedCarryLayout fused_carry_layout(const BuildPlan& p, int height) {
+    FusedCarryLayout L{};
+    const size_t lb = static_cast<size_t>(p.Lb);
+    L.lt_off = 0;
+    L.lt_bytes = p.nstrips > 1 ? round_up(static_cast<int64_t>(p.nstrips) * height * lb * 2, 256) : 0;
+    L.r_off = L.lt_off + L.lt_bytes;
+    L.r_bytes = p.nstrips > 1 ? round_up(static_cast<int64_t>(p.nstrips - 1) * height * lb, 256) : 0;
+    L.c_off = L.r_off + L.r_bytes;
+    L.c_bytes = p.nbands > 1 ? round_up(static_cast<int64_t>(p.nbands - 1) * lb * p.Wp * 2, 256) : 0;
+    L.a_off = L.c_off + L.c_bytes;
+    L.a_bytes = p.nbands > 1 ? round_up(static_cast<int64_t>(p.nbands - 1) * p.nstrips * lb * 4, 256) : 0;
+    L.total = L.a_off + L.a_bytes;
+    return L;
+}
+
+spct_status build_fused_carries(const QuantParams& q, const spct_ih& out, const BuildPlan& p, void* workspace,
+                                size_t ws_bytes, cudaStream_t s, FusedCarries* fc) {
+    *fc = FusedCarries{};
+    const FusedCarryLayout L = fused_carry_layout(p, out.height);
+    if (L.total > 0 && (!workspace || ws_bytes < L.total))
+        return contract("ih_build_match: workspace too small (query spct_cu_ih_build_workspace)");
+    if (L.total == 0) return SPCT_OK;
+    char* ws = static_cast<char*>(workspace);
+    uint8_t* R8 = L.r_bytes ? reinterpret_cast<uint8_t*>(ws + L.r_off) : nullptr;
+    uint16_t* Lt16 = L.lt_bytes ? reinterpret_cast<uint16_t*>(ws + L.lt_off) : nullptr;
+    uint16_t* C16 = L.c_bytes ? reinterpret_cast<uint16_t*>(ws + L.c_off) : nullptr;
+    uint32_t* A32 = L.a_bytes ? reinterpret_cast<uint32_t*>(ws + L.a_off) : nullptr;
+    const size_t smem = (kTileBins * kStrip + 8 * kTileBins) * 4;
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(fcarry_tiles_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaFuncSetAttribute(fcarry_tiles_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        attr = true;
+    }
+    dim3 g(p.nstrips, p.nbands, static_cast<unsigned>(ceil_div(p.Lb, kTileBins)));
+    if (q.kind == SPCT_SRC_GRAY_U8 && q.fast_u8)
+        fcarry_tiles_kernel<true><<<g, 256, smem, s>>>(q, out.bin0, out.bins, p.Lb, p.nstrips, p.nbands, p.band_rows, R8,
+                                                        C16, A32);
+    else
+        fcarry_tiles_kernel<false><<<g, 256, smem, s>>>(q, out.bin0, out.bins, p.Lb, p.nstrips, p.nbands, p.band_rows, R8,
+                                                         C16, A32);
+    if (auto st = launch_status("fcarry_tiles_kernel")) return st;
+    const int nb_lt = Lt16 ? static_cast<int>(ceil_div(static_cast<int64_t>(out.height) * (p.Lb / 4), 256)) : 0;
+    const int nb_c = C16 ? static_cast<int>(ceil_div(static_cast<int64_t>(p.Lb) * p.Wp / 4, 256)) : 0;
+    if (nb_lt + nb_c > 0) {
+        fcarry_prefix_kernel<<<nb_lt + nb_c, 256, 0, s>>>(out.height, p.Lb, p.Wp, p.nstrips, p.nbands, nb_lt, R8, Lt16,
+                                                          C16);
+        if (auto st = launch_status("fcarry_prefix_kernel")) return st;
+    }
+    if (A32) {
+        const size_t tsm = static_cast<size_t>(p.nbands - 1) * p.nstrips * 4;
+        if (tsm > 200 * 1024) return contract("ih_build_match: image too large for the fused carry tables");
+        if (tsm > 48 * 1024)
+            cudaFuncSetAttribute(fcarry_corner_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tsm);
+        fcarry_corner_kernel<<<p.Lb, 256, tsm, s>>>(p.nstrips, p.nbands, A32);
+        if (auto st = launch_status("fcarry_corner_kernel")) return st;
+    }
+    fc->Lt = Lt16;
+    fc->C = C16;
+    fc->A = A32;
+    return SPCT_OK;
+}
+
+}  // namespace spct_impl

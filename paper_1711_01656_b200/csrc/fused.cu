@@ -83,13 +83,14 @@ spct_status build_match(const spct_source* src, const spct_ih* out, const double
         return spct_cu_hist_partial(out, tmpl, kw, kh, p, metric, partial, 0, stream);
     }
     const BuildPlan bp = plan_fused_sweep(out->width, out->height, out->bins);
-    const size_t need = (out->data ? bp.lt_bytes + bp.hb_bytes : 0) + fused_prep_bytes(out->bins);
+    const size_t carry_bytes = out->data ? fused_carry_layout(bp, out->height).total : 0;
+    const size_t need = carry_bytes + fused_prep_bytes(out->bins);
     if (!workspace || workspace_bytes < need) return contract("ih_build_match: workspace too small");
-    uint32_t *Lt = nullptr, *Hb = nullptr;
+    FusedCarries fc{};
     char* ws = static_cast<char*>(workspace);
     if (out->data) {
-        if (auto st = build_carries(q, *out, bp, workspace, workspace_bytes, s, &Lt, &Hb)) return st;
-        ws += bp.lt_bytes + bp.hb_bytes;
+        if (auto st = build_fused_carries(q, *out, bp, workspace, workspace_bytes, s, &fc)) return st;
+        ws += carry_bytes;
     }
     uint32_t* prep = reinterpret_cast<uint32_t*>(ws);
     long long* Sg = reinterpret_cast<long long*>(ws + round_up((static_cast<int64_t>(out->bins) + 1) * 4, 256));
@@ -130,9 +131,9 @@ spct_status build_match(const spct_source* src, const spct_ih* out, const double
         // the group is the whole histogram: window totals over its bins are kw * kh
         const bool allb = out->bin0 == 0 && out->bins == out->nbins_total && ngroups == 1;
         const bool g8 = q.kind == SPCT_SRC_GRAY_U8 && q.fast_u8;
-        if (kw == 64) launch_kw64(allb, g8, grid, s, q, pm, *out, bp, Lt, Hb, f);
-        else if (kw == 128) launch_kw128(allb, g8, grid, s, q, pm, *out, bp, Lt, Hb, f);
-        else launch_kw_any(allb, g8, grid, s, q, pm, *out, bp, Lt, Hb, f);
+        if (kw == 64) launch_kw64(allb, g8, grid, s, q, pm, *out, bp, fc, f);
+        else if (kw == 128) launch_kw128(allb, g8, grid, s, q, pm, *out, bp, fc, f);
+        else launch_kw_any(allb, g8, grid, s, q, pm, *out, bp, fc, f);
         prof_end(prof, s);
         note_launch();
         if (auto st = launch_status("sweep_match_kernel")) return st;

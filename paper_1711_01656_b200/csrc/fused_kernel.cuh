@@ -240,8 +240,7 @@ __device__ __forceinline__ void quarter_reduce(uint32_t (&v)[8], int q) {
 // and quantises without the generic per-kind dispatch.
 template <bool STORE, bool FAST, int KWM, bool ALLB, bool G8>
 __global__ void __launch_bounds__(256, 2) sweep_match_kernel(QuantParams q, PixelMode pm, spct_ih out, int Lb, int Wp,
-                                                             int band_rows, const uint32_t* __restrict__ Lt,
-                                                             const uint32_t* __restrict__ Hb, FusedParams f) {
+                                                             int band_rows, FusedCarries fc, FusedParams f) {
     extern __shared__ uint4 smem_raw[];
     uint32_t* vc = reinterpret_cast<uint32_t*>(smem_raw);                 // [128 bins][144 words], padded
     uint32_t* gbuf = vc + kGroupBins * kVcStride;                           // [8 warps][4][128 words] (general path)
@@ -250,7 +249,8 @@ __global__ void __launch_bounds__(256, 2) sweep_match_kernel(QuantParams q, Pixe
     uint32_t* lrow = srep_s + kGroupBins;                                   // [2 rows][128] row carries
     uint16_t* rowbins = reinterpret_cast<uint16_t*>(lrow + 2 * kGroupBins);  // [2 rows][128] strip bins
     uint32_t* amask = reinterpret_cast<uint32_t*>(rowbins + 2 * kStrip);    // [8 lanes][8 words] anchor masks
-    // integer path: per row parity, warp and window pair, the packed {I, I} sums (and C after them)
+    // integer path: per row parity and window pair, the packed sums over the warps (atomic
+    // adds), I at [parity][64] and C at 128 + [parity][64]
     uint32_t* red32 = reinterpret_cast<uint32_t*>(red);
 
     // Both variants are launched; the one that does not match the template prep exits.
@@ -280,6 +280,7 @@ __global__ void __launch_bounds__(256, 2) sweep_match_kernel(QuantParams q, Pixe
     };
 
     for (int i = tid; i < kGroupBins * kVcStride; i += blockDim.x) vc[i] = 0;
+    if (FAST) red32[tid] = 0;  // row accumulators {I} [2][64] and {C} [2][64]
     if (tid < kGroupBins) srep_s[tid] = (FAST && tid < nb_cta) ? __ldg(f.prep + 1 + g0 + tid) : 0u;
     if (FAST && KWM == 0 && tid < 64) {
         // anchor masks: u16 i of lane m's word j is valid iff 16m + 2j + i < kw
@@ -288,7 +289,28 @@ __global__ void __launch_bounds__(256, 2) sweep_match_kernel(QuantParams q, Pixe
     }
 
     uint32_t V[4][kB];
-    if (STORE && warp_live) vpart_init<kB>(V, Hb, band, Lb, kl0, Wp, xl);
+    if (STORE && warp_live) {
+        // H(y0, x + 1, k) above the band: the corner sum A (rows < y0, columns left of the
+        // strip) plus the prefix along the strip of the column counts C
+        if (band > 0 && fc.C) {
+            const uint16_t* cb = fc.C + (static_cast<int64_t>(band - 1) * Lb + kl0) * Wp + xl;
+            const uint32_t* ab = fc.A + (static_cast<int64_t>(kl0) * (gridDim.y - 1) + band - 1) * gridDim.x + strip;
+#pragma unroll
+            for (int k = 0; k < kB; ++k) {
+                const uint2 c = *reinterpret_cast<const uint2*>(cb + static_cast<int64_t>(k) * Wp);
+                const uint32_t p0 = c.x & 0xFFFFu, p1 = p0 + (c.x >> 16), p2 = p1 + (c.y & 0xFFFFu), p3 = p2 + (c.y >> 16);
+                const uint32_t base = __ldg(ab + static_cast<int64_t>(k) * (gridDim.y - 1) * gridDim.x) +
+                                      warp_incl_scan(p3) - p3;
+                V[0][k] = base + p0;
+                V[1][k] = base + p1;
+                V[2][k] = base + p2;
+                V[3][k] = base + p3;
+            }
+        } else {
+#pragma unroll
+            for (int k = 0; k < kB; ++k) V[0][k] = V[1][k] = V[2][k] = V[3][k] = 0;
+        }
+    }
     uint32_t* base_ptr = STORE ? out.data + static_cast<int64_t>(kl0) * out.plane_pitch + xl : nullptr;
     const bool lane_live = xl < out.row_pitch;
     const uint32_t store_mask = lane_live ? (k_live >= 32 ? 0xFFFFFFFFu : (1u << max(k_live, 0)) - 1u) : 0u;
@@ -310,13 +332,13 @@ __global__ void __launch_bounds__(256, 2) sweep_match_kernel(QuantParams q, Pixe
     const bool xt_live = xt >= 0 && xt < W;
     const int vcol_w = vcw(tid >> 1);        // the staging column's (padded) vc word
     const uint32_t vinc = 1u << (16 * (tid & 1));
-    const uint32_t* lt_cta = (STORE && Lt && strip > 0 && tid < kGroupBins && g0 + tid < Lb)
-                                 ? Lt + static_cast<int64_t>(strip) * H * Lb + g0 + tid
+    const uint16_t* lt_cta = (STORE && fc.Lt && strip > 0 && tid < kGroupBins && g0 + tid < Lb)
+                                 ? fc.Lt + static_cast<int64_t>(strip) * H * Lb + g0 + tid
                                  : nullptr;
     // raw pixel values of the staging column, quantised one row after the load
     uint64_t rn = xt_live ? raw_at(xt, y0) : 0, ro = 0;
     bool have_o = false;  // y0 - kh < ystart: nothing to remove on the first row
-    uint32_t lpre = lt_cta ? __ldg(lt_cta + static_cast<int64_t>(y0) * Lb) : 0u;
+    uint32_t lpre = lt_cta ? static_cast<uint32_t>(__ldg(lt_cta + static_cast<int64_t>(y0) * Lb)) : 0u;
     __syncthreads();  // vc zeroed
 
     // Pre-roll rows [ystart, y0) only feed vc, and nothing leaves the window there: one
@@ -346,15 +368,16 @@ __global__ void __launch_bounds__(256, 2) sweep_match_kernel(QuantParams q, Pixe
             const int t = tid;
             double term = 0.0;
             if (FAST) {
-                // packed window pairs; every sum stays below 2^16 (at most kw * kh)
-                const uint32_t* rw = red32 + (yy & 1) * (kWarps * 64) + (t >> 1);
-                uint32_t xi = 0, xc = 0;
-#pragma unroll
-                for (int w = 0; w < kWarps; ++w)
-                    if (w < nwarps_live) {
-                        xi += rw[w * 64];
-                        if (!ALLB) xc += rw[2 * kWarps * 64 + w * 64];
-                    }
+                // the warps' packed window-pair sums, accumulated in shared memory; every
+                // sum stays below 2^16 (at most kw * kh).  Read, then clear for row yy + 2.
+                uint32_t* ai = red32 + (yy & 1) * 64 + (t >> 1);
+                const uint32_t xi = *ai;
+                const uint32_t xc = ALLB ? 0u : ai[128];
+                __syncwarp();
+                if (!(t & 1)) {
+                    *ai = 0;
+                    if (!ALLB) ai[128] = 0;
+                }
                 const long long I = (xi >> (16 * (t & 1))) & 0xFFFFu;
                 const long long C = ALLB ? static_cast<long long>(f.kw) * f.kh : (xc >> (16 * (t & 1))) & 0xFFFFu;
                 term = f.metric == SPCT_METRIC_INTERSECTION ? static_cast<double>(I) * f.invT
@@ -493,11 +516,13 @@ __global__ void __launch_bounds__(256, 2) sweep_match_kernel(QuantParams q, Pixe
                 // the quarters hold the same 16 windows per lane for different bins
                 quarter_reduce(Iw, qq);
                 const int jb = 4 * (qq >> 1) + 2 * (qq & 1);
-                uint32_t* rw = red32 + (y & 1) * (kWarps * 64) + warp * 64 + 8 * mq + jb;
-                *reinterpret_cast<uint2*>(rw) = make_uint2(Iw[0], Iw[1]);
+                uint32_t* rw = red32 + (y & 1) * 64 + 8 * mq + jb;
+                atomicAdd(rw, Iw[0]);
+                atomicAdd(rw + 1, Iw[1]);
                 if (!ALLB) {
                     quarter_reduce(Cw, qq);
-                    *reinterpret_cast<uint2*>(rw + 2 * kWarps * 64) = make_uint2(Cw[0], Cw[1]);
+                    atomicAdd(rw + 128, Cw[0]);
+                    atomicAdd(rw + 129, Cw[1]);
                 }
             } else {
                 double* rb = red + (y & 1) * (kWarps * kStrip) + warp * kStrip;
@@ -519,7 +544,7 @@ constexpr size_t kSmemBytes = (size_t(kGroupBins) * kVcStride + size_t(kWarps) *
 
 template <int KWM, bool ALLB, bool G8>
 void launch_variants(dim3 grid, cudaStream_t s, const QuantParams& q, const PixelMode& pm, const spct_ih& out,
-                     const BuildPlan& bp, const uint32_t* Lt, const uint32_t* Hb, const FusedParams& f) {
+                     const BuildPlan& bp, const FusedCarries& fc, const FusedParams& f) {
     static bool attr_set = false;
     if (!attr_set) {
         cudaFuncSetAttribute(sweep_match_kernel<true, true, KWM, ALLB, G8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBytes);
@@ -531,23 +556,23 @@ void launch_variants(dim3 grid, cudaStream_t s, const QuantParams& q, const Pixe
     // integer (template-crop) variant and FP64 variant: the one not selected by the
     // device-side template prep exits on entry
     if (out.data) {
-        sweep_match_kernel<true, true, KWM, ALLB, G8><<<grid, 256, kSmemBytes, s>>>(q, pm, out, bp.Lb, bp.Wp, bp.band_rows, Lt, Hb, f);
-        sweep_match_kernel<true, false, KWM, false, G8><<<grid, 256, kSmemBytes, s>>>(q, pm, out, bp.Lb, bp.Wp, bp.band_rows, Lt, Hb, f);
+        sweep_match_kernel<true, true, KWM, ALLB, G8><<<grid, 256, kSmemBytes, s>>>(q, pm, out, bp.Lb, bp.Wp, bp.band_rows, fc, f);
+        sweep_match_kernel<true, false, KWM, false, G8><<<grid, 256, kSmemBytes, s>>>(q, pm, out, bp.Lb, bp.Wp, bp.band_rows, fc, f);
     } else {
-        sweep_match_kernel<false, true, KWM, ALLB, G8><<<grid, 256, kSmemBytes, s>>>(q, pm, out, bp.Lb, bp.Wp, bp.band_rows, nullptr, nullptr, f);
-        sweep_match_kernel<false, false, KWM, false, G8><<<grid, 256, kSmemBytes, s>>>(q, pm, out, bp.Lb, bp.Wp, bp.band_rows, nullptr, nullptr, f);
+        sweep_match_kernel<false, true, KWM, ALLB, G8><<<grid, 256, kSmemBytes, s>>>(q, pm, out, bp.Lb, bp.Wp, bp.band_rows, FusedCarries{}, f);
+        sweep_match_kernel<false, false, KWM, false, G8><<<grid, 256, kSmemBytes, s>>>(q, pm, out, bp.Lb, bp.Wp, bp.band_rows, FusedCarries{}, f);
     }
 }
 
 template <int KWM>
 void launch_kw_impl(bool allb, bool g8, dim3 grid, cudaStream_t s, const QuantParams& q, const PixelMode& pm,
-                    const spct_ih& out, const BuildPlan& bp, const uint32_t* Lt, const uint32_t* Hb, const FusedParams& f) {
+                    const spct_ih& out, const BuildPlan& bp, const FusedCarries& fc, const FusedParams& f) {
     if (g8) {
-        if (allb) launch_variants<KWM, true, true>(grid, s, q, pm, out, bp, Lt, Hb, f);
-        else launch_variants<KWM, false, true>(grid, s, q, pm, out, bp, Lt, Hb, f);
+        if (allb) launch_variants<KWM, true, true>(grid, s, q, pm, out, bp, fc, f);
+        else launch_variants<KWM, false, true>(grid, s, q, pm, out, bp, fc, f);
     } else {
-        if (allb) launch_variants<KWM, true, false>(grid, s, q, pm, out, bp, Lt, Hb, f);
-        else launch_variants<KWM, false, false>(grid, s, q, pm, out, bp, Lt, Hb, f);
+        if (allb) launch_variants<KWM, true, false>(grid, s, q, pm, out, bp, fc, f);
+        else launch_variants<KWM, false, false>(grid, s, q, pm, out, bp, fc, f);
     }
 }
 
@@ -558,7 +583,7 @@ namespace spct_fused {
 // kernel variants compile in parallel.
 #define SPCT_FUSED_LAUNCHER(NAME)                                                                              \
     void NAME(bool allb, bool g8, dim3 grid, cudaStream_t s, const QuantParams& q, const PixelMode& pm,       \
-              const spct_ih& out, const BuildPlan& bp, const uint32_t* Lt, const uint32_t* Hb, const FusedParams& f);
+              const spct_ih& out, const BuildPlan& bp, const FusedCarries& fc, const FusedParams& f);
 SPCT_FUSED_LAUNCHER(launch_kw64)
 SPCT_FUSED_LAUNCHER(launch_kw128)
 SPCT_FUSED_LAUNCHER(launch_kw_any)

@@ -4,8 +4,8 @@
 
 namespace spct_fused {
 void launch_kw64(bool allb, bool g8, dim3 grid, cudaStream_t s, const QuantParams& q, const PixelMode& pm, const spct_ih& out,
-          const BuildPlan& bp, const uint32_t* Lt, const uint32_t* Hb, const FusedParams& f) {
-    launch_kw_impl<64>(allb, g8, grid, s, q, pm, out, bp, Lt, Hb, f);
+          const BuildPlan& bp, const FusedCarries& fc, const FusedParams& f) {
+    launch_kw_impl<64>(allb, g8, grid, s, q, pm, out, bp, fc, f);
 }
 size_t smem_bytes() { return kSmemBytes; }
 }  // namespace spct_fused

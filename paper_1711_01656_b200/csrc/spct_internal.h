@@ -77,4 +77,18 @@ size_t fused_prep_bytes(int bins);
 spct_status build_carries(const spct_dev::QuantParams& q, const spct_ih& out, const BuildPlan& p, void* workspace,
                           size_t ws_bytes, cudaStream_t s, uint32_t** Lt, uint32_t** Hb);
 
+// Carry tables of the fused build+match sweep (carries.cu): row carries (u16), column
+// counts above each band boundary (u16) and the band x strip corner sums (u32).
+struct FusedCarries {
+    const uint16_t* Lt;  // [nstrips][H][Lb]        (strip 0 unused)
+    const uint16_t* C;   // [nbands - 1][Lb][Wp]
+    const uint32_t* A;   // [Lb][nbands - 1][nstrips]
+};
+struct FusedCarryLayout {
+    size_t lt_off, lt_bytes, r_off, r_bytes, c_off, c_bytes, a_off, a_bytes, total;
+};
+FusedCarryLayout fused_carry_layout(const BuildPlan& p, int height);
+spct_status build_fused_carries(const spct_dev::QuantParams& q, const spct_ih& out, const BuildPlan& p,
+                                void* workspace, size_t ws_bytes, cudaStream_t s, FusedCarries* fc);
+
 }  // namespace spct_impl
