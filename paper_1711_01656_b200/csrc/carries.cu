@@ -206,23 +206,24 @@ __global__ void __launch_bounds__(256) fcarry_tiles_kernel(QuantParams q, int bi
     const int x = s * kStrip + 4 * lane;
     const int klo = bin0 + kc0, khi = min(kcn, bins - kc0);
     uint32_t* rw = rh + warp * kTileBins;
-    for (int y = y0 + warp; y < y1; y += 8) {
-        int b[4];
-        if (G8 && x + 3 < q.width &&
-            ((reinterpret_cast<uintptr_t>(q.p0) + static_cast<int64_t>(y) * q.pitch + x) & 3) == 0) {
-            const uint32_t w = __ldg(reinterpret_cast<const uint32_t*>(static_cast<const uint8_t*>(q.p0) +
-                                                                        static_cast<int64_t>(y) * q.pitch + x));
+    // column 4 lane + c of the strip is counted at c * 32 + lane (conflict-free atomics)
+    const bool wide = G8 && x + 3 < q.width &&
+                      ((reinterpret_cast<uintptr_t>(q.p0) + x) & 3) == 0 && (q.pitch & 3) == 0;
+    auto bins4 = [&](int y, uint32_t w, int (&b)[4]) {
+        if (wide) {
 #pragma unroll
             for (int c = 0; c < 4; ++c) b[c] = static_cast<int>((((w >> (8 * c)) & 0xFFu) * q.nbins) >> 8);
         } else {
 #pragma unroll
             for (int c = 0; c < 4; ++c) b[c] = x + c < q.width ? pixel_bin(q, x + c, y) : -1;
         }
+    };
+    auto count_row = [&](int y, const int (&b)[4]) {
 #pragma unroll
         for (int c = 0; c < 4; ++c) {
             const int k = b[c] - klo;
             if (b[c] >= 0 && static_cast<unsigned>(k) < static_cast<unsigned>(khi)) {
-                if (need_c) atomicAdd(&cnt[k * kStrip + 4 * lane + c], 1u);
+                if (need_c) atomicAdd(&cnt[k * kStrip + c * 32 + lane], 1u);
                 if (need_r) atomicAdd(&rw[k], 1u);
             }
         }
@@ -236,19 +237,43 @@ __global__ void __launch_bounds__(256) fcarry_tiles_kernel(QuantParams q, int bi
             }
             __syncwarp();
         }
+    };
+    // rows y0 + warp + 8 i; the 8-bit gray words of four rows are loaded before any is counted
+    const uint8_t* colp = static_cast<const uint8_t*>(q.p0) + x;
+    int y = y0 + warp;
+    for (; y + 24 < y1; y += 32) {
+        uint32_t w[4] = {0, 0, 0, 0};
+        if (wide) {
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+                w[u] = __ldg(reinterpret_cast<const uint32_t*>(colp + static_cast<int64_t>(y + 8 * u) * q.pitch));
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            int b[4];
+            bins4(y + 8 * u, w[u], b);
+            count_row(y + 8 * u, b);
+        }
+    }
+    for (; y < y1; y += 8) {
+        const uint32_t w = wide ? __ldg(reinterpret_cast<const uint32_t*>(colp + static_cast<int64_t>(y) * q.pitch)) : 0u;
+        int b[4];
+        bins4(y, w, b);
+        count_row(y, b);
     }
     if (!need_c) return;
     __syncthreads();
     const int Wp = nstrips * kStrip;
-    for (int i = tid; i < kcn * (kStrip / 2); i += 256) {
-        const int k = i / (kStrip / 2), c2 = 2 * (i % (kStrip / 2));
-        const uint32_t v = cnt[k * kStrip + c2] | (cnt[k * kStrip + c2 + 1] << 16);
-        *reinterpret_cast<uint32_t*>(C16 + (static_cast<int64_t>(j) * Lb + kc0 + k) * Wp + s * kStrip + c2) = v;
+    for (int i = tid; i < kcn * (kStrip / 4); i += 256) {
+        const int k = i / (kStrip / 4), l = i % (kStrip / 4);  // columns 4 l .. 4 l + 3
+        const uint32_t* ck = cnt + k * kStrip + l;
+        const uint2 v = make_uint2(ck[0] | (ck[32] << 16), ck[64] | (ck[96] << 16));
+        *reinterpret_cast<uint2*>(C16 + (static_cast<int64_t>(j) * Lb + kc0 + k) * Wp + s * kStrip + 4 * l) = v;
     }
     // band x strip totals, [kl][j][s]
     for (int k = warp; k < kcn; k += 8) {
-        const uint4 v = *reinterpret_cast<const uint4*>(cnt + k * kStrip + 4 * lane);
-        uint32_t t = v.x + v.y + v.z + v.w;
+        const uint32_t* ck = cnt + k * kStrip + lane;
+        uint32_t t = ck[0] + ck[32] + ck[64] + ck[96];
 #pragma unroll
         for (int o = 16; o; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
         if (lane == 0) T1[(static_cast<int64_t>(kc0 + k) * (nbands - 1) + j) * nstrips + s] = t;
@@ -267,11 +292,19 @@ __global__ void __launch_bounds__(256) fcarry_prefix_kernel(int H, int Lb, int W
         const int64_t off = (i / quads) * Lb + 4 * (i % quads);
         const int64_t sstride = static_cast<int64_t>(H) * Lb;
         uint32_t a0 = 0, a1 = 0;  // u16 pairs: bins {0,1}, {2,3}
-        for (int s = 0; s + 1 < nstrips; ++s) {
-            const uint32_t v = __ldg(reinterpret_cast<const uint32_t*>(R8 + s * sstride + off));
-            a0 += __byte_perm(v, 0, 0x4140);  // {b0, b1} as u16 pair
-            a1 += __byte_perm(v, 0, 0x4342);
-            *reinterpret_cast<uint2*>(Lt16 + (s + 1) * sstride + off) = make_uint2(a0, a1);
+        constexpr int U = 8;       // loads in flight
+        for (int s0 = 0; s0 + 1 < nstrips; s0 += U) {
+            uint32_t v[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u)
+                v[u] = s0 + u + 1 < nstrips ? __ldg(reinterpret_cast<const uint32_t*>(R8 + (s0 + u) * sstride + off)) : 0u;
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                if (s0 + u + 1 >= nstrips) break;
+                a0 += __byte_perm(v[u], 0, 0x4140);  // {b0, b1} as u16 pair
+                a1 += __byte_perm(v[u], 0, 0x4342);
+                *reinterpret_cast<uint2*>(Lt16 + (s0 + u + 1) * sstride + off) = make_uint2(a0, a1);
+            }
         }
     } else {
         const int64_t i = static_cast<int64_t>(blockIdx.x - nb_lt) * 256 + threadIdx.x;  // (bin, quad)
@@ -279,11 +312,19 @@ __global__ void __launch_bounds__(256) fcarry_prefix_kernel(int H, int Lb, int W
         if (i >= plane / 4) return;
         uint16_t* p = C16 + 4 * i;
         uint2 acc = make_uint2(0, 0);
-        for (int j = 0; j + 1 < nbands; ++j) {
-            const uint2 v = *reinterpret_cast<const uint2*>(p + j * plane);
-            acc.x += v.x;  // u16 pairs: column counts stay below 2^16 (H < 65536)
-            acc.y += v.y;
-            *reinterpret_cast<uint2*>(p + j * plane) = acc;
+        constexpr int U = 8;  // loads in flight
+        for (int j0 = 0; j0 + 1 < nbands; j0 += U) {
+            uint2 v[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u)
+                v[u] = j0 + u + 1 < nbands ? *reinterpret_cast<const uint2*>(p + (j0 + u) * plane) : make_uint2(0, 0);
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                if (j0 + u + 1 >= nbands) break;
+                acc.x += v[u].x;  // u16 pairs: column counts stay below 2^16 (H < 65536)
+                acc.y += v[u].y;
+                *reinterpret_cast<uint2*>(p + (j0 + u) * plane) = acc;
+            }
         }
     }
 }

@@ -94,7 +94,9 @@ spct_status build_match(const spct_source* src, const spct_ih* out, const double
     }
     uint32_t* prep = reinterpret_cast<uint32_t*>(ws);
     long long* Sg = reinterpret_cast<long long*>(ws + round_up((static_cast<int64_t>(out->bins) + 1) * 4, 256));
-    const int fast_metric = (metric == SPCT_METRIC_MINKOWSKI && p == 1.0) || metric == SPCT_METRIC_INTERSECTION;
+    // the integer path's signed 16-bit min needs kw * kh <= 24576 (fused_kernel.cuh)
+    const int fast_metric = ((metric == SPCT_METRIC_MINKOWSKI && p == 1.0) || metric == SPCT_METRIC_INTERSECTION) &&
+                            T <= 24576;
     prep_kernel<<<1, 256, 0, s>>>(tmpl, out->bin0, out->bins, static_cast<double>(T), fast_metric, prep, Sg, ngroups);
     if (auto st = launch_status("prep_kernel")) return st;
 

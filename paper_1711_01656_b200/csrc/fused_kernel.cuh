@@ -76,6 +76,12 @@ __device__ __forceinline__ uint32_t min_u16x2(uint32_t a, uint32_t b) {
     return r;
 }
 
+__device__ __forceinline__ uint32_t min_s16x2(uint32_t a, uint32_t b) {
+    uint32_t r;
+    asm("min.s16x2 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(b));
+    return r;
+}
+
 // Per-bin term of the general path (same arithmetic as hist_match.cu bin_term).
 __device__ __forceinline__ double general_term(uint32_t c, double t, const FusedParams& f) {
     const double cd = static_cast<double>(c);
@@ -167,12 +173,13 @@ __device__ __forceinline__ uint32_t scan_add8(uint32_t v, int o) {
 // a word's high half is exact; the same offset per lane is removed once, with the anchor,
 // where the true counts 0 <= c <= kw*kh < 2^16 make the packed pairs exact.  One 8-lane
 // scan of {anchor partial, lane prefix total} per bin: 3 shuffle steps + 1 broadcast.
-// Result: c[j] = {c(16m + 2j), c(16m + 2j + 1)} packed u16 pairs.
+// Result: the window counts c(16m + 2j + h) = w[j].half(h) + off, with w[j] packed u16 pairs
+// in [0, 8160] and `off` the lane's (signed) offset.
 // pb: the lane's strip quad (word 64 + 8m, padded); the vc(e - kw) quads of kw = 64 / 128
 // are at fixed offsets from it; the general kw reads 9 words from `vrow`.
 template <int KWM>
 __device__ __forceinline__ void window_counts_q(const uint32_t* pb, const uint32_t* vrow, int m, int aw0, int apsh,
-                                                const uint32_t* amask, uint32_t (&c)[8]) {
+                                                const uint32_t* amask, uint32_t (&w)[8], int& off) {
     uint32_t b[8], a[8];
     {
         const uint4 x = *reinterpret_cast<const uint4*>(pb), y = *reinterpret_cast<const uint4*>(pb + 4);
@@ -189,7 +196,6 @@ __device__ __forceinline__ void window_counts_q(const uint32_t* pb, const uint32
 #pragma unroll
         for (int j = 0; j < 8; ++j) a[j] = __funnelshift_r(r[j], r[j + 1], apsh);
     }
-    uint32_t w[8];
 #pragma unroll
     for (int j = 0; j < 8; ++j) {
         const uint32_t d = b[j] - a[j];  // {delta, delta} pair, linear encoding
@@ -210,10 +216,7 @@ __device__ __forceinline__ void window_counts_q(const uint32_t* pb, const uint32
 #pragma unroll
     for (int o = 1; o < 8; o <<= 1) inc = scan_add8(inc, o);
     const uint32_t tot = __shfl_sync(0xffffffffu, inc, 7, 8);
-    const uint32_t s = (tot & 0xFFFFu) + ((inc - pack) >> 16) - 4080u * static_cast<uint32_t>(m + 1);
-    const uint32_t S2 = s * 0x10001u;
-#pragma unroll
-    for (int j = 0; j < 8; ++j) c[j] = w[j] + S2;
+    off = static_cast<int>((tot & 0xFFFFu) + ((inc - pack) >> 16)) - 4080 * (m + 1);
 }
 
 // Cross-quarter reduce-scatter of 8 packed words: afterwards lane (q, m) holds in v[0..1]
@@ -461,6 +464,7 @@ __global__ void __launch_bounds__(256, 2) sweep_match_kernel(QuantParams q, Pixe
         uint32_t* prow = STORE ? base_ptr + static_cast<int64_t>(y) * out.row_pitch : nullptr;
 
         uint32_t Iw[8] = {0, 0, 0, 0, 0, 0, 0, 0}, Cw[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+        int Ioff = 0, Coff = 0;  // per-lane offsets summed over the lane's bins (integer path)
         double acc[4] = {0.0, 0.0, 0.0, 0.0};
 #pragma unroll
         for (int g = 0; g < kB / 4; ++g) {
@@ -468,14 +472,21 @@ __global__ void __launch_bounds__(256, 2) sweep_match_kernel(QuantParams q, Pixe
                 vpart_group_q<kB>(V, g, t4, lr[g], prow + static_cast<int64_t>(4 * g) * out.plane_pitch, out.plane_pitch,
                                   store_mask);
             if (FAST && match_row) {
-                uint32_t c[8];
+                uint32_t w[8];
+                int off;
                 const int go = 4 * g * kVcStride;
-                window_counts_q<KWM>(pb + go, vq + go, mq, aw0, apsh, amask, c);
-                const uint32_t sk = srep_s[warp * kB + 4 * g + qq];
+                window_counts_q<KWM>(pb + go, vq + go, mq, aw0, apsh, amask, w, off);
+                const int sk = static_cast<int>(srep_s[warp * kB + 4 * g + qq] & 0xFFFFu);
+                // min(w + off, s_k) = min(w, s_k - off) + off in signed 16-bit halves: the
+                // integer path runs only for kw * kh <= 24576, so -32768 <= s_k - off <= 32767
+                const uint32_t thr = static_cast<uint32_t>((sk - off) & 0xFFFF) * 0x10001u;
 #pragma unroll
-                for (int j = 0; j < 8; ++j) {
-                    Iw[j] += min_u16x2(c[j], sk);
-                    if (!ALLB) Cw[j] += c[j];
+                for (int j = 0; j < 8; ++j) Iw[j] += min_s16x2(w[j], thr);
+                Ioff += off;
+                if (!ALLB) {
+#pragma unroll
+                    for (int j = 0; j < 8; ++j) Cw[j] += w[j];
+                    Coff += off;
                 }
             } else if (match_row) {
                 uint32_t aw[4][2], bw[4][2];
@@ -514,6 +525,11 @@ __global__ void __launch_bounds__(256, 2) sweep_match_kernel(QuantParams q, Pixe
         if (match_row) {
             if (FAST) {
                 // the quarters hold the same 16 windows per lane for different bins
+#pragma unroll
+                for (int j = 0; j < 8; ++j) {
+                    Iw[j] += static_cast<uint32_t>(Ioff) * 0x10001u;
+                    if (!ALLB) Cw[j] += static_cast<uint32_t>(Coff) * 0x10001u;
+                }
                 quarter_reduce(Iw, qq);
                 const int jb = 4 * (qq >> 1) + 2 * (qq & 1);
                 uint32_t* rw = red32 + (y & 1) * 64 + 8 * mq + jb;

@@ -215,15 +215,17 @@ __device__ __forceinline__ void vpart_group_q(uint32_t (&V)[4][B], int g, const 
         Q[j] = j ? Q[j - 1] + m : m;
     }
     const uint32_t excl = warp_incl_scan(Q[3]) - Q[3];
+    // bytes of Q + excl stay <= 128: the exclusive count folds in before the extraction
+#pragma unroll
+    for (int j = 0; j < 4; ++j) Q[j] += excl;
     const uint32_t Lk[4] = {L.x, L.y, L.z, L.w};
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
         const int k = 4 * g + i;
-        const uint32_t base = Lk[i] + __byte_perm(excl, 0, 0x4440 + i);
-        V[0][k] += base + __byte_perm(Q[0], 0, 0x4440 + i);
-        V[1][k] += base + __byte_perm(Q[1], 0, 0x4440 + i);
-        V[2][k] += base + __byte_perm(Q[2], 0, 0x4440 + i);
-        V[3][k] += base + __byte_perm(Q[3], 0, 0x4440 + i);
+        V[0][k] += Lk[i] + __byte_perm(Q[0], 0, 0x4440 + i);
+        V[1][k] += Lk[i] + __byte_perm(Q[1], 0, 0x4440 + i);
+        V[2][k] += Lk[i] + __byte_perm(Q[2], 0, 0x4440 + i);
+        V[3][k] += Lk[i] + __byte_perm(Q[3], 0, 0x4440 + i);
         st_cs_v4_pred(store_mask & (1u << k), p, V[0][k], V[1][k], V[2][k], V[3][k]);
         p += plane_pitch;
     }

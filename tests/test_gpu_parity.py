@@ -276,7 +276,9 @@ def _crop_template(qb, bins, x0, y0, kw, kh):
 
 FUSED_CASES = [  # w, h, bins, kw, kh
     (333, 211, 48, 64, 64), (130, 67, 9, 13, 11), (257, 140, 130, 64, 64), (300, 200, 128, 128, 100),
-    (97, 301, 20, 1, 1), (128, 128, 16, 127, 5), (45, 33, 7, 45, 33), (700, 90, 256, 31, 17), (520, 260, 33, 65, 3)]
+    (97, 301, 20, 1, 1), (128, 128, 16, 127, 5), (45, 33, 7, 45, 33), (700, 90, 256, 31, 17), (520, 260, 33, 65, 3),
+    # kw * kh > 24576: the unsigned 16-bit window-count path (kw = 128 and a general kw)
+    (260, 300, 24, 128, 255), (310, 280, 40, 100, 250)]
 
 
 @pytest.mark.parametrize("w,h,bins,kw,kh", FUSED_CASES)

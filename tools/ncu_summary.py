@@ -2,12 +2,14 @@
 import csv, subprocess, sys, io
 
 rep = sys.argv[1]
+kid = int(sys.argv[3]) if len(sys.argv) > 3 else 0
 def page(*a):
     out = subprocess.run(["ncu", "-i", rep, *a, "--csv"], capture_output=True, text=True).stdout
     return list(csv.reader(io.StringIO(out)))
 
 raw = page("--page", "raw")
-h, v = raw[0], raw[2]
+h, v = raw[0], raw[2 + kid]
+print("kernel:", v[h.index("Kernel Name")][:100])
 d = dict(zip(h, v))
 keys = ["gpu__time_duration.sum", "smsp__inst_executed.sum", "sm__inst_executed.avg.per_cycle_active",
         "smsp__issue_active.avg.pct_of_peak_sustained_active", "dram__bytes_read.sum", "dram__bytes_write.sum",
