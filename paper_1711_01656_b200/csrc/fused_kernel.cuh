@@ -363,49 +363,67 @@ __global__ void __launch_bounds__(256, 2) sweep_match_kernel(QuantParams q, Pixe
         }
     }
 
-    // Cross-warp combine of row yy: thread t < 128 sums the 8 warps' partials of the
-    // window ending at strip column t in a fixed order.  (Spreading it over all 8 warps
-    // was measured slower: every warp then carries the combine's latency.)
+    // Cross-warp combine of row yy: thread t < 128 finishes the window ending at strip
+    // column t.  Integer path with a finished map (ALLB): L = alpha + beta I (one FMA).
+    const bool intersect = f.metric == SPCT_METRIC_INTERSECTION;
+    const double lin_b = f.invT;
+    const double lin_a = intersect ? 0.0 : 1.0 - static_cast<double>(static_cast<long long>(f.kw) * f.kh + S) * f.invT * 0.5;
+    auto write_map = [&](int u, int v, double L) {
+        // spread_valid's border replication (likelihood.cpp:44-58)
+        const int x = u + (f.kw - 1) / 2, yc = v + (f.kh - 1) / 2;
+        if (u > 0 && u < f.nu - 1 && v > 0 && v < f.nv - 1) {
+            f.map[static_cast<int64_t>(yc) * f.W + x] = L;
+            return;
+        }
+        const int xa = u == 0 ? 0 : x, xb = u == f.nu - 1 ? f.W - 1 : x;
+        const int ya = v == 0 ? 0 : yc, yb = v == f.nv - 1 ? f.H - 1 : yc;
+        for (int yy = ya; yy <= yb; ++yy)
+            for (int xx = xa; xx <= xb; ++xx) f.map[static_cast<int64_t>(yy) * f.W + xx] = L;
+    };
     auto combine = [&](int yy) {
-        if (tid < kStrip) {
-            const int t = tid;
-            double term = 0.0;
-            if (FAST) {
-                // the warps' packed window-pair sums, accumulated in shared memory; every
-                // sum stays below 2^16 (at most kw * kh).  Read, then clear for row yy + 2.
-                uint32_t* ai = red32 + (yy & 1) * 64 + (t >> 1);
-                const uint32_t xi = *ai;
-                const uint32_t xc = ALLB ? 0u : ai[128];
-                __syncwarp();
-                if (!(t & 1)) {
-                    *ai = 0;
-                    if (!ALLB) ai[128] = 0;
-                }
-                const long long I = (xi >> (16 * (t & 1))) & 0xFFFFu;
-                const long long C = ALLB ? static_cast<long long>(f.kw) * f.kh : (xc >> (16 * (t & 1))) & 0xFFFFu;
-                term = f.metric == SPCT_METRIC_INTERSECTION ? static_cast<double>(I) * f.invT
-                                                            : static_cast<double>(C + S - 2 * I) * f.invT;
-            } else {
-                const double* rb = red + (yy & 1) * (kWarps * kStrip);
-#pragma unroll
-                for (int w = 0; w < kWarps; ++w)
-                    if (w < nwarps_live) term = __dadd_rn(term, rb[w * kStrip + t]);
+        if (tid >= kStrip) return;
+        const int t = tid;
+        const int e = xs + t;
+        const int u = e - f.kw + 1, v = yy - f.kh + 1;
+        if (FAST) {
+            // the warps' packed window-pair sums, accumulated in shared memory; every
+            // sum stays below 2^16 (at most kw * kh).  Read, then clear for row yy + 2.
+            uint32_t* ai = red32 + (yy & 1) * 64 + (t >> 1);
+            const uint32_t xi = *ai;
+            const uint32_t xc = ALLB ? 0u : ai[128];
+            __syncwarp();
+            if (!(t & 1)) {
+                *ai = 0;
+                if (!ALLB) ai[128] = 0;
             }
-            const int e = xs + t;
-            const int u = e - f.kw + 1, v = yy - f.kh + 1;
-            if (u >= 0 && e < W) {
-                if (f.map) {
-                    // finished map with spread_valid's border replication (likelihood.cpp:44-58)
-                    const double L = finalize_L(term, f);
-                    const int x = u + (f.kw - 1) / 2, yc = v + (f.kh - 1) / 2;
-                    const int xa = u == 0 ? 0 : x, xb = u == f.nu - 1 ? f.W - 1 : x;
-                    const int ya = v == 0 ? 0 : yc, yb = v == f.nv - 1 ? f.H - 1 : yc;
-                    for (int yy = ya; yy <= yb; ++yy)
-                        for (int xx = xa; xx <= xb; ++xx) f.map[static_cast<int64_t>(yy) * f.W + xx] = L;
-                } else {
-                    double* dst = f.partial + static_cast<int64_t>(v) * f.nu + u;
-                    *dst = f.accumulate ? __dadd_rn(*dst, term) : term;
-                }
+            if (u < 0 || e >= W) return;
+            const uint32_t I = (xi >> (16 * (t & 1))) & 0xFFFFu;
+            if (ALLB && f.map) {
+                const double L = fma(lin_b, static_cast<double>(I), lin_a);
+                write_map(u, v, fmin(fmax(L, 0.0), 1.0));
+                return;
+            }
+            const long long C = ALLB ? static_cast<long long>(f.kw) * f.kh : (xc >> (16 * (t & 1))) & 0xFFFFu;
+            const double term = intersect ? static_cast<double>(I) * f.invT
+                                          : static_cast<double>(C + S - 2 * static_cast<long long>(I)) * f.invT;
+            if (f.map) {
+                write_map(u, v, finalize_L(term, f));
+            } else {
+                double* dst = f.partial + static_cast<int64_t>(v) * f.nu + u;
+                *dst = f.accumulate ? __dadd_rn(*dst, term) : term;
+            }
+        } else {
+            if (u < 0 || e >= W) return;
+            const double* rb = red + (yy & 1) * (kWarps * kStrip);
+            double term = 0.0;
+#pragma unroll
+            for (int w = 0; w < kWarps; ++w)
+                if (w < nwarps_live) term = __dadd_rn(term, rb[w * kStrip + t]);
+            if (f.map) {
+                write_map(u, v, finalize_L(term, f));
+            } else {
+                double* dst = f.partial + static_cast<int64_t>(v) * f.nu + u;
+                *dst = f.accumulate ? __dadd_rn(*dst, term) : term;
             }
         }
     };
