@@ -279,6 +279,27 @@ def run_ours(args) -> None:
             kernels[name] = (kt / kn, kn)
     profiling.reset()
 
+    # plain build (BASELINE config "4096x4096 WAMI frame, 128-bin integral histogram on 1 B200"):
+    # the drop-in build_integral_histogram path alone, same frame, same timing protocol
+    build_only = None
+    if world == 1:
+        def build_step():
+            P.build_integral_histogram(frame, nbins, memory_budget=None, out=t, validate=False)
+        for _ in range(args.warmup):
+            build_step()
+        profiling.reset()
+        profiling.enable(True)
+        ms_b = timed(build_step, args.steps)
+        profiling.enable(False)
+        kt, kn = profiling.kernel_time("ih_sweep")
+        profiling.reset()
+        alg_b = BINS_PER_GPU * W_IMG * H_IMG * 4 + W_IMG * H_IMG
+        build_only = {"ms_per_step": round(ms_b, 4), "value": round(nbins * W_IMG * H_IMG / (ms_b * 1e-3) / 1e9, 2),
+                      "unit": UNIT, "kernel": "ih_sweep",
+                      "kernel_ms": round(kt / kn, 4) if kn else None,
+                      "frac": round(alg_b / (kt / kn * 1e-3) / 1e9 / peaks()["hbm_gbs"], 4) if kn else None,
+                      "alg_bytes": alg_b}
+
     # end to end through the public API: pinned host frame in, host map out, every step
     host_frame = torch.from_numpy(frame_h).pin_memory()
     host_map = torch.empty((H_IMG, W_IMG), dtype=torch.float64).pin_memory()
@@ -356,6 +377,7 @@ def run_ours(args) -> None:
                 "h2d_bytes_per_step": W_IMG * H_IMG * world, "d2h_bytes_per_step": W_IMG * H_IMG * 8,
                 "ms_per_step": round(ms_e2e, 4), "mode": e2e_mode},
         "gpu_launches": int(launches),
+        "build_only": build_only,
         "clocks": clk.summary(),
     }
     if world == 1 and not args.no_cpu_baseline:

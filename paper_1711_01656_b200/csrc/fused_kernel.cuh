@@ -292,28 +292,8 @@ __global__ void __launch_bounds__(256, 2) sweep_match_kernel(QuantParams q, Pixe
     }
 
     uint32_t V[4][kB];
-    if (STORE && warp_live) {
-        // H(y0, x + 1, k) above the band: the corner sum A (rows < y0, columns left of the
-        // strip) plus the prefix along the strip of the column counts C
-        if (band > 0 && fc.C) {
-            const uint16_t* cb = fc.C + (static_cast<int64_t>(band - 1) * Lb + kl0) * Wp + xl;
-            const uint32_t* ab = fc.A + (static_cast<int64_t>(kl0) * (gridDim.y - 1) + band - 1) * gridDim.x + strip;
-#pragma unroll
-            for (int k = 0; k < kB; ++k) {
-                const uint2 c = *reinterpret_cast<const uint2*>(cb + static_cast<int64_t>(k) * Wp);
-                const uint32_t p0 = c.x & 0xFFFFu, p1 = p0 + (c.x >> 16), p2 = p1 + (c.y & 0xFFFFu), p3 = p2 + (c.y >> 16);
-                const uint32_t base = __ldg(ab + static_cast<int64_t>(k) * (gridDim.y - 1) * gridDim.x) +
-                                      warp_incl_scan(p3) - p3;
-                V[0][k] = base + p0;
-                V[1][k] = base + p1;
-                V[2][k] = base + p2;
-                V[3][k] = base + p3;
-            }
-        } else {
-#pragma unroll
-            for (int k = 0; k < kB; ++k) V[0][k] = V[1][k] = V[2][k] = V[3][k] = 0;
-        }
-    }
+    if (STORE && warp_live)
+        vpart_init_ca<kB>(V, fc.C, fc.A, band, strip, gridDim.y, gridDim.x, Lb, Wp, kl0, xl);
     uint32_t* base_ptr = STORE ? out.data + static_cast<int64_t>(kl0) * out.plane_pitch + xl : nullptr;
     const bool lane_live = xl < out.row_pitch;
     const uint32_t store_mask = lane_live ? (k_live >= 32 ? 0xFFFFFFFFu : (1u << max(k_live, 0)) - 1u) : 0u;

@@ -3,14 +3,15 @@
 // Replaces build_integral_histogram / build_tensor and its four CPU schedules
 // (reference proj/src/integral.cpp:348-551).  Data flow:
 //
-//   carries.cu        row carries Lt[s][y][kl] (count of each slab bin left of strip s)
-//                     and band carries Hb[j][kl][x] (IH row at the top of band j)
+//   carries.cu        row carries Lt16[s][y][kl] (count of each slab bin left of strip s),
+//                     column counts above each band C16 and corner sums A32, from which
+//                     each warp rebuilds the IH row at the top of its band
 //   ih_sweep_kernel   per (band, strip, bin slab): one warp per B-bin slab sweeps the
 //                     band top to bottom; lane l owns columns 4l..4l+3 of the strip and
 //                     keeps H(y, x, k) for those 4 columns x B bins in registers.  A row
 //                     update is  H(y,x,k) = H(y-1,x,k) + L(y,k) + #{c <= x in strip : bin = k},
-//                     the in-strip count coming from byte-SIMD one-hot matches and one
-//                     warp shuffle scan of 4 bins packed per word.  Each plane-row of the
+//                     the in-strip count coming from one-hot shifts (four bins per word)
+//                     and one warp shuffle scan of 4 bins packed per word.  Each plane-row of the
 //                     strip leaves as one coalesced 512-byte run of 16-byte stores.
 //
 // The pixel -> bin stage (to_grayscale + quantize) is fused into every load.
@@ -80,8 +81,6 @@ BuildPlan plan_build(int width, int height, int bins, int force_B, int ctas_per_
     band_rows = std::max(1, std::min(band_rows, height));
     p.band_rows = band_rows;
     p.nbands = static_cast<int>(ceil_div(height, band_rows));
-    p.lt_bytes = p.nstrips > 1 ? static_cast<size_t>(p.nstrips) * height * p.Lb * 4 : 0;
-    p.hb_bytes = p.nbands > 1 ? static_cast<size_t>(p.nbands - 1) * p.Lb * p.Wp * 4 : 0;
     return p;
 }
 
@@ -133,8 +132,7 @@ namespace spct_build {
 
 template <int B, bool GUARD>
 __global__ void __launch_bounds__(256) ih_sweep_kernel(QuantParams q, PixelMode pm, spct_ih out, int Lb, int Wp,
-                                                       int band_rows, int warps_per_cta, const uint32_t* __restrict__ Lt,
-                                                       const uint32_t* __restrict__ Hb) {
+                                                       int band_rows, int warps_per_cta, FusedCarries fc) {
     const int lane = lane_id();
     const int warp = threadIdx.x >> 5;
     const int strip = blockIdx.x;
@@ -149,19 +147,26 @@ __global__ void __launch_bounds__(256) ih_sweep_kernel(QuantParams q, PixelMode 
     const bool lane_live = x0 < out.row_pitch;
     const int k0 = out.bin0 + kl0;
     const uint32_t kpat0 = pm.byte_mode ? 0x01010101u * static_cast<uint32_t>(k0) : 0u;
+    const uint32_t store_mask = lane_live ? (1u << k_live) - 1u : 0u;
 
     uint32_t V[4][B];
-    vpart_init<B>(V, Hb, band, Lb, kl0, Wp, x0);
+    vpart_init_ca<B>(V, fc.C, fc.A, band, strip, gridDim.y, gridDim.x, Lb, Wp, kl0, x0);
     uint32_t* base_ptr = out.data + static_cast<int64_t>(kl0) * out.plane_pitch + x0;
-    const uint32_t* lt_strip =
-        (Lt && strip > 0) ? Lt + static_cast<int64_t>(strip) * out.height * Lb + kl0 : nullptr;
+    const uint16_t* lt_strip =
+        (fc.Lt && strip > 0) ? fc.Lt + static_cast<int64_t>(strip) * out.height * Lb + kl0 : nullptr;
 
     uint32_t nxt = load_bins4(q, pm, x0, y0, k0, B);
     for (int y = y0; y < y1; ++y) {
         const uint32_t cur = nxt;
         if (y + 1 < y1) nxt = load_bins4(q, pm, x0, y + 1, k0, B);
-        vpart_row<B, GUARD>(V, cur, kpat0, lt_strip ? lt_strip + static_cast<int64_t>(y) * Lb : nullptr,
-                            base_ptr + static_cast<int64_t>(y) * out.row_pitch, out.plane_pitch, lane_live, k_live);
+        uint32_t t4[4];
+        onehot_shifts(cur ^ kpat0, t4);
+        const uint16_t* lt_row = lt_strip ? lt_strip + static_cast<int64_t>(y) * Lb : nullptr;
+        uint32_t* prow = base_ptr + static_cast<int64_t>(y) * out.row_pitch;
+#pragma unroll
+        for (int g = 0; g < B / 4; ++g)
+            vpart_group_q<B>(V, g, t4, lt16_group(lt_row, g), prow + static_cast<int64_t>(4 * g) * out.plane_pitch,
+                             out.plane_pitch, store_mask);
     }
 }
 
@@ -305,7 +310,8 @@ extern "C" spct_status spct_cu_ih_build_workspace(const spct_source* src, int bi
     if (!(src->width > 0 && src->height > 0 && bins >= 1)) return contract("build: empty bin map");
     const BuildPlan p = plan_build_sweep(src->width, src->height, bins);
     const BuildPlan pf = plan_fused_sweep(src->width, src->height, bins);  // fused sweep: 16 bins per warp
-    *bytes = std::max(p.lt_bytes + p.hb_bytes, fused_carry_layout(pf, src->height).total) + fused_prep_bytes(bins) + 256;
+    *bytes = std::max(fused_carry_layout(p, src->height).total, fused_carry_layout(pf, src->height).total) +
+             fused_prep_bytes(bins) + 256;
     return SPCT_OK;
 }
 
@@ -321,16 +327,16 @@ extern "C" spct_status spct_cu_ih_build(const spct_source* src, const spct_ih* o
     if (reinterpret_cast<uintptr_t>(out->data) % 16 != 0) return contract("ih_build: tensor data must be 16-byte aligned");
     const BuildPlan p = plan_build_sweep(out->width, out->height, out->bins);
     cudaStream_t s = as_stream(stream);
-    uint32_t *Lt, *Hb;
-    if (auto st = build_carries(q, *out, p, workspace, workspace_bytes, s, &Lt, &Hb)) return st;
+    FusedCarries fc{};
+    if (auto st = build_fused_carries(q, *out, p, workspace, workspace_bytes, s, &fc)) return st;
     dim3 grid(p.nstrips, p.nbands, p.slab_groups);
     const int threads = 32 * p.warps;
     const int prof = prof_begin("ih_sweep", s);
     const PixelMode pm = make_pixel_mode(q, out->bin0);
     switch (p.B) {
 #define SPCT_SWEEP(BB)                                                                                          \
-    ih_sweep_kernel<BB, false><<<grid, threads, 0, s>>>(q, pm, *out, p.Lb, p.Wp, p.band_rows, p.warps, Lt, Hb); \
-    if (out->bins % BB) ih_sweep_kernel<BB, true><<<grid, threads, 0, s>>>(q, pm, *out, p.Lb, p.Wp, p.band_rows, p.warps, Lt, Hb);
+    ih_sweep_kernel<BB, false><<<grid, threads, 0, s>>>(q, pm, *out, p.Lb, p.Wp, p.band_rows, p.warps, fc); \
+    if (out->bins % BB) ih_sweep_kernel<BB, true><<<grid, threads, 0, s>>>(q, pm, *out, p.Lb, p.Wp, p.band_rows, p.warps, fc);
         case 4: SPCT_SWEEP(4) break;
         case 8: SPCT_SWEEP(8) break;
         default: SPCT_SWEEP(16) break;

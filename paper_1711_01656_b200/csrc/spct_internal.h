@@ -56,7 +56,6 @@ struct BuildPlan {
     int band_rows;  // rows per band
     int nbands;
     int slab_groups;  // CTAs along the bin axis
-    size_t lt_bytes, hb_bytes;
 };
 BuildPlan plan_build(int width, int height, int bins, int force_B = 0, int ctas_per_sm = 2, int min_band_rows = 32);
 
@@ -72,10 +71,6 @@ BuildPlan plan_fused_sweep(int width, int height, int bins);
 // Workspace of the fused path's template prep (fused.cu).
 size_t fused_prep_bytes(int bins);
 
-// Carry pre-passes of a build (ih_build.cu); fills the row-carry (Lt) and band-carry
-// (Hb) tables inside `workspace`.
-spct_status build_carries(const spct_dev::QuantParams& q, const spct_ih& out, const BuildPlan& p, void* workspace,
-                          size_t ws_bytes, cudaStream_t s, uint32_t** Lt, uint32_t** Hb);
 
 // Carry tables of the fused build+match sweep (carries.cu): row carries (u16), column
 // counts above each band boundary (u16) and the band x strip corner sums (u32).

@@ -7,7 +7,7 @@
 //     V[j][k] += L(y, k) + E_k(l) + P_k(j)
 // where L is the count of k in the row left of the strip (carry table), E_k the count
 // of k in lanes < l (one warp shuffle scan over four bins packed per word) and P_k(j)
-// the count of k among the lane's columns <= j (byte-SIMD prefix of one-hot matches).
+// the count of k among the lane's columns <= j (one-hot shifts, vpart_group_q).
 // V is then the unpadded integral-histogram value H(y+1, x+1, k) and leaves as one
 // 16-byte streaming store per lane: each plane-row of the strip is a 512-byte run.
 #pragma once
@@ -92,88 +92,6 @@ __device__ __forceinline__ uint32_t warp_incl_scan(uint32_t v) {
     return v;
 }
 
-template <int B>
-__device__ __forceinline__ void vpart_init(uint32_t (&V)[4][B], const uint32_t* __restrict__ Hb, int band, int Lb,
-                                           int kl0, int Wp, int x0) {
-    if (band > 0 && Hb) {
-        const uint32_t* hb = Hb + (static_cast<int64_t>(band - 1) * Lb + kl0) * Wp + x0;
-#pragma unroll
-        for (int k = 0; k < B; ++k) {
-            uint4 v = *reinterpret_cast<const uint4*>(hb + static_cast<int64_t>(k) * Wp);
-            V[0][k] = v.x;
-            V[1][k] = v.y;
-            V[2][k] = v.z;
-            V[3][k] = v.w;
-        }
-    } else {
-#pragma unroll
-        for (int k = 0; k < B; ++k) V[0][k] = V[1][k] = V[2][k] = V[3][k] = 0;
-    }
-}
-
-// One row of the sweep.  `kpat0` = k0 * 0x01010101 in byte mode (k0 = global bin of
-// the warp's first plane), 0 in relative mode.  `lt_row` points at L(y, kl0 ..) or is
-// null for the first strip; `p` at column x0 of the warp's first plane in row y.
-// GUARD: the slab has fewer than B live planes (k_live); `store`: lane inside the pitch.
-template <int B, bool GUARD>
-__device__ __forceinline__ void vpart_row(uint32_t (&V)[4][B], uint32_t bins4, uint32_t kpat0,
-                                          const uint32_t* __restrict__ lt_row, uint32_t* p, int64_t plane_pitch,
-                                          bool store, int k_live) {
-#pragma unroll
-    for (int g = 0; g < B / 4; ++g) {
-        uint4 L = make_uint4(0, 0, 0, 0);
-        if (lt_row) L = __ldg(reinterpret_cast<const uint4*>(lt_row) + g);
-        uint32_t P[4];
-#pragma unroll
-        for (int i = 0; i < 4; ++i)
-            P[i] = match_prefix(bins4 ^ kpat0, 0x01010101u * static_cast<uint32_t>(4 * g + i));
-        // lane totals (byte 3 of each prefix) -> one word, four bins
-        const uint32_t packed = __byte_perm(__byte_perm(P[0], P[1], 0x0073), __byte_perm(P[2], P[3], 0x0073), 0x5410);
-        const uint32_t excl = warp_incl_scan(packed) - packed;
-        const uint32_t Lk[4] = {L.x, L.y, L.z, L.w};
-#pragma unroll
-        for (int i = 0; i < 4; ++i) {
-            const int k = 4 * g + i;
-            const uint32_t base = Lk[i] + __byte_perm(excl, 0, 0x4440 + i);
-            V[0][k] += base + __byte_perm(P[i], 0, 0x4440);
-            V[1][k] += base + __byte_perm(P[i], 0, 0x4441);
-            V[2][k] += base + __byte_perm(P[i], 0, 0x4442);
-            V[3][k] += base + (P[i] >> 24);
-            st_cs_v4_pred(store && (!GUARD || k < k_live), p, V[0][k], V[1][k], V[2][k], V[3][k]);
-            p += plane_pitch;
-        }
-    }
-}
-
-}  // namespace spct_dev
-
-namespace spct_dev {
-
-// One group of four planes (4g .. 4g+3) of vpart_row, for callers that interleave
-// the row update with other work.  `p` points at plane 4g of the row.
-template <int B>
-__device__ __forceinline__ void vpart_group(uint32_t (&V)[4][B], int g, uint32_t dbins, uint4 L, uint32_t* p,
-                                            int64_t plane_pitch, uint32_t store_mask) {
-    // dbins = bins4 ^ kpat0; store_mask bit k: plane k is live and the lane is inside the pitch
-    uint32_t P[4];
-#pragma unroll
-    for (int i = 0; i < 4; ++i) P[i] = match_prefix(dbins, 0x01010101u * static_cast<uint32_t>(4 * g + i));
-    const uint32_t packed = __byte_perm(__byte_perm(P[0], P[1], 0x0073), __byte_perm(P[2], P[3], 0x0073), 0x5410);
-    const uint32_t excl = warp_incl_scan(packed) - packed;
-    const uint32_t Lk[4] = {L.x, L.y, L.z, L.w};
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-        const int k = 4 * g + i;
-        const uint32_t base = Lk[i] + __byte_perm(excl, 0, 0x4440 + i);
-        V[0][k] += base + __byte_perm(P[i], 0, 0x4440);
-        V[1][k] += base + __byte_perm(P[i], 0, 0x4441);
-        V[2][k] += base + __byte_perm(P[i], 0, 0x4442);
-        V[3][k] += base + (P[i] >> 24);
-        st_cs_v4_pred((store_mask >> k) & 1u, p, V[0][k], V[1][k], V[2][k], V[3][k]);
-        p += plane_pitch;
-    }
-}
-
 }  // namespace spct_dev
 
 namespace spct_dev {
@@ -183,13 +101,6 @@ __device__ __forceinline__ uint32_t shl_clamp(uint32_t v, uint32_t n) {
     uint32_t r;
     asm("shl.b32 %0, %1, %2;" : "=r"(r) : "r"(v), "r"(n));
     return r;
-}
-
-// Address of plane k of a row: prow + k * ppb bytes in one IMAD.WIDE (k * ppb < 2^32).
-__device__ __forceinline__ uint32_t* plane_addr(uint32_t* prow, uint32_t k, uint32_t ppb) {
-    uint64_t a;
-    asm("mad.wide.u32 %0, %1, %2, %3;" : "=l"(a) : "r"(k), "r"(ppb), "l"(reinterpret_cast<uint64_t>(prow)));
-    return reinterpret_cast<uint32_t*>(a);
 }
 
 // 8 x (relative bin) of the lane's four columns, from dbins = bins4 ^ kpat0; a column off
@@ -229,6 +140,44 @@ __device__ __forceinline__ void vpart_group_q(uint32_t (&V)[4][B], int g, const 
         st_cs_v4_pred(store_mask & (1u << k), p, V[0][k], V[1][k], V[2][k], V[3][k]);
         p += plane_pitch;
     }
+}
+
+}  // namespace spct_dev
+
+namespace spct_dev {
+
+// V at the top of a band (the unpadded IH row y0 - 1) from the carry tables of
+// carries.cu: H(y0, x + 1, k) = A[k][band-1][strip] (rows < y0, columns left of the strip)
+// + the inclusive prefix along the strip of C[band-1][k][x] (column counts above y0).
+// Lane l owns columns x0 .. x0+3 of the strip; kl0 is the warp's first slab-local bin.
+template <int B>
+__device__ __forceinline__ void vpart_init_ca(uint32_t (&V)[4][B], const uint16_t* __restrict__ C,
+                                              const uint32_t* __restrict__ A, int band, int strip, int nbands,
+                                              int nstrips, int Lb, int Wp, int kl0, int x0) {
+    if (band > 0 && C) {
+        const uint16_t* cb = C + (static_cast<int64_t>(band - 1) * Lb + kl0) * Wp + x0;
+        const uint32_t* ab = A + (static_cast<int64_t>(kl0) * (nbands - 1) + band - 1) * nstrips + strip;
+#pragma unroll
+        for (int k = 0; k < B; ++k) {
+            const uint2 c = *reinterpret_cast<const uint2*>(cb + static_cast<int64_t>(k) * Wp);
+            const uint32_t p0 = c.x & 0xFFFFu, p1 = p0 + (c.x >> 16), p2 = p1 + (c.y & 0xFFFFu), p3 = p2 + (c.y >> 16);
+            const uint32_t base = __ldg(ab + static_cast<int64_t>(k) * (nbands - 1) * nstrips) + warp_incl_scan(p3) - p3;
+            V[0][k] = base + p0;
+            V[1][k] = base + p1;
+            V[2][k] = base + p2;
+            V[3][k] = base + p3;
+        }
+    } else {
+#pragma unroll
+        for (int k = 0; k < B; ++k) V[0][k] = V[1][k] = V[2][k] = V[3][k] = 0;
+    }
+}
+
+// Row carries of group g (4 bins) from a u16 carry row (null: first strip, all zero).
+__device__ __forceinline__ uint4 lt16_group(const uint16_t* lt_row, int g) {
+    if (!lt_row) return make_uint4(0, 0, 0, 0);
+    const uint2 v = __ldg(reinterpret_cast<const uint2*>(lt_row) + g);
+    return make_uint4(v.x & 0xFFFFu, v.x >> 16, v.y & 0xFFFFu, v.y >> 16);
 }
 
 }  // namespace spct_dev
