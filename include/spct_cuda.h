@@ -97,6 +97,17 @@ spct_status spct_cu_to_grayscale(const uint8_t* r, const uint8_t* g, const uint8
  * 1 <= nbins <= 65536, hi > lo (imagecore.cpp:30-31,46,51). */
 spct_status spct_cu_quantize(const spct_source* src, uint16_t* out_bins, void* stream);
 
+/* Gradient-orientation BinMap (the orientation channel of the tracking batch): the
+ * reference's gradient_maps(GrayImage, sigma) orientation (features.cpp:200-203, :78-93:
+ * Gaussian smoothing, central differences, atan fold to degrees) binned by
+ * phog.cpp:15-20 orientation_bin.  gray (dev) with row pitch `pitch`; out (dev) uint16
+ * with row pitch out_pitch.  Contract: sigma >= 0 (features.cpp:201), width,height > 0,
+ * 1 <= bins <= 65536, ceil(3 sigma) <= 31.  Workspace: spct_cu_orientation_workspace. */
+spct_status spct_cu_orientation_workspace(int width, int height, size_t* bytes);
+spct_status spct_cu_orientation_bins(const uint8_t* gray, int64_t pitch, int width, int height, double sigma,
+                                     int bins, uint16_t* out, int64_t out_pitch, void* workspace,
+                                     size_t workspace_bytes, void* stream);
+
 /* Validation pass of build_tensor (integral.cpp:337-343): max BinMap value (dev -> host,
  * synchronises the stream). */
 spct_status spct_cu_binmap_max(const uint16_t* bins, int64_t pitch, int width, int height,

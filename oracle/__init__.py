@@ -72,6 +72,7 @@ def _load_c():
         "or_hist_partial": (_i, [_u16p, _i, _i, _i, _f64p, _i, _i, _d, _i, _i, _f64p]),
         "or_hist_finalize": (_i, [_f64p, _i, _i, _i, _i, _d, _f64p]),
         "or_xorshift_image": (None, [_u32, _i64, _u8p]),
+        "or_orientation_bins": (_i, [_u8p, _i, _i, _d, _i, _u16p]),
         "fx_noise_image": (None, [_i, _i, _u32, _u8p]),
         "fx_smooth_image": (None, [_i, _i, _u32, _i, _u8p]),
         "fx_noise_color": (None, [_i, _i, _u32, _u8p, _u8p, _u8p]),
@@ -107,6 +108,7 @@ def _load_ref():
         "ref_schedule_stats": (_i, [_i, _i, _i, _i, C.POINTER(C.c_longlong), C.POINTER(C.c_longlong), C.POINTER(_d)]),
         "ref_estimate_memory": (_i, [_i, _i, _i, _i, C.POINTER(_u64), C.POINTER(_u64), C.POINTER(_i)]),
         "ref_schedule_from_string": (_i, [C.c_char_p]),
+        "ref_orientation_bins": (_i, [_u8p, _i, _i, _d, _i, _u16p]),
     }
     for name, (res, args) in sig.items():
         f = getattr(lib, name)
@@ -290,6 +292,25 @@ def hist_partial(bm, nbins, tmpl, kw, kh, p, k0, k1) -> np.ndarray:
     out = np.empty((h - kh + 1, w - kw + 1), np.float64)
     _check(clib().or_hist_partial(bm.reshape(-1), nbins, w, h, tmpl, kw, kh, p, k0, k1,
                                   out.reshape(-1)), "hist_partial")
+    return out
+
+
+def orientation_bins(gray: np.ndarray, bins: int, sigma: float = 1.0) -> np.ndarray:
+    """Gradient-orientation BinMap (features.cpp:78-93 + phog.cpp:15-20), C restatement."""
+    gray = np.ascontiguousarray(gray, np.uint8)
+    h, w = gray.shape
+    out = np.empty((h, w), np.uint16)
+    _check(clib().or_orientation_bins(gray.reshape(-1), w, h, sigma, bins, out.reshape(-1)), "orientation_bins")
+    return out
+
+
+def ref_orientation_bins(gray: np.ndarray, bins: int, sigma: float = 1.0) -> np.ndarray:
+    """The same through the unmodified reference (gradient_maps) — oracle/_ref."""
+    gray = np.ascontiguousarray(gray, np.uint8)
+    h, w = gray.shape
+    out = np.empty((h, w), np.uint16)
+    _check(reflib().ref_orientation_bins(gray.reshape(-1), w, h, sigma, bins, out.reshape(-1)), "orientation_bins",
+           reflib())
     return out
 
 

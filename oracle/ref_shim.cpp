@@ -16,7 +16,10 @@
 #include <string>
 #include <vector>
 
+#include <cmath>
+
 #include "spct/error.hpp"
+#include "spct/features.hpp"
 #include "spct/imagecore.hpp"
 #include "spct/integral.hpp"
 #include "spct/likelihood.hpp"
@@ -189,6 +192,24 @@ int ref_schedule_from_string(const char* s) {
     int kind = -1;
     guarded([&] { kind = static_cast<int>(spct::schedule_from_string(s)); });
     return kind;
+}
+
+// gradient_maps(GrayImage, sigma) (features.cpp:200-203) of the unmodified reference, then
+// the binning of phog.cpp:15-20 (orientation_bin is file-local there; restated verbatim).
+int ref_orientation_bins(const std::uint8_t* gray, int w, int h, double sigma, int bins, std::uint16_t* out) {
+    return guarded([&] {
+        spct::GrayImage img;
+        img.width = w;
+        img.height = h;
+        img.data.assign(gray, gray + static_cast<std::size_t>(w) * h);
+        const spct::GradientMaps g = spct::gradient_maps(img, sigma);
+        for (std::size_t i = 0; i < g.orientation.data.size(); ++i) {
+            int b = static_cast<int>(std::floor((g.orientation.data[i] + 90.0) * bins / 180.0));
+            if (b < 0) b = 0;
+            if (b >= bins) b = bins - 1;
+            out[i] = static_cast<std::uint16_t>(b);
+        }
+    });
 }
 
 }  // extern "C"

@@ -10,12 +10,14 @@ from . import _capi, profiling
 from ._capi import ContractError, SpctError, lib
 from .api import (DEFAULT_BUDGET, IntegralHistogramTensor, ScanSchedule, build_and_match, build_and_match_map,
                   build_integral_histogram, estimate_memory, hist_distance_map, hist_finalize,
-                  hist_match_map, hist_partial, quantize, region_count, region_histogram,
+                  hist_match_map, hist_partial, orientation_bins, quantize, region_count, region_histogram,
                   region_histograms, schedule_from_string, schedule_stats, to_grayscale)
+from .channels import CHANNELS, channel_sources, likelihood_channels
 
 __all__ = [
     "ContractError", "SpctError", "lib", "DEFAULT_BUDGET", "IntegralHistogramTensor", "ScanSchedule",
     "build_and_match", "build_and_match_map", "build_integral_histogram", "estimate_memory", "hist_distance_map",
     "hist_finalize", "hist_match_map", "hist_partial", "quantize", "region_count", "region_histogram",
-    "region_histograms", "schedule_from_string", "schedule_stats", "to_grayscale",
+    "region_histograms", "schedule_from_string", "schedule_stats", "to_grayscale", "orientation_bins",
+    "CHANNELS", "channel_sources", "likelihood_channels",
 ]

@@ -109,6 +109,23 @@ def quantize(img, bins: int, lo: float = 0.0, hi: float = 256.0, stream=None) ->
     return out
 
 
+def orientation_bins(gray, bins: int, sigma: float = 1.0, stream=None) -> torch.Tensor:
+    """Gradient-orientation BinMap of a gray uint8 frame (features.cpp:200-203 orientation,
+    phog.cpp:15-20 orientation_bin): device int16 tensor carrying uint16 bins, usable as a
+    BinMap source of build_integral_histogram / build_and_match (tracking batch, config 5)."""
+    g = _dev(gray, torch.uint8)
+    if g.dim() != 2 or g.numel() == 0:
+        raise ContractError(A.SPCT_ERR_CONTRACT, "gradient_maps: empty image")
+    h, w = g.shape
+    out = torch.empty((h, w), dtype=torch.int16, device=g.device)
+    ws = C.c_size_t()
+    check(A.lib().spct_cu_orientation_workspace(w, h, C.byref(ws)))
+    wbuf = _WS_ORIENT.get(ws.value, g.device)
+    check(A.lib().spct_cu_orientation_bins(_ptr(g), w, w, h, float(sigma), int(bins), _ptr(out), w, _ptr(wbuf),
+                                           wbuf.numel(), _stream(stream)))
+    return out
+
+
 def as_numpy_u16(t: torch.Tensor) -> np.ndarray:
     return t.cpu().numpy().view(np.uint16)
 
@@ -200,6 +217,7 @@ class Workspace:
 
 
 _WS = Workspace()
+_WS_ORIENT = Workspace()
 
 
 def frame_source(frame, nbins: int, lo: float = 0.0, hi: float = 256.0):

@@ -1,0 +1,44 @@
+"""Multi-feature likelihood maps of a tracking batch (BASELINE config 5).
+
+Per frame and per feature channel — intensity (to_grayscale of the RGB frame),
+gradient orientation (features.cpp:200-203 + phog.cpp:15-20), and the R, G, B planes —
+one fused quantise -> integral histogram -> sliding-window likelihood map
+(build_integral_histogram + hist_distance_map, spct_main.cpp:332-333) against that
+channel's template histogram.  The reference computes these channels one at a time on
+the CPU (track_loop.cpp's channel fan-out); here each channel is one fused sweep on the
+device, and frames stream through pinned host buffers.
+"""
+from __future__ import annotations
+
+import torch
+
+from . import api as _api
+from ._capi import METRIC_MINKOWSKI
+
+CHANNELS = ("intensity", "orientation", "red", "green", "blue")
+
+
+def channel_sources(r, g, b, nbins: int, sigma: float = 1.0, stream=None) -> dict:
+    """Device sources of the five channels: RGB planes (intensity is quantised from the
+    fused gray of the RGB source), the orientation BinMap, and the single planes."""
+    rd, gd, bd = (_api._dev(p, torch.uint8) for p in (r, g, b))
+    gray = _api.to_grayscale(rd, gd, bd, stream=stream)
+    return {"intensity": (rd, gd, bd), "orientation": _api.orientation_bins(gray, nbins, sigma, stream=stream),
+            "red": rd, "green": gd, "blue": bd}
+
+
+def likelihood_channels(r, g, b, nbins: int, templates: dict, kw: int, kh: int, p: float = 1.0,
+                        metric: int = METRIC_MINKOWSKI, sigma: float = 1.0, tensors: dict | None = None,
+                        maps: dict | None = None, tmpl_dev: dict | None = None, stream=None) -> dict:
+    """{channel: (height, width) float64 device map} for one RGB frame.  ``templates`` maps
+    each channel to its normalised template histogram (nbins values); ``tensors`` /
+    ``maps`` / ``tmpl_dev`` may hold preallocated per-channel outputs for a batch."""
+    srcs = channel_sources(r, g, b, nbins, sigma, stream)
+    out = {}
+    for c in CHANNELS:
+        t = tensors.get(c) if tensors else None
+        m = maps.get(c) if maps else None
+        td = tmpl_dev.get(c) if tmpl_dev else None
+        _, out[c] = _api.build_and_match_map(srcs[c], nbins, None if td is not None else templates[c], kw, kh, p,
+                                             metric, out=t, lmap=m, tmpl_dev=td, stream=stream)
+    return out

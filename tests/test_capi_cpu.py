@@ -104,6 +104,20 @@ def test_contract_errors_before_device_work():
     assert lib.spct_cu_hist_partial(C.byref(t), 1, 3, 3, 1.0, 0, 1, 0, None) == A.SPCT_ERR_CONTRACT
 
 
+def test_orientation_contracts_before_device_work():
+    lib = A.lib()
+    ws = C.c_size_t()
+    A.check(lib.spct_cu_orientation_workspace(2048, 2048, C.byref(ws)))
+    assert ws.value >= 2 * 2048 * 2048 * 8
+    # gradient_maps: sigma must be nonnegative (features.cpp:201) — checked before any launch
+    assert lib.spct_cu_orientation_bins(1, 8, 8, 8, -1.0, 16, 1, 8, 1, 1 << 20, None) == A.SPCT_ERR_CONTRACT
+    assert b"sigma must be nonnegative" in lib.spct_cu_last_error()
+    assert lib.spct_cu_orientation_bins(1, 8, 8, 8, 1.0, 0, 1, 8, 1, 1 << 20, None) == A.SPCT_ERR_CONTRACT
+    assert lib.spct_cu_orientation_bins(1, 8, 8, 8, 11.0, 16, 1, 8, 1, 1 << 20, None) == A.SPCT_ERR_CONTRACT
+    assert lib.spct_cu_orientation_bins(1, 8, 8, 8, 1.0, 16, 1, 8, 1, 16, None) == A.SPCT_ERR_CONTRACT  # workspace
+    assert lib.spct_cu_orientation_workspace(0, 3, C.byref(ws)) == A.SPCT_ERR_CONTRACT
+
+
 def test_python_api_contracts_without_gpu():
     import paper_1711_01656_b200 as P
 

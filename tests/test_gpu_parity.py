@@ -413,3 +413,38 @@ def test_against_live_reference(P):
     th = np.bincount(crop.reshape(-1), minlength=9).astype(np.float64) / crop.size
     assert np.array_equal(P.hist_distance_map(t, th, 13, 11, 1.0, exact=True).cpu().numpy(),
                           rt.hist_distance_map(th, 13, 11, 1.0))
+
+
+# ------------------------------------------------------------------ tracking batch (config 5)
+
+@pytest.mark.parametrize("w,h,sigma,bins", [(1, 1, 1.0, 8), (64, 48, 1.0, 32), (300, 211, 1.0, 32), (131, 97, 1.5, 16),
+                                            (257, 140, 0.0, 9)])
+def test_orientation_bins_exact(P, w, h, sigma, bins):
+    """Device orientation BinMap == the oracle restatement (== the reference, test_oracle.py)."""
+    for img in (oracle.smooth_image(w, h, w + 2 * h), oracle.noise_image(w, h, 3 * w + h)):
+        got = P.api.as_numpy_u16(P.orientation_bins(img, bins, sigma))
+        assert np.array_equal(got, oracle.orientation_bins(img, bins, sigma))
+
+
+@pytest.mark.parametrize("frames", [2])
+def test_tracking_batch_channels(P, frames):
+    """Config 5 in miniature: per frame, intensity / orientation / R / G / B likelihood maps
+    (fused build + match per channel) against the oracle on each channel's BinMap."""
+    w, h, nbins, kw, kh = 280, 190, 32, 32, 24
+    x0, y0 = 120, 70
+    for f in range(frames):
+        r, g, b = oracle.noise_color(w, h, 500 + f) if f % 2 else (oracle.smooth_image(w, h, 600 + f),
+                                                                  oracle.smooth_image(w, h, 700 + f),
+                                                                  oracle.smooth_image(w, h, 800 + f))
+        gray = oracle.to_grayscale(r, g, b)
+        chan_bins = {"intensity": oracle.quantize(gray, nbins), "orientation": oracle.orientation_bins(gray, nbins, 1.0),
+                     "red": oracle.quantize(r, nbins), "green": oracle.quantize(g, nbins),
+                     "blue": oracle.quantize(b, nbins)}
+        templates = {c: _crop_template(qb, nbins, x0, y0, kw, kh) for c, qb in chan_bins.items()}
+        maps = P.likelihood_channels(r, g, b, nbins, templates, kw, kh, 1.0)
+        assert set(maps) == set(P.CHANNELS)
+        for c, qb in chan_bins.items():
+            want = oracle.hist_match_map_direct(qb, nbins, templates[c], kw, kh, 1.0)
+            got = maps[c].cpu().numpy()
+            assert close(got, want), c
+            assert got[y0 + (kh - 1) // 2, x0 + (kw - 1) // 2] == 1.0, c  # the template's own window

@@ -174,3 +174,17 @@ def test_oracle_vs_live_reference_maps():
         t.hist_distance_map(th * 2, 13, 11, 1.0)
     with pytest.raises(oracle.ContractError):
         t.hist_distance_map(th, 13, 11, 0.5)
+
+
+@ref
+@pytest.mark.parametrize("w,h,sigma,bins", [(1, 1, 1.0, 8), (5, 3, 0.0, 9), (64, 48, 1.0, 32), (131, 97, 1.5, 16),
+                                            (200, 150, 0.7, 36)])
+def test_orientation_bins_vs_live_reference(w, h, sigma, bins):
+    """Orientation channel of the tracking batch: the C restatement of gradient_maps
+    (features.cpp:78-93) + orientation_bin (phog.cpp:15-20) equals the reference."""
+    for img in (oracle.smooth_image(w, h, w + h), oracle.noise_image(w, h, 7 * w + h)):
+        assert np.array_equal(oracle.orientation_bins(img, bins, sigma), oracle.ref_orientation_bins(img, bins, sigma))
+    flat = np.full((h, w), 77, np.uint8)  # flat: fold_orientation gives 0 degrees -> the middle bin
+    assert np.all(oracle.orientation_bins(flat, bins, sigma) == min(bins - 1, (90 * bins) // 180))
+    with pytest.raises(oracle.ContractError):
+        oracle.ref_orientation_bins(flat, bins, -1.0)
