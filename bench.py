@@ -201,6 +201,46 @@ def ncu_traffic(kernel: str):
     return None if v is None else float(v.get("dram_bytes_per_launch"))
 
 
+def run_c5(P, dev, stream, args, frames: int = 100, side: int = 2048, nbins: int = 32, kw: int = 64, kh: int = 64):
+    import torch
+
+    g = torch.Generator(device=dev)
+    g.manual_seed(5)
+    rgb = torch.randint(0, 256, (frames, 3, side, side), dtype=torch.uint8, device=dev, generator=g)
+    # templates: each channel's histogram of the centred kw x kh crop of frame 0
+    srcs = P.channel_sources(rgb[0, 0], rgb[0, 1], rgb[0, 2], nbins)
+    y0, x0 = (side - kh) // 2, (side - kw) // 2
+    tdev = {}
+    for c, s in srcs.items():
+        if c == "orientation":
+            qb = s
+        else:
+            qb = P.quantize(P.to_grayscale(*s) if isinstance(s, tuple) else s, nbins)
+        crop = qb[y0:y0 + kh, x0:x0 + kw].to(torch.int64).reshape(-1) & 0xFFFF
+        tdev[c] = (torch.bincount(crop, minlength=nbins).to(torch.float64) / crop.numel()).contiguous()
+    tens = {c: P.IntegralHistogramTensor(side, side, nbins, device=dev) for c in P.CHANNELS}
+    maps = {c: torch.empty((side, side), dtype=torch.float64, device=dev) for c in P.CHANNELS}
+
+    def frame(i):
+        P.likelihood_channels(rgb[i, 0], rgb[i, 1], rgb[i, 2], nbins, None, kw, kh, 1.0, tensors=tens, maps=maps,
+                              tmpl_dev=tdev)
+    for i in range(3):
+        frame(i)
+    torch.cuda.synchronize()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record(stream)
+    for i in range(frames):
+        frame(i)
+    b.record(stream)
+    torch.cuda.synchronize()
+    ms = a.elapsed_time(b)
+    binpx = frames * len(P.CHANNELS) * nbins * side * side
+    return {"frames": frames, "channels": list(P.CHANNELS), "bins": nbins, "side": side, "window": [kw, kh],
+            "ms_per_frame": round(ms / frames, 4), "value": round(binpx / (ms * 1e-3) / 1e9, 2), "unit": UNIT,
+            "data": "synthetic uint8 RGB (torch RNG on the device), frames resident; every channel's IH written",
+            "l2": f"frames and tensors ({frames * 3 * side * side / 2**20:.0f} MiB of frames) exceed L2"}
+
+
 def run_ours(args) -> None:
     import torch
     import torch.distributed as dist
@@ -300,6 +340,13 @@ def run_ours(args) -> None:
                       "frac": round(alg_b / (kt / kn * 1e-3) / 1e9 / peaks()["hbm_gbs"], 4) if kn else None,
                       "alg_bytes": alg_b}
 
+    # tracking batch (BASELINE config 5): 100 synthetic 2048x2048 RGB frames x 32 bins, five
+    # feature channels (intensity, gradient orientation, R, G, B) -> five likelihood maps per
+    # frame, each channel one fused quantise -> integral histogram -> map sweep; frames resident
+    c5 = None
+    if world == 1 and not args.no_c5:
+        c5 = run_c5(P, dev, stream, args)
+
     # end to end through the public API: pinned host frame in, host map out, every step
     host_frame = torch.from_numpy(frame_h).pin_memory()
     host_map = torch.empty((H_IMG, W_IMG), dtype=torch.float64).pin_memory()
@@ -378,6 +425,7 @@ def run_ours(args) -> None:
                 "ms_per_step": round(ms_e2e, 4), "mode": e2e_mode},
         "gpu_launches": int(launches),
         "build_only": build_only,
+        "c5_batch": c5,
         "clocks": clk.summary(),
     }
     if world == 1 and not args.no_cpu_baseline:
@@ -400,6 +448,7 @@ def main():
     ap.add_argument("--ref-rows", type=int, default=192,
                     help="rows of the frame in the bounded CPU sample (window rows = rows - 63)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-c5", action="store_true", help="skip the config-5 tracking-batch measurement")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
