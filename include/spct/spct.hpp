@@ -7,6 +7,7 @@
 //   build_integral_histogram           (integral.hpp:98-100)
 //   region_histogram / region_count    (integral.hpp:111-114)
 //   schedule_stats / estimate_memory   (integral.hpp:116-130)
+//   dump_tensor / load_tensor          (integral.hpp:132-135, the IHT1 wire format)
 //   hist_distance_map                  (likelihood.hpp:59-61)
 // What changes underneath: the tensor lives in HBM as uint32 (exact, h*w < 2^32) and
 // `IntegralHistogramTensor::data` is a host mirror in the reference layout (padded,
@@ -171,6 +172,11 @@ struct MemoryEstimate {
     bool degenerate;
 };
 MemoryEstimate estimate_memory(int w, int h, int bins, int elem_bytes);
+
+// Binary dump (integral.hpp:132-135): magic "IHT1", little-endian u32 bins/h/w/elem_bytes,
+// then the planes in storage order as little-endian u64.  Streamed from / to HBM.
+void dump_tensor(const IntegralHistogramTensor& t, const std::string& path);
+IntegralHistogramTensor load_tensor(const std::string& path);
 
 // ---------------------------------------------------------------- likelihood (likelihood.hpp)
 struct LikelihoodMap {

@@ -145,6 +145,18 @@ spct_status spct_cu_ih_build(const spct_source* src, const spct_ih* out, void* w
  * (height+1) x (width+1) uint64 block with zero padding row/column (dev dst). */
 spct_status spct_cu_ih_export_u64(const spct_ih* t, int k0, int k1, uint64_t* dst, void* stream);
 
+/* IHT1 wire format (integral.hpp:132-135; dump_tensor / load_tensor integral.cpp:619-659):
+ * "IHT1", LE u32 bins/height/width/elem_bytes, then the padded planes as LE elements.
+ * spct_cu_ih_dump streams the device tensor (all of its planes) to `path`; elem_bytes 8 is
+ * the reference format, 4 an extension.  spct_cu_ih_load_header reads and validates the
+ * header (SPCT_ERR_IO with the reference's messages: cannot open / bad magic / truncated
+ * header / unsupported element size / bad dimensions); spct_cu_ih_load fills a device
+ * tensor of matching dims (truncated payload, nonzero padding or a value above 2^32-1 are
+ * SPCT_ERR_IO).  Both synchronise `stream` (host file IO). */
+spct_status spct_cu_ih_dump(const spct_ih* t, const char* path, int elem_bytes, void* stream);
+spct_status spct_cu_ih_load_header(const char* path, int* bins, int* height, int* width, int* elem_bytes);
+spct_status spct_cu_ih_load(const char* path, const spct_ih* t, void* stream);
+
 /* region_histogram / region_count (integral.cpp:561-577), batched: rects (dev) are
  * n x {x, y, w, h} int32; out (dev) is n x t->bins uint32 (counts of planes
  * [0, t->bins)).  Rects are validated on the host by the caller (Rect::inside). */

@@ -42,6 +42,10 @@ class ContractError(ValueError):
     """Oracle-side contract violation (status 2), mirrors spct::contract_error."""
 
 
+class RefIOError(OSError):
+    """Status 3, mirrors spct::io_error."""
+
+
 def _check(st: int, what: str, lib=None):
     if st == 0:
         return
@@ -50,6 +54,8 @@ def _check(st: int, what: str, lib=None):
         msg += ": " + lib.ref_last_error().decode()
     if st == 2:
         raise ContractError(msg)
+    if st == 3:
+        raise RefIOError(msg)
     raise RuntimeError(f"{msg} (status {st})")
 
 
@@ -109,6 +115,8 @@ def _load_ref():
         "ref_estimate_memory": (_i, [_i, _i, _i, _i, C.POINTER(_u64), C.POINTER(_u64), C.POINTER(_i)]),
         "ref_schedule_from_string": (_i, [C.c_char_p]),
         "ref_orientation_bins": (_i, [_u8p, _i, _i, _d, _i, _u16p]),
+        "ref_dump_tensor": (_i, [_vp, C.c_char_p]),
+        "ref_load_tensor": (_i, [C.c_char_p, C.POINTER(_vp)]),
     }
     for name, (res, args) in sig.items():
         f = getattr(lib, name)
@@ -363,6 +371,25 @@ class RefTensor:
         if getattr(self, "_h", None):
             self._lib.ref_ih_free(self._h)
             self._h = None
+
+    def dump(self, path: str) -> None:
+        """dump_tensor (integral.cpp:619-633) of the reference."""
+        _check(self._lib.ref_dump_tensor(self._h, str(path).encode()), "dump_tensor", self._lib)
+
+    @classmethod
+    def load(cls, path: str) -> "RefTensor":
+        """load_tensor (integral.cpp:635-659) of the reference."""
+        lib = reflib()
+        hdl = _vp()
+        _check(lib.ref_load_tensor(str(path).encode(), C.byref(hdl)), "load_tensor", lib)
+        t = cls.__new__(cls)
+        t._lib, t._h = lib, hdl
+        n = int(lib.ref_ih_size(hdl))
+        with open(path, "rb") as f:
+            hdr = np.frombuffer(f.read(20)[4:], np.uint32)
+        t.bins, t.h, t.w = int(hdr[0]), int(hdr[1]), int(hdr[2])
+        assert n == t.bins * (t.h + 1) * (t.w + 1)
+        return t
 
     def array(self) -> np.ndarray:
         n = int(self._lib.ref_ih_size(self._h))

@@ -212,4 +212,13 @@ int ref_orientation_bins(const std::uint8_t* gray, int w, int h, double sigma, i
     });
 }
 
+// dump_tensor / load_tensor (integral.cpp:619-659), the IHT1 wire format.
+int ref_dump_tensor(void* handle, const char* path) {
+    return guarded([&] { spct::dump_tensor(*static_cast<spct::IntegralHistogramTensor*>(handle), path); });
+}
+
+int ref_load_tensor(const char* path, void** out) {
+    return guarded([&] { *out = new spct::IntegralHistogramTensor(spct::load_tensor(path)); });
+}
+
 }  // extern "C"

@@ -9,7 +9,7 @@ interface in Python; include/spct/spct.hpp mirrors it in C++.
 from . import _capi, profiling
 from ._capi import ContractError, SpctError, lib
 from .api import (DEFAULT_BUDGET, IntegralHistogramTensor, ScanSchedule, build_and_match, build_and_match_map,
-                  build_integral_histogram, estimate_memory, hist_distance_map, hist_finalize,
+                  build_integral_histogram, dump_tensor, estimate_memory, load_tensor, hist_distance_map, hist_finalize,
                   hist_match_map, hist_partial, orientation_bins, quantize, region_count, region_histogram,
                   region_histograms, schedule_from_string, schedule_stats, to_grayscale)
 from .channels import CHANNELS, channel_sources, likelihood_channels
@@ -19,5 +19,5 @@ __all__ = [
     "build_and_match", "build_and_match_map", "build_integral_histogram", "estimate_memory", "hist_distance_map",
     "hist_finalize", "hist_match_map", "hist_partial", "quantize", "region_count", "region_histogram",
     "region_histograms", "schedule_from_string", "schedule_stats", "to_grayscale", "orientation_bins",
-    "CHANNELS", "channel_sources", "likelihood_channels",
+    "CHANNELS", "channel_sources", "likelihood_channels", "dump_tensor", "load_tensor",
 ]

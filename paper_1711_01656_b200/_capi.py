@@ -71,6 +71,9 @@ SIGNATURES = {
     "spct_cu_ih_build_match_map": (_i, [_src_p, _ih_p, _vp, _i, _i, _d, _i, _vp, _vp, _sz, _vp]),
     "spct_cu_orientation_workspace": (_i, [_i, _i, C.POINTER(_sz)]),
     "spct_cu_orientation_bins": (_i, [_vp, _i64, _i, _i, _d, _i, _vp, _i64, _vp, _sz, _vp]),
+    "spct_cu_ih_dump": (_i, [_ih_p, C.c_char_p, _i, _vp]),
+    "spct_cu_ih_load_header": (_i, [C.c_char_p, C.POINTER(_i), C.POINTER(_i), C.POINTER(_i), C.POINTER(_i)]),
+    "spct_cu_ih_load": (_i, [C.c_char_p, _ih_p, _vp]),
     "spct_cu_launch_count": (C.c_uint64, []),
     "spct_cu_profile_enable": (None, [_i]),
     "spct_cu_profile_reset": (None, []),

@@ -177,6 +177,22 @@ class IntegralHistogramTensor:
         return self.width + 1
 
 
+def dump_tensor(t: IntegralHistogramTensor, path: str, elem_bytes: int = 8, stream=None) -> None:
+    """integral.cpp:619-633: the IHT1 file of ``t`` (elem_bytes 8 = the reference format;
+    4 = half-size extension the reference loader rejects).  Raises IOError-like SpctError
+    (status 3) where the reference throws io_error."""
+    check(A.lib().spct_cu_ih_dump(C.byref(t.desc), str(path).encode(), int(elem_bytes), _stream(stream)))
+
+
+def load_tensor(path: str, device=None, stream=None) -> IntegralHistogramTensor:
+    """integral.cpp:635-659: an IHT1 file (elem 8, or 4) into a new device tensor."""
+    b, h, w, e = C.c_int(), C.c_int(), C.c_int(), C.c_int()
+    check(A.lib().spct_cu_ih_load_header(str(path).encode(), C.byref(b), C.byref(h), C.byref(w), C.byref(e)))
+    t = IntegralHistogramTensor(w.value, h.value, b.value, device=device)
+    check(A.lib().spct_cu_ih_load(str(path).encode(), C.byref(t.desc), _stream(stream)))
+    return t
+
+
 def estimate_memory(w: int, h: int, bins: int, elem_bytes: int):
     pad, raw, deg = C.c_uint64(), C.c_uint64(), C.c_int()
     check(A.lib().spct_cu_estimate_memory(w, h, bins, elem_bytes, C.byref(pad), C.byref(raw), C.byref(deg)))

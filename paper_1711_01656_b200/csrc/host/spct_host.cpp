@@ -284,6 +284,34 @@ std::uint64_t region_count(const IntegralHistogramTensor& t, int bin, const Rect
     return region_histogram(t, r)[bin];
 }
 
+// IHT1 wire format (integral.cpp:619-659): streamed from / to HBM by the C-ABI.
+void dump_tensor(const IntegralHistogramTensor& t, const std::string& path) {
+    check(spct_cu_ih_dump(&desc_of(t), path.c_str(), 8, nullptr));
+}
+
+IntegralHistogramTensor load_tensor(const std::string& path) {
+    int bins = 0, h = 0, w = 0, elem = 0;
+    check(spct_cu_ih_load_header(path.c_str(), &bins, &h, &w, &elem));
+    auto dt = std::make_shared<detail::DeviceTensor>();
+    spct_ih& d = dt->desc;
+    std::uint64_t bytes = 0;
+    check(spct_cu_ih_layout(w, h, bins, &d.row_pitch, &d.plane_pitch, &bytes));
+    dt->mem = std::make_unique<DevBuf>(bytes);
+    d.data = dt->mem->as<std::uint32_t>();
+    d.bins = bins;
+    d.bin0 = 0;
+    d.nbins_total = bins;
+    d.height = h;
+    d.width = w;
+    check(spct_cu_ih_load(path.c_str(), &d, nullptr));
+    IntegralHistogramTensor t;
+    t.bins = bins;
+    t.height = h;
+    t.width = w;
+    t.data.dev = std::move(dt);
+    return t;
+}
+
 ScheduleStats schedule_stats(int w, int h, int tile, int scan_len) {
     ScheduleStats s{};
     check(spct_cu_schedule_stats(w, h, tile, scan_len, &s.wavefront_iterations, &s.tile_count, &s.scan_efficiency));

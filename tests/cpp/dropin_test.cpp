@@ -180,6 +180,23 @@ int main() {
         for (std::size_t i = 0; i < mf.values.size(); ++i)
             CHECK(std::abs(mf.values[i] - map.values[i]) <= 1e-5 * std::abs(map.values[i]) + 1e-12);
     }
+    {  // IHT1 round trip (test_integral.cpp:208-238)
+        BinMap bm(33, 31, 16);
+        for (std::size_t i = 0; i < bm.data.size(); ++i) bm.data[i] = static_cast<std::uint16_t>((i * 7 + i / 33) % 16);
+        auto t = build_integral_histogram(bm);
+        const std::string path = "/tmp/spct_dropin_t.iht";
+        dump_tensor(t, path);
+        std::FILE* f = std::fopen(path.c_str(), "rb");
+        char head[4] = {};
+        CHECK(f && std::fread(head, 1, 4, f) == 4);
+        if (f) std::fclose(f);
+        CHECK(std::string(head, 4) == "IHT1");
+        auto t2 = load_tensor(path);
+        CHECK(t2.bins == 16 && t2.height == 31 && t2.width == 33);
+        CHECK(t2.data == t.data);
+        CHECK_THROWS_AS(load_tensor("/nonexistent/t.iht"), io_error);
+        std::remove(path.c_str());
+    }
     {  // analytics (test_integral.cpp:155-188)
         auto s = schedule_stats(1024, 1024, 32, 1024);
         CHECK(s.wavefront_iterations == 63 && s.tile_count == 1024);

@@ -131,3 +131,46 @@ def test_python_api_contracts_without_gpu():
     with pytest.raises(P.ContractError):
         P.api._check_budget(16, 16, 4, 64)  # test_integral.cpp:196-198
     P.api._check_budget(16, 16, 4, P.DEFAULT_BUDGET)
+
+
+# ------------------------------------------------------------------ IHT1 (integral.cpp:619-659)
+
+def _hdr(path):
+    b, h, w, e = C.c_int(), C.c_int(), C.c_int(), C.c_int()
+    st = A.lib().spct_cu_ih_load_header(str(path).encode(), C.byref(b), C.byref(h), C.byref(w), C.byref(e))
+    return st, (b.value, h.value, w.value, e.value)
+
+
+@pytest.mark.skipif(not oracle.have_ref(), reason="oracle/_ref not built")
+def test_iht1_header_of_reference_dumps(tmp_path):
+    bm = oracle.random_binmap(13, 7, 5, 31)
+    path = tmp_path / "t.iht"
+    oracle.RefTensor(bm, 5).dump(path)
+    raw = path.read_bytes()
+    assert raw[:4] == b"IHT1" and len(raw) == 20 + 5 * 8 * 14 * 8  # test_integral.cpp:214-228
+    assert _hdr(path) == (0, (5, 7, 13, 8))
+
+
+@pytest.mark.skipif(not oracle.have_ref(), reason="oracle/_ref not built")
+def test_iht1_errors_match_reference(tmp_path):
+    """load_tensor's io_error cases (integral.cpp:636-655), same status and message prefix."""
+    good = tmp_path / "g.iht"
+    oracle.RefTensor(oracle.random_binmap(6, 4, 3, 5), 3).dump(good)
+    raw = good.read_bytes()
+    cases = {"/nonexistent/t.iht": "cannot open tensor",  # test_integral.cpp:237
+             "magic": "bad tensor magic", "short": "truncated tensor header", "elem": "unsupported element size",
+             "dims": "bad tensor dimensions"}
+    for name, msg in cases.items():
+        p = name if name.startswith("/") else tmp_path / f"{name}.iht"
+        if name == "magic":
+            p.write_bytes(b"IHT2" + raw[4:])
+        elif name == "short":
+            p.write_bytes(raw[:13])
+        elif name == "elem":
+            p.write_bytes(raw[:16] + (5).to_bytes(4, "little") + raw[20:])
+        elif name == "dims":
+            p.write_bytes(raw[:4] + (0).to_bytes(4, "little") + raw[8:])
+        st, _ = _hdr(p)
+        assert st == A.SPCT_ERR_IO and A.lib().spct_cu_last_error().decode().startswith(msg), name
+        with pytest.raises(oracle.RefIOError, match=msg):
+            oracle.RefTensor.load(p)

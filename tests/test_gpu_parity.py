@@ -448,3 +448,62 @@ def test_tracking_batch_channels(P, frames):
             got = maps[c].cpu().numpy()
             assert close(got, want), c
             assert got[y0 + (kh - 1) // 2, x0 + (kw - 1) // 2] == 1.0, c  # the template's own window
+
+
+# ------------------------------------------------------------------ IHT1 wire format
+
+@pytest.mark.parametrize("w,h,bins", [(1, 1, 8), (70, 129, 16), (257, 140, 37)])
+def test_iht1_dump_is_byte_identical_to_reference(P, tmp_path, w, h, bins):
+    """dump_tensor of the device tensor == the reference's dump_tensor of the same BinMap
+    (integral.cpp:619-633), and both load back (either loader) to the same tensor."""
+    bm = oracle.random_binmap(w, h, bins, 900 + w)
+    t = P.build_integral_histogram(bm, bins)
+    mine, ref = tmp_path / "mine.iht", tmp_path / "ref.iht"
+    P.dump_tensor(t, mine)
+    if oracle.have_ref():
+        oracle.RefTensor(bm, bins).dump(ref)
+        assert mine.read_bytes() == ref.read_bytes()
+        assert np.array_equal(oracle.RefTensor.load(mine).array(), oracle.build_ih(bm, bins))
+        assert np.array_equal(P.load_tensor(ref).padded_u64(), oracle.build_ih(bm, bins))
+    assert np.array_equal(P.load_tensor(mine).padded_u64(), oracle.build_ih(bm, bins))
+
+
+def test_iht1_chunked_and_elem4(P, tmp_path):
+    """A plane larger than one 32 MiB staging chunk, and the elem_bytes = 4 extension."""
+    w, h, bins = 2304, 1900, 3
+    img = oracle.smooth_image(w, h, 77)
+    t = P.build_integral_histogram(img, bins)
+    want = t.padded_u64()
+    p8, p4 = tmp_path / "t8.iht", tmp_path / "t4.iht"
+    P.dump_tensor(t, p8)
+    P.dump_tensor(t, p4, elem_bytes=4)
+    assert p8.stat().st_size == 20 + want.size * 8 and p4.stat().st_size == 20 + want.size * 4
+    hdr = np.frombuffer(p8.read_bytes()[:20][4:], np.uint32)
+    assert list(hdr) == [bins, h, w, 8]
+    assert np.array_equal(np.fromfile(p8, np.uint64, offset=20).reshape(want.shape), want)
+    assert np.array_equal(P.load_tensor(p8).padded_u64(), want)
+    assert np.array_equal(P.load_tensor(p4).padded_u64(), want)
+
+
+def test_iht1_load_rejects_bad_payloads(P, tmp_path):
+    bm = oracle.random_binmap(9, 6, 4, 3)
+    t = P.build_integral_histogram(bm, 4)
+    good = tmp_path / "g.iht"
+    P.dump_tensor(t, good)
+    raw = bytearray(good.read_bytes())
+    (tmp_path / "trunc.iht").write_bytes(bytes(raw[:-8]))
+    with pytest.raises(P.SpctError, match="truncated tensor payload"):  # integral.cpp:655
+        P.load_tensor(tmp_path / "trunc.iht")
+    pad = bytearray(raw)
+    pad[20:28] = (1).to_bytes(8, "little")  # cell (0, 0, 0) is padding
+    (tmp_path / "pad.iht").write_bytes(bytes(pad))
+    with pytest.raises(P.SpctError, match="nonzero padding"):
+        P.load_tensor(tmp_path / "pad.iht")
+    big = bytearray(raw)
+    off = 20 + 8 * (1 * 10 + 1)  # plane 0, row 1, column 1
+    big[off:off + 8] = (1 << 33).to_bytes(8, "little")
+    (tmp_path / "big.iht").write_bytes(bytes(big))
+    with pytest.raises(P.SpctError, match="exceeds the uint32"):
+        P.load_tensor(tmp_path / "big.iht")
+    with pytest.raises(P.SpctError, match="cannot write tensor"):
+        P.dump_tensor(t, "/nonexistent/dir/t.iht")
