@@ -9,6 +9,7 @@
 //   schedule_stats / estimate_memory   (integral.hpp:116-130)
 //   dump_tensor / load_tensor          (integral.hpp:132-135, the IHT1 wire format)
 //   hist_distance_map                  (likelihood.hpp:59-61)
+//   fuse_maps / find_peaks / score_map (likelihood.hpp:63-88), camshift_refine (tracker.hpp:62-64)
 // What changes underneath: the tensor lives in HBM as uint32 (exact, h*w < 2^32) and
 // `IntegralHistogramTensor::data` is a host mirror in the reference layout (padded,
 // uint64) that is materialised from the device only when a caller touches it.
@@ -189,6 +190,26 @@ struct LikelihoodMap {
 
 LikelihoodMap hist_distance_map(const IntegralHistogramTensor& t, const std::vector<double>& template_hist, int kw,
                                 int kh, double p = 1.0);
+
+// Map consumers (likelihood.hpp:63-88), computed on the device, bit-identical.
+LikelihoodMap fuse_maps(const std::vector<LikelihoodMap>& maps, std::vector<double> weights = {});
+
+struct Peak {
+    int x = 0, y = 0;
+    double height = 0.0;
+    int rank = 0;  // 1 = highest
+};
+std::vector<Peak> find_peaks(const LikelihoodMap& map);
+int score_map(const LikelihoodMap& map, const Rect& gt);
+
+// camshift_refine (tracker.hpp:54-64; the reference declares it next to its Eigen tracker).
+struct CamshiftResult {
+    double cx = 0, cy = 0;
+    int iterations = 0;
+    bool zero_mass = false;  // window mass was zero; center left at init
+};
+CamshiftResult camshift_refine(const LikelihoodMap& map, double cx, double cy, int win_w, int win_h,
+                               double delta = 0.5, int max_iter = 20);
 
 // ---------------------------------------------------------------- extensions (not in the reference)
 enum class HistMetric { Minkowski = 0, Intersection = 1, Bhattacharyya = 2, ChiSquare = 3 };

@@ -145,6 +145,27 @@ spct_status spct_cu_ih_build(const spct_source* src, const spct_ih* out, void* w
  * (height+1) x (width+1) uint64 block with zero padding row/column (dev dst). */
 spct_status spct_cu_ih_export_u64(const spct_ih* t, int k0, int k1, uint64_t* dst, void* stream);
 
+/* ----------------------------------------------------------------- map consumers
+ * (likelihood.cpp:257-330, tracker.cpp:77-113), bit-identical to the reference.
+ * fuse_maps: `maps` is a host array of nmaps device pointers to n doubles each; weights a
+ *   host array (nweights == 0: equal weights).  Contract: likelihood.cpp:258-269.
+ * find_peaks: peaks of the (w x h) device map sorted by height (descending, ties in
+ *   row-major order); the first min(count, max_out) go to xs / ys / heights (device);
+ *   rank = index + 1.  Synchronises `stream` (count).
+ * score_map: rank of the best peak inside gt (count + 1 if none).  Synchronises.
+ * camshift: one refinement per start point (host arrays: starts, out = 2n doubles,
+ *   iterations, zero_mass); synchronises. */
+spct_status spct_cu_fuse_maps(const double* const* maps, int nmaps, const double* weights, int nweights, int64_t n,
+                              double* out, void* stream);
+spct_status spct_cu_find_peaks_workspace(int w, int h, size_t* bytes);
+spct_status spct_cu_find_peaks(const double* map, int w, int h, int32_t* xs, int32_t* ys, double* heights,
+                               int64_t max_out, int64_t* count, void* workspace, size_t workspace_bytes, void* stream);
+spct_status spct_cu_score_map(const double* map, int w, int h, int gx, int gy, int gw, int gh, int64_t* rank,
+                              void* workspace, size_t workspace_bytes, void* stream);
+spct_status spct_cu_camshift(const double* map, int w, int h, const double* starts, int n, int win_w, int win_h,
+                             double delta, int max_iter, double* out, int32_t* iterations, int32_t* zero_mass,
+                             void* stream);
+
 /* IHT1 wire format (integral.hpp:132-135; dump_tensor / load_tensor integral.cpp:619-659):
  * "IHT1", LE u32 bins/height/width/elem_bytes, then the padded planes as LE elements.
  * spct_cu_ih_dump streams the device tensor (all of its planes) to `path`; elem_bytes 8 is

@@ -35,6 +35,7 @@ _u16p = np.ctypeslib.ndpointer(np.uint16, flags="C_CONTIGUOUS")
 _u32p = np.ctypeslib.ndpointer(np.uint32, flags="C_CONTIGUOUS")
 _u64p = np.ctypeslib.ndpointer(np.uint64, flags="C_CONTIGUOUS")
 _f64p = np.ctypeslib.ndpointer(np.float64, flags="C_CONTIGUOUS")
+_i32p = np.ctypeslib.ndpointer(np.int32, flags="C_CONTIGUOUS")
 _i, _u32, _u64, _i64, _d, _vp = C.c_int, C.c_uint32, C.c_uint64, C.c_int64, C.c_double, C.c_void_p
 
 
@@ -79,6 +80,11 @@ def _load_c():
         "or_hist_finalize": (_i, [_f64p, _i, _i, _i, _i, _d, _f64p]),
         "or_xorshift_image": (None, [_u32, _i64, _u8p]),
         "or_orientation_bins": (_i, [_u8p, _i, _i, _d, _i, _u16p]),
+        "or_fuse_maps": (_i, [C.POINTER(_vp), _i, _vp, _i64, _f64p]),
+        "or_find_peaks": (_i, [_f64p, _i, _i, _i32p, _i32p, _f64p, _i, C.POINTER(_i)]),
+        "or_score_map": (_i, [_f64p, _i, _i, _i, _i, _i, _i, C.POINTER(_i)]),
+        "or_camshift": (_i, [_f64p, _i, _i, _d, _d, _i, _i, _d, _i, C.POINTER(_d), C.POINTER(_d), C.POINTER(_i),
+                             C.POINTER(_i)]),
         "fx_noise_image": (None, [_i, _i, _u32, _u8p]),
         "fx_smooth_image": (None, [_i, _i, _u32, _i, _u8p]),
         "fx_noise_color": (None, [_i, _i, _u32, _u8p, _u8p, _u8p]),
@@ -116,6 +122,9 @@ def _load_ref():
         "ref_schedule_from_string": (_i, [C.c_char_p]),
         "ref_orientation_bins": (_i, [_u8p, _i, _i, _d, _i, _u16p]),
         "ref_dump_tensor": (_i, [_vp, C.c_char_p]),
+        "ref_fuse_maps": (_i, [C.POINTER(_vp), _i, _vp, _i, _i, _i, _f64p]),
+        "ref_find_peaks": (_i, [_f64p, _i, _i, _i32p, _i32p, _f64p, _i32p, _i, C.POINTER(_i)]),
+        "ref_score_map": (_i, [_f64p, _i, _i, _i, _i, _i, _i, C.POINTER(_i)]),
         "ref_load_tensor": (_i, [C.c_char_p, C.POINTER(_vp)]),
     }
     for name, (res, args) in sig.items():
@@ -320,6 +329,84 @@ def ref_orientation_bins(gray: np.ndarray, bins: int, sigma: float = 1.0) -> np.
     _check(reflib().ref_orientation_bins(gray.reshape(-1), w, h, sigma, bins, out.reshape(-1)), "orientation_bins",
            reflib())
     return out
+
+
+def _ptrs(maps):
+    arrs = [np.ascontiguousarray(m, np.float64) for m in maps]
+    return arrs, (_vp * max(1, len(arrs)))(*[a.ctypes.data for a in arrs])
+
+
+def fuse_maps(maps, weights=None) -> np.ndarray:
+    """likelihood.cpp:257-283 (C restatement)."""
+    arrs, ptrs = _ptrs(maps)
+    if not arrs:
+        raise ContractError("fuse_maps: no maps to fuse")
+    if any(a.shape != arrs[0].shape for a in arrs):
+        raise ContractError("fuse_maps: map dimensions differ")
+    if weights is not None and len(weights) != len(arrs):
+        raise ContractError("fuse_maps: weight count mismatch")
+    wv = None if weights is None else np.ascontiguousarray(weights, np.float64)
+    out = np.empty(arrs[0].shape, np.float64)
+    _check(clib().or_fuse_maps(ptrs, len(arrs), None if wv is None else wv.ctypes.data, arrs[0].size,
+                               out.reshape(-1)), "fuse_maps")
+    return out
+
+
+def ref_fuse_maps(maps, weights=None) -> np.ndarray:
+    arrs, ptrs = _ptrs(maps)
+    wv = np.ascontiguousarray([] if weights is None else weights, np.float64)
+    h, w = arrs[0].shape if arrs else (0, 0)
+    out = np.empty((h, w), np.float64)
+    _check(reflib().ref_fuse_maps(ptrs, len(arrs), wv.ctypes.data, wv.size, w, h, out.reshape(-1)), "fuse_maps",
+           reflib())
+    return out
+
+
+def find_peaks(m: np.ndarray):
+    """likelihood.cpp:285-322: (xs, ys, heights) sorted by height desc (rank = index + 1)."""
+    m = np.ascontiguousarray(m, np.float64)
+    h, w = m.shape
+    xs, ys, hs = np.empty(w * h, np.int32), np.empty(w * h, np.int32), np.empty(w * h, np.float64)
+    n = _i()
+    _check(clib().or_find_peaks(m.reshape(-1), w, h, xs, ys, hs, w * h, C.byref(n)), "find_peaks")
+    return xs[:n.value], ys[:n.value], hs[:n.value]
+
+
+def ref_find_peaks(m: np.ndarray):
+    m = np.ascontiguousarray(m, np.float64)
+    h, w = m.shape
+    xs, ys, hs, rk = (np.empty(w * h, np.int32), np.empty(w * h, np.int32), np.empty(w * h, np.float64),
+                      np.empty(w * h, np.int32))
+    n = _i()
+    _check(reflib().ref_find_peaks(m.reshape(-1), w, h, xs, ys, hs, rk, w * h, C.byref(n)), "find_peaks", reflib())
+    assert np.array_equal(rk[:n.value], np.arange(1, n.value + 1))
+    return xs[:n.value], ys[:n.value], hs[:n.value]
+
+
+def score_map(m: np.ndarray, gx: int, gy: int, gw: int, gh: int) -> int:
+    m = np.ascontiguousarray(m, np.float64)
+    h, w = m.shape
+    r = _i()
+    _check(clib().or_score_map(m.reshape(-1), w, h, gx, gy, gw, gh, C.byref(r)), "score_map")
+    return r.value
+
+
+def ref_score_map(m: np.ndarray, gx: int, gy: int, gw: int, gh: int) -> int:
+    m = np.ascontiguousarray(m, np.float64)
+    h, w = m.shape
+    r = _i()
+    _check(reflib().ref_score_map(m.reshape(-1), w, h, gx, gy, gw, gh, C.byref(r)), "score_map", reflib())
+    return r.value
+
+
+def camshift(m: np.ndarray, cx: float, cy: float, win_w: int, win_h: int, delta: float = 0.5, max_iter: int = 20):
+    """tracker.cpp:77-113: (cx, cy, iterations, zero_mass)."""
+    m = np.ascontiguousarray(m, np.float64)
+    h, w = m.shape
+    ox, oy, it, zm = _d(), _d(), _i(), _i()
+    _check(clib().or_camshift(m.reshape(-1), w, h, cx, cy, win_w, win_h, delta, max_iter, C.byref(ox), C.byref(oy),
+                              C.byref(it), C.byref(zm)), "camshift_refine")
+    return ox.value, oy.value, it.value, bool(zm.value)
 
 
 def hist_finalize(dsum, w, h, kw, kh, p) -> np.ndarray:

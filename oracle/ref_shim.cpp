@@ -212,6 +212,44 @@ int ref_orientation_bins(const std::uint8_t* gray, int w, int h, double sigma, i
     });
 }
 
+// Map consumers (likelihood.cpp:257-330).
+namespace {
+spct::LikelihoodMap make_map(const double* v, int w, int h) {
+    spct::LikelihoodMap m;
+    m.width = w;
+    m.height = h;
+    m.values.assign(v, v + static_cast<std::size_t>(w) * h);
+    return m;
+}
+}  // namespace
+
+int ref_fuse_maps(const double* const* maps, int nmaps, const double* weights, int nweights, int w, int h, double* out) {
+    return guarded([&] {
+        std::vector<spct::LikelihoodMap> ms;
+        for (int m = 0; m < nmaps; ++m) ms.push_back(make_map(maps[m], w, h));
+        std::vector<double> wv(weights, weights + nweights);
+        const spct::LikelihoodMap f = spct::fuse_maps(ms, wv);
+        std::memcpy(out, f.values.data(), f.values.size() * sizeof(double));
+    });
+}
+
+int ref_find_peaks(const double* map, int w, int h, int* xs, int* ys, double* hs, int* ranks, int max_out, int* count) {
+    return guarded([&] {
+        const auto pk = spct::find_peaks(make_map(map, w, h));
+        *count = static_cast<int>(pk.size());
+        for (int i = 0; i < static_cast<int>(pk.size()) && i < max_out; ++i) {
+            xs[i] = pk[i].x;
+            ys[i] = pk[i].y;
+            hs[i] = pk[i].height;
+            ranks[i] = pk[i].rank;
+        }
+    });
+}
+
+int ref_score_map(const double* map, int w, int h, int gx, int gy, int gw, int gh, int* rank) {
+    return guarded([&] { *rank = spct::score_map(make_map(map, w, h), spct::Rect{gx, gy, gw, gh}); });
+}
+
 // dump_tensor / load_tensor (integral.cpp:619-659), the IHT1 wire format.
 int ref_dump_tensor(void* handle, const char* path) {
     return guarded([&] { spct::dump_tensor(*static_cast<spct::IntegralHistogramTensor*>(handle), path); });

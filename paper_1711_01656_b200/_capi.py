@@ -74,6 +74,12 @@ SIGNATURES = {
     "spct_cu_ih_dump": (_i, [_ih_p, C.c_char_p, _i, _vp]),
     "spct_cu_ih_load_header": (_i, [C.c_char_p, C.POINTER(_i), C.POINTER(_i), C.POINTER(_i), C.POINTER(_i)]),
     "spct_cu_ih_load": (_i, [C.c_char_p, _ih_p, _vp]),
+    "spct_cu_fuse_maps": (_i, [C.POINTER(_vp), _i, C.POINTER(_d), _i, _i64, _vp, _vp]),
+    "spct_cu_find_peaks_workspace": (_i, [_i, _i, C.POINTER(_sz)]),
+    "spct_cu_find_peaks": (_i, [_vp, _i, _i, _vp, _vp, _vp, _i64, C.POINTER(_i64), _vp, _sz, _vp]),
+    "spct_cu_score_map": (_i, [_vp, _i, _i, _i, _i, _i, _i, C.POINTER(_i64), _vp, _sz, _vp]),
+    "spct_cu_camshift": (_i, [_vp, _i, _i, C.POINTER(_d), _i, _i, _i, _d, _i, C.POINTER(_d), C.POINTER(C.c_int32),
+                              C.POINTER(C.c_int32), _vp]),
     "spct_cu_launch_count": (C.c_uint64, []),
     "spct_cu_profile_enable": (None, [_i]),
     "spct_cu_profile_reset": (None, []),

@@ -1,0 +1,484 @@
+// Likelihood-map consumers on the device: the step after the map,
+// so a tracker need not copy each map to the host.
+//
+//   fuse_maps        likelihood.cpp:257-283  weighted sum (weights normalised on the host
+//                                            exactly as the reference), map-by-map FP64
+//                                            accumulation in the reference order, clamp01
+//   find_peaks       likelihood.cpp:285-322  3x3 in-bounds mean (same summation order),
+//                                            strict 8-neighbour maxima with the 1e-9 flat
+//                                            margin, deterministic row-major compaction, then
+//                                            a stable LSD radix sort by height (descending)
+//   score_map        likelihood.cpp:324-330  rank of the best peak inside gt (k + 1 if none)
+//   camshift_refine  tracker.cpp:77-113      one thread per start point, the reference's
+//                                            sequential window sums (same rounding)
+// All results are bit-identical to the reference (no reassociation, no FMA contraction).
+#include <cmath>
+#include <vector>
+
+#include "spct_internal.h"
+
+using namespace spct_impl;
+
+namespace spct_cons {
+
+constexpr int kMaxFuse = 8;
+
+struct FuseArgs {
+    const double* maps[kMaxFuse];
+    double wt[kMaxFuse];
+    int nmaps, first, last;
+};
+
+__device__ __forceinline__ double clamp01(double v) { return v < 0.0 ? 0.0 : (v > 1.0 ? 1.0 : v); }
+
+__global__ void fuse_kernel(FuseArgs a, int64_t n, double* __restrict__ out) {
+    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        double acc = a.first ? 0.0 : out[i];
+        for (int m = 0; m < a.nmaps; ++m) acc = __dadd_rn(acc, __dmul_rn(a.wt[m], __ldg(a.maps[m] + i)));
+        out[i] = a.last ? clamp01(acc) : acc;
+    }
+}
+
+// ---------------------------------------------------------------- find_peaks
+
+constexpr int kPeakTile = 1024;   // pixels per compaction block (256 threads x 4)
+constexpr int kSortTile = 2048;   // keys per radix block (256 threads x 8)
+
+__global__ void smooth3_kernel(const double* __restrict__ map, int w, int h, double* __restrict__ s) {
+    const int64_t n = static_cast<int64_t>(w) * h;
+    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int y = static_cast<int>(i / w), x = static_cast<int>(i % w);
+        double acc = 0.0;
+        int cnt = 0;
+        for (int dy = -1; dy <= 1; ++dy)
+            for (int dx = -1; dx <= 1; ++dx) {
+                const int nx = x + dx, ny = y + dy;
+                if (nx < 0 || ny < 0 || nx >= w || ny >= h) continue;
+                acc = __dadd_rn(acc, map[static_cast<int64_t>(ny) * w + nx]);
+                ++cnt;
+            }
+        s[i] = __ddiv_rn(acc, static_cast<double>(cnt));
+    }
+}
+
+__device__ __forceinline__ bool is_peak(const double* s, int w, int h, int64_t i) {
+    const int y = static_cast<int>(i / w), x = static_cast<int>(i % w);
+    const double v = s[i];
+    for (int dy = -1; dy <= 1; ++dy)
+        for (int dx = -1; dx <= 1; ++dx) {
+            if (dx == 0 && dy == 0) continue;
+            const int nx = x + dx, ny = y + dy;
+            if (nx < 0 || ny < 0 || nx >= w || ny >= h) continue;
+            if (__dadd_rn(s[static_cast<int64_t>(ny) * w + nx], 1e-9) >= v) return false;
+        }
+    return true;
+}
+
+// Block-wide exclusive scan of one value per thread (256 threads); returns the total too.
+__device__ __forceinline__ uint32_t block_excl_scan(uint32_t v, uint32_t* total, uint32_t* wsum) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    uint32_t inc = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t t = __shfl_up_sync(0xffffffffu, inc, o);
+        if (lane >= o) inc += t;
+    }
+    if (lane == 31) wsum[warp] = inc;
+    __syncthreads();
+    uint32_t off = 0, tot = 0;
+    for (int k = 0; k < 8; ++k) {
+        if (k < warp) off += wsum[k];
+        tot += wsum[k];
+    }
+    __syncthreads();
+    *total = tot;
+    return off + inc - v;
+}
+
+__global__ void __launch_bounds__(256) peak_count_kernel(const double* __restrict__ s, int w, int h,
+                                                         uint32_t* __restrict__ bcount) {
+    __shared__ uint32_t wsum[8];
+    const int64_t n = static_cast<int64_t>(w) * h;
+    const int64_t base = static_cast<int64_t>(blockIdx.x) * kPeakTile + 4 * threadIdx.x;
+    uint32_t c = 0;
+    for (int j = 0; j < 4; ++j)
+        if (base + j < n && is_peak(s, w, h, base + j)) ++c;
+    uint32_t tot;
+    block_excl_scan(c, &tot, wsum);
+    if (threadIdx.x == 0) bcount[blockIdx.x] = tot;
+}
+
+// Single-CTA exclusive scan of n values in place (1024 threads, sequential chunks).
+__global__ void __launch_bounds__(1024) excl_scan_kernel(uint32_t* __restrict__ v, int64_t n, uint32_t* total) {
+    __shared__ uint32_t wsum[32];
+    __shared__ uint32_t carry;
+    if (threadIdx.x == 0) carry = 0;
+    __syncthreads();
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    for (int64_t b = 0; b < n; b += 1024) {
+        const int64_t i = b + threadIdx.x;
+        const uint32_t x = i < n ? v[i] : 0u;
+        uint32_t inc = x;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t t = __shfl_up_sync(0xffffffffu, inc, o);
+            if (lane >= o) inc += t;
+        }
+        if (lane == 31) wsum[warp] = inc;
+        __syncthreads();
+        if (warp == 0) {
+            const uint32_t ws = wsum[lane];
+            uint32_t wi = ws;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t t = __shfl_up_sync(0xffffffffu, wi, o);
+                if (lane >= o) wi += t;
+            }
+            wsum[lane] = wi - ws;  // exclusive warp offsets
+        }
+        __syncthreads();
+        const uint32_t c0 = carry;
+        if (i < n) v[i] = c0 + wsum[warp] + inc - x;
+        __syncthreads();
+        if (threadIdx.x == 1023) carry = c0 + wsum[warp] + inc;
+        __syncthreads();
+    }
+    if (threadIdx.x == 0 && total) *total = carry;
+}
+
+// Descending order of heights as ascending uint64 keys.
+__device__ __forceinline__ uint64_t desc_key(double h) {
+    const uint64_t u = static_cast<uint64_t>(__double_as_longlong(h));
+    const uint64_t asc = (u >> 63) ? ~u : (u | 0x8000000000000000ull);
+    return ~asc;
+}
+
+__global__ void __launch_bounds__(256) peak_compact_kernel(const double* __restrict__ s, int w, int h,
+                                                           const uint32_t* __restrict__ boff,
+                                                           uint64_t* __restrict__ keys, uint32_t* __restrict__ idx) {
+    __shared__ uint32_t wsum[8];
+    const int64_t n = static_cast<int64_t>(w) * h;
+    const int64_t base = static_cast<int64_t>(blockIdx.x) * kPeakTile + 4 * threadIdx.x;
+    bool f[4];
+    uint32_t c = 0;
+    for (int j = 0; j < 4; ++j) {
+        f[j] = base + j < n && is_peak(s, w, h, base + j);
+        c += f[j];
+    }
+    uint32_t tot;
+    uint32_t pos = boff[blockIdx.x] + block_excl_scan(c, &tot, wsum);
+    for (int j = 0; j < 4; ++j)
+        if (f[j]) {
+            keys[pos] = desc_key(s[base + j]);
+            idx[pos] = static_cast<uint32_t>(base + j);
+            ++pos;
+        }
+}
+
+// Radix pass p: digit (key >> 8p) & 255.  counts are digit-major: counts[d * nblk + b].
+__global__ void __launch_bounds__(256) radix_hist_kernel(const uint64_t* __restrict__ keys, int64_t n, int shift,
+                                                         int nblk, uint32_t* __restrict__ counts) {
+    __shared__ uint32_t c[256];
+    c[threadIdx.x] = 0;
+    __syncthreads();
+    const int64_t base = static_cast<int64_t>(blockIdx.x) * kSortTile;
+    for (int j = threadIdx.x; j < kSortTile; j += 256)
+        if (base + j < n) atomicAdd(&c[(keys[base + j] >> shift) & 255u], 1u);
+    __syncthreads();
+    counts[static_cast<int64_t>(threadIdx.x) * nblk + blockIdx.x] = c[threadIdx.x];
+}
+
+// Stable scatter: elements are ranked in index order (round-major, then thread order).
+__global__ void __launch_bounds__(256) radix_scatter_kernel(const uint64_t* __restrict__ kin,
+                                                            const uint32_t* __restrict__ vin, int64_t n, int shift,
+                                                            int nblk, const uint32_t* __restrict__ offs,
+                                                            uint64_t* __restrict__ kout, uint32_t* __restrict__ vout) {
+    __shared__ uint32_t run[256];       // per digit: elements of this block already placed
+    __shared__ uint32_t wcnt[8][256];   // this round's per-warp digit counts, then prefixes
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    run[threadIdx.x] = offs[static_cast<int64_t>(threadIdx.x) * nblk + blockIdx.x];
+    const int64_t base = static_cast<int64_t>(blockIdx.x) * kSortTile;
+    for (int r = 0; r < kSortTile / 256; ++r) {
+        for (int k = 0; k < 8; ++k) wcnt[k][threadIdx.x] = 0;
+        __syncthreads();
+        const int64_t i = base + r * 256 + threadIdx.x;
+        const bool live = i < n;
+        const uint64_t key = live ? kin[i] : 0;
+        const uint32_t d = live ? static_cast<uint32_t>((key >> shift) & 255u) : 256u;
+        const uint32_t peers = __match_any_sync(0xffffffffu, d);
+        const uint32_t rank = __popc(peers & ((1u << lane) - 1u));
+        if (live && rank == 0) wcnt[warp][d] = __popc(peers);
+        __syncthreads();
+        uint32_t acc = 0;  // thread = digit: exclusive prefix over the warps, round total
+        for (int k = 0; k < 8; ++k) {
+            const uint32_t c = wcnt[k][threadIdx.x];
+            wcnt[k][threadIdx.x] = acc;
+            acc += c;
+        }
+        __syncthreads();
+        if (live) {
+            const uint32_t pos = run[d] + wcnt[warp][d] + rank;
+            kout[pos] = key;
+            vout[pos] = vin[i];
+        }
+        __syncthreads();
+        run[threadIdx.x] += acc;
+    }
+}
+
+__global__ void peak_gather_kernel(const uint32_t* __restrict__ idx, const double* __restrict__ s, int w, int64_t n,
+                                   int32_t* __restrict__ xs, int32_t* __restrict__ ys, double* __restrict__ hs) {
+    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const uint32_t p = idx[i];
+        xs[i] = static_cast<int32_t>(p % static_cast<uint32_t>(w));
+        ys[i] = static_cast<int32_t>(p / static_cast<uint32_t>(w));
+        hs[i] = s[p];
+    }
+}
+
+// First sorted position whose peak lies inside gt (min over a device counter).
+__global__ void score_kernel(const uint32_t* __restrict__ idx, int64_t n, int w, int gx, int gy, int gw, int gh,
+                             unsigned* __restrict__ best) {
+    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const uint32_t p = idx[i];
+        const int x = static_cast<int>(p % static_cast<uint32_t>(w)), y = static_cast<int>(p / static_cast<uint32_t>(w));
+        if (x >= gx && x < gx + gw && y >= gy && y < gy + gh) atomicMin(best, static_cast<unsigned>(i));
+    }
+}
+
+// ---------------------------------------------------------------- camshift_refine
+
+__global__ void camshift_kernel(const double* __restrict__ map, int w, int h, const double* __restrict__ starts,
+                                int n, int win_w, int win_h, double delta, int max_iter, double* __restrict__ out,
+                                int32_t* __restrict__ iters, int32_t* __restrict__ zero_mass) {
+    const int q = blockIdx.x * blockDim.x + threadIdx.x;
+    if (q >= n) return;
+    double cx = starts[2 * q], cy = starts[2 * q + 1];
+    int it_done = 0, zm = 0;
+    for (int it = 0; it < max_iter; ++it) {
+        const int x0 = static_cast<int>(llround(__dsub_rn(cx, (win_w - 1) / 2.0)));
+        const int y0 = static_cast<int>(llround(__dsub_rn(cy, (win_h - 1) / 2.0)));
+        const int xa = max(x0, 0), ya = max(y0, 0), xb = min(x0 + win_w, w), yb = min(y0 + win_h, h);
+        double m00 = 0.0, m10 = 0.0, m01 = 0.0;
+        for (int y = ya; y < yb; ++y)
+            for (int x = xa; x < xb; ++x) {
+                const double p = map[static_cast<int64_t>(y) * w + x];
+                m00 = __dadd_rn(m00, p);
+                m10 = __dadd_rn(m10, __dmul_rn(static_cast<double>(x), p));
+                m01 = __dadd_rn(m01, __dmul_rn(static_cast<double>(y), p));
+            }
+        if (m00 <= 0.0) {
+            zm = 1;
+            break;
+        }
+        const double nx = __ddiv_rn(m10, m00), ny = __ddiv_rn(m01, m00);
+        const double d = hypot(__dsub_rn(nx, cx), __dsub_rn(ny, cy));
+        cx = nx;
+        cy = ny;
+        ++it_done;
+        if (d < delta) break;
+    }
+    out[2 * q] = cx;
+    out[2 * q + 1] = cy;
+    iters[q] = it_done;
+    zero_mass[q] = zm;
+}
+
+int grid1(int64_t n) { return static_cast<int>(std::min<int64_t>(std::max<int64_t>((n + 255) / 256, 1), 148 * 16)); }
+
+struct PeakWs {
+    double* s;
+    uint32_t* bcount;
+    uint64_t* k[2];
+    uint32_t* v[2];
+    uint32_t* counts;
+    uint32_t* scalars;  // [0] total peaks, [1] score best
+};
+
+size_t peak_ws_bytes(int w, int h, int64_t* nblk_peak, int64_t* nblk_sort) {
+    const int64_t n = static_cast<int64_t>(w) * h;
+    const int64_t cap = n / 4 + 2;  // strict 8-neighbour maxima: at most one per 2 x 2 cell
+    *nblk_peak = ceil_div(n, kPeakTile);
+    *nblk_sort = std::max<int64_t>(1, ceil_div(cap, kSortTile));
+    auto r = [](int64_t b) { return static_cast<size_t>(round_up(b, 256)); };
+    return r(n * 8) + r(*nblk_peak * 4) + 2 * r(cap * 8) + 2 * r(cap * 4) + r(256 * *nblk_sort * 4) + r(16);
+}
+
+PeakWs carve(void* ws, int w, int h) {
+    int64_t nbp, nbs;
+    peak_ws_bytes(w, h, &nbp, &nbs);
+    const int64_t n = static_cast<int64_t>(w) * h, cap = n / 4 + 2;
+    char* p = static_cast<char*>(ws);
+    auto take = [&](int64_t bytes) {
+        char* q = p;
+        p += round_up(bytes, 256);
+        return q;
+    };
+    PeakWs s;
+    s.s = reinterpret_cast<double*>(take(n * 8));
+    s.bcount = reinterpret_cast<uint32_t*>(take(nbp * 4));
+    s.k[0] = reinterpret_cast<uint64_t*>(take(cap * 8));
+    s.k[1] = reinterpret_cast<uint64_t*>(take(cap * 8));
+    s.v[0] = reinterpret_cast<uint32_t*>(take(cap * 4));
+    s.v[1] = reinterpret_cast<uint32_t*>(take(cap * 4));
+    s.counts = reinterpret_cast<uint32_t*>(take(256 * nbs * 4));
+    s.scalars = reinterpret_cast<uint32_t*>(take(16));
+    return s;
+}
+
+// Peaks of `map` sorted (keys/values end in k[0]/v[0]); returns the count (synchronises).
+spct_status sorted_peaks(const double* map, int w, int h, void* ws, size_t ws_bytes, cudaStream_t st, PeakWs* out,
+                         int64_t* count) {
+    int64_t nbp, nbs;
+    if (!ws || ws_bytes < peak_ws_bytes(w, h, &nbp, &nbs)) return contract("find_peaks: workspace too small");
+    PeakWs P = carve(ws, w, h);
+    const int64_t n = static_cast<int64_t>(w) * h;
+    smooth3_kernel<<<grid1(n), 256, 0, st>>>(map, w, h, P.s);
+    peak_count_kernel<<<static_cast<unsigned>(nbp), 256, 0, st>>>(P.s, w, h, P.bcount);
+    excl_scan_kernel<<<1, 1024, 0, st>>>(P.bcount, nbp, P.scalars);
+    peak_compact_kernel<<<static_cast<unsigned>(nbp), 256, 0, st>>>(P.s, w, h, P.bcount, P.k[0], P.v[0]);
+    if (auto e = launch_status("find_peaks compaction")) return e;
+    uint32_t total = 0;
+    if (auto e = cuda_status(cudaMemcpyAsync(&total, P.scalars, 4, cudaMemcpyDeviceToHost, st), "find_peaks count")) return e;
+    if (auto e = cuda_status(cudaStreamSynchronize(st), "find_peaks")) return e;
+    const int64_t m = total;
+    if (m > 1) {
+        const int nb = static_cast<int>(ceil_div(m, kSortTile));
+        int cur = 0;
+        for (int pass = 0; pass < 8; ++pass) {
+            radix_hist_kernel<<<nb, 256, 0, st>>>(P.k[cur], m, 8 * pass, nb, P.counts);
+            excl_scan_kernel<<<1, 1024, 0, st>>>(P.counts, static_cast<int64_t>(256) * nb, nullptr);
+            radix_scatter_kernel<<<nb, 256, 0, st>>>(P.k[cur], P.v[cur], m, 8 * pass, nb, P.counts, P.k[cur ^ 1],
+                                                     P.v[cur ^ 1]);
+            cur ^= 1;
+        }
+        if (auto e = launch_status("find_peaks sort")) return e;
+        // eight passes: the sorted data is back in buffer 0
+    }
+    *out = P;
+    *count = m;
+    return SPCT_OK;
+}
+
+}  // namespace spct_cons
+
+using namespace spct_cons;
+
+extern "C" spct_status spct_cu_fuse_maps(const double* const* maps, int nmaps, const double* weights, int nweights,
+                                         int64_t n, double* out, void* stream) {
+    if (nmaps < 1 || !maps) return contract("fuse_maps: no maps to fuse");  // likelihood.cpp:258
+    if (nweights != 0 && nweights != nmaps) return contract("fuse_maps: weight count mismatch");  // :263
+    if (n < 0 || (n > 0 && !out)) return contract("fuse_maps: bad output");
+    std::vector<double> wv(nmaps);
+    for (int m = 0; m < nmaps; ++m) wv[m] = nweights ? weights[m] : 1.0 / nmaps;  // :262
+    double wsum = 0.0;
+    for (double x : wv) {
+        if (!(x >= 0.0)) return contract("fuse_maps: negative weight");  // :266
+        wsum += x;
+    }
+    if (!(wsum > 0.0)) return contract("fuse_maps: weights sum to zero");  // :269
+    if (n == 0) return SPCT_OK;
+    cudaStream_t s = as_stream(stream);
+    for (int m0 = 0; m0 < nmaps; m0 += kMaxFuse) {
+        FuseArgs a{};
+        a.nmaps = std::min(kMaxFuse, nmaps - m0);
+        for (int j = 0; j < a.nmaps; ++j) {
+            if (!maps[m0 + j]) return contract("fuse_maps: null map");
+            a.maps[j] = maps[m0 + j];
+            a.wt[j] = wv[m0 + j] / wsum;  // :278
+        }
+        a.first = m0 == 0;
+        a.last = m0 + a.nmaps == nmaps;
+        fuse_kernel<<<grid1(n), 256, 0, s>>>(a, n, out);
+        if (auto st = launch_status("fuse_kernel")) return st;
+    }
+    return SPCT_OK;
+}
+
+extern "C" spct_status spct_cu_find_peaks_workspace(int w, int h, size_t* bytes) {
+    if (!bytes) return contract("find_peaks_workspace: null argument");
+    if (!(w > 0 && h > 0)) return contract("find_peaks: empty map");  // likelihood.cpp:286
+    int64_t a, b;
+    *bytes = peak_ws_bytes(w, h, &a, &b);
+    return SPCT_OK;
+}
+
+extern "C" spct_status spct_cu_find_peaks(const double* map, int w, int h, int32_t* xs, int32_t* ys, double* heights,
+                                          int64_t max_out, int64_t* count, void* workspace, size_t workspace_bytes,
+                                          void* stream) {
+    if (!(w > 0 && h > 0)) return contract("find_peaks: empty map");  // likelihood.cpp:286
+    if (!map || !count || max_out < 0 || (max_out > 0 && !(xs && ys && heights)))
+        return contract("find_peaks: bad arguments");
+    cudaStream_t s = as_stream(stream);
+    PeakWs P;
+    int64_t m = 0;
+    if (auto st = sorted_peaks(map, w, h, workspace, workspace_bytes, s, &P, &m)) return st;
+    *count = m;
+    const int64_t k = std::min(m, max_out);
+    if (k > 0) {
+        peak_gather_kernel<<<grid1(k), 256, 0, s>>>(P.v[0], P.s, w, k, xs, ys, heights);
+        return launch_status("peak_gather_kernel");
+    }
+    return SPCT_OK;
+}
+
+extern "C" spct_status spct_cu_score_map(const double* map, int w, int h, int gx, int gy, int gw, int gh, int64_t* rank,
+                                         void* workspace, size_t workspace_bytes, void* stream) {
+    if (!(gw > 0 && gh > 0 && gx >= 0 && gy >= 0 && gx + gw <= w && gy + gh <= h))  // likelihood.cpp:325-326
+        return contract("score_map: ground truth rect must lie inside the map");
+    if (!map || !rank) return contract("score_map: bad arguments");
+    cudaStream_t s = as_stream(stream);
+    PeakWs P;
+    int64_t m = 0;
+    if (auto st = sorted_peaks(map, w, h, workspace, workspace_bytes, s, &P, &m)) return st;
+    unsigned best = 0xFFFFFFFFu;
+    if (m > 0) {
+        cudaMemcpyAsync(P.scalars + 1, &best, 4, cudaMemcpyHostToDevice, s);
+        score_kernel<<<grid1(m), 256, 0, s>>>(P.v[0], m, w, gx, gy, gw, gh, P.scalars + 1);
+        if (auto st = launch_status("score_kernel")) return st;
+        if (auto st = cuda_status(cudaMemcpyAsync(&best, P.scalars + 1, 4, cudaMemcpyDeviceToHost, s), "score")) return st;
+        if (auto st = cuda_status(cudaStreamSynchronize(s), "score_map")) return st;
+    }
+    *rank = best == 0xFFFFFFFFu ? m + 1 : static_cast<int64_t>(best) + 1;
+    return SPCT_OK;
+}
+
+extern "C" spct_status spct_cu_camshift(const double* map, int w, int h, const double* starts, int n, int win_w,
+                                        int win_h, double delta, int max_iter, double* out, int32_t* iterations,
+                                        int32_t* zero_mass, void* stream) {
+    if (!(w > 0 && h > 0)) return contract("camshift_refine: empty map");  // tracker.cpp:79
+    if (!(win_w >= 1 && win_h >= 1)) return contract("camshift_refine: empty window");  // :82
+    if (!(delta > 0.0)) return contract("camshift_refine: delta must be positive");  // :83
+    if (!(max_iter >= 1)) return contract("camshift_refine: need at least one iteration");  // :84
+    if (n < 0 || (n > 0 && !(map && starts && out && iterations && zero_mass)))
+        return contract("camshift_refine: bad arguments");
+    for (int q = 0; q < n; ++q) {  // host copy of the start points: the reference's check (:80-81)
+        const double cx = starts[2 * q], cy = starts[2 * q + 1];
+        if (!(cx >= 0 && cy >= 0 && cx < w && cy < h)) return contract("camshift_refine: start point outside the map");
+    }
+    if (n == 0) return SPCT_OK;
+    cudaStream_t s = as_stream(stream);
+    double *dstart = nullptr, *dout = nullptr;
+    int32_t* dint = nullptr;
+    spct_status st = cuda_status(cudaMallocAsync(&dstart, 2 * n * sizeof(double), s), "camshift alloc");
+    if (!st) st = cuda_status(cudaMallocAsync(&dout, 2 * n * sizeof(double), s), "camshift alloc");
+    if (!st) st = cuda_status(cudaMallocAsync(&dint, 2 * n * sizeof(int32_t), s), "camshift alloc");
+    if (!st) st = cuda_status(cudaMemcpyAsync(dstart, starts, 2 * n * sizeof(double), cudaMemcpyHostToDevice, s), "H2D");
+    if (!st) {
+        camshift_kernel<<<static_cast<unsigned>(ceil_div(n, 128)), 128, 0, s>>>(map, w, h, dstart, n, win_w, win_h, delta,
+                                                                               max_iter, dout, dint, dint + n);
+        st = launch_status("camshift_kernel");
+    }
+    if (!st) st = cuda_status(cudaMemcpyAsync(out, dout, 2 * n * sizeof(double), cudaMemcpyDeviceToHost, s), "D2H");
+    if (!st) st = cuda_status(cudaMemcpyAsync(iterations, dint, n * sizeof(int32_t), cudaMemcpyDeviceToHost, s), "D2H");
+    if (!st) st = cuda_status(cudaMemcpyAsync(zero_mass, dint + n, n * sizeof(int32_t), cudaMemcpyDeviceToHost, s), "D2H");
+    if (!st) st = cuda_status(cudaStreamSynchronize(s), "camshift_refine");
+    cudaFreeAsync(dstart, s);
+    cudaFreeAsync(dout, s);
+    cudaFreeAsync(dint, s);
+    return st;
+}

@@ -359,6 +359,85 @@ LikelihoodMap hist_distance_map(const IntegralHistogramTensor& t, const std::vec
     return hist_match_map(t, th, kw, kh, HistMetric::Minkowski, p);
 }
 
+namespace {
+std::unique_ptr<DevBuf> upload_map(const LikelihoodMap& m) {
+    require(m.values.size() == std::size_t(m.width) * std::size_t(m.height), "map: values do not match width * height");
+    auto d = std::make_unique<DevBuf>(m.values.size() * 8);
+    upload(*d, m.values);
+    return d;
+}
+}  // namespace
+
+LikelihoodMap fuse_maps(const std::vector<LikelihoodMap>& maps, std::vector<double> weights) {
+    require(!maps.empty(), "fuse_maps: no maps to fuse");  // likelihood.cpp:258
+    const int w = maps[0].width, h = maps[0].height;
+    for (const auto& m : maps) require(m.width == w && m.height == h, "fuse_maps: map dimensions differ");
+    std::vector<std::unique_ptr<DevBuf>> dev;
+    std::vector<const double*> ptrs;
+    for (const auto& m : maps) {
+        dev.push_back(upload_map(m));
+        ptrs.push_back(dev.back()->as<double>());
+    }
+    const std::size_t n = std::size_t(w) * h;
+    DevBuf out(n * 8);
+    check(spct_cu_fuse_maps(ptrs.data(), int(ptrs.size()), weights.data(), int(weights.size()), std::int64_t(n),
+                            out.as<double>(), nullptr));
+    LikelihoodMap f;
+    f.width = w;
+    f.height = h;
+    f.tag = "fused";
+    f.values.resize(n);
+    cuda(cudaMemcpy(f.values.data(), out.p, n * 8, cudaMemcpyDeviceToHost), "D2H");
+    return f;
+}
+
+std::vector<Peak> find_peaks(const LikelihoodMap& map) {
+    require(map.width > 0 && map.height > 0, "find_peaks: empty map");  // likelihood.cpp:286
+    auto d = upload_map(map);
+    std::size_t ws = 0;
+    check(spct_cu_find_peaks_workspace(map.width, map.height, &ws));
+    DevBuf work(ws);
+    const std::int64_t cap = std::int64_t(map.width) * map.height / 4 + 2;
+    DevBuf xs(cap * 4), ys(cap * 4), hs(cap * 8);
+    std::int64_t count = 0;
+    check(spct_cu_find_peaks(d->as<double>(), map.width, map.height, xs.as<std::int32_t>(), ys.as<std::int32_t>(),
+                             hs.as<double>(), cap, &count, work.p, ws, nullptr));
+    std::vector<std::int32_t> hx(count), hy(count);
+    std::vector<double> hh(count);
+    if (count) {
+        cuda(cudaMemcpy(hx.data(), xs.p, count * 4, cudaMemcpyDeviceToHost), "D2H");
+        cuda(cudaMemcpy(hy.data(), ys.p, count * 4, cudaMemcpyDeviceToHost), "D2H");
+        cuda(cudaMemcpy(hh.data(), hs.p, count * 8, cudaMemcpyDeviceToHost), "D2H");
+    }
+    std::vector<Peak> peaks(count);
+    for (std::int64_t i = 0; i < count; ++i) peaks[i] = Peak{hx[i], hy[i], hh[i], int(i) + 1};
+    return peaks;
+}
+
+int score_map(const LikelihoodMap& map, const Rect& gt) {
+    require(gt.w > 0 && gt.h > 0 && gt.inside(map.width, map.height),
+            "score_map: ground truth rect must lie inside the map");  // likelihood.cpp:325-326
+    auto d = upload_map(map);
+    std::size_t ws = 0;
+    check(spct_cu_find_peaks_workspace(map.width, map.height, &ws));
+    DevBuf work(ws);
+    std::int64_t rank = 0;
+    check(spct_cu_score_map(d->as<double>(), map.width, map.height, gt.x, gt.y, gt.w, gt.h, &rank, work.p, ws, nullptr));
+    return int(rank);
+}
+
+CamshiftResult camshift_refine(const LikelihoodMap& map, double cx, double cy, int win_w, int win_h, double delta,
+                               int max_iter) {
+    require(map.width > 0 && map.height > 0, "camshift_refine: empty map");  // tracker.cpp:79
+    auto d = upload_map(map);
+    const double start[2] = {cx, cy};
+    double out[2] = {cx, cy};
+    std::int32_t it = 0, zm = 0;
+    check(spct_cu_camshift(d->as<double>(), map.width, map.height, start, 1, win_w, win_h, delta, max_iter, out, &it,
+                           &zm, nullptr));
+    return CamshiftResult{out[0], out[1], int(it), zm != 0};
+}
+
 LikelihoodMap likelihood_from_frame(const GrayImage& img, int bins, const std::vector<double>& th, int kw, int kh,
                                     double p, IntegralHistogramTensor* tensor_out, std::uint64_t memory_budget) {
     require(img.width > 0 && img.height > 0, "quantize: empty image");

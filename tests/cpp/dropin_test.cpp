@@ -180,6 +180,33 @@ int main() {
         for (std::size_t i = 0; i < mf.values.size(); ++i)
             CHECK(std::abs(mf.values[i] - map.values[i]) <= 1e-5 * std::abs(map.values[i]) + 1e-12);
     }
+    {  // map consumers (test_likelihood.cpp:296-362, test_tracker.cpp:150-176)
+        LikelihoodMap a;
+        a.width = 4;
+        a.height = 3;
+        a.values.assign(12, 0.2);
+        LikelihoodMap b = a;
+        for (double& v : b.values) v = 0.8;
+        CHECK(fuse_maps({a}).values == a.values);
+        for (double v : fuse_maps({a, b}).values) CHECK(std::abs(v - 0.5) <= 1e-12);
+        CHECK_THROWS_AS((void)fuse_maps({a, b}, {1.0}), contract_error);
+        LikelihoodMap m;
+        m.width = 30;
+        m.height = 24;
+        m.values.assign(720, 0.0);
+        for (int y = 8; y < 13; ++y)
+            for (int x = 10; x < 15; ++x) m.at(x, y) = 1.0 - 0.15 * (std::abs(x - 12) + std::abs(y - 10));
+        auto peaks = find_peaks(m);
+        CHECK(!peaks.empty() && peaks.front().rank == 1);
+        CHECK(score_map(m, Rect{9, 7, 8, 8}) == 1);
+        CHECK_THROWS_AS((void)score_map(m, Rect{28, 20, 5, 5}), contract_error);
+        LikelihoodMap imp;
+        imp.width = imp.height = 12;
+        imp.values.assign(144, 0.0);
+        imp.at(5, 7) = 1.0;
+        CamshiftResult r = camshift_refine(imp, 3.0, 3.0, 9, 9);
+        CHECK(!r.zero_mass && std::abs(r.cx - 5.0) <= 1e-12 && std::abs(r.cy - 7.0) <= 1e-12 && r.iterations >= 1);
+    }
     {  // IHT1 round trip (test_integral.cpp:208-238)
         BinMap bm(33, 31, 16);
         for (std::size_t i = 0; i < bm.data.size(); ++i) bm.data[i] = static_cast<std::uint16_t>((i * 7 + i / 33) % 16);

@@ -507,3 +507,55 @@ def test_iht1_load_rejects_bad_payloads(P, tmp_path):
         P.load_tensor(tmp_path / "big.iht")
     with pytest.raises(P.SpctError, match="cannot write tensor"):
         P.dump_tensor(t, "/nonexistent/dir/t.iht")
+
+
+# ------------------------------------------------------------------ map consumers (§8(f) #2)
+
+def _consumer_maps(seed):
+    rng = np.random.default_rng(seed)
+    img = oracle.smooth_image(301, 211, seed)
+    qb = oracle.quantize(img, 24)
+    th = _crop_template(qb, 24, 120, 80, 40, 30)
+    lmap = oracle.hist_match_map_direct(qb, 24, th, 40, 30, 1.0)
+    return [lmap, rng.random((211, 301)), np.round(rng.random((211, 301)) * 3) / 3, np.full((211, 301), 0.37)]
+
+
+@pytest.mark.parametrize("seed", [4, 5])
+def test_fuse_maps_bit_exact(P, seed):
+    maps = _consumer_maps(seed)
+    dm = [torch.from_numpy(m).cuda() for m in maps]
+    for wts in (None, [0.1, 0.2, 0.3, 0.4], [0.0, 1.0, 0.0, 3.0]):
+        assert np.array_equal(P.fuse_maps(dm, wts).cpu().numpy(), oracle.fuse_maps(maps, wts))
+    many = [dm[i % 4] for i in range(11)]  # more maps than one fuse launch takes
+    assert np.array_equal(P.fuse_maps(many).cpu().numpy(), oracle.fuse_maps([maps[i % 4] for i in range(11)]))
+    with pytest.raises(P.ContractError):
+        P.fuse_maps([dm[0], dm[1]], [1.0])
+    with pytest.raises(P.ContractError):
+        P.fuse_maps([dm[0]], [-1.0])
+
+
+@pytest.mark.parametrize("seed", [4, 5])
+def test_find_peaks_and_score_bit_exact(P, seed):
+    for m in _consumer_maps(seed) + [np.random.default_rng(seed).random((600, 700))]:
+        xs, ys, hs = (t.cpu().numpy() for t in P.find_peaks(torch.from_numpy(m).cuda()))
+        wx, wy, wh = oracle.find_peaks(m)
+        assert np.array_equal(xs, wx) and np.array_equal(ys, wy) and np.array_equal(hs, wh)
+        h, w = m.shape
+        for g in [(0, 0, 5, 5), (w // 3, h // 4, w // 3, h // 2), (w - 6, h - 5, 6, 5)]:
+            assert P.score_map(torch.from_numpy(m).cuda(), *g) == oracle.score_map(m, *g)
+
+
+def test_camshift_bit_exact(P):
+    maps = _consumer_maps(6)
+    rng = np.random.default_rng(6)
+    starts = np.c_[rng.uniform(0, 300, 64), rng.uniform(0, 210, 64)]
+    for m in maps:
+        c, it, zm = P.camshift_batch(torch.from_numpy(m).cuda(), starts, 33, 21)
+        for q, (cx, cy) in enumerate(starts):
+            wcx, wcy, wit, wzm = oracle.camshift(m, cx, cy, 33, 21)
+            assert (c[q, 0], c[q, 1], it[q], zm[q]) == (wcx, wcy, wit, wzm)
+    imp = np.zeros((12, 12))
+    imp[7, 5] = 1.0
+    assert P.camshift_refine(torch.from_numpy(imp).cuda(), 3.0, 3.0, 9, 9)[:2] == (5.0, 7.0)  # test_tracker.cpp:151-158
+    with pytest.raises(P.ContractError):
+        P.camshift_refine(torch.from_numpy(imp).cuda(), 12.0, 3.0, 9, 9)

@@ -188,3 +188,59 @@ def test_orientation_bins_vs_live_reference(w, h, sigma, bins):
     assert np.all(oracle.orientation_bins(flat, bins, sigma) == min(bins - 1, (90 * bins) // 180))
     with pytest.raises(oracle.ContractError):
         oracle.ref_orientation_bins(flat, bins, -1.0)
+
+
+# ------------------------------------------------------------------ map consumers (§8(f) #2)
+
+def _bump_map(w, h, bumps):
+    """test_likelihood.cpp:325-336 bump_map."""
+    m = np.zeros((h, w))
+    for (rx, ry, rw, rh), v in bumps:
+        for y in range(ry, ry + rh):
+            for x in range(rx, rx + rw):
+                m[y, x] = max(m[y, x], v * (1.0 - 0.15 * (abs(x - (rx + rw // 2)) + abs(y - (ry + rh // 2)))))
+    return m
+
+
+def test_consumers_known_answers():
+    """test_likelihood.cpp:296-362 and test_tracker.cpp:150-176 on the C restatement."""
+    a, b = np.full((3, 4), 0.2), np.full((3, 4), 0.8)
+    assert np.array_equal(oracle.fuse_maps([a]), a)
+    assert np.allclose(oracle.fuse_maps([a, a], [0.3, 0.7]), 0.2)
+    assert np.allclose(oracle.fuse_maps([a, b]), 0.5)
+    for bad in ([a, np.full((3, 5), 0.1)], []):
+        with pytest.raises(oracle.ContractError):
+            oracle.fuse_maps(bad)
+    with pytest.raises(oracle.ContractError):
+        oracle.fuse_maps([a, b], [1.0])
+    m = _bump_map(30, 24, [((10, 8, 5, 5), 1.0)])
+    xs, ys, hs = oracle.find_peaks(m)
+    assert len(xs) and np.all(np.diff(hs) <= 0)
+    assert oracle.score_map(m, 9, 7, 8, 8) == 1
+    two = _bump_map(40, 30, [((5, 5, 5, 5), 1.0), ((28, 20, 5, 5), 0.6)])
+    assert oracle.score_map(two, 26, 18, 9, 9) == 2
+    assert oracle.score_map(two, 20, 2, 4, 4) == len(oracle.find_peaks(two)[0]) + 1
+    assert oracle.score_map(two * 0.25, 26, 18, 9, 9) == 2
+    with pytest.raises(oracle.ContractError):
+        oracle.score_map(two, 38, 28, 5, 5)
+    imp = np.zeros((12, 12))
+    imp[7, 5] = 1.0
+    cx, cy, it, zm = oracle.camshift(imp, 3.0, 3.0, 9, 9)
+    assert (cx, cy, zm) == (5.0, 7.0, False) and it >= 1
+    assert oracle.camshift(np.zeros((10, 10)), 4.0, 4.0, 5, 5)[3]
+    assert oracle.camshift(np.full((20, 20), 0.25), 10.0, 9.0, 5, 5)[:2] == (10.0, 9.0)
+
+
+@ref
+@pytest.mark.parametrize("seed", [1, 2, 3])
+def test_consumers_vs_live_reference(seed):
+    rng = np.random.default_rng(seed)
+    maps = [rng.random((37, 53)), np.round(rng.random((37, 53)) * 3) / 3, _bump_map(53, 37, [((4, 4, 9, 9), 0.9)])]
+    for wts in (None, [0.2, 0.5, 0.3], [0.0, 2.0, 1.0]):
+        assert np.array_equal(oracle.fuse_maps(maps, wts), oracle.ref_fuse_maps(maps, wts))
+    for m in maps + [np.full((9, 11), 0.4)]:
+        mine, ref_ = oracle.find_peaks(m), oracle.ref_find_peaks(m)
+        assert all(np.array_equal(p, q) for p, q in zip(mine, ref_))
+        h, w = m.shape
+        for g in [(0, 0, 5, 5), (w // 3, h // 4, w // 3, h // 2), (w - 6, h - 5, 6, 5)]:
+            assert oracle.score_map(m, *g) == oracle.ref_score_map(m, *g)
