@@ -166,6 +166,38 @@ spct_status spct_cu_camshift(const double* map, int w, int h, const double* star
                              double delta, int max_iter, double* out, int32_t* iterations, int32_t* zero_mass,
                              void* stream);
 
+/* ----------------------------------------------------------------- SWIH (swih.hpp)
+ * Weighted integral histogram: uint64 cells (16.16 fixed-point weight sums), unpadded
+ * and pitched like spct_ih: data[k*plane_pitch + y*row_pitch + x] == H(k, y+1, x+1). */
+typedef struct {
+    uint64_t* data;
+    int bins;
+    int height;
+    int width;
+    int64_t row_pitch;
+    int64_t plane_pitch;
+} spct_wih;
+
+spct_status spct_cu_wih_layout(int width, int height, int bins, int64_t* row_pitch, int64_t* plane_pitch,
+                               uint64_t* bytes);
+/* build_weighted_tensor (integral.cpp:553-559): bins (dev uint16, row pitch `pitch`, values
+ * >= out->bins count nowhere) with per-pixel weights (dev uint64, same pitch), or, with
+ * weights == NULL, the quadrant ramp field `field_dir` (0 NW, 1 NE, 2 SW, 3 SE; swih.cpp:45-53)
+ * of a kw x kh kernel (build_quadrant_set swih.cpp:115-126). */
+spct_status spct_cu_wih_build(const uint16_t* bins, int64_t pitch, const uint64_t* weights, int field_dir, int kw,
+                              int kh, const spct_wih* out, void* stream);
+spct_status spct_cu_wih_export_u64(const spct_wih* t, int k0, int k1, uint64_t* dst, void* stream);
+/* swlh_query_fixed (swih.cpp:128-164) at n centres (host array of (cx, cy)) over the four
+ * quadrant tensors set4[NW, NE, SW, SE]; out (dev) n x bins int64, 16.16.  Synchronises. */
+spct_status spct_cu_swlh_query(const spct_wih* set4, int kw, int kh, const int32_t* centres, int n, int64_t* out,
+                               void* stream);
+/* brute_force_swlh_fixed (swih.cpp:166-178) at n centres (host array); out (dev). */
+spct_status spct_cu_swlh_brute(const uint16_t* bins, int64_t pitch, int width, int height, int nbins, int kw, int kh,
+                               const int32_t* centres, int n, int64_t* out, void* stream);
+/* The tracker's swlh-distance map (track_loop.cpp:264-283): model (dev, bins doubles),
+ * map (dev, width x height doubles).  Synchronises. */
+spct_status spct_cu_swlh_map(const spct_wih* set4, int kw, int kh, const double* model, double* map, void* stream);
+
 /* IHT1 wire format (integral.hpp:132-135; dump_tensor / load_tensor integral.cpp:619-659):
  * "IHT1", LE u32 bins/height/width/elem_bytes, then the padded planes as LE elements.
  * spct_cu_ih_dump streams the device tensor (all of its planes) to `path`; elem_bytes 8 is

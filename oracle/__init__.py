@@ -36,6 +36,7 @@ _u32p = np.ctypeslib.ndpointer(np.uint32, flags="C_CONTIGUOUS")
 _u64p = np.ctypeslib.ndpointer(np.uint64, flags="C_CONTIGUOUS")
 _f64p = np.ctypeslib.ndpointer(np.float64, flags="C_CONTIGUOUS")
 _i32p = np.ctypeslib.ndpointer(np.int32, flags="C_CONTIGUOUS")
+_i64p = np.ctypeslib.ndpointer(np.int64, flags="C_CONTIGUOUS")
 _i, _u32, _u64, _i64, _d, _vp = C.c_int, C.c_uint32, C.c_uint64, C.c_int64, C.c_double, C.c_void_p
 
 
@@ -81,6 +82,10 @@ def _load_c():
         "or_xorshift_image": (None, [_u32, _i64, _u8p]),
         "or_orientation_bins": (_i, [_u8p, _i, _i, _d, _i, _u16p]),
         "or_fuse_maps": (_i, [C.POINTER(_vp), _i, _vp, _i64, _f64p]),
+        "or_weighted_ih_u64": (None, [_u16p, _u64p, _i, _i, _i, _u64p]),
+        "or_swlh_fixed_brute": (_i, [_u16p, _i, _i, _i, _i, _i, _i, _i, _i64p]),
+        "or_swlh_normalized": (_i, [_u16p, _i, _i, _i, _i, _i, _i, _i, _f64p]),
+        "or_swlh_map": (_i, [_u16p, _i, _i, _i, _f64p, _i, _i, _f64p]),
         "or_find_peaks": (_i, [_f64p, _i, _i, _i32p, _i32p, _f64p, _i, C.POINTER(_i)]),
         "or_score_map": (_i, [_f64p, _i, _i, _i, _i, _i, _i, C.POINTER(_i)]),
         "or_camshift": (_i, [_f64p, _i, _i, _d, _d, _i, _i, _d, _i, C.POINTER(_d), C.POINTER(_d), C.POINTER(_i),
@@ -123,6 +128,10 @@ def _load_ref():
         "ref_orientation_bins": (_i, [_u8p, _i, _i, _d, _i, _u16p]),
         "ref_dump_tensor": (_i, [_vp, C.c_char_p]),
         "ref_fuse_maps": (_i, [C.POINTER(_vp), _i, _vp, _i, _i, _i, _f64p]),
+        "ref_swlh_query_fixed": (_i, [_u16p, _i, _i, _i, _i, _i, _i32p, _i, _i64p]),
+        "ref_swlh_query": (_i, [_u16p, _i, _i, _i, _i, _i, _i32p, _i, _f64p]),
+        "ref_brute_force_swlh_fixed": (_i, [_u16p, _i, _i, _i, _i, _i, _i, _i, _i64p]),
+        "ref_ih_build_weighted": (_i, [_u16p, _u64p, _i, _i, _i, _i, _i, _i, _u64, C.POINTER(_vp)]),
         "ref_find_peaks": (_i, [_f64p, _i, _i, _i32p, _i32p, _f64p, _i32p, _i, C.POINTER(_i)]),
         "ref_score_map": (_i, [_f64p, _i, _i, _i, _i, _i, _i, C.POINTER(_i)]),
         "ref_load_tensor": (_i, [C.c_char_p, C.POINTER(_vp)]),
@@ -407,6 +416,79 @@ def camshift(m: np.ndarray, cx: float, cy: float, win_w: int, win_h: int, delta:
     _check(clib().or_camshift(m.reshape(-1), w, h, cx, cy, win_w, win_h, delta, max_iter, C.byref(ox), C.byref(oy),
                               C.byref(it), C.byref(zm)), "camshift_refine")
     return ox.value, oy.value, it.value, bool(zm.value)
+
+
+def weighted_ih(bm: np.ndarray, weights: np.ndarray, nbins: int) -> np.ndarray:
+    """build_weighted_tensor (integral.cpp:553-559), reference layout uint64 (C restatement)."""
+    bm = np.ascontiguousarray(bm, np.uint16)
+    wt = np.ascontiguousarray(weights, np.uint64)
+    h, w = bm.shape
+    out = np.empty((nbins, h + 1, w + 1), np.uint64)
+    clib().or_weighted_ih_u64(bm.reshape(-1), wt.reshape(-1), w, h, nbins, out.reshape(-1))
+    return out
+
+
+def ref_weighted_ih(bm: np.ndarray, weights: np.ndarray, nbins: int) -> np.ndarray:
+    lib = reflib()
+    bm = np.ascontiguousarray(bm, np.uint16)
+    wt = np.ascontiguousarray(weights, np.uint64)
+    h, w = bm.shape
+    hdl = _vp()
+    _check(lib.ref_ih_build_weighted(bm.reshape(-1), wt.reshape(-1), w, h, nbins, SEQUENTIAL, 32, 1, (1 << 64) - 1,
+                                     C.byref(hdl)), "build_weighted_tensor", lib)
+    try:
+        n = int(lib.ref_ih_size(hdl))
+        return np.ctypeslib.as_array(lib.ref_ih_data(hdl), shape=(n,)).reshape(nbins, h + 1, w + 1).copy()
+    finally:
+        lib.ref_ih_free(hdl)
+
+
+def swlh_fixed(bm: np.ndarray, nbins: int, cx: int, cy: int, kw: int, kh: int) -> np.ndarray:
+    """brute_force_swlh_fixed (swih.cpp:166-178), int64 16.16."""
+    bm = np.ascontiguousarray(bm, np.uint16)
+    h, w = bm.shape
+    out = np.empty(nbins, np.int64)
+    _check(clib().or_swlh_fixed_brute(bm.reshape(-1), w, h, nbins, cx, cy, kw, kh, out), "swlh")
+    return out
+
+
+def swlh(bm: np.ndarray, nbins: int, cx: int, cy: int, kw: int, kh: int) -> np.ndarray:
+    """brute_force_swlh (swih.cpp:199-202): normalised with the reference's long double."""
+    bm = np.ascontiguousarray(bm, np.uint16)
+    h, w = bm.shape
+    out = np.empty(nbins, np.float64)
+    _check(clib().or_swlh_normalized(bm.reshape(-1), w, h, nbins, cx, cy, kw, kh, out), "swlh")
+    return out
+
+
+def swlh_map(bm: np.ndarray, nbins: int, model, kw: int, kh: int) -> np.ndarray:
+    """The tracker's swlh-distance channel (track_loop.cpp:264-283)."""
+    bm = np.ascontiguousarray(bm, np.uint16)
+    h, w = bm.shape
+    md = np.ascontiguousarray(model, np.float64)
+    out = np.empty((h, w), np.float64)
+    _check(clib().or_swlh_map(bm.reshape(-1), w, h, nbins, md, kw, kh, out.reshape(-1)), "swlh_map")
+    return out
+
+
+def ref_swlh_query_fixed(bm, nbins, centres, kw, kh) -> np.ndarray:
+    bm = np.ascontiguousarray(bm, np.uint16)
+    h, w = bm.shape
+    c = np.ascontiguousarray(np.asarray(centres, np.int32).reshape(-1, 2))
+    out = np.empty((len(c), nbins), np.int64)
+    _check(reflib().ref_swlh_query_fixed(bm.reshape(-1), w, h, nbins, kw, kh, c.reshape(-1), len(c),
+                                         out.reshape(-1)), "swlh_query_fixed", reflib())
+    return out
+
+
+def ref_swlh_query(bm, nbins, centres, kw, kh) -> np.ndarray:
+    bm = np.ascontiguousarray(bm, np.uint16)
+    h, w = bm.shape
+    c = np.ascontiguousarray(np.asarray(centres, np.int32).reshape(-1, 2))
+    out = np.empty((len(c), nbins), np.float64)
+    _check(reflib().ref_swlh_query(bm.reshape(-1), w, h, nbins, kw, kh, c.reshape(-1), len(c), out.reshape(-1)),
+           "swlh_query", reflib())
+    return out
 
 
 def hist_finalize(dsum, w, h, kw, kh, p) -> np.ndarray:

@@ -20,6 +20,7 @@
 
 #include "spct/error.hpp"
 #include "spct/features.hpp"
+#include "spct/swih.hpp"
 #include "spct/imagecore.hpp"
 #include "spct/integral.hpp"
 #include "spct/likelihood.hpp"
@@ -248,6 +249,41 @@ int ref_find_peaks(const double* map, int w, int h, int* xs, int* ys, double* hs
 
 int ref_score_map(const double* map, int w, int h, int gx, int gy, int gw, int gh, int* rank) {
     return guarded([&] { *rank = spct::score_map(make_map(map, w, h), spct::Rect{gx, gy, gw, gh}); });
+}
+
+// SWIH (swih.cpp:115-191): quadrant set + exact query, the brute-force oracle, normalised.
+int ref_swlh_query_fixed(const std::uint16_t* bins, int w, int h, int nbins, int kw, int kh, const int* centres, int n,
+                         std::int64_t* out) {
+    return guarded([&] {
+        spct::BinMap bm = make_binmap(bins, w, h, nbins);
+        const spct::KernelSpec spec{kw, kh};
+        const spct::WeightedQuadrantSet set = spct::build_quadrant_set(bm, spec);
+        for (int i = 0; i < n; ++i) {
+            const auto v = spct::swlh_query_fixed(set, centres[2 * i], centres[2 * i + 1], spec);
+            std::memcpy(out + static_cast<std::size_t>(i) * nbins, v.data(), v.size() * sizeof(std::int64_t));
+        }
+    });
+}
+
+int ref_swlh_query(const std::uint16_t* bins, int w, int h, int nbins, int kw, int kh, const int* centres, int n,
+                   double* out) {
+    return guarded([&] {
+        spct::BinMap bm = make_binmap(bins, w, h, nbins);
+        const spct::KernelSpec spec{kw, kh};
+        const spct::WeightedQuadrantSet set = spct::build_quadrant_set(bm, spec);
+        for (int i = 0; i < n; ++i) {
+            const auto v = spct::swlh_query(set, centres[2 * i], centres[2 * i + 1], spec);
+            std::memcpy(out + static_cast<std::size_t>(i) * nbins, v.data(), v.size() * sizeof(double));
+        }
+    });
+}
+
+int ref_brute_force_swlh_fixed(const std::uint16_t* bins, int w, int h, int nbins, int kw, int kh, int cx, int cy,
+                               std::int64_t* out) {
+    return guarded([&] {
+        const auto v = spct::brute_force_swlh_fixed(make_binmap(bins, w, h, nbins), cx, cy, spct::KernelSpec{kw, kh});
+        std::memcpy(out, v.data(), v.size() * sizeof(std::int64_t));
+    });
 }
 
 // dump_tensor / load_tensor (integral.cpp:619-659), the IHT1 wire format.

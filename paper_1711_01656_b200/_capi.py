@@ -32,6 +32,11 @@ class spct_source(C.Structure):
     ]
 
 
+class spct_wih(C.Structure):
+    _fields_ = [("data", C.c_void_p), ("bins", C.c_int), ("height", C.c_int), ("width", C.c_int),
+                ("row_pitch", C.c_int64), ("plane_pitch", C.c_int64)]
+
+
 class spct_ih(C.Structure):
     _fields_ = [
         ("data", C.c_void_p),
@@ -80,6 +85,12 @@ SIGNATURES = {
     "spct_cu_score_map": (_i, [_vp, _i, _i, _i, _i, _i, _i, C.POINTER(_i64), _vp, _sz, _vp]),
     "spct_cu_camshift": (_i, [_vp, _i, _i, C.POINTER(_d), _i, _i, _i, _d, _i, C.POINTER(_d), C.POINTER(C.c_int32),
                               C.POINTER(C.c_int32), _vp]),
+    "spct_cu_wih_layout": (_i, [_i, _i, _i, C.POINTER(_i64), C.POINTER(_i64), C.POINTER(_u64)]),
+    "spct_cu_wih_build": (_i, [_vp, _i64, _vp, _i, _i, _i, C.POINTER(spct_wih), _vp]),
+    "spct_cu_wih_export_u64": (_i, [C.POINTER(spct_wih), _i, _i, _vp, _vp]),
+    "spct_cu_swlh_query": (_i, [C.POINTER(spct_wih), _i, _i, C.POINTER(C.c_int32), _i, _vp, _vp]),
+    "spct_cu_swlh_brute": (_i, [_vp, _i64, _i, _i, _i, _i, _i, C.POINTER(C.c_int32), _i, _vp, _vp]),
+    "spct_cu_swlh_map": (_i, [C.POINTER(spct_wih), _i, _i, _vp, _vp, _vp]),
     "spct_cu_launch_count": (C.c_uint64, []),
     "spct_cu_profile_enable": (None, [_i]),
     "spct_cu_profile_reset": (None, []),

@@ -559,3 +559,67 @@ def test_camshift_bit_exact(P):
     assert P.camshift_refine(torch.from_numpy(imp).cuda(), 3.0, 3.0, 9, 9)[:2] == (5.0, 7.0)  # test_tracker.cpp:151-158
     with pytest.raises(P.ContractError):
         P.camshift_refine(torch.from_numpy(imp).cuda(), 12.0, 3.0, 9, 9)
+
+
+# ------------------------------------------------------------------ SWIH (§8(f) #1)
+
+SWIH_KERNELS = [(1, 1), (2, 2), (3, 3), (4, 4), (5, 3), (1, 7), (8, 1), (9, 9), (6, 10)]  # test_swih.cpp:100-101
+
+
+def test_weighted_tensor_bit_exact(P):
+    bm = oracle.random_binmap(131, 77, 9, 5)
+    wts = np.random.default_rng(5).integers(0, 1 << 40, bm.size, dtype=np.uint64).reshape(bm.shape)
+    t = P.swih.build_weighted_tensor(bm, wts, 9)
+    assert np.array_equal(t.padded_u64(), oracle.weighted_ih(bm, wts, 9))
+    with pytest.raises(P.ContractError):
+        P.swih.build_weighted_tensor(bm, wts, 8)  # bin index out of range (integral.cpp:337-343)
+
+
+@pytest.mark.parametrize("kw,kh", SWIH_KERNELS)
+def test_swlh_query_bit_exact(P, kw, kh):
+    """test_swih.cpp:98-114 / acceptance criterion 3: the device quadrant query equals the
+    brute force (device and oracle), 16.16 fixed point, bit for bit."""
+    w, h, nb = 40, 36, 8
+    bm = oracle.random_binmap(w, h, nb, 606 + kw * 10 + kh)
+    s = P.swih.build_quadrant_set(bm, nb, kw, kh)
+    rng = np.random.default_rng(kw * 100 + kh)
+    cs = [(kw // 2 + int(rng.integers(0, w - kw + 1)), kh // 2 + int(rng.integers(0, h - kh + 1))) for _ in range(25)]
+    fast = P.swih.swlh_query_fixed(s, cs)
+    slow = P.swih.brute_force_swlh_fixed(bm, nb, cs, kw, kh)
+    want = np.stack([oracle.swlh_fixed(bm, nb, cx, cy, kw, kh) for cx, cy in cs])
+    assert np.array_equal(fast, want) and np.array_equal(slow, want)
+    q = P.swih.swlh_query(s, cs)
+    ref = np.stack([oracle.swlh(bm, nb, cx, cy, kw, kh) for cx, cy in cs])
+    assert np.all(np.abs(q - ref) <= 2.3e-16 * np.abs(ref))  # FP64 vs x87 long double: <= 1 ulp
+    with pytest.raises(P.ContractError):
+        P.swih.swlh_query_fixed(s, [(0, 0)] if kw > 1 or kh > 1 else [(w, 0)])  # window outside the image
+
+
+def test_swlh_quadrant_tensors_match_reference_fields(P):
+    """build_quadrant_set's four tensors == build_weighted_tensor of quadrant_weight_fields."""
+    w, h, nb, kw, kh = 33, 21, 5, 7, 4
+    bm = oracle.random_binmap(w, h, nb, 17)
+    s = P.swih.build_quadrant_set(bm, nb, kw, kh)
+    sx, sy = int(kw >= 3), int(kh >= 3)
+    x, y = np.meshgrid(np.arange(w), np.arange(h))
+    fields = [1 + sx * x + sy * y, 1 + sx * (w - 1 - x) + sy * y, 1 + sx * x + sy * (h - 1 - y),
+              1 + sx * (w - 1 - x) + sy * (h - 1 - y)]  # NW, NE, SW, SE (swih.cpp:45-53)
+    for t, f in zip(s.tensors, fields):
+        assert np.array_equal(t.padded_u64(), oracle.weighted_ih(bm, (f.astype(np.uint64) << np.uint64(16)), nb))
+
+
+@pytest.mark.parametrize("kw,kh,w,h", [(9, 7, 64, 48), (4, 4, 37, 29), (1, 1, 12, 9), (20, 30, 15, 12)])
+def test_swlh_distance_map(P, kw, kh, w, h):
+    """The tracker's swlh-distance channel (track_loop.cpp:264-283) vs the C restatement."""
+    nb = 8
+    img = oracle.smooth_image(w, h, kw + w)
+    bm = oracle.quantize(img, nb)
+    if w >= kw and h >= kh:
+        model = oracle.swlh(bm, nb, w // 2, h // 2, kw, kh)
+    else:
+        model = np.full(nb, 1.0 / nb)
+    got = P.swih.swlh_distance_map(bm, nb, model, kw, kh).cpu().numpy()
+    want = oracle.swlh_map(bm, nb, model, kw, kh)
+    assert close(got, want)
+    if w >= kw and h >= kh:
+        assert got[h // 2, w // 2] == 1.0

@@ -244,3 +244,43 @@ def test_consumers_vs_live_reference(seed):
         h, w = m.shape
         for g in [(0, 0, 5, 5), (w // 3, h // 4, w // 3, h // 2), (w - 6, h - 5, 6, 5)]:
             assert oracle.score_map(m, *g) == oracle.ref_score_map(m, *g)
+
+
+# ------------------------------------------------------------------ SWIH (§8(f) #1)
+
+SWIH_KERNELS = [(1, 1), (2, 2), (3, 3), (4, 4), (5, 3), (1, 7), (8, 1), (9, 9), (6, 10)]  # test_swih.cpp:100-101
+
+
+@ref
+def test_weighted_ih_vs_live_reference():
+    bm = oracle.random_binmap(23, 17, 6, 11)
+    wts = np.random.default_rng(11).integers(0, 1 << 30, bm.size, dtype=np.uint64).reshape(bm.shape)
+    assert np.array_equal(oracle.weighted_ih(bm, wts, 6), oracle.ref_weighted_ih(bm, wts, 6))
+
+
+@ref
+@pytest.mark.parametrize("kw,kh", SWIH_KERNELS)
+def test_swlh_brute_force_vs_live_reference(kw, kh):
+    """The C brute force (swih.cpp:166-178) == the reference's exact quadrant query
+    (test_swih.cpp:98-114, acceptance criterion 3), fixed and normalised."""
+    w, h, nb = 40, 36, 8
+    bm = oracle.random_binmap(w, h, nb, 606 + kw * 10 + kh)
+    rng = np.random.default_rng(kw * 100 + kh)
+    cs = [(kw // 2 + int(rng.integers(0, w - kw + 1)), kh // 2 + int(rng.integers(0, h - kh + 1))) for _ in range(25)]
+    fixed = oracle.ref_swlh_query_fixed(bm, nb, cs, kw, kh)
+    norm = oracle.ref_swlh_query(bm, nb, cs, kw, kh)
+    for i, (cx, cy) in enumerate(cs):
+        assert np.array_equal(oracle.swlh_fixed(bm, nb, cx, cy, kw, kh), fixed[i])
+        assert np.array_equal(oracle.swlh(bm, nb, cx, cy, kw, kh), norm[i])
+
+
+def test_swlh_degenerate_known_answers():
+    """test_swih.cpp:116-135."""
+    bm = np.full((12, 12), 2, np.uint16)
+    q = oracle.swlh(bm, 4, 6, 6, 5, 5)
+    assert q[2] == 1.0 and q[0] == 0.0
+    bm = oracle.random_binmap(9, 9, 5, 81)
+    for y in range(9):
+        for x in range(9):
+            q = oracle.swlh(bm, 5, x, y, 1, 1)
+            assert q[bm[y, x]] == 1.0 and q.sum() == 1.0
