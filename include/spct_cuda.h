@@ -198,6 +198,20 @@ spct_status spct_cu_swlh_brute(const uint16_t* bins, int64_t pitch, int width, i
  * map (dev, width x height doubles).  Synchronises. */
 spct_status spct_cu_swlh_map(const spct_wih* set4, int kw, int kh, const double* model, double* map, void* stream);
 
+/* ----------------------------------------------------------------- joint-IH median (motion.hpp)
+ * spct_cu_ih_accumulate: the build of spct_cu_ih_build, added (sign +1) to or subtracted
+ * (sign -1) from the tensor already in `acc` (uint32 wrap arithmetic; a joint histogram of
+ * frames stays exact while frames * H * W < 2^32) — MedianBackgroundIH::add_frame
+ * (motion.cpp:51-60).  spct_cu_median_background: background() (motion.cpp:71-99) of a
+ * joint tensor over `nframes` frames, out (dev uint8).  spct_cu_median_sort:
+ * median_background_sort (motion.cpp:103-118), frames a host array of nf device planes. */
+spct_status spct_cu_ih_accumulate(const spct_source* src, const spct_ih* acc, int sign, void* workspace,
+                                  size_t workspace_bytes, void* stream);
+spct_status spct_cu_median_background(const spct_ih* joint, int nframes, int m, int n, uint8_t* out, int64_t out_pitch,
+                                      void* stream);
+spct_status spct_cu_median_sort(const uint8_t* const* frames, int nf, int width, int height, int64_t pitch,
+                                uint8_t* out, int64_t out_pitch, void* stream);
+
 /* IHT1 wire format (integral.hpp:132-135; dump_tensor / load_tensor integral.cpp:619-659):
  * "IHT1", LE u32 bins/height/width/elem_bytes, then the padded planes as LE elements.
  * spct_cu_ih_dump streams the device tensor (all of its planes) to `path`; elem_bytes 8 is

@@ -86,6 +86,8 @@ def _load_c():
         "or_swlh_fixed_brute": (_i, [_u16p, _i, _i, _i, _i, _i, _i, _i, _i64p]),
         "or_swlh_normalized": (_i, [_u16p, _i, _i, _i, _i, _i, _i, _i, _f64p]),
         "or_swlh_map": (_i, [_u16p, _i, _i, _i, _f64p, _i, _i, _f64p]),
+        "or_median_bg_ih": (_i, [_u8p, _i, _i, _i, _i, _i, _i, _i, _u8p]),
+        "or_median_bg_sort": (_i, [_u8p, _i, _i, _i, _u8p]),
         "or_find_peaks": (_i, [_f64p, _i, _i, _i32p, _i32p, _f64p, _i, C.POINTER(_i)]),
         "or_score_map": (_i, [_f64p, _i, _i, _i, _i, _i, _i, C.POINTER(_i)]),
         "or_camshift": (_i, [_f64p, _i, _i, _d, _d, _i, _i, _d, _i, C.POINTER(_d), C.POINTER(_d), C.POINTER(_i),
@@ -129,6 +131,8 @@ def _load_ref():
         "ref_dump_tensor": (_i, [_vp, C.c_char_p]),
         "ref_fuse_maps": (_i, [C.POINTER(_vp), _i, _vp, _i, _i, _i, _f64p]),
         "ref_swlh_query_fixed": (_i, [_u16p, _i, _i, _i, _i, _i, _i32p, _i, _i64p]),
+        "ref_median_bg_ih": (_i, [_u8p, _i, _i, _i, _i, _i, _i, _i, _u8p]),
+        "ref_median_bg_sort": (_i, [_u8p, _i, _i, _i, _u8p]),
         "ref_swlh_query": (_i, [_u16p, _i, _i, _i, _i, _i, _i32p, _i, _f64p]),
         "ref_brute_force_swlh_fixed": (_i, [_u16p, _i, _i, _i, _i, _i, _i, _i, _i64p]),
         "ref_ih_build_weighted": (_i, [_u16p, _u64p, _i, _i, _i, _i, _i, _i, _u64, C.POINTER(_vp)]),
@@ -488,6 +492,28 @@ def ref_swlh_query(bm, nbins, centres, kw, kh) -> np.ndarray:
     out = np.empty((len(c), nbins), np.float64)
     _check(reflib().ref_swlh_query(bm.reshape(-1), w, h, nbins, kw, kh, c.reshape(-1), len(c), out.reshape(-1)),
            "swlh_query", reflib())
+    return out
+
+
+def median_bg_ih(frames, nf: int, bins: int, m: int, n: int, ref: bool = False) -> np.ndarray:
+    """MedianBackgroundIH on frames[:nf], slid through frames[nf:], background()."""
+    fr = np.ascontiguousarray(np.stack(frames), np.uint8)
+    h, w = fr.shape[1:]
+    out = np.empty((h, w), np.uint8)
+    lib = reflib() if ref else clib()
+    fn = lib.ref_median_bg_ih if ref else lib.or_median_bg_ih
+    _check(fn(fr.reshape(-1), nf, len(fr) - nf, w, h, bins, m, n, out.reshape(-1)), "median_background_ih",
+           lib if ref else None)
+    return out
+
+
+def median_bg_sort(frames, ref: bool = False) -> np.ndarray:
+    fr = np.ascontiguousarray(np.stack(frames), np.uint8)
+    h, w = fr.shape[1:]
+    out = np.empty((h, w), np.uint8)
+    lib = reflib() if ref else clib()
+    fn = lib.ref_median_bg_sort if ref else lib.or_median_bg_sort
+    _check(fn(fr.reshape(-1), len(fr), w, h, out.reshape(-1)), "median_background_sort", lib if ref else None)
     return out
 
 

@@ -21,6 +21,7 @@
 #include "spct/error.hpp"
 #include "spct/features.hpp"
 #include "spct/swih.hpp"
+#include "spct/motion.hpp"
 #include "spct/imagecore.hpp"
 #include "spct/integral.hpp"
 #include "spct/likelihood.hpp"
@@ -283,6 +284,39 @@ int ref_brute_force_swlh_fixed(const std::uint16_t* bins, int w, int h, int nbin
     return guarded([&] {
         const auto v = spct::brute_force_swlh_fixed(make_binmap(bins, w, h, nbins), cx, cy, spct::KernelSpec{kw, kh});
         std::memcpy(out, v.data(), v.size() * sizeof(std::int64_t));
+    });
+}
+
+// MedianBackgroundIH (motion.cpp:35-99): construct on frames [0, nf), slide() through the
+// rest, background(); and median_background_sort (motion.cpp:103-118).
+namespace {
+spct::GrayImage gray_of(const std::uint8_t* p, int w, int h) {
+    spct::GrayImage g(w, h);
+    std::memcpy(g.data.data(), p, static_cast<std::size_t>(w) * h);
+    return g;
+}
+}  // namespace
+
+int ref_median_bg_ih(const std::uint8_t* frames, int nf, int nslide, int w, int h, int bins, int m, int n,
+                     std::uint8_t* out) {
+    return guarded([&] {
+        const std::size_t px = static_cast<std::size_t>(w) * h;
+        spct::FrameWindow win;
+        for (int f = 0; f < nf; ++f) win.frames.push_back(gray_of(frames + f * px, w, h));
+        spct::MedianBackgroundIH bg(win, bins, m, n);
+        for (int s = 0; s < nslide; ++s) bg.slide(gray_of(frames + (nf + s) * px, w, h));
+        const spct::GrayImage o = bg.background();
+        std::memcpy(out, o.data.data(), px);
+    });
+}
+
+int ref_median_bg_sort(const std::uint8_t* frames, int nf, int w, int h, std::uint8_t* out) {
+    return guarded([&] {
+        const std::size_t px = static_cast<std::size_t>(w) * h;
+        spct::FrameWindow win;
+        for (int f = 0; f < nf; ++f) win.frames.push_back(gray_of(frames + f * px, w, h));
+        const spct::GrayImage o = spct::median_background_sort(win);
+        std::memcpy(out, o.data.data(), px);
     });
 }
 

@@ -14,7 +14,7 @@ from .api import (DEFAULT_BUDGET, IntegralHistogramTensor, ScanSchedule, build_a
                   region_histograms, schedule_from_string, schedule_stats, to_grayscale)
 from .channels import CHANNELS, channel_sources, likelihood_channels
 from .consumers import camshift_batch, camshift_refine, find_peaks, fuse_maps, score_map
-from . import swih
+from . import motion, swih
 
 __all__ = [
     "ContractError", "SpctError", "lib", "DEFAULT_BUDGET", "IntegralHistogramTensor", "ScanSchedule",
@@ -22,5 +22,5 @@ __all__ = [
     "hist_finalize", "hist_match_map", "hist_partial", "quantize", "region_count", "region_histogram",
     "region_histograms", "schedule_from_string", "schedule_stats", "to_grayscale", "orientation_bins",
     "CHANNELS", "channel_sources", "likelihood_channels", "dump_tensor", "load_tensor",
-    "fuse_maps", "find_peaks", "score_map", "camshift_refine", "camshift_batch", "swih",
+    "fuse_maps", "find_peaks", "score_map", "camshift_refine", "camshift_batch", "swih", "motion",
 ]

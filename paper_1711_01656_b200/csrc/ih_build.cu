@@ -130,7 +130,7 @@ namespace spct_build {
 
 // ------------------------------------------------------------------ main sweep
 
-template <int B, bool GUARD>
+template <int B, bool GUARD, int MODE>
 __global__ void __launch_bounds__(256) ih_sweep_kernel(QuantParams q, PixelMode pm, spct_ih out, int Lb, int Wp,
                                                        int band_rows, int warps_per_cta, FusedCarries fc) {
     const int lane = lane_id();
@@ -165,8 +165,8 @@ __global__ void __launch_bounds__(256) ih_sweep_kernel(QuantParams q, PixelMode 
         uint32_t* prow = base_ptr + static_cast<int64_t>(y) * out.row_pitch;
 #pragma unroll
         for (int g = 0; g < B / 4; ++g)
-            vpart_group_q<B>(V, g, t4, lt16_group(lt_row, g), prow + static_cast<int64_t>(4 * g) * out.plane_pitch,
-                             out.plane_pitch, store_mask);
+            vpart_group_q<B, MODE>(V, g, t4, lt16_group(lt_row, g),
+                                   prow + static_cast<int64_t>(4 * g) * out.plane_pitch, out.plane_pitch, store_mask);
     }
 }
 
@@ -231,9 +231,9 @@ int build_ctas_per_sm(int B, int threads) {
     if (cache[bi][wi]) return cache[bi][wi];
     int n = 0;
     cudaError_t e;
-    if (B == 4) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, ih_sweep_kernel<4, false>, threads, 0);
-    else if (B == 8) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, ih_sweep_kernel<8, false>, threads, 0);
-    else e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, ih_sweep_kernel<16, false>, threads, 0);
+    if (B == 4) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, ih_sweep_kernel<4, false, 0>, threads, 0);
+    else if (B == 8) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, ih_sweep_kernel<8, false, 0>, threads, 0);
+    else e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, ih_sweep_kernel<16, false, 0>, threads, 0);
     if (e != cudaSuccess || n <= 0) {
         cudaGetLastError();
         n = 2;
@@ -316,8 +316,25 @@ extern "C" spct_status spct_cu_ih_build_workspace(const spct_source* src, int bi
 }
 
 
-extern "C" spct_status spct_cu_ih_build(const spct_source* src, const spct_ih* out, void* workspace,
-                                        size_t workspace_bytes, void* stream) {
+namespace {
+
+template <int MODE>
+void launch_sweep(const BuildPlan& p, dim3 grid, int threads, cudaStream_t s, const QuantParams& q, const PixelMode& pm,
+                  const spct_ih& out, const FusedCarries& fc) {
+    switch (p.B) {
+#define SPCT_SWEEP(BB)                                                                                               \
+    ih_sweep_kernel<BB, false, MODE><<<grid, threads, 0, s>>>(q, pm, out, p.Lb, p.Wp, p.band_rows, p.warps, fc);     \
+    if (out.bins % BB) ih_sweep_kernel<BB, true, MODE><<<grid, threads, 0, s>>>(q, pm, out, p.Lb, p.Wp, p.band_rows, \
+                                                                                p.warps, fc);
+        case 4: SPCT_SWEEP(4) break;
+        case 8: SPCT_SWEEP(8) break;
+        default: SPCT_SWEEP(16) break;
+#undef SPCT_SWEEP
+    }
+}
+
+spct_status build_mode(const spct_source* src, const spct_ih* out, void* workspace, size_t workspace_bytes,
+                       void* stream, int mode) {
     QuantParams q;
     if (auto st = make_quant(src, &q)) return st;
     if (auto st = check_ih(out)) return st;
@@ -331,19 +348,26 @@ extern "C" spct_status spct_cu_ih_build(const spct_source* src, const spct_ih* o
     if (auto st = build_fused_carries(q, *out, p, workspace, workspace_bytes, s, &fc)) return st;
     dim3 grid(p.nstrips, p.nbands, p.slab_groups);
     const int threads = 32 * p.warps;
-    const int prof = prof_begin("ih_sweep", s);
+    const int prof = prof_begin(mode ? "ih_accumulate" : "ih_sweep", s);
     const PixelMode pm = make_pixel_mode(q, out->bin0);
-    switch (p.B) {
-#define SPCT_SWEEP(BB)                                                                                          \
-    ih_sweep_kernel<BB, false><<<grid, threads, 0, s>>>(q, pm, *out, p.Lb, p.Wp, p.band_rows, p.warps, fc); \
-    if (out->bins % BB) ih_sweep_kernel<BB, true><<<grid, threads, 0, s>>>(q, pm, *out, p.Lb, p.Wp, p.band_rows, p.warps, fc);
-        case 4: SPCT_SWEEP(4) break;
-        case 8: SPCT_SWEEP(8) break;
-        default: SPCT_SWEEP(16) break;
-#undef SPCT_SWEEP
-    }
+    if (mode == 0) launch_sweep<0>(p, grid, threads, s, q, pm, *out, fc);
+    else if (mode > 0) launch_sweep<1>(p, grid, threads, s, q, pm, *out, fc);
+    else launch_sweep<2>(p, grid, threads, s, q, pm, *out, fc);
     prof_end(prof, s);
     return launch_status("ih_sweep_kernel");
+}
+
+}  // namespace
+
+extern "C" spct_status spct_cu_ih_build(const spct_source* src, const spct_ih* out, void* workspace,
+                                        size_t workspace_bytes, void* stream) {
+    return build_mode(src, out, workspace, workspace_bytes, stream, 0);
+}
+
+extern "C" spct_status spct_cu_ih_accumulate(const spct_source* src, const spct_ih* acc, int sign, void* workspace,
+                                             size_t workspace_bytes, void* stream) {
+    if (sign != 1 && sign != -1) return contract("ih_accumulate: sign must be +1 or -1");
+    return build_mode(src, acc, workspace, workspace_bytes, stream, sign);
 }
 
 extern "C" spct_status spct_cu_ih_export_u64(const spct_ih* t, int k0, int k1, uint64_t* dst, void* stream) {

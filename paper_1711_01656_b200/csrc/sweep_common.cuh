@@ -116,7 +116,9 @@ __device__ __forceinline__ void onehot_shifts(uint32_t dbins, uint32_t (&t)[4]) 
 // i, the count of bin 4g+i among the lane's columns <= j (the one-hot of column j is
 // 1 << (8 r_j - 32 g)).  Q[3] is then already the packed per-lane total of the four bins
 // that the cross-lane scan needs.  `p` points at plane 4g of the row.
-template <int B>
+// MODE 0 stores the row; 1 / 2 add / subtract it into the tensor already there (the joint
+// integral histogram of a frame window, motion.cpp:51-60).
+template <int B, int MODE = 0>
 __device__ __forceinline__ void vpart_group_q(uint32_t (&V)[4][B], int g, const uint32_t (&t)[4], uint4 L, uint32_t* p,
                                               int64_t plane_pitch, uint32_t store_mask) {
     uint32_t Q[4];
@@ -137,7 +139,14 @@ __device__ __forceinline__ void vpart_group_q(uint32_t (&V)[4][B], int g, const 
         V[1][k] += Lk[i] + __byte_perm(Q[1], 0, 0x4440 + i);
         V[2][k] += Lk[i] + __byte_perm(Q[2], 0, 0x4440 + i);
         V[3][k] += Lk[i] + __byte_perm(Q[3], 0, 0x4440 + i);
-        st_cs_v4_pred(store_mask & (1u << k), p, V[0][k], V[1][k], V[2][k], V[3][k]);
+        if (MODE == 0) {
+            st_cs_v4_pred(store_mask & (1u << k), p, V[0][k], V[1][k], V[2][k], V[3][k]);
+        } else if (store_mask & (1u << k)) {
+            uint4 o = *reinterpret_cast<const uint4*>(p);
+            if (MODE == 1) o = make_uint4(o.x + V[0][k], o.y + V[1][k], o.z + V[2][k], o.w + V[3][k]);
+            else o = make_uint4(o.x - V[0][k], o.y - V[1][k], o.z - V[2][k], o.w - V[3][k]);
+            *reinterpret_cast<uint4*>(p) = o;
+        }
         p += plane_pitch;
     }
 }

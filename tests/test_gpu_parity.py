@@ -623,3 +623,22 @@ def test_swlh_distance_map(P, kw, kh, w, h):
     assert close(got, want)
     if w >= kw and h >= kh:
         assert got[h // 2, w // 2] == 1.0
+
+
+# ------------------------------------------------------------------ joint-IH median (§8(f) #4)
+
+@pytest.mark.parametrize("w,h,bins,m,n,nf,nslide", [(23, 17, 8, 3, 5, 5, 0), (140, 131, 16, 7, 7, 3, 4),
+                                                      (9, 9, 4, 1, 1, 1, 2), (260, 150, 32, 5, 3, 7, 1),
+                                                      (300, 40, 5, 9, 9, 5, 3)])
+def test_median_background_bit_exact(P, w, h, bins, m, n, nf, nslide):
+    rng = np.random.default_rng(w * h + bins)
+    frames = [rng.integers(0, bins, (h, w), dtype=np.uint8) for _ in range(nf + nslide)]
+    bg = P.motion.MedianBackgroundIH(frames[:nf], bins, m, n)
+    for f in frames[nf:]:
+        bg.slide(f)
+    assert np.array_equal(bg.background().cpu().numpy(), oracle.median_bg_ih(frames, nf, bins, m, n))
+    assert np.array_equal(P.motion.median_background_sort(frames[:nf]).cpu().numpy(), oracle.median_bg_sort(frames[:nf]))
+    with pytest.raises(P.ContractError):
+        P.motion.MedianBackgroundIH(frames[:nf], max(1, int(frames[0].max())), m, n)  # value exceeds bin count
+    with pytest.raises(P.ContractError):
+        P.motion.MedianBackgroundIH(frames[:2], bins, m, n)  # even window

@@ -284,3 +284,17 @@ def test_swlh_degenerate_known_answers():
         for x in range(9):
             q = oracle.swlh(bm, 5, x, y, 1, 1)
             assert q[bm[y, x]] == 1.0 and q.sum() == 1.0
+
+
+# ------------------------------------------------------------------ joint-IH median (§8(f) #4)
+
+@ref
+@pytest.mark.parametrize("w,h,bins,m,n,nf,nslide", [(23, 17, 8, 3, 5, 5, 0), (40, 31, 16, 7, 7, 3, 4),
+                                                      (9, 9, 4, 1, 1, 1, 2), (31, 20, 32, 5, 3, 7, 1)])
+def test_median_bg_vs_live_reference(w, h, bins, m, n, nf, nslide):
+    rng = np.random.default_rng(w * h + bins)
+    frames = [rng.integers(0, bins, (h, w), dtype=np.uint8) for _ in range(nf + nslide)]
+    assert np.array_equal(oracle.median_bg_ih(frames, nf, bins, m, n), oracle.median_bg_ih(frames, nf, bins, m, n, True))
+    assert np.array_equal(oracle.median_bg_sort(frames[:nf]), oracle.median_bg_sort(frames[:nf], True))
+    with pytest.raises(oracle.ContractError):
+        oracle.median_bg_ih(frames, nf, bins - 1 if bins > 1 else 0, m, n, True)  # value exceeds bin count
