@@ -133,9 +133,19 @@ spct_status build_match(const spct_source* src, const spct_ih* out, const double
         // the group is the whole histogram: window totals over its bins are kw * kh
         const bool allb = out->bin0 == 0 && out->bins == out->nbins_total && ngroups == 1;
         const bool g8 = q.kind == SPCT_SRC_GRAY_U8 && q.fast_u8;
-        if (kw == 64) launch_kw64(allb, g8, grid, s, q, pm, *out, bp, fc, f);
-        else if (kw == 128) launch_kw128(allb, g8, grid, s, q, pm, *out, bp, fc, f);
-        else launch_kw_any(allb, g8, grid, s, q, pm, *out, bp, fc, f);
+        const int nw = fused_nw(out->bins);
+#define SPCT_LAUNCH(KW)                                                                                     \
+    if (nw == 8) launch_##KW##_nw8(allb, g8, grid, s, q, pm, *out, bp, fc, f);                                  \
+    else if (nw == 4) launch_##KW##_nw4(allb, g8, grid, s, q, pm, *out, bp, fc, f);                             \
+    else launch_##KW##_nw2(allb, g8, grid, s, q, pm, *out, bp, fc, f);
+        if (kw == 64) {
+            SPCT_LAUNCH(kw64)
+        } else if (kw == 128) {
+            SPCT_LAUNCH(kw128)
+        } else {
+            SPCT_LAUNCH(kw_any)
+        }
+#undef SPCT_LAUNCH
         prof_end(prof, s);
         note_launch();
         if (auto st = launch_status("sweep_match_kernel")) return st;

@@ -35,9 +35,8 @@ namespace spct_fused {
 using namespace spct_dev;
 using namespace spct_impl;
 
-constexpr int kWarps = 8;
 constexpr int kB = 16;
-constexpr int kGroupBins = kWarps * kB;  // 128 bins per CTA
+constexpr int kGroupBins = 128;          // bins per launch group (the widest CTA: 8 warps x 16)
 constexpr int kExt = 256;                // extended columns per CTA (128 halo + 128 strip)
 constexpr int kVcWords = kExt / 2;       // u16 pairs per bin row
 constexpr int kVcStride = kVcWords + kVcWords / 8;  // row stride: 4 padding words after every 32
@@ -241,16 +240,28 @@ __device__ __forceinline__ void quarter_reduce(uint32_t (&v)[8], int q) {
 // total over the group's bins is kw * kh and need not be accumulated.
 // G8: 8-bit gray input with the default range (bin = v * nbins >> 8): the staging loads
 // and quantises without the generic per-kind dispatch.
-template <bool STORE, bool FAST, int KWM, bool ALLB, bool G8>
-__global__ void __launch_bounds__(256, 2) sweep_match_kernel(QuantParams q, PixelMode pm, spct_ih out, int Lb, int Wp,
-                                                             int band_rows, FusedCarries fc, FusedParams f) {
+// NW: warps per CTA (16 NW bins of the group): 8 for >= 65 bins, fewer for small
+// histograms so that every warp of a CTA has bins (configs 2 and 5 use 32 bins).
+template <int NW>
+constexpr size_t smem_bytes_nw() {
+    return (size_t(NW * kB) * kVcStride + size_t(NW) * 4 * kVcWords) * 4 + size_t(2) * NW * kStrip * 8 +
+           size_t(NW * kB) * 4 * 3 + size_t(2) * kStrip * 2 + 64 * 4;
+}
+
+template <bool STORE, bool FAST, int KWM, bool ALLB, bool G8, int NW>
+__global__ void __launch_bounds__(32 * NW, 16 / NW) sweep_match_kernel(QuantParams q, PixelMode pm, spct_ih out, int Lb,
+                                                                       int Wp, int band_rows, FusedCarries fc,
+                                                                       FusedParams f) {
+    constexpr int NB = NW * kB;              // bins per CTA
+    constexpr int NT = 32 * NW;              // threads per CTA
+    constexpr int CPT = kExt / NT;           // staged extended columns per thread
     extern __shared__ uint4 smem_raw[];
-    uint32_t* vc = reinterpret_cast<uint32_t*>(smem_raw);                 // [128 bins][144 words], padded
-    uint32_t* gbuf = vc + kGroupBins * kVcStride;                           // [8 warps][4][128 words] (general path)
-    double* red = reinterpret_cast<double*>(gbuf + kWarps * 4 * kVcWords);  // [2 rows][8 warps][128]
-    uint32_t* srep_s = reinterpret_cast<uint32_t*>(red + 2 * kWarps * kStrip);  // [128]
-    uint32_t* lrow = srep_s + kGroupBins;                                   // [2 rows][128] row carries
-    uint16_t* rowbins = reinterpret_cast<uint16_t*>(lrow + 2 * kGroupBins);  // [2 rows][128] strip bins
+    uint32_t* vc = reinterpret_cast<uint32_t*>(smem_raw);                 // [NB bins][144 words], padded
+    uint32_t* gbuf = vc + NB * kVcStride;                                   // [NW warps][4][128 words] (general path)
+    double* red = reinterpret_cast<double*>(gbuf + NW * 4 * kVcWords);      // [2 rows][NW warps][128]
+    uint32_t* srep_s = reinterpret_cast<uint32_t*>(red + 2 * NW * kStrip);  // [NB]
+    uint32_t* lrow = srep_s + NB;                                           // [2 rows][NB] row carries
+    uint16_t* rowbins = reinterpret_cast<uint16_t*>(lrow + 2 * NB);         // [2 rows][128] strip bins
     uint32_t* amask = reinterpret_cast<uint32_t*>(rowbins + 2 * kStrip);    // [8 lanes][8 words] anchor masks
     // integer path: per row parity and window pair, the packed sums over the warps (atomic
     // adds), I at [parity][64] and C at 128 + [parity][64]
@@ -262,7 +273,7 @@ __global__ void __launch_bounds__(256, 2) sweep_match_kernel(QuantParams q, Pixe
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int strip = blockIdx.x, band = blockIdx.y;
     const int g0 = f.group0;                               // slab-local first bin of the CTA
-    const int nb_cta = min(kGroupBins, out.bins - g0);
+    const int nb_cta = min(NB, out.bins - g0);
     const int nwarps_live = (nb_cta + kB - 1) / kB;
     const int kl0 = g0 + warp * kB;                        // warp's first slab-local bin
     const bool warp_live = warp < nwarps_live;
@@ -282,14 +293,16 @@ __global__ void __launch_bounds__(256, 2) sweep_match_kernel(QuantParams q, Pixe
         return G8 ? static_cast<int>((static_cast<uint32_t>(r) * static_cast<uint32_t>(q.nbins)) >> 8) : bin_of_raw(r, q);
     };
 
-    for (int i = tid; i < kGroupBins * kVcStride; i += blockDim.x) vc[i] = 0;
-    if (FAST) red32[tid] = 0;  // row accumulators {I} [2][64] and {C} [2][64]
-    if (tid < kGroupBins) srep_s[tid] = (FAST && tid < nb_cta) ? __ldg(f.prep + 1 + g0 + tid) : 0u;
-    if (FAST && KWM == 0 && tid < 64) {
-        // anchor masks: u16 i of lane m's word j is valid iff 16m + 2j + i < kw
-        const int n = f.kw - 16 * (tid >> 3) - 2 * (tid & 7);
-        amask[tid] = n >= 2 ? 0xFFFFFFFFu : (n == 1 ? 0xFFFFu : 0u);
-    }
+    for (int i = tid; i < NB * kVcStride; i += NT) vc[i] = 0;
+    if (FAST)
+        for (int i = tid; i < 256; i += NT) red32[i] = 0;  // row accumulators {I} [2][64] and {C} [2][64]
+    if (tid < NB) srep_s[tid] = (FAST && tid < nb_cta) ? __ldg(f.prep + 1 + g0 + tid) : 0u;
+    if (FAST && KWM == 0)
+        for (int i = tid; i < 64; i += NT) {
+            // anchor masks: u16 i of lane m's word j is valid iff 16m + 2j + i < kw
+            const int n = f.kw - 16 * (i >> 3) - 2 * (i & 7);
+            amask[i] = n >= 2 ? 0xFFFFFFFFu : (n == 1 ? 0xFFFFu : 0u);
+        }
 
     uint32_t V[4][kB];
     if (STORE && warp_live)
@@ -310,16 +323,25 @@ __global__ void __launch_bounds__(256, 2) sweep_match_kernel(QuantParams q, Pixe
     const uint32_t* vq = vwarp + qq * kVcStride;  // the quarter's bin row for g = 0
     const uint32_t* pb = vq + vcw(64 + 8 * mq);
 
-    // staging thread: extended column tid; prefetch one row ahead
-    const int xt = xs - kStrip + tid;
-    const bool xt_live = xt >= 0 && xt < W;
-    const int vcol_w = vcw(tid >> 1);        // the staging column's (padded) vc word
-    const uint32_t vinc = 1u << (16 * (tid & 1));
-    const uint16_t* lt_cta = (STORE && fc.Lt && strip > 0 && tid < kGroupBins && g0 + tid < Lb)
+    // staging: thread tid owns extended columns tid + c NT (c < CPT); with one column per
+    // thread (NW = 8) its raw pixels are prefetched one row ahead
+    constexpr bool PREFETCH = CPT == 1;
+    int xt[CPT], vcol_w[CPT];
+    bool xt_live[CPT];
+    uint32_t vinc[CPT];
+#pragma unroll
+    for (int c = 0; c < CPT; ++c) {
+        const int col = tid + c * NT;
+        xt[c] = xs - kStrip + col;
+        xt_live[c] = xt[c] >= 0 && xt[c] < W;
+        vcol_w[c] = vcw(col >> 1);  // the column's (padded) vc word
+        vinc[c] = 1u << (16 * (col & 1));
+    }
+    const uint16_t* lt_cta = (STORE && fc.Lt && strip > 0 && tid < NB && g0 + tid < Lb)
                                  ? fc.Lt + static_cast<int64_t>(strip) * H * Lb + g0 + tid
                                  : nullptr;
     // raw pixel values of the staging column, quantised one row after the load
-    uint64_t rn = xt_live ? raw_at(xt, y0) : 0, ro = 0;
+    uint64_t rn = (PREFETCH && xt_live[0]) ? raw_at(xt[0], y0) : 0, ro = 0;
     bool have_o = false;  // y0 - kh < ystart: nothing to remove on the first row
     uint32_t lpre = lt_cta ? static_cast<uint32_t>(__ldg(lt_cta + static_cast<int64_t>(y0) * Lb)) : 0u;
     __syncthreads();  // vc zeroed
@@ -327,21 +349,23 @@ __global__ void __launch_bounds__(256, 2) sweep_match_kernel(QuantParams q, Pixe
     // Pre-roll rows [ystart, y0) only feed vc, and nothing leaves the window there: one
     // barrier-free pass with several loads in flight (a per-row loop would pay the full
     // DRAM latency on every row).
-    if (xt_live) {
-        const int nb_lo = out.bin0 + g0;
-        uint32_t* vcol = vc + vcol_w;
-        for (int y = ystart; y < y0; y += 8) {
-            uint64_t r[8];
 #pragma unroll
-            for (int i = 0; i < 8; ++i) r[i] = y + i < y0 ? raw_at(xt, y + i) : 0;
+    for (int c = 0; c < CPT; ++c)
+        if (xt_live[c]) {
+            const int nb_lo = out.bin0 + g0;
+            uint32_t* vcol = vc + vcol_w[c];
+            for (int y = ystart; y < y0; y += 8) {
+                uint64_t r[8];
 #pragma unroll
-            for (int i = 0; i < 8; ++i) {
-                const int bn = bin_of(r[i]) - nb_lo;
-                if (y + i < y0 && static_cast<unsigned>(bn) < static_cast<unsigned>(nb_cta))
-                    atomicAdd(vcol + bn * kVcStride, vinc);
+                for (int i = 0; i < 8; ++i) r[i] = y + i < y0 ? raw_at(xt[c], y + i) : 0;
+#pragma unroll
+                for (int i = 0; i < 8; ++i) {
+                    const int bn = bin_of(r[i]) - nb_lo;
+                    if (y + i < y0 && static_cast<unsigned>(bn) < static_cast<unsigned>(nb_cta))
+                        atomicAdd(vcol + bn * kVcStride, vinc[c]);
+                }
             }
         }
-    }
 
     // Cross-warp combine of row yy: thread t < 128 finishes the window ending at strip
     // column t.  Integer path with a finished map (ALLB): L = alpha + beta I (one FMA).
@@ -360,9 +384,7 @@ __global__ void __launch_bounds__(256, 2) sweep_match_kernel(QuantParams q, Pixe
         for (int yy = ya; yy <= yb; ++yy)
             for (int xx = xa; xx <= xb; ++xx) f.map[static_cast<int64_t>(yy) * f.W + xx] = L;
     };
-    auto combine = [&](int yy) {
-        if (tid >= kStrip) return;
-        const int t = tid;
+    auto combine_one = [&](int yy, int t) {
         const int e = xs + t;
         const int u = e - f.kw + 1, v = yy - f.kh + 1;
         if (FAST) {
@@ -394,10 +416,10 @@ __global__ void __launch_bounds__(256, 2) sweep_match_kernel(QuantParams q, Pixe
             }
         } else {
             if (u < 0 || e >= W) return;
-            const double* rb = red + (yy & 1) * (kWarps * kStrip);
+            const double* rb = red + (yy & 1) * (NW * kStrip);
             double term = 0.0;
 #pragma unroll
-            for (int w = 0; w < kWarps; ++w)
+            for (int w = 0; w < NW; ++w)
                 if (w < nwarps_live) term = __dadd_rn(term, rb[w * kStrip + t]);
             if (f.map) {
                 write_map(u, v, finalize_L(term, f));
@@ -406,6 +428,10 @@ __global__ void __launch_bounds__(256, 2) sweep_match_kernel(QuantParams q, Pixe
                 *dst = f.accumulate ? __dadd_rn(*dst, term) : term;
             }
         }
+    };
+    auto combine = [&](int yy) {
+#pragma unroll
+        for (int t = tid; t < kStrip; t += NT) combine_one(yy, t);
     };
 
     // row yy's partials are in `red` (and must be combined) iff it is a match row
@@ -417,23 +443,34 @@ __global__ void __launch_bounds__(256, 2) sweep_match_kernel(QuantParams q, Pixe
         if (pending(y - 1)) combine(y - 1);
         {   // stage row y: vertical running histogram (add row y, remove row y - kh),
             // the strip's bins and row carries for the sweep, then prefetch row y + 1
-            const int pn = xt_live ? bin_of(rn) : 0xFFFF;
-            const int po = (xt_live && have_o) ? bin_of(ro) : -1;
-            if (xt_live) {
-                const int bn = pn - out.bin0 - g0;
-                if (static_cast<unsigned>(bn) < static_cast<unsigned>(nb_cta)) atomicAdd(&vc[bn * kVcStride + vcol_w], vinc);
-                const int bo = po - out.bin0 - g0;
-                if (po >= 0 && static_cast<unsigned>(bo) < static_cast<unsigned>(nb_cta))
-                    atomicSub(&vc[bo * kVcStride + vcol_w], vinc);
+            const bool old_row = y - f.kh >= ystart;
+#pragma unroll
+            for (int c = 0; c < CPT; ++c) {
+                const uint64_t rnc = PREFETCH ? rn : (xt_live[c] ? raw_at(xt[c], y) : 0);
+                const uint64_t roc = PREFETCH ? ro : ((xt_live[c] && old_row) ? raw_at(xt[c], y - f.kh) : 0);
+                const bool ho = PREFETCH ? have_o : old_row;
+                const int pn = xt_live[c] ? bin_of(rnc) : 0xFFFF;
+                const int po = (xt_live[c] && ho) ? bin_of(roc) : -1;
+                if (xt_live[c]) {
+                    const int bn = pn - out.bin0 - g0;
+                    if (static_cast<unsigned>(bn) < static_cast<unsigned>(nb_cta))
+                        atomicAdd(&vc[bn * kVcStride + vcol_w[c]], vinc[c]);
+                    const int bo = po - out.bin0 - g0;
+                    if (po >= 0 && static_cast<unsigned>(bo) < static_cast<unsigned>(nb_cta))
+                        atomicSub(&vc[bo * kVcStride + vcol_w[c]], vinc[c]);
+                }
+                const int col = tid + c * NT;
+                if (col >= kStrip) rowbins[(y & 1) * kStrip + col - kStrip] = static_cast<uint16_t>(pn);
             }
-            if (tid >= kStrip) rowbins[(y & 1) * kStrip + tid - kStrip] = static_cast<uint16_t>(pn);
-            else lrow[(y & 1) * kGroupBins + tid] = lpre;
+            if (tid < NB) lrow[(y & 1) * NB + tid] = lpre;
             if (y + 1 < y1) {
-                const int yo = y + 1 - f.kh;
-                have_o = yo >= ystart;
-                if (xt_live) {
-                    rn = raw_at(xt, y + 1);
-                    if (have_o) ro = raw_at(xt, yo);
+                if (PREFETCH) {
+                    const int yo = y + 1 - f.kh;
+                    have_o = yo >= ystart;
+                    if (xt_live[0]) {
+                        rn = raw_at(xt[0], y + 1);
+                        if (have_o) ro = raw_at(xt[0], yo);
+                    }
                 }
                 if (lt_cta) lpre = __ldg(lt_cta + static_cast<int64_t>(y + 1) * Lb);
             }
@@ -458,7 +495,7 @@ __global__ void __launch_bounds__(256, 2) sweep_match_kernel(QuantParams q, Pixe
             }
             onehot_shifts(bins4 ^ kpat0, t4);
         }
-        const uint4* lr = reinterpret_cast<const uint4*>(lrow + (y & 1) * kGroupBins + warp * kB);
+        const uint4* lr = reinterpret_cast<const uint4*>(lrow + (y & 1) * NB + warp * kB);
         uint32_t* prow = STORE ? base_ptr + static_cast<int64_t>(y) * out.row_pitch : nullptr;
 
         uint32_t Iw[8] = {0, 0, 0, 0, 0, 0, 0, 0}, Cw[8] = {0, 0, 0, 0, 0, 0, 0, 0};
@@ -539,7 +576,7 @@ __global__ void __launch_bounds__(256, 2) sweep_match_kernel(QuantParams q, Pixe
                     atomicAdd(rw + 129, Cw[1]);
                 }
             } else {
-                double* rb = red + (y & 1) * (kWarps * kStrip) + warp * kStrip;
+                double* rb = red + (y & 1) * (NW * kStrip) + warp * kStrip;
                 rb[4 * lane + 0] = acc[0];
                 rb[4 * lane + 1] = acc[1];
                 rb[4 * lane + 2] = acc[2];
@@ -551,56 +588,64 @@ __global__ void __launch_bounds__(256, 2) sweep_match_kernel(QuantParams q, Pixe
     if (y1 > y0 && pending(y1 - 1)) combine(y1 - 1);
 }
 
-constexpr size_t kSmemBytes = (size_t(kGroupBins) * kVcStride + size_t(kWarps) * 4 * kVcWords) * 4 +
-                              size_t(2) * kWarps * kStrip * 8 + size_t(kGroupBins) * 4 * 3 + size_t(2) * kStrip * 2 +
-                              64 * 4;
+constexpr size_t kSmemBytes = smem_bytes_nw<8>();
 
 
-template <int KWM, bool ALLB, bool G8>
+template <int KWM, bool ALLB, bool G8, int NW>
 void launch_variants(dim3 grid, cudaStream_t s, const QuantParams& q, const PixelMode& pm, const spct_ih& out,
                      const BuildPlan& bp, const FusedCarries& fc, const FusedParams& f) {
+    constexpr int NT = 32 * NW;
+    constexpr size_t SM = smem_bytes_nw<NW>();
     static bool attr_set = false;
     if (!attr_set) {
-        cudaFuncSetAttribute(sweep_match_kernel<true, true, KWM, ALLB, G8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBytes);
-        cudaFuncSetAttribute(sweep_match_kernel<true, false, KWM, false, G8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBytes);
-        cudaFuncSetAttribute(sweep_match_kernel<false, true, KWM, ALLB, G8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBytes);
-        cudaFuncSetAttribute(sweep_match_kernel<false, false, KWM, false, G8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBytes);
+        cudaFuncSetAttribute(sweep_match_kernel<true, true, KWM, ALLB, G8, NW>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SM);
+        cudaFuncSetAttribute(sweep_match_kernel<true, false, KWM, false, G8, NW>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SM);
+        cudaFuncSetAttribute(sweep_match_kernel<false, true, KWM, ALLB, G8, NW>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SM);
+        cudaFuncSetAttribute(sweep_match_kernel<false, false, KWM, false, G8, NW>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SM);
         attr_set = true;
     }
     // integer (template-crop) variant and FP64 variant: the one not selected by the
     // device-side template prep exits on entry
     if (out.data) {
-        sweep_match_kernel<true, true, KWM, ALLB, G8><<<grid, 256, kSmemBytes, s>>>(q, pm, out, bp.Lb, bp.Wp, bp.band_rows, fc, f);
-        sweep_match_kernel<true, false, KWM, false, G8><<<grid, 256, kSmemBytes, s>>>(q, pm, out, bp.Lb, bp.Wp, bp.band_rows, fc, f);
+        sweep_match_kernel<true, true, KWM, ALLB, G8, NW><<<grid, NT, SM, s>>>(q, pm, out, bp.Lb, bp.Wp, bp.band_rows, fc, f);
+        sweep_match_kernel<true, false, KWM, false, G8, NW><<<grid, NT, SM, s>>>(q, pm, out, bp.Lb, bp.Wp, bp.band_rows, fc, f);
     } else {
-        sweep_match_kernel<false, true, KWM, ALLB, G8><<<grid, 256, kSmemBytes, s>>>(q, pm, out, bp.Lb, bp.Wp, bp.band_rows, FusedCarries{}, f);
-        sweep_match_kernel<false, false, KWM, false, G8><<<grid, 256, kSmemBytes, s>>>(q, pm, out, bp.Lb, bp.Wp, bp.band_rows, FusedCarries{}, f);
+        sweep_match_kernel<false, true, KWM, ALLB, G8, NW><<<grid, NT, SM, s>>>(q, pm, out, bp.Lb, bp.Wp, bp.band_rows, FusedCarries{}, f);
+        sweep_match_kernel<false, false, KWM, false, G8, NW><<<grid, NT, SM, s>>>(q, pm, out, bp.Lb, bp.Wp, bp.band_rows, FusedCarries{}, f);
     }
 }
 
-template <int KWM>
+template <int KWM, int NW>
 void launch_kw_impl(bool allb, bool g8, dim3 grid, cudaStream_t s, const QuantParams& q, const PixelMode& pm,
                     const spct_ih& out, const BuildPlan& bp, const FusedCarries& fc, const FusedParams& f) {
     if (g8) {
-        if (allb) launch_variants<KWM, true, true>(grid, s, q, pm, out, bp, fc, f);
-        else launch_variants<KWM, false, true>(grid, s, q, pm, out, bp, fc, f);
+        if (allb) launch_variants<KWM, true, true, NW>(grid, s, q, pm, out, bp, fc, f);
+        else launch_variants<KWM, false, true, NW>(grid, s, q, pm, out, bp, fc, f);
     } else {
-        if (allb) launch_variants<KWM, true, false>(grid, s, q, pm, out, bp, fc, f);
-        else launch_variants<KWM, false, false>(grid, s, q, pm, out, bp, fc, f);
+        if (allb) launch_variants<KWM, true, false, NW>(grid, s, q, pm, out, bp, fc, f);
+        else launch_variants<KWM, false, false, NW>(grid, s, q, pm, out, bp, fc, f);
     }
 }
 
 }  // namespace spct_fused
 
 namespace spct_fused {
-// One translation unit per window-width specialisation (fused_kw{64,128,0}.cu), so the
-// kernel variants compile in parallel.
+// One translation unit per (window-width specialisation, warps per CTA), so the kernel
+// variants compile in parallel: fused_kw{64,128,0}_nw{2,4,8}.cu.
 #define SPCT_FUSED_LAUNCHER(NAME)                                                                              \
     void NAME(bool allb, bool g8, dim3 grid, cudaStream_t s, const QuantParams& q, const PixelMode& pm,       \
               const spct_ih& out, const BuildPlan& bp, const FusedCarries& fc, const FusedParams& f);
-SPCT_FUSED_LAUNCHER(launch_kw64)
-SPCT_FUSED_LAUNCHER(launch_kw128)
-SPCT_FUSED_LAUNCHER(launch_kw_any)
+SPCT_FUSED_LAUNCHER(launch_kw64_nw8)
+SPCT_FUSED_LAUNCHER(launch_kw64_nw4)
+SPCT_FUSED_LAUNCHER(launch_kw64_nw2)
+SPCT_FUSED_LAUNCHER(launch_kw128_nw8)
+SPCT_FUSED_LAUNCHER(launch_kw128_nw4)
+SPCT_FUSED_LAUNCHER(launch_kw128_nw2)
+SPCT_FUSED_LAUNCHER(launch_kw_any_nw8)
+SPCT_FUSED_LAUNCHER(launch_kw_any_nw4)
+SPCT_FUSED_LAUNCHER(launch_kw_any_nw2)
 #undef SPCT_FUSED_LAUNCHER
 size_t smem_bytes();
+// Warps per CTA of the fused sweep for a slab of `bins` bins (2, 4 or 8).
+inline int fused_nw(int bins) { return bins > 64 ? 8 : (bins > 32 ? 4 : 2); }
 }  // namespace spct_fused

@@ -1,0 +1,39 @@
+// Instantiations of the fused build+match sweep for kw = 64,
+// 8 warps per CTA (see fused_kernel.cuh).
+#include "fused_kernel.cuh"
+
+namespace spct_fused {
+void launch_kw64_nw8(bool allb, bool g8, dim3 grid, cudaStream_t s, const QuantParams& q, const PixelMode& pm, const spct_ih& out,
+          const BuildPlan& bp, const FusedCarries& fc, const FusedParams& f) {
+    launch_kw_impl<64, 8>(allb, g8, grid, s, q, pm, out, bp, fc, f);
+}
+size_t smem_bytes() { return kSmemBytes; }
+}  // namespace spct_fused
+
+namespace spct_impl {
+int fused_ctas_per_sm(int nw) {
+    static int n[9] = {};
+    nw = nw >= 8 ? 8 : (nw >= 4 ? 4 : 2);
+    if (n[nw]) return n[nw];
+    int v = 0;
+    cudaError_t e;
+    if (nw == 8) {
+        auto k = spct_fused::sweep_match_kernel<true, true, 64, true, true, 8>;
+        cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)spct_fused::smem_bytes_nw<8>());
+        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&v, k, 256, spct_fused::smem_bytes_nw<8>());
+    } else if (nw == 4) {
+        auto k = spct_fused::sweep_match_kernel<true, true, 64, true, true, 4>;
+        cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)spct_fused::smem_bytes_nw<4>());
+        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&v, k, 128, spct_fused::smem_bytes_nw<4>());
+    } else {
+        auto k = spct_fused::sweep_match_kernel<true, true, 64, true, true, 2>;
+        cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)spct_fused::smem_bytes_nw<2>());
+        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&v, k, 64, spct_fused::smem_bytes_nw<2>());
+    }
+    if (e != cudaSuccess || v <= 0) {
+        cudaGetLastError();
+        v = 16 / nw;
+    }
+    return n[nw] = v;
+}
+}  // namespace spct_impl

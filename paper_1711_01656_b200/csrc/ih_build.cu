@@ -247,7 +247,11 @@ BuildPlan plan_build_sweep(int width, int height, int bins) {
 }
 
 BuildPlan plan_fused_sweep(int width, int height, int bins) {
-    return plan_build(width, height, bins, 16, fused_ctas_per_sm(), 64);
+    // warps per CTA as in spct_fused::fused_nw (fused_kernel.cuh)
+    // The band floor trades the kh - 1 pre-roll rows of every band against filling the
+    // GPU: narrow CTAs (small histograms) need more bands to reach full occupancy.
+    const int nw = bins > 64 ? 8 : (bins > 32 ? 4 : 2);
+    return plan_build(width, height, bins, 16, fused_ctas_per_sm(nw), 8 * nw);
 }
 
 }  // namespace spct_impl

@@ -62,7 +62,7 @@ BuildPlan plan_build(int width, int height, int bins, int force_B = 0, int ctas_
 // Resident CTAs per SM of the build sweep (B bins per warp, `threads` per CTA) and of the
 // fused sweep; used to size bands in whole waves.  Fall back to 2 without a device.
 int build_ctas_per_sm(int B, int threads);
-int fused_ctas_per_sm();
+int fused_ctas_per_sm(int nw = 8);
 int device_sms();
 // The two plans every caller (workspace query included) must agree on.
 BuildPlan plan_build_sweep(int width, int height, int bins);
