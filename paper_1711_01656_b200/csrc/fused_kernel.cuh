@@ -196,9 +196,15 @@ __device__ __forceinline__ void window_counts_q(const uint32_t* pb, const uint32
         for (int j = 0; j < 8; ++j) a[j] = __funnelshift_r(r[j], r[j + 1], apsh);
     }
 #pragma unroll
-    for (int j = 0; j < 8; ++j) {
+    for (int j = 0; j < 8; ++j) {  // two independent 4-word chains, joined below
         const uint32_t d = b[j] - a[j];  // {delta, delta} pair, linear encoding
-        w[j] = d * 0x10001u + (j ? __byte_perm(w[j - 1], 0, 0x3232) : 0x0FF00FF0u);
+        w[j] = d * 0x10001u + ((j & 3) ? __byte_perm(w[j - 1], 0, 0x3232) : 0x0FF00FF0u);
+    }
+    {   // words 4..7 started from the same +4080 offset: add the first half's total
+        const uint32_t join = (w[3] >> 16) - 4080u;  // >= -4080: the halves stay non-negative
+        const uint32_t j2 = join * 0x10001u;
+#pragma unroll
+        for (int j = 4; j < 8; ++j) w[j] += j2;
     }
     uint32_t x;  // anchor partial as a u16 pair sum
     if (KWM == 64 || KWM == 128) {
