@@ -215,7 +215,7 @@ def run_c5(P, dev, stream, args, frames: int = 100, side: int = 2048, nbins: int
         if c == "orientation":
             qb = s
         else:
-            qb = P.quantize(P.to_grayscale(*s) if isinstance(s, tuple) else s, nbins)
+            qb = P.quantize(s, nbins)
         crop = qb[y0:y0 + kh, x0:x0 + kw].to(torch.int64).reshape(-1) & 0xFFFF
         tdev[c] = (torch.bincount(crop, minlength=nbins).to(torch.float64) / crop.numel()).contiguous()
     tens = {c: P.IntegralHistogramTensor(side, side, nbins, device=dev) for c in P.CHANNELS}

@@ -19,11 +19,12 @@ CHANNELS = ("intensity", "orientation", "red", "green", "blue")
 
 
 def channel_sources(r, g, b, nbins: int, sigma: float = 1.0, stream=None) -> dict:
-    """Device sources of the five channels: RGB planes (intensity is quantised from the
-    fused gray of the RGB source), the orientation BinMap, and the single planes."""
+    """Device sources of the five channels: the gray frame (to_grayscale, quantised in the
+    sweep's load stage: quantize(to_grayscale(rgb)) exactly), the orientation BinMap of
+    the gray frame, and the single R, G, B planes."""
     rd, gd, bd = (_api._dev(p, torch.uint8) for p in (r, g, b))
     gray = _api.to_grayscale(rd, gd, bd, stream=stream)
-    return {"intensity": (rd, gd, bd), "orientation": _api.orientation_bins(gray, nbins, sigma, stream=stream),
+    return {"intensity": gray, "orientation": _api.orientation_bins(gray, nbins, sigma, stream=stream),
             "red": rd, "green": gd, "blue": bd}
 
 

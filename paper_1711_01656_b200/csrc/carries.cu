@@ -13,9 +13,9 @@ using namespace spct_dev;
 // no 32-bit band-carry table is written or read.  Two passes over 1 B/px:
 //   fcarry_tiles_kernel   one CTA per (strip, band, 128-bin chunk): the strip-row
 //                         histograms (u8), the band's column counts and band x strip totals;
-//   fcarry_prefix_kernel  prefix of the strip-row histograms over strips (-> Lt16) and of
-//                         the column counts over bands (in place -> C16);
-//   fcarry_corner_kernel  one CTA per bin: 2-D prefix of the band x strip totals (-> A32).
+//   fcarry_prefix_kernel  prefix of the strip-row histograms over strips (-> Lt16), of the
+//                         column counts over bands (in place -> C16), and one CTA per bin
+//                         for the 2-D prefix of the band x strip totals (-> A32).
 
 namespace spct_carry {
 
@@ -117,9 +117,18 @@ __global__ void __launch_bounds__(256) fcarry_tiles_kernel(QuantParams q, int bi
 
 // Blocks [0, nb_lt): row carries (thread = (row, 4 bins)); blocks [nb_lt, ...): column
 // counts over bands (thread = (bin, 4 columns)), in place.
+// ... and blocks [nb_lt + nb_c, + Lb): the corner sums of one bin each (corner_block).
+__device__ void corner_block(int kl, int nstrips, int nbands, uint32_t* __restrict__ T1, uint32_t* tsm);
+
 __global__ void __launch_bounds__(256) fcarry_prefix_kernel(int H, int Lb, int Wp, int nstrips, int nbands, int nb_lt,
-                                                            const uint8_t* __restrict__ R8,
-                                                            uint16_t* __restrict__ Lt16, uint16_t* __restrict__ C16) {
+                                                            int nb_c, const uint8_t* __restrict__ R8,
+                                                            uint16_t* __restrict__ Lt16, uint16_t* __restrict__ C16,
+                                                            uint32_t* __restrict__ A32) {
+    extern __shared__ uint32_t corner_sm[];
+    if (static_cast<int>(blockIdx.x) >= nb_lt + nb_c) {
+        corner_block(static_cast<int>(blockIdx.x) - nb_lt - nb_c, nstrips, nbands, A32, corner_sm);
+        return;
+    }
     if (static_cast<int>(blockIdx.x) < nb_lt) {
         const int64_t i = static_cast<int64_t>(blockIdx.x) * 256 + threadIdx.x;  // (y, quad)
         const int quads = Lb / 4;
@@ -165,10 +174,9 @@ __global__ void __launch_bounds__(256) fcarry_prefix_kernel(int H, int Lb, int W
 }
 
 // One CTA per bin: A[kl][j][s] = sum_{j' <= j} sum_{s' < s} T1[kl][j'][s'], in place.
-__global__ void __launch_bounds__(256) fcarry_corner_kernel(int nstrips, int nbands, uint32_t* __restrict__ T1) {
-    extern __shared__ uint32_t tsm[];
+__device__ void corner_block(int kl, int nstrips, int nbands, uint32_t* __restrict__ T1, uint32_t* tsm) {
     const int J = nbands - 1, S = nstrips;
-    uint32_t* t = T1 + static_cast<int64_t>(blockIdx.x) * J * S;
+    uint32_t* t = T1 + static_cast<int64_t>(kl) * J * S;
     for (int i = threadIdx.x; i < J * S; i += blockDim.x) tsm[i] = t[i];
     __syncthreads();
     for (int jj = threadIdx.x; jj < J; jj += blockDim.x) {  // exclusive prefix over strips
@@ -239,18 +247,18 @@ spct_status build_fused_carries(const QuantParams& q, const spct_ih& out, const 
     if (auto st = launch_status("fcarry_tiles_kernel")) return st;
     const int nb_lt = Lt16 ? static_cast<int>(ceil_div(static_cast<int64_t>(out.height) * (p.Lb / 4), 256)) : 0;
     const int nb_c = C16 ? static_cast<int>(ceil_div(static_cast<int64_t>(p.Lb) * p.Wp / 4, 256)) : 0;
-    if (nb_lt + nb_c > 0) {
-        fcarry_prefix_kernel<<<nb_lt + nb_c, 256, 0, s>>>(out.height, p.Lb, p.Wp, p.nstrips, p.nbands, nb_lt, R8, Lt16,
-                                                          C16);
+    const int nb_a = A32 ? p.Lb : 0;
+    const size_t tsm = A32 ? static_cast<size_t>(p.nbands - 1) * p.nstrips * 4 : 0;
+    if (tsm > 200 * 1024) return contract("ih_build_match: image too large for the fused carry tables");
+    if (nb_lt + nb_c + nb_a > 0) {
+        static size_t attr = 48 * 1024;
+        if (tsm > attr) {
+            cudaFuncSetAttribute(fcarry_prefix_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tsm);
+            attr = tsm;
+        }
+        fcarry_prefix_kernel<<<nb_lt + nb_c + nb_a, 256, tsm, s>>>(out.height, p.Lb, p.Wp, p.nstrips, p.nbands, nb_lt,
+                                                                   nb_c, R8, Lt16, C16, A32);
         if (auto st = launch_status("fcarry_prefix_kernel")) return st;
-    }
-    if (A32) {
-        const size_t tsm = static_cast<size_t>(p.nbands - 1) * p.nstrips * 4;
-        if (tsm > 200 * 1024) return contract("ih_build_match: image too large for the fused carry tables");
-        if (tsm > 48 * 1024)
-            cudaFuncSetAttribute(fcarry_corner_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tsm);
-        fcarry_corner_kernel<<<p.Lb, 256, tsm, s>>>(p.nstrips, p.nbands, A32);
-        if (auto st = launch_status("fcarry_corner_kernel")) return st;
     }
     fc->Lt = Lt16;
     fc->C = C16;

@@ -132,12 +132,12 @@ spct_status build_match(const spct_source* src, const spct_ih* out, const double
         const int prof = prof_begin(out->data ? "ih_sweep_match" : "sweep_match_nostore", s);
         // the group is the whole histogram: window totals over its bins are kw * kh
         const bool allb = out->bin0 == 0 && out->bins == out->nbins_total && ngroups == 1;
-        const bool g8 = q.kind == SPCT_SRC_GRAY_U8 && q.fast_u8;
+        const int sk = (q.kind == SPCT_SRC_GRAY_U8 && q.fast_u8) ? 1 : (q.kind == SPCT_SRC_BINS_U16 ? 2 : 0);
         const int nw = fused_nw(out->bins);
 #define SPCT_LAUNCH(KW)                                                                                     \
-    if (nw == 8) launch_##KW##_nw8(allb, g8, grid, s, q, pm, *out, bp, fc, f);                                  \
-    else if (nw == 4) launch_##KW##_nw4(allb, g8, grid, s, q, pm, *out, bp, fc, f);                             \
-    else launch_##KW##_nw2(allb, g8, grid, s, q, pm, *out, bp, fc, f);
+    if (nw == 8) launch_##KW##_nw8(allb, sk, grid, s, q, pm, *out, bp, fc, f);                                  \
+    else if (nw == 4) launch_##KW##_nw4(allb, sk, grid, s, q, pm, *out, bp, fc, f);                             \
+    else launch_##KW##_nw2(allb, sk, grid, s, q, pm, *out, bp, fc, f);
         if (kw == 64) {
             SPCT_LAUNCH(kw64)
         } else if (kw == 128) {

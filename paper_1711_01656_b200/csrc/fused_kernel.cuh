@@ -244,8 +244,8 @@ __device__ __forceinline__ void quarter_reduce(uint32_t (&v)[8], int q) {
 
 // ALLB (integer path only): the CTA's bin group is the whole histogram, so the window
 // total over the group's bins is kw * kh and need not be accumulated.
-// G8: 8-bit gray input with the default range (bin = v * nbins >> 8): the staging loads
-// and quantises without the generic per-kind dispatch.
+// SK (source kind of the staging loads): 1 = 8-bit gray with the default range
+// (bin = v * nbins >> 8), 2 = a uint16 BinMap (bin = v), 0 = the generic per-kind dispatch.
 // NW: warps per CTA (16 NW bins of the group): 8 for >= 65 bins, fewer for small
 // histograms so that every warp of a CTA has bins (configs 2 and 5 use 32 bins).
 template <int NW>
@@ -254,7 +254,7 @@ constexpr size_t smem_bytes_nw() {
            size_t(NW * kB) * 4 * 3 + size_t(2) * kStrip * 2 + 64 * 4;
 }
 
-template <bool STORE, bool FAST, int KWM, bool ALLB, bool G8, int NW>
+template <bool STORE, bool FAST, int KWM, bool ALLB, int SK, int NW>
 __global__ void __launch_bounds__(32 * NW, 16 / NW) sweep_match_kernel(QuantParams q, PixelMode pm, spct_ih out, int Lb,
                                                                        int Wp, int band_rows, FusedCarries fc,
                                                                        FusedParams f) {
@@ -293,10 +293,14 @@ __global__ void __launch_bounds__(32 * NW, 16 / NW) sweep_match_kernel(QuantPara
     const uint32_t kpat0 = pm.byte_mode ? 0x01010101u * static_cast<uint32_t>(k0) : 0u;
     const uint8_t* g8p = static_cast<const uint8_t*>(q.p0);
     auto raw_at = [&](int x, int y) -> uint64_t {
-        return G8 ? static_cast<uint64_t>(__ldg(g8p + static_cast<int64_t>(y) * q.pitch + x)) : pixel_raw(q, x, y);
+        if (SK == 1) return static_cast<uint64_t>(__ldg(g8p + static_cast<int64_t>(y) * q.pitch + x));
+        if (SK == 2) return static_cast<uint64_t>(__ldg(static_cast<const uint16_t*>(q.p0) + static_cast<int64_t>(y) * q.pitch + x));
+        return pixel_raw(q, x, y);
     };
     auto bin_of = [&](uint64_t r) -> int {
-        return G8 ? static_cast<int>((static_cast<uint32_t>(r) * static_cast<uint32_t>(q.nbins)) >> 8) : bin_of_raw(r, q);
+        if (SK == 1) return static_cast<int>((static_cast<uint32_t>(r) * static_cast<uint32_t>(q.nbins)) >> 8);
+        if (SK == 2) return static_cast<int>(r);
+        return bin_of_raw(r, q);
     };
 
     for (int i = tid; i < NB * kVcStride; i += NT) vc[i] = 0;
@@ -597,40 +601,44 @@ __global__ void __launch_bounds__(32 * NW, 16 / NW) sweep_match_kernel(QuantPara
 constexpr size_t kSmemBytes = smem_bytes_nw<8>();
 
 
-template <int KWM, bool ALLB, bool G8, int NW>
+template <int KWM, bool ALLB, int SK, int NW>
 void launch_variants(dim3 grid, cudaStream_t s, const QuantParams& q, const PixelMode& pm, const spct_ih& out,
                      const BuildPlan& bp, const FusedCarries& fc, const FusedParams& f) {
     constexpr int NT = 32 * NW;
     constexpr size_t SM = smem_bytes_nw<NW>();
     static bool attr_set = false;
     if (!attr_set) {
-        cudaFuncSetAttribute(sweep_match_kernel<true, true, KWM, ALLB, G8, NW>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SM);
-        cudaFuncSetAttribute(sweep_match_kernel<true, false, KWM, false, G8, NW>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SM);
-        cudaFuncSetAttribute(sweep_match_kernel<false, true, KWM, ALLB, G8, NW>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SM);
-        cudaFuncSetAttribute(sweep_match_kernel<false, false, KWM, false, G8, NW>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SM);
+        cudaFuncSetAttribute(sweep_match_kernel<true, true, KWM, ALLB, SK, NW>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SM);
+        cudaFuncSetAttribute(sweep_match_kernel<true, false, KWM, false, SK, NW>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SM);
+        cudaFuncSetAttribute(sweep_match_kernel<false, true, KWM, ALLB, SK, NW>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SM);
+        cudaFuncSetAttribute(sweep_match_kernel<false, false, KWM, false, SK, NW>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SM);
         attr_set = true;
     }
     // integer (template-crop) variant and FP64 variant: the one not selected by the
     // device-side template prep exits on entry
     if (out.data) {
-        sweep_match_kernel<true, true, KWM, ALLB, G8, NW><<<grid, NT, SM, s>>>(q, pm, out, bp.Lb, bp.Wp, bp.band_rows, fc, f);
-        sweep_match_kernel<true, false, KWM, false, G8, NW><<<grid, NT, SM, s>>>(q, pm, out, bp.Lb, bp.Wp, bp.band_rows, fc, f);
+        sweep_match_kernel<true, true, KWM, ALLB, SK, NW><<<grid, NT, SM, s>>>(q, pm, out, bp.Lb, bp.Wp, bp.band_rows, fc, f);
+        sweep_match_kernel<true, false, KWM, false, SK, NW><<<grid, NT, SM, s>>>(q, pm, out, bp.Lb, bp.Wp, bp.band_rows, fc, f);
     } else {
-        sweep_match_kernel<false, true, KWM, ALLB, G8, NW><<<grid, NT, SM, s>>>(q, pm, out, bp.Lb, bp.Wp, bp.band_rows, FusedCarries{}, f);
-        sweep_match_kernel<false, false, KWM, false, G8, NW><<<grid, NT, SM, s>>>(q, pm, out, bp.Lb, bp.Wp, bp.band_rows, FusedCarries{}, f);
+        sweep_match_kernel<false, true, KWM, ALLB, SK, NW><<<grid, NT, SM, s>>>(q, pm, out, bp.Lb, bp.Wp, bp.band_rows, FusedCarries{}, f);
+        sweep_match_kernel<false, false, KWM, false, SK, NW><<<grid, NT, SM, s>>>(q, pm, out, bp.Lb, bp.Wp, bp.band_rows, FusedCarries{}, f);
     }
 }
 
 template <int KWM, int NW>
-void launch_kw_impl(bool allb, bool g8, dim3 grid, cudaStream_t s, const QuantParams& q, const PixelMode& pm,
+void launch_kw_impl(bool allb, int sk, dim3 grid, cudaStream_t s, const QuantParams& q, const PixelMode& pm,
                     const spct_ih& out, const BuildPlan& bp, const FusedCarries& fc, const FusedParams& f) {
-    if (g8) {
-        if (allb) launch_variants<KWM, true, true, NW>(grid, s, q, pm, out, bp, fc, f);
-        else launch_variants<KWM, false, true, NW>(grid, s, q, pm, out, bp, fc, f);
+#define SPCT_SK(SKV)                                                                      \
+    if (allb) launch_variants<KWM, true, SKV, NW>(grid, s, q, pm, out, bp, fc, f);          \
+    else launch_variants<KWM, false, SKV, NW>(grid, s, q, pm, out, bp, fc, f);
+    if (sk == 1) {
+        SPCT_SK(1)
+    } else if (sk == 2) {
+        SPCT_SK(2)
     } else {
-        if (allb) launch_variants<KWM, true, false, NW>(grid, s, q, pm, out, bp, fc, f);
-        else launch_variants<KWM, false, false, NW>(grid, s, q, pm, out, bp, fc, f);
+        SPCT_SK(0)
     }
+#undef SPCT_SK
 }
 
 }  // namespace spct_fused
@@ -639,7 +647,7 @@ namespace spct_fused {
 // One translation unit per (window-width specialisation, warps per CTA), so the kernel
 // variants compile in parallel: fused_kw{64,128,0}_nw{2,4,8}.cu.
 #define SPCT_FUSED_LAUNCHER(NAME)                                                                              \
-    void NAME(bool allb, bool g8, dim3 grid, cudaStream_t s, const QuantParams& q, const PixelMode& pm,       \
+    void NAME(bool allb, int sk, dim3 grid, cudaStream_t s, const QuantParams& q, const PixelMode& pm,        \
               const spct_ih& out, const BuildPlan& bp, const FusedCarries& fc, const FusedParams& f);
 SPCT_FUSED_LAUNCHER(launch_kw64_nw8)
 SPCT_FUSED_LAUNCHER(launch_kw64_nw4)

@@ -3,8 +3,8 @@
 #include "fused_kernel.cuh"
 
 namespace spct_fused {
-void launch_kw_any_nw4(bool allb, bool g8, dim3 grid, cudaStream_t s, const QuantParams& q, const PixelMode& pm, const spct_ih& out,
+void launch_kw_any_nw4(bool allb, int sk, dim3 grid, cudaStream_t s, const QuantParams& q, const PixelMode& pm, const spct_ih& out,
           const BuildPlan& bp, const FusedCarries& fc, const FusedParams& f) {
-    launch_kw_impl<0, 4>(allb, g8, grid, s, q, pm, out, bp, fc, f);
+    launch_kw_impl<0, 4>(allb, sk, grid, s, q, pm, out, bp, fc, f);
 }
 }  // namespace spct_fused

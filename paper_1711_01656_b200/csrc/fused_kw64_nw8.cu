@@ -3,9 +3,9 @@
 #include "fused_kernel.cuh"
 
 namespace spct_fused {
-void launch_kw64_nw8(bool allb, bool g8, dim3 grid, cudaStream_t s, const QuantParams& q, const PixelMode& pm, const spct_ih& out,
+void launch_kw64_nw8(bool allb, int sk, dim3 grid, cudaStream_t s, const QuantParams& q, const PixelMode& pm, const spct_ih& out,
           const BuildPlan& bp, const FusedCarries& fc, const FusedParams& f) {
-    launch_kw_impl<64, 8>(allb, g8, grid, s, q, pm, out, bp, fc, f);
+    launch_kw_impl<64, 8>(allb, sk, grid, s, q, pm, out, bp, fc, f);
 }
 size_t smem_bytes() { return kSmemBytes; }
 }  // namespace spct_fused
@@ -18,15 +18,15 @@ int fused_ctas_per_sm(int nw) {
     int v = 0;
     cudaError_t e;
     if (nw == 8) {
-        auto k = spct_fused::sweep_match_kernel<true, true, 64, true, true, 8>;
+        auto k = spct_fused::sweep_match_kernel<true, true, 64, true, 1, 8>;
         cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)spct_fused::smem_bytes_nw<8>());
         e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&v, k, 256, spct_fused::smem_bytes_nw<8>());
     } else if (nw == 4) {
-        auto k = spct_fused::sweep_match_kernel<true, true, 64, true, true, 4>;
+        auto k = spct_fused::sweep_match_kernel<true, true, 64, true, 1, 4>;
         cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)spct_fused::smem_bytes_nw<4>());
         e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&v, k, 128, spct_fused::smem_bytes_nw<4>());
     } else {
-        auto k = spct_fused::sweep_match_kernel<true, true, 64, true, true, 2>;
+        auto k = spct_fused::sweep_match_kernel<true, true, 64, true, 1, 2>;
         cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)spct_fused::smem_bytes_nw<2>());
         e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&v, k, 64, spct_fused::smem_bytes_nw<2>());
     }
