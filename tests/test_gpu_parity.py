@@ -642,3 +642,24 @@ def test_median_background_bit_exact(P, w, h, bins, m, n, nf, nslide):
         P.motion.MedianBackgroundIH(frames[:nf], max(1, int(frames[0].max())), m, n)  # value exceeds bin count
     with pytest.raises(P.ContractError):
         P.motion.MedianBackgroundIH(frames[:2], bins, m, n)  # even window
+
+
+def test_channel_graph_replays_exactly(P):
+    """The CUDA-graph replay of a frame's five channels equals the eager calls."""
+    from paper_1711_01656_b200.channels import ChannelGraph
+
+    w, h, nbins, kw, kh = 300, 200, 32, 32, 24
+    frames = [oracle.noise_color(w, h, 40 + i) for i in range(3)]
+    srcs = P.channel_sources(*frames[0], nbins)
+    tdev = {}
+    for c, s in srcs.items():
+        qb = s if c == "orientation" else P.quantize(s, nbins)
+        crop = qb[90:90 + kh, 120:120 + kw].to(torch.int64).reshape(-1) & 0xFFFF
+        tdev[c] = (torch.bincount(crop, minlength=nbins).to(torch.float64) / crop.numel()).contiguous()
+    g = ChannelGraph(w, h, nbins, tdev, kw, kh, device="cuda")
+    for r, gg, b in frames:
+        got = {c: m.clone() for c, m in g.run(torch.from_numpy(r).cuda(), torch.from_numpy(gg).cuda(),
+                                             torch.from_numpy(b).cuda()).items()}
+        want = P.likelihood_channels(r, gg, b, nbins, None, kw, kh, 1.0, tmpl_dev=tdev)
+        for c in P.CHANNELS:
+            assert torch.equal(got[c], want[c]), c
