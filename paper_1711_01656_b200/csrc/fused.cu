@@ -114,6 +114,9 @@ spct_status build_match(const spct_source* src, const spct_ih* out, const double
         f.inv_dmax = std::frexp(f.dmax, &e) == 0.5 ? 1.0 / f.dmax : 0.0;
     }
     f.p_kind = p == 1.0 ? 1 : (p == 2.0 ? 2 : 0);
+    f.fp_kind = metric == SPCT_METRIC_MINKOWSKI ? (f.p_kind == 1 ? 0 : (f.p_kind == 2 ? 1 : 2))
+                                                : (metric == SPCT_METRIC_INTERSECTION ? 3
+                                                   : (metric == SPCT_METRIC_BHATTACHARYYA ? 4 : 5));
     f.T = static_cast<double>(T);
     f.invT = 1.0 / f.T;
     f.T_pow2 = (T & (T - 1)) == 0;

@@ -26,6 +26,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <type_traits>
 
 #include "spct_internal.h"
 #include "sweep_common.cuh"
@@ -53,6 +54,7 @@ struct FusedParams {
     double* map;                 // non-null: write the finished likelihood map (one group = every bin)
     double inv_p, dmax, inv_dmax;  // inv_dmax != 0 iff dmax is a power of two (exact product)
     int W, H;
+    int fp_kind;  // FP64 path term: 0 Minkowski p=1, 1 p=2, 2 general p, 3 intersection, 4 Bhattacharyya, 5 chi-square
 };
 
 // likelihood.cpp:220-221 (and the extension metrics), as in hist_match.cu finalize_kernel.
@@ -81,6 +83,10 @@ __device__ __forceinline__ uint32_t min_s16x2(uint32_t a, uint32_t b) {
     return r;
 }
 
+// pow for a general Minkowski order, kept out of line (inlined at every call site it
+// bloats the sweep past the instruction cache).
+static __device__ __noinline__ double pow_term(double a, double p) { return pow(a, p); }
+
 // Per-bin term of the general path (same arithmetic as hist_match.cu bin_term).
 __device__ __forceinline__ double general_term(uint32_t c, double t, const FusedParams& f) {
     const double cd = static_cast<double>(c);
@@ -90,7 +96,7 @@ __device__ __forceinline__ double general_term(uint32_t c, double t, const Fused
             const double a = fabs(__dsub_rn(q, t));
             if (f.p_kind == 1) return a;
             if (f.p_kind == 2) return __dmul_rn(a, a);
-            return pow(a, f.p);
+            return pow_term(a, f.p);
         }
         case SPCT_METRIC_INTERSECTION:
             return fmin(q, t);
@@ -111,6 +117,27 @@ __device__ __forceinline__ double general_term(uint32_t c, double t, const Fused
 // distinct bank groups, and every quad the integer path reads sits at a fixed offset
 // from the lane's strip quad.
 __device__ __forceinline__ int vcw(int w) { return w + ((w >> 3) & ~3); }
+
+// FP64 path term of one window count, specialised per metric (FusedParams::fp_kind) so
+// the hot loop carries only its own arithmetic (likelihood.cpp:215-219 and the thesis
+// metrics).  q = c * (1 / T): within an ulp of the reference's division, inside the
+// fused path's tolerance.
+template <int FK>
+__device__ __forceinline__ double fp_term(uint32_t c, double t, double invT, double p) {
+    const double q = __dmul_rn(static_cast<double>(c), invT);
+    if (FK == 0) return fabs(__dsub_rn(q, t));
+    if (FK == 1) {
+        const double a = __dsub_rn(q, t);
+        return __dmul_rn(a, a);
+    }
+    if (FK == 2) return pow_term(fabs(__dsub_rn(q, t)), p);
+    if (FK == 3) return fmin(q, t);
+    if (FK == 4) return sqrt(__dmul_rn(q, t));
+    const double den = __dadd_rn(q, t);
+    if (!(den > 0.0)) return 0.0;
+    const double df = __dsub_rn(q, t);
+    return __ddiv_rn(__dmul_rn(df, df), den);
+}
 
 // Window counts (general path), phase 1: for bin row `vrow`, the inclusive prefix G of the
 // 256 extended columns for the lane's 8 columns (u16 pairs): the halo half (a0, a1) and
@@ -533,38 +560,56 @@ __global__ void __launch_bounds__(32 * NW, 16 / NW) sweep_match_kernel(QuantPara
                     for (int j = 0; j < 8; ++j) Cw[j] += w[j];
                     Coff += off;
                 }
-            } else if (match_row) {
-                uint32_t aw[4][2], bw[4][2];
+            }
+        }
+        if constexpr (!FAST) if (match_row) {
+            // FP64 path: the window terms in a rolled loop over the bin groups, one loop per
+            // metric (a per-row switch) so the running loop stays small
+            auto rows = [&](auto fk_tag) {
+                constexpr int FK = decltype(fk_tag)::value;
+                const double invT = f.invT, pp = f.p;
+#pragma unroll 1
+                for (int g = 0; g < kB / 4; ++g) {
+                    uint32_t aw[4][2], bw[4][2];
 #pragma unroll
-                for (int i = 0; i < 4; ++i)
-                    window_prefix<KWM == 0>(vwarp + (4 * g + i) * kVcStride, gb + i * kVcWords, lane, aw[i][0], aw[i][1],
-                                            bw[i][0], bw[i][1]);
-                if (KWM == 0) __syncwarp();
+                    for (int i = 0; i < 4; ++i)
+                        window_prefix<KWM == 0>(vwarp + (4 * g + i) * kVcStride, gb + i * kVcWords, lane, aw[i][0],
+                                                aw[i][1], bw[i][0], bw[i][1]);
+                    if (KWM == 0) __syncwarp();
 #pragma unroll
-                for (int i = 0; i < 4; ++i) {
-                    const int k = 4 * g + i;
-                    uint32_t c0, c1;
-                    if (KWM == 64) {
-                        // G(e - 64): the partner lane^16's halo half (lanes < 16) or strip half (>= 16)
-                        const uint32_t r0 = __shfl_xor_sync(0xffffffffu, lane >= 16 ? aw[i][0] : bw[i][0], 16);
-                        const uint32_t r1 = __shfl_xor_sync(0xffffffffu, lane >= 16 ? aw[i][1] : bw[i][1], 16);
-                        c0 = bw[i][0] - r0;
-                        c1 = bw[i][1] - r1;
-                    } else if (KWM == 128) {
-                        c0 = bw[i][0] - aw[i][0];  // G(e - 128) is the lane's own halo half
-                        c1 = bw[i][1] - aw[i][1];
-                    } else {
-                        window_diff(gb + i * kVcWords, pw, psh, bw[i][0], bw[i][1], c0, c1);
+                    for (int i = 0; i < 4; ++i) {
+                        const int k = 4 * g + i;
+                        uint32_t c0, c1;
+                        if (KWM == 64) {
+                            // G(e - 64): the partner lane^16's halo half (lanes < 16) or strip half (>= 16)
+                            const uint32_t r0 = __shfl_xor_sync(0xffffffffu, lane >= 16 ? aw[i][0] : bw[i][0], 16);
+                            const uint32_t r1 = __shfl_xor_sync(0xffffffffu, lane >= 16 ? aw[i][1] : bw[i][1], 16);
+                            c0 = bw[i][0] - r0;
+                            c1 = bw[i][1] - r1;
+                        } else if (KWM == 128) {
+                            c0 = bw[i][0] - aw[i][0];  // G(e - 128) is the lane's own halo half
+                            c1 = bw[i][1] - aw[i][1];
+                        } else {
+                            window_diff(gb + i * kVcWords, pw, psh, bw[i][0], bw[i][1], c0, c1);
+                        }
+                        if (k < k_live) {
+                            const double t = __ldg(f.tmpl + k0 + k);
+                            acc[0] = __dadd_rn(acc[0], fp_term<FK>(c0 & 0xFFFFu, t, invT, pp));
+                            acc[1] = __dadd_rn(acc[1], fp_term<FK>(c0 >> 16, t, invT, pp));
+                            acc[2] = __dadd_rn(acc[2], fp_term<FK>(c1 & 0xFFFFu, t, invT, pp));
+                            acc[3] = __dadd_rn(acc[3], fp_term<FK>(c1 >> 16, t, invT, pp));
+                        }
                     }
-                    if (k < k_live) {
-                        const double t = __ldg(f.tmpl + k0 + k);
-                        acc[0] = __dadd_rn(acc[0], general_term(c0 & 0xFFFFu, t, f));
-                        acc[1] = __dadd_rn(acc[1], general_term(c0 >> 16, t, f));
-                        acc[2] = __dadd_rn(acc[2], general_term(c1 & 0xFFFFu, t, f));
-                        acc[3] = __dadd_rn(acc[3], general_term(c1 >> 16, t, f));
-                    }
+                    if (KWM == 0) __syncwarp();
                 }
-                if (KWM == 0) __syncwarp();
+            };
+            switch (f.fp_kind) {
+                case 0: rows(std::integral_constant<int, 0>{}); break;
+                case 1: rows(std::integral_constant<int, 1>{}); break;
+                case 2: rows(std::integral_constant<int, 2>{}); break;
+                case 3: rows(std::integral_constant<int, 3>{}); break;
+                case 4: rows(std::integral_constant<int, 4>{}); break;
+                default: rows(std::integral_constant<int, 5>{}); break;
             }
         }
         if (match_row) {

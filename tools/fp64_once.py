@@ -1,0 +1,11 @@
+import os, sys
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np, torch, bench, paper_1711_01656_b200 as P
+dev = torch.device("cuda", 0)
+frame = torch.from_numpy(bench.make_frame(4096, 4096)).to(dev)
+t = P.IntegralHistogramTensor(4096, 4096, 128, device=dev)
+lmap = torch.empty((4096, 4096), dtype=torch.float64, device=dev)
+td = torch.from_numpy(bench.template_hist(bench.make_frame(4096, 4096), 128, 64, 64)).to(dev)
+for _ in range(2):
+    P.build_and_match_map(frame, 128, None, 64, 64, 2.0, 0, out=t, lmap=lmap, tmpl_dev=td)
+torch.cuda.synchronize()
