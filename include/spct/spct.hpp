@@ -157,6 +157,10 @@ inline constexpr std::uint64_t kDefaultMemoryBudget = 2ull << 30;
 
 IntegralHistogramTensor build_integral_histogram(const BinMap& bins, const ScanSchedule& schedule = {},
                                                  std::uint64_t memory_budget = kDefaultMemoryBudget);
+// integral.hpp:102-104: each pixel contributes its (16.16 fixed-point) weight instead of 1.
+IntegralHistogramTensor build_weighted_tensor(const BinMap& bins, const std::vector<std::uint64_t>& weights,
+                                              const ScanSchedule& schedule = {},
+                                              std::uint64_t memory_budget = kDefaultMemoryBudget);
 std::vector<std::uint64_t> region_histogram(const IntegralHistogramTensor& t, const Rect& r);
 std::uint64_t region_count(const IntegralHistogramTensor& t, int bin, const Rect& r);
 

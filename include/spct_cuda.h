@@ -187,6 +187,9 @@ spct_status spct_cu_wih_layout(int width, int height, int bins, int64_t* row_pit
 spct_status spct_cu_wih_build(const uint16_t* bins, int64_t pitch, const uint64_t* weights, int field_dir, int kw,
                               int kh, const spct_wih* out, void* stream);
 spct_status spct_cu_wih_export_u64(const spct_wih* t, int k0, int k1, uint64_t* dst, void* stream);
+/* region_histogram (integral.cpp:561-577) of a weighted tensor: rects (dev) n x {x, y, w, h}
+ * (checked by the caller), out (dev) n x bins uint64. */
+spct_status spct_cu_wih_region_counts(const spct_wih* t, const int32_t* rects, int n, uint64_t* out, void* stream);
 /* swlh_query_fixed (swih.cpp:128-164) at n centres (host array of (cx, cy)) over the four
  * quadrant tensors set4[NW, NE, SW, SE]; out (dev) n x bins int64, 16.16.  Synchronises. */
 spct_status spct_cu_swlh_query(const spct_wih* set4, int kw, int kh, const int32_t* centres, int n, int64_t* out,

@@ -88,6 +88,7 @@ SIGNATURES = {
     "spct_cu_wih_layout": (_i, [_i, _i, _i, C.POINTER(_i64), C.POINTER(_i64), C.POINTER(_u64)]),
     "spct_cu_wih_build": (_i, [_vp, _i64, _vp, _i, _i, _i, C.POINTER(spct_wih), _vp]),
     "spct_cu_wih_export_u64": (_i, [C.POINTER(spct_wih), _i, _i, _vp, _vp]),
+    "spct_cu_wih_region_counts": (_i, [C.POINTER(spct_wih), _vp, _i, _vp, _vp]),
     "spct_cu_swlh_query": (_i, [C.POINTER(spct_wih), _i, _i, C.POINTER(C.c_int32), _i, _vp, _vp]),
     "spct_cu_swlh_brute": (_i, [_vp, _i64, _i, _i, _i, _i, _i, C.POINTER(C.c_int32), _i, _vp, _vp]),
     "spct_cu_swlh_map": (_i, [C.POINTER(spct_wih), _i, _i, _vp, _vp, _vp]),

@@ -6,13 +6,16 @@
 // Device failures throw spct::device_error.
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <mutex>
 
 #include <cuda_runtime.h>
 
+#include "spct/motion.hpp"
 #include "spct/spct.hpp"
+#include "spct/swih.hpp"
 #include "spct_cuda.h"
 
 namespace spct {
@@ -70,6 +73,9 @@ namespace detail {
 struct DeviceTensor {
     spct_ih desc{};
     std::unique_ptr<DevBuf> mem;
+    // Weighted tensors (build_weighted_tensor, SWIH): uint64 cells in `wdesc` instead.
+    bool weighted = false;
+    spct_wih wdesc{};
     // The frame the tensor was built from (device copy): hist_distance_map recomputes
     // window counts from it (1 B/px) instead of re-reading b*H*W*4 tensor bytes.
     spct_source src{};
@@ -78,11 +84,29 @@ struct DeviceTensor {
 
 std::size_t HostMirror::size() const {
     if (!dev) return host_.size();
+    if (dev->weighted)
+        return std::size_t(dev->wdesc.bins) * std::size_t(dev->wdesc.height + 1) * std::size_t(dev->wdesc.width + 1);
     return std::size_t(dev->desc.bins) * std::size_t(dev->desc.height + 1) * std::size_t(dev->desc.width + 1);
 }
 
 void HostMirror::fill() const {
     if (valid_ || !dev) return;
+    if (dev->weighted) {
+        const spct_wih& w = dev->wdesc;
+        const std::size_t plane = std::size_t(w.height + 1) * (w.width + 1);
+        host_.resize(plane * w.bins);
+        const std::size_t per = std::max<std::size_t>(1, (std::size_t(256) << 20) / (plane * 8));
+        DevBuf stage(std::min<std::size_t>(per, w.bins) * plane * 8);
+        for (int k0 = 0; k0 < w.bins; k0 += int(per)) {
+            const int k1 = std::min<int>(w.bins, k0 + int(per));
+            check(spct_cu_wih_export_u64(&w, k0, k1, stage.as<std::uint64_t>(), nullptr));
+            cuda(cudaMemcpy(host_.data() + std::size_t(k0) * plane, stage.p, std::size_t(k1 - k0) * plane * 8,
+                            cudaMemcpyDeviceToHost),
+                 "D2H");
+        }
+        valid_ = true;
+        return;
+    }
     const spct_ih& d = dev->desc;
     const std::size_t plane = std::size_t(d.height + 1) * (d.width + 1);
     host_.resize(plane * d.bins);
@@ -261,6 +285,7 @@ IntegralHistogramTensor build_integral_histogram(const BinMap& bins, const ScanS
 namespace {
 const spct_ih& desc_of(const IntegralHistogramTensor& t) {
     require(t.data.dev != nullptr, "tensor has no device storage");
+    require(!t.data.dev->weighted, "operation needs a count tensor (this one is weighted)");
     return t.data.dev->desc;
 }
 }  // namespace
@@ -268,6 +293,16 @@ const spct_ih& desc_of(const IntegralHistogramTensor& t) {
 std::vector<std::uint64_t> region_histogram(const IntegralHistogramTensor& t, const Rect& r) {
     require(r.w >= 0 && r.h >= 0, "region_histogram: negative extent");       // integral.cpp:562
     require(r.inside(t.width, t.height), "region_histogram: rect outside image");  // :563
+    if (t.data.dev && t.data.dev->weighted) {
+        const spct_wih& w = t.data.dev->wdesc;
+        DevBuf rect(16), out(std::size_t(t.bins) * 8);
+        const std::int32_t rr[4] = {r.x, r.y, r.w, r.h};
+        cuda(cudaMemcpy(rect.p, rr, 16, cudaMemcpyHostToDevice), "H2D");
+        check(spct_cu_wih_region_counts(&w, rect.as<std::int32_t>(), 1, out.as<std::uint64_t>(), nullptr));
+        std::vector<std::uint64_t> h(t.bins);
+        cuda(cudaMemcpy(h.data(), out.p, h.size() * 8, cudaMemcpyDeviceToHost), "D2H");
+        return h;
+    }
     const spct_ih& d = desc_of(t);
     DevBuf rect(16), out(std::size_t(t.bins) * 4);
     const std::int32_t rr[4] = {r.x, r.y, r.w, r.h};
@@ -286,6 +321,19 @@ std::uint64_t region_count(const IntegralHistogramTensor& t, int bin, const Rect
 
 // IHT1 wire format (integral.cpp:619-659): streamed from / to HBM by the C-ABI.
 void dump_tensor(const IntegralHistogramTensor& t, const std::string& path) {
+    if (t.data.dev && t.data.dev->weighted) {  // uint64 cells: the file is the host mirror itself
+        std::FILE* f = std::fopen(path.c_str(), "wb");
+        if (!f) throw io_error("cannot write tensor: " + path);  // integral.cpp:621
+        unsigned char hdr[20] = {'I', 'H', 'T', '1'};
+        const std::uint32_t v[4] = {std::uint32_t(t.bins), std::uint32_t(t.height), std::uint32_t(t.width), 8u};
+        for (int i = 0; i < 4; ++i)
+            for (int b = 0; b < 4; ++b) hdr[4 + 4 * i + b] = static_cast<unsigned char>(v[i] >> (8 * b));
+        bool ok = std::fwrite(hdr, 1, 20, f) == 20;
+        ok = ok && std::fwrite(t.data.data(), 8, t.data.size(), f) == t.data.size();
+        ok = (std::fclose(f) == 0) && ok;
+        if (!ok) throw io_error("write failed: " + path);  // :631
+        return;
+    }
     check(spct_cu_ih_dump(&desc_of(t), path.c_str(), 8, nullptr));
 }
 
@@ -492,6 +540,339 @@ LikelihoodMap likelihood_from_frame(const GrayImage& img, int bins, const std::v
         tensor_out->data.dev = std::move(dt);
     }
     return out;
+}
+
+// ---------------------------------------------------------------- weighted tensors (integral.hpp:102-104)
+namespace {
+
+// A device weighted tensor over a device bin map: explicit weights (dev uint64, 16.16) or
+// the quadrant ramp field `dir` of a kw x kh kernel (spct_cu_wih_build).
+IntegralHistogramTensor make_weighted(const std::uint16_t* dbins, int w, int h, int bins, const std::uint64_t* dweights,
+                                      int dir, int kw, int kh) {
+    auto dt = std::make_shared<detail::DeviceTensor>();
+    dt->weighted = true;
+    spct_wih& d = dt->wdesc;
+    std::uint64_t bytes = 0;
+    check(spct_cu_wih_layout(w, h, bins, &d.row_pitch, &d.plane_pitch, &bytes));
+    dt->mem = std::make_unique<DevBuf>(bytes);
+    d.data = dt->mem->as<std::uint64_t>();
+    d.bins = bins;
+    d.height = h;
+    d.width = w;
+    check(spct_cu_wih_build(dbins, w, dweights, dir, kw, kh, &d, nullptr));
+    cuda(cudaDeviceSynchronize(), "build_weighted_tensor");
+    IntegralHistogramTensor t;
+    t.bins = bins;
+    t.height = h;
+    t.width = w;
+    t.data.dev = std::move(dt);
+    return t;
+}
+
+const spct_wih& wdesc_of(const IntegralHistogramTensor& t) {
+    require(t.data.dev != nullptr && t.data.dev->weighted, "swlh_query: quadrant tensors must be weighted tensors");
+    return t.data.dev->wdesc;
+}
+
+}  // namespace
+
+IntegralHistogramTensor build_weighted_tensor(const BinMap& bins, const std::vector<std::uint64_t>& weights,
+                                              const ScanSchedule& schedule, std::uint64_t memory_budget) {
+    require(weights.size() == bins.data.size(), "build_weighted_tensor: weight size mismatch");  // integral.cpp:557
+    validate_build(bins, schedule, memory_budget);
+    DevBuf db(bins.data.size() * 2), dw(weights.size() * 8);
+    upload(db, bins.data);
+    upload(dw, weights);
+    return make_weighted(db.as<std::uint16_t>(), bins.width, bins.height, bins.bins, dw.as<std::uint64_t>(), -1, 1, 1);
+}
+
+// ---------------------------------------------------------------- SWIH (swih.hpp)
+const char* to_string(Quadrant q) {
+    static const char* names[] = {"NW", "NE", "SW", "SE"};
+    const int i = static_cast<int>(q);
+    return (i >= 0 && i < 4) ? names[i] : "?";
+}
+
+KernelExtents kernel_extents(const KernelSpec& spec) {  // swih.cpp:19-27
+    require(spec.kw >= 1 && spec.kh >= 1, "kernel extents must be >= 1");
+    const int sxl = spec.kw / 2, syt = spec.kh / 2;
+    return KernelExtents{sxl, spec.kw - sxl, syt, spec.kh - syt, sxl + syt + 1};
+}
+
+std::uint64_t quantize_weight(double w) {  // swih.cpp:29-32
+    require(std::isfinite(w) && w >= 0.0, "weights must be finite and nonnegative");
+    return static_cast<std::uint64_t>(std::llround(w * kWeightScale));
+}
+
+namespace {
+// Slope 1 on an axis the kernel spans with >= 3 cells, else 0 (swih.cpp:40-43).
+int ramp_slope(int k) { return k >= 3 ? 1 : 0; }
+}  // namespace
+
+std::array<WeightField, 4> quadrant_weight_fields(int img_w, int img_h, const KernelSpec& spec) {
+    require(img_w > 0 && img_h > 0, "quadrant_weight_fields: empty image");  // swih.cpp:86
+    kernel_extents(spec);
+    const int sx = ramp_slope(spec.kw), sy = ramp_slope(spec.kh);
+    std::array<WeightField, 4> out;
+    for (int d = 0; d < 4; ++d) {
+        WeightField& f = out[d];
+        f.width = img_w;
+        f.height = img_h;
+        f.dir = static_cast<Quadrant>(d);
+        f.w.resize(std::size_t(img_w) * img_h);
+        // the field falls by one per step away from its anchor corner (swih.cpp:45-53):
+        // NW / SW count x from the left, NE / SE from the right; NW / NE y from the top
+        const bool from_left = f.dir == Quadrant::NW || f.dir == Quadrant::SW;
+        const bool from_top = f.dir == Quadrant::NW || f.dir == Quadrant::NE;
+        for (int y = 0; y < img_h; ++y)
+            for (int x = 0; x < img_w; ++x) {
+                const int ax = from_left ? x : img_w - 1 - x, ay = from_top ? y : img_h - 1 - y;
+                f.w[std::size_t(y) * img_w + x] = 1.0 + sx * ax + sy * ay;
+            }
+    }
+    return out;
+}
+
+IntegralHistogramTensor build_weighted_ih(const BinMap& bins, const WeightField& field, const ScanSchedule& schedule) {
+    require(field.width == bins.width && field.height == bins.height,
+            "build_weighted_ih: field/bin map size mismatch");  // swih.cpp:104-105
+    std::vector<std::uint64_t> wq(field.w.size());
+    std::transform(field.w.begin(), field.w.end(), wq.begin(), quantize_weight);
+    return build_weighted_tensor(bins, wq, schedule);
+}
+
+// The four ramp tensors are built on the device straight from the bin map (the field is
+// generated in the build kernel), one upload of the map for all four.
+WeightedQuadrantSet build_quadrant_set(const BinMap& bins, const KernelSpec& spec, const ScanSchedule& schedule) {
+    require(bins.width > 0 && bins.height > 0, "quadrant_weight_fields: empty image");
+    kernel_extents(spec);
+    validate_build(bins, schedule, kDefaultMemoryBudget);
+    WeightedQuadrantSet set;
+    set.kernel = spec;
+    set.sx = ramp_slope(spec.kw);
+    set.sy = ramp_slope(spec.kh);
+    set.pair_sum = 2 + std::int64_t(set.sx) * (bins.width - 1) + std::int64_t(set.sy) * (bins.height - 1);
+    DevBuf db(bins.data.size() * 2);
+    upload(db, bins.data);
+    for (int d = 0; d < 4; ++d)
+        set.tensors[d] =
+            make_weighted(db.as<std::uint16_t>(), bins.width, bins.height, bins.bins, nullptr, d, spec.kw, spec.kh);
+    return set;
+}
+
+std::vector<std::int64_t> swlh_query_fixed(const WeightedQuadrantSet& set, int cx, int cy, const KernelSpec& spec) {
+    require(spec == set.kernel, "swlh_query: kernel spec differs from the built set");  // swih.cpp:130
+    kernel_extents(spec);
+    const spct_wih descs[4] = {wdesc_of(set.tensors[0]), wdesc_of(set.tensors[1]), wdesc_of(set.tensors[2]),
+                               wdesc_of(set.tensors[3])};
+    const std::int32_t c[2] = {cx, cy};
+    const int bins = set.tensors[0].bins;
+    DevBuf out(std::size_t(bins) * 8);
+    check(spct_cu_swlh_query(descs, spec.kw, spec.kh, c, 1, out.as<std::int64_t>(), nullptr));
+    std::vector<std::int64_t> h(bins);
+    cuda(cudaMemcpy(h.data(), out.p, h.size() * 8, cudaMemcpyDeviceToHost), "D2H");
+    return h;
+}
+
+namespace {
+// Unit-mass normalisation with the reference's extended-precision total (swih.cpp:182-192).
+std::vector<double> unit_mass(const std::vector<std::int64_t>& fx) {
+    long double total = 0;
+    for (std::int64_t v : fx) total += v;
+    std::vector<double> out(fx.size(), 0.0);
+    if (total > 0)
+        for (std::size_t k = 0; k < fx.size(); ++k) out[k] = static_cast<double>(fx[k] / total);
+    return out;
+}
+}  // namespace
+
+std::vector<double> swlh_query(const WeightedQuadrantSet& set, int cx, int cy, const KernelSpec& spec) {
+    return unit_mass(swlh_query_fixed(set, cx, cy, spec));
+}
+
+std::vector<std::int64_t> brute_force_swlh_fixed(const BinMap& bins, int cx, int cy, const KernelSpec& spec) {
+    kernel_extents(spec);
+    require(bins.data.empty() || *std::max_element(bins.data.begin(), bins.data.end()) < bins.bins,
+            "build: bin index out of range");
+    DevBuf db(bins.data.size() * 2), out(std::size_t(std::max(bins.bins, 1)) * 8);
+    upload(db, bins.data);
+    const std::int32_t c[2] = {cx, cy};
+    check(spct_cu_swlh_brute(db.as<std::uint16_t>(), bins.width, bins.width, bins.height, bins.bins, spec.kw, spec.kh, c,
+                             1, out.as<std::int64_t>(), nullptr));
+    std::vector<std::int64_t> h(bins.bins);
+    cuda(cudaMemcpy(h.data(), out.p, h.size() * 8, cudaMemcpyDeviceToHost), "D2H");
+    return h;
+}
+
+std::vector<double> brute_force_swlh(const BinMap& bins, int cx, int cy, const KernelSpec& spec) {
+    return unit_mass(brute_force_swlh_fixed(bins, cx, cy, spec));
+}
+
+// Nested-rectangle ("wedding cake") approximation over a plain tensor (swih.cpp:200-262):
+// ring l between rect l and rect l+1 gets the exact mean pyramid weight over the ring,
+// rounded half up in 16.16.  All rect histograms come from one device query.
+std::vector<double> wedding_cake_swlh(const IntegralHistogramTensor& plain, int cx, int cy, const KernelSpec& spec,
+                                      int layers) {
+    require(layers >= 1, "wedding_cake_swlh: layers must be >= 1");
+    const KernelExtents e = kernel_extents(spec);
+    require(cx - e.sxl >= 0 && cy - e.syt >= 0 && cx + e.sxr <= plain.width && cy + e.syb <= plain.height,
+            "kernel window must lie inside the image");
+    struct Ext {
+        std::int64_t xl, xr, yt, yb;
+        std::int64_t area() const { return (xl + xr) * (yt + yb); }
+        // sum over dx in [-xl, xr), dy in [-yt, yb) of (c - |dx| - |dy|)
+        std::int64_t mass(std::int64_t c) const {
+            const std::int64_t nx = xl + xr, ny = yt + yb;
+            const std::int64_t ax = xl * (xl + 1) / 2 + (xr - 1) * xr / 2, ay = yt * (yt + 1) / 2 + (yb - 1) * yb / 2;
+            return c * nx * ny - ax * ny - ay * nx;
+        }
+    };
+    std::vector<Ext> ext(layers + 1, Ext{0, 0, 0, 0});  // ext[layers]: the empty rect
+    std::vector<std::int32_t> rects;
+    for (int l = 0; l < layers; ++l) {
+        const double f = static_cast<double>(layers - l) / layers;
+        ext[l] = Ext{std::lround(e.sxl * f), std::max<long>(1, std::lround(e.sxr * f)), std::lround(e.syt * f),
+                     std::max<long>(1, std::lround(e.syb * f))};
+        rects.insert(rects.end(), {std::int32_t(cx - ext[l].xl), std::int32_t(cy - ext[l].yt),
+                                   std::int32_t(ext[l].xl + ext[l].xr), std::int32_t(ext[l].yt + ext[l].yb)});
+    }
+    const spct_ih& d = desc_of(plain);
+    const int bins = plain.bins;
+    DevBuf drect(rects.size() * 4), dout(std::size_t(layers) * bins * 4);
+    upload(drect, rects);
+    check(spct_cu_region_counts(&d, drect.as<std::int32_t>(), layers, dout.as<std::uint32_t>(), nullptr));
+    std::vector<std::uint32_t> hist(std::size_t(layers) * bins);
+    cuda(cudaMemcpy(hist.data(), dout.p, hist.size() * 4, cudaMemcpyDeviceToHost), "D2H");
+    std::vector<std::int64_t> acc(bins, 0);
+    for (int l = 0; l < layers; ++l) {
+        const std::int64_t d_area = ext[l].area() - ext[l + 1].area();
+        if (d_area <= 0) continue;
+        const std::int64_t d_mass = ext[l].mass(e.c) - ext[l + 1].mass(e.c);
+        const std::int64_t wfix = (2 * d_mass * kWeightScale + d_area) / (2 * d_area);
+        for (int k = 0; k < bins; ++k) {
+            const std::uint64_t outer = hist[std::size_t(l) * bins + k];
+            const std::uint64_t inner = l + 1 < layers ? hist[std::size_t(l + 1) * bins + k] : 0;
+            acc[k] += static_cast<std::int64_t>(outer - inner) * wfix;
+        }
+    }
+    return unit_mass(acc);
+}
+
+double histogram_mse(const std::vector<double>& a, const std::vector<double>& b) {
+    require(a.size() == b.size() && !a.empty(), "histogram_mse: size mismatch");
+    double acc = 0;
+    for (std::size_t i = 0; i < a.size(); ++i) acc += (a[i] - b[i]) * (a[i] - b[i]);
+    return acc / static_cast<double>(a.size());
+}
+
+// ---------------------------------------------------------------- joint-IH median (motion.hpp)
+void FrameWindow::validate() const {  // motion.cpp:12-19
+    require(!frames.empty(), "FrameWindow: empty window");
+    require(frames.size() % 2 == 1, "FrameWindow: window length must be odd");
+    const int w = frames[0].width, h = frames[0].height;
+    require(w > 0 && h > 0, "FrameWindow: empty frames");
+    for (const auto& f : frames) require(f.width == w && f.height == h, "FrameWindow: frame dimensions differ");
+}
+
+struct MedianBackgroundIH::State {
+    spct_ih joint{};
+    std::unique_ptr<DevBuf> mem, frame, ws;
+    std::size_t ws_bytes = 0;
+};
+
+MedianBackgroundIH::~MedianBackgroundIH() = default;
+MedianBackgroundIH::MedianBackgroundIH(MedianBackgroundIH&&) noexcept = default;
+MedianBackgroundIH& MedianBackgroundIH::operator=(MedianBackgroundIH&&) noexcept = default;
+
+MedianBackgroundIH::MedianBackgroundIH(const FrameWindow& window, int bins, int m, int n)
+    : bins_(bins), m_(m), n_(n) {
+    window.validate();
+    require(bins >= 1 && bins <= 256, "median_background_ih: bins must be in [1,256]");  // motion.cpp:38
+    require(m >= 1 && n >= 1 && m % 2 == 1 && n % 2 == 1, "median_background_ih: kernel sides must be odd and positive");
+    width_ = window.frames[0].width;
+    height_ = window.frames[0].height;
+    require(m <= width_ && n <= height_, "median_background_ih: kernel exceeds image");
+    // the joint tensor is uint32: exact while every window count fits
+    require(std::uint64_t(window.frames.size()) * width_ * height_ < (std::uint64_t(1) << 32),
+            "median_background_ih: frames * H * W must be < 2^32");
+    st_ = std::make_unique<State>();
+    spct_ih& J = st_->joint;
+    std::uint64_t bytes = 0;
+    check(spct_cu_ih_layout(width_, height_, bins_, &J.row_pitch, &J.plane_pitch, &bytes));
+    st_->mem = std::make_unique<DevBuf>(bytes);
+    cuda(cudaMemset(st_->mem->p, 0, bytes), "memset");
+    J.data = st_->mem->as<std::uint32_t>();
+    J.bins = bins_;
+    J.bin0 = 0;
+    J.nbins_total = bins_;
+    J.height = height_;
+    J.width = width_;
+    st_->frame = std::make_unique<DevBuf>(std::size_t(width_) * height_ * 2);
+    spct_source s{};
+    s.kind = SPCT_SRC_BINS_U16;
+    s.width = width_;
+    s.height = height_;
+    s.nbins = bins_;
+    check(spct_cu_ih_build_workspace(&s, 0, bins_, &st_->ws_bytes));
+    st_->ws = std::make_unique<DevBuf>(st_->ws_bytes);
+    for (const auto& f : window.frames) {
+        add_frame(f, +1);
+        frames_.push_back(f);
+    }
+}
+
+void MedianBackgroundIH::add_frame(const GrayImage& f, int sign) {  // motion.cpp:51-60
+    for (auto v : f.data) require(v < bins_, "median_background_ih: frame value exceeds bin count");
+    const std::vector<std::uint16_t> b(f.data.begin(), f.data.end());  // the frame's values are its bins
+    upload(*st_->frame, b);
+    spct_source s{};
+    s.kind = SPCT_SRC_BINS_U16;
+    s.plane[0] = st_->frame->p;
+    s.pitch = width_;
+    s.width = width_;
+    s.height = height_;
+    s.nbins = bins_;
+    check(spct_cu_ih_accumulate(&s, &st_->joint, sign, st_->ws->p, st_->ws_bytes, nullptr));
+    cuda(cudaDeviceSynchronize(), "median_background_ih");  // the staging buffer is reused
+}
+
+void MedianBackgroundIH::slide(const GrayImage& next) {  // motion.cpp:62-69
+    require(next.width == width_ && next.height == height_, "median_background_ih: slide frame dimensions differ");
+    add_frame(next, +1);
+    add_frame(frames_.front(), -1);
+    frames_.pop_front();
+    frames_.push_back(next);
+}
+
+GrayImage MedianBackgroundIH::background() const {  // motion.cpp:71-99
+    DevBuf out(std::size_t(width_) * height_);
+    check(spct_cu_median_background(&st_->joint, static_cast<int>(frames_.size()), m_, n_, out.as<std::uint8_t>(),
+                                    width_, nullptr));
+    GrayImage g(width_, height_);
+    cuda(cudaMemcpy(g.data.data(), out.p, g.data.size(), cudaMemcpyDeviceToHost), "D2H");
+    return g;
+}
+
+GrayImage median_background_ih(const FrameWindow& window, int bins, int m, int n) {
+    return MedianBackgroundIH(window, bins, m, n).background();
+}
+
+GrayImage median_background_sort(const FrameWindow& window) {  // motion.cpp:105-118
+    window.validate();
+    const int w = window.frames[0].width, h = window.frames[0].height;
+    const std::size_t px = std::size_t(w) * h, nf = window.frames.size();
+    DevBuf stack(px * (nf + 1));
+    std::vector<const std::uint8_t*> ptrs(nf);
+    for (std::size_t f = 0; f < nf; ++f) {
+        ptrs[f] = stack.as<std::uint8_t>() + f * px;
+        cuda(cudaMemcpy(stack.as<std::uint8_t>() + f * px, window.frames[f].data.data(), px, cudaMemcpyHostToDevice),
+             "H2D");
+    }
+    std::uint8_t* out = stack.as<std::uint8_t>() + nf * px;
+    check(spct_cu_median_sort(ptrs.data(), static_cast<int>(nf), w, h, w, out, w, nullptr));
+    GrayImage g(w, h);
+    cuda(cudaMemcpy(g.data.data(), out, px, cudaMemcpyDeviceToHost), "D2H");
+    return g;
 }
 
 }  // namespace spct

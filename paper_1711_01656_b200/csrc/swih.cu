@@ -113,6 +113,14 @@ __device__ __forceinline__ uint64_t region(const spct_wih& t, int k, int x, int 
     return H(t, k, y + h, x + w) - H(t, k, y, x + w) - H(t, k, y + h, x) + H(t, k, y, x);
 }
 
+__global__ void wih_region_kernel(spct_wih t, const int32_t* __restrict__ rects, int n, uint64_t* __restrict__ out) {
+    const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;  // (rect, bin)
+    if (i >= static_cast<int64_t>(n) * t.bins) return;
+    const int r = static_cast<int>(i / t.bins), k = static_cast<int>(i % t.bins);
+    const int32_t* q = rects + 4 * r;
+    out[i] = region(t, k, q[0], q[1], q[2], q[3]);
+}
+
 struct QuadSet {
     spct_wih t[4];  // NW, NE, SW, SE
     int kw, kh, sx, sy;
@@ -268,6 +276,16 @@ extern "C" spct_status spct_cu_wih_export_u64(const spct_wih* t, int k0, int k1,
     const int64_t n = static_cast<int64_t>(k1 - k0) * (t->height + 1) * (t->width + 1);
     wih_export_kernel<<<blocks_for(std::min<int64_t>(n, 148 * 2048), 256), 256, 0, as_stream(stream)>>>(*t, k0, k1, dst);
     return launch_status("wih_export");
+}
+
+extern "C" spct_status spct_cu_wih_region_counts(const spct_wih* t, const int32_t* rects, int n, uint64_t* out,
+                                                 void* stream) {
+    if (auto st = check_wih(t)) return st;
+    if (n < 0 || (n > 0 && !(rects && out))) return contract("region_histogram: bad arguments");
+    if (n == 0) return SPCT_OK;
+    const int64_t m = static_cast<int64_t>(n) * t->bins;
+    wih_region_kernel<<<blocks_for(m, 256), 256, 0, as_stream(stream)>>>(*t, rects, n, out);
+    return launch_status("wih_region_kernel");
 }
 
 extern "C" spct_status spct_cu_swlh_query(const spct_wih* set4, int kw, int kh, const int32_t* centres_host, int n,

@@ -5,6 +5,7 @@
 // on a GPU box; exits non-zero on the first failed check.
 #include <cmath>
 #include <cstdio>
+#include <algorithm>
 #include <cstdlib>
 #include <random>
 #include <string>
@@ -13,6 +14,8 @@
 #include "spct/imagecore.hpp"
 #include "spct/integral.hpp"
 #include "spct/likelihood.hpp"
+#include "spct/motion.hpp"
+#include "spct/swih.hpp"
 
 using namespace spct;
 
@@ -232,6 +235,114 @@ int main() {
         CHECK(e.padded_bytes == 32ull * 513 * 513 * 8 && e.raw_bytes == 64ull * 1024 * 1024);
         CHECK(estimate_memory(100, 100, 0, 8).degenerate);
         CHECK_THROWS_AS(estimate_memory(-1, 4, 4, 4), contract_error);
+    }
+    {  // weighted IH vs direct accumulation (test_swih.cpp:78-96)
+        BinMap bm = random_binmap(21, 14, 6, 55);
+        auto fields = quadrant_weight_fields(21, 14, {5, 7});
+        for (const auto& f : fields) {
+            auto t = build_weighted_ih(bm, f);
+            std::mt19937 rng(2);
+            for (int trial = 0; trial < 40; ++trial) {
+                int x1 = static_cast<int>(rng() % 21), y1 = static_cast<int>(rng() % 14);
+                Rect r{x1, y1, static_cast<int>(rng() % (21 - x1 + 1)), static_cast<int>(rng() % (14 - y1 + 1))};
+                std::vector<std::uint64_t> want(6, 0);
+                for (int y = r.y; y < r.bottom(); ++y)
+                    for (int x = r.x; x < r.right(); ++x) want[bm.at(x, y)] += quantize_weight(f.at(x, y));
+                CHECK(region_histogram(t, r) == want);
+            }
+        }
+        CHECK_THROWS_AS(build_weighted_tensor(bm, std::vector<std::uint64_t>(5, 1)), contract_error);
+    }
+    {  // swlh query bit-exact against the brute force (test_swih.cpp:98-114)
+        std::mt19937 rng(606);
+        const KernelSpec kernels[] = {{1, 1}, {2, 2}, {3, 3}, {4, 4}, {5, 3}, {1, 7}, {8, 1}, {9, 9}, {6, 10}};
+        for (const auto& spec : kernels) {
+            BinMap bm = random_binmap(40, 36, 8, rng());
+            auto set = build_quadrant_set(bm, spec);
+            KernelExtents e = kernel_extents(spec);
+            for (int trial = 0; trial < 25; ++trial) {
+                int cx = e.sxl + static_cast<int>(rng() % (40 - spec.kw + 1));
+                int cy = e.syt + static_cast<int>(rng() % (36 - spec.kh + 1));
+                CHECK(swlh_query_fixed(set, cx, cy, spec) == brute_force_swlh_fixed(bm, cx, cy, spec));
+            }
+        }
+        BinMap u(12, 12, 4);
+        for (auto& v : u.data) v = 2;
+        auto h = swlh_query(build_quadrant_set(u, {5, 5}), 6, 6, {5, 5});
+        CHECK(h[2] == 1.0 && h[0] == 0.0);
+        BinMap bm = random_binmap(10, 10, 4, 5);
+        auto set = build_quadrant_set(bm, {5, 5});
+        CHECK_THROWS_AS(swlh_query(set, 0, 5, {5, 5}), contract_error);
+        CHECK_THROWS_AS(swlh_query(set, 5, 9, {5, 5}), contract_error);
+        CHECK_THROWS_AS(swlh_query(set, 5, 5, KernelSpec{3, 3}), contract_error);
+    }
+    {  // wedding cake (test_swih.cpp:143-183): one layer = the plain local histogram
+        BinMap bm = random_binmap(120, 100, 16, 20257);
+        auto plain = build_integral_histogram(bm);
+        KernelSpec spec{9, 7};
+        auto cake = wedding_cake_swlh(plain, 30, 30, spec, 1);
+        KernelExtents e = kernel_extents(spec);
+        auto counts = region_histogram(plain, Rect{30 - e.sxl, 30 - e.syt, spec.kw, spec.kh});
+        for (int k = 0; k < 16; ++k) CHECK(std::abs(cake[k] - counts[k] / 63.0) <= 1e-12);
+        double prev = -1;
+        for (int layers : {2, 4}) {
+            const double mse = histogram_mse(wedding_cake_swlh(plain, 60, 50, {31, 41}, layers),
+                                             brute_force_swlh(bm, 60, 50, {31, 41}));
+            CHECK(mse > 0.0);
+            if (prev >= 0) CHECK(mse <= prev);
+            prev = mse;
+        }
+        CHECK_THROWS_AS(wedding_cake_swlh(plain, 30, 30, spec, 0), contract_error);
+    }
+    {  // temporal medians (test_motion.cpp:96-195)
+        std::mt19937 rng(77);
+        auto window = [&](int w, int h, int bins, int count) {
+            FrameWindow win;
+            std::uniform_int_distribution<int> d(0, bins - 1);
+            for (int f = 0; f < count; ++f) {
+                GrayImage g(w, h);
+                for (auto& v : g.data) v = static_cast<std::uint8_t>(d(rng));
+                win.frames.push_back(g);
+            }
+            return win;
+        };
+        FrameWindow win = window(13, 10, 256, 9);
+        GrayImage bg = median_background_sort(win);
+        for (int y = 0; y < 10; ++y)
+            for (int x = 0; x < 13; ++x) {
+                std::vector<int> vals;
+                for (const auto& f : win.frames) vals.push_back(f.at(x, y));
+                std::sort(vals.begin(), vals.end());
+                CHECK(bg.at(x, y) == vals[4]);
+            }
+        // 1x1 kernel, 256 bins: the IH median is the sorting median (test_motion.cpp:148-155)
+        CHECK(median_background_ih(win, 256, 1, 1).data == bg.data);
+        // sliding equals rebuilding (test_motion.cpp:166-185); brute-force spatiotemporal median
+        FrameWindow all = window(23, 17, 16, 9);
+        FrameWindow first{std::vector<GrayImage>(all.frames.begin(), all.frames.begin() + 5)};
+        MedianBackgroundIH model(first, 16, 5, 3);
+        for (int i = 5; i < 9; ++i) {
+            model.slide(all.frames[i]);
+            FrameWindow cur{std::vector<GrayImage>(all.frames.begin() + i - 4, all.frames.begin() + i + 1)};
+            const GrayImage got = model.background();
+            CHECK(got.data == median_background_ih(cur, 16, 5, 3).data);
+            for (int y = 0; y < 17; ++y)
+                for (int x = 0; x < 23; ++x) {
+                    std::vector<int> vals;
+                    for (const auto& f : cur.frames)
+                        for (int yy = std::max(0, y - 1); yy < std::min(17, y + 2); ++yy)
+                            for (int xx = std::max(0, x - 2); xx < std::min(23, x + 3); ++xx) vals.push_back(f.at(xx, yy));
+                    std::sort(vals.begin(), vals.end());
+                    const int med = vals[(vals.size() - 1) / 2];
+                    CHECK(got.at(x, y) == (2 * med + 1) * 128 / 16);
+                }
+        }
+        CHECK_THROWS_AS(MedianBackgroundIH(first, 8, 3, 3), contract_error);   // value >= bins
+        CHECK_THROWS_AS(MedianBackgroundIH(first, 16, 2, 3), contract_error);  // even side
+        CHECK_THROWS_AS(model.slide(GrayImage(5, 5)), contract_error);
+        FrameWindow even{std::vector<GrayImage>(all.frames.begin(), all.frames.begin() + 4)};
+        CHECK_THROWS_AS(median_background_sort(even), contract_error);
+        CHECK_THROWS_AS(median_background_sort(FrameWindow{}), contract_error);
     }
     std::printf("dropin_test: %d checks passed\n", g_checks);
     return 0;
