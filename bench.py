@@ -251,9 +251,17 @@ def run_ours(args) -> None:
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if not torch.cuda.is_available():
         raise SystemExit("bench.py: no CUDA device")
+    # SPCT_BENCH_SHARED_GPU=1: every rank on cuda:0 with a gloo group (functional check of
+    # the N > 1 path on a one-GPU box; its numbers are not scaling numbers)
+    shared = os.environ.get("SPCT_BENCH_SHARED_GPU") == "1"
+    if shared:
+        local = 0
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if shared:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
 
     import paper_1711_01656_b200 as P
     from paper_1711_01656_b200 import profiling
@@ -273,10 +281,26 @@ def run_ours(args) -> None:
     lmap = torch.empty((H_IMG, W_IMG), dtype=torch.float64, device=dev)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
 
+    peer = None
+    if world > 1 and args.reduce == "peer":
+        from paper_1711_01656_b200.sharding import PeerSlabReduce
+
+        peer = PeerSlabReduce(nu, nv, device=dev)
+
     def step(src):
         if world == 1:
             # every bin on this GPU: the sweep writes the finished map itself
             P.build_and_match_map(src, nbins, None, KW, KH, P_ORDER, out=t, lmap=lmap, tmpl_dev=tm)
+            return
+        if peer is not None:
+            # the sweep writes its slab's partial map into its slot on rank 0 over NVLink;
+            # rank 0 waits for every rank's flag, sums the slots while finalising
+            peer.begin()
+            P.build_and_match(src, nbins, None, KW, KH, P_ORDER, bin0=bin0, bins=bin1 - bin0, out=t,
+                              partial=peer.slot(), tmpl_dev=tm)
+            peer.publish()
+            if rank == 0:
+                peer.finalize(lmap, W_IMG, H_IMG, KW, KH, P_ORDER)
             return
         P.build_and_match(src, nbins, None, KW, KH, P_ORDER, bin0=bin0, bins=bin1 - bin0, out=t, partial=part,
                           tmpl_dev=tm)
@@ -300,7 +324,7 @@ def run_ours(args) -> None:
             b.record(stream)
         barrier()
         ms = sum(a.elapsed_time(b) for a, b in ev)
-        return max_over_ranks(ms, dev) / k
+        return max_over_ranks(ms, None if shared else dev) / k
 
     for _ in range(args.warmup):
         step(frame)
@@ -383,6 +407,10 @@ def run_ours(args) -> None:
             e2e_step()
         ms_e2e = timed(e2e_step, args.steps)
 
+    if peer is not None:
+        if peer.error():
+            raise SystemExit("bench.py: a peer-reduce wait timed out")
+        peer.close()
     if rank != 0:
         if world > 1:
             dist.destroy_process_group()
@@ -418,7 +446,10 @@ def run_ours(args) -> None:
         "config": {"workload": ("C3: 4096x4096 uint8 frame -> quantise -> %d-bin uint32 integral histogram "
                                 "+ 64x64 p=1 likelihood map (float64)" % nbins),
                    "bins_total": nbins, "bins_per_gpu": BINS_PER_GPU, "window": [KW, KH], "p": P_ORDER,
-                   "parallelism": f"bin-slab x{world}" + (" + NCCL reduce of partial maps" if world > 1 else ""),
+                   "parallelism": f"bin-slab x{world}" + (
+                       "" if world == 1 else (" + partial maps written to rank 0 over peer memory (fused reduce)"
+                                              if args.reduce == "peer" else " + NCCL reduce of partial maps")),
+                   **({"shared_gpu": True} if shared else {}),
                    "l2": "256 MiB memset between timed steps (outside the events); step writes 8.6 GB/GPU"},
         "roofline": roof,
         "e2e": {"value": round(total_binpx / (ms_e2e * 1e-3) / 1e9, 2), "unit": UNIT,
@@ -450,6 +481,8 @@ def main():
                     help="rows of the frame in the bounded CPU sample (window rows = rows - 63)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-c5", action="store_true", help="skip the config-5 tracking-batch measurement")
+    ap.add_argument("--reduce", choices=["peer", "nccl"], default="peer",
+                    help="N > 1: partial maps via peer-memory slots (default) or an NCCL reduce")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

@@ -275,6 +275,27 @@ spct_status spct_cu_ih_build_match_map(const spct_source* src, const spct_ih* ou
                                        int kw, int kh, double p, int metric, double* map,
                                        void* workspace, size_t workspace_bytes, void* stream);
 
+/* ----------------------------------------------------------------- bin-slab reduce over peer memory
+ * (peer.cu).  The multi-GPU form of hist_distance_map (likelihood.cpp:193-225)
+ * with the bins sharded across ranks: rank r passes a slot of the root's slot buffer
+ * (opened with spct_cu_peer_open) as the `partial` of spct_cu_ih_build_match, so its
+ * sweep writes the partial map over NVLink; then publishes with spct_cu_flag_signal.
+ * The root waits (spct_cu_flag_wait) and runs spct_cu_hist_finalize_slots, which sums
+ * the slots in rank order and finalises (spread_valid + clamp, likelihood.cpp:44-58,
+ * 220-221).  Buffers shared this way come from spct_cu_peer_alloc (zeroed cudaMalloc +
+ * its IPC handle, SPCT_IPC_HANDLE_BYTES bytes).  Flags are uint64 epochs; a wait that
+ * exceeds timeout_ns sets *err (device) to 1 and returns instead of hanging. */
+#define SPCT_IPC_HANDLE_BYTES 64
+spct_status spct_cu_peer_alloc(size_t bytes, void** ptr, void* handle);
+spct_status spct_cu_peer_free(void* ptr);
+spct_status spct_cu_peer_open(const void* handle, void** ptr);
+spct_status spct_cu_peer_close(void* ptr);
+spct_status spct_cu_flag_signal(uint64_t* flag, uint64_t value, void* stream);
+spct_status spct_cu_flag_wait(const uint64_t* flags, int n, int64_t stride, uint64_t value, uint64_t timeout_ns,
+                              uint32_t* err, void* stream);
+spct_status spct_cu_hist_finalize_slots(const double* slots, int nslots, int64_t slot_stride, int width, int height,
+                                        int kw, int kh, double p, int metric, double* map, void* stream);
+
 /* ----------------------------------------------------------------- instrumentation */
 
 /* Every kernel launch of this library increments a process-wide counter.  With

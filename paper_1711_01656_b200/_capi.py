@@ -16,6 +16,7 @@ LIB_PATH = os.environ.get("SPCT_LIB_PATH") or os.path.join(HERE, "libspct_b200.s
 SPCT_OK, SPCT_ERR_CONTRACT, SPCT_ERR_IO, SPCT_ERR_CUDA, SPCT_ERR_OOM = 0, 2, 3, 4, 5
 SRC_BINS_U16, SRC_GRAY_U8, SRC_RGB_U8, SRC_SCALAR_F64 = 0, 1, 2, 3
 METRIC_MINKOWSKI, METRIC_INTERSECTION, METRIC_BHATTACHARYYA, METRIC_CHISQ = 0, 1, 2, 3
+SPCT_IPC_HANDLE_BYTES = 64
 SCHED_SEQUENTIAL, SCHED_STS, SCHED_CW_TIS, SCHED_WF_TIS = 0, 1, 2, 3
 
 
@@ -95,6 +96,13 @@ SIGNATURES = {
     "spct_cu_ih_accumulate": (_i, [_src_p, _ih_p, _i, _vp, _sz, _vp]),
     "spct_cu_median_background": (_i, [_ih_p, _i, _i, _i, _vp, _i64, _vp]),
     "spct_cu_median_sort": (_i, [C.POINTER(_vp), _i, _i, _i, _i64, _vp, _i64, _vp]),
+    "spct_cu_peer_alloc": (_i, [_sz, C.POINTER(_vp), _vp]),
+    "spct_cu_peer_free": (_i, [_vp]),
+    "spct_cu_peer_open": (_i, [_vp, C.POINTER(_vp)]),
+    "spct_cu_peer_close": (_i, [_vp]),
+    "spct_cu_flag_signal": (_i, [_vp, C.c_uint64, _vp]),
+    "spct_cu_flag_wait": (_i, [_vp, _i, _i64, C.c_uint64, C.c_uint64, _vp, _vp]),
+    "spct_cu_hist_finalize_slots": (_i, [_vp, _i, _i64, _i, _i, _i, _i, _d, _i, _vp, _vp]),
     "spct_cu_launch_count": (C.c_uint64, []),
     "spct_cu_profile_enable": (None, [_i]),
     "spct_cu_profile_reset": (None, []),

@@ -1,0 +1,77 @@
+"""The bin-slab reduce over peer memory (PeerSlabReduce, peer.cu) with two ranks.
+
+Both ranks run on cuda:0 (the GPU boxes of this run have one GPU): the IPC mappings,
+the cross-process flags and the slot double-buffering are the same code as across
+GPUs, only the NVLink hop is missing.  Rank 1's sweep writes its slab's partial map
+into rank 0's slot buffer; rank 0 finalises.  Over several epochs (frames) the map
+must equal the single-GPU map of the full histogram (FP64, slab-sum rounding only).
+"""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _frames(n, w, h):
+    rng = np.random.default_rng(5)
+    base = rng.integers(0, 256, (h, w), dtype=np.uint8)
+    return [np.roll(base, 3 * i, axis=1) for i in range(n)]
+
+
+def _worker(rank, world, port, out_path, nbins, kw, kh, p):
+    import torch.distributed as dist
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    import paper_1711_01656_b200 as P
+    from paper_1711_01656_b200.sharding import PeerSlabReduce, slab_bounds
+
+    w, h = 300, 170
+    frames = _frames(5, w, h)
+    crop = (frames[0][40:40 + kh, 70:70 + kw].astype(np.int64) * nbins) >> 8
+    tmpl = np.bincount(crop.reshape(-1), minlength=nbins).astype(np.float64) / crop.size
+    k0, k1 = slab_bounds(nbins, world, rank)
+    red = PeerSlabReduce(w - kw + 1, h - kh + 1)
+    got = []
+    try:
+        for f in frames:
+            src = torch.from_numpy(f).cuda()
+            red.begin()
+            P.build_and_match(src, nbins, tmpl, kw, kh, p, bin0=k0, bins=k1 - k0, partial=red.slot())
+            red.publish()
+            if rank == 0:
+                lmap = torch.empty((h, w), dtype=torch.float64, device="cuda")
+                red.finalize(lmap, w, h, kw, kh, p)
+                got.append(lmap.cpu().numpy())
+        assert not red.error(), "peer wait timed out"
+        if rank == 0:
+            want = [P.build_and_match_map(torch.from_numpy(f).cuda(), nbins, tmpl, kw, kh, p)[1].cpu().numpy()
+                    for f in frames]
+            np.save(out_path, np.stack([np.stack(got), np.stack(want)]))
+    finally:
+        red.close()
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("nbins,kw,kh,p", [(64, 33, 21, 1.0), (40, 16, 16, 2.0)])
+def test_peer_slab_reduce_two_ranks(tmp_path, nbins, kw, kh, p):
+    import torch.multiprocessing as mp
+
+    out = str(tmp_path / "maps.npy")
+    mp.spawn(_worker, args=(2, _free_port(), out, nbins, kw, kh, p), nprocs=2, join=True)
+    got, want = np.load(out)
+    assert got.shape == want.shape
+    err = np.abs(got - want)
+    assert np.all(err <= 1e-5 * np.maximum(np.abs(want), 1e-12) + 1e-12), err.max()

@@ -69,3 +69,25 @@ def test_reduce_of_slab_partials_matches_single_rank(tmp_path, world, p):
     mp.spawn(_worker, args=(world, _free_port(), out, p), nprocs=world, join=True)
     got, want = np.load(out)
     assert np.all(np.abs(got - want) <= 1e-5 * np.abs(want) + 1e-12)
+
+
+def test_peer_slot_schedule():
+    """PeerSlabReduce bookkeeping: slots of consecutive epochs never overlap, every slot
+    lies inside the 2 * world slot buffer, and a rank waits for exactly the epoch that
+    last used its slot."""
+    from paper_1711_01656_b200.sharding import ack_needed, slot_offset
+
+    for world in (1, 2, 3, 8):
+        stride = 96
+        for e in range(1, 7):
+            cur = {slot_offset(e, r, world, stride) for r in range(world)}
+            nxt = {slot_offset(e + 1, r, world, stride) for r in range(world)}
+            assert len(cur) == world and not cur & nxt
+            assert all(0 <= o and o + stride <= 2 * world * stride for o in cur)
+            need = ack_needed(e)
+            if need:
+                assert slot_offset(need, 0, world, stride) == slot_offset(e, 0, world, stride)
+            else:
+                assert e <= 2
+    with pytest.raises(ValueError):
+        slot_offset(0, 0, 2, 8)
