@@ -152,21 +152,22 @@ __global__ void __launch_bounds__(256) ih_sweep_kernel(QuantParams q, PixelMode 
     uint32_t V[4][B];
     vpart_init_ca<B>(V, fc.C, fc.A, band, strip, gridDim.y, gridDim.x, Lb, Wp, kl0, x0);
     uint32_t* base_ptr = out.data + static_cast<int64_t>(kl0) * out.plane_pitch + x0;
-    const uint16_t* lt_strip =
-        (fc.Lt && strip > 0) ? fc.Lt + static_cast<int64_t>(strip) * out.height * Lb + kl0 : nullptr;
+    LtRows<B> lt{(fc.Lt && strip > 0) ? fc.Lt + (static_cast<int64_t>(strip) * out.height + y0) * Lb + kl0 : nullptr,
+                 Lb, y1 - y0};
+    lt.start();
 
-    uint32_t nxt = load_bins4(q, pm, x0, y0, k0, B);
+    uint32_t nxt = load_bins4_raw(q, pm, x0, y0, k0, B);
     for (int y = y0; y < y1; ++y) {
-        const uint32_t cur = nxt;
-        if (y + 1 < y1) nxt = load_bins4(q, pm, x0, y + 1, k0, B);
+        const uint32_t cur = decode_bins4(pm, nxt);
+        if (y + 1 < y1) nxt = load_bins4_raw(q, pm, x0, y + 1, k0, B);
         uint32_t t4[4];
         onehot_shifts(cur ^ kpat0, t4);
-        const uint16_t* lt_row = lt_strip ? lt_strip + static_cast<int64_t>(y) * Lb : nullptr;
+        lt.row(y - y0);
         uint32_t* prow = base_ptr + static_cast<int64_t>(y) * out.row_pitch;
 #pragma unroll
         for (int g = 0; g < B / 4; ++g)
-            vpart_group_q<B, MODE>(V, g, t4, lt16_group(lt_row, g),
-                                   prow + static_cast<int64_t>(4 * g) * out.plane_pitch, out.plane_pitch, store_mask);
+            vpart_group_q<B, MODE>(V, g, t4, lt.group(y - y0, g), prow + static_cast<int64_t>(4 * g) * out.plane_pitch,
+                                   out.plane_pitch, store_mask);
     }
 }
 

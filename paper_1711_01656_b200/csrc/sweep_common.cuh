@@ -74,6 +74,26 @@ __device__ __forceinline__ uint32_t load_bins4(const QuantParams& q, const Pixel
     return load_rel4(q, x, y, k0, nb);
 }
 
+// load_bins4 split in two for the gray shift mode, so a row-ahead prefetch keeps only the
+// raw load in flight and the decode sits at the consumer (the shift would otherwise
+// wait on the load right where it is issued).
+__device__ __forceinline__ uint32_t load_bins4_raw(const QuantParams& q, const PixelMode& m, int x, int y, int k0,
+                                                   int nb) {
+    if (m.shift < 0) return load_bins4(q, m, x, y, k0, nb);
+    const int64_t off = static_cast<int64_t>(y) * q.pitch + x;
+    const uint8_t* p = static_cast<const uint8_t*>(q.p0) + off;
+    if (x + 3 < q.width && (reinterpret_cast<uintptr_t>(p) & 3) == 0) return __ldg(reinterpret_cast<const uint32_t*>(p));
+    uint32_t w = 0;
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+        if (x + j < q.width) w |= static_cast<uint32_t>(__ldg(p + j)) << (8 * j);
+    return w;
+}
+
+__device__ __forceinline__ uint32_t decode_bins4(const PixelMode& m, uint32_t raw) {
+    return m.shift < 0 ? raw : (raw >> m.shift) & (0x01010101u * (0xFFu >> m.shift));
+}
+
 // Inclusive warp scan step with the shuffle's in-range predicate (no select).
 __device__ __forceinline__ uint32_t scan_add(uint32_t v, int o) {
     uint32_t r;
@@ -181,6 +201,38 @@ __device__ __forceinline__ void vpart_init_ca(uint32_t (&V)[4][B], const uint16_
         for (int k = 0; k < B; ++k) V[0][k] = V[1][k] = V[2][k] = V[3][k] = 0;
     }
 }
+
+// Row carries of a warp's B-bin slab (B / 2 words of u16 pairs per row), fetched as one
+// coalesced load of 64 / B rows per lane-word and one chunk ahead, so the L2 latency of
+// the carry table never sits on a row's critical path; row r of the chunk is read back
+// with shuffles.  `p` is row 0's carries of the warp's first bin (null: first strip).
+template <int B>
+struct LtRows {
+    static constexpr int kWords = B / 2;          // words per row
+    static constexpr int kRows = 32 / kWords;     // rows per chunk
+    const uint16_t* p;
+    int Lb, nrows;
+    uint32_t cur = 0, nxt = 0;
+    __device__ __forceinline__ uint32_t fetch(int r0) const {
+        const int l = static_cast<int>(threadIdx.x & 31);
+        const int r = r0 + l / kWords;
+        return (p && r < nrows) ? __ldg(reinterpret_cast<const uint32_t*>(p + static_cast<int64_t>(r) * Lb) + l % kWords)
+                                : 0u;
+    }
+    __device__ __forceinline__ void start() { nxt = fetch(0); }
+    // call once per row r = 0, 1, ... before group()
+    __device__ __forceinline__ void row(int r) {
+        if (r % kRows == 0) {
+            cur = nxt;
+            nxt = fetch(r + kRows);
+        }
+    }
+    __device__ __forceinline__ uint4 group(int r, int g) const {
+        const int sl = (r % kRows) * kWords + 2 * g;
+        const uint32_t a = __shfl_sync(0xffffffffu, cur, sl), b = __shfl_sync(0xffffffffu, cur, sl + 1);
+        return make_uint4(a & 0xFFFFu, a >> 16, b & 0xFFFFu, b >> 16);
+    }
+};
 
 // Row carries of group g (4 bins) from a u16 carry row (null: first strip, all zero).
 __device__ __forceinline__ uint4 lt16_group(const uint16_t* lt_row, int g) {
