@@ -39,3 +39,6 @@ if len(sys.argv) > 2:
     segs.sort(key=lambda s: -s[0] * len(s[2]))
     for n, a, rs in segs[: int(sys.argv[2])]:
         print(a[-5:], n, len(rs), f"{n*len(rs)/tot*100:.1f}%", "stall", sum(int(x[ist] or 0) for x in rs), rs[0][isrc][:50])
+    print("top stalled instructions:")
+    for r in sorted(data, key=lambda r: -int(r[ist] or 0))[:12]:
+        print(" ", r[iad][-5:], r[ist], r[isrc][:80])
