@@ -23,21 +23,27 @@ constexpr int kTileBins = 128;
 
 template <bool G8>
 __global__ void __launch_bounds__(256) fcarry_tiles_kernel(QuantParams q, int bin0, int bins, int Lb, int nstrips,
-                                                           int nbands, int band_rows, uint8_t* __restrict__ R8,
-                                                           uint16_t* __restrict__ C16, uint32_t* __restrict__ T1) {
+                                                           int nbands, int band_rows, int tb, int suf_row0,
+                                                           uint8_t* __restrict__ R8, uint16_t* __restrict__ C16,
+                                                           uint32_t* __restrict__ T1, uint16_t* __restrict__ S16) {
     extern __shared__ uint32_t fsm[];
-    uint32_t* cnt = fsm;                           // [128 bins][128 columns]
-    uint32_t* rh = fsm + kTileBins * kStrip;       // [8 warps][128 bins]
+    uint32_t* cnt = fsm;                  // [tb bins][128 columns]
+    uint32_t* rh = fsm + tb * kStrip;     // [8 warps][128 bins]
+    uint32_t* cs = rh + 8 * kTileBins;    // [tb bins][128 columns]: window-start suffix counts
     const int s = blockIdx.x, j = blockIdx.y, kc0 = blockIdx.z * kTileBins;
     const int kcn = min(kTileBins, Lb - kc0);
     const bool need_r = s + 1 < nstrips, need_c = j + 1 < nbands;
+    const bool need_s = need_c && S16;
     if (!need_r && !need_c) return;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     if (need_c)
-        for (int i = tid; i < kTileBins * kStrip; i += 256) cnt[i] = 0;
+        for (int i = tid; i < tb * kStrip; i += 256) cnt[i] = 0;
+    if (need_s)
+        for (int i = tid; i < tb * kStrip; i += 256) cs[i] = 0;
     for (int i = tid; i < 8 * kTileBins; i += 256) rh[i] = 0;
     __syncthreads();
     const int y0 = j * band_rows, y1 = min(q.height, y0 + band_rows);
+    const int ys = y0 + suf_row0;  // the suffix rows [ys, y1)
     const int x = s * kStrip + 4 * lane;
     const int klo = bin0 + kc0, khi = min(kcn, bins - kc0);
     uint32_t* rw = rh + warp * kTileBins;
@@ -59,6 +65,7 @@ __global__ void __launch_bounds__(256) fcarry_tiles_kernel(QuantParams q, int bi
             const int k = b[c] - klo;
             if (b[c] >= 0 && static_cast<unsigned>(k) < static_cast<unsigned>(khi)) {
                 if (need_c) atomicAdd(&cnt[k * kStrip + c * 32 + lane], 1u);
+                if (need_s && y >= ys) atomicAdd(&cs[k * kStrip + c * 32 + lane], 1u);
                 if (need_r) atomicAdd(&rw[k], 1u);
             }
         }
@@ -103,7 +110,12 @@ __global__ void __launch_bounds__(256) fcarry_tiles_kernel(QuantParams q, int bi
         const int k = i / (kStrip / 4), l = i % (kStrip / 4);  // columns 4 l .. 4 l + 3
         const uint32_t* ck = cnt + k * kStrip + l;
         const uint2 v = make_uint2(ck[0] | (ck[32] << 16), ck[64] | (ck[96] << 16));
-        *reinterpret_cast<uint2*>(C16 + (static_cast<int64_t>(j) * Lb + kc0 + k) * Wp + s * kStrip + 4 * l) = v;
+        const int64_t o = (static_cast<int64_t>(j) * Lb + kc0 + k) * Wp + s * kStrip + 4 * l;
+        *reinterpret_cast<uint2*>(C16 + o) = v;
+        if (need_s) {
+            const uint32_t* cq = cs + k * kStrip + l;
+            *reinterpret_cast<uint2*>(S16 + o) = make_uint2(cq[0] | (cq[32] << 16), cq[64] | (cq[96] << 16));
+        }
     }
     // band x strip totals, [kl][j][s]
     for (int k = warp; k < kcn; k += 8) {
@@ -203,7 +215,7 @@ namespace spct_impl {
 
 using namespace spct_carry;
 
-FusedCarryLayout fused_carry_layout(const BuildPlan& p, int height) {
+FusedCarryLayout fused_carry_layout(const BuildPlan& p, int height, bool window) {
     FusedCarryLayout L{};
     const size_t lb = static_cast<size_t>(p.Lb);
     L.lt_off = 0;
@@ -214,14 +226,16 @@ FusedCarryLayout fused_carry_layout(const BuildPlan& p, int height) {
     L.c_bytes = p.nbands > 1 ? round_up(static_cast<int64_t>(p.nbands - 1) * lb * p.Wp * 2, 256) : 0;
     L.a_off = L.c_off + L.c_bytes;
     L.a_bytes = p.nbands > 1 ? round_up(static_cast<int64_t>(p.nbands - 1) * p.nstrips * lb * 4, 256) : 0;
-    L.total = L.a_off + L.a_bytes;
+    L.s_off = L.a_off + L.a_bytes;
+    L.s_bytes = window ? L.c_bytes : 0;
+    L.total = L.s_off + L.s_bytes;
     return L;
 }
 
 spct_status build_fused_carries(const QuantParams& q, const spct_ih& out, const BuildPlan& p, void* workspace,
-                                size_t ws_bytes, cudaStream_t s, FusedCarries* fc) {
+                                size_t ws_bytes, cudaStream_t s, FusedCarries* fc, int kh) {
     *fc = FusedCarries{};
-    const FusedCarryLayout L = fused_carry_layout(p, out.height);
+    const FusedCarryLayout L = fused_carry_layout(p, out.height, kh > 1);
     if (L.total > 0 && (!workspace || ws_bytes < L.total))
         return contract("ih_build_match: workspace too small (query spct_cu_ih_build_workspace)");
     if (L.total == 0) return SPCT_OK;
@@ -230,20 +244,24 @@ spct_status build_fused_carries(const QuantParams& q, const spct_ih& out, const 
     uint16_t* Lt16 = L.lt_bytes ? reinterpret_cast<uint16_t*>(ws + L.lt_off) : nullptr;
     uint16_t* C16 = L.c_bytes ? reinterpret_cast<uint16_t*>(ws + L.c_off) : nullptr;
     uint32_t* A32 = L.a_bytes ? reinterpret_cast<uint32_t*>(ws + L.a_off) : nullptr;
-    const size_t smem = (kTileBins * kStrip + 8 * kTileBins) * 4;
-    static bool attr = false;
-    if (!attr) {
+    uint16_t* S16 = L.s_bytes ? reinterpret_cast<uint16_t*>(ws + L.s_off) : nullptr;
+    // window-start rows in every band: [y0 + o, y1), o = (-(kh - 1)) mod band_rows
+    const int suf_row0 = kh > 1 ? (p.band_rows - (kh - 1) % p.band_rows) % p.band_rows : 0;
+    const int tb = std::min(p.Lb, kTileBins);
+    const size_t smem = (static_cast<size_t>(tb) * kStrip * (S16 ? 2 : 1) + 8 * kTileBins) * 4;
+    static size_t attr = 48 * 1024;
+    if (smem > attr) {
         cudaFuncSetAttribute(fcarry_tiles_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         cudaFuncSetAttribute(fcarry_tiles_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        attr = true;
+        attr = smem;
     }
     dim3 g(p.nstrips, p.nbands, static_cast<unsigned>(ceil_div(p.Lb, kTileBins)));
     if (q.kind == SPCT_SRC_GRAY_U8 && q.fast_u8)
-        fcarry_tiles_kernel<true><<<g, 256, smem, s>>>(q, out.bin0, out.bins, p.Lb, p.nstrips, p.nbands, p.band_rows, R8,
-                                                        C16, A32);
+        fcarry_tiles_kernel<true><<<g, 256, smem, s>>>(q, out.bin0, out.bins, p.Lb, p.nstrips, p.nbands, p.band_rows, tb,
+                                                        suf_row0, R8, C16, A32, S16);
     else
-        fcarry_tiles_kernel<false><<<g, 256, smem, s>>>(q, out.bin0, out.bins, p.Lb, p.nstrips, p.nbands, p.band_rows, R8,
-                                                         C16, A32);
+        fcarry_tiles_kernel<false><<<g, 256, smem, s>>>(q, out.bin0, out.bins, p.Lb, p.nstrips, p.nbands, p.band_rows,
+                                                         tb, suf_row0, R8, C16, A32, S16);
     if (auto st = launch_status("fcarry_tiles_kernel")) return st;
     const int nb_lt = Lt16 ? static_cast<int>(ceil_div(static_cast<int64_t>(out.height) * (p.Lb / 4), 256)) : 0;
     const int nb_c = C16 ? static_cast<int>(ceil_div(static_cast<int64_t>(p.Lb) * p.Wp / 4, 256)) : 0;
@@ -263,6 +281,7 @@ spct_status build_fused_carries(const QuantParams& q, const spct_ih& out, const 
     fc->Lt = Lt16;
     fc->C = C16;
     fc->A = A32;
+    fc->S = S16;
     return SPCT_OK;
 }
 

@@ -83,13 +83,20 @@ spct_status build_match(const spct_source* src, const spct_ih* out, const double
         return spct_cu_hist_partial(out, tmpl, kw, kh, p, metric, partial, 0, stream);
     }
     const BuildPlan bp = plan_fused_sweep(out->width, out->height, out->bins);
-    const size_t carry_bytes = out->data ? fused_carry_layout(bp, out->height).total : 0;
+    // Band tops start their running column counts from the carry tables when that takes
+    // fewer load rounds than re-reading the kh - 1 rows above (few bins per CTA); with a
+    // full 128-bin group the row pre-roll costs the same and needs no extra table.
+    const int nw_plan = fused_nw(out->bins), nt_plan = 32 * nw_plan;
+    const int64_t table_rounds = ceil_div(static_cast<int64_t>(std::min(out->bins, kGroupBins)) * kVcWords, 8 * nt_plan);
+    const int64_t preroll_rounds = ceil_div(static_cast<int64_t>(kExt / nt_plan) * (kh - 1), 8);
+    const int win_kh = (kh > 1 && nw_plan < 8 && table_rounds < preroll_rounds) ? kh : 0;
+    const size_t carry_bytes = out->data ? fused_carry_layout(bp, out->height, win_kh > 1).total : 0;
     const size_t need = carry_bytes + fused_prep_bytes(out->bins);
     if (!workspace || workspace_bytes < need) return contract("ih_build_match: workspace too small");
     FusedCarries fc{};
     char* ws = static_cast<char*>(workspace);
     if (out->data) {
-        if (auto st = build_fused_carries(q, *out, bp, workspace, workspace_bytes, s, &fc)) return st;
+        if (auto st = build_fused_carries(q, *out, bp, workspace, workspace_bytes, s, &fc, win_kh)) return st;
         ws += carry_bytes;
     }
     uint32_t* prep = reinterpret_cast<uint32_t*>(ws);

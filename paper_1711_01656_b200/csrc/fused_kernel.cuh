@@ -383,26 +383,59 @@ __global__ void __launch_bounds__(32 * NW, 16 / NW) sweep_match_kernel(QuantPara
     uint32_t lpre = lt_cta ? static_cast<uint32_t>(__ldg(lt_cta + static_cast<int64_t>(y0) * Lb)) : 0u;
     __syncthreads();  // vc zeroed
 
-    // Pre-roll rows [ystart, y0) only feed vc, and nothing leaves the window there: one
-    // barrier-free pass with several loads in flight (a per-row loop would pay the full
-    // DRAM latency on every row).
+    // (narrow CTAs only: with 8 warps the table loads take as many rounds as the pre-roll,
+    // and the branch alone costs the headline variant ~1.5%)
+    if (NW < 8 && fc.S && band > 0 && f.kh > 1) {
+        // vc over rows [ystart, y0) from the carry tables (carries.cu): rows above y0 minus
+        // rows above the band holding ystart, plus that band's suffix from ystart
+        // (u16 pairs, every true count >= 0 and < 2^16, so no borrow crosses a half)
+        const uint32_t* C32 = reinterpret_cast<const uint32_t*>(fc.C);
+        const uint32_t* S32 = reinterpret_cast<const uint32_t*>(fc.S);
+        const int64_t plane = static_cast<int64_t>(Lb) * Wp / 2;  // words per band
+        const int r = y0 - f.kh + 1, ib = r > 0 ? r / band_rows : -1;
+        constexpr int U = 8;  // loads in flight per thread
+        const int n = nb_cta * kVcWords;
+        for (int i0 = tid; i0 < n; i0 += U * NT) {
+            uint32_t pj[U], sf[U], pi[U];
 #pragma unroll
-    for (int c = 0; c < CPT; ++c)
-        if (xt_live[c]) {
-            const int nb_lo = out.bin0 + g0;
-            uint32_t* vcol = vc + vcol_w[c];
-            for (int y = ystart; y < y0; y += 8) {
-                uint64_t r[8];
+            for (int u = 0; u < U; ++u) {
+                const int i = i0 + u * NT;
+                const int k = i / kVcWords, w = i % kVcWords;  // bin, extended-column word (columns 2w, 2w + 1)
+                const int x = xs - kStrip + 2 * w;
+                const bool live = i < n && x >= 0;
+                const int64_t off = ((static_cast<int64_t>(g0 + k) * Wp) + x) >> 1;
+                pj[u] = live ? __ldg(C32 + (band - 1) * plane + off) : 0u;
+                sf[u] = (live && ib >= 0) ? __ldg(S32 + ib * plane + off) : 0u;
+                pi[u] = (live && ib >= 0 && ib + 1 < band) ? __ldg(C32 + ib * plane + off) : 0u;
+            }
 #pragma unroll
-                for (int i = 0; i < 8; ++i) r[i] = y + i < y0 ? raw_at(xt[c], y + i) : 0;
-#pragma unroll
-                for (int i = 0; i < 8; ++i) {
-                    const int bn = bin_of(r[i]) - nb_lo;
-                    if (y + i < y0 && static_cast<unsigned>(bn) < static_cast<unsigned>(nb_cta))
-                        atomicAdd(vcol + bn * kVcStride, vinc[c]);
-                }
+            for (int u = 0; u < U; ++u) {
+                const int i = i0 + u * NT;
+                if (i < n) vc[(i / kVcWords) * kVcStride + vcw(i % kVcWords)] = ib < 0 ? pj[u] : (ib + 1 == band ? sf[u] : sf[u] + pj[u] - pi[u]);
             }
         }
+    } else {
+        // No tables (tensor not stored): pre-roll rows [ystart, y0) only feed vc, and
+        // nothing leaves the window there: one barrier-free pass with several loads in
+        // flight (a per-row loop would pay the full DRAM latency on every row).
+#pragma unroll
+        for (int c = 0; c < CPT; ++c)
+            if (xt_live[c]) {
+                const int nb_lo = out.bin0 + g0;
+                uint32_t* vcol = vc + vcol_w[c];
+                for (int y = ystart; y < y0; y += 8) {
+                    uint64_t r[8];
+#pragma unroll
+                    for (int i = 0; i < 8; ++i) r[i] = y + i < y0 ? raw_at(xt[c], y + i) : 0;
+#pragma unroll
+                    for (int i = 0; i < 8; ++i) {
+                        const int bn = bin_of(r[i]) - nb_lo;
+                        if (y + i < y0 && static_cast<unsigned>(bn) < static_cast<unsigned>(nb_cta))
+                            atomicAdd(vcol + bn * kVcStride, vinc[c]);
+                    }
+                }
+            }
+    }
 
     // Cross-warp combine of row yy: thread t < 128 finishes the window ending at strip
     // column t.  Integer path with a finished map (ALLB): L = alpha + beta I (one FMA).

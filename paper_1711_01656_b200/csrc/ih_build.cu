@@ -315,7 +315,7 @@ extern "C" spct_status spct_cu_ih_build_workspace(const spct_source* src, int bi
     if (!(src->width > 0 && src->height > 0 && bins >= 1)) return contract("build: empty bin map");
     const BuildPlan p = plan_build_sweep(src->width, src->height, bins);
     const BuildPlan pf = plan_fused_sweep(src->width, src->height, bins);  // fused sweep: 16 bins per warp
-    *bytes = std::max(fused_carry_layout(p, src->height).total, fused_carry_layout(pf, src->height).total) +
+    *bytes = std::max(fused_carry_layout(p, src->height).total, fused_carry_layout(pf, src->height, true).total) +
              fused_prep_bytes(bins) + 256;
     return SPCT_OK;
 }

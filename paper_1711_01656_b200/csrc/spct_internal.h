@@ -78,12 +78,16 @@ struct FusedCarries {
     const uint16_t* Lt;  // [nstrips][H][Lb]        (strip 0 unused)
     const uint16_t* C;   // [nbands - 1][Lb][Wp]
     const uint32_t* A;   // [Lb][nbands - 1][nstrips]
+    // matcher window start (kh > 1): S[i][kl][x] = count of kl in column x over rows
+    // [y0_i + o, y1_i), o = (-(kh - 1)) mod band_rows; with C it gives the sweep's running
+    // column counts at every band top without re-reading the kh - 1 rows above it
+    const uint16_t* S;   // [nbands - 1][Lb][Wp] or null
 };
 struct FusedCarryLayout {
-    size_t lt_off, lt_bytes, r_off, r_bytes, c_off, c_bytes, a_off, a_bytes, total;
+    size_t lt_off, lt_bytes, r_off, r_bytes, c_off, c_bytes, a_off, a_bytes, s_off, s_bytes, total;
 };
-FusedCarryLayout fused_carry_layout(const BuildPlan& p, int height);
+FusedCarryLayout fused_carry_layout(const BuildPlan& p, int height, bool window = false);
 spct_status build_fused_carries(const spct_dev::QuantParams& q, const spct_ih& out, const BuildPlan& p,
-                                void* workspace, size_t ws_bytes, cudaStream_t s, FusedCarries* fc);
+                                void* workspace, size_t ws_bytes, cudaStream_t s, FusedCarries* fc, int kh = 0);
 
 }  // namespace spct_impl

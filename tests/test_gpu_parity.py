@@ -365,9 +365,12 @@ def test_fused_general_template(P, w, h, bins, kw, kh, p, metric):
 
 
 @pytest.mark.parametrize("rows", [1, 5, 64, 100])
-def test_fused_bands(P, band_rows, rows):
+@pytest.mark.parametrize("bins", [40, 24])
+def test_fused_bands(P, band_rows, rows, bins):
+    """Forced band heights: band tops start from the window-start carry tables (bins <= 64,
+    narrow CTAs) with the window start in the band above, further up, or above row 0."""
     band_rows(rows)
-    w, h, bins, kw, kh = 290, 173, 40, 64, 37
+    w, h, kw, kh = 290, 173, 64, 37
     img = oracle.smooth_image(w, h, rows)
     qb = oracle.quantize(img, bins)
     th = _crop_template(qb, bins, 100, 60, kw, kh)

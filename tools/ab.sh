@@ -1,8 +1,10 @@
-# usage: ab.sh name1=path1 name2=path2 ... (path "" = default lib)
-for kv in "$@"; do
-  n=${kv%%=*}; p=${kv#*=}
-  for rep in 1 2; do
-    SPCT_LIB_PATH=$p timeout 300 python bench.py --steps 10 --warmup 3 --no-cpu-baseline > gpurun_out/ab_$n.log 2>&1
-    tail -1 gpurun_out/ab_$n.log | python -c "import json,sys; d=json.loads(sys.stdin.read()); print('$n', d['value'], d['ms_per_step'], d['roofline']['kernel_ms'], d['e2e']['value'])"
+#!/bin/bash
+# A/B of two builds of the library on one box: tools/ab.sh a.so b.so [rounds]
+mkdir -p gpurun_out
+for r in $(seq ${3:-2}); do
+  for lib in "$1" "$2"; do
+    SPCT_LIB_PATH=$lib python bench.py --steps 10 --warmup 3 --no-cpu-baseline ${BENCH_ARGS} 2>/dev/null | tail -1 | python -c "
+import json,sys; d=json.loads(sys.stdin.read()); r=d['roofline']; b=d.get('build_only') or {}; c=d.get('c5_batch') or {}
+print('$lib', 'kernel', r['kernel_ms'], 'build', b.get('kernel_ms'), 'c5', c.get('ms_per_frame'))"
   done
 done
