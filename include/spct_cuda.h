@@ -102,7 +102,8 @@ spct_status spct_cu_quantize(const spct_source* src, uint16_t* out_bins, void* s
  * Gaussian smoothing, central differences, atan fold to degrees) binned by
  * phog.cpp:15-20 orientation_bin.  gray (dev) with row pitch `pitch`; out (dev) uint16
  * with row pitch out_pitch.  Contract: sigma >= 0 (features.cpp:201), width,height > 0,
- * 1 <= bins <= 65536, ceil(3 sigma) <= 31.  Workspace: spct_cu_orientation_workspace. */
+ * 1 <= bins <= 65536, ceil(3 sigma) <= 31.  Workspace: spct_cu_orientation_workspace (the
+ * bin-boundary table, 2 KiB). */
 spct_status spct_cu_orientation_workspace(int width, int height, size_t* bytes);
 spct_status spct_cu_orientation_bins(const uint8_t* gray, int64_t pitch, int width, int height, double sigma,
                                      int bins, uint16_t* out, int64_t out_pitch, void* workspace,

@@ -429,6 +429,26 @@ def test_orientation_bins_exact(P, w, h, sigma, bins):
         assert np.array_equal(got, oracle.orientation_bins(img, bins, sigma))
 
 
+@pytest.mark.parametrize("bins", [32, 8, 12, 256, 300])
+def test_orientation_bins_on_bin_boundaries(P, bins):
+    """Ramps whose gradient ratio dy/dx sits exactly on (or next to) a bin boundary
+    (q = 0, +-1, +-2, +-1/2, ...): the boundary search hands those pixels to the reference
+    formula; bins > 256 take the formula everywhere.  Plus tiles with flat and dx == 0
+    regions, a 1-pixel-wide and a 1-pixel-tall frame."""
+    h, w = 70, 150
+    y, x = np.mgrid[0:h, 0:w]
+    imgs = [(x + y) % 256, (x - y) % 256, (2 * x + y) % 256, (x + 2 * y) % 256, (3 * y) % 256, np.full((h, w), 77),
+            (x // 16 * 9 + y // 8 * 9) % 256]
+    for img in imgs:
+        img = np.ascontiguousarray(img, np.uint8)
+        for sigma in (1.0, 0.0):
+            got = P.api.as_numpy_u16(P.orientation_bins(img, bins, sigma))
+            assert np.array_equal(got, oracle.orientation_bins(img, bins, sigma)), (bins, sigma)
+    for img in (oracle.noise_image(1, 97, 5), oracle.noise_image(131, 1, 6)):
+        got = P.api.as_numpy_u16(P.orientation_bins(img, bins, 1.0))
+        assert np.array_equal(got, oracle.orientation_bins(img, bins, 1.0))
+
+
 @pytest.mark.parametrize("frames", [2])
 def test_tracking_batch_channels(P, frames):
     """Config 5 in miniature: per frame, intensity / orientation / R / G / B likelihood maps
