@@ -362,7 +362,10 @@ __global__ void __launch_bounds__(32 * NW, 16 / NW) sweep_match_kernel(QuantPara
 
     // staging: thread tid owns extended columns tid + c NT (c < CPT); with one column per
     // thread (NW = 8) its raw pixels are prefetched one row ahead
-    constexpr bool PREFETCH = CPT == 1;
+    // (narrow CTAs, several columns per thread: prefetched as 32-bit raw values for the
+    // 8/16-bit sources; the generic source keeps the in-row loads)
+    constexpr bool PREFETCH = CPT == 1 || SK != 0;
+    using RawT = std::conditional_t<CPT == 1 || SK == 0, uint64_t, uint32_t>;
     int xt[CPT], vcol_w[CPT];
     bool xt_live[CPT];
     uint32_t vinc[CPT];
@@ -378,7 +381,12 @@ __global__ void __launch_bounds__(32 * NW, 16 / NW) sweep_match_kernel(QuantPara
                                  ? fc.Lt + static_cast<int64_t>(strip) * H * Lb + g0 + tid
                                  : nullptr;
     // raw pixel values of the staging column, quantised one row after the load
-    uint64_t rn = (PREFETCH && xt_live[0]) ? raw_at(xt[0], y0) : 0, ro = 0;
+    RawT rn[CPT], ro[CPT];
+#pragma unroll
+    for (int c = 0; c < CPT; ++c) {
+        rn[c] = (PREFETCH && xt_live[c]) ? static_cast<RawT>(raw_at(xt[c], y0)) : 0;
+        ro[c] = 0;
+    }
     bool have_o = false;  // y0 - kh < ystart: nothing to remove on the first row
     uint32_t lpre = lt_cta ? static_cast<uint32_t>(__ldg(lt_cta + static_cast<int64_t>(y0) * Lb)) : 0u;
     __syncthreads();  // vc zeroed
@@ -516,8 +524,8 @@ __global__ void __launch_bounds__(32 * NW, 16 / NW) sweep_match_kernel(QuantPara
             const bool old_row = y - f.kh >= ystart;
 #pragma unroll
             for (int c = 0; c < CPT; ++c) {
-                const uint64_t rnc = PREFETCH ? rn : (xt_live[c] ? raw_at(xt[c], y) : 0);
-                const uint64_t roc = PREFETCH ? ro : ((xt_live[c] && old_row) ? raw_at(xt[c], y - f.kh) : 0);
+                const uint64_t rnc = PREFETCH ? rn[c] : (xt_live[c] ? raw_at(xt[c], y) : 0);
+                const uint64_t roc = PREFETCH ? ro[c] : ((xt_live[c] && old_row) ? raw_at(xt[c], y - f.kh) : 0);
                 const bool ho = PREFETCH ? have_o : old_row;
                 const int pn = xt_live[c] ? bin_of(rnc) : 0xFFFF;
                 const int po = (xt_live[c] && ho) ? bin_of(roc) : -1;
@@ -537,10 +545,12 @@ __global__ void __launch_bounds__(32 * NW, 16 / NW) sweep_match_kernel(QuantPara
                 if (PREFETCH) {
                     const int yo = y + 1 - f.kh;
                     have_o = yo >= ystart;
-                    if (xt_live[0]) {
-                        rn = raw_at(xt[0], y + 1);
-                        if (have_o) ro = raw_at(xt[0], yo);
-                    }
+#pragma unroll
+                    for (int c = 0; c < CPT; ++c)
+                        if (xt_live[c]) {
+                            rn[c] = static_cast<RawT>(raw_at(xt[c], y + 1));
+                            if (have_o) ro[c] = static_cast<RawT>(raw_at(xt[c], yo));
+                        }
                 }
                 if (lt_cta) lpre = __ldg(lt_cta + static_cast<int64_t>(y + 1) * Lb);
             }
