@@ -281,11 +281,14 @@ def run_ours(args) -> None:
     lmap = torch.empty((H_IMG, W_IMG), dtype=torch.float64, device=dev)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
 
-    peer = None
+    peer, reduce_note = None, args.reduce
     if world > 1 and args.reduce == "peer":
         from paper_1711_01656_b200.sharding import PeerSlabReduce
 
-        peer = PeerSlabReduce(nu, nv, device=dev)
+        try:  # fails on every rank or on none (PeerSlabReduce agrees on the outcome)
+            peer = PeerSlabReduce(nu, nv, device=dev)
+        except RuntimeError as e:  # no IPC / peer access between these GPUs: the NCCL reduce instead
+            reduce_note = "nccl (peer setup failed: %s)" % str(e)[:120]
 
     def step(src):
         if world == 1:
@@ -448,7 +451,8 @@ def run_ours(args) -> None:
                    "bins_total": nbins, "bins_per_gpu": BINS_PER_GPU, "window": [KW, KH], "p": P_ORDER,
                    "parallelism": f"bin-slab x{world}" + (
                        "" if world == 1 else (" + partial maps written to rank 0 over peer memory (fused reduce)"
-                                              if args.reduce == "peer" else " + NCCL reduce of partial maps")),
+                                              if peer is not None else " + NCCL reduce of partial maps")),
+                   **({"reduce": reduce_note} if world > 1 else {}),
                    **({"shared_gpu": True} if shared else {}),
                    "l2": "256 MiB memset between timed steps (outside the events); step writes 8.6 GB/GPU"},
         "roofline": roof,

@@ -113,20 +113,35 @@ class PeerSlabReduce:
             self._opened.append(p.value)
             return p.value
 
-        self.ack, ack_h = alloc(128)  # [0]: last epoch the root finalised; [8]: error word
-        self.err = self.ack + 64
-        mine = {"ack": ack_h}
-        if self.rank == root:
-            self.slots, mine["slots"] = alloc(2 * self.world * self.stride * 8)
-            self.flags, mine["flags"] = alloc(self.world * self.FLAG_STRIDE * 8)
+        # Setup fails on every rank or on none: each step's errors are collected, the ranks
+        # agree on the outcome, and a failed setup releases everything before raising.
+        err, mine = None, {}
+        try:
+            self.ack, mine["ack"] = alloc(128)  # [0]: last epoch the root finalised; [8]: error word
+            self.err = self.ack + 64
+            if self.rank == root:
+                self.slots, mine["slots"] = alloc(2 * self.world * self.stride * 8)
+                self.flags, mine["flags"] = alloc(self.world * self.FLAG_STRIDE * 8)
+        except Exception as e:  # noqa: BLE001 (reported below, on every rank)
+            err = e
         handles = [None] * self.world
-        dist.all_gather_object(handles, mine, group=group)
-        if self.rank == root:
-            self.acks = [self.ack if q == root else open_(handles[q]["ack"]) for q in range(self.world)]
-        else:
-            self.slots = open_(handles[root]["slots"])
-            self.flags = open_(handles[root]["flags"])
-        dist.barrier(group=group)
+        dist.all_gather_object(handles, None if err else mine, group=group)
+        if err is None and any(hd is None for hd in handles):
+            err = RuntimeError("peer setup failed on another rank")
+        if err is None:
+            try:
+                if self.rank == root:
+                    self.acks = [self.ack if q == root else open_(handles[q]["ack"]) for q in range(self.world)]
+                else:
+                    self.slots = open_(handles[root]["slots"])
+                    self.flags = open_(handles[root]["flags"])
+            except Exception as e:  # noqa: BLE001
+                err = e
+        ok = [None] * self.world
+        dist.all_gather_object(ok, err is None, group=group)
+        if not all(ok):
+            self._release(group)
+            raise RuntimeError(f"PeerSlabReduce setup failed: {err or 'on another rank'}")
 
     def _s(self, stream):
         return (stream if stream is not None else self._torch.cuda.current_stream()).cuda_stream
@@ -167,7 +182,7 @@ class PeerSlabReduce:
         self._torch.cuda.synchronize(self.device)
         return bool(int(t.item()))
 
-    def close(self, group=None) -> None:
+    def _release(self, group=None) -> None:
         import torch.distributed as dist
 
         self._torch.cuda.synchronize(self.device)
@@ -179,3 +194,6 @@ class PeerSlabReduce:
         for p in self._own:
             lib.spct_cu_peer_free(p)
         self._own = []
+
+    def close(self, group=None) -> None:
+        self._release(group)
