@@ -10,9 +10,13 @@ Throughput is Gbin*px/s = b * H * W / step time, whole job over all ranks.
   python bench.py --impl reference [...]                   the reference CPU path
 
 Multi-GPU (N > 1): bin-slab sharding.  Rank r owns bins [128 r, 128 r + 128) of a
-b = 128 N histogram over the same frame (weak scaling: fixed work per GPU); each rank
-writes its slab of the integral histogram and its partial window sums, one NCCL
-reduce adds the partial maps on rank 0, which finalises the likelihood map.
+b = 128 N histogram over the same frame (weak scaling: fixed work per GPU); each rank's
+sweep writes its slab of the integral histogram and its partial window sums straight
+into its slot on rank 0 over peer memory (--reduce peer, default; --reduce nccl: one
+NCCL reduce instead), and rank 0 sums the slots while finalising the likelihood map.
+
+Extra lines of the JSON: build_only (plain build), c5_batch (config 5 tracking batch)
+and next_rows (SWIH, map consumers, temporal median).
 
 Timing: W untimed warm-up steps; K timed steps, each bracketed by CUDA events on the
 compute stream; a 256 MiB memset flushes L2 between steps outside the events;
@@ -242,6 +246,68 @@ def run_c5(P, dev, stream, args, frames: int = 100, side: int = 2048, nbins: int
             "l2": f"frames and tensors ({frames * 3 * side * side / 2**20:.0f} MiB of frames) exceed L2"}
 
 
+def run_next_rows(P, dev, pk_gbs: float) -> dict:
+    """SURVEY §8(f) rows on resident inputs, device-timed (CUDA events, synchronised): the
+    SWIH tracker channel, the map consumers at the C3 map size and the joint-IH temporal
+    median.  Each entry: ms per call, algorithmic bytes, GB/s and fraction of the HBM peak
+    (bytes that must move: outputs written + inputs read once)."""
+    import torch
+
+    def timed(fn, reps=5):
+        for _ in range(2):
+            fn()
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        for _ in range(reps):
+            fn()
+        b.record()
+        torch.cuda.synchronize()
+        return a.elapsed_time(b) / reps
+
+    def line(cfg, ms, alg):
+        gbs = alg / (ms * 1e-3) / 1e9 if alg else None
+        return {"config": cfg, "ms": round(ms, 4), "alg_bytes": alg,
+                "gbs": round(gbs, 1) if gbs else None, "frac": round(gbs / pk_gbs, 4) if gbs else None}
+
+    out = {}
+    g = torch.Generator(device=dev)
+    g.manual_seed(11)
+    # 1. SWIH (swih.cpp:115-164, track_loop.cpp:264-283): 1024^2 BinMap, 32 bins, 31 x 31 kernel
+    n, nb, k = 1024, 32, 31
+    bm = torch.randint(0, nb, (n, n), dtype=torch.int16, device=dev, generator=g)
+    model = np.full(nb, 1.0 / nb)
+    ms_b = timed(lambda: P.swih.build_quadrant_set(bm, nb, k, k))
+    out["swih_quadrant_set"] = line(f"{n}x{n} BinMap, {nb} bins, {k}x{k} kernel: four uint64 16.16 tensors", ms_b,
+                                    4 * nb * n * n * 8 + n * n * 2)
+    ms_m = timed(lambda: P.swih.swlh_distance_map(bm, nb, model, k, k))
+    out["swih_distance_map"] = line("quadrant set + swlh-distance map (float64)", ms_m,
+                                    4 * nb * n * n * 8 + n * n * 2 + n * n * 8)
+    # 2. map consumers (likelihood.cpp:257-330, tracker.cpp:77-113) at the C3 map size
+    m4 = [torch.rand((H_IMG, W_IMG), dtype=torch.float64, device=dev, generator=g) for _ in range(5)]
+    fused = torch.empty_like(m4[0])
+    ms_f = timed(lambda: P.fuse_maps(m4, [1, 2, 3, 4, 5], out=fused))
+    out["fuse_maps"] = line("5 maps 4096x4096 float64, weighted", ms_f, 6 * H_IMG * W_IMG * 8)
+    ms_p = timed(lambda: P.find_peaks(fused))
+    out["find_peaks"] = line("4096x4096: 3x3 mean, strict local maxima, stable sort by height", ms_p,
+                             H_IMG * W_IMG * 8)
+    ms_s = timed(lambda: P.score_map(fused, 1000, 1000, 64, 64))
+    out["score_map"] = line("4096x4096, 64x64 ground-truth rect", ms_s, H_IMG * W_IMG * 8)
+    starts = [[64 + 61 * i, 64 + 57 * i] for i in range(64)]
+    ms_c = timed(lambda: P.camshift_batch(fused, starts, 64, 64))
+    out["camshift_batch"] = line("64 starts, 64x64 windows, 4096x4096 map", ms_c, None)
+    # 3. joint-IH temporal median (motion.cpp:35-99): 1024^2, 16 bins, 5-frame window, 7x7
+    fr = [torch.randint(0, 16, (n, n), dtype=torch.uint8, device=dev, generator=g) for _ in range(8)]
+    mb = P.motion.MedianBackgroundIH(fr[:5], 16, 7, 7)
+    it = iter(range(10 ** 9))
+    ms_sl = timed(lambda: mb.slide(fr[5 + next(it) % 3]))
+    out["median_slide"] = line(f"{n}x{n}, 16 bins, 5 frames: joint tensor += IH(new), -= IH(old)", ms_sl,
+                               2 * 2 * 16 * n * n * 4 + 2 * n * n)
+    ms_bg = timed(lambda: mb.background())
+    out["median_background"] = line("7x7 windows, per-pixel CDF walk over 16 bins", ms_bg, 16 * n * n * 4 + n * n)
+    return out
+
+
 def run_ours(args) -> None:
     import torch
     import torch.distributed as dist
@@ -371,6 +437,10 @@ def run_ours(args) -> None:
     # tracking batch (BASELINE config 5): 100 synthetic 2048x2048 RGB frames x 32 bins, five
     # feature channels (intensity, gradient orientation, R, G, B) -> five likelihood maps per
     # frame, each channel one fused quantise -> integral histogram -> map sweep; frames resident
+    nxt = None
+    if world == 1 and not args.no_next:
+        nxt = run_next_rows(P, dev, peaks()["hbm_gbs"])
+
     c5 = None
     if world == 1 and not args.no_c5:
         c5 = run_c5(P, dev, stream, args)
@@ -462,6 +532,7 @@ def run_ours(args) -> None:
         "gpu_launches": int(launches),
         "build_only": build_only,
         "c5_batch": c5,
+        "next_rows": nxt,
         "clocks": clk.summary(),
     }
     if world == 1 and not args.no_cpu_baseline:
@@ -485,6 +556,7 @@ def main():
                     help="rows of the frame in the bounded CPU sample (window rows = rows - 63)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-c5", action="store_true", help="skip the config-5 tracking-batch measurement")
+    ap.add_argument("--no-next", action="store_true", help="skip the SURVEY 8(f) rows (SWIH, consumers, median)")
     ap.add_argument("--reduce", choices=["peer", "nccl"], default="peer",
                     help="N > 1: partial maps via peer-memory slots (default) or an NCCL reduce")
     args = ap.parse_args()

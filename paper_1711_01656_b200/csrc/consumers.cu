@@ -110,8 +110,11 @@ __global__ void __launch_bounds__(256) peak_count_kernel(const double* __restric
     if (threadIdx.x == 0) bcount[blockIdx.x] = tot;
 }
 
-// Single-CTA exclusive scan of n values in place (1024 threads, sequential chunks).
+// Exclusive scan of n values in place (1024 threads, sequential chunks); CTA b scans the
+// b-th run of n values (v + b n) and writes its sum to total[b].
 __global__ void __launch_bounds__(1024) excl_scan_kernel(uint32_t* __restrict__ v, int64_t n, uint32_t* total) {
+    v += static_cast<int64_t>(blockIdx.x) * n;
+    if (total) total += blockIdx.x;
     __shared__ uint32_t wsum[32];
     __shared__ uint32_t carry;
     if (threadIdx.x == 0) carry = 0;
@@ -191,14 +194,16 @@ __global__ void __launch_bounds__(256) radix_hist_kernel(const uint64_t* __restr
 }
 
 // Stable scatter: elements are ranked in index order (round-major, then thread order).
+// offs: per digit, the exclusive prefix over blocks (digit-major); dstart: the digits' starts.
 __global__ void __launch_bounds__(256) radix_scatter_kernel(const uint64_t* __restrict__ kin,
                                                             const uint32_t* __restrict__ vin, int64_t n, int shift,
                                                             int nblk, const uint32_t* __restrict__ offs,
+                                                            const uint32_t* __restrict__ dstart,
                                                             uint64_t* __restrict__ kout, uint32_t* __restrict__ vout) {
     __shared__ uint32_t run[256];       // per digit: elements of this block already placed
     __shared__ uint32_t wcnt[8][256];   // this round's per-warp digit counts, then prefixes
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    run[threadIdx.x] = offs[static_cast<int64_t>(threadIdx.x) * nblk + blockIdx.x];
+    run[threadIdx.x] = dstart[threadIdx.x] + offs[static_cast<int64_t>(threadIdx.x) * nblk + blockIdx.x];
     const int64_t base = static_cast<int64_t>(blockIdx.x) * kSortTile;
     for (int r = 0; r < kSortTile / 256; ++r) {
         for (int k = 0; k < 8; ++k) wcnt[k][threadIdx.x] = 0;
@@ -305,7 +310,7 @@ size_t peak_ws_bytes(int w, int h, int64_t* nblk_peak, int64_t* nblk_sort) {
     *nblk_peak = ceil_div(n, kPeakTile);
     *nblk_sort = std::max<int64_t>(1, ceil_div(cap, kSortTile));
     auto r = [](int64_t b) { return static_cast<size_t>(round_up(b, 256)); };
-    return r(n * 8) + r(*nblk_peak * 4) + 2 * r(cap * 8) + 2 * r(cap * 4) + r(256 * *nblk_sort * 4) + r(16);
+    return r(n * 8) + r(*nblk_peak * 4) + 2 * r(cap * 8) + 2 * r(cap * 4) + r(256 * *nblk_sort * 4) + r(16 + 1024);
 }
 
 PeakWs carve(void* ws, int w, int h) {
@@ -326,7 +331,7 @@ PeakWs carve(void* ws, int w, int h) {
     s.v[0] = reinterpret_cast<uint32_t*>(take(cap * 4));
     s.v[1] = reinterpret_cast<uint32_t*>(take(cap * 4));
     s.counts = reinterpret_cast<uint32_t*>(take(256 * nbs * 4));
-    s.scalars = reinterpret_cast<uint32_t*>(take(16));
+    s.scalars = reinterpret_cast<uint32_t*>(take(16 + 1024));  // [0]: peak count, [4 ..]: digit starts
     return s;
 }
 
@@ -349,11 +354,14 @@ spct_status sorted_peaks(const double* map, int w, int h, void* ws, size_t ws_by
     if (m > 1) {
         const int nb = static_cast<int>(ceil_div(m, kSortTile));
         int cur = 0;
+        uint32_t* digit = P.scalars + 4;  // [256] digit totals -> digit starts
         for (int pass = 0; pass < 8; ++pass) {
             radix_hist_kernel<<<nb, 256, 0, st>>>(P.k[cur], m, 8 * pass, nb, P.counts);
-            excl_scan_kernel<<<1, 1024, 0, st>>>(P.counts, static_cast<int64_t>(256) * nb, nullptr);
-            radix_scatter_kernel<<<nb, 256, 0, st>>>(P.k[cur], P.v[cur], m, 8 * pass, nb, P.counts, P.k[cur ^ 1],
-                                                     P.v[cur ^ 1]);
+            // per digit (one CTA each): prefix over the blocks; then the digits' starts
+            excl_scan_kernel<<<256, 1024, 0, st>>>(P.counts, nb, digit);
+            excl_scan_kernel<<<1, 1024, 0, st>>>(digit, 256, nullptr);
+            radix_scatter_kernel<<<nb, 256, 0, st>>>(P.k[cur], P.v[cur], m, 8 * pass, nb, P.counts, digit,
+                                                     P.k[cur ^ 1], P.v[cur ^ 1]);
             cur ^= 1;
         }
         if (auto e = launch_status("find_peaks sort")) return e;

@@ -13,6 +13,8 @@
 //                                                  d = sum |q_k - model_k|, replicate_borders
 // Integer results are bit-identical to the reference.  Normalisation divides in FP64
 // (the reference divides in x87 long double, then rounds to double: <= 1 ulp apart).
+#include <algorithm>
+
 #include "spct_internal.h"
 
 using namespace spct_impl;
@@ -89,6 +91,178 @@ __global__ void wih_col_kernel(spct_wih t) {
     for (int y = 0; y < t.height; ++y) {
         acc += p[static_cast<int64_t>(y) * t.row_pitch];
         p[static_cast<int64_t>(y) * t.row_pitch] = acc;
+    }
+}
+
+// ---- single-pass build (widths <= 4096): a CTA spans the whole row width, so the only
+// carry is the weighted column sum above its band.
+constexpr int kSweepThreads = 256;
+
+__device__ __forceinline__ uint64_t pixel_weight(const uint64_t* __restrict__ wts, int64_t pitch, int dir, int sx,
+                                                 int sy, int x, int y, int w, int h) {
+    if (wts) return __ldg(wts + static_cast<int64_t>(y) * pitch + x);
+    return static_cast<uint64_t>(field_int(dir, x, y, w, h, sx, sy)) << 16;
+}
+
+// T[j][k][x] = sum over the rows of band j of w * [bin == k], bins [kc0, kc0 + kcn); one
+// thread per column (its counters in shared memory, no atomics).
+__global__ void __launch_bounds__(kSweepThreads) wih_band_kernel(const uint16_t* __restrict__ bins, int64_t pitch,
+                                                                 const uint64_t* __restrict__ wts, int dir, int sx,
+                                                                 int sy, int w, int h, int nbins, int band_rows,
+                                                                 int kc0, int kcn, uint64_t* __restrict__ T) {
+    extern __shared__ uint64_t acc[];  // [kcn][256]
+    const int x = blockIdx.x * kSweepThreads + threadIdx.x, j = blockIdx.y;
+    for (int k = 0; k < kcn; ++k) acc[k * kSweepThreads + threadIdx.x] = 0;
+    if (x < w) {
+        const int y0 = j * band_rows, y1 = min(h, y0 + band_rows);
+        for (int y = y0; y < y1; ++y) {
+            const int b = static_cast<int>(__ldg(bins + static_cast<int64_t>(y) * pitch + x)) - kc0;
+            if (static_cast<unsigned>(b) < static_cast<unsigned>(kcn))
+                acc[b * kSweepThreads + threadIdx.x] += pixel_weight(wts, pitch, dir, sx, sy, x, y, w, h);
+        }
+        for (int k = 0; k < kcn; ++k) T[(static_cast<int64_t>(j) * nbins + kc0 + k) * w + x] = acc[k * kSweepThreads + threadIdx.x];
+    }
+}
+
+// In place over bands: T[j] = column sums over rows < y0_{j+1}.
+__global__ void wih_band_prefix_kernel(uint64_t* __restrict__ T, int64_t plane, int nb) {
+    const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+    if (i >= plane) return;
+    uint64_t run = 0;
+    constexpr int U = 8;  // loads in flight
+    for (int j0 = 0; j0 < nb; j0 += U) {
+        uint64_t v[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) v[u] = j0 + u < nb ? T[(j0 + u) * plane + i] : 0;
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+            if (j0 + u < nb) {
+                run += v[u];
+                T[(j0 + u) * plane + i] = run;
+            }
+    }
+}
+
+// Exclusive block scan of NBC values per thread; one barrier (sh double-buffered by the
+// caller's parity).
+template <int NBC>
+__device__ __forceinline__ void block_excl_scan_u64(const uint64_t (&v)[NBC], uint64_t (&e)[NBC], uint64_t* sh) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    uint64_t inc[NBC];
+#pragma unroll
+    for (int k = 0; k < NBC; ++k) inc[k] = v[k];
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1)
+#pragma unroll
+        for (int k = 0; k < NBC; ++k) {
+            const uint64_t t = __shfl_up_sync(0xffffffffu, inc[k], o);
+            if (lane >= o) inc[k] += t;
+        }
+    if (lane == 31)
+#pragma unroll
+        for (int k = 0; k < NBC; ++k) sh[warp * NBC + k] = inc[k];
+    __syncthreads();
+    // lanes 0..7 hold the 8 warp totals: a 3-step scan, then this warp's exclusive base
+#pragma unroll
+    for (int k = 0; k < NBC; ++k) {
+        const uint64_t wt = lane < 8 ? sh[lane * NBC + k] : 0;
+        uint64_t ws = wt;
+#pragma unroll
+        for (int o = 1; o < 8; o <<= 1) {
+            const uint64_t t = __shfl_up_sync(0xffffffffu, ws, o);
+            if (lane >= o) ws += t;
+        }
+        e[k] = __shfl_sync(0xffffffffu, ws - wt, warp) + inc[k] - v[k];
+    }
+}
+
+// CTA = (band, NBC bins); thread t owns columns [t PER, t PER + PER) of every row.
+template <int PER, int NBC>
+__global__ void __launch_bounds__(kSweepThreads) wih_sweep_kernel(const uint16_t* __restrict__ bins, int64_t pitch,
+                                                                  const uint64_t* __restrict__ wts, int dir, int sx,
+                                                                  int sy, spct_wih t, int band_rows,
+                                                                  const uint64_t* __restrict__ C) {
+    __shared__ uint64_t sh[2][8 * NBC];
+    const int j = blockIdx.x, k0 = blockIdx.y * NBC;
+    const int W = t.width, Hh = t.height;
+    const int x0 = threadIdx.x * PER;
+    const int y0 = j * band_rows, y1 = min(Hh, y0 + band_rows);
+    uint64_t V[NBC][PER];
+    {   // the band-top row: row prefix of the column sums above the band
+        uint64_t tot[NBC], e[NBC];
+#pragma unroll
+        for (int k = 0; k < NBC; ++k) {
+            uint64_t run = 0;
+#pragma unroll
+            for (int i = 0; i < PER; ++i) {
+                const int x = x0 + i;
+                if (j > 0 && x < W && k0 + k < t.bins) run += C[(static_cast<int64_t>(j - 1) * t.bins + k0 + k) * W + x];
+                V[k][i] = run;
+            }
+            tot[k] = run;
+        }
+        block_excl_scan_u64<NBC>(tot, e, sh[(y0 + 1) & 1]);  // the parity of row y0 - 1
+#pragma unroll
+        for (int k = 0; k < NBC; ++k)
+#pragma unroll
+            for (int i = 0; i < PER; ++i) V[k][i] += e[k];
+    }
+    // the row's bins arrive one row ahead (one vector load when the row is aligned)
+    const bool vec = PER >= 4 && (pitch % 4) == 0 && (reinterpret_cast<uintptr_t>(bins) & 7) == 0 && x0 + PER <= W;
+    auto load_bins = [&](int y, int (&b)[PER]) {
+        const uint16_t* r = bins + static_cast<int64_t>(y) * pitch + x0;
+        if (vec) {
+#pragma unroll
+            for (int i = 0; i < PER; i += 4) {
+                const uint2 v = __ldg(reinterpret_cast<const uint2*>(r + i));
+                b[i] = v.x & 0xFFFF;
+                b[i + 1] = v.x >> 16;
+                b[i + 2] = v.y & 0xFFFF;
+                b[i + 3] = v.y >> 16;
+            }
+        } else {
+#pragma unroll
+            for (int i = 0; i < PER; ++i) b[i] = x0 + i < W ? static_cast<int>(__ldg(r + i)) : -1;
+        }
+    };
+    int bn[PER];
+    if (y0 < y1) load_bins(y0, bn);
+    for (int y = y0; y < y1; ++y) {
+        int b[PER];
+        uint64_t wv[PER];
+#pragma unroll
+        for (int i = 0; i < PER; ++i) b[i] = bn[i];
+        if (y + 1 < y1) load_bins(y + 1, bn);
+#pragma unroll
+        for (int i = 0; i < PER; ++i) wv[i] = x0 + i < W ? pixel_weight(wts, pitch, dir, sx, sy, x0 + i, y, W, Hh) : 0;
+        uint64_t p[NBC][PER], tot[NBC], e[NBC];
+#pragma unroll
+        for (int k = 0; k < NBC; ++k) {
+            uint64_t run = 0;
+#pragma unroll
+            for (int i = 0; i < PER; ++i) {
+                run += b[i] == k0 + k ? wv[i] : 0;
+                p[k][i] = run;
+            }
+            tot[k] = run;
+        }
+        block_excl_scan_u64<NBC>(tot, e, sh[y & 1]);
+#pragma unroll
+        for (int k = 0; k < NBC; ++k) {
+            if (k0 + k >= t.bins) break;
+            uint64_t* row = t.data + static_cast<int64_t>(k0 + k) * t.plane_pitch + static_cast<int64_t>(y) * t.row_pitch;
+#pragma unroll
+            for (int i = 0; i < PER; ++i) V[k][i] += e[k] + p[k][i];
+            if (PER >= 2 && x0 + PER <= W) {  // 16-byte stores (row pitch is a multiple of 16 cells)
+#pragma unroll
+                for (int i = 0; i < PER; i += 2)
+                    *reinterpret_cast<ulonglong2*>(row + x0 + i) = make_ulonglong2(V[k][i], V[k][i + 1]);
+            } else {
+#pragma unroll
+                for (int i = 0; i < PER; ++i)
+                    if (x0 + i < W) row[x0 + i] = V[k][i];
+            }
+        }
     }
 }
 
@@ -239,6 +413,62 @@ spct_status check_set(const spct_wih* set4, int kw, int kh, QuadSet* s) {
     return SPCT_OK;
 }
 
+template <int PER, int NBC>
+spct_status wih_sweep_launch(const uint16_t* bins, int64_t pitch, const uint64_t* wts, int dir, int sx, int sy,
+                             const spct_wih& t, cudaStream_t s) {
+    // bands: about two waves of 256-thread CTAs (two resident per SM at ~124 registers),
+    // rows >= 16
+    const int groups = static_cast<int>(ceil_div(t.bins, NBC));
+    int sms = 148;
+    {
+        int dev = 0;
+        if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    }
+    const int64_t want = static_cast<int64_t>(sms) * 2 * 2;
+    int nbands = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(t.height / 16, ceil_div(want, groups))));
+    const int band_rows = static_cast<int>(ceil_div(t.height, nbands));
+    nbands = static_cast<int>(ceil_div(t.height, band_rows));
+    uint64_t* C = nullptr;
+    if (nbands > 1) {
+        const int64_t plane = static_cast<int64_t>(t.bins) * t.width;
+        if (auto st = cuda_status(cudaMallocAsync(&C, static_cast<size_t>(nbands - 1) * plane * 8, s), "wih alloc"))
+            return st;
+        const int kc = std::min(t.bins, 64);
+        const size_t smem = static_cast<size_t>(kc) * kSweepThreads * 8;
+        static bool attr = false;
+        if (!attr) {
+            cudaFuncSetAttribute(wih_band_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * kSweepThreads * 8);
+            attr = true;
+        }
+        for (int kc0 = 0; kc0 < t.bins; kc0 += kc) {
+            const int kcn = std::min(kc, t.bins - kc0);
+            wih_band_kernel<<<dim3(static_cast<unsigned>(ceil_div(t.width, kSweepThreads)), nbands - 1), kSweepThreads,
+                              smem, s>>>(bins, pitch, wts, dir, sx, sy, t.width, t.height, t.bins, band_rows, kc0, kcn,
+                                         C);
+        }
+        if (auto st = launch_status("wih_band_kernel")) {
+            cudaFreeAsync(C, s);
+            return st;
+        }
+        wih_band_prefix_kernel<<<blocks_for(plane, 256), 256, 0, s>>>(C, plane, nbands - 1);
+    }
+    wih_sweep_kernel<PER, NBC><<<dim3(nbands, groups), kSweepThreads, 0, s>>>(bins, pitch, wts, dir, sx, sy, t, band_rows,
+                                                                           C);
+    const spct_status st = launch_status("wih_sweep_kernel");
+    if (C) cudaFreeAsync(C, s);
+    return st;
+}
+
+spct_status wih_sweep(const uint16_t* bins, int64_t pitch, const uint64_t* wts, int dir, int sx, int sy,
+                      const spct_wih& t, cudaStream_t s) {
+    const int per = static_cast<int>(ceil_div(t.width, kSweepThreads));
+    if (per <= 1) return wih_sweep_launch<1, 16>(bins, pitch, wts, dir, sx, sy, t, s);
+    if (per <= 2) return wih_sweep_launch<2, 8>(bins, pitch, wts, dir, sx, sy, t, s);
+    if (per <= 4) return wih_sweep_launch<4, 4>(bins, pitch, wts, dir, sx, sy, t, s);
+    if (per <= 8) return wih_sweep_launch<8, 2>(bins, pitch, wts, dir, sx, sy, t, s);
+    return wih_sweep_launch<16, 1>(bins, pitch, wts, dir, sx, sy, t, s);
+}
+
 }  // namespace spct_swih
 
 using namespace spct_swih;
@@ -261,11 +491,14 @@ extern "C" spct_status spct_cu_wih_build(const uint16_t* bins, int64_t pitch, co
         return contract("build_weighted_tensor: need weights or a quadrant field");
     cudaStream_t s = as_stream(stream);
     const int sx = kw >= 3 ? 1 : 0, sy = kh >= 3 ? 1 : 0;
-    wih_row_kernel<<<dim3(out->height, out->bins), 256, 0, s>>>(bins, pitch, weights, field_dir, sx, sy, *out);
-    if (auto st = launch_status("wih_row_kernel")) return st;
-    const int64_t nc = static_cast<int64_t>(out->bins) * out->width;
-    wih_col_kernel<<<blocks_for(nc, 256), 256, 0, s>>>(*out);
-    return launch_status("wih_col_kernel");
+    if (out->width > kSweepThreads * 16) {  // wider than one CTA's row span: row pass + column pass
+        wih_row_kernel<<<dim3(out->height, out->bins), 256, 0, s>>>(bins, pitch, weights, field_dir, sx, sy, *out);
+        if (auto st = launch_status("wih_row_kernel")) return st;
+        const int64_t nc = static_cast<int64_t>(out->bins) * out->width;
+        wih_col_kernel<<<blocks_for(nc, 256), 256, 0, s>>>(*out);
+        return launch_status("wih_col_kernel");
+    }
+    return wih_sweep(bins, pitch, weights, field_dir, sx, sy, *out, s);
 }
 
 extern "C" spct_status spct_cu_wih_export_u64(const spct_wih* t, int k0, int k1, uint64_t* dst, void* stream) {
