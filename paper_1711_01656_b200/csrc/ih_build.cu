@@ -190,16 +190,21 @@ __global__ void quantize_kernel(QuantParams q, uint16_t* __restrict__ out) {
 }
 
 __global__ void binmax_kernel(const uint16_t* __restrict__ bins, int64_t pitch, int w, int h, int* out) {
+    __shared__ int wmax[8];
     int m = 0;
-    const int64_t n = static_cast<int64_t>(w) * h;
-    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
-         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-        const int y = static_cast<int>(i / w), x = static_cast<int>(i % w);
-        m = max(m, static_cast<int>(bins[static_cast<int64_t>(y) * pitch + x]));
+    for (int y = blockIdx.y; y < h; y += gridDim.y) {
+        const uint16_t* row = bins + static_cast<int64_t>(y) * pitch;
+        for (int x = blockIdx.x * blockDim.x + threadIdx.x; x < w; x += gridDim.x * blockDim.x)
+            m = max(m, static_cast<int>(__ldg(row + x)));
     }
 #pragma unroll
     for (int o = 16; o; o >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
-    if ((threadIdx.x & 31) == 0) atomicMax(out, m);
+    if ((threadIdx.x & 31) == 0) wmax[threadIdx.x >> 5] = m;
+    __syncthreads();
+    if (threadIdx.x == 0) {  // one atomic per block
+        for (int i = 1; i < static_cast<int>(blockDim.x >> 5); ++i) m = max(m, wmax[i]);
+        atomicMax(out, m);
+    }
 }
 
 __global__ void export_kernel(spct_ih t, int k0, int k1, uint64_t* __restrict__ dst) {
@@ -287,8 +292,9 @@ extern "C" spct_status spct_cu_binmap_max(const uint16_t* bins, int64_t pitch, i
     cudaStream_t s = as_stream(stream);
     if (auto st = cuda_status(cudaMallocAsync(&d, sizeof(int), s), "binmap_max alloc")) return st;
     cudaMemsetAsync(d, 0, sizeof(int), s);
-    const int64_t n = static_cast<int64_t>(width) * height;
-    binmax_kernel<<<grid_for(n, 256), 256, 0, s>>>(bins, pitch, width, height, d);
+    const unsigned gx = static_cast<unsigned>(std::min<int64_t>(ceil_div(width, 256), 8));
+    const unsigned gy = static_cast<unsigned>(std::min<int64_t>(height, std::max<int64_t>(1, 148 * 8 / gx)));
+    binmax_kernel<<<dim3(gx, gy), 256, 0, s>>>(bins, pitch, width, height, d);
     spct_status st = launch_status("binmap_max");
     int h = 0;
     if (st == SPCT_OK) st = cuda_status(cudaMemcpyAsync(&h, d, sizeof(int), cudaMemcpyDeviceToHost, s), "binmap_max copy");
