@@ -281,8 +281,11 @@ def run_next_rows(P, dev, pk_gbs: float) -> dict:
     out["swih_quadrant_set"] = line(f"{n}x{n} BinMap, {nb} bins, {k}x{k} kernel: four uint64 16.16 tensors", ms_b,
                                     4 * nb * n * n * 8 + n * n * 2)
     ms_m = timed(lambda: P.swih.swlh_distance_map(bm, nb, model, k, k))
-    out["swih_distance_map"] = line("quadrant set + swlh-distance map (float64)", ms_m,
-                                    4 * nb * n * n * 8 + n * n * 2 + n * n * 8)
+    out["swih_distance_map"] = line("swlh-distance map (float64) in one sweep over the BinMap (no tensors; "
+                                    "bound by the FP64 division per window and bin)", ms_m, n * n * 2 + n * n * 8)
+    ms_q = timed(lambda: P.swih.swlh_distance_map(bm, nb, model, k, k, method="quadrant"))
+    out["swih_distance_map_quadrant"] = line("the same map through the quadrant tensors (reference construction)",
+                                             ms_q, 4 * nb * n * n * 8 + n * n * 2 + n * n * 8)
     # 2. map consumers (likelihood.cpp:257-330, tracker.cpp:77-113) at the C3 map size
     m4 = [torch.rand((H_IMG, W_IMG), dtype=torch.float64, device=dev, generator=g) for _ in range(5)]
     fused = torch.empty_like(m4[0])

@@ -201,6 +201,11 @@ spct_status spct_cu_swlh_brute(const uint16_t* bins, int64_t pitch, int width, i
 /* The tracker's swlh-distance map (track_loop.cpp:264-283): model (dev, bins doubles),
  * map (dev, width x height doubles).  Synchronises. */
 spct_status spct_cu_swlh_map(const spct_wih* set4, int kw, int kh, const double* model, double* map, void* stream);
+/* The same map in one sweep over the BinMap (dev uint16, nbins bins), without the quadrant
+ * tensors: exact pyramid-weighted window sums from running column states (swlh_fused.cu),
+ * bit-identical to spct_cu_swlh_map.  kw <= 128, kh <= 255. */
+spct_status spct_cu_swlh_map_direct(const uint16_t* bins, int64_t pitch, int width, int height, int nbins, int kw,
+                                    int kh, const double* model, double* map, void* stream);
 
 /* ----------------------------------------------------------------- joint-IH median (motion.hpp)
  * spct_cu_ih_accumulate: the build of spct_cu_ih_build, added (sign +1) to or subtracted

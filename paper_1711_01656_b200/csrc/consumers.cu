@@ -472,9 +472,9 @@ extern "C" spct_status spct_cu_camshift(const double* map, int w, int h, const d
     cudaStream_t s = as_stream(stream);
     double *dstart = nullptr, *dout = nullptr;
     int32_t* dint = nullptr;
-    spct_status st = cuda_status(cudaMallocAsync(&dstart, 2 * n * sizeof(double), s), "camshift alloc");
-    if (!st) st = cuda_status(cudaMallocAsync(&dout, 2 * n * sizeof(double), s), "camshift alloc");
-    if (!st) st = cuda_status(cudaMallocAsync(&dint, 2 * n * sizeof(int32_t), s), "camshift alloc");
+    spct_status st = cuda_status(malloc_async(&dstart, 2 * n * sizeof(double), s), "camshift alloc");
+    if (!st) st = cuda_status(malloc_async(&dout, 2 * n * sizeof(double), s), "camshift alloc");
+    if (!st) st = cuda_status(malloc_async(&dint, 2 * n * sizeof(int32_t), s), "camshift alloc");
     if (!st) st = cuda_status(cudaMemcpyAsync(dstart, starts, 2 * n * sizeof(double), cudaMemcpyHostToDevice, s), "H2D");
     if (!st) {
         camshift_kernel<<<static_cast<unsigned>(ceil_div(n, 128)), 128, 0, s>>>(map, w, h, dstart, n, win_w, win_h, delta,

@@ -68,7 +68,7 @@ spct_status build_match(const spct_source* src, const spct_ih* out, const double
         // more than one 128-bin group: accumulate the groups' partials, then finalise
         double* part = nullptr;
         const size_t n = static_cast<size_t>(out->width - kw + 1) * (out->height - kh + 1);
-        if (auto st = cuda_status(cudaMallocAsync(&part, n * sizeof(double), s), "ih_build_match_map alloc")) return st;
+        if (auto st = cuda_status(malloc_async(&part, n * sizeof(double), s), "ih_build_match_map alloc")) return st;
         spct_status st = build_match(src, out, tmpl, kw, kh, p, metric, part, nullptr, workspace, workspace_bytes, stream);
         if (st == SPCT_OK) st = spct_cu_hist_finalize(part, out->width, out->height, kw, kh, p, metric, map, stream);
         cudaFreeAsync(part, s);

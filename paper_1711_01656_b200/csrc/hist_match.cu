@@ -259,7 +259,7 @@ extern "C" spct_status spct_cu_hist_match(const spct_ih* t, const double* tmpl, 
     cudaStream_t s = as_stream(stream);
     double* part = nullptr;
     const int64_t n = static_cast<int64_t>(m.nu) * m.nv;
-    if (auto st = cuda_status(cudaMallocAsync(&part, n * sizeof(double), s), "hist_match alloc")) return st;
+    if (auto st = cuda_status(malloc_async(&part, n * sizeof(double), s), "hist_match alloc")) return st;
     spct_status st = spct_cu_hist_partial(t, tmpl, kw, kh, p, metric, part, 0, stream);
     if (st == SPCT_OK) st = spct_cu_hist_finalize(part, t->width, t->height, kw, kh, p, metric, map, stream);
     cudaFreeAsync(part, s);

@@ -290,7 +290,7 @@ extern "C" spct_status spct_cu_binmap_max(const uint16_t* bins, int64_t pitch, i
     if (!bins || !out_max || pitch < width) return contract("binmap_max: bad arguments");
     int* d = nullptr;
     cudaStream_t s = as_stream(stream);
-    if (auto st = cuda_status(cudaMallocAsync(&d, sizeof(int), s), "binmap_max alloc")) return st;
+    if (auto st = cuda_status(malloc_async(&d, sizeof(int), s), "binmap_max alloc")) return st;
     cudaMemsetAsync(d, 0, sizeof(int), s);
     const unsigned gx = static_cast<unsigned>(std::min<int64_t>(ceil_div(width, 256), 8));
     const unsigned gy = static_cast<unsigned>(std::min<int64_t>(height, std::max<int64_t>(1, 148 * 8 / gx)));

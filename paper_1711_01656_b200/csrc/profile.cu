@@ -81,3 +81,26 @@ extern "C" spct_status spct_cu_profile_read(const char* kernel, double* total_ms
     if (launches) *launches = n;
     return SPCT_OK;
 }
+
+namespace spct_impl {
+
+cudaError_t malloc_async(void** p, size_t bytes, cudaStream_t s) {
+    static std::mutex mu;
+    static bool done[64] = {};
+    int dev = 0;
+    if (cudaGetDevice(&dev) == cudaSuccess && dev >= 0 && dev < 64) {
+        std::lock_guard<std::mutex> lock(mu);
+        if (!done[dev]) {
+            cudaMemPool_t pool;
+            if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+                uint64_t keep = ~0ull;
+                cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+            }
+            cudaGetLastError();
+            done[dev] = true;
+        }
+    }
+    return cudaMallocAsync(p, bytes, s);
+}
+
+}  // namespace spct_impl

@@ -37,6 +37,15 @@ inline spct_status launch_status(const char* where) {
 
 inline cudaStream_t as_stream(void* s) { return static_cast<cudaStream_t>(s); }
 
+// Stream-ordered scratch allocation (profile.cu): cudaMallocAsync from the device's default
+// pool, which is set once per device to keep freed memory (no release threshold), so
+// repeated calls reuse it instead of going back to the driver.
+cudaError_t malloc_async(void** p, size_t bytes, cudaStream_t s);
+template <class T>
+cudaError_t malloc_async(T** p, size_t bytes, cudaStream_t s) {
+    return malloc_async(reinterpret_cast<void**>(p), bytes, s);
+}
+
 inline int64_t round_up(int64_t v, int64_t m) { return (v + m - 1) / m * m; }
 inline int64_t ceil_div(int64_t v, int64_t m) { return (v + m - 1) / m; }
 

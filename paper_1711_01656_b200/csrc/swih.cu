@@ -431,7 +431,7 @@ spct_status wih_sweep_launch(const uint16_t* bins, int64_t pitch, const uint64_t
     uint64_t* C = nullptr;
     if (nbands > 1) {
         const int64_t plane = static_cast<int64_t>(t.bins) * t.width;
-        if (auto st = cuda_status(cudaMallocAsync(&C, static_cast<size_t>(nbands - 1) * plane * 8, s), "wih alloc"))
+        if (auto st = cuda_status(malloc_async(&C, static_cast<size_t>(nbands - 1) * plane * 8, s), "wih alloc"))
             return st;
         const int kc = std::min(t.bins, 64);
         const size_t smem = static_cast<size_t>(kc) * kSweepThreads * 8;
@@ -536,7 +536,7 @@ extern "C" spct_status spct_cu_swlh_query(const spct_wih* set4, int kw, int kh, 
     cudaStream_t st = as_stream(stream);
     int32_t* dc = nullptr;
     unsigned* bad = nullptr;
-    spct_status r = cuda_status(cudaMallocAsync(&dc, 8 * static_cast<size_t>(n) + 16, st), "swlh alloc");
+    spct_status r = cuda_status(malloc_async(&dc, 8 * static_cast<size_t>(n) + 16, st), "swlh alloc");
     if (!r) {
         bad = reinterpret_cast<unsigned*>(dc + 2 * n);
         cudaMemsetAsync(bad, 0, 4, st);
@@ -569,7 +569,7 @@ extern "C" spct_status spct_cu_swlh_brute(const uint16_t* bins, int64_t pitch, i
     if (n == 0) return SPCT_OK;
     cudaStream_t st = as_stream(stream);
     int32_t* dc = nullptr;
-    spct_status r = cuda_status(cudaMallocAsync(&dc, 8 * static_cast<size_t>(n), st), "swlh alloc");
+    spct_status r = cuda_status(malloc_async(&dc, 8 * static_cast<size_t>(n), st), "swlh alloc");
     if (!r) r = cuda_status(cudaMemcpyAsync(dc, centres_host, 8 * static_cast<size_t>(n), cudaMemcpyHostToDevice, st), "H2D");
     if (!r) {
         swlh_brute_kernel<<<n, 128, 0, st>>>(bins, pitch, nbins, kw, kh, dc, n, out);
@@ -598,7 +598,7 @@ extern "C" spct_status spct_cu_swlh_map(const spct_wih* set4, int kw, int kh, co
     for (int dy = -e.syt; dy < e.syb; ++dy)
         for (int dx = -e.sxl; dx < e.sxr; ++dx) mass += e.c - std::abs(dx) - std::abs(dy);
     unsigned* bad = nullptr;
-    spct_status r = cuda_status(cudaMallocAsync(&bad, 4, st), "swlh alloc");
+    spct_status r = cuda_status(malloc_async(&bad, 4, st), "swlh alloc");
     if (!r) r = cuda_status(cudaMemsetAsync(bad, 0, 4, st), "memset");
     if (!r) {
         const int64_t nc = static_cast<int64_t>(W - kw + 1) * (Hh - kh + 1);

@@ -139,8 +139,24 @@ def brute_force_swlh_fixed(bm, nbins: int, centres, kw: int, kh: int, stream=Non
     return out.cpu().numpy()
 
 
-def swlh_distance_map(bm, nbins: int, model, kw: int, kh: int, stream=None) -> torch.Tensor:
-    """The tracker's swlh-distance likelihood map (track_loop.cpp:264-283), (h, w) float64."""
+def swlh_distance_map(bm, nbins: int, model, kw: int, kh: int, stream=None, method: str = "direct") -> torch.Tensor:
+    """The tracker's swlh-distance likelihood map (track_loop.cpp:264-283), (h, w) float64.
+
+    method "direct" (kw <= 128, kh <= 255): one sweep over the BinMap with exact running
+    pyramid sums (swlh_fused.cu); "quadrant": the reference's construction, the four
+    weighted tensors of build_quadrant_set then a query per centre.  Same bits."""
+    if method not in ("direct", "quadrant"):
+        raise ContractError(A.SPCT_ERR_CONTRACT, "swlh_map: method must be 'direct' or 'quadrant'")
+    if method == "direct" and kw <= 128 and kh <= 255:
+        kernel_extents(kw, kh)
+        b = _binmap(bm, nbins)
+        h, w = b.shape
+        md = torch.from_numpy(np.ascontiguousarray(model, np.float64).reshape(-1)).to(b.device)
+        if md.numel() != nbins:
+            raise ContractError(A.SPCT_ERR_CONTRACT, "swlh_map: model length must equal bins")
+        out = torch.empty((h, w), dtype=torch.float64, device=b.device)
+        check(A.lib().spct_cu_swlh_map_direct(_ptr(b), w, w, h, nbins, kw, kh, _ptr(md), _ptr(out), _stream(stream)))
+        return out
     s = build_quadrant_set(bm, nbins, kw, kh, stream)
     md = torch.from_numpy(np.ascontiguousarray(model, np.float64).reshape(-1)).to(s.tensors[0].storage.device)
     if md.numel() != nbins:

@@ -641,11 +641,29 @@ def test_swlh_distance_map(P, kw, kh, w, h):
         model = oracle.swlh(bm, nb, w // 2, h // 2, kw, kh)
     else:
         model = np.full(nb, 1.0 / nb)
-    got = P.swih.swlh_distance_map(bm, nb, model, kw, kh).cpu().numpy()
     want = oracle.swlh_map(bm, nb, model, kw, kh)
-    assert close(got, want)
+    quad = P.swih.swlh_distance_map(bm, nb, model, kw, kh, method="quadrant").cpu().numpy()
+    assert close(quad, want)
+    got = P.swih.swlh_distance_map(bm, nb, model, kw, kh).cpu().numpy()
+    assert np.array_equal(got, quad)  # the direct sweep reproduces the quadrant path bit for bit
     if w >= kw and h >= kh:
         assert got[h // 2, w // 2] == 1.0
+
+
+@pytest.mark.parametrize("w,h,nb,kw,kh", [(300, 170, 32, 31, 31), (260, 150, 70, 17, 40), (140, 300, 5, 128, 9),
+                                           (129, 130, 16, 2, 255), (64, 40, 33, 1, 1), (200, 90, 8, 64, 64)])
+def test_swlh_direct_map_matches_quadrant_path(P, w, h, nb, kw, kh):
+    """The single-sweep swlh map (many bands, several bin groups, kernel extremes) equals
+    the quadrant-tensor path exactly."""
+    rng = np.random.default_rng(w * h + kw)
+    bm = rng.integers(0, nb, (h, w)).astype(np.uint16)
+    model = rng.random(nb)
+    model /= model.sum()
+    if h < kh:
+        return
+    quad = P.swih.swlh_distance_map(bm, nb, model, kw, kh, method="quadrant").cpu().numpy()
+    got = P.swih.swlh_distance_map(bm, nb, model, kw, kh).cpu().numpy()
+    assert np.array_equal(got, quad)
 
 
 # ------------------------------------------------------------------ joint-IH median (§8(f) #4)
