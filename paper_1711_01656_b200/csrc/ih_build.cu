@@ -248,8 +248,11 @@ int build_ctas_per_sm(int B, int threads) {
 }
 
 BuildPlan plan_build_sweep(int width, int height, int bins) {
-    const BuildPlan probe = plan_build(width, height, bins, 0, 2, 32);
-    return plan_build(width, height, bins, 0, build_ctas_per_sm(probe.B, 32 * probe.warps), 32);
+    // Small histograms: fewer bins per warp so a CTA still has ~4 warps (16 bins as one
+    // 16-bin warp left a single warp per strip and band, far too little to hide latency).
+    const int B = bins >= 64 ? 16 : (bins >= 32 ? 8 : 4);
+    const BuildPlan probe = plan_build(width, height, bins, B, 2, 32);
+    return plan_build(width, height, bins, B, build_ctas_per_sm(probe.B, 32 * probe.warps), 32);
 }
 
 BuildPlan plan_fused_sweep(int width, int height, int bins) {
