@@ -1,9 +1,9 @@
-"""The bin-slab reduce over peer memory (PeerSlabReduce, peer.cu) with two ranks.
+"""The bin-slab reduce over peer memory (PeerSlabReduce, peer.cu) with two and three ranks.
 
 Both ranks run on cuda:0 (the GPU boxes of this run have one GPU): the IPC mappings,
 the cross-process flags and the slot double-buffering are the same code as across
-GPUs, only the NVLink hop is missing.  Rank 1's sweep writes its slab's partial map
-into rank 0's slot buffer; rank 0 finalises.  Over several epochs (frames) the map
+GPUs, only the NVLink hop is missing.  Ranks >= 1 write their slabs' partial maps into
+rank 0's slot buffer; rank 0 finalises.  Over several epochs (frames) the map
 must equal the single-GPU map of the full histogram (FP64, slab-sum rounding only).
 """
 import os
@@ -65,12 +65,12 @@ def _worker(rank, world, port, out_path, nbins, kw, kh, p):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("nbins,kw,kh,p", [(64, 33, 21, 1.0), (40, 16, 16, 2.0)])
-def test_peer_slab_reduce_two_ranks(tmp_path, nbins, kw, kh, p):
+@pytest.mark.parametrize("world,nbins,kw,kh,p", [(2, 64, 33, 21, 1.0), (2, 40, 16, 16, 2.0), (3, 50, 20, 9, 1.0)])
+def test_peer_slab_reduce(tmp_path, world, nbins, kw, kh, p):
     import torch.multiprocessing as mp
 
     out = str(tmp_path / "maps.npy")
-    mp.spawn(_worker, args=(2, _free_port(), out, nbins, kw, kh, p), nprocs=2, join=True)
+    mp.spawn(_worker, args=(world, _free_port(), out, nbins, kw, kh, p), nprocs=world, join=True)
     got, want = np.load(out)
     assert got.shape == want.shape
     err = np.abs(got - want)
