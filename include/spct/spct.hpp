@@ -129,6 +129,7 @@ public:
     bool operator==(const HostMirror& o) const;
     bool operator==(const std::vector<std::uint64_t>& o) const;
     void clear();
+    bool mirrored() const { return valid_; }  // the host copy is filled (non-reference addition)
 
     std::shared_ptr<DeviceTensor> dev;  // null for a default-constructed tensor
 private:

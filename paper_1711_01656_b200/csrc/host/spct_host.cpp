@@ -80,6 +80,10 @@ struct DeviceTensor {
     // window counts from it (1 B/px) instead of re-reading b*H*W*4 tensor bytes.
     spct_source src{};
     std::unique_ptr<DevBuf> src_mem;
+    // region queries: a reusable device buffer, and a count that switches small tensors to
+    // answering from the host mirror (the reference's own arithmetic) after a few queries
+    std::unique_ptr<DevBuf> qbuf;
+    int queries = 0;
 };
 
 std::size_t HostMirror::size() const {
@@ -290,27 +294,50 @@ const spct_ih& desc_of(const IntegralHistogramTensor& t) {
 }
 }  // namespace
 
+namespace {
+// Mirrors of at most this many cells (256 MiB of uint64) are filled after kQueriesBeforeMirror
+// device round trips; later queries read the host copy like the reference does.
+constexpr std::size_t kMirrorCells = std::size_t(32) << 20;
+constexpr int kQueriesBeforeMirror = 16;
+
+std::vector<std::uint64_t> region_from_mirror(const IntegralHistogramTensor& t, const Rect& r) {
+    std::vector<std::uint64_t> out(t.bins);
+    const std::uint64_t* d = t.data.data();
+    const std::size_t ps = t.plane_stride(), rs = t.row_stride();
+    const std::size_t y1 = r.y, y2 = std::size_t(r.y) + r.h, x1 = r.x, x2 = std::size_t(r.x) + r.w;
+    for (int k = 0; k < t.bins; ++k) {  // integral.cpp:569-577, uint64 wrap arithmetic
+        const std::uint64_t* pl = d + std::size_t(k) * ps;
+        out[k] = pl[y2 * rs + x2] - pl[y1 * rs + x2] - pl[y2 * rs + x1] + pl[y1 * rs + x1];
+    }
+    return out;
+}
+}  // namespace
+
 std::vector<std::uint64_t> region_histogram(const IntegralHistogramTensor& t, const Rect& r) {
     require(r.w >= 0 && r.h >= 0, "region_histogram: negative extent");       // integral.cpp:562
     require(r.inside(t.width, t.height), "region_histogram: rect outside image");  // :563
-    if (t.data.dev && t.data.dev->weighted) {
-        const spct_wih& w = t.data.dev->wdesc;
-        DevBuf rect(16), out(std::size_t(t.bins) * 8);
-        const std::int32_t rr[4] = {r.x, r.y, r.w, r.h};
-        cuda(cudaMemcpy(rect.p, rr, 16, cudaMemcpyHostToDevice), "H2D");
-        check(spct_cu_wih_region_counts(&w, rect.as<std::int32_t>(), 1, out.as<std::uint64_t>(), nullptr));
-        std::vector<std::uint64_t> h(t.bins);
-        cuda(cudaMemcpy(h.data(), out.p, h.size() * 8, cudaMemcpyDeviceToHost), "D2H");
-        return h;
-    }
-    const spct_ih& d = desc_of(t);
-    DevBuf rect(16), out(std::size_t(t.bins) * 4);
+    detail::DeviceTensor* dt = t.data.dev.get();
+    if (!dt || t.data.mirrored()) return region_from_mirror(t, r);
+    if (++dt->queries > kQueriesBeforeMirror && t.data.size() <= kMirrorCells) return region_from_mirror(t, r);
+    const std::size_t cell = dt->weighted ? 8 : 4;
+    if (!dt->qbuf) dt->qbuf = std::make_unique<DevBuf>(16 + std::size_t(t.bins) * 8);
+    auto* rect = dt->qbuf->as<std::int32_t>();
+    void* out = dt->qbuf->as<char>() + 16;
     const std::int32_t rr[4] = {r.x, r.y, r.w, r.h};
-    cuda(cudaMemcpy(rect.p, rr, 16, cudaMemcpyHostToDevice), "H2D");
-    check(spct_cu_region_counts(&d, rect.as<std::int32_t>(), 1, out.as<std::uint32_t>(), nullptr));
-    std::vector<std::uint32_t> h32(t.bins);
-    cuda(cudaMemcpy(h32.data(), out.p, h32.size() * 4, cudaMemcpyDeviceToHost), "D2H");
-    return std::vector<std::uint64_t>(h32.begin(), h32.end());
+    cuda(cudaMemcpy(rect, rr, 16, cudaMemcpyHostToDevice), "H2D");
+    if (dt->weighted)
+        check(spct_cu_wih_region_counts(&dt->wdesc, rect, 1, static_cast<std::uint64_t*>(out), nullptr));
+    else
+        check(spct_cu_region_counts(&desc_of(t), rect, 1, static_cast<std::uint32_t*>(out), nullptr));
+    std::vector<std::uint64_t> h(t.bins);
+    if (cell == 8) {
+        cuda(cudaMemcpy(h.data(), out, h.size() * 8, cudaMemcpyDeviceToHost), "D2H");
+    } else {
+        std::vector<std::uint32_t> h32(t.bins);
+        cuda(cudaMemcpy(h32.data(), out, h32.size() * 4, cudaMemcpyDeviceToHost), "D2H");
+        std::copy(h32.begin(), h32.end(), h.begin());
+    }
+    return h;
 }
 
 std::uint64_t region_count(const IntegralHistogramTensor& t, int bin, const Rect& r) {
