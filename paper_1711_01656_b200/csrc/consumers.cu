@@ -9,8 +9,8 @@
 //                                            margin, deterministic row-major compaction, then
 //                                            a stable LSD radix sort by height (descending)
 //   score_map        likelihood.cpp:324-330  rank of the best peak inside gt (k + 1 if none)
-//   camshift_refine  tracker.cpp:77-113      one thread per start point, the reference's
-//                                            sequential window sums (same rounding)
+//   camshift_refine  tracker.cpp:77-113      one warp per start point; the three window
+//                                            sums stay sequential chains (same rounding)
 // All results are bit-identical to the reference (no reassociation, no FMA contraction).
 #include <cmath>
 #include <vector>
@@ -257,10 +257,20 @@ __global__ void score_kernel(const uint32_t* __restrict__ idx, int64_t n, int w,
 
 // ---------------------------------------------------------------- camshift_refine
 
-__global__ void camshift_kernel(const double* __restrict__ map, int w, int h, const double* __restrict__ starts,
-                                int n, int win_w, int win_h, double delta, int max_iter, double* __restrict__ out,
-                                int32_t* __restrict__ iters, int32_t* __restrict__ zero_mass) {
-    const int q = blockIdx.x * blockDim.x + threadIdx.x;
+// camshift_refine (tracker.cpp:77-113) for n start points, one warp per start: the warp
+// streams the window in 32-pixel chunks through shared memory (the next chunk's loads in
+// flight while the current one is summed) and
+// lanes 0, 1, 2 run the three sums m00, m10, m01 — each still one sequential chain in the
+// reference's row-major order, so every bit matches.
+constexpr int kCamWarps = 4;
+
+__global__ void __launch_bounds__(32 * kCamWarps) camshift_warp_kernel(
+    const double* __restrict__ map, int w, int h, const double* __restrict__ starts, int n, int win_w, int win_h,
+    double delta, int max_iter, double* __restrict__ out, int32_t* __restrict__ iters, int32_t* __restrict__ zero_mass) {
+    __shared__ double buf[kCamWarps][2][32];
+    __shared__ double mom[kCamWarps][3];
+    const int lane = threadIdx.x & 31, wi = threadIdx.x >> 5;
+    const int q = blockIdx.x * kCamWarps + wi;
     if (q >= n) return;
     double cx = starts[2 * q], cy = starts[2 * q + 1];
     int it_done = 0, zm = 0;
@@ -268,14 +278,35 @@ __global__ void camshift_kernel(const double* __restrict__ map, int w, int h, co
         const int x0 = static_cast<int>(llround(__dsub_rn(cx, (win_w - 1) / 2.0)));
         const int y0 = static_cast<int>(llround(__dsub_rn(cy, (win_h - 1) / 2.0)));
         const int xa = max(x0, 0), ya = max(y0, 0), xb = min(x0 + win_w, w), yb = min(y0 + win_h, h);
-        double m00 = 0.0, m10 = 0.0, m01 = 0.0;
-        for (int y = ya; y < yb; ++y)
-            for (int x = xa; x < xb; ++x) {
-                const double p = map[static_cast<int64_t>(y) * w + x];
-                m00 = __dadd_rn(m00, p);
-                m10 = __dadd_rn(m10, __dmul_rn(static_cast<double>(x), p));
-                m01 = __dadd_rn(m01, __dmul_rn(static_cast<double>(y), p));
+        const int rw = max(0, xb - xa), nch = (rw + 31) / 32;
+        const int64_t total = static_cast<int64_t>(max(0, yb - ya)) * nch;  // chunks, row-major
+        double acc = 0.0;  // lane 0: m00, lane 1: m10, lane 2: m01
+        auto load = [&](int64_t c) {
+            const int y = ya + static_cast<int>(c / nch), x = xa + static_cast<int>(c % nch) * 32 + lane;
+            return x < xb ? __ldg(map + static_cast<int64_t>(y) * w + x) : 0.0;
+        };
+        double nxt = total > 0 ? load(0) : 0.0;
+        for (int64_t c = 0; c < total; ++c) {
+            buf[wi][c & 1][lane] = nxt;
+            __syncwarp();
+            if (c + 1 < total) nxt = load(c + 1);
+            if (lane < 3) {
+                const int y = ya + static_cast<int>(c / nch), xs = xa + static_cast<int>(c % nch) * 32;
+                const int m = min(32, xb - xs);
+                const double* b = buf[wi][c & 1];
+                if (lane == 0)
+                    for (int i = 0; i < m; ++i) acc = __dadd_rn(acc, b[i]);
+                else if (lane == 1)
+                    for (int i = 0; i < m; ++i) acc = __dadd_rn(acc, __dmul_rn(static_cast<double>(xs + i), b[i]));
+                else
+                    for (int i = 0; i < m; ++i) acc = __dadd_rn(acc, __dmul_rn(static_cast<double>(y), b[i]));
             }
+            __syncwarp();
+        }
+        if (lane < 3) mom[wi][lane] = acc;
+        __syncwarp();
+        const double m00 = mom[wi][0], m10 = mom[wi][1], m01 = mom[wi][2];
+        __syncwarp();
         if (m00 <= 0.0) {
             zm = 1;
             break;
@@ -287,10 +318,12 @@ __global__ void camshift_kernel(const double* __restrict__ map, int w, int h, co
         ++it_done;
         if (d < delta) break;
     }
-    out[2 * q] = cx;
-    out[2 * q + 1] = cy;
-    iters[q] = it_done;
-    zero_mass[q] = zm;
+    if (lane == 0) {
+        out[2 * q] = cx;
+        out[2 * q + 1] = cy;
+        iters[q] = it_done;
+        zero_mass[q] = zm;
+    }
 }
 
 int grid1(int64_t n) { return static_cast<int>(std::min<int64_t>(std::max<int64_t>((n + 255) / 256, 1), 148 * 16)); }
@@ -477,9 +510,9 @@ extern "C" spct_status spct_cu_camshift(const double* map, int w, int h, const d
     if (!st) st = cuda_status(malloc_async(&dint, 2 * n * sizeof(int32_t), s), "camshift alloc");
     if (!st) st = cuda_status(cudaMemcpyAsync(dstart, starts, 2 * n * sizeof(double), cudaMemcpyHostToDevice, s), "H2D");
     if (!st) {
-        camshift_kernel<<<static_cast<unsigned>(ceil_div(n, 128)), 128, 0, s>>>(map, w, h, dstart, n, win_w, win_h, delta,
-                                                                               max_iter, dout, dint, dint + n);
-        st = launch_status("camshift_kernel");
+        camshift_warp_kernel<<<static_cast<unsigned>(ceil_div(n, kCamWarps)), 32 * kCamWarps, 0, s>>>(
+            map, w, h, dstart, n, win_w, win_h, delta, max_iter, dout, dint, dint + n);
+        st = launch_status("camshift_warp_kernel");
     }
     if (!st) st = cuda_status(cudaMemcpyAsync(out, dout, 2 * n * sizeof(double), cudaMemcpyDeviceToHost, s), "D2H");
     if (!st) st = cuda_status(cudaMemcpyAsync(iterations, dint, n * sizeof(int32_t), cudaMemcpyDeviceToHost, s), "D2H");
