@@ -8,7 +8,8 @@
 //                                            strict 8-neighbour maxima with the 1e-9 flat
 //                                            margin, deterministic row-major compaction, then
 //                                            a stable LSD radix sort by height (descending)
-//   score_map        likelihood.cpp:324-330  rank of the best peak inside gt (k + 1 if none)
+//   score_map        likelihood.cpp:332-339  rank of the best peak inside gt (k + 1 if none),
+//                                            counted without sorting
 //   camshift_refine  tracker.cpp:77-113      one warp per start point; the three window
 //                                            sums stay sequential chains (same rounding)
 // All results are bit-identical to the reference (no reassociation, no FMA contraction).
@@ -245,14 +246,50 @@ __global__ void peak_gather_kernel(const uint32_t* __restrict__ idx, const doubl
 }
 
 // First sorted position whose peak lies inside gt (min over a device counter).
-__global__ void score_kernel(const uint32_t* __restrict__ idx, int64_t n, int w, int gx, int gy, int gw, int gh,
-                             unsigned* __restrict__ best) {
+// score_map without the sort: the first in-rect peak of the sorted list is the in-rect
+// peak with the smallest (descending-height key, index) — stable_sort keeps row-major
+// order among equal heights — and its rank is 1 + the number of peaks before it in that
+// order (or, with no peak in the rect, the peak count + 1).
+__global__ void rect_best_key_kernel(const double* __restrict__ s, int w, int h, int gx, int gy, int gw, int gh,
+                                     unsigned long long* __restrict__ best_key) {
+    const int64_t n = static_cast<int64_t>(gw) * gh;
+    for (int64_t j = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; j < n;
+         j += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int64_t i = static_cast<int64_t>(gy + j / gw) * w + gx + j % gw;
+        if (is_peak(s, w, h, i)) atomicMin(best_key, static_cast<unsigned long long>(desc_key(s[i])));
+    }
+}
+
+__global__ void rect_best_idx_kernel(const double* __restrict__ s, int w, int h, int gx, int gy, int gw, int gh,
+                                     const unsigned long long* __restrict__ best_key, unsigned* __restrict__ best_idx) {
+    const int64_t n = static_cast<int64_t>(gw) * gh;
+    const unsigned long long bk = *best_key;
+    for (int64_t j = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; j < n;
+         j += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int64_t i = static_cast<int64_t>(gy + j / gw) * w + gx + j % gw;
+        if (desc_key(s[i]) == bk && is_peak(s, w, h, i)) atomicMin(best_idx, static_cast<unsigned>(i));
+    }
+}
+
+// found: count the peaks ordered before (best_key, best_idx); else count every peak.
+__global__ void __launch_bounds__(256) rank_count_kernel(const double* __restrict__ s, int w, int h,
+                                                         const unsigned* __restrict__ best_idx,
+                                                         const unsigned long long* __restrict__ best_key,
+                                                         unsigned long long* __restrict__ count) {
+    const int64_t n = static_cast<int64_t>(w) * h;
+    const unsigned bi = *best_idx;
+    const bool found = bi != 0xFFFFFFFFu;
+    const unsigned long long bk = *best_key;
+    unsigned c = 0;
     for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
          i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-        const uint32_t p = idx[i];
-        const int x = static_cast<int>(p % static_cast<uint32_t>(w)), y = static_cast<int>(p / static_cast<uint32_t>(w));
-        if (x >= gx && x < gx + gw && y >= gy && y < gy + gh) atomicMin(best, static_cast<unsigned>(i));
+        if (!is_peak(s, w, h, i)) continue;
+        const unsigned long long k = desc_key(s[i]);
+        c += !found || k < bk || (k == bk && static_cast<unsigned>(i) < bi);
     }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+    if ((threadIdx.x & 31) == 0 && c) atomicAdd(count, static_cast<unsigned long long>(c));
 }
 
 // ---------------------------------------------------------------- camshift_refine
@@ -469,22 +506,30 @@ extern "C" spct_status spct_cu_find_peaks(const double* map, int w, int h, int32
 
 extern "C" spct_status spct_cu_score_map(const double* map, int w, int h, int gx, int gy, int gw, int gh, int64_t* rank,
                                          void* workspace, size_t workspace_bytes, void* stream) {
-    if (!(gw > 0 && gh > 0 && gx >= 0 && gy >= 0 && gx + gw <= w && gy + gh <= h))  // likelihood.cpp:325-326
+    if (!(gw > 0 && gh > 0 && gx >= 0 && gy >= 0 && gx + gw <= w && gy + gh <= h))  // likelihood.cpp:333-334
         return contract("score_map: ground truth rect must lie inside the map");
     if (!map || !rank) return contract("score_map: bad arguments");
+    int64_t nbp, nbs;
+    if (!workspace || workspace_bytes < peak_ws_bytes(w, h, &nbp, &nbs)) return contract("find_peaks: workspace too small");
     cudaStream_t s = as_stream(stream);
-    PeakWs P;
-    int64_t m = 0;
-    if (auto st = sorted_peaks(map, w, h, workspace, workspace_bytes, s, &P, &m)) return st;
-    unsigned best = 0xFFFFFFFFu;
-    if (m > 0) {
-        cudaMemcpyAsync(P.scalars + 1, &best, 4, cudaMemcpyHostToDevice, s);
-        score_kernel<<<grid1(m), 256, 0, s>>>(P.v[0], m, w, gx, gy, gw, gh, P.scalars + 1);
-        if (auto st = launch_status("score_kernel")) return st;
-        if (auto st = cuda_status(cudaMemcpyAsync(&best, P.scalars + 1, 4, cudaMemcpyDeviceToHost, s), "score")) return st;
-        if (auto st = cuda_status(cudaStreamSynchronize(s), "score_map")) return st;
-    }
-    *rank = best == 0xFFFFFFFFu ? m + 1 : static_cast<int64_t>(best) + 1;
+    PeakWs P = carve(workspace, w, h);
+    const int64_t n = static_cast<int64_t>(w) * h;
+    // scalars: [0..1] best key (u64), [2] best index, [4..5] count (u64)
+    unsigned long long* bk = reinterpret_cast<unsigned long long*>(P.scalars);
+    unsigned* bi = P.scalars + 2;
+    unsigned long long* cnt = reinterpret_cast<unsigned long long*>(P.scalars + 4);
+    cudaMemsetAsync(P.scalars, 0xFF, 12, s);  // key and index: "none"
+    cudaMemsetAsync(cnt, 0, 8, s);
+    smooth3_kernel<<<grid1(n), 256, 0, s>>>(map, w, h, P.s);
+    const int64_t nr = static_cast<int64_t>(gw) * gh;
+    rect_best_key_kernel<<<grid1(nr), 256, 0, s>>>(P.s, w, h, gx, gy, gw, gh, bk);
+    rect_best_idx_kernel<<<grid1(nr), 256, 0, s>>>(P.s, w, h, gx, gy, gw, gh, bk, bi);
+    rank_count_kernel<<<grid1(n), 256, 0, s>>>(P.s, w, h, bi, bk, cnt);
+    if (auto st = launch_status("score_map")) return st;
+    unsigned long long c = 0;
+    if (auto st = cuda_status(cudaMemcpyAsync(&c, cnt, 8, cudaMemcpyDeviceToHost, s), "score")) return st;
+    if (auto st = cuda_status(cudaStreamSynchronize(s), "score_map")) return st;
+    *rank = static_cast<int64_t>(c) + 1;
     return SPCT_OK;
 }
 

@@ -568,6 +568,19 @@ def test_find_peaks_and_score_bit_exact(P, seed):
             assert P.score_map(torch.from_numpy(m).cuda(), *g) == oracle.score_map(m, *g)
 
 
+def test_score_map_ties_and_empty_rects(P):
+    """Equal-height peaks rank in row-major order (stable_sort, likelihood.cpp:319-321);
+    a rect without a peak scores peak count + 1 (:337-338)."""
+    m = np.zeros((90, 120))
+    bumps = [(20, 10), (90, 10), (20, 60), (90, 60), (55, 35)]
+    for i, (x, y) in enumerate(bumps):
+        m[y - 2:y + 3, x - 2:x + 3] = 0.5 if i < 4 else 0.25
+    md = torch.from_numpy(m).cuda()
+    for g in [(85, 5, 10, 10), (15, 55, 10, 10), (50, 30, 10, 10), (0, 80, 120, 10), (100, 40, 20, 5),
+              (0, 0, 120, 90)]:
+        assert P.score_map(md, *g) == oracle.score_map(m, *g), g
+
+
 def test_camshift_bit_exact(P):
     maps = _consumer_maps(6)
     rng = np.random.default_rng(6)
