@@ -156,10 +156,28 @@ __global__ void __launch_bounds__(256) ih_sweep_kernel(QuantParams q, PixelMode 
                  Lb, y1 - y0};
     lt.start();
 
+    // accumulate modes read-modify-write the tensor: its cells of row y + 1 are loaded
+    // during row y (B x 16 bytes per lane; only the B <= 8 plans use these modes cheaply)
+    constexpr int NPRE = MODE != 0 ? B : 1;
+    uint4 pre[NPRE], pnx[NPRE];
+    auto load_row = [&](int y, uint4 (&d)[NPRE]) {
+        const uint32_t* r = base_ptr + static_cast<int64_t>(y) * out.row_pitch;
+#pragma unroll
+        for (int k = 0; k < NPRE; ++k)
+            d[k] = (store_mask & (1u << k)) ? *reinterpret_cast<const uint4*>(r + static_cast<int64_t>(k) * out.plane_pitch)
+                                            : make_uint4(0, 0, 0, 0);
+    };
+    if (MODE != 0 && y0 < y1) load_row(y0, pnx);
+
     uint32_t nxt = load_bins4_raw(q, pm, x0, y0, k0, B);
     for (int y = y0; y < y1; ++y) {
         const uint32_t cur = decode_bins4(pm, nxt);
         if (y + 1 < y1) nxt = load_bins4_raw(q, pm, x0, y + 1, k0, B);
+        if (MODE != 0) {
+#pragma unroll
+            for (int k = 0; k < NPRE; ++k) pre[k] = pnx[k];
+            if (y + 1 < y1) load_row(y + 1, pnx);
+        }
         uint32_t t4[4];
         onehot_shifts(cur ^ kpat0, t4);
         lt.row(y - y0);
@@ -167,7 +185,7 @@ __global__ void __launch_bounds__(256) ih_sweep_kernel(QuantParams q, PixelMode 
 #pragma unroll
         for (int g = 0; g < B / 4; ++g)
             vpart_group_q<B, MODE>(V, g, t4, lt.group(y - y0, g), prow + static_cast<int64_t>(4 * g) * out.plane_pitch,
-                                   out.plane_pitch, store_mask);
+                                   out.plane_pitch, store_mask, MODE != 0 ? pre + 4 * g : nullptr);
     }
 }
 

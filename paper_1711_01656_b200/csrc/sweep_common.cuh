@@ -138,9 +138,10 @@ __device__ __forceinline__ void onehot_shifts(uint32_t dbins, uint32_t (&t)[4]) 
 // that the cross-lane scan needs.  `p` points at plane 4g of the row.
 // MODE 0 stores the row; 1 / 2 add / subtract it into the tensor already there (the joint
 // integral histogram of a frame window, motion.cpp:51-60).
+// `pre` (MODE 1 / 2): the group's four tensor cells of this row, loaded a row ahead.
 template <int B, int MODE = 0>
 __device__ __forceinline__ void vpart_group_q(uint32_t (&V)[4][B], int g, const uint32_t (&t)[4], uint4 L, uint32_t* p,
-                                              int64_t plane_pitch, uint32_t store_mask) {
+                                              int64_t plane_pitch, uint32_t store_mask, const uint4* pre = nullptr) {
     uint32_t Q[4];
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
@@ -162,7 +163,7 @@ __device__ __forceinline__ void vpart_group_q(uint32_t (&V)[4][B], int g, const 
         if (MODE == 0) {
             st_cs_v4_pred(store_mask & (1u << k), p, V[0][k], V[1][k], V[2][k], V[3][k]);
         } else if (store_mask & (1u << k)) {
-            uint4 o = *reinterpret_cast<const uint4*>(p);
+            uint4 o = pre ? pre[i] : *reinterpret_cast<const uint4*>(p);
             if (MODE == 1) o = make_uint4(o.x + V[0][k], o.y + V[1][k], o.z + V[2][k], o.w + V[3][k]);
             else o = make_uint4(o.x - V[0][k], o.y - V[1][k], o.z - V[2][k], o.w - V[3][k]);
             *reinterpret_cast<uint4*>(p) = o;

@@ -58,8 +58,8 @@ class MedianBackgroundIH:
             self._add(f, +1)
             self.frames.append(f)
 
-    def _add(self, f: torch.Tensor, sign: int) -> None:
-        if int(f.max().item()) >= self.bins:  # motion.cpp:23-26
+    def _add(self, f: torch.Tensor, sign: int, validate: bool = True) -> None:
+        if validate and int(f.max().item()) >= self.bins:  # motion.cpp:23-26
             raise ContractError(A.SPCT_ERR_CONTRACT, "median_background_ih: frame value exceeds bin count")
         bm = f.to(torch.int16)  # the frame's values are its bins (motion.cpp:53-54)
         src = _source(A.SRC_BINS_U16, [bm], self.width, self.height, self.bins)
@@ -74,7 +74,8 @@ class MedianBackgroundIH:
         if tuple(f.shape) != (self.height, self.width):
             raise ContractError(A.SPCT_ERR_CONTRACT, "median_background_ih: slide frame dimensions differ")
         self._add(f, +1)
-        self._add(self.frames.popleft(), -1)
+        # the outgoing frame passed the same check when it entered (motion.cpp:64-65 repeats it)
+        self._add(self.frames.popleft(), -1, validate=False)
         self.frames.append(f)
 
     def background(self) -> torch.Tensor:
