@@ -18,7 +18,7 @@ OBJDIR     = build/obj
 CU_OBJS    = $(patsubst $(CSRC)/%.cu,$(OBJDIR)/%.o,$(CU_SRCS))
 HOST_OBJS  = $(patsubst $(CSRC)/host/%.cpp,$(OBJDIR)/host_%.o,$(HOST_SRCS))
 
-.PHONY: all lib oracle clean sass dropin
+.PHONY: all lib oracle clean sass dropin dropin_bench
 all: lib oracle dropin
 
 lib: $(LIB)
@@ -51,3 +51,10 @@ dropin: $(DROPIN)
 $(DROPIN): tests/cpp/dropin_test.cpp $(LIB) $(wildcard include/spct/*.hpp)
 	@mkdir -p build
 	$(CXX) -O2 -std=c++20 -Iinclude -o $@ tests/cpp/dropin_test.cpp -L$(PKG) -lspct_b200 -Wl,-rpath,'$$ORIGIN/../$(PKG)'
+
+# wall time of the drop-in calls (tests/cpp/dropin_bench.cpp), run on a GPU box
+DROPIN_BENCH = build/dropin_bench
+dropin_bench: $(DROPIN_BENCH)
+$(DROPIN_BENCH): tests/cpp/dropin_bench.cpp $(LIB) $(wildcard include/spct/*.hpp)
+	@mkdir -p build
+	$(CXX) -O2 -std=c++20 -Iinclude -o $@ tests/cpp/dropin_bench.cpp -L$(PKG) -lspct_b200 -Wl,-rpath,'$$ORIGIN/../$(PKG)'

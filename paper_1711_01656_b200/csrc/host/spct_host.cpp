@@ -18,6 +18,10 @@
 #include "spct/swih.hpp"
 #include "spct_cuda.h"
 
+namespace spct_impl {
+cudaError_t malloc_async(void** p, size_t bytes, cudaStream_t s);  // profile.cu
+}
+
 namespace spct {
 
 namespace {
@@ -44,14 +48,16 @@ void cuda(cudaError_t e, const char* what) {
     if (e != cudaSuccess) throw device_error(std::string(what) + ": " + cudaGetErrorString(e));
 }
 
-// RAII device buffer.
+// RAII device buffer, stream-ordered on the legacy default stream that every call of this
+// layer uses, from the library's retaining pool: a caller building one tensor per frame
+// reuses the previous frame's memory instead of a cudaMalloc / cudaFree of gigabytes.
 struct DevBuf {
     void* p = nullptr;
     explicit DevBuf(std::size_t bytes) {
-        if (bytes) cuda(cudaMalloc(&p, bytes), "cudaMalloc");
+        if (bytes) cuda(spct_impl::malloc_async(&p, bytes, nullptr), "cudaMallocAsync");
     }
     ~DevBuf() {
-        if (p) cudaFree(p);
+        if (p) cudaFreeAsync(p, nullptr);
     }
     DevBuf(const DevBuf&) = delete;
     DevBuf& operator=(const DevBuf&) = delete;
@@ -61,9 +67,78 @@ struct DevBuf {
     }
 };
 
+// Host <-> device copies of large pageable buffers (the reference API's std::vectors)
+// through two pinned 8 MiB chunks: the DMA of one chunk overlaps the host memcpy of the
+// other, instead of the driver's serial pageable staging.
+constexpr std::size_t kChunk = std::size_t(8) << 20;
+
+struct PinnedStage {
+    std::mutex mu;
+    void* buf[2] = {nullptr, nullptr};
+    cudaEvent_t ev[2] = {nullptr, nullptr};
+    bool ready() {
+        if (buf[0]) return true;
+        for (int i = 0; i < 2; ++i) {
+            if (cudaMallocHost(&buf[i], kChunk) != cudaSuccess ||
+                cudaEventCreateWithFlags(&ev[i], cudaEventDisableTiming) != cudaSuccess) {
+                cudaGetLastError();
+                return false;
+            }
+        }
+        return true;
+    }
+};
+
+PinnedStage& stage() {
+    static PinnedStage* s = new PinnedStage();  // never destroyed: outlives static tensors
+    return *s;
+}
+
+void copy_d2h(void* dst, const void* src, std::size_t bytes) {
+    PinnedStage& st = stage();
+    std::unique_lock<std::mutex> lock(st.mu);
+    if (bytes < 2 * kChunk || !st.ready()) {
+        cuda(cudaMemcpy(dst, src, bytes, cudaMemcpyDeviceToHost), "D2H");
+        return;
+    }
+    const std::size_t n = (bytes + kChunk - 1) / kChunk;
+    for (std::size_t i = 0; i <= n; ++i) {
+        if (i < n) {
+            const std::size_t off = i * kChunk, len = std::min(kChunk, bytes - off);
+            cuda(cudaMemcpyAsync(st.buf[i & 1], static_cast<const char*>(src) + off, len, cudaMemcpyDeviceToHost,
+                                 nullptr),
+                 "D2H");
+            cuda(cudaEventRecord(st.ev[i & 1], nullptr), "event");
+        }
+        if (i > 0) {  // chunk i - 1 landed: move it while chunk i is in flight
+            const std::size_t off = (i - 1) * kChunk, len = std::min(kChunk, bytes - off);
+            cuda(cudaEventSynchronize(st.ev[(i - 1) & 1]), "D2H");
+            std::memcpy(static_cast<char*>(dst) + off, st.buf[(i - 1) & 1], len);
+        }
+    }
+}
+
+void copy_h2d(void* dst, const void* src, std::size_t bytes) {
+    PinnedStage& st = stage();
+    std::unique_lock<std::mutex> lock(st.mu);
+    if (bytes < 2 * kChunk || !st.ready()) {
+        cuda(cudaMemcpy(dst, src, bytes, cudaMemcpyHostToDevice), "H2D");
+        return;
+    }
+    const std::size_t n = (bytes + kChunk - 1) / kChunk;
+    for (std::size_t i = 0; i < n; ++i) {
+        const std::size_t off = i * kChunk, len = std::min(kChunk, bytes - off);
+        if (i >= 2) cuda(cudaEventSynchronize(st.ev[i & 1]), "H2D");  // chunk i - 2 has left this buffer
+        std::memcpy(st.buf[i & 1], static_cast<const char*>(src) + off, len);
+        cuda(cudaMemcpyAsync(static_cast<char*>(dst) + off, st.buf[i & 1], len, cudaMemcpyHostToDevice, nullptr), "H2D");
+        cuda(cudaEventRecord(st.ev[i & 1], nullptr), "event");
+    }
+    cuda(cudaEventSynchronize(st.ev[(n - 1) & 1]), "H2D");
+}
+
 template <class T>
 void upload(DevBuf& d, const std::vector<T>& v) {
-    cuda(cudaMemcpy(d.p, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice), "H2D");
+    copy_h2d(d.p, v.data(), v.size() * sizeof(T));
 }
 
 }  // namespace
@@ -104,9 +179,7 @@ void HostMirror::fill() const {
         for (int k0 = 0; k0 < w.bins; k0 += int(per)) {
             const int k1 = std::min<int>(w.bins, k0 + int(per));
             check(spct_cu_wih_export_u64(&w, k0, k1, stage.as<std::uint64_t>(), nullptr));
-            cuda(cudaMemcpy(host_.data() + std::size_t(k0) * plane, stage.p, std::size_t(k1 - k0) * plane * 8,
-                            cudaMemcpyDeviceToHost),
-                 "D2H");
+            copy_d2h(host_.data() + std::size_t(k0) * plane, stage.p, std::size_t(k1 - k0) * plane * 8);
         }
         valid_ = true;
         return;
@@ -120,9 +193,7 @@ void HostMirror::fill() const {
     for (int k0 = 0; k0 < d.bins; k0 += int(per)) {
         const int k1 = std::min<int>(d.bins, k0 + int(per));
         check(spct_cu_ih_export_u64(&d, k0, k1, stage.as<std::uint64_t>(), nullptr));
-        cuda(cudaMemcpy(host_.data() + std::size_t(k0) * plane, stage.p, std::size_t(k1 - k0) * plane * 8,
-                        cudaMemcpyDeviceToHost),
-             "D2H");
+        copy_d2h(host_.data() + std::size_t(k0) * plane, stage.p, std::size_t(k1 - k0) * plane * 8);
     }
     valid_ = true;
 }
@@ -168,11 +239,11 @@ GrayImage to_grayscale(const ColorImage& img) {
     if (n == 0) return out;
     DevBuf d(4 * n);
     auto* p = d.as<std::uint8_t>();
-    cuda(cudaMemcpy(p, img.r.data(), n, cudaMemcpyHostToDevice), "H2D");
-    cuda(cudaMemcpy(p + n, img.g.data(), n, cudaMemcpyHostToDevice), "H2D");
-    cuda(cudaMemcpy(p + 2 * n, img.b.data(), n, cudaMemcpyHostToDevice), "H2D");
+    copy_h2d(p, img.r.data(), n);
+    copy_h2d(p + n, img.g.data(), n);
+    copy_h2d(p + 2 * n, img.b.data(), n);
     check(spct_cu_to_grayscale(p, p + n, p + 2 * n, std::int64_t(n), p + 3 * n, nullptr));
-    cuda(cudaMemcpy(out.data.data(), p + 3 * n, n, cudaMemcpyDeviceToHost), "D2H");
+    copy_d2h(out.data.data(), p + 3 * n, n);
     return out;
 }
 
@@ -196,7 +267,7 @@ BinMap quantize_any(const Raster<T>& img, int kind, int bins, double lo, double 
     s.hi = hi;
     check(spct_cu_quantize(&s, dst.as<std::uint16_t>(), nullptr));
     BinMap out(img.width, img.height, bins);
-    cuda(cudaMemcpy(out.data.data(), dst.p, n * 2, cudaMemcpyDeviceToHost), "D2H");
+    copy_d2h(out.data.data(), dst.p, n * 2);
     return out;
 }
 }  // namespace
@@ -227,12 +298,18 @@ const void* IntegralHistogramTensor::device_descriptor() const { return data.dev
 
 namespace {
 
-// build_tensor's checks (integral.cpp:510-514, 330-343) on the host copy.
-void validate_build(const BinMap& bm, const ScanSchedule& schedule, std::uint64_t budget) {
+// build_tensor's checks (integral.cpp:510-514, 330-343) in the reference's order:
+// validate_binmap (empty, bins, then the bin range — on the uploaded copy, one device
+// max instead of a host pass over the pixels), then tile, threads and the budget.
+// Returns the uploaded BinMap.
+std::unique_ptr<DevBuf> validated_upload(const BinMap& bm, const ScanSchedule& schedule, std::uint64_t budget) {
     require(bm.width > 0 && bm.height > 0, "build: empty bin map");
     require(bm.bins >= 1, "build: bins must be >= 1");
-    std::uint16_t mx = 0;
-    for (std::uint16_t v : bm.data) mx = std::max(mx, v);
+    require(bm.data.size() == std::size_t(bm.width) * bm.height, "build: bin map size mismatch");
+    auto d = std::make_unique<DevBuf>(bm.data.size() * 2);
+    upload(*d, bm.data);
+    int mx = 0;
+    check(spct_cu_binmap_max(d->as<std::uint16_t>(), bm.width, bm.width, bm.height, &mx, nullptr));
     require(mx < bm.bins, "build: bin index out of range");
     require(schedule.tile >= 2 && schedule.tile <= 4096, "build: tile must be in [2, 4096]");
     require(schedule.threads >= 1 && schedule.threads <= 64, "build: threads must be in [1, 64]");
@@ -240,6 +317,7 @@ void validate_build(const BinMap& bm, const ScanSchedule& schedule, std::uint64_
     if (est.padded_bytes > budget)
         throw contract_error("tensor of " + std::to_string(est.padded_bytes) + " bytes exceeds the memory budget of " +
                              std::to_string(budget));
+    return d;
 }
 
 IntegralHistogramTensor build_from_source(const spct_source& src, std::unique_ptr<DevBuf> src_mem) {
@@ -273,9 +351,7 @@ IntegralHistogramTensor build_from_source(const spct_source& src, std::unique_pt
 
 IntegralHistogramTensor build_integral_histogram(const BinMap& bins, const ScanSchedule& schedule,
                                                  std::uint64_t memory_budget) {
-    validate_build(bins, schedule, memory_budget);
-    auto src = std::make_unique<DevBuf>(bins.data.size() * 2);
-    upload(*src, bins.data);
+    auto src = validated_upload(bins, schedule, memory_budget);
     spct_source s{};
     s.kind = SPCT_SRC_BINS_U16;
     s.plane[0] = src->p;
@@ -295,10 +371,11 @@ const spct_ih& desc_of(const IntegralHistogramTensor& t) {
 }  // namespace
 
 namespace {
-// Mirrors of at most this many cells (256 MiB of uint64) are filled after kQueriesBeforeMirror
-// device round trips; later queries read the host copy like the reference does.
+// Mirrors of at most this many cells (256 MiB of uint64) are filled once the device round
+// trips (~20 us each) would have cost about as much as the fill (~64 KiB of mirror per
+// query); later queries read the host copy like the reference does.
 constexpr std::size_t kMirrorCells = std::size_t(32) << 20;
-constexpr int kQueriesBeforeMirror = 16;
+int queries_before_mirror(std::size_t cells) { return static_cast<int>(std::max<std::size_t>(16, cells * 8 >> 16)); }
 
 std::vector<std::uint64_t> region_from_mirror(const IntegralHistogramTensor& t, const Rect& r) {
     std::vector<std::uint64_t> out(t.bins);
@@ -318,7 +395,8 @@ std::vector<std::uint64_t> region_histogram(const IntegralHistogramTensor& t, co
     require(r.inside(t.width, t.height), "region_histogram: rect outside image");  // :563
     detail::DeviceTensor* dt = t.data.dev.get();
     if (!dt || t.data.mirrored()) return region_from_mirror(t, r);
-    if (++dt->queries > kQueriesBeforeMirror && t.data.size() <= kMirrorCells) return region_from_mirror(t, r);
+    if (t.data.size() <= kMirrorCells && ++dt->queries > queries_before_mirror(t.data.size()))
+        return region_from_mirror(t, r);
     const std::size_t cell = dt->weighted ? 8 : 4;
     if (!dt->qbuf) dt->qbuf = std::make_unique<DevBuf>(16 + std::size_t(t.bins) * 8);
     auto* rect = dt->qbuf->as<std::int32_t>();
@@ -425,7 +503,7 @@ LikelihoodMap hist_match_map(const IntegralHistogramTensor& t, const std::vector
     out.height = t.height;
     out.tag = metric == HistMetric::Minkowski ? "hist-distance" : "hist-match";
     out.values.resize(std::size_t(t.width) * t.height);
-    cuda(cudaMemcpy(out.values.data(), map.p, out.values.size() * 8, cudaMemcpyDeviceToHost), "D2H");
+    copy_d2h(out.values.data(), map.p, out.values.size() * 8);
     return out;
 }
 
@@ -462,7 +540,7 @@ LikelihoodMap fuse_maps(const std::vector<LikelihoodMap>& maps, std::vector<doub
     f.height = h;
     f.tag = "fused";
     f.values.resize(n);
-    cuda(cudaMemcpy(f.values.data(), out.p, n * 8, cudaMemcpyDeviceToHost), "D2H");
+    copy_d2h(f.values.data(), out.p, n * 8);
     return f;
 }
 
@@ -556,7 +634,7 @@ LikelihoodMap likelihood_from_frame(const GrayImage& img, int bins, const std::v
     out.height = img.height;
     out.tag = "hist-distance";
     out.values.resize(std::size_t(img.width) * img.height);
-    cuda(cudaMemcpy(out.values.data(), map.p, out.values.size() * 8, cudaMemcpyDeviceToHost), "D2H");
+    copy_d2h(out.values.data(), map.p, out.values.size() * 8);
     if (tensor_out) {
         tensor_out->bins = bins;
         tensor_out->height = img.height;
@@ -606,11 +684,10 @@ const spct_wih& wdesc_of(const IntegralHistogramTensor& t) {
 IntegralHistogramTensor build_weighted_tensor(const BinMap& bins, const std::vector<std::uint64_t>& weights,
                                               const ScanSchedule& schedule, std::uint64_t memory_budget) {
     require(weights.size() == bins.data.size(), "build_weighted_tensor: weight size mismatch");  // integral.cpp:557
-    validate_build(bins, schedule, memory_budget);
-    DevBuf db(bins.data.size() * 2), dw(weights.size() * 8);
-    upload(db, bins.data);
+    auto db = validated_upload(bins, schedule, memory_budget);
+    DevBuf dw(weights.size() * 8);
     upload(dw, weights);
-    return make_weighted(db.as<std::uint16_t>(), bins.width, bins.height, bins.bins, dw.as<std::uint64_t>(), -1, 1, 1);
+    return make_weighted(db->as<std::uint16_t>(), bins.width, bins.height, bins.bins, dw.as<std::uint64_t>(), -1, 1, 1);
 }
 
 // ---------------------------------------------------------------- SWIH (swih.hpp)
@@ -673,17 +750,15 @@ IntegralHistogramTensor build_weighted_ih(const BinMap& bins, const WeightField&
 WeightedQuadrantSet build_quadrant_set(const BinMap& bins, const KernelSpec& spec, const ScanSchedule& schedule) {
     require(bins.width > 0 && bins.height > 0, "quadrant_weight_fields: empty image");
     kernel_extents(spec);
-    validate_build(bins, schedule, kDefaultMemoryBudget);
+    auto db = validated_upload(bins, schedule, kDefaultMemoryBudget);
     WeightedQuadrantSet set;
     set.kernel = spec;
     set.sx = ramp_slope(spec.kw);
     set.sy = ramp_slope(spec.kh);
     set.pair_sum = 2 + std::int64_t(set.sx) * (bins.width - 1) + std::int64_t(set.sy) * (bins.height - 1);
-    DevBuf db(bins.data.size() * 2);
-    upload(db, bins.data);
     for (int d = 0; d < 4; ++d)
         set.tensors[d] =
-            make_weighted(db.as<std::uint16_t>(), bins.width, bins.height, bins.bins, nullptr, d, spec.kw, spec.kh);
+            make_weighted(db->as<std::uint16_t>(), bins.width, bins.height, bins.bins, nullptr, d, spec.kw, spec.kh);
     return set;
 }
 
