@@ -230,6 +230,12 @@ bool exact_maps();
 LikelihoodMap hist_match_map(const IntegralHistogramTensor& t, const std::vector<double>& template_hist, int kw,
                              int kh, HistMetric metric, double p = 1.0);
 
+// The same into a caller-owned map whose storage is reused when the size matches: a
+// per-frame loop then skips allocating (and page-faulting) W x H doubles every call,
+// which at 4096^2 costs more than the whole device computation.
+void hist_match_map_into(const IntegralHistogramTensor& t, const std::vector<double>& template_hist, int kw, int kh,
+                         HistMetric metric, double p, LikelihoodMap& out);
+
 // quantize -> build -> match in one fused device pass over a gray frame; the tensor is
 // returned as well (device resident).  Equivalent to
 //   t = build_integral_histogram(quantize(img, bins)); map = hist_distance_map(t, tmpl, kw, kh, p)

@@ -6,10 +6,12 @@
 // Device failures throw spct::device_error.
 #include <algorithm>
 #include <cmath>
+#include <condition_variable>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <mutex>
+#include <thread>
 
 #include <cuda_runtime.h>
 
@@ -89,6 +91,66 @@ struct PinnedStage {
     }
 };
 
+// memcpy between pinned staging and pageable memory on a few host threads (one thread
+// moves ~10 GB/s; the PCIe link moves ~50).
+class CopyPool {
+public:
+    static CopyPool& get() {
+        static CopyPool* p = new CopyPool();  // never destroyed: workers outlive static teardown
+        return *p;
+    }
+    void memcpy_par(void* dst, const void* src, std::size_t n) {
+        if (n < (std::size_t(1) << 20) || workers_.empty()) {
+            std::memcpy(dst, src, n);
+            return;
+        }
+        const std::size_t parts = workers_.size() + 1, step = (n / parts + 63) / 64 * 64;
+        {
+            std::lock_guard<std::mutex> lock(mu_);
+            for (std::size_t i = 1; i < parts; ++i) {
+                const std::size_t off = std::min(n, i * step), len = std::min(n, off + step) - off;
+                jobs_.push_back({static_cast<char*>(dst) + off, static_cast<const char*>(src) + off, len});
+            }
+            pending_ += parts - 1;
+        }
+        cv_.notify_all();
+        std::memcpy(dst, src, std::min(n, step));
+        std::unique_lock<std::mutex> lock(mu_);
+        done_cv_.wait(lock, [&] { return pending_ == 0; });
+    }
+
+private:
+    struct Job {
+        char* dst;
+        const char* src;
+        std::size_t len;
+    };
+    CopyPool() {
+        const unsigned hw = std::thread::hardware_concurrency();
+        const unsigned n = hw >= 8 ? 3 : (hw >= 4 ? 1 : 0);
+        for (unsigned i = 0; i < n; ++i) workers_.emplace_back([this] { run(); }).detach();
+    }
+    void run() {
+        for (;;) {
+            Job j;
+            {
+                std::unique_lock<std::mutex> lock(mu_);
+                cv_.wait(lock, [&] { return !jobs_.empty(); });
+                j = jobs_.back();
+                jobs_.pop_back();
+            }
+            std::memcpy(j.dst, j.src, j.len);
+            std::lock_guard<std::mutex> lock(mu_);
+            if (--pending_ == 0) done_cv_.notify_all();
+        }
+    }
+    std::mutex mu_;
+    std::condition_variable cv_, done_cv_;
+    std::vector<Job> jobs_;
+    std::size_t pending_ = 0;
+    std::vector<std::thread> workers_;
+};
+
 PinnedStage& stage() {
     static PinnedStage* s = new PinnedStage();  // never destroyed: outlives static tensors
     return *s;
@@ -113,7 +175,7 @@ void copy_d2h(void* dst, const void* src, std::size_t bytes) {
         if (i > 0) {  // chunk i - 1 landed: move it while chunk i is in flight
             const std::size_t off = (i - 1) * kChunk, len = std::min(kChunk, bytes - off);
             cuda(cudaEventSynchronize(st.ev[(i - 1) & 1]), "D2H");
-            std::memcpy(static_cast<char*>(dst) + off, st.buf[(i - 1) & 1], len);
+            CopyPool::get().memcpy_par(static_cast<char*>(dst) + off, st.buf[(i - 1) & 1], len);
         }
     }
 }
@@ -129,7 +191,7 @@ void copy_h2d(void* dst, const void* src, std::size_t bytes) {
     for (std::size_t i = 0; i < n; ++i) {
         const std::size_t off = i * kChunk, len = std::min(kChunk, bytes - off);
         if (i >= 2) cuda(cudaEventSynchronize(st.ev[i & 1]), "H2D");  // chunk i - 2 has left this buffer
-        std::memcpy(st.buf[i & 1], static_cast<const char*>(src) + off, len);
+        CopyPool::get().memcpy_par(st.buf[i & 1], static_cast<const char*>(src) + off, len);
         cuda(cudaMemcpyAsync(static_cast<char*>(dst) + off, st.buf[i & 1], len, cudaMemcpyHostToDevice, nullptr), "H2D");
         cuda(cudaEventRecord(st.ev[i & 1], nullptr), "event");
     }
@@ -479,8 +541,8 @@ MemoryEstimate estimate_memory(int w, int h, int bins, int elem_bytes) {
     return e;
 }
 
-LikelihoodMap hist_match_map(const IntegralHistogramTensor& t, const std::vector<double>& th, int kw, int kh,
-                             HistMetric metric, double p) {
+void hist_match_map_into(const IntegralHistogramTensor& t, const std::vector<double>& th, int kw, int kh,
+                         HistMetric metric, double p, LikelihoodMap& out) {
     check(spct_cu_hist_check(t.bins, t.width, t.height, th.data(), int(th.size()), kw, kh, p));
     const spct_ih& d = desc_of(t);
     DevBuf tm(th.size() * 8), map(std::size_t(t.width) * t.height * 8);
@@ -498,12 +560,17 @@ LikelihoodMap hist_match_map(const IntegralHistogramTensor& t, const std::vector
     } else {
         check(spct_cu_hist_match(&d, tm.as<double>(), kw, kh, p, int(metric), map.as<double>(), nullptr));
     }
-    LikelihoodMap out;
     out.width = t.width;
     out.height = t.height;
     out.tag = metric == HistMetric::Minkowski ? "hist-distance" : "hist-match";
-    out.values.resize(std::size_t(t.width) * t.height);
+    out.values.resize(std::size_t(t.width) * t.height);  // no-op when the caller's map is already this size
     copy_d2h(out.values.data(), map.p, out.values.size() * 8);
+}
+
+LikelihoodMap hist_match_map(const IntegralHistogramTensor& t, const std::vector<double>& th, int kw, int kh,
+                             HistMetric metric, double p) {
+    LikelihoodMap out;
+    hist_match_map_into(t, th, kw, kh, metric, p, out);
     return out;
 }
 

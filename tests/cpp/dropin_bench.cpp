@@ -51,5 +51,14 @@ int main(int argc, char** argv) {
         if (v[7] != 0.0) std::printf(" ");
     }
     std::printf("  (std::vector<double>(W*H) alone: %.3f ms)\n", tv / frames);
+    // the reusing overload (non-reference extension)
+    auto t = build_integral_histogram(bm, {}, ~0ull);
+    LikelihoodMap m;
+    hist_match_map_into(t, tmpl, 64, 64, HistMetric::Minkowski, 1.0, m);
+    auto a = clk::now();
+    for (int f = 0; f < frames; ++f) hist_match_map_into(t, tmpl, 64, 64, HistMetric::Minkowski, 1.0, m);
+    auto b = clk::now();
+    std::printf("  hist_match_map_into (map storage reused): %.3f ms\n",
+                std::chrono::duration<double, std::milli>(b - a).count() / frames);
     return 0;
 }
