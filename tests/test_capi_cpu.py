@@ -174,3 +174,41 @@ def test_iht1_errors_match_reference(tmp_path):
         assert st == A.SPCT_ERR_IO and A.lib().spct_cu_last_error().decode().startswith(msg), name
         with pytest.raises(oracle.RefIOError, match=msg):
             oracle.RefTensor.load(p)
+
+
+def test_next_rows_and_peer_contracts_before_device_work():
+    """SWIH / swlh map / median / consumers / peer-reduce entry points reject bad arguments
+    with the reference's messages before touching the device."""
+    lib = A.lib()
+    err = lambda: lib.spct_cu_last_error()  # noqa: E731
+    # swlh map, direct sweep: kernel_extents (swih.cpp:20), the sweep's own limits
+    assert lib.spct_cu_swlh_map_direct(1, 16, 16, 16, 4, 0, 3, 1, 1, None) == A.SPCT_ERR_CONTRACT
+    assert b"kernel extents must be >= 1" in err()
+    assert lib.spct_cu_swlh_map_direct(1, 256, 256, 256, 4, 129, 3, 1, 1, None) == A.SPCT_ERR_CONTRACT
+    assert lib.spct_cu_swlh_map_direct(1, 8, 16, 16, 4, 3, 3, 1, 1, None) == A.SPCT_ERR_CONTRACT  # pitch < width
+    # swlh brute force / weighted layout
+    assert lib.spct_cu_swlh_brute(1, 16, 16, 16, 4, 0, 3, None, 0, None, None) == A.SPCT_ERR_CONTRACT
+    rp, pp, nb = C.c_int64(), C.c_int64(), C.c_uint64()
+    assert lib.spct_cu_wih_layout(0, 4, 4, C.byref(rp), C.byref(pp), C.byref(nb)) == A.SPCT_ERR_CONTRACT
+    A.check(lib.spct_cu_wih_layout(33, 7, 3, C.byref(rp), C.byref(pp), C.byref(nb)))
+    assert rp.value % 16 == 0 and rp.value >= 33 and pp.value == rp.value * 7 and nb.value == pp.value * 3 * 8
+    # joint-IH median (motion.cpp:13-14, 38-43)
+    assert lib.spct_cu_median_sort(None, 0, 4, 4, 4, 1, 4, None) == A.SPCT_ERR_CONTRACT
+    assert b"empty window" in err()
+    ptrs = (C.c_void_p * 2)(1, 1)
+    assert lib.spct_cu_median_sort(ptrs, 2, 4, 4, 4, 1, 4, None) == A.SPCT_ERR_CONTRACT
+    assert b"window length must be odd" in err()
+    # map consumers (likelihood.cpp:258-266, tracker.cpp:79-84)
+    assert lib.spct_cu_fuse_maps(None, 0, None, 0, 16, 1, None) == A.SPCT_ERR_CONTRACT
+    assert b"no maps to fuse" in err()
+    r = C.c_int64()
+    assert lib.spct_cu_score_map(1, 10, 10, 8, 8, 5, 5, C.byref(r), 1, 1 << 20, None) == A.SPCT_ERR_CONTRACT
+    assert b"ground truth rect must lie inside the map" in err()
+    # peer reduce: flags and the slot finaliser
+    assert lib.spct_cu_flag_wait(None, 1, 1, 1, 1000, None, None) == A.SPCT_ERR_CONTRACT
+    assert lib.spct_cu_flag_wait(1, 0, 1, 1, 1000, 1, None) == A.SPCT_ERR_CONTRACT
+    assert lib.spct_cu_flag_signal(None, 1, None) == A.SPCT_ERR_CONTRACT
+    assert lib.spct_cu_hist_finalize_slots(1, 2, 10, 8, 8, 3, 3, 1.0, 0, 1, None) == A.SPCT_ERR_CONTRACT  # stride < nu*nv
+    assert lib.spct_cu_hist_finalize_slots(1, 2, 36, 8, 8, 3, 3, 0.5, 0, 1, None) == A.SPCT_ERR_CONTRACT
+    assert b"Minkowski order must be >= 1" in err()
+    assert lib.spct_cu_peer_open(None, None) == A.SPCT_ERR_CONTRACT
