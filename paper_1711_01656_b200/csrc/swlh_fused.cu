@@ -34,6 +34,17 @@ constexpr int kNC = 128;   // centres per strip
 constexpr int kNT = 256;   // threads (>= extended columns)
 constexpr int kNBG = 32;   // bins per pass
 constexpr int kWarps = kNT / 32;
+constexpr int kPS = kNT + 1 + (kNT + 1) / 32 + 1;  // prefix array with one pad word per 32
+
+// Prefix index with a pad word every 32: lane l's eight entries 8l .. 8l + 7 then fall
+// into 32 different banks for each i (8-way conflicts without the pad).
+__device__ __forceinline__ int pidx(int t) { return t + (t >> 5); }
+
+__global__ void qtab_kernel(double* __restrict__ q, int64_t mass) {
+    for (int64_t w = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; w <= mass;
+         w += static_cast<int64_t>(gridDim.x) * blockDim.x)
+        q[w] = __ddiv_rn(static_cast<double>(w), static_cast<double>(mass));
+}
 
 struct Params {
     const uint16_t* bins;
@@ -41,6 +52,7 @@ struct Params {
     int W, H, k0, nbg;
     int kw, kh, sxl, syt, syb, c;
     double mass;
+    const double* qtab;   // qtab[W] = W / mass (correctly rounded), W = 0 .. mass
     const double* model;  // the group's bins
     double* dpart;        // nu * nv partial distances (groups before / after this one), or null
     double* map;          // final group only
@@ -54,8 +66,8 @@ __device__ __forceinline__ int pix(const Params& p, int x, int y) {
 __global__ void __launch_bounds__(kNT, 2) swlh_fused_kernel(Params p) {
     extern __shared__ uint32_t sm[];
     uint32_t* S = sm;                                            // [kNBG][kNT] column state
-    int32_t* Pw = reinterpret_cast<int32_t*>(S + kNBG * kNT);     // [warp][3][kNT + 1] prefixes
-    int32_t* Wb = Pw + kWarps * 3 * (kNT + 1);                    // [kNBG][kNC] window sums
+    int32_t* Pw = reinterpret_cast<int32_t*>(S + kNBG * kNT);     // [warp][3][kPS] prefixes (padded)
+    int32_t* Wb = Pw + kWarps * 3 * kPS;                          // [kNBG][kNC] window sums
     double* Tm = reinterpret_cast<double*>(Wb + kNBG * kNC);      // [kNBG][kNC] |q - model|
     double* mdl = Tm + kNBG * kNC;                                // [kNBG]
     const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
@@ -82,9 +94,9 @@ __global__ void __launch_bounds__(kNT, 2) swlh_fused_kernel(Params p) {
     }
     __syncthreads();
 
-    int32_t* P0 = Pw + warp * 3 * (kNT + 1);
-    int32_t* P1 = P0 + (kNT + 1);
-    int32_t* PM = P1 + (kNT + 1);
+    int32_t* P0 = Pw + warp * 3 * kPS;
+    int32_t* P1 = P0 + kPS;
+    int32_t* PM = P1 + kPS;
     for (int v = v0; v < v1; ++v) {
         const int cy = p.syt + v;
         // 1. window sums of every bin of the row: warp w takes bins w, w + 8, ...; lane l the
@@ -119,14 +131,15 @@ __global__ void __launch_bounds__(kNT, 2) swlh_fused_kernel(Params p) {
             const int32_t b0 = i0 - r0, b1 = i1 - r1, bm = im - rm;
 #pragma unroll
             for (int i = 0; i < 8; ++i) {
-                P0[8 * lane + i] = b0 + e0[i];
-                P1[8 * lane + i] = b1 + e1[i];
-                PM[8 * lane + i] = bm + em[i];
+                const int a = pidx(8 * lane + i);
+                P0[a] = b0 + e0[i];
+                P1[a] = b1 + e1[i];
+                PM[a] = bm + em[i];
             }
             if (lane == 31) {
-                P0[kNT] = i0;
-                P1[kNT] = i1;
-                PM[kNT] = im;
+                P0[pidx(kNT)] = i0;
+                P1[pidx(kNT)] = i1;
+                PM[pidx(kNT)] = im;
             }
             __syncwarp();
 #pragma unroll
@@ -134,9 +147,10 @@ __global__ void __launch_bounds__(kNT, 2) swlh_fused_kernel(Params p) {
                 const int u = lane + 32 * j;  // window columns [u, u + kw), centre column u + sxl
                 if (u0 + u >= nu) continue;
                 const int uc = u + p.sxl, ue = u + p.kw;
-                const int32_t n = P0[ue] - P0[u];
-                const int32_t gy = PM[ue] - PM[u];
-                const int32_t gx = uc * (P0[uc] - P0[u]) - (P1[uc] - P1[u]) + (P1[ue] - P1[uc]) - uc * (P0[ue] - P0[uc]);
+                const int iu = pidx(u), ic = pidx(uc), ie = pidx(ue);
+                const int32_t n = P0[ie] - P0[iu];
+                const int32_t gy = PM[ie] - PM[iu];
+                const int32_t gx = uc * (P0[ic] - P0[iu]) - (P1[ic] - P1[iu]) + (P1[ie] - P1[ic]) - uc * (P0[ie] - P0[ic]);
                 Wb[k * kNC + u] = p.c * n - gx - gy;
             }
             __syncwarp();
@@ -160,7 +174,7 @@ __global__ void __launch_bounds__(kNT, 2) swlh_fused_kernel(Params p) {
         for (int i = t; i < nbg * kNC; i += kNT) {
             const int k = i / kNC, u = i % kNC;
             if (u0 + u >= nu) continue;
-            const double q = __ddiv_rn(static_cast<double>(Wb[i]), p.mass);
+            const double q = __ldg(p.qtab + Wb[i]);  // == W / mass, the division done once per W
             Tm[i] = fabs(__dsub_rn(q, mdl[k]));
         }
         __syncthreads();  // B: terms ready, state at cy + 1
@@ -195,7 +209,7 @@ __global__ void fill_kernel(double* __restrict__ map, int64_t n, double v) {
 }
 
 size_t smem_bytes() {
-    return static_cast<size_t>(kNBG) * kNT * 4 + static_cast<size_t>(kWarps) * 3 * (kNT + 1) * 4 +
+    return static_cast<size_t>(kNBG) * kNT * 4 + static_cast<size_t>(kWarps) * 3 * kPS * 4 +
            static_cast<size_t>(kNBG) * kNC * 4 + static_cast<size_t>(kNBG) * kNC * 8 + kNBG * 8 + 16;
 }
 
@@ -249,10 +263,23 @@ extern "C" spct_status spct_cu_swlh_map_direct(const uint16_t* bins, int64_t pit
         cudaFuncSetAttribute(swlh_fused_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
         attr = true;
     }
+    // W / mass for every possible window sum W (0 .. mass): one division per value instead
+    // of one per window and bin
+    double* qtab = nullptr;
+    if (auto st = cuda_status(malloc_async(&qtab, static_cast<size_t>(mass + 1) * 8, s), "swlh alloc")) return st;
+    qtab_kernel<<<static_cast<unsigned>(std::min<int64_t>(ceil_div(mass + 1, 256), 148 * 8)), 256, 0, s>>>(qtab, mass);
+    if (auto st = launch_status("qtab_kernel")) {
+        cudaFreeAsync(qtab, s);
+        return st;
+    }
+    p.qtab = qtab;
     double* dpart = nullptr;
     const int groups = static_cast<int>(ceil_div(nbins, kNBG));
     if (groups > 1)
-        if (auto st = cuda_status(malloc_async(&dpart, static_cast<size_t>(nu) * nv * 8, s), "swlh alloc")) return st;
+        if (auto st = cuda_status(malloc_async(&dpart, static_cast<size_t>(nu) * nv * 8, s), "swlh alloc")) {
+            cudaFreeAsync(qtab, s);
+            return st;
+        }
     spct_status st = SPCT_OK;
     for (int g = 0; g < groups && st == SPCT_OK; ++g) {
         p.k0 = g * kNBG;
@@ -266,6 +293,7 @@ extern "C" spct_status spct_cu_swlh_map_direct(const uint16_t* bins, int64_t pit
         st = launch_status("swlh_fused_kernel");
     }
     if (dpart) cudaFreeAsync(dpart, s);
+    cudaFreeAsync(qtab, s);
     if (st != SPCT_OK) return st;
     replicate_kernel<<<static_cast<unsigned>(std::max<int64_t>(1, ceil_div(n, 256))), 256, 0, s>>>(
         map, width, height, p.sxl, width - (kw - p.sxl), p.syt, height - p.syb);
