@@ -14,6 +14,8 @@
 //                                            sums stay sequential chains (same rounding)
 // All results are bit-identical to the reference (no reassociation, no FMA contraction).
 #include <cmath>
+#include <cstring>
+#include <utility>
 #include <vector>
 
 #include "spct_internal.h"
@@ -159,9 +161,12 @@ __device__ __forceinline__ uint64_t desc_key(double h) {
     return ~asc;
 }
 
+// kminmax[0..1]: the smallest and largest key (atomics; the sort skips the digit passes
+// above the highest bit in which any two keys differ).
 __global__ void __launch_bounds__(256) peak_compact_kernel(const double* __restrict__ s, int w, int h,
                                                            const uint32_t* __restrict__ boff,
-                                                           uint64_t* __restrict__ keys, uint32_t* __restrict__ idx) {
+                                                           uint64_t* __restrict__ keys, uint32_t* __restrict__ idx,
+                                                           unsigned long long* __restrict__ kminmax) {
     __shared__ uint32_t wsum[8];
     const int64_t n = static_cast<int64_t>(w) * h;
     const int64_t base = static_cast<int64_t>(blockIdx.x) * kPeakTile + 4 * threadIdx.x;
@@ -173,12 +178,26 @@ __global__ void __launch_bounds__(256) peak_compact_kernel(const double* __restr
     }
     uint32_t tot;
     uint32_t pos = boff[blockIdx.x] + block_excl_scan(c, &tot, wsum);
+    unsigned long long kmin = ~0ull, kmax = 0ull;
     for (int j = 0; j < 4; ++j)
         if (f[j]) {
-            keys[pos] = desc_key(s[base + j]);
+            const unsigned long long k = desc_key(s[base + j]);
+            keys[pos] = k;
             idx[pos] = static_cast<uint32_t>(base + j);
             ++pos;
+            kmin = k < kmin ? k : kmin;
+            kmax = k > kmax ? k : kmax;
         }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+        const unsigned long long a = __shfl_xor_sync(0xffffffffu, kmin, o), b = __shfl_xor_sync(0xffffffffu, kmax, o);
+        kmin = a < kmin ? a : kmin;
+        kmax = b > kmax ? b : kmax;
+    }
+    if ((threadIdx.x & 31) == 0 && kmin <= kmax) {
+        atomicMin(kminmax, kmin);
+        atomicMax(kminmax + 1, kmax);
+    }
 }
 
 // Radix pass p: digit (key >> 8p) & 255.  counts are digit-major: counts[d * nblk + b].
@@ -380,7 +399,7 @@ size_t peak_ws_bytes(int w, int h, int64_t* nblk_peak, int64_t* nblk_sort) {
     *nblk_peak = ceil_div(n, kPeakTile);
     *nblk_sort = std::max<int64_t>(1, ceil_div(cap, kSortTile));
     auto r = [](int64_t b) { return static_cast<size_t>(round_up(b, 256)); };
-    return r(n * 8) + r(*nblk_peak * 4) + 2 * r(cap * 8) + 2 * r(cap * 4) + r(256 * *nblk_sort * 4) + r(16 + 1024);
+    return r(n * 8) + r(*nblk_peak * 4) + 2 * r(cap * 8) + 2 * r(cap * 4) + r(256 * *nblk_sort * 4) + r(16 + 1024 + 16);
 }
 
 PeakWs carve(void* ws, int w, int h) {
@@ -401,7 +420,8 @@ PeakWs carve(void* ws, int w, int h) {
     s.v[0] = reinterpret_cast<uint32_t*>(take(cap * 4));
     s.v[1] = reinterpret_cast<uint32_t*>(take(cap * 4));
     s.counts = reinterpret_cast<uint32_t*>(take(256 * nbs * 4));
-    s.scalars = reinterpret_cast<uint32_t*>(take(16 + 1024));  // [0]: peak count, [4 ..]: digit starts
+    // [0]: peak count, [4 .. 259]: digit starts, [260 .. 263]: key min / max (u64)
+    s.scalars = reinterpret_cast<uint32_t*>(take(16 + 1024 + 16));
     return s;
 }
 
@@ -415,17 +435,28 @@ spct_status sorted_peaks(const double* map, int w, int h, void* ws, size_t ws_by
     smooth3_kernel<<<grid1(n), 256, 0, st>>>(map, w, h, P.s);
     peak_count_kernel<<<static_cast<unsigned>(nbp), 256, 0, st>>>(P.s, w, h, P.bcount);
     excl_scan_kernel<<<1, 1024, 0, st>>>(P.bcount, nbp, P.scalars);
-    peak_compact_kernel<<<static_cast<unsigned>(nbp), 256, 0, st>>>(P.s, w, h, P.bcount, P.k[0], P.v[0]);
+    unsigned long long* kminmax = reinterpret_cast<unsigned long long*>(P.scalars + 260);
+    const unsigned long long init[2] = {~0ull, 0ull};
+    cudaMemcpyAsync(kminmax, init, 16, cudaMemcpyHostToDevice, st);
+    peak_compact_kernel<<<static_cast<unsigned>(nbp), 256, 0, st>>>(P.s, w, h, P.bcount, P.k[0], P.v[0], kminmax);
     if (auto e = launch_status("find_peaks compaction")) return e;
-    uint32_t total = 0;
-    if (auto e = cuda_status(cudaMemcpyAsync(&total, P.scalars, 4, cudaMemcpyDeviceToHost, st), "find_peaks count")) return e;
+    uint32_t hdr[264];
+    if (auto e = cuda_status(cudaMemcpyAsync(hdr, P.scalars, sizeof(hdr), cudaMemcpyDeviceToHost, st), "find_peaks count"))
+        return e;
     if (auto e = cuda_status(cudaStreamSynchronize(st), "find_peaks")) return e;
-    const int64_t m = total;
+    const int64_t m = hdr[0];
+    int cur = 0;
     if (m > 1) {
         const int nb = static_cast<int>(ceil_div(m, kSortTile));
-        int cur = 0;
         uint32_t* digit = P.scalars + 4;  // [256] digit totals -> digit starts
-        for (int pass = 0; pass < 8; ++pass) {
+        // digits above the highest bit in which two keys differ are the same for every key:
+        // those passes would be identity permutations
+        unsigned long long kmin, kmax;
+        std::memcpy(&kmin, hdr + 260, 8);
+        std::memcpy(&kmax, hdr + 262, 8);
+        const unsigned long long diff = kmin ^ kmax;
+        const int npass = diff ? (63 - __builtin_clzll(diff)) / 8 + 1 : 0;
+        for (int pass = 0; pass < npass; ++pass) {
             radix_hist_kernel<<<nb, 256, 0, st>>>(P.k[cur], m, 8 * pass, nb, P.counts);
             // per digit (one CTA each): prefix over the blocks; then the digits' starts
             excl_scan_kernel<<<256, 1024, 0, st>>>(P.counts, nb, digit);
@@ -435,7 +466,10 @@ spct_status sorted_peaks(const double* map, int w, int h, void* ws, size_t ws_by
             cur ^= 1;
         }
         if (auto e = launch_status("find_peaks sort")) return e;
-        // eight passes: the sorted data is back in buffer 0
+    }
+    if (cur) {  // an odd number of passes: the sorted data is in buffer 1
+        std::swap(P.k[0], P.k[1]);
+        std::swap(P.v[0], P.v[1]);
     }
     *out = P;
     *count = m;
