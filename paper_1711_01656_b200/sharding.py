@@ -62,6 +62,18 @@ class _DevArray:
                                          "version": 3, "strides": None}
 
 
+class DeviceSlot:
+    """A (nv, nu) float64 slot that may live on another GPU (an IPC mapping of the root's
+    buffer).  Deliberately not a torch tensor: torch would attribute the memory to the
+    owning device and could copy it; the library only needs the address (data_ptr)."""
+
+    def __init__(self, ptr: int, shape):
+        self._ptr, self.shape, self.dtype = ptr, tuple(shape), "float64"
+
+    def data_ptr(self) -> int:
+        return self._ptr
+
+
 class PeerSlabReduce:
     """The bin-slab reduce of the likelihood map over peer memory (peer.cu).
 
@@ -153,10 +165,11 @@ class PeerSlabReduce:
             self._check(self._A.lib().spct_cu_flag_wait(self.ack, 1, 1, need, self.TIMEOUT_NS, self.err,
                                                         self._s(stream)))
 
-    def slot(self):
-        """This rank's slot of the current epoch, (nv, nu) float64 on the root's memory."""
+    def slot(self) -> DeviceSlot:
+        """This rank's slot of the current epoch, (nv, nu) float64 on the root's memory
+        (pass it as the `partial` of build_and_match)."""
         off = slot_offset(self.epoch, self.rank, self.world, self.stride)
-        return self._torch.as_tensor(_DevArray(self.slots + 8 * off, (self.nv, self.nu), "<f8"), device=self.device)
+        return DeviceSlot(self.slots + 8 * off, (self.nv, self.nu))
 
     def publish(self, stream=None) -> None:
         flag = self.flags + 8 * self.FLAG_STRIDE * self.rank
