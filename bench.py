@@ -351,18 +351,30 @@ def run_ours(args) -> None:
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
 
     peer, reduce_note = None, args.reduce
-    if world > 1 and args.reduce == "peer":
-        from paper_1711_01656_b200.sharding import PeerSlabReduce
+    if world > 1 and args.reduce in ("band", "root"):
+        from paper_1711_01656_b200.sharding import PeerBandReduce, PeerSlabReduce
 
-        try:  # fails on every rank or on none (PeerSlabReduce agrees on the outcome)
-            peer = PeerSlabReduce(nu, nv, device=dev)
+        try:  # fails on every rank or on none (the reducers agree on the outcome)
+            peer = PeerBandReduce(W_IMG, H_IMG, KW, KH, device=dev) if args.reduce == "band" else \
+                PeerSlabReduce(nu, nv, device=dev)
         except RuntimeError as e:  # no IPC / peer access between these GPUs: the NCCL reduce instead
             reduce_note = "nccl (peer setup failed: %s)" % str(e)[:120]
+        if peer is not None and args.reduce == "band" and rank == 0:
+            lmap = peer.map  # the final map lives in the shared buffer the band owners write
 
     def step(src):
         if world == 1:
             # every bin on this GPU: the sweep writes the finished map itself
             P.build_and_match_map(src, nbins, None, KW, KH, P_ORDER, out=t, lmap=lmap, tmpl_dev=tm)
+            return
+        if peer is not None and args.reduce == "band":
+            # partials stay in each rank's HBM; every rank pulls its band of rows from all
+            # partials over NVLink, sums and finalises them into rank 0's map
+            peer.begin()
+            P.build_and_match(src, nbins, None, KW, KH, P_ORDER, bin0=bin0, bins=bin1 - bin0, out=t,
+                              partial=peer.slot(), tmpl_dev=tm)
+            peer.publish()
+            peer.finalize(P_ORDER)
             return
         if peer is not None:
             # the sweep writes its slab's partial map into its slot on rank 0 over NVLink;
@@ -523,8 +535,11 @@ def run_ours(args) -> None:
                                 "+ 64x64 p=1 likelihood map (float64)" % nbins),
                    "bins_total": nbins, "bins_per_gpu": BINS_PER_GPU, "window": [KW, KH], "p": P_ORDER,
                    "parallelism": f"bin-slab x{world}" + (
-                       "" if world == 1 else (" + partial maps written to rank 0 over peer memory (fused reduce)"
-                                              if peer is not None else " + NCCL reduce of partial maps")),
+                       "" if world == 1 else (
+                           " + band-owned reduce over peer memory (each rank pulls and finalises a band of rows)"
+                           if peer is not None and args.reduce == "band" else
+                           " + partial maps written to rank 0 over peer memory" if peer is not None
+                           else " + NCCL reduce of partial maps")),
                    **({"reduce": reduce_note} if world > 1 else {}),
                    **({"shared_gpu": True} if shared else {}),
                    "l2": "256 MiB memset between timed steps (outside the events); step writes 8.6 GB/GPU"},
@@ -560,8 +575,9 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-c5", action="store_true", help="skip the config-5 tracking-batch measurement")
     ap.add_argument("--no-next", action="store_true", help="skip the SURVEY 8(f) rows (SWIH, consumers, median)")
-    ap.add_argument("--reduce", choices=["peer", "nccl"], default="peer",
-                    help="N > 1: partial maps via peer-memory slots (default) or an NCCL reduce")
+    ap.add_argument("--reduce", choices=["band", "root", "nccl"], default="band",
+                    help="N > 1: band-owned reduce over peer memory (default), partials pushed into the "
+                         "root's slots, or one NCCL reduce")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

@@ -301,6 +301,15 @@ spct_status spct_cu_flag_wait(const uint64_t* flags, int n, int64_t stride, uint
                               uint32_t* err, void* stream);
 spct_status spct_cu_hist_finalize_slots(const double* slots, int nslots, int64_t slot_stride, int width, int height,
                                         int kw, int kh, double p, int metric, double* map, void* stream);
+/* Band-owned variant: the caller owns valid rows [v0, v1); `partials` is a
+ * host array of nsrc (<= 16) device pointers to the ranks' full (H-kh+1) x (W-kw+1)
+ * partial maps (peer mappings), summed in array order; writes the final map rows of the
+ * band (with the replicated top / bottom borders for the first / last band) into `map`
+ * (W x H, may be a peer mapping).  spct_cu_flag_signal_many publishes one epoch to n
+ * (<= 16) flags with one release. */
+spct_status spct_cu_hist_finalize_band(const double* const* partials, int nsrc, int width, int height, int kw, int kh,
+                                       double p, int metric, int v0, int v1, double* map, void* stream);
+spct_status spct_cu_flag_signal_many(uint64_t* const* flags, int n, uint64_t value, void* stream);
 
 /* ----------------------------------------------------------------- instrumentation */
 

@@ -103,6 +103,8 @@ SIGNATURES = {
     "spct_cu_flag_signal": (_i, [_vp, C.c_uint64, _vp]),
     "spct_cu_flag_wait": (_i, [_vp, _i, _i64, C.c_uint64, C.c_uint64, _vp, _vp]),
     "spct_cu_hist_finalize_slots": (_i, [_vp, _i, _i64, _i, _i, _i, _i, _d, _i, _vp, _vp]),
+    "spct_cu_hist_finalize_band": (_i, [C.POINTER(_vp), _i, _i, _i, _i, _i, _d, _i, _i, _i, _vp, _vp]),
+    "spct_cu_flag_signal_many": (_i, [C.POINTER(_vp), _i, C.c_uint64, _vp]),
     "spct_cu_swlh_map_direct": (_i, [_vp, _i64, _i, _i, _i, _i, _i, _vp, _vp, _vp]),
     "spct_cu_launch_count": (C.c_uint64, []),
     "spct_cu_profile_enable": (None, [_i]),

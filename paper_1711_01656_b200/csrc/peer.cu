@@ -94,9 +94,98 @@ __global__ void __launch_bounds__(256) finalize_slots_kernel(const double* __res
     }
 }
 
+// ---- band-owned reduce: every rank keeps its partial map in its own HBM; rank r owns the
+// valid rows [v0, v1) and pulls them from all N partials (NVLink loads from the peers'
+// IPC mappings), sums in rank order, finalises and writes the final map rows (borders
+// included, spread_valid) into the map on the root.  The reduction work and the NVLink
+// traffic are spread over all ranks instead of converging on the root.
+constexpr int kMaxPeers = 16;
+
+struct PeerPtrs {
+    const double* p[kMaxPeers];
+};
+
+struct FlagPtrs {
+    uint64_t* p[kMaxPeers];
+};
+
+__global__ void signal_many_kernel(FlagPtrs f, int n, uint64_t value) {
+    asm volatile("fence.sc.sys;" ::: "memory");
+    const int i = threadIdx.x;
+    if (i < n) asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(f.p[i]), "l"(value) : "memory");
+}
+
+__global__ void __launch_bounds__(256) finalize_band_kernel(PeerPtrs src, int nsrc, FinParams f, int v0, int v1,
+                                                            double* __restrict__ map) {
+    // output rows whose clamped valid row lies in [v0, v1): the band, plus the replicated
+    // top (first band) and bottom (last band) borders
+    const int y0 = v0 == 0 ? 0 : v0 + f.cy0, y1 = v1 == f.nv ? f.H : v1 + f.cy0;
+    const int64_t n = static_cast<int64_t>(y1 - y0) * f.W;
+    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int x = static_cast<int>(i % f.W), y = y0 + static_cast<int>(i / f.W);
+        const int vx = min(max(x, f.cx0), f.cx0 + f.nu - 1) - f.cx0;
+        const int vy = min(max(y, f.cy0), f.cy0 + f.nv - 1) - f.cy0;
+        const int64_t o = static_cast<int64_t>(vy) * f.nu + vx;
+        double s = src.p[0][o];
+        for (int r = 1; r < nsrc; ++r) s = __dadd_rn(s, src.p[r][o]);
+        map[static_cast<int64_t>(y) * f.W + x] = finalize_L(s, f);
+    }
+}
+
+spct_status make_fin(int width, int height, int kw, int kh, double p, int metric, FinParams* f) {
+    if (!(width > 0 && height > 0)) return contract("hist_finalize: empty map");
+    if (!(p >= 1.0)) return contract("hist_distance_map: Minkowski order must be >= 1");
+    if (!(kw >= 1 && kh >= 1 && kw <= width && kh <= height)) return contract("hist_distance_map: kernel exceeds image");
+    if (metric < SPCT_METRIC_MINKOWSKI || metric > SPCT_METRIC_CHISQ) return contract("hist_match: unknown metric");
+    *f = FinParams{};
+    f->W = width;
+    f->H = height;
+    f->nu = width - kw + 1;
+    f->nv = height - kh + 1;
+    f->cx0 = (kw - 1) / 2;
+    f->cy0 = (kh - 1) / 2;
+    f->metric = metric;
+    f->p_kind = p == 1.0 ? 1 : 0;
+    f->inv_p = 1.0 / p;
+    f->dmax = std::pow(2.0, 1.0 / p);  // likelihood.cpp:208
+    return SPCT_OK;
+}
+
 }  // namespace spct_peer
 
 using namespace spct_peer;
+
+extern "C" spct_status spct_cu_flag_signal_many(uint64_t* const* flags, int n, uint64_t value, void* stream) {
+    if (!flags || n < 1 || n > kMaxPeers) return contract("flag_signal_many: bad arguments");
+    FlagPtrs f{};
+    for (int i = 0; i < n; ++i) {
+        if (!flags[i]) return contract("flag_signal_many: null flag");
+        f.p[i] = flags[i];
+    }
+    signal_many_kernel<<<1, 32, 0, as_stream(stream)>>>(f, n, value);
+    return launch_status("signal_many_kernel");
+}
+
+extern "C" spct_status spct_cu_hist_finalize_band(const double* const* partials, int nsrc, int width, int height,
+                                                  int kw, int kh, double p, int metric, int v0, int v1, double* map,
+                                                  void* stream) {
+    FinParams f;
+    if (auto st = make_fin(width, height, kw, kh, p, metric, &f)) return st;
+    if (!partials || !map || nsrc < 1 || nsrc > kMaxPeers || !(0 <= v0 && v0 <= v1 && v1 <= f.nv))
+        return contract("hist_finalize_band: bad arguments");
+    if (v0 == v1) return SPCT_OK;
+    PeerPtrs src{};
+    for (int i = 0; i < nsrc; ++i) {
+        if (!partials[i]) return contract("hist_finalize_band: null partial");
+        src.p[i] = partials[i];
+    }
+    const int y0 = v0 == 0 ? 0 : v0 + f.cy0, y1 = v1 == f.nv ? f.H : v1 + f.cy0;
+    const int64_t n = static_cast<int64_t>(y1 - y0) * width;
+    const int64_t blocks = std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, 148 * 8));
+    finalize_band_kernel<<<static_cast<unsigned>(blocks), 256, 0, as_stream(stream)>>>(src, nsrc, f, v0, v1, map);
+    return launch_status("finalize_band_kernel");
+}
 
 static_assert(sizeof(cudaIpcMemHandle_t) == SPCT_IPC_HANDLE_BYTES, "IPC handle size");
 

@@ -210,3 +210,163 @@ class PeerSlabReduce:
 
     def close(self, group=None) -> None:
         self._release(group)
+
+
+def band_rows(nv: int, world: int, rank: int) -> tuple[int, int]:
+    """Valid-window rows [v0, v1) whose map rows rank `rank` finalises (contiguous bands)."""
+    if not (world >= 1 and 0 <= rank < world and nv >= 1):
+        raise ValueError("band_rows: need world >= 1, 0 <= rank < world, nv >= 1")
+    b = -(-nv // world)
+    return min(nv, rank * b), min(nv, (rank + 1) * b)
+
+
+class PeerBandReduce:
+    """Band-owned bin-slab reduce over peer memory (peer.cu).
+
+    Every rank's sweep writes its partial map into its own HBM; rank r then pulls the rows
+    of its band from all ranks' partials over NVLink, sums them in rank order while
+    finalising, and writes those rows of the final map (borders included) into the map
+    on the root.  Per step::
+
+        r.begin()
+        build_and_match(..., partial=r.slot())     # local
+        r.publish()                                 # "my partial of this epoch is complete"
+        r.finalize(kw, kh, p)                       # my band; the root also waits for all bands
+        r.map                                       # the root's (H, W) float64 map
+
+    Flags are uint64 epochs written with system-scope releases; partials are double
+    buffered by epoch parity and reused only after every band owner acknowledged them.
+    """
+
+    FLAG_STRIDE = 16
+    TIMEOUT_NS = 60_000_000_000
+
+    def __init__(self, width: int, height: int, kw: int, kh: int, *, root: int = 0, group=None, device=None):
+        import ctypes as C
+
+        import torch
+        import torch.distributed as dist
+
+        from . import _capi as A
+        from ._capi import check
+
+        self._C, self._A, self._check, self._torch = C, A, check, torch
+        self.world, self.rank = dist.get_world_size(group), dist.get_rank(group)
+        if self.world > 15:
+            raise ValueError("PeerBandReduce: at most 15 ranks")
+        self.root = root
+        self.W, self.H, self.kw, self.kh = width, height, kw, kh
+        self.nu, self.nv = width - kw + 1, height - kh + 1
+        self.v0, self.v1 = band_rows(self.nv, self.world, self.rank)
+        self.plane = (self.nu * self.nv + 31) // 32 * 32  # doubles per partial
+        self.device = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+        self.epoch = 0
+        self._own, self._opened = [], []
+        lib = A.lib()
+        fs = 8 * self.FLAG_STRIDE
+
+        def alloc(nbytes):
+            p, h = C.c_void_p(), (C.c_char * A.SPCT_IPC_HANDLE_BYTES)()
+            check(lib.spct_cu_peer_alloc(nbytes, C.byref(p), h))
+            self._own.append(p.value)
+            return p.value, bytes(h)
+
+        def open_(h):
+            p = C.c_void_p()
+            check(lib.spct_cu_peer_open(h, C.byref(p)))
+            self._opened.append(p.value)
+            return p.value
+
+        err, mine = None, {}
+        try:
+            self.part, mine["part"] = alloc(2 * self.plane * 8)     # my partials, two parities
+            self.flags, mine["flags"] = alloc(self.world * fs)     # writers -> me (band owner)
+            self.acks, mine["acks"] = alloc(self.world * fs)       # band owners -> me (writer)
+            self.err, _ = alloc(64)
+            if self.rank == root:
+                self.map_ptr, mine["map"] = alloc(width * height * 8)
+                self.mapflags, mine["mapflags"] = alloc(self.world * fs)  # band owners -> root
+        except Exception as e:  # noqa: BLE001 (reported below, on every rank)
+            err = e
+        hs = [None] * self.world
+        dist.all_gather_object(hs, None if err else mine, group=group)
+        if err is None and any(h is None for h in hs):
+            err = RuntimeError("peer setup failed on another rank")
+        if err is None:
+            try:
+                me = self.rank
+                self.parts = [self.part if q == me else open_(hs[q]["part"]) for q in range(self.world)]
+                self.peer_flags = [self.flags if q == me else open_(hs[q]["flags"]) for q in range(self.world)]
+                self.peer_acks = [self.acks if q == me else open_(hs[q]["acks"]) for q in range(self.world)]
+                if me == root:
+                    self.root_map, self.root_mapflags = self.map_ptr, self.mapflags
+                else:
+                    self.root_map, self.root_mapflags = open_(hs[root]["map"]), open_(hs[root]["mapflags"])
+            except Exception as e:  # noqa: BLE001
+                err = e
+        ok = [None] * self.world
+        dist.all_gather_object(ok, err is None, group=group)
+        if not all(ok):
+            self.close(group)
+            raise RuntimeError(f"PeerBandReduce setup failed: {err or 'on another rank'}")
+
+    def _s(self, stream):
+        return (stream if stream is not None else self._torch.cuda.current_stream()).cuda_stream
+
+    def _wait(self, flags: int, value: int, stream) -> None:
+        self._check(self._A.lib().spct_cu_flag_wait(flags, self.world, self.FLAG_STRIDE, value, self.TIMEOUT_NS,
+                                                    self.err, self._s(stream)))
+
+    def _signal(self, ptrs, value: int, stream) -> None:
+        arr = (self._C.c_void_p * len(ptrs))(*ptrs)
+        self._check(self._A.lib().spct_cu_flag_signal_many(arr, len(ptrs), value, self._s(stream)))
+
+    def begin(self, stream=None) -> None:
+        self.epoch += 1
+        if self.epoch > 2:  # every owner has pulled this parity's partial two epochs ago
+            self._wait(self.acks, self.epoch - 2, stream)
+
+    def slot(self) -> DeviceSlot:
+        return DeviceSlot(self.part + 8 * self.plane * (self.epoch % 2), (self.nv, self.nu))
+
+    def publish(self, stream=None) -> None:
+        fs = 8 * self.FLAG_STRIDE
+        self._signal([f + fs * self.rank for f in self.peer_flags], self.epoch, stream)
+
+    def finalize(self, p: float = 1.0, metric: int = 0, stream=None) -> None:
+        C, lib, s = self._C, self._A.lib(), self._s(stream)
+        fs = 8 * self.FLAG_STRIDE
+        self._wait(self.flags, self.epoch, stream)  # every writer's partial of this epoch
+        off = 8 * self.plane * (self.epoch % 2)
+        src = (C.c_void_p * self.world)(*[q + off for q in self.parts])
+        self._check(lib.spct_cu_hist_finalize_band(src, self.world, self.W, self.H, self.kw, self.kh, p, metric,
+                                                   self.v0, self.v1, self.root_map, s))
+        self._signal([self.root_mapflags + fs * self.rank] + [a + fs * self.rank for a in self.peer_acks],
+                     self.epoch, stream)
+        if self.rank == self.root:
+            self._wait(self.mapflags, self.epoch, stream)
+
+    @property
+    def map(self):
+        """The final (H, W) float64 map on the root (a tensor view of the shared buffer)."""
+        if self.rank != self.root:
+            raise RuntimeError("PeerBandReduce.map lives on the root")
+        return self._torch.as_tensor(_DevArray(self.map_ptr, (self.H, self.W), "<f8"), device=self.device)
+
+    def error(self) -> bool:
+        t = self._torch.as_tensor(_DevArray(self.err, (1,), "<u4"), device=self.device)
+        self._torch.cuda.synchronize(self.device)
+        return bool(int(t.item()))
+
+    def close(self, group=None) -> None:
+        import torch.distributed as dist
+
+        self._torch.cuda.synchronize(self.device)
+        lib = self._A.lib()
+        for p in self._opened:
+            lib.spct_cu_peer_close(p)
+        self._opened = []
+        dist.barrier(group=group)
+        for p in self._own:
+            lib.spct_cu_peer_free(p)
+        self._own = []

@@ -28,7 +28,7 @@ def _frames(n, w, h):
     return [np.roll(base, 3 * i, axis=1) for i in range(n)]
 
 
-def _worker(rank, world, port, out_path, nbins, kw, kh, p):
+def _worker(rank, world, port, out_path, nbins, kw, kh, p, mode="root"):
     import torch.distributed as dist
 
     os.environ["MASTER_ADDR"] = "127.0.0.1"
@@ -36,14 +36,14 @@ def _worker(rank, world, port, out_path, nbins, kw, kh, p):
     torch.cuda.set_device(0)
     dist.init_process_group("gloo", rank=rank, world_size=world)
     import paper_1711_01656_b200 as P
-    from paper_1711_01656_b200.sharding import PeerSlabReduce, slab_bounds
+    from paper_1711_01656_b200.sharding import PeerBandReduce, PeerSlabReduce, slab_bounds
 
     w, h = 300, 170
     frames = _frames(5, w, h)
     crop = (frames[0][40:40 + kh, 70:70 + kw].astype(np.int64) * nbins) >> 8
     tmpl = np.bincount(crop.reshape(-1), minlength=nbins).astype(np.float64) / crop.size
     k0, k1 = slab_bounds(nbins, world, rank)
-    red = PeerSlabReduce(w - kw + 1, h - kh + 1)
+    red = PeerSlabReduce(w - kw + 1, h - kh + 1) if mode == "root" else PeerBandReduce(w, h, kw, kh)
     got = []
     try:
         for f in frames:
@@ -51,7 +51,11 @@ def _worker(rank, world, port, out_path, nbins, kw, kh, p):
             red.begin()
             P.build_and_match(src, nbins, tmpl, kw, kh, p, bin0=k0, bins=k1 - k0, partial=red.slot())
             red.publish()
-            if rank == 0:
+            if mode == "band":
+                red.finalize(p)
+                if rank == 0:
+                    got.append(red.map.cpu().numpy())
+            elif rank == 0:
                 lmap = torch.empty((h, w), dtype=torch.float64, device="cuda")
                 red.finalize(lmap, w, h, kw, kh, p)
                 got.append(lmap.cpu().numpy())
@@ -65,12 +69,15 @@ def _worker(rank, world, port, out_path, nbins, kw, kh, p):
         dist.destroy_process_group()
 
 
+@pytest.mark.parametrize("mode", ["root", "band"])
 @pytest.mark.parametrize("world,nbins,kw,kh,p", [(2, 64, 33, 21, 1.0), (2, 40, 16, 16, 2.0), (3, 50, 20, 9, 1.0)])
-def test_peer_slab_reduce(tmp_path, world, nbins, kw, kh, p):
+def test_peer_slab_reduce(tmp_path, world, nbins, kw, kh, p, mode):
+    """root: every partial into the root's slots, the root finalises; band: partials stay
+    local, each rank finalises a band of rows into the root's map."""
     import torch.multiprocessing as mp
 
     out = str(tmp_path / "maps.npy")
-    mp.spawn(_worker, args=(world, _free_port(), out, nbins, kw, kh, p), nprocs=world, join=True)
+    mp.spawn(_worker, args=(world, _free_port(), out, nbins, kw, kh, p, mode), nprocs=world, join=True)
     got, want = np.load(out)
     assert got.shape == want.shape
     err = np.abs(got - want)
