@@ -91,3 +91,17 @@ def test_peer_slot_schedule():
                 assert e <= 2
     with pytest.raises(ValueError):
         slot_offset(0, 0, 2, 8)
+
+
+def test_band_rows_partition():
+    """PeerBandReduce's row bands tile the valid rows exactly once, in rank order."""
+    from paper_1711_01656_b200.sharding import band_rows
+
+    for nv in (1, 7, 100, 4033):
+        for world in (1, 2, 3, 8):
+            spans = [band_rows(nv, world, r) for r in range(world)]
+            assert spans[0][0] == 0 and spans[-1][1] == nv
+            assert all(a[1] == b[0] for a, b in zip(spans, spans[1:]))
+            assert all(v0 <= v1 for v0, v1 in spans)
+    with pytest.raises(ValueError):
+        band_rows(10, 2, 2)
