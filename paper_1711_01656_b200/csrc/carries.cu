@@ -168,19 +168,26 @@ __global__ void __launch_bounds__(256) fcarry_prefix_kernel(int H, int Lb, int W
         if (i >= plane / 4) return;
         uint16_t* p = C16 + 4 * i;
         uint2 acc = make_uint2(0, 0);
-        constexpr int U = 8;  // loads in flight
-        for (int j0 = 0; j0 + 1 < nbands; j0 += U) {
-            uint2 v[U];
+        constexpr int U = 8;  // loads in flight; the next group is loaded before this one is
+                              // stored (in place: the loads could not move past the stores)
+        auto load = [&](int j0, uint2 (&v)[U]) {
 #pragma unroll
             for (int u = 0; u < U; ++u)
                 v[u] = j0 + u + 1 < nbands ? *reinterpret_cast<const uint2*>(p + (j0 + u) * plane) : make_uint2(0, 0);
+        };
+        uint2 cur[U], nxt[U];
+        load(0, cur);
+        for (int j0 = 0; j0 + 1 < nbands; j0 += U) {
+            if (j0 + U + 1 < nbands) load(j0 + U, nxt);
 #pragma unroll
             for (int u = 0; u < U; ++u) {
                 if (j0 + u + 1 >= nbands) break;
-                acc.x += v[u].x;  // u16 pairs: column counts stay below 2^16 (H < 65536)
-                acc.y += v[u].y;
+                acc.x += cur[u].x;  // u16 pairs: column counts stay below 2^16 (H < 65536)
+                acc.y += cur[u].y;
                 *reinterpret_cast<uint2*>(p + (j0 + u) * plane) = acc;
             }
+#pragma unroll
+            for (int u = 0; u < U; ++u) cur[u] = nxt[u];
         }
     }
 }
