@@ -51,7 +51,6 @@ struct Params {
     int64_t pitch;
     int W, H, k0, nbg;
     int kw, kh, sxl, syt, syb, c;
-    double mass;
     const double* qtab;   // qtab[W] = W / mass (correctly rounded), W = 0 .. mass
     const double* model;  // the group's bins
     double* dpart;        // nu * nv partial distances (groups before / after this one), or null
@@ -243,7 +242,6 @@ extern "C" spct_status spct_cu_swlh_map_direct(const uint16_t* bins, int64_t pit
     int64_t mass = 0;  // sum of the pyramid weights (the constant window mass / 2^16)
     for (int dy = -p.syt; dy < p.syb; ++dy)
         for (int dx = -p.sxl; dx < kw - p.sxl; ++dx) mass += p.c - std::abs(dx) - std::abs(dy);
-    p.mass = static_cast<double>(mass);
     const int nu = width - kw + 1, nv = height - kh + 1;
     const int strips = static_cast<int>(ceil_div(nu, kNC));
     // bands: about two waves of the resident CTA slots, at least kh rows each (the
