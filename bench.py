@@ -11,9 +11,10 @@ Throughput is Gbin*px/s = b * H * W / step time, whole job over all ranks.
 
 Multi-GPU (N > 1): bin-slab sharding.  Rank r owns bins [128 r, 128 r + 128) of a
 b = 128 N histogram over the same frame (weak scaling: fixed work per GPU); each rank's
-sweep writes its slab of the integral histogram and its partial window sums straight
-into its slot on rank 0 over peer memory (--reduce peer, default; --reduce nccl: one
-NCCL reduce instead), and rank 0 sums the slots while finalising the likelihood map.
+sweep writes its slab of the integral histogram and its partial window sums; then
+(--reduce band, default) every rank pulls one band of rows from all partials over peer
+memory, sums and finalises them into rank 0's map; --reduce root pushes every partial
+into a slot on rank 0, which finalises; --reduce nccl runs one NCCL reduce instead.
 
 Extra lines of the JSON: build_only (plain build), c5_batch (config 5 tracking batch)
 and next_rows (SWIH, map consumers, temporal median).

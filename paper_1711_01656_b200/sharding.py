@@ -2,9 +2,12 @@
 
 Each rank owns a contiguous slab of bins [k0, k1), builds that slab of the integral
 histogram and the slab's partial window statistic (the per-bin terms summed over its
-bins), and one reduce adds the partial maps on the destination rank, which then runs
-the finalisation.  Everything here is plumbing on torch.distributed (NCCL on GPUs,
-gloo in the CPU tests); the computation lives in the CUDA kernels.
+bins); the partial maps are then summed and finalised by one of three reducers:
+PeerBandReduce (every rank finalises a band of rows, pulling from all partials over
+peer memory), PeerSlabReduce (partials pushed into slots on the root) or
+reduce_partials (one torch.distributed reduce: NCCL on GPUs, gloo in the CPU tests).
+torch.distributed only exchanges IPC handles and synchronises; the computation lives
+in the CUDA kernels (peer.cu).
 
 The reference has no multi-device path; the decomposition is exact
 because every plane depends only on [bin == k] and the window statistic is a sum
