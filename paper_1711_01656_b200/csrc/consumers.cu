@@ -66,9 +66,17 @@ __global__ void smooth3_kernel(const double* __restrict__ map, int w, int h, dou
     }
 }
 
-__device__ __forceinline__ bool is_peak(const double* s, int w, int h, int64_t i) {
-    const int y = static_cast<int>(i / w), x = static_cast<int>(i % w);
-    const double v = s[i];
+// likelihood.cpp:312-322 at (x, y): every in-bounds neighbour + 1e-9 below the value.
+__device__ __forceinline__ bool is_peak_xy(const double* s, int w, int h, int x, int y) {
+    const double* c = s + static_cast<int64_t>(y) * w + x;
+    const double v = *c;
+    if (x > 0 && y > 0 && x + 1 < w && y + 1 < h) {  // interior: no bounds checks
+        const double* up = c - w;
+        const double* dn = c + w;
+        return __dadd_rn(up[-1], 1e-9) < v && __dadd_rn(up[0], 1e-9) < v && __dadd_rn(up[1], 1e-9) < v &&
+               __dadd_rn(c[-1], 1e-9) < v && __dadd_rn(c[1], 1e-9) < v && __dadd_rn(dn[-1], 1e-9) < v &&
+               __dadd_rn(dn[0], 1e-9) < v && __dadd_rn(dn[1], 1e-9) < v;
+    }
     for (int dy = -1; dy <= 1; ++dy)
         for (int dx = -1; dx <= 1; ++dx) {
             if (dx == 0 && dy == 0) continue;
@@ -77,6 +85,10 @@ __device__ __forceinline__ bool is_peak(const double* s, int w, int h, int64_t i
             if (__dadd_rn(s[static_cast<int64_t>(ny) * w + nx], 1e-9) >= v) return false;
         }
     return true;
+}
+
+__device__ __forceinline__ bool is_peak(const double* s, int w, int h, int64_t i) {
+    return is_peak_xy(s, w, h, static_cast<int>(i % w), static_cast<int>(i / w));
 }
 
 // Block-wide exclusive scan of one value per thread (256 threads); returns the total too.
@@ -106,8 +118,14 @@ __global__ void __launch_bounds__(256) peak_count_kernel(const double* __restric
     const int64_t n = static_cast<int64_t>(w) * h;
     const int64_t base = static_cast<int64_t>(blockIdx.x) * kPeakTile + 4 * threadIdx.x;
     uint32_t c = 0;
-    for (int j = 0; j < 4; ++j)
-        if (base + j < n && is_peak(s, w, h, base + j)) ++c;
+    int x = static_cast<int>(base % w), y = static_cast<int>(base / w);
+    for (int j = 0; j < 4; ++j) {
+        if (base + j < n && is_peak_xy(s, w, h, x, y)) ++c;
+        if (++x == w) {
+            x = 0;
+            ++y;
+        }
+    }
     uint32_t tot;
     block_excl_scan(c, &tot, wsum);
     if (threadIdx.x == 0) bcount[blockIdx.x] = tot;
@@ -172,9 +190,14 @@ __global__ void __launch_bounds__(256) peak_compact_kernel(const double* __restr
     const int64_t base = static_cast<int64_t>(blockIdx.x) * kPeakTile + 4 * threadIdx.x;
     bool f[4];
     uint32_t c = 0;
+    int x = static_cast<int>(base % w), y = static_cast<int>(base / w);
     for (int j = 0; j < 4; ++j) {
-        f[j] = base + j < n && is_peak(s, w, h, base + j);
+        f[j] = base + j < n && is_peak_xy(s, w, h, x, y);
         c += f[j];
+        if (++x == w) {
+            x = 0;
+            ++y;
+        }
     }
     uint32_t tot;
     uint32_t pos = boff[blockIdx.x] + block_excl_scan(c, &tot, wsum);
@@ -295,17 +318,17 @@ __global__ void __launch_bounds__(256) rank_count_kernel(const double* __restric
                                                          const unsigned* __restrict__ best_idx,
                                                          const unsigned long long* __restrict__ best_key,
                                                          unsigned long long* __restrict__ count) {
-    const int64_t n = static_cast<int64_t>(w) * h;
     const unsigned bi = *best_idx;
     const bool found = bi != 0xFFFFFFFFu;
     const unsigned long long bk = *best_key;
     unsigned c = 0;
-    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
-         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-        if (!is_peak(s, w, h, i)) continue;
-        const unsigned long long k = desc_key(s[i]);
-        c += !found || k < bk || (k == bk && static_cast<unsigned>(i) < bi);
-    }
+    for (int y = blockIdx.y; y < h; y += gridDim.y)
+        for (int x = blockIdx.x * blockDim.x + threadIdx.x; x < w; x += gridDim.x * blockDim.x) {
+            if (!is_peak_xy(s, w, h, x, y)) continue;
+            const int64_t i = static_cast<int64_t>(y) * w + x;
+            const unsigned long long k = desc_key(s[i]);
+            c += !found || k < bk || (k == bk && static_cast<unsigned>(i) < bi);
+        }
 #pragma unroll
     for (int o = 16; o; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
     if ((threadIdx.x & 31) == 0 && c) atomicAdd(count, static_cast<unsigned long long>(c));
@@ -380,6 +403,12 @@ __global__ void __launch_bounds__(32 * kCamWarps) camshift_warp_kernel(
         iters[q] = it_done;
         zero_mass[q] = zm;
     }
+}
+
+// (columns of 256 threads, rows) for the row-wise 2-D kernels, about 16 CTAs per SM
+dim3 grid2d(int w, int h) {
+    const unsigned gx = static_cast<unsigned>(std::min<int64_t>(ceil_div(w, 256), 16));
+    return dim3(gx, static_cast<unsigned>(std::min<int64_t>(h, std::max<int64_t>(1, 148 * 16 / gx))));
 }
 
 int grid1(int64_t n) { return static_cast<int>(std::min<int64_t>(std::max<int64_t>((n + 255) / 256, 1), 148 * 16)); }
@@ -558,7 +587,9 @@ extern "C" spct_status spct_cu_score_map(const double* map, int w, int h, int gx
     const int64_t nr = static_cast<int64_t>(gw) * gh;
     rect_best_key_kernel<<<grid1(nr), 256, 0, s>>>(P.s, w, h, gx, gy, gw, gh, bk);
     rect_best_idx_kernel<<<grid1(nr), 256, 0, s>>>(P.s, w, h, gx, gy, gw, gh, bk, bi);
-    rank_count_kernel<<<grid1(n), 256, 0, s>>>(P.s, w, h, bi, bk, cnt);
+    {
+        rank_count_kernel<<<grid2d(w, h), 256, 0, s>>>(P.s, w, h, bi, bk, cnt);
+    }
     if (auto st = launch_status("score_map")) return st;
     unsigned long long c = 0;
     if (auto st = cuda_status(cudaMemcpyAsync(&c, cnt, 8, cudaMemcpyDeviceToHost, s), "score")) return st;
