@@ -130,6 +130,7 @@ public:
     bool operator==(const std::vector<std::uint64_t>& o) const;
     void clear();
     bool mirrored() const { return valid_; }  // the host copy is filled (non-reference addition)
+    void adopt(std::vector<std::uint64_t>&& host);  // library-internal: install a filled host copy
 
     std::shared_ptr<DeviceTensor> dev;  // null for a default-constructed tensor
 private:

@@ -280,6 +280,11 @@ bool HostMirror::operator==(const std::vector<std::uint64_t>& o) const {
     return std::equal(begin(), end(), o.begin());
 }
 
+void HostMirror::adopt(std::vector<std::uint64_t>&& host) {
+    host_ = std::move(host);
+    valid_ = true;
+}
+
 void HostMirror::clear() {
     dev.reset();
     host_.clear();
@@ -504,6 +509,43 @@ void dump_tensor(const IntegralHistogramTensor& t, const std::string& path) {
     check(spct_cu_ih_dump(&desc_of(t), path.c_str(), 8, nullptr));
 }
 
+namespace {
+// A file whose cells do not fit the uint32 device tensor (a dumped weighted tensor: 16.16
+// sums) loads, like the reference's load_tensor, as uint64 cells: the padded payload is
+// the host mirror itself, and a weighted device tensor is filled from it plane by plane.
+IntegralHistogramTensor load_tensor_u64(const std::string& path, int bins, int h, int w) {
+    std::FILE* f = std::fopen(path.c_str(), "rb");
+    if (!f) throw io_error("cannot open tensor: " + path);  // integral.cpp:636
+    const std::size_t cells = std::size_t(bins) * (h + 1) * (w + 1);
+    std::vector<std::uint64_t> host(cells);
+    const bool ok = std::fseek(f, 20, SEEK_SET) == 0 && std::fread(host.data(), 8, cells, f) == cells;
+    std::fclose(f);
+    if (!ok) throw io_error("truncated tensor payload: " + path);  // :655
+    auto dt = std::make_shared<detail::DeviceTensor>();
+    dt->weighted = true;
+    spct_wih& d = dt->wdesc;
+    std::uint64_t bytes = 0;
+    check(spct_cu_wih_layout(w, h, bins, &d.row_pitch, &d.plane_pitch, &bytes));
+    dt->mem = std::make_unique<DevBuf>(bytes);
+    d.data = dt->mem->as<std::uint64_t>();
+    d.bins = bins;
+    d.height = h;
+    d.width = w;
+    const std::size_t ps = std::size_t(h + 1) * (w + 1);
+    for (int k = 0; k < bins; ++k)  // cells (y, x) >= (1, 1) of plane k, unpadded and pitched
+        cuda(cudaMemcpy2D(d.data + std::size_t(k) * d.plane_pitch, d.row_pitch * 8, host.data() + k * ps + (w + 1) + 1,
+                          (w + 1) * 8, std::size_t(w) * 8, h, cudaMemcpyHostToDevice),
+             "H2D");
+    IntegralHistogramTensor t;
+    t.bins = bins;
+    t.height = h;
+    t.width = w;
+    t.data.dev = std::move(dt);
+    t.data.adopt(std::move(host));
+    return t;
+}
+}  // namespace
+
 IntegralHistogramTensor load_tensor(const std::string& path) {
     int bins = 0, h = 0, w = 0, elem = 0;
     check(spct_cu_ih_load_header(path.c_str(), &bins, &h, &w, &elem));
@@ -518,7 +560,11 @@ IntegralHistogramTensor load_tensor(const std::string& path) {
     d.nbins_total = bins;
     d.height = h;
     d.width = w;
-    check(spct_cu_ih_load(path.c_str(), &d, nullptr));
+    const spct_status st = spct_cu_ih_load(path.c_str(), &d, nullptr);
+    if (st == SPCT_ERR_IO && elem == 8 &&
+        std::string(spct_cu_last_error()).rfind("tensor value exceeds the uint32 device cell", 0) == 0)
+        return load_tensor_u64(path, bins, h, w);
+    check(st);
     IntegralHistogramTensor t;
     t.bins = bins;
     t.height = h;

@@ -252,6 +252,18 @@ int main() {
             }
         }
         CHECK_THROWS_AS(build_weighted_tensor(bm, std::vector<std::uint64_t>(5, 1)), contract_error);
+        // a dumped weighted tensor (16.16 sums beyond 2^32) loads back with uint64 cells
+        std::vector<std::uint64_t> big(bm.data.size());
+        for (std::size_t i = 0; i < big.size(); ++i) big[i] = (std::uint64_t(1) << 31) + i * 65536;
+        auto wt = build_weighted_tensor(bm, big);
+        const std::string wpath = "/tmp/spct_dropin_w.iht";
+        dump_tensor(wt, wpath);
+        auto wl = load_tensor(wpath);
+        CHECK(wl.bins == 6 && wl.height == 14 && wl.width == 21);
+        CHECK(wl.data == wt.data);
+        CHECK(wl.at(0, 14, 21) + wl.at(1, 14, 21) > (std::uint64_t(1) << 32));
+        CHECK(region_histogram(wl, Rect{3, 2, 9, 7}) == region_histogram(wt, Rect{3, 2, 9, 7}));
+        std::remove(wpath.c_str());
     }
     {  // swlh query bit-exact against the brute force (test_swih.cpp:98-114)
         std::mt19937 rng(606);
