@@ -184,12 +184,27 @@ def dump_tensor(t: IntegralHistogramTensor, path: str, elem_bytes: int = 8, stre
     check(A.lib().spct_cu_ih_dump(C.byref(t.desc), str(path).encode(), int(elem_bytes), _stream(stream)))
 
 
-def load_tensor(path: str, device=None, stream=None) -> IntegralHistogramTensor:
-    """integral.cpp:635-659: an IHT1 file (elem 8, or 4) into a new device tensor."""
+def load_tensor(path: str, device=None, stream=None):
+    """integral.cpp:635-659: an IHT1 file (elem 8, or 4) into a new device tensor.  A file
+    whose cells exceed 2^32 (a dumped weighted tensor) comes back as a swih.WeightedTensor
+    with uint64 cells, as the reference's load_tensor keeps them."""
     b, h, w, e = C.c_int(), C.c_int(), C.c_int(), C.c_int()
     check(A.lib().spct_cu_ih_load_header(str(path).encode(), C.byref(b), C.byref(h), C.byref(w), C.byref(e)))
     t = IntegralHistogramTensor(w.value, h.value, b.value, device=device)
-    check(A.lib().spct_cu_ih_load(str(path).encode(), C.byref(t.desc), _stream(stream)))
+    st = A.lib().spct_cu_ih_load(str(path).encode(), C.byref(t.desc), _stream(stream))
+    if (st == A.SPCT_ERR_IO and e.value == 8 and
+            A.lib().spct_cu_last_error().startswith(b"tensor value exceeds the uint32 device cell")):
+        from .swih import WeightedTensor
+
+        pad = np.fromfile(str(path), dtype="<u8", offset=20, count=b.value * (h.value + 1) * (w.value + 1))
+        if pad.size != b.value * (h.value + 1) * (w.value + 1):
+            raise A.SpctError(A.SPCT_ERR_IO, f"truncated tensor payload: {path}")  # integral.cpp:655
+        wt = WeightedTensor(w.value, h.value, b.value, device=t.storage.device)
+        cells = pad.reshape(b.value, h.value + 1, w.value + 1)[:, 1:, 1:].view(np.int64)
+        view = wt.storage[:b.value * wt.desc.plane_pitch].view(b.value, h.value, wt.desc.row_pitch)
+        view[:, :, :w.value].copy_(torch.from_numpy(np.ascontiguousarray(cells)))
+        return wt
+    check(st)
     return t
 
 

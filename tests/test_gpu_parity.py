@@ -508,6 +508,24 @@ def test_iht1_chunked_and_elem4(P, tmp_path):
     assert np.array_equal(P.load_tensor(p4).padded_u64(), want)
 
 
+def test_iht1_weighted_tensor_round_trip(P, tmp_path):
+    """A weighted tensor with cells beyond 2^32 dumps like the reference and loads back
+    with uint64 cells (a WeightedTensor), as the reference's load_tensor keeps them."""
+    rng = np.random.default_rng(3)
+    bm = rng.integers(0, 5, (23, 31)).astype(np.uint16)
+    wts = (np.uint64(1) << np.uint64(31)) + rng.integers(0, 1 << 20, (23, 31)).astype(np.uint64)
+    wt = P.swih.build_weighted_tensor(bm, wts, 5)
+    path = str(tmp_path / "w.iht")
+    want = wt.padded_u64()
+    header = np.array([5, 23, 31, 8], "<u4").tobytes()
+    with open(path, "wb") as f:  # the reference's IHT1 layout (integral.cpp:619-631)
+        f.write(b"IHT1" + header + want.astype("<u8").tobytes())
+    got = P.load_tensor(path)
+    assert isinstance(got, P.swih.WeightedTensor)
+    assert np.array_equal(got.padded_u64(), want)
+    assert want.max() > (1 << 32)
+
+
 def test_iht1_load_rejects_bad_payloads(P, tmp_path):
     bm = oracle.random_binmap(9, 6, 4, 3)
     t = P.build_integral_histogram(bm, 4)
@@ -526,8 +544,8 @@ def test_iht1_load_rejects_bad_payloads(P, tmp_path):
     off = 20 + 8 * (1 * 10 + 1)  # plane 0, row 1, column 1
     big[off:off + 8] = (1 << 33).to_bytes(8, "little")
     (tmp_path / "big.iht").write_bytes(bytes(big))
-    with pytest.raises(P.SpctError, match="exceeds the uint32"):
-        P.load_tensor(tmp_path / "big.iht")
+    wt = P.load_tensor(tmp_path / "big.iht")  # cells beyond 2^32: uint64 cells, as the reference keeps them
+    assert isinstance(wt, P.swih.WeightedTensor) and int(wt.padded_u64()[0, 1, 1]) == 1 << 33
     with pytest.raises(P.SpctError, match="cannot write tensor"):
         P.dump_tensor(t, "/nonexistent/dir/t.iht")
 
