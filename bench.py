@@ -195,6 +195,38 @@ def peaks() -> dict:
     return {"hbm_gbs": 6650.0, "source": "fallback"}
 
 
+def box_peaks(dev) -> dict:
+    """Copy and write-only bandwidth of this device, measured live ("also
+    record a measured device write/copy peak on the box").  2 GiB buffers (> L2), torch's
+    own copy_/fill_ kernels, CUDA events over 10 back-to-back launches each.  Outside
+    every timed region; the sweep is write-dominated (8.6 GB written, 17 MB read), so the
+    write peak is its tightest like-for-like denominator."""
+    import torch
+
+    n = 1 << 31
+    a = torch.empty(n, dtype=torch.uint8, device=dev)
+    b = torch.empty_like(a)
+    a.fill_(1)
+    b.copy_(a)
+    torch.cuda.synchronize(dev)
+
+    def t(fn, reps=10):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(reps):
+            fn()
+        e1.record()
+        e1.synchronize()
+        return e0.elapsed_time(e1) / reps
+
+    copy_ms = t(lambda: b.copy_(a))
+    write_ms = t(lambda: a.fill_(3))
+    del a, b
+    torch.cuda.empty_cache()
+    return {"copy_gbs": round(2 * n / (copy_ms * 1e-3) / 1e9, 1), "write_gbs": round(n / (write_ms * 1e-3) / 1e9, 1),
+            "method": "torch copy_ (read + write bytes) and fill_ of 2 GiB, CUDA events, outside the timed region"}
+
+
 def ncu_traffic(kernel: str):
     """dram bytes per launch of `kernel` from the committed ncu summary, if any."""
     path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
@@ -528,6 +560,13 @@ def run_ours(args) -> None:
                 "kernel_ms": round(kms, 4), "step_share": round(kms / ms, 3), "alg_bytes": alg,
                 "peak_source": pk["source"],
                 "kernels_ms": {k: round(v[0], 4) for k, v in kernels.items()}}
+        try:
+            bx = box_peaks(dev)
+            bx["frac_vs_copy"] = round(achieved / bx["copy_gbs"], 4)
+            bx["frac_vs_write"] = round(achieved / bx["write_gbs"], 4)
+            roof["box_measured"] = bx
+        except RuntimeError as e:  # e.g. no room for the 4 GiB of probe buffers
+            roof["box_measured"] = {"unavailable": str(e).splitlines()[0]}
     line = {
         "metric": METRIC, "value": round(value, 2), "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": round(ms, 4), "higher_is_better": True, "scaling": "weak",
