@@ -26,10 +26,14 @@ __global__ void __launch_bounds__(256) fcarry_tiles_kernel(QuantParams q, int bi
                                                            int nbands, int band_rows, int tb, int suf_row0,
                                                            uint8_t* __restrict__ R8, uint16_t* __restrict__ C16,
                                                            uint32_t* __restrict__ T1, uint16_t* __restrict__ S16) {
+    // column counts as u16 pairs (a column's count within a band is < 2^16, as in C16):
+    // word h * 32 + lane of a bin row holds strip columns 4 lane + 2h (low) and + 2h + 1
+    // (high), i.e. already the C16 layout; half the shared memory of u32 counters, so a
+    // whole grid of tiles is resident in one wave
     extern __shared__ uint32_t fsm[];
-    uint32_t* cnt = fsm;                  // [tb bins][128 columns]
-    uint32_t* rh = fsm + tb * kStrip;     // [8 warps][128 bins]
-    uint32_t* cs = rh + 8 * kTileBins;    // [tb bins][128 columns]: window-start suffix counts
+    uint32_t* cnt = fsm;                     // [tb bins][64 words]
+    uint32_t* rh = fsm + tb * kStrip / 2;    // [8 warps][128 bins]
+    uint32_t* cs = rh + 8 * kTileBins;       // [tb bins][64 words]: window-start suffix counts
     const int s = blockIdx.x, j = blockIdx.y, kc0 = blockIdx.z * kTileBins;
     const int kcn = min(kTileBins, Lb - kc0);
     const bool need_r = s + 1 < nstrips, need_c = j + 1 < nbands;
@@ -37,9 +41,9 @@ __global__ void __launch_bounds__(256) fcarry_tiles_kernel(QuantParams q, int bi
     if (!need_r && !need_c) return;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     if (need_c)
-        for (int i = tid; i < tb * kStrip; i += 256) cnt[i] = 0;
+        for (int i = tid; i < tb * kStrip / 2; i += 256) cnt[i] = 0;
     if (need_s)
-        for (int i = tid; i < tb * kStrip; i += 256) cs[i] = 0;
+        for (int i = tid; i < tb * kStrip / 2; i += 256) cs[i] = 0;
     for (int i = tid; i < 8 * kTileBins; i += 256) rh[i] = 0;
     __syncthreads();
     const int y0 = j * band_rows, y1 = min(q.height, y0 + band_rows);
@@ -47,7 +51,8 @@ __global__ void __launch_bounds__(256) fcarry_tiles_kernel(QuantParams q, int bi
     const int x = s * kStrip + 4 * lane;
     const int klo = bin0 + kc0, khi = min(kcn, bins - kc0);
     uint32_t* rw = rh + warp * kTileBins;
-    // column 4 lane + c of the strip is counted at c * 32 + lane (conflict-free atomics)
+    // column 4 lane + c of the strip is counted in word (c >> 1) * 32 + lane, half c & 1
+    // (conflict-free atomics)
     const bool wide = G8 && x + 3 < q.width &&
                       ((reinterpret_cast<uintptr_t>(q.p0) + x) & 3) == 0 && (q.pitch & 3) == 0;
     auto bins4 = [&](int y, uint32_t w, int (&b)[4]) {
@@ -64,8 +69,8 @@ __global__ void __launch_bounds__(256) fcarry_tiles_kernel(QuantParams q, int bi
         for (int c = 0; c < 4; ++c) {
             const int k = b[c] - klo;
             if (b[c] >= 0 && static_cast<unsigned>(k) < static_cast<unsigned>(khi)) {
-                if (need_c) atomicAdd(&cnt[k * kStrip + c * 32 + lane], 1u);
-                if (need_s && y >= ys) atomicAdd(&cs[k * kStrip + c * 32 + lane], 1u);
+                if (need_c) atomicAdd(&cnt[k * (kStrip / 2) + (c >> 1) * 32 + lane], 1u << (16 * (c & 1)));
+                if (need_s && y >= ys) atomicAdd(&cs[k * (kStrip / 2) + (c >> 1) * 32 + lane], 1u << (16 * (c & 1)));
                 if (need_r) atomicAdd(&rw[k], 1u);
             }
         }
@@ -108,19 +113,19 @@ __global__ void __launch_bounds__(256) fcarry_tiles_kernel(QuantParams q, int bi
     const int Wp = nstrips * kStrip;
     for (int i = tid; i < kcn * (kStrip / 4); i += 256) {
         const int k = i / (kStrip / 4), l = i % (kStrip / 4);  // columns 4 l .. 4 l + 3
-        const uint32_t* ck = cnt + k * kStrip + l;
-        const uint2 v = make_uint2(ck[0] | (ck[32] << 16), ck[64] | (ck[96] << 16));
+        const uint32_t* ck = cnt + k * (kStrip / 2) + l;
         const int64_t o = (static_cast<int64_t>(j) * Lb + kc0 + k) * Wp + s * kStrip + 4 * l;
-        *reinterpret_cast<uint2*>(C16 + o) = v;
+        *reinterpret_cast<uint2*>(C16 + o) = make_uint2(ck[0], ck[32]);
         if (need_s) {
-            const uint32_t* cq = cs + k * kStrip + l;
-            *reinterpret_cast<uint2*>(S16 + o) = make_uint2(cq[0] | (cq[32] << 16), cq[64] | (cq[96] << 16));
+            const uint32_t* cq = cs + k * (kStrip / 2) + l;
+            *reinterpret_cast<uint2*>(S16 + o) = make_uint2(cq[0], cq[32]);
         }
     }
     // band x strip totals, [kl][j][s]
     for (int k = warp; k < kcn; k += 8) {
-        const uint32_t* ck = cnt + k * kStrip + lane;
-        uint32_t t = ck[0] + ck[32] + ck[64] + ck[96];
+        const uint32_t* ck = cnt + k * (kStrip / 2) + lane;
+        const uint32_t p0 = ck[0], p1 = ck[32];
+        uint32_t t = (p0 & 0xFFFFu) + (p0 >> 16) + (p1 & 0xFFFFu) + (p1 >> 16);
 #pragma unroll
         for (int o = 16; o; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
         if (lane == 0) T1[(static_cast<int64_t>(kc0 + k) * (nbands - 1) + j) * nstrips + s] = t;
@@ -255,7 +260,7 @@ spct_status build_fused_carries(const QuantParams& q, const spct_ih& out, const 
     // window-start rows in every band: [y0 + o, y1), o = (-(kh - 1)) mod band_rows
     const int suf_row0 = kh > 1 ? (p.band_rows - (kh - 1) % p.band_rows) % p.band_rows : 0;
     const int tb = std::min(p.Lb, kTileBins);
-    const size_t smem = (static_cast<size_t>(tb) * kStrip * (S16 ? 2 : 1) + 8 * kTileBins) * 4;
+    const size_t smem = (static_cast<size_t>(tb) * (kStrip / 2) * (S16 ? 2 : 1) + 8 * kTileBins) * 4;
     static size_t attr = 48 * 1024;
     if (smem > attr) {
         cudaFuncSetAttribute(fcarry_tiles_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
