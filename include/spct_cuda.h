@@ -248,7 +248,10 @@ spct_status spct_cu_hist_check(int nbins, int width, int height, const double* t
 /* hist_distance_map (likelihood.cpp:193-225) over a device tensor that holds ALL bins
  * (t->bin0 == 0, t->bins == t->nbins_total): map (dev) is height x width float64,
  * borders replicated as spread_valid (:44-58).  tmpl (dev) has nbins doubles.
- * MINKOWSKI follows the reference's operation order (k = 0..b-1, divide, pow). */
+ * MINKOWSKI follows the reference's operation order (k = 0..b-1, divide, pow); each
+ * window is divided by its actual total (:212-214; kw*kh for any tensor built from a
+ * bin map) and a massless window scores 0 (:215), so arbitrary (e.g. IHT1-loaded)
+ * tensors give the reference's map. */
 spct_status spct_cu_hist_match(const spct_ih* t, const double* tmpl, int kw, int kh, double p,
                                int metric, double* map, void* stream);
 
@@ -263,6 +266,11 @@ spct_status spct_cu_hist_partial(const spct_ih* t, const double* tmpl, int kw, i
  * reference's finalisation (likelihood.cpp:220-224) and spread_valid border replication. */
 spct_status spct_cu_hist_finalize(const double* partial, int width, int height, int kw, int kh,
                                   double p, int metric, double* map, void* stream);
+
+/* 1 if the fused sweeps below can produce a kw x kh window statistic without a stored
+ * tensor (16-bit running-histogram cells: kw <= 128, kh <= 255, kw*kh <= 65535), else 0.
+ * Callers recomputing a map from a tensor's source frame take that path only then. */
+int spct_cu_fused_window_ok(int kw, int kh);
 
 /* Fused build + match: one pass that writes the integral histogram of the slab
  * [out->bin0, out->bin0+out->bins) AND the slab's partial window statistic (as

@@ -73,6 +73,7 @@ SIGNATURES = {
     "spct_cu_hist_match": (_i, [_ih_p, _vp, _i, _i, _d, _i, _vp, _vp]),
     "spct_cu_hist_partial": (_i, [_ih_p, _vp, _i, _i, _d, _i, _vp, _i, _vp]),
     "spct_cu_hist_finalize": (_i, [_vp, _i, _i, _i, _i, _d, _i, _vp, _vp]),
+    "spct_cu_fused_window_ok": (_i, [_i, _i]),
     "spct_cu_ih_build_match": (_i, [_src_p, _ih_p, _vp, _i, _i, _d, _i, _vp, _vp, _sz, _vp]),
     "spct_cu_ih_build_match_map": (_i, [_src_p, _ih_p, _vp, _i, _i, _d, _i, _vp, _vp, _sz, _vp]),
     "spct_cu_orientation_workspace": (_i, [_i, _i, C.POINTER(_sz)]),

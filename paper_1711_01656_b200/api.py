@@ -120,7 +120,7 @@ def orientation_bins(gray, bins: int, sigma: float = 1.0, stream=None) -> torch.
     out = torch.empty((h, w), dtype=torch.int16, device=g.device)
     ws = C.c_size_t()
     check(A.lib().spct_cu_orientation_workspace(w, h, C.byref(ws)))
-    wbuf = _WS_ORIENT.get(ws.value, g.device)
+    wbuf = _WS_ORIENT.get(ws.value, g.device, stream)
     check(A.lib().spct_cu_orientation_bins(_ptr(g), w, w, h, float(sigma), int(bins), _ptr(out), w, _ptr(wbuf),
                                            wbuf.numel(), _stream(stream)))
     return out
@@ -236,15 +236,24 @@ def _check_budget(w, h, bins, budget):
 
 
 class Workspace:
-    """Reusable device scratch for builds (carry tables)."""
+    """Reusable device scratch (carry tables), one buffer per device.  The buffer handed out
+    is recorded on the stream that will use it, so the caching allocator keeps a replaced
+    (smaller) buffer alive until work already queued on that stream has finished."""
 
     def __init__(self):
-        self.buf = None
+        self.bufs = {}
 
-    def get(self, nbytes: int, device) -> torch.Tensor:
-        if self.buf is None or self.buf.numel() < nbytes:
-            self.buf = torch.empty(max(nbytes, 256), dtype=torch.uint8, device=device)
-        return self.buf
+    def get(self, nbytes: int, device, stream=None) -> torch.Tensor:
+        dev = torch.device(device)
+        idx = dev.index if dev.index is not None else torch.cuda.current_device()
+        buf = self.bufs.get(idx)
+        if buf is None or buf.numel() < nbytes:
+            buf = torch.empty(max(nbytes, 256), dtype=torch.uint8, device=torch.device("cuda", idx))
+            self.bufs[idx] = buf
+        s = stream if stream is not None else torch.cuda.current_stream(idx)
+        if s != torch.cuda.default_stream(idx):
+            buf.record_stream(s)
+        return buf
 
 
 _WS = Workspace()
@@ -299,7 +308,7 @@ def build_integral_histogram(bm, nbins: int | None = None, schedule: ScanSchedul
     t = out or IntegralHistogramTensor(src.width, src.height, nbins, bin0, bins, device=keep[0].device)
     ws = C.c_size_t()
     check(A.lib().spct_cu_ih_build_workspace(C.byref(src), t.bin0, t.bins, C.byref(ws)))
-    wbuf = _WS.get(ws.value, keep[0].device)
+    wbuf = _WS.get(ws.value, keep[0].device, stream)
     check(A.lib().spct_cu_ih_build(C.byref(src), C.byref(t.desc), _ptr(wbuf), wbuf.numel(), _stream(stream)))
     if isinstance(bm, torch.Tensor) and bm.is_cuda:  # caller-owned device memory: keep a private copy
         keep = [k.clone() for k in keep]
@@ -357,12 +366,13 @@ def hist_match_map(t: IntegralHistogramTensor, tmpl, kw: int, kh: int, p: float 
     the reference's operation order instead: bit-identical to the reference for p = 1."""
     dt = _tmpl(tmpl, t.bins, t.width, t.height, kw, kh, p)
     out = torch.empty((t.height, t.width), dtype=torch.float64, device=dt.device)
-    if not exact and t.source is not None and t.bin0 == 0 and t.bins == t.nbins_total:
+    if (not exact and t.source is not None and t.bin0 == 0 and t.bins == t.nbins_total
+            and A.lib().spct_cu_fused_window_ok(kw, kh)):
         src, _keep = t.source
         nodata = A.spct_ih(None, t.bins, t.bin0, t.nbins_total, t.height, t.width, t.row_pitch, t.plane_pitch)
         ws = C.c_size_t()
         check(A.lib().spct_cu_ih_build_workspace(C.byref(src), 0, t.bins, C.byref(ws)))
-        wbuf = _WS.get(ws.value, dt.device)
+        wbuf = _WS.get(ws.value, dt.device, stream)
         check(A.lib().spct_cu_ih_build_match_map(C.byref(src), C.byref(nodata), _ptr(dt), kw, kh, p, metric,
                                                  _ptr(out), _ptr(wbuf), wbuf.numel(), _stream(stream)))
         return out
@@ -412,7 +422,7 @@ def build_and_match(frame, nbins: int, tmpl, kw: int, kh: int, p: float = 1.0, m
         partial = torch.empty((nv, nu), dtype=torch.float64, device=keep[0].device)
     ws = C.c_size_t()
     check(A.lib().spct_cu_ih_build_workspace(C.byref(src), t.bin0, t.bins, C.byref(ws)))
-    wbuf = _WS.get(ws.value, keep[0].device)
+    wbuf = _WS.get(ws.value, keep[0].device, stream)
     check(A.lib().spct_cu_ih_build_match(C.byref(src), C.byref(t.desc), _ptr(tmpl_dev), kw, kh, p, metric,
                                          _ptr(partial), _ptr(wbuf), wbuf.numel(), _stream(stream)))
     return t, partial
@@ -433,7 +443,7 @@ def build_and_match_map(frame, nbins: int, tmpl, kw: int, kh: int, p: float = 1.
         lmap = torch.empty((src.height, src.width), dtype=torch.float64, device=keep[0].device)
     ws = C.c_size_t()
     check(A.lib().spct_cu_ih_build_workspace(C.byref(src), t.bin0, t.bins, C.byref(ws)))
-    wbuf = _WS.get(ws.value, keep[0].device)
+    wbuf = _WS.get(ws.value, keep[0].device, stream)
     check(A.lib().spct_cu_ih_build_match_map(C.byref(src), C.byref(t.desc), _ptr(tmpl_dev), kw, kh, p, metric,
                                              _ptr(lmap), _ptr(wbuf), wbuf.numel(), _stream(stream)))
     return t, lmap

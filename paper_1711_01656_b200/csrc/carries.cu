@@ -261,12 +261,8 @@ spct_status build_fused_carries(const QuantParams& q, const spct_ih& out, const 
     const int suf_row0 = kh > 1 ? (p.band_rows - (kh - 1) % p.band_rows) % p.band_rows : 0;
     const int tb = std::min(p.Lb, kTileBins);
     const size_t smem = (static_cast<size_t>(tb) * (kStrip / 2) * (S16 ? 2 : 1) + 8 * kTileBins) * 4;
-    static size_t attr = 48 * 1024;
-    if (smem > attr) {
-        cudaFuncSetAttribute(fcarry_tiles_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        cudaFuncSetAttribute(fcarry_tiles_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        attr = smem;
-    }
+    ensure_smem(fcarry_tiles_kernel<true>, smem);
+    ensure_smem(fcarry_tiles_kernel<false>, smem);
     dim3 g(p.nstrips, p.nbands, static_cast<unsigned>(ceil_div(p.Lb, kTileBins)));
     if (q.kind == SPCT_SRC_GRAY_U8 && q.fast_u8)
         fcarry_tiles_kernel<true><<<g, 256, smem, s>>>(q, out.bin0, out.bins, p.Lb, p.nstrips, p.nbands, p.band_rows, tb,
@@ -281,11 +277,7 @@ spct_status build_fused_carries(const QuantParams& q, const spct_ih& out, const 
     const size_t tsm = A32 ? static_cast<size_t>(p.nbands - 1) * p.nstrips * 4 : 0;
     if (tsm > 200 * 1024) return contract("ih_build_match: image too large for the fused carry tables");
     if (nb_lt + nb_c + nb_a > 0) {
-        static size_t attr = 48 * 1024;
-        if (tsm > attr) {
-            cudaFuncSetAttribute(fcarry_prefix_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tsm);
-            attr = tsm;
-        }
+        ensure_smem(fcarry_prefix_kernel, tsm);
         fcarry_prefix_kernel<<<nb_lt + nb_c + nb_a, 256, tsm, s>>>(out.height, p.Lb, p.Wp, p.nstrips, p.nbands, nb_lt,
                                                                    nb_c, R8, Lt16, C16, A32);
         if (auto st = launch_status("fcarry_prefix_kernel")) return st;

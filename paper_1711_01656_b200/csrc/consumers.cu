@@ -71,11 +71,13 @@ __device__ __forceinline__ bool is_peak_xy(const double* s, int w, int h, int x,
     const double* c = s + static_cast<int64_t>(y) * w + x;
     const double v = *c;
     if (x > 0 && y > 0 && x + 1 < w && y + 1 < h) {  // interior: no bounds checks
+        // the exact negation of the reference's rejection test `n + 1e-9 >= v`
+        // (likelihood.cpp:316), so NaN neighbours / centres behave as on the border
         const double* up = c - w;
         const double* dn = c + w;
-        return __dadd_rn(up[-1], 1e-9) < v && __dadd_rn(up[0], 1e-9) < v && __dadd_rn(up[1], 1e-9) < v &&
-               __dadd_rn(c[-1], 1e-9) < v && __dadd_rn(c[1], 1e-9) < v && __dadd_rn(dn[-1], 1e-9) < v &&
-               __dadd_rn(dn[0], 1e-9) < v && __dadd_rn(dn[1], 1e-9) < v;
+        return !(__dadd_rn(up[-1], 1e-9) >= v) && !(__dadd_rn(up[0], 1e-9) >= v) && !(__dadd_rn(up[1], 1e-9) >= v) &&
+               !(__dadd_rn(c[-1], 1e-9) >= v) && !(__dadd_rn(c[1], 1e-9) >= v) && !(__dadd_rn(dn[-1], 1e-9) >= v) &&
+               !(__dadd_rn(dn[0], 1e-9) >= v) && !(__dadd_rn(dn[1], 1e-9) >= v);
     }
     for (int dy = -1; dy <= 1; ++dy)
         for (int dx = -1; dx <= 1; ++dx) {

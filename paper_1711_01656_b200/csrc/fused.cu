@@ -50,6 +50,7 @@ spct_status build_match(const spct_source* src, const spct_ih* out, const double
     if (auto st = check_ih(out)) return st;
     if (out->width != src->width || out->height != src->height || out->nbins_total != src->nbins)
         return contract("ih_build_match: tensor dims do not match the source");
+    if (auto st = check_carry_dims(out->width, out->height)) return st;
     if (out->data && reinterpret_cast<uintptr_t>(out->data) % 16 != 0)
         return contract("ih_build_match: tensor data must be 16-byte aligned");
     if (!(p >= 1.0)) return contract("hist_distance_map: Minkowski order must be >= 1");
@@ -61,8 +62,7 @@ spct_status build_match(const spct_source* src, const spct_ih* out, const double
         return contract("ih_build_match_map: the slab must hold every bin (use the partial form for slabs)");
     cudaStream_t s = as_stream(stream);
     const int64_t T = static_cast<int64_t>(kw) * kh;
-    // 16-bit running-histogram cells
-    const bool fusable = kw <= 128 && kh <= 255 && T <= 65535;
+    const bool fusable = spct_cu_fused_window_ok(kw, kh) != 0;
     const int ngroups = static_cast<int>(ceil_div(out->bins, kGroupBins));
     if (fusable && map && ngroups > 1) {
         // more than one 128-bin group: accumulate the groups' partials, then finalise
@@ -164,6 +164,11 @@ spct_status build_match(const spct_source* src, const spct_ih* out, const double
 }
 
 }  // namespace spct_fused
+
+extern "C" int spct_cu_fused_window_ok(int kw, int kh) {
+    // 16-bit running-histogram cells (fused_kernel.cuh)
+    return kw >= 1 && kh >= 1 && kw <= 128 && kh <= 255 && static_cast<int64_t>(kw) * kh <= 65535;
+}
 
 extern "C" spct_status spct_cu_ih_build_match(const spct_source* src, const spct_ih* out, const double* tmpl, int kw,
                                               int kh, double p, int metric, double* partial, void* workspace,

@@ -694,14 +694,10 @@ void launch_variants(dim3 grid, cudaStream_t s, const QuantParams& q, const Pixe
                      const BuildPlan& bp, const FusedCarries& fc, const FusedParams& f) {
     constexpr int NT = 32 * NW;
     constexpr size_t SM = smem_bytes_nw<NW>();
-    static bool attr_set = false;
-    if (!attr_set) {
-        cudaFuncSetAttribute(sweep_match_kernel<true, true, KWM, ALLB, SK, NW>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SM);
-        cudaFuncSetAttribute(sweep_match_kernel<true, false, KWM, false, SK, NW>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SM);
-        cudaFuncSetAttribute(sweep_match_kernel<false, true, KWM, ALLB, SK, NW>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SM);
-        cudaFuncSetAttribute(sweep_match_kernel<false, false, KWM, false, SK, NW>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SM);
-        attr_set = true;
-    }
+    ensure_smem(sweep_match_kernel<true, true, KWM, ALLB, SK, NW>, SM);
+    ensure_smem(sweep_match_kernel<true, false, KWM, false, SK, NW>, SM);
+    ensure_smem(sweep_match_kernel<false, true, KWM, ALLB, SK, NW>, SM);
+    ensure_smem(sweep_match_kernel<false, false, KWM, false, SK, NW>, SM);
     // integer (template-crop) variant and FP64 variant: the one not selected by the
     // device-side template prep exits on entry
     if (out.data) {

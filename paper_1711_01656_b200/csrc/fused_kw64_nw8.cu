@@ -12,28 +12,29 @@ size_t smem_bytes() { return kSmemBytes; }
 
 namespace spct_impl {
 int fused_ctas_per_sm(int nw) {
-    static int n[9] = {};
     nw = nw >= 8 ? 8 : (nw >= 4 ? 4 : 2);
-    if (n[nw]) return n[nw];
-    int v = 0;
-    cudaError_t e;
-    if (nw == 8) {
-        auto k = spct_fused::sweep_match_kernel<true, true, 64, true, 1, 8>;
-        cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)spct_fused::smem_bytes_nw<8>());
-        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&v, k, 256, spct_fused::smem_bytes_nw<8>());
-    } else if (nw == 4) {
-        auto k = spct_fused::sweep_match_kernel<true, true, 64, true, 1, 4>;
-        cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)spct_fused::smem_bytes_nw<4>());
-        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&v, k, 128, spct_fused::smem_bytes_nw<4>());
-    } else {
-        auto k = spct_fused::sweep_match_kernel<true, true, 64, true, 1, 2>;
-        cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)spct_fused::smem_bytes_nw<2>());
-        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&v, k, 64, spct_fused::smem_bytes_nw<2>());
-    }
-    if (e != cudaSuccess || v <= 0) {
-        cudaGetLastError();
-        v = 16 / nw;
-    }
-    return n[nw] = v;
+    return per_device_int(200 + nw, [](int key) {
+        const int nw = key - 200;
+        int v = 0;
+        cudaError_t e;
+        if (nw == 8) {
+            auto k = spct_fused::sweep_match_kernel<true, true, 64, true, 1, 8>;
+            ensure_smem(k, spct_fused::smem_bytes_nw<8>());
+            e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&v, k, 256, spct_fused::smem_bytes_nw<8>());
+        } else if (nw == 4) {
+            auto k = spct_fused::sweep_match_kernel<true, true, 64, true, 1, 4>;
+            ensure_smem(k, spct_fused::smem_bytes_nw<4>());
+            e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&v, k, 128, spct_fused::smem_bytes_nw<4>());
+        } else {
+            auto k = spct_fused::sweep_match_kernel<true, true, 64, true, 1, 2>;
+            ensure_smem(k, spct_fused::smem_bytes_nw<2>());
+            e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&v, k, 64, spct_fused::smem_bytes_nw<2>());
+        }
+        if (e != cudaSuccess || v <= 0) {
+            cudaGetLastError();
+            v = 16 / nw;
+        }
+        return v;
+    });
 }
 }  // namespace spct_impl

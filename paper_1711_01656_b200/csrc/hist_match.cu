@@ -35,14 +35,14 @@ struct MatchParams {
     int T_pow2;   // kw*kh is a power of two: c / T == c * (1/T) exactly
     int metric;
     int p_kind;   // 1: p == 1, 2: p == 2, 0: general pow
+    int norm;     // 1: divide by the window's actual total (full tensors, likelihood.cpp:212-214)
 };
 
 // Per-bin term of the window statistic.  MINKOWSKI follows likelihood.cpp:218-219
 // operation by operation: q = h[k] / total (IEEE divide; exact multiply when T is a
 // power of two), |q - t|, pow(., p) (identity for p == 1, x*x for p == 2).
-__device__ __forceinline__ double bin_term(uint32_t c, double t, const MatchParams& m) {
-    const double cd = static_cast<double>(c);
-    const double q = m.T_pow2 ? __dmul_rn(cd, m.invT) : __ddiv_rn(cd, m.T);
+__device__ __forceinline__ double bin_term(double cd, double t, const MatchParams& m, double total, double inv_total) {
+    const double q = inv_total != 0.0 ? __dmul_rn(cd, inv_total) : __ddiv_rn(cd, total);
     switch (m.metric) {
         case SPCT_METRIC_MINKOWSKI: {
             const double a = fabs(__dsub_rn(q, t));
@@ -64,6 +64,7 @@ __device__ __forceinline__ double bin_term(uint32_t c, double t, const MatchPara
 }
 
 __device__ __forceinline__ double finalize_value(double s, const MatchParams& m, double dmax) {
+    if (s < 0.0) return 0.0;  // massless window (likelihood.cpp:215): no match
     double L;
     switch (m.metric) {
         case SPCT_METRIC_MINKOWSKI: {
@@ -80,21 +81,52 @@ __device__ __forceinline__ double finalize_value(double s, const MatchParams& m,
     return L < 0.0 ? 0.0 : (L > 1.0 ? 1.0 : L);
 }
 
+// Window count of plane k: region_histogram (integral.cpp:561-577) in the reference's
+// uint64 arithmetic (wraps like the reference for a tensor that is not monotone), as the
+// double the reference divides.
+__device__ __forceinline__ double window_count(const spct_ih& t, int k, int ya, int yb, int xa, int xb) {
+    const uint32_t* pl = t.data + static_cast<int64_t>(k) * t.plane_pitch;
+    const uint64_t c = static_cast<uint64_t>(H_at(pl, t.row_pitch, yb, xb)) - H_at(pl, t.row_pitch, ya, xb) -
+                       H_at(pl, t.row_pitch, yb, xa) + H_at(pl, t.row_pitch, ya, xa);
+    return static_cast<double>(c);
+}
+
 // One thread per valid window (u, v); planes visited in order k = 0 .. bins-1 so the
-// per-window sum has the reference's rounding sequence when the tensor holds every bin.
+// per-window sum has the reference's rounding sequence when the tensor holds every bin
+// (likelihood.cpp:211-219).  With m.norm the window's histogram is divided by its actual
+// total (the reference's `total`); the first pass assumes total == kw * kh (true for every
+// tensor built from a bin map) while summing the real total, and a window whose total
+// differs is recomputed; a massless window gets the sentinel -1 (finalised to 0).
 __global__ void __launch_bounds__(256) match_partial_kernel(spct_ih t, const double* __restrict__ tmpl, MatchParams m,
                                                             double* __restrict__ partial, int accumulate) {
     const int64_t n = static_cast<int64_t>(m.nu) * m.nv;
     for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
          i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
         const int u = static_cast<int>(i % m.nu), v = static_cast<int>(i / m.nu);
-        double s = accumulate ? partial[i] : 0.0;
+        const double s0 = accumulate ? partial[i] : 0.0;
         const int ya = v, yb = v + m.kh, xa = u, xb = u + m.kw;
-        for (int k = 0; k < t.bins; ++k) {
-            const uint32_t* pl = t.data + static_cast<int64_t>(k) * t.plane_pitch;
-            const uint32_t c = H_at(pl, t.row_pitch, yb, xb) - H_at(pl, t.row_pitch, ya, xb) -
-                               H_at(pl, t.row_pitch, yb, xa) + H_at(pl, t.row_pitch, ya, xa);
-            s = __dadd_rn(s, bin_term(c, __ldg(tmpl + t.bin0 + k), m));
+        const double invT = m.T_pow2 ? m.invT : 0.0;
+        double s = s0, total = 0.0;
+        for (int k = 0; k < t.bins; k += 4) {
+            double c[4];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) c[j] = k + j < t.bins ? window_count(t, k + j, ya, yb, xa, xb) : 0.0;
+#pragma unroll
+            for (int j = 0; j < 4; ++j)
+                if (k + j < t.bins) {
+                    total = __dadd_rn(total, c[j]);
+                    s = __dadd_rn(s, bin_term(c[j], __ldg(tmpl + t.bin0 + k + j), m, m.T, invT));
+                }
+        }
+        if (m.norm && total != m.T) {
+            if (!(total > 0.0)) {
+                s = -1.0;
+            } else {
+                s = s0;
+                for (int k = 0; k < t.bins; ++k)
+                    s = __dadd_rn(s, bin_term(window_count(t, k, ya, yb, xa, xb), __ldg(tmpl + t.bin0 + k), m, total,
+                                              0.0));
+            }
         }
         partial[i] = s;
     }
@@ -154,6 +186,7 @@ spct_status make_match(int width, int height, int kw, int kh, double p, int metr
     m->T = static_cast<double>(T);
     m->invT = 1.0 / m->T;
     m->T_pow2 = (T & (T - 1)) == 0;
+    m->norm = 0;
     return SPCT_OK;
 }
 
@@ -223,17 +256,25 @@ extern "C" spct_status spct_cu_region_counts(const spct_ih* t, const int32_t* re
     return launch_status("region_counts");
 }
 
-extern "C" spct_status spct_cu_hist_partial(const spct_ih* t, const double* tmpl, int kw, int kh, double p, int metric,
-                                            double* partial, int accumulate, void* stream) {
+namespace {
+spct_status hist_partial_impl(const spct_ih* t, const double* tmpl, int kw, int kh, double p, int metric,
+                              double* partial, int accumulate, int norm, void* stream) {
     if (auto st = check_ih(t)) return st;
     MatchParams m;
     if (auto st = make_match(t->width, t->height, kw, kh, p, metric, &m)) return st;
+    m.norm = norm;
     if (!tmpl || !partial || !t->data) return contract("hist_partial: null pointer");
     const int64_t n = static_cast<int64_t>(m.nu) * m.nv;
     const int prof = prof_begin("match_partial", as_stream(stream));
     match_partial_kernel<<<grid_for(n, 256), 256, 0, as_stream(stream)>>>(*t, tmpl, m, partial, accumulate);
     prof_end(prof, as_stream(stream));
     return launch_status("match_partial_kernel");
+}
+}  // namespace
+
+extern "C" spct_status spct_cu_hist_partial(const spct_ih* t, const double* tmpl, int kw, int kh, double p, int metric,
+                                            double* partial, int accumulate, void* stream) {
+    return hist_partial_impl(t, tmpl, kw, kh, p, metric, partial, accumulate, 0, stream);
 }
 
 extern "C" spct_status spct_cu_hist_finalize(const double* partial, int width, int height, int kw, int kh, double p,
@@ -260,7 +301,8 @@ extern "C" spct_status spct_cu_hist_match(const spct_ih* t, const double* tmpl, 
     double* part = nullptr;
     const int64_t n = static_cast<int64_t>(m.nu) * m.nv;
     if (auto st = cuda_status(malloc_async(&part, n * sizeof(double), s), "hist_match alloc")) return st;
-    spct_status st = spct_cu_hist_partial(t, tmpl, kw, kh, p, metric, part, 0, stream);
+    // the full histogram is here: normalise by each window's actual total like the reference
+    spct_status st = hist_partial_impl(t, tmpl, kw, kh, p, metric, part, 0, 1, stream);
     if (st == SPCT_OK) st = spct_cu_hist_finalize(part, t->width, t->height, kw, kh, p, metric, map, stream);
     cudaFreeAsync(part, s);
     return st;

@@ -594,7 +594,7 @@ void hist_match_map_into(const IntegralHistogramTensor& t, const std::vector<dou
     DevBuf tm(th.size() * 8), map(std::size_t(t.width) * t.height * 8);
     upload(tm, th);
     const detail::DeviceTensor& dt = *t.data.dev;
-    if (dt.src_mem && !exact_maps()) {
+    if (dt.src_mem && !exact_maps() && spct_cu_fused_window_ok(kw, kh)) {
         // recompute the window counts from the source in the fused sweep (no tensor re-read)
         spct_ih nodata = d;
         nodata.data = nullptr;

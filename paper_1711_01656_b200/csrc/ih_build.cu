@@ -29,16 +29,14 @@ namespace spct_impl {
 // ------------------------------------------------------------------ planning
 
 int device_sms() {
-    static int sms = [] {
-        int dev = 0, n = 0;
-        if (cudaGetDevice(&dev) != cudaSuccess ||
-            cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || n <= 0) {
+    return per_device_int(0, [](int) {
+        int n = 0;
+        if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, current_device()) != cudaSuccess || n <= 0) {
             cudaGetLastError();
             return 148;  // B200
         }
         return n;
-    }();
-    return sms;
+    });
 }
 
 BuildPlan plan_build(int width, int height, int bins, int force_B, int ctas_per_sm, int min_band_rows) {
@@ -119,6 +117,12 @@ spct_status check_ih(const spct_ih* t) {
     if (t->row_pitch < t->width || t->row_pitch % 32 != 0) return contract("tensor: row_pitch must be >= width and a multiple of 32");
     if (t->plane_pitch < t->row_pitch * t->height || t->plane_pitch % 32 != 0)
         return contract("tensor: plane_pitch must be >= height*row_pitch and a multiple of 32");
+    return SPCT_OK;
+}
+
+spct_status check_carry_dims(int width, int height) {
+    if (width >= 65536 || height >= 65536)
+        return contract("build: width and height must be below 65536 (16-bit carry tables)");
     return SPCT_OK;
 }
 
@@ -250,19 +254,20 @@ using namespace spct_build;
 namespace spct_impl {
 
 int build_ctas_per_sm(int B, int threads) {
-    static int cache[3][9] = {};
     const int bi = B == 4 ? 0 : (B == 8 ? 1 : 2), wi = std::min(8, std::max(1, threads / 32));
-    if (cache[bi][wi]) return cache[bi][wi];
-    int n = 0;
-    cudaError_t e;
-    if (B == 4) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, ih_sweep_kernel<4, false, 0>, threads, 0);
-    else if (B == 8) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, ih_sweep_kernel<8, false, 0>, threads, 0);
-    else e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, ih_sweep_kernel<16, false, 0>, threads, 0);
-    if (e != cudaSuccess || n <= 0) {
-        cudaGetLastError();
-        n = 2;
-    }
-    return cache[bi][wi] = n;
+    return per_device_int(100 + 16 * bi + wi, [](int key) {
+        const int bi = (key - 100) / 16, threads = 32 * ((key - 100) % 16);
+        int n = 0;
+        cudaError_t e;
+        if (bi == 0) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, ih_sweep_kernel<4, false, 0>, threads, 0);
+        else if (bi == 1) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, ih_sweep_kernel<8, false, 0>, threads, 0);
+        else e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, ih_sweep_kernel<16, false, 0>, threads, 0);
+        if (e != cudaSuccess || n <= 0) {
+            cudaGetLastError();
+            n = 2;
+        }
+        return n;
+    });
 }
 
 BuildPlan plan_build_sweep(int width, int height, int bins) {
@@ -371,6 +376,7 @@ spct_status build_mode(const spct_source* src, const spct_ih* out, void* workspa
     if (auto st = make_quant(src, &q)) return st;
     if (auto st = check_ih(out)) return st;
     if (!out->data) return contract("ih_build: null tensor data");
+    if (auto st = check_carry_dims(out->width, out->height)) return st;
     if (out->width != src->width || out->height != src->height || out->nbins_total != src->nbins)
         return contract("ih_build: tensor dims do not match the source");
     if (reinterpret_cast<uintptr_t>(out->data) % 16 != 0) return contract("ih_build: tensor data must be 16-byte aligned");

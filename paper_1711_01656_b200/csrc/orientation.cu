@@ -236,13 +236,8 @@ extern "C" spct_status spct_cu_orientation_bins(const uint8_t* gray, int64_t pit
         bounds_kernel<<<1, 256, 0, s>>>(bins, bounds);
         if (auto st = launch_status("bounds_kernel")) return st;
     }
-    static bool attr = false;
-    if (!attr) {
-        const int mx = static_cast<int>(tile_smem(kMaxRadius));
-        cudaFuncSetAttribute(orientation_tile_kernel<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
-        cudaFuncSetAttribute(orientation_tile_kernel<-1>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
-        attr = true;
-    }
+    ensure_smem(orientation_tile_kernel<3>, tile_smem(kMaxRadius));
+    ensure_smem(orientation_tile_kernel<-1>, tile_smem(kMaxRadius));
     const dim3 grid(static_cast<unsigned>(ceil_div(width, kTX)), static_cast<unsigned>(ceil_div(height, kTY)));
     const size_t smem = tile_smem(t.radius);
     static const bool force_generic = std::getenv("SPCT_ORIENT_GENERIC") != nullptr;

@@ -1,5 +1,6 @@
 // Launch counting and per-kernel CUDA-event timing for bench.py (spct_cu_profile_*).
 #include <atomic>
+#include <map>
 #include <mutex>
 #include <string>
 #include <vector>
@@ -83,6 +84,41 @@ extern "C" spct_status spct_cu_profile_read(const char* kernel, double* total_ms
 }
 
 namespace spct_impl {
+
+int current_device() {
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) {
+        cudaGetLastError();
+        dev = 0;
+    }
+    return dev;
+}
+
+void ensure_smem(const void* func, size_t bytes) {
+    static std::mutex mu;
+    static std::map<std::pair<int, const void*>, size_t> done;
+    const int dev = current_device();
+    std::lock_guard<std::mutex> lock(mu);
+    size_t& cur = done[{dev, func}];
+    if (bytes <= cur || bytes <= 48 * 1024) return;
+    cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(bytes));
+    cudaGetLastError();
+    cur = bytes;
+}
+
+int per_device_int(int key, int (*compute)(int key)) {
+    static std::mutex mu;
+    static std::map<std::pair<int, int>, int> cache;
+    const int dev = current_device();
+    {
+        std::lock_guard<std::mutex> lock(mu);
+        auto it = cache.find({dev, key});
+        if (it != cache.end()) return it->second;
+    }
+    const int v = compute(key);  // outside the lock: may itself call ensure_smem
+    std::lock_guard<std::mutex> lock(mu);
+    return cache.emplace(std::make_pair(dev, key), v).first->second;
+}
 
 cudaError_t malloc_async(void** p, size_t bytes, cudaStream_t s) {
     static std::mutex mu;

@@ -37,6 +37,19 @@ inline spct_status launch_status(const char* where) {
 
 inline cudaStream_t as_stream(void* s) { return static_cast<cudaStream_t>(s); }
 
+// Per-device launch state (profile.cu).  A process may drive several GPUs from one or more
+// host threads, so nothing launch-related is cached process-wide: the dynamic shared-memory
+// limit of a kernel is raised once per (device, kernel) and cached occupancy / SM counts
+// are keyed by the current device; both are guarded by a mutex.
+int current_device();
+void ensure_smem(const void* func, size_t bytes);
+template <class F>
+void ensure_smem(F* func, size_t bytes) {
+    ensure_smem(reinterpret_cast<const void*>(func), bytes);
+}
+// Cached per-device integer: compute() runs once per (device, key).
+int per_device_int(int key, int (*compute)(int key));
+
 // Stream-ordered scratch allocation (profile.cu): cudaMallocAsync from the device's default
 // pool, which is set once per device to keep freed memory (no release threshold), so
 // repeated calls reuse it instead of going back to the driver.
@@ -54,6 +67,9 @@ spct_status make_quant(const spct_source* src, spct_dev::QuantParams* q);
 
 // Validate a device tensor descriptor.
 spct_status check_ih(const spct_ih* t);
+// The sweeps' carry tables hold row / column counts as u16 (carries.cu): both image
+// dimensions must stay below 2^16 on the build and fused paths.
+spct_status check_carry_dims(int width, int height);
 
 // Bins per warp and band height used by the build for a given slab size / image.
 struct BuildPlan {

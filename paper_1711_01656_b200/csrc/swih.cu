@@ -435,11 +435,7 @@ spct_status wih_sweep_launch(const uint16_t* bins, int64_t pitch, const uint64_t
             return st;
         const int kc = std::min(t.bins, 64);
         const size_t smem = static_cast<size_t>(kc) * kSweepThreads * 8;
-        static bool attr = false;
-        if (!attr) {
-            cudaFuncSetAttribute(wih_band_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * kSweepThreads * 8);
-            attr = true;
-        }
+        ensure_smem(wih_band_kernel, 64 * kSweepThreads * 8);
         for (int kc0 = 0; kc0 < t.bins; kc0 += kc) {
             const int kcn = std::min(kc, t.bins - kc0);
             wih_band_kernel<<<dim3(static_cast<unsigned>(ceil_div(t.width, kSweepThreads)), nbands - 1), kSweepThreads,

@@ -246,21 +246,13 @@ extern "C" spct_status spct_cu_swlh_map_direct(const uint16_t* bins, int64_t pit
     const int strips = static_cast<int>(ceil_div(nu, kNC));
     // bands: about two waves of the resident CTA slots, at least kh rows each (the
     // band-start state costs kh rows of loads)
-    int sms = 148;
-    {
-        int dev = 0;
-        if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    }
+    const int sms = device_sms();
     const int64_t want = ceil_div(static_cast<int64_t>(sms) * 2 * 2, strips);
     const int nbands = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(want, nv / std::max(1, kh))));
     p.band_rows = static_cast<int>(ceil_div(nv, nbands));
     const dim3 grid(strips, static_cast<unsigned>(ceil_div(nv, p.band_rows)));
     const size_t smem = smem_bytes();
-    static bool attr = false;
-    if (!attr) {
-        cudaFuncSetAttribute(swlh_fused_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-        attr = true;
-    }
+    ensure_smem(swlh_fused_kernel, smem);
     // W / mass for every possible window sum W (0 .. mass): one division per value instead
     // of one per window and bin
     double* qtab = nullptr;

@@ -65,7 +65,7 @@ class MedianBackgroundIH:
         src = _source(A.SRC_BINS_U16, [bm], self.width, self.height, self.bins)
         ws = C.c_size_t()
         check(A.lib().spct_cu_ih_build_workspace(C.byref(src), 0, self.bins, C.byref(ws)))
-        wb = _WS.get(ws.value, bm.device)
+        wb = _WS.get(ws.value, bm.device, self.stream)
         check(A.lib().spct_cu_ih_accumulate(C.byref(src), C.byref(self.joint.desc), sign, _ptr(wb), wb.numel(),
                                             _stream(self.stream)))
 

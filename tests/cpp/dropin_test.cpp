@@ -182,6 +182,17 @@ int main() {
         CHECK(tf.data == t.data);
         for (std::size_t i = 0; i < mf.values.size(); ++i)
             CHECK(std::abs(mf.values[i] - map.values[i]) <= 1e-5 * std::abs(map.values[i]) + 1e-12);
+        // a window too large for the fused sweep (kw > 128): the map comes from the stored
+        // tensor in the default mode too, no contract error
+        GrayImage big(240, 180);
+        for (auto& p : big.data) p = static_cast<std::uint8_t>(d(rng));
+        auto tb = build_integral_histogram(quantize(big, 6));
+        std::vector<double> flat(6, 1.0 / 6);
+        LikelihoodMap lb = hist_distance_map(tb, flat, 200, 150, 1.0);
+        set_exact_maps(true);
+        LikelihoodMap lbx = hist_distance_map(tb, flat, 200, 150, 1.0);
+        set_exact_maps(false);
+        CHECK(lb.values == lbx.values && lb.width == 240 && lb.height == 180);
     }
     {  // map consumers (test_likelihood.cpp:296-362, test_tracker.cpp:150-176)
         LikelihoodMap a;

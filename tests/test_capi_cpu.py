@@ -212,3 +212,33 @@ def test_next_rows_and_peer_contracts_before_device_work():
     assert lib.spct_cu_hist_finalize_slots(1, 2, 36, 8, 8, 3, 3, 0.5, 0, 1, None) == A.SPCT_ERR_CONTRACT
     assert b"Minkowski order must be >= 1" in err()
     assert lib.spct_cu_peer_open(None, None) == A.SPCT_ERR_CONTRACT
+
+
+def test_carry_tables_reject_dims_beyond_u16():
+    """Row / column counts of the sweeps' carry tables are 16-bit (carries.cu): a build or
+    fused sweep over a 70000 x 500 image is refused with a contract error before any
+    launch, instead of silently wrapping."""
+    lib = A.lib()
+    fake = 0x1000  # never dereferenced: the checks run before any device work
+    for w, h in [(70000, 500), (500, 70000)]:
+        src = A.spct_source()
+        src.kind, src.width, src.height, src.nbins, src.pitch, src.lo, src.hi = A.SRC_GRAY_U8, w, h, 8, w, 0.0, 256.0
+        src.plane[0] = fake
+        rp, pp, nb = C.c_int64(), C.c_int64(), C.c_uint64()
+        A.check(lib.spct_cu_ih_layout(w, h, 8, C.byref(rp), C.byref(pp), C.byref(nb)))
+        t = A.spct_ih(fake * 16, 8, 0, 8, h, w, rp.value, pp.value)
+        assert lib.spct_cu_ih_build(C.byref(src), C.byref(t), None, 0, None) == A.SPCT_ERR_CONTRACT
+        assert b"65536" in lib.spct_cu_last_error()
+        tm = (C.c_double * 8)()
+        assert lib.spct_cu_ih_build_match_map(C.byref(src), C.byref(t), tm, 4, 4, 1.0, 0, fake * 16, None, 0,
+                                              None) == A.SPCT_ERR_CONTRACT
+        assert b"65536" in lib.spct_cu_last_error()
+
+
+def test_fused_window_predicate():
+    lib = A.lib()
+    assert lib.spct_cu_fused_window_ok(64, 64) == 1
+    assert lib.spct_cu_fused_window_ok(128, 255) == 1
+    assert lib.spct_cu_fused_window_ok(129, 10) == 0
+    assert lib.spct_cu_fused_window_ok(10, 256) == 0
+    assert lib.spct_cu_fused_window_ok(0, 10) == 0
