@@ -62,6 +62,8 @@ def find_peaks(m, max_out: int | None = None, stream=None):
     wb = _ws(h, w, t.device)
     check(A.lib().spct_cu_find_peaks(_ptr(t), w, h, _ptr(xs), _ptr(ys), _ptr(hs), cap, C.byref(cnt), _ptr(wb),
                                      wb.numel(), _stream(stream)))
+    if max_out is None and cnt.value > cap:  # NaN maps: more peaks than strict maxima allow
+        return find_peaks(m, cnt.value, stream)
     k = min(cnt.value, cap)
     return xs[:k], ys[:k], hs[:k]
 

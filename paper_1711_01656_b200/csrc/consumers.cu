@@ -186,7 +186,7 @@ __device__ __forceinline__ uint64_t desc_key(double h) {
 __global__ void __launch_bounds__(256) peak_compact_kernel(const double* __restrict__ s, int w, int h,
                                                            const uint32_t* __restrict__ boff,
                                                            uint64_t* __restrict__ keys, uint32_t* __restrict__ idx,
-                                                           unsigned long long* __restrict__ kminmax) {
+                                                           unsigned long long* __restrict__ kminmax, int64_t cap) {
     __shared__ uint32_t wsum[8];
     const int64_t n = static_cast<int64_t>(w) * h;
     const int64_t base = static_cast<int64_t>(blockIdx.x) * kPeakTile + 4 * threadIdx.x;
@@ -207,8 +207,10 @@ __global__ void __launch_bounds__(256) peak_compact_kernel(const double* __restr
     for (int j = 0; j < 4; ++j)
         if (f[j]) {
             const unsigned long long k = desc_key(s[base + j]);
-            keys[pos] = k;
-            idx[pos] = static_cast<uint32_t>(base + j);
+            if (pos < cap) {  // NaN maps can hold more peaks than the n / 4 + 2 of strict maxima
+                keys[pos] = k;
+                idx[pos] = static_cast<uint32_t>(base + j);
+            }
             ++pos;
             kmin = k < kmin ? k : kmin;
             kmax = k > kmax ? k : kmax;
@@ -422,6 +424,7 @@ struct PeakWs {
     uint32_t* v[2];
     uint32_t* counts;
     uint32_t* scalars;  // [0] total peaks, [1] score best
+    void* extra;        // stream-ordered overflow buffers (freed by the caller after use), or null
 };
 
 size_t peak_ws_bytes(int w, int h, int64_t* nblk_peak, int64_t* nblk_sort) {
@@ -453,6 +456,7 @@ PeakWs carve(void* ws, int w, int h) {
     s.counts = reinterpret_cast<uint32_t*>(take(256 * nbs * 4));
     // [0]: peak count, [4 .. 259]: digit starts, [260 .. 263]: key min / max (u64)
     s.scalars = reinterpret_cast<uint32_t*>(take(16 + 1024 + 16));
+    s.extra = nullptr;
     return s;
 }
 
@@ -469,13 +473,34 @@ spct_status sorted_peaks(const double* map, int w, int h, void* ws, size_t ws_by
     unsigned long long* kminmax = reinterpret_cast<unsigned long long*>(P.scalars + 260);
     const unsigned long long init[2] = {~0ull, 0ull};
     cudaMemcpyAsync(kminmax, init, 16, cudaMemcpyHostToDevice, st);
-    peak_compact_kernel<<<static_cast<unsigned>(nbp), 256, 0, st>>>(P.s, w, h, P.bcount, P.k[0], P.v[0], kminmax);
+    const int64_t cap = n / 4 + 2;
+    peak_compact_kernel<<<static_cast<unsigned>(nbp), 256, 0, st>>>(P.s, w, h, P.bcount, P.k[0], P.v[0], kminmax, cap);
     if (auto e = launch_status("find_peaks compaction")) return e;
     uint32_t hdr[264];
     if (auto e = cuda_status(cudaMemcpyAsync(hdr, P.scalars, sizeof(hdr), cudaMemcpyDeviceToHost, st), "find_peaks count"))
         return e;
     if (auto e = cuda_status(cudaStreamSynchronize(st), "find_peaks")) return e;
     const int64_t m = hdr[0];
+    if (m > cap) {
+        // more peaks than strict maxima allow (NaN cells pass the reference's test,
+        // likelihood.cpp:316): compact again into buffers sized for the real count
+        const int64_t nbm = ceil_div(m, kSortTile);
+        const size_t kb = round_up(m * 8, 256), vb = round_up(m * 4, 256);
+        char* x = nullptr;
+        if (auto e = cuda_status(malloc_async(&x, 2 * kb + 2 * vb + 256 * nbm * 4, st), "find_peaks alloc")) return e;
+        P.k[0] = reinterpret_cast<uint64_t*>(x);
+        P.k[1] = reinterpret_cast<uint64_t*>(x + kb);
+        P.v[0] = reinterpret_cast<uint32_t*>(x + 2 * kb);
+        P.v[1] = reinterpret_cast<uint32_t*>(x + 2 * kb + vb);
+        P.counts = reinterpret_cast<uint32_t*>(x + 2 * kb + 2 * vb);
+        P.extra = x;
+        cudaMemcpyAsync(kminmax, init, 16, cudaMemcpyHostToDevice, st);
+        peak_compact_kernel<<<static_cast<unsigned>(nbp), 256, 0, st>>>(P.s, w, h, P.bcount, P.k[0], P.v[0], kminmax, m);
+        if (auto e = launch_status("find_peaks compaction")) return e;
+        if (auto e = cuda_status(cudaMemcpyAsync(hdr, P.scalars, sizeof(hdr), cudaMemcpyDeviceToHost, st), "find_peaks"))
+            return e;
+        if (auto e = cuda_status(cudaStreamSynchronize(st), "find_peaks")) return e;
+    }
     int cur = 0;
     if (m > 1) {
         const int nb = static_cast<int>(ceil_div(m, kSortTile));
@@ -562,11 +587,13 @@ extern "C" spct_status spct_cu_find_peaks(const double* map, int w, int h, int32
     if (auto st = sorted_peaks(map, w, h, workspace, workspace_bytes, s, &P, &m)) return st;
     *count = m;
     const int64_t k = std::min(m, max_out);
+    spct_status st = SPCT_OK;
     if (k > 0) {
         peak_gather_kernel<<<grid1(k), 256, 0, s>>>(P.v[0], P.s, w, k, xs, ys, heights);
-        return launch_status("peak_gather_kernel");
+        st = launch_status("peak_gather_kernel");
     }
-    return SPCT_OK;
+    if (P.extra) cudaFreeAsync(P.extra, s);
+    return st;
 }
 
 extern "C" spct_status spct_cu_score_map(const double* map, int w, int h, int gx, int gy, int gw, int gh, int64_t* rank,

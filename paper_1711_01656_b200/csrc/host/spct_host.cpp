@@ -99,9 +99,12 @@ public:
         static CopyPool* p = new CopyPool();  // never destroyed: workers outlive static teardown
         return *p;
     }
+    // Fault in the pages of fresh (untouched) memory on every worker: the kernel's
+    // first-touch cost (~1.4 us per 4 KiB page) dominates a large new result vector.
+    void touch_par(void* dst, std::size_t n) { memcpy_par(dst, nullptr, n); }
     void memcpy_par(void* dst, const void* src, std::size_t n) {
         if (n < (std::size_t(1) << 20) || workers_.empty()) {
-            std::memcpy(dst, src, n);
+            copy_or_touch(dst, src, n);
             return;
         }
         const std::size_t parts = workers_.size() + 1, step = (n / parts + 63) / 64 * 64;
@@ -114,7 +117,7 @@ public:
             pending_ += parts - 1;
         }
         cv_.notify_all();
-        std::memcpy(dst, src, std::min(n, step));
+        copy_or_touch(dst, src, std::min(n, step));
         std::unique_lock<std::mutex> lock(mu_);
         done_cv_.wait(lock, [&] { return pending_ == 0; });
     }
@@ -125,9 +128,17 @@ private:
         const char* src;
         std::size_t len;
     };
+    static void copy_or_touch(void* dst, const void* src, std::size_t n) {
+        if (src) {
+            std::memcpy(dst, src, n);
+            return;
+        }
+        volatile char* d = static_cast<volatile char*>(dst);
+        for (std::size_t o = 0; o < n; o += 4096) d[o] = 0;
+    }
     CopyPool() {
         const unsigned hw = std::thread::hardware_concurrency();
-        const unsigned n = hw >= 8 ? 3 : (hw >= 4 ? 1 : 0);
+        const unsigned n = hw >= 16 ? 7 : (hw >= 8 ? 3 : (hw >= 4 ? 1 : 0));
         for (unsigned i = 0; i < n; ++i) workers_.emplace_back([this] { run(); }).detach();
     }
     void run() {
@@ -139,7 +150,7 @@ private:
                 j = jobs_.back();
                 jobs_.pop_back();
             }
-            std::memcpy(j.dst, j.src, j.len);
+            copy_or_touch(j.dst, j.src, j.len);
             std::lock_guard<std::mutex> lock(mu_);
             if (--pending_ == 0) done_cv_.notify_all();
         }
@@ -178,6 +189,22 @@ void copy_d2h(void* dst, const void* src, std::size_t bytes) {
             CopyPool::get().memcpy_par(static_cast<char*>(dst) + off, st.buf[(i - 1) & 1], len);
         }
     }
+}
+
+// Size a result vector of the reference API (LikelihoodMap::values) to n doubles.  A new
+// large vector's pages are faulted in on the copy pool's threads before std::vector
+// zero-fills them, instead of one page fault at a time inside that fill.
+void resize_prefaulted(std::vector<double>& v, std::size_t n) {
+    if (v.size() == n) return;
+    if (v.capacity() < n && n * sizeof(double) >= (std::size_t(16) << 20)) {
+        std::vector<double> fresh;
+        fresh.reserve(n);
+        CopyPool::get().touch_par(fresh.data(), n * sizeof(double));
+        fresh.resize(n);
+        v.swap(fresh);
+        return;
+    }
+    v.resize(n);
 }
 
 void copy_h2d(void* dst, const void* src, std::size_t bytes) {
@@ -609,7 +636,7 @@ void hist_match_map_into(const IntegralHistogramTensor& t, const std::vector<dou
     out.width = t.width;
     out.height = t.height;
     out.tag = metric == HistMetric::Minkowski ? "hist-distance" : "hist-match";
-    out.values.resize(std::size_t(t.width) * t.height);  // no-op when the caller's map is already this size
+    resize_prefaulted(out.values, std::size_t(t.width) * t.height);  // no-op when the caller's map is this size
     copy_d2h(out.values.data(), map.p, out.values.size() * 8);
 }
 
@@ -652,7 +679,7 @@ LikelihoodMap fuse_maps(const std::vector<LikelihoodMap>& maps, std::vector<doub
     f.width = w;
     f.height = h;
     f.tag = "fused";
-    f.values.resize(n);
+    resize_prefaulted(f.values, n);
     copy_d2h(f.values.data(), out.p, n * 8);
     return f;
 }
@@ -663,17 +690,24 @@ std::vector<Peak> find_peaks(const LikelihoodMap& map) {
     std::size_t ws = 0;
     check(spct_cu_find_peaks_workspace(map.width, map.height, &ws));
     DevBuf work(ws);
-    const std::int64_t cap = std::int64_t(map.width) * map.height / 4 + 2;
-    DevBuf xs(cap * 4), ys(cap * 4), hs(cap * 8);
+    std::int64_t cap = std::int64_t(map.width) * map.height / 4 + 2;  // strict maxima
     std::int64_t count = 0;
-    check(spct_cu_find_peaks(d->as<double>(), map.width, map.height, xs.as<std::int32_t>(), ys.as<std::int32_t>(),
-                             hs.as<double>(), cap, &count, work.p, ws, nullptr));
+    std::unique_ptr<DevBuf> xs, ys, hs;
+    for (;;) {  // NaN cells are peaks too (likelihood.cpp:316): then size for the real count
+        xs = std::make_unique<DevBuf>(cap * 4);
+        ys = std::make_unique<DevBuf>(cap * 4);
+        hs = std::make_unique<DevBuf>(cap * 8);
+        check(spct_cu_find_peaks(d->as<double>(), map.width, map.height, xs->as<std::int32_t>(),
+                                 ys->as<std::int32_t>(), hs->as<double>(), cap, &count, work.p, ws, nullptr));
+        if (count <= cap) break;
+        cap = count;
+    }
     std::vector<std::int32_t> hx(count), hy(count);
     std::vector<double> hh(count);
     if (count) {
-        cuda(cudaMemcpy(hx.data(), xs.p, count * 4, cudaMemcpyDeviceToHost), "D2H");
-        cuda(cudaMemcpy(hy.data(), ys.p, count * 4, cudaMemcpyDeviceToHost), "D2H");
-        cuda(cudaMemcpy(hh.data(), hs.p, count * 8, cudaMemcpyDeviceToHost), "D2H");
+        cuda(cudaMemcpy(hx.data(), xs->p, count * 4, cudaMemcpyDeviceToHost), "D2H");
+        cuda(cudaMemcpy(hy.data(), ys->p, count * 4, cudaMemcpyDeviceToHost), "D2H");
+        cuda(cudaMemcpy(hh.data(), hs->p, count * 8, cudaMemcpyDeviceToHost), "D2H");
     }
     std::vector<Peak> peaks(count);
     for (std::int64_t i = 0; i < count; ++i) peaks[i] = Peak{hx[i], hy[i], hh[i], int(i) + 1};
@@ -746,7 +780,7 @@ LikelihoodMap likelihood_from_frame(const GrayImage& img, int bins, const std::v
     out.width = img.width;
     out.height = img.height;
     out.tag = "hist-distance";
-    out.values.resize(std::size_t(img.width) * img.height);
+    resize_prefaulted(out.values, std::size_t(img.width) * img.height);
     copy_d2h(out.values.data(), map.p, out.values.size() * 8);
     if (tensor_out) {
         tensor_out->bins = bins;

@@ -15,6 +15,8 @@ over bins (likelihood.cpp:215-219).
 """
 from __future__ import annotations
 
+import numpy as np
+
 
 def slab_bounds(nbins: int, world: int, rank: int) -> tuple[int, int]:
     """Contiguous, near-equal bin slab of `rank` (the first nbins % world ranks get one more)."""
@@ -373,3 +375,106 @@ class PeerBandReduce:
         for p in self._own:
             lib.spct_cu_peer_free(p)
         self._own = []
+
+
+class ShardedMapStep:
+    """One frame of the bin-sharded likelihood-map path on this rank.
+
+    ``bins_per_rank=None`` shards a fixed histogram of ``nbins`` bins over the ranks
+    (strong scaling: rank r owns ``slab_bounds(nbins, world, r)``); an integer gives every
+    rank that many bins of a ``bins_per_rank * world`` histogram (weak scaling).  With one
+    rank the fused sweep writes the finished map itself; with several, each rank's sweep
+    writes its slab of the tensor and its partial window sums, and ``reduce`` sums them:
+    "band" (every rank pulls and finalises a band of rows over peer memory, default),
+    "root" (partials written into the root's slots by the sweep) or "nccl" (one
+    ``dist.reduce`` + ``hist_finalize`` on the root).  Peer setup that fails (no IPC / P2P
+    between the devices) falls back to "nccl" on every rank.
+
+        s = ShardedMapStep(W, H, nbins, tmpl, kw, kh, device=dev)
+        s.step(frame)            # device frame (uint8), stream-ordered
+        s.map                    # root: the (H, W) float64 likelihood map
+    """
+
+    def __init__(self, width: int, height: int, nbins: int, tmpl, kw: int, kh: int, p: float = 1.0, *,
+                 bins_per_rank: int | None = None, reduce: str = "band", root: int = 0, device=None,
+                 store_tensor: bool = True):
+        import torch
+        import torch.distributed as dist
+
+        from . import api
+
+        self._api, self._torch = api, torch
+        init = dist.is_available() and dist.is_initialized()
+        self.world = dist.get_world_size() if init else 1
+        self.rank = dist.get_rank() if init else 0
+        self.root = root
+        self.W, self.H, self.kw, self.kh, self.p = width, height, kw, kh, p
+        self.nbins = nbins if bins_per_rank is None else bins_per_rank * self.world
+        if self.world == 1:
+            self.bin0, self.bin1 = 0, self.nbins
+        elif bins_per_rank is None:
+            self.bin0, self.bin1 = slab_bounds(self.nbins, self.world, self.rank)
+        else:
+            self.bin0, self.bin1 = self.rank * bins_per_rank, (self.rank + 1) * bins_per_rank
+        self.device = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+        self.tmpl_dev = torch.as_tensor(np.asarray(tmpl, dtype=np.float64)).to(self.device) \
+            if not isinstance(tmpl, torch.Tensor) else tmpl.to(self.device, torch.float64)
+        self.tensor = api.IntegralHistogramTensor(width, height, self.nbins, self.bin0, self.bin1 - self.bin0,
+                                                  device=self.device)
+        if not store_tensor:
+            self.tensor.desc.data = None
+        self.nu, self.nv = width - kw + 1, height - kh + 1
+        self.reduce, self.note = reduce, reduce
+        self.peer = None
+        self._map = None
+        self.partial = None
+        if self.world > 1 and reduce in ("band", "root"):
+            try:  # fails on every rank or on none (the reducers agree on the outcome)
+                self.peer = PeerBandReduce(width, height, kw, kh, root=root, device=self.device) \
+                    if reduce == "band" else PeerSlabReduce(self.nu, self.nv, root=root, device=self.device)
+            except RuntimeError as e:
+                self.reduce, self.note = "nccl", "nccl (peer setup failed: %s)" % str(e)[:120]
+        if self.world == 1 or self.peer is None or reduce == "root":
+            if self.world == 1 or self.rank == root:
+                self._map = torch.empty((height, width), dtype=torch.float64, device=self.device)
+        elif self.rank == root:
+            self._map = self.peer.map  # the band owners write the root's shared buffer
+        if self.world > 1 and self.peer is None:
+            self.partial = torch.empty((self.nv, self.nu), dtype=torch.float64, device=self.device)
+
+    @property
+    def map(self):
+        if self.rank != self.root and self.world > 1:
+            raise RuntimeError("ShardedMapStep.map lives on the root")
+        return self._map
+
+    def step(self, frame, stream=None) -> None:
+        api, kw, kh, p = self._api, self.kw, self.kh, self.p
+        if self.world == 1:
+            api.build_and_match_map(frame, self.nbins, None, kw, kh, p, out=self.tensor, lmap=self._map,
+                                    tmpl_dev=self.tmpl_dev, stream=stream)
+            return
+        b0, nb = self.bin0, self.bin1 - self.bin0
+        if self.peer is not None:
+            self.peer.begin(stream)
+            api.build_and_match(frame, self.nbins, None, kw, kh, p, bin0=b0, bins=nb, out=self.tensor,
+                                partial=self.peer.slot(), tmpl_dev=self.tmpl_dev, stream=stream)
+            self.peer.publish(stream)
+            if self.reduce == "band":
+                self.peer.finalize(p, stream=stream)
+            elif self.rank == self.root:
+                self.peer.finalize(self._map, self.W, self.H, kw, kh, p, stream=stream)
+            return
+        api.build_and_match(frame, self.nbins, None, kw, kh, p, bin0=b0, bins=nb, out=self.tensor,
+                            partial=self.partial, tmpl_dev=self.tmpl_dev, stream=stream)
+        reduce_partials(self.partial, dst=self.root)
+        if self.rank == self.root:
+            api.hist_finalize(self.partial, self.W, self.H, kw, kh, p, out=self._map, stream=stream)
+
+    def error(self) -> bool:
+        return self.peer.error() if self.peer is not None else False
+
+    def close(self) -> None:
+        if self.peer is not None:
+            self.peer.close()
+            self.peer = None
