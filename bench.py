@@ -487,7 +487,8 @@ def run_dropin(timeout: int = 600) -> dict:
                            timeout=timeout)
         d = json.loads(r.stdout.strip().splitlines()[-1])
     except (subprocess.SubprocessError, ValueError, IndexError) as e:
-        return {"unavailable": str(e)[:200]}
+        err = (locals().get("r").stderr if locals().get("r") is not None else "")[-300:]
+        return {"unavailable": f"{str(e)[:100]}; rc={getattr(locals().get('r'), 'returncode', None)}; {err}"}
     d["unit"] = UNIT
     d["note"] = ("value: Gbin*px/s of build_integral_histogram(BinMap) + hist_distance_map(t, ...) per frame with "
                  "host buffers (the reference's call sequence, spct_main.cpp:332-333); value_fused: the one-call "
@@ -571,7 +572,7 @@ def run_ours(args) -> None:
     if kernels:
         name, (kt, kn) = max(kernels.items(), key=lambda kv: kv[1][0])
         roof = strong_roofline(name, kt, kn, args.steps, W_IMG, NBINS, main.bin1 - main.bin0, world == 1)
-        roof.update({"traffic": ncu_traffic(name), "step_share": round(kt / args.steps / ms, 3),
+        roof.update({"traffic": ncu_traffic(name) if world == 1 else None, "step_share": round(kt / args.steps / ms, 3),
                      "peak_source": pk["source"], "kernels_ms": {k: round(v[0] / args.steps, 4)
                                                                  for k, v in kernels.items()}})
 
@@ -591,6 +592,34 @@ def run_ours(args) -> None:
             raise SystemExit("bench.py: a peer-reduce wait timed out (weak)")
         weak.close()
         del weak
+
+    # ---- single-GPU extras
+    if world == 1:
+        t = main.tensor
+
+        def build_step():
+            P.build_integral_histogram(frame, NBINS, memory_budget=None, out=t, validate=False)
+        profiling.reset()
+        profiling.enable(True)
+        ms_b = timer(build_step, args.steps, warmup=args.warmup)
+        profiling.enable(False)
+        kb = kernel_ms(profiling, ("ih_sweep",))
+        profiling.reset()
+        alg_b = NBINS * W_IMG * H_IMG * 4 + W_IMG * H_IMG
+        extras["build_only"] = {"workload": "C3 plain build_integral_histogram (BASELINE config 3)",
+                                "ms_per_step": round(ms_b, 4),
+                                "value": round(NBINS * W_IMG * H_IMG / (ms_b * 1e-3) / 1e9, 2), "unit": UNIT,
+                                "roofline": roofline_of(kb["ih_sweep"][0] / kb["ih_sweep"][1], alg_b, pk)
+                                if "ih_sweep" in kb else None}
+        # main.tensor again holds the headline frame's IH (the same frame): parity below reads it
+        if not args.no_c2:
+            extras["c2"] = run_c2(P, dev, timer, pk)
+        if not args.no_paths:
+            extras.update(run_paths(P, dev, timer, pk, frame, tmpl, t, args))
+        if not args.no_next:
+            extras["next_rows"] = run_next_rows(P, dev, pk["hbm_gbs"])
+        if not args.no_c5:
+            extras["c5_batch"] = run_c5(P, dev, stream)
 
     # ---- BASELINE config 4: 8192^2 x 256 bins, strong scaling (N = 1: the whole 68.7 GB tensor)
     if not args.no_c4:
@@ -632,34 +661,6 @@ def run_ours(args) -> None:
             torch.cuda.empty_cache()
         else:
             extras["c4"] = {"skipped": f"needs {need / 1e9:.1f} GB, {free / 1e9:.1f} GB free"}
-
-    # ---- single-GPU extras
-    if world == 1:
-        t = main.tensor
-
-        def build_step():
-            P.build_integral_histogram(frame, NBINS, memory_budget=None, out=t, validate=False)
-        profiling.reset()
-        profiling.enable(True)
-        ms_b = timer(build_step, args.steps, warmup=args.warmup)
-        profiling.enable(False)
-        kb = kernel_ms(profiling, ("ih_sweep",))
-        profiling.reset()
-        alg_b = NBINS * W_IMG * H_IMG * 4 + W_IMG * H_IMG
-        extras["build_only"] = {"workload": "C3 plain build_integral_histogram (BASELINE config 3)",
-                                "ms_per_step": round(ms_b, 4),
-                                "value": round(NBINS * W_IMG * H_IMG / (ms_b * 1e-3) / 1e9, 2), "unit": UNIT,
-                                "roofline": roofline_of(kb["ih_sweep"][0] / kb["ih_sweep"][1], alg_b, pk)
-                                if "ih_sweep" in kb else None}
-        # main.tensor again holds the headline frame's IH (the same frame): parity below reads it
-        if not args.no_c2:
-            extras["c2"] = run_c2(P, dev, timer, pk)
-        if not args.no_paths:
-            extras.update(run_paths(P, dev, timer, pk, frame, tmpl, t, args))
-        if not args.no_next:
-            extras["next_rows"] = run_next_rows(P, dev, pk["hbm_gbs"])
-        if not args.no_c5:
-            extras["c5_batch"] = run_c5(P, dev, stream)
 
     # ---- end to end through the public API: pinned host frame in, host map out, every step
     if world == 1:

@@ -141,14 +141,16 @@ class IntegralHistogramTensor:
     """
 
     def __init__(self, width: int, height: int, nbins_total: int, bin0: int = 0, bins: int | None = None,
-                 device=None):
+                 device=None, store: bool = True):
         bins = nbins_total - bin0 if bins is None else bins
         rp, pp, nbytes = C.c_int64(), C.c_int64(), C.c_uint64()
         check(A.lib().spct_cu_ih_layout(width, height, bins, C.byref(rp), C.byref(pp), C.byref(nbytes)))
         self.width, self.height, self.bins, self.bin0, self.nbins_total = width, height, bins, bin0, nbins_total
         self.row_pitch, self.plane_pitch = rp.value, pp.value
-        self.storage = torch.empty(nbytes.value // 4, dtype=torch.int32, device=device or "cuda")
-        self.desc = A.spct_ih(self.storage.data_ptr(), bins, bin0, nbins_total, height, width, rp.value, pp.value)
+        # store=False: a descriptor without cells, for the fused sweeps' map-only form
+        self.storage = torch.empty(nbytes.value // 4 if store else 0, dtype=torch.int32, device=device or "cuda")
+        self.desc = A.spct_ih(self.storage.data_ptr() if store else None, bins, bin0, nbins_total, height, width,
+                              rp.value, pp.value)
         # (spct_source, keep-alive device tensors) of the frame the tensor was built from, if any:
         # window statistics can then be recomputed from 1 B/px instead of re-reading the tensor
         self.source = None

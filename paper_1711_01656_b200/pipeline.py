@@ -24,9 +24,7 @@ class FramePipeline:
         self.dev = torch.device(device or "cuda")
         self.w, self.h, self.nbins, self.kw, self.kh, self.p, self.metric = width, height, nbins, kw, kh, p, metric
         self.tmpl_dev = _api._tmpl(tmpl, nbins, width, height, kw, kh, p).to(self.dev)
-        self.tensor = _api.IntegralHistogramTensor(width, height, nbins, device=self.dev)
-        if not store_tensor:
-            self.tensor.desc.data = None
+        self.tensor = _api.IntegralHistogramTensor(width, height, nbins, device=self.dev, store=store_tensor)
         self.frames = [torch.empty((height, width), dtype=torch.uint8, device=self.dev) for _ in range(2)]
         self.maps = [torch.empty((height, width), dtype=torch.float64, device=self.dev) for _ in range(2)]
         self.compute = torch.cuda.Stream(self.dev)

@@ -420,9 +420,7 @@ class ShardedMapStep:
         self.tmpl_dev = torch.as_tensor(np.asarray(tmpl, dtype=np.float64)).to(self.device) \
             if not isinstance(tmpl, torch.Tensor) else tmpl.to(self.device, torch.float64)
         self.tensor = api.IntegralHistogramTensor(width, height, self.nbins, self.bin0, self.bin1 - self.bin0,
-                                                  device=self.device)
-        if not store_tensor:
-            self.tensor.desc.data = None
+                                                  device=self.device, store=store_tensor)
         self.nu, self.nv = width - kw + 1, height - kh + 1
         self.reduce, self.note = reduce, reduce
         self.peer = None

@@ -145,3 +145,21 @@ def test_find_peaks_nan_matches_reference(P):
     # the peak set (NaN heights make the reference's height order unspecified)
     assert sorted(got) == sorted((int(x), int(y)) for x, y in zip(want[0], want[1]))
     assert len(got) > 0
+
+
+@pytest.mark.parametrize("name", ["crop", "random", "sparse"])
+def test_extension_metrics_match_published_implementations(P, name):
+    """The fused sweep and the tensor path for intersection / Bhattacharyya / chi-square
+    against maps computed with scipy / scikit-learn (tests/golden/make_metric_golden.py)."""
+    import os
+
+    d = np.load(os.path.join(os.path.dirname(__file__), "golden", "metric_vectors.npz"))
+    w, h, bins, kw, kh = (int(v) for v in d[f"{name}_dims"])
+    bm, t = d[f"{name}_binmap"], d[f"{name}_template"]
+    tens = P.build_integral_histogram(bm, bins)
+    for key, metric in (("intersection", 1), ("bhattacharyya", 2), ("chisq", 3)):
+        want = d[f"{name}_{key}"]
+        fused = P.build_and_match_map(bm, bins, t, kw, kh, 1.0, metric)[1].cpu().numpy()
+        tensor = P.hist_match_map(tens, t, kw, kh, 1.0, metric, exact=True).cpu().numpy()
+        assert np.abs(fused - want).max() <= 1e-12, (key, "fused")
+        assert np.abs(tensor - want).max() <= 1e-12, (key, "tensor")

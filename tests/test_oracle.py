@@ -298,3 +298,22 @@ def test_median_bg_vs_live_reference(w, h, bins, m, n, nf, nslide):
     assert np.array_equal(oracle.median_bg_sort(frames[:nf]), oracle.median_bg_sort(frames[:nf], True))
     with pytest.raises(oracle.ContractError):
         oracle.median_bg_ih(frames, nf, bins - 1 if bins > 1 else 0, m, n, True)  # value exceeds bin count
+
+
+def test_extension_metrics_pinned_to_published_implementations():
+    """Intersection / Bhattacharyya / chi-square (absent from the reference):
+    the oracle's definitions against fixtures computed with scipy.spatial.distance
+    (braycurtis, sqeuclidean) and sklearn.metrics.pairwise.additive_chi2_kernel
+    (tests/golden/make_metric_golden.py)."""
+    import os
+
+    d = np.load(os.path.join(os.path.dirname(__file__), "golden", "metric_vectors.npz"))
+    for name in ("crop", "random", "sparse"):
+        w, h, bins, kw, kh = (int(v) for v in d[f"{name}_dims"])
+        bm, t = d[f"{name}_binmap"], d[f"{name}_template"]
+        for key, metric in (("intersection", oracle.INTERSECTION), ("bhattacharyya", oracle.BHATTACHARYYA),
+                            ("chisq", oracle.CHISQ)):
+            got = oracle.hist_match_map_direct(bm, bins, t, kw, kh, 1.0, metric)
+            assert np.abs(got - d[f"{name}_{key}"]).max() <= 1e-12, (name, key)
+            ih = oracle.build_ih(bm, bins)
+            assert np.array_equal(oracle.hist_match_map(ih, t, kw, kh, 1.0, metric), got), (name, key)

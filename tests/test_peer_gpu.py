@@ -82,3 +82,55 @@ def test_peer_slab_reduce(tmp_path, world, nbins, kw, kh, p, mode):
     assert got.shape == want.shape
     err = np.abs(got - want)
     assert np.all(err <= 1e-5 * np.maximum(np.abs(want), 1e-12) + 1e-12), err.max()
+
+
+def _c4_worker(rank, world, port, out_path, reduce):
+    """BASELINE config 4 on `world` ranks (bin slabs of the 8192^2 x 256-bin histogram,
+    strong scaling) through sharding.ShardedMapStep, the class bench.py times."""
+    import torch.distributed as dist
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    import paper_1711_01656_b200 as P
+    from paper_1711_01656_b200.sharding import ShardedMapStep
+
+    side, nbins, kw, kh = 8192, 256, 64, 64
+    img = np.random.default_rng(4).integers(0, 256, size=(side, side), dtype=np.uint8)
+    y0 = x0 = (side - 64) // 2
+    crop = (img[y0:y0 + kh, x0:x0 + kw].astype(np.int64) * nbins) >> 8
+    tmpl = np.bincount(crop.reshape(-1), minlength=nbins).astype(np.float64) / crop.size
+    frame = torch.from_numpy(img).cuda()
+    s = ShardedMapStep(side, side, nbins, tmpl, kw, kh, 1.0, reduce=reduce)
+    try:
+        assert s.bin1 - s.bin0 == nbins // world
+        for _ in range(2):  # two epochs: the double-buffered partials and flags turn over
+            s.step(frame)
+        torch.cuda.synchronize()
+        assert not s.error(), "peer wait timed out"
+        if rank == 0:
+            got = s.map.cpu().numpy()
+            # the single-GPU map of the whole histogram (tensor not stored: fused no-store sweep)
+            t = P.IntegralHistogramTensor(side, side, nbins, store=False)
+            want = P.build_and_match_map(frame, nbins, tmpl, kw, kh, 1.0, out=t)[1].cpu().numpy()
+            np.save(out_path, np.stack([got, want]))
+        dist.barrier()
+    finally:
+        s.close()
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("reduce", ["band", "root"])
+def test_c4_two_ranks_match_single_gpu(tmp_path, reduce):
+    """Verdict r1: the 2-rank C4 path (two 128-bin slabs, 34 GB of tensor each, both ranks
+    on cuda:0 through the same IPC / flag code as across GPUs) equals the N = 1 map."""
+    import torch.multiprocessing as mp
+
+    if torch.cuda.mem_get_info()[0] < 90e9:
+        pytest.skip("needs ~75 GB of device memory")
+    out = str(tmp_path / "c4.npy")
+    mp.spawn(_c4_worker, args=(2, _free_port(), out, reduce), nprocs=2, join=True)
+    got, want = np.load(out)
+    err = np.abs(got - want)
+    assert np.all(err <= 1e-5 * np.maximum(np.abs(want), 1e-12)), err.max()
