@@ -254,6 +254,16 @@ spct_status spct_cu_hist_check(int nbins, int width, int height, const double* t
  * tensors give the reference's map. */
 spct_status spct_cu_hist_match(const spct_ih* t, const double* tmpl, int kw, int kh, double p,
                                int metric, double* map, void* stream);
+/* The same map computed the reference's way from the tensor: one thread per window, the
+ * b planes visited in order k = 0..b-1 with the reference's divide and pow (bit-identical
+ * to likelihood.cpp:211-221 for p = 1; 4 b scattered reads per window).  spct_cu_hist_match
+ * instead reads the tensor once (tensor_match.cu: per-pixel bins recovered and checked,
+ * then the fused sweep; bit-identical for p = 1 with an integral template and a
+ * power-of-two kw*kh, within 1e-5 otherwise) and falls back to this arithmetic for tensors
+ * that are not the integral histogram of a bin map.  SPCT_EXACT_MAPS=1 makes
+ * spct_cu_hist_match take this path too. */
+spct_status spct_cu_hist_match_exact(const spct_ih* t, const double* tmpl, int kw, int kh, double p,
+                                     int metric, double* map, void* stream);
 
 /* Bin-slab partial of the window statistic over the valid grid (nv x nu, nu = width-kw+1,
  * nv = height-kh+1): partial[v*nu+u] (+)= sum_{k in slab} term_k.  With accumulate = 0

@@ -71,6 +71,7 @@ SIGNATURES = {
     "spct_cu_region_counts": (_i, [_ih_p, _vp, _i, _vp, _vp]),
     "spct_cu_hist_check": (_i, [_i, _i, _i, C.POINTER(_d), _i, _i, _i, _d]),
     "spct_cu_hist_match": (_i, [_ih_p, _vp, _i, _i, _d, _i, _vp, _vp]),
+    "spct_cu_hist_match_exact": (_i, [_ih_p, _vp, _i, _i, _d, _i, _vp, _vp]),
     "spct_cu_hist_partial": (_i, [_ih_p, _vp, _i, _i, _d, _i, _vp, _i, _vp]),
     "spct_cu_hist_finalize": (_i, [_vp, _i, _i, _i, _i, _d, _i, _vp, _vp]),
     "spct_cu_fused_window_ok": (_i, [_i, _i]),

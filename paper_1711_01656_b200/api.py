@@ -363,9 +363,13 @@ def hist_match_map(t: IntegralHistogramTensor, tmpl, kw: int, kh: int, p: float 
     """likelihood.cpp:193-225 (metric MINKOWSKI) -> (height, width) float64 device map.
 
     A tensor built by this library remembers its source frame, and the map is then
-    recomputed by the fused sweep from 1 B/px (no tensor re-read; within the 1e-5 map
-    tolerance).  ``exact=True`` (or a tensor without a source) reads the tensor with
-    the reference's operation order instead: bit-identical to the reference for p = 1."""
+    recomputed by the fused sweep from 1 B/px (no tensor re-read).  A tensor without a
+    source (e.g. loaded from an IHT1 file) is read once: the device recovers and checks
+    every pixel's bin, then runs the same sweep (tensor_match.cu); a tensor that is not the
+    integral histogram of a bin map gets the reference's arithmetic with actual window
+    totals.  Both are bit-identical to the reference for p = 1 with an integral template and
+    a power-of-two kw*kh, within the 1e-5 map tolerance otherwise.  ``exact=True`` reads
+    the tensor with the reference's operation order (bit-identical for p = 1)."""
     dt = _tmpl(tmpl, t.bins, t.width, t.height, kw, kh, p)
     out = torch.empty((t.height, t.width), dtype=torch.float64, device=dt.device)
     if (not exact and t.source is not None and t.bin0 == 0 and t.bins == t.nbins_total
@@ -378,7 +382,8 @@ def hist_match_map(t: IntegralHistogramTensor, tmpl, kw: int, kh: int, p: float 
         check(A.lib().spct_cu_ih_build_match_map(C.byref(src), C.byref(nodata), _ptr(dt), kw, kh, p, metric,
                                                  _ptr(out), _ptr(wbuf), wbuf.numel(), _stream(stream)))
         return out
-    check(A.lib().spct_cu_hist_match(C.byref(t.desc), _ptr(dt), kw, kh, p, metric, _ptr(out), _stream(stream)))
+    fn = A.lib().spct_cu_hist_match_exact if exact else A.lib().spct_cu_hist_match
+    check(fn(C.byref(t.desc), _ptr(dt), kw, kh, p, metric, _ptr(out), _stream(stream)))
     return out
 
 

@@ -97,8 +97,12 @@ __device__ __forceinline__ double window_count(const spct_ih& t, int k, int ya, 
 // total (the reference's `total`); the first pass assumes total == kw * kh (true for every
 // tensor built from a bin map) while summing the real total, and a window whose total
 // differs is recomputed; a massless window gets the sentinel -1 (finalised to 0).
+// `gate` (optional, device): run only if *gate != 0 (the tensor matcher found a tensor that
+// is not the integral histogram of a bin map, tensor_match.cu).
 __global__ void __launch_bounds__(256) match_partial_kernel(spct_ih t, const double* __restrict__ tmpl, MatchParams m,
-                                                            double* __restrict__ partial, int accumulate) {
+                                                            double* __restrict__ partial, int accumulate,
+                                                            const uint32_t* __restrict__ gate) {
+    if (gate && *gate == 0) return;
     const int64_t n = static_cast<int64_t>(m.nu) * m.nv;
     for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
          i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
@@ -134,7 +138,8 @@ __global__ void __launch_bounds__(256) match_partial_kernel(spct_ih t, const dou
 
 // spread_valid (likelihood.cpp:44-58) fused with the finalisation (:220-221).
 __global__ void finalize_kernel(const double* __restrict__ partial, int W, int H, MatchParams m, double dmax,
-                                double* __restrict__ map) {
+                                double* __restrict__ map, const uint32_t* __restrict__ gate) {
+    if (gate && *gate == 0) return;
     const int cx0 = (m.kw - 1) / 2, cy0 = (m.kh - 1) / 2;
     const int64_t n = static_cast<int64_t>(W) * H;
     for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
@@ -258,7 +263,7 @@ extern "C" spct_status spct_cu_region_counts(const spct_ih* t, const int32_t* re
 
 namespace {
 spct_status hist_partial_impl(const spct_ih* t, const double* tmpl, int kw, int kh, double p, int metric,
-                              double* partial, int accumulate, int norm, void* stream) {
+                              double* partial, int accumulate, int norm, void* stream, const uint32_t* gate = nullptr) {
     if (auto st = check_ih(t)) return st;
     MatchParams m;
     if (auto st = make_match(t->width, t->height, kw, kh, p, metric, &m)) return st;
@@ -266,7 +271,7 @@ spct_status hist_partial_impl(const spct_ih* t, const double* tmpl, int kw, int 
     if (!tmpl || !partial || !t->data) return contract("hist_partial: null pointer");
     const int64_t n = static_cast<int64_t>(m.nu) * m.nv;
     const int prof = prof_begin("match_partial", as_stream(stream));
-    match_partial_kernel<<<grid_for(n, 256), 256, 0, as_stream(stream)>>>(*t, tmpl, m, partial, accumulate);
+    match_partial_kernel<<<grid_for(n, 256), 256, 0, as_stream(stream)>>>(*t, tmpl, m, partial, accumulate, gate);
     prof_end(prof, as_stream(stream));
     return launch_status("match_partial_kernel");
 }
@@ -277,33 +282,87 @@ extern "C" spct_status spct_cu_hist_partial(const spct_ih* t, const double* tmpl
     return hist_partial_impl(t, tmpl, kw, kh, p, metric, partial, accumulate, 0, stream);
 }
 
-extern "C" spct_status spct_cu_hist_finalize(const double* partial, int width, int height, int kw, int kh, double p,
-                                             int metric, double* map, void* stream) {
+namespace {
+spct_status finalize_impl(const double* partial, int width, int height, int kw, int kh, double p, int metric,
+                          double* map, void* stream, const uint32_t* gate) {
     MatchParams m;
     if (!(width > 0 && height > 0)) return contract("hist_finalize: empty map");
     if (auto st = make_match(width, height, kw, kh, p, metric, &m)) return st;
     if (!partial || !map) return contract("hist_finalize: null pointer");
     const double dmax = std::pow(2.0, 1.0 / p);  // likelihood.cpp:208
     const int64_t n = static_cast<int64_t>(width) * height;
-    finalize_kernel<<<grid_for(n, 256), 256, 0, as_stream(stream)>>>(partial, width, height, m, dmax, map);
+    finalize_kernel<<<grid_for(n, 256), 256, 0, as_stream(stream)>>>(partial, width, height, m, dmax, map, gate);
     return launch_status("finalize_kernel");
 }
+}  // namespace
 
-extern "C" spct_status spct_cu_hist_match(const spct_ih* t, const double* tmpl, int kw, int kh, double p, int metric,
-                                          double* map, void* stream) {
+extern "C" spct_status spct_cu_hist_finalize(const double* partial, int width, int height, int kw, int kh, double p,
+                                             int metric, double* map, void* stream) {
+    return finalize_impl(partial, width, height, kw, kh, p, metric, map, stream, nullptr);
+}
+
+namespace {
+spct_status hist_match_impl(const spct_ih* t, const double* tmpl, int kw, int kh, double p, int metric, double* map,
+                            void* stream, bool exact) {
     if (auto st = check_ih(t)) return st;
     if (t->bin0 != 0 || t->bins != t->nbins_total)
         return contract("hist_match: the tensor must hold every bin (use hist_partial for slabs)");
     MatchParams m;
     if (auto st = make_match(t->width, t->height, kw, kh, p, metric, &m)) return st;
-    if (!map) return contract("hist_match: null map");
+    if (!map || !t->data) return contract("hist_match: null pointer");
     cudaStream_t s = as_stream(stream);
-    double* part = nullptr;
     const int64_t n = static_cast<int64_t>(m.nu) * m.nv;
+    double* part = nullptr;
     if (auto st = cuda_status(malloc_async(&part, n * sizeof(double), s), "hist_match alloc")) return st;
-    // the full histogram is here: normalise by each window's actual total like the reference
-    spct_status st = hist_partial_impl(t, tmpl, kw, kh, p, metric, part, 0, 1, stream);
-    if (st == SPCT_OK) st = spct_cu_hist_finalize(part, t->width, t->height, kw, kh, p, metric, map, stream);
+    spct_status st = SPCT_OK;
+    uint32_t* gate = nullptr;
+    void* scratch = nullptr;
+    if (!exact && spct_cu_fused_window_ok(kw, kh) && t->nbins_total <= 65536 &&
+        check_carry_dims(t->width, t->height) == SPCT_OK) {
+        // read the tensor once: recover the bin map (tensor_match.cu), then the fused
+        // no-store sweep; the exact kernels below run only if the tensor is not one-hot
+        const size_t nb = round_up(static_cast<int64_t>(t->width) * t->height * 2, 256);
+        const size_t gs = t->bins > 128 ? static_cast<size_t>(t->width) * t->height * 8 : 0;
+        size_t ws = 0;
+        spct_source src{};
+        src.kind = SPCT_SRC_BINS_U16;
+        src.pitch = t->width;
+        src.width = t->width;
+        src.height = t->height;
+        src.nbins = t->nbins_total;
+        st = spct_cu_ih_build_workspace(&src, 0, t->bins, &ws);
+        if (st == SPCT_OK)
+            st = cuda_status(malloc_async(&scratch, nb + 256 + gs + ws, s), "hist_match alloc");
+        if (st == SPCT_OK) {
+            char* sp = static_cast<char*>(scratch);
+            uint16_t* bins = reinterpret_cast<uint16_t*>(sp);
+            gate = reinterpret_cast<uint32_t*>(sp + nb);
+            uint32_t* gsum = gs ? reinterpret_cast<uint32_t*>(sp + nb + 256) : nullptr;
+            src.plane[0] = bins;
+            st = ih_recover_bins(*t, bins, t->width, gate, gsum, s);
+            spct_ih nodata = *t;
+            nodata.data = nullptr;
+            if (st == SPCT_OK)
+                st = spct_cu_ih_build_match_map(&src, &nodata, tmpl, kw, kh, p, metric, map, sp + nb + 256 + gs, ws,
+                                                stream);
+        }
+    }
+    // the reference's operation order over the tensor itself, each window normalised by its
+    // actual total (gated by the one-hot check above when that ran)
+    if (st == SPCT_OK) st = hist_partial_impl(t, tmpl, kw, kh, p, metric, part, 0, 1, stream, gate);
+    if (st == SPCT_OK) st = finalize_impl(part, t->width, t->height, kw, kh, p, metric, map, stream, gate);
     cudaFreeAsync(part, s);
+    if (scratch) cudaFreeAsync(scratch, s);
     return st;
+}
+}  // namespace
+
+extern "C" spct_status spct_cu_hist_match(const spct_ih* t, const double* tmpl, int kw, int kh, double p, int metric,
+                                          double* map, void* stream) {
+    return hist_match_impl(t, tmpl, kw, kh, p, metric, map, stream, std::getenv("SPCT_EXACT_MAPS") != nullptr);
+}
+
+extern "C" spct_status spct_cu_hist_match_exact(const spct_ih* t, const double* tmpl, int kw, int kh, double p,
+                                                int metric, double* map, void* stream) {
+    return hist_match_impl(t, tmpl, kw, kh, p, metric, map, stream, true);
 }

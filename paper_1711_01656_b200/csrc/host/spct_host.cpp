@@ -112,7 +112,7 @@ public:
             std::lock_guard<std::mutex> lock(mu_);
             for (std::size_t i = 1; i < parts; ++i) {
                 const std::size_t off = std::min(n, i * step), len = std::min(n, off + step) - off;
-                jobs_.push_back({static_cast<char*>(dst) + off, static_cast<const char*>(src) + off, len});
+                jobs_.push_back({static_cast<char*>(dst) + off, src ? static_cast<const char*>(src) + off : nullptr, len});
             }
             pending_ += parts - 1;
         }
@@ -631,7 +631,10 @@ void hist_match_map_into(const IntegralHistogramTensor& t, const std::vector<dou
         check(spct_cu_ih_build_match_map(&dt.src, &nodata, tm.as<double>(), kw, kh, p, int(metric), map.as<double>(),
                                          work.p, ws, nullptr));
     } else {
-        check(spct_cu_hist_match(&d, tm.as<double>(), kw, kh, p, int(metric), map.as<double>(), nullptr));
+        // a stored tensor: read once (bins recovered on the device), or the reference's
+        // operation order in exact mode
+        check((exact_maps() ? spct_cu_hist_match_exact : spct_cu_hist_match)(&d, tm.as<double>(), kw, kh, p,
+                                                                           int(metric), map.as<double>(), nullptr));
     }
     out.width = t.width;
     out.height = t.height;

@@ -93,6 +93,10 @@ int device_sms();
 BuildPlan plan_build_sweep(int width, int height, int bins);
 BuildPlan plan_fused_sweep(int width, int height, int bins);
 
+// Recover the bin map of a one-hot device tensor (tensor_match.cu).
+spct_status ih_recover_bins(const spct_ih& t, uint16_t* bins, int64_t bins_pitch, uint32_t* flag, uint32_t* gsum,
+                            cudaStream_t s);
+
 // Workspace of the fused path's template prep (fused.cu).
 size_t fused_prep_bytes(int bins);
 

@@ -163,3 +163,60 @@ def test_extension_metrics_match_published_implementations(P, name):
         tensor = P.hist_match_map(tens, t, kw, kh, 1.0, metric, exact=True).cpu().numpy()
         assert np.abs(fused - want).max() <= 1e-12, (key, "fused")
         assert np.abs(tensor - want).max() <= 1e-12, (key, "tensor")
+
+
+def _roundtrip(P, tmp_path, t):
+    path = tmp_path / "t.iht"
+    P.dump_tensor(t, path)
+    return P.load_tensor(path)  # no source frame: hist_distance_map reads the tensor
+
+
+@pytest.mark.parametrize("w,h,bins,kw,kh", [(300, 170, 16, 64, 32), (517, 389, 128, 64, 64),
+                                           (129, 260, 200, 17, 9), (1000, 77, 7, 128, 31), (64, 64, 1, 8, 8)])
+def test_tensor_matcher_reads_loaded_tensor_once(P, tmp_path, w, h, bins, kw, kh):
+    """spct_cu_hist_match on a tensor without a source frame: recovered bin map + fused
+    sweep.  Crop templates (p = 1, kw*kh a power of two where it is) are bit-exact with the
+    reference arithmetic (exact=True and the oracle); general templates within 1e-5."""
+    img = oracle.smooth_image(w, h, 3 + w) if bins <= 256 else None
+    qb = oracle.quantize(img, bins) if bins <= 256 else oracle.random_binmap(w, h, bins, 5)
+    t = _roundtrip(P, tmp_path, P.build_integral_histogram(qb.astype(np.uint16), bins))
+    assert t.source is None
+    y0, x0 = (h - kh) // 2, (w - kw) // 2
+    crop = qb[y0:y0 + kh, x0:x0 + kw]
+    tc = np.bincount(crop.reshape(-1), minlength=bins).astype(np.float64) / crop.size
+    ref_t = oracle.build_ih(qb, bins)
+    got = P.hist_distance_map(t, tc, kw, kh, 1.0).cpu().numpy()
+    want = oracle.hist_distance_map(ref_t, tc, kw, kh, 1.0)
+    if (kw * kh) & (kw * kh - 1) == 0:
+        assert np.array_equal(got, want)
+    else:
+        assert _close(got, want)
+    assert np.array_equal(P.hist_distance_map(t, tc, kw, kh, 1.0, exact=True).cpu().numpy(), want)
+    tg = _template(bins, 7)
+    for p, metric in ((1.0, 0), (2.0, 0), (1.0, 1), (1.0, 2), (1.0, 3)):
+        got = P.hist_match_map(t, tg, kw, kh, p, metric).cpu().numpy()
+        want = oracle.hist_match_map(ref_t, tg, kw, kh, p, metric)
+        assert _close(got, want), (p, metric)
+
+
+def test_tensor_matcher_detects_non_one_hot_pixels(P, tmp_path):
+    """One pixel counted in two bins, one pixel with a negative count (cells stay >= 0):
+    the bin check flags the tensor and the reference arithmetic runs instead."""
+    rng = np.random.default_rng(21)
+    h, w, b = 150, 190, 9
+    bm = rng.integers(0, b, (h, w))
+    for case in ("double", "negative", "sum-one-but-not-one-hot"):
+        counts = np.zeros((b, h, w), np.int64)
+        np.put_along_axis(counts, bm[None], 1, axis=0)
+        if case == "double":
+            counts[(bm[70, 90] + 1) % b, 70, 90] += 1
+        elif case == "negative":
+            counts[:, 40, 40] = 0
+            counts[2, 40, 40], counts[3, 40, 40] = 2, -1  # the count still sums to 1
+        else:
+            counts[:, 100, 150] = 0
+            counts[1, 100, 150], counts[2, 100, 150], counts[3, 100, 150] = 2, -2, 1
+        t = _padded_ih(counts)
+        assert t.min() >= 0
+        got, want = _loaded_map_case(P, tmp_path, counts, 13, 11, 1.0, 4)
+        assert np.array_equal(got, want), case
