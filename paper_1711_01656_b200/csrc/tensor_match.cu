@@ -30,108 +30,166 @@ namespace spct_tmatch {
 constexpr int kWarps = 16;
 constexpr int kBinsPerWarp = 8;
 constexpr int kGroup = kWarps * kBinsPerWarp;  // bins per CTA (grid.z = bin groups)
-constexpr int kBatch = 4;                      // planes loaded per batch (16-byte loads in flight)
+constexpr int kStages = 3;                     // rows of every plane in flight per warp
+constexpr int kRowWords = kStrip + 4;          // staged plane row: 4 words left of the strip + the strip
+constexpr size_t kStageBytes = size_t(kWarps) * kBinsPerWarp * kRowWords * 4;
+constexpr size_t kSmemBytes = kStages * kStageBytes + 2 * kWarps * kStrip * 4 + kStages * kWarps * 8;
 
-// CTA = (128-column strip, band of rows, group of 128 bins); warp w owns bins
-// 128 g + 8 w .. +7; lane l owns columns 4l .. 4l+3 of the strip.  Per row and column the
-// warp accumulates the moments of its bins' vertical differences dv_k = H_k(y+1, x+1) -
-// H_k(y, x+1):  Mk = sum_k k dv_k and N = sum_k dv_k; their horizontal differences are the
-// pixel's bin and count (linearity), and every p_k is checked to lie in {0, 1}.  The 16
-// warps' partials are summed through shared memory (double-buffered by row parity, one
-// barrier per row).  One group: the bin is final and written as uint16; several groups:
-// the partials are added into gsum (u32 bin sum, u32 count) and bins_finalize_kernel
-// converts them.
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+// One bulk (TMA) copy global -> shared that completes on `bar` (16-byte aligned, size % 16 == 0).
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+    asm volatile("cp.async.bulk.shared::cta.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     smem_u32(dst)),
+                 "l"(src), "r"(bytes), "r"(smem_u32(bar))
+                 : "memory");
+}
+
+// CTA = (128-column strip, band of rows, group of 128 bins); warp w owns bins 128 g + 8 w ..
+// +7; lane l owns columns 4l .. 4l+3 of the strip.  Each warp streams its own planes:
+// lane 0 issues, per row and plane, one bulk copy of the plane row's 132 words (the strip
+// and the 4 words to its left) into a 3-stage shared ring armed on the warp's mbarrier,
+// so three rows of every plane are in flight without holding registers.  Per row and
+// column the warp accumulates the moments of its planes' vertical differences dv_k =
+// H_k(y+1, x+1) - H_k(y, x+1): M = sum_k (k - 128 g) dv_k and N = sum_k dv_k, whose
+// horizontal differences are the pixel's bin and count (linearity), and checks every
+// p_k = dv_k(x) - dv_k(x - 1) to lie in {0, 1}.  The 16 warps' partials (u16 bin | u16
+// count) are summed through shared memory, double-buffered by row parity: one barrier
+// per row.  One group: the bin is final and written as uint16; several groups: the
+// partials are added into gsum (u32 bin, u32 count) and bins_finalize_kernel converts.
 __global__ void __launch_bounds__(512, 1) ih_bins_kernel(spct_ih t, int band_rows, uint16_t* __restrict__ bins,
                                                          int64_t bins_pitch, uint32_t* __restrict__ gsum,
                                                          uint32_t* __restrict__ flag) {
-    __shared__ uint32_t part[2][2][kWarps][kStrip];  // [parity][idx | cnt][warp][column]
+    extern __shared__ __align__(128) uint32_t sm[];
+    uint32_t* ring = sm;                                                       // [stage][warp][plane][132]
+    uint32_t* part = ring + kStages * kStageBytes / 4;                         // [parity][warp][column]
+    uint64_t* bars = reinterpret_cast<uint64_t*>(part + 2 * kWarps * kStrip);  // [stage][warp]
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int xs = blockIdx.x * kStrip, x0 = xs + 4 * lane;
     const int y0 = blockIdx.y * band_rows, y1 = min(t.height, y0 + band_rows);
-    const int kb = blockIdx.z * kGroup + warp * kBinsPerWarp;  // warp's first bin
+    const int g0 = blockIdx.z * kGroup;
+    const int kb = g0 + warp * kBinsPerWarp;  // warp's first bin
     const int nk = max(0, min(kBinsPerWarp, t.bins - kb));
-    const bool lane_live = x0 < t.width;                        // row_pitch is a multiple of 128 B
-    const uint32_t* base = t.data + static_cast<int64_t>(kb) * t.plane_pitch + x0;
-    const uint32_t* lbase = t.data + static_cast<int64_t>(kb) * t.plane_pitch + (xs - 1);
+    const bool lane_live = x0 < t.width;
+    // columns past the image edge (row-pitch padding) carry no pixels: not checked
+    const int ncols = min(4, max(0, t.width - x0));
+    // bytes of a staged plane row: the strip (clipped to the row pitch) plus, right of the
+    // first strip, the 16 bytes before it (column xs - 1 is word 3)
+    const int strip_words = static_cast<int>(t.row_pitch - xs < kStrip ? t.row_pitch - xs : kStrip);
+    const int lead = xs > 0 ? 4 : 0;
+    const uint32_t row_bytes = static_cast<uint32_t>(4 * (strip_words + lead));
+    const uint32_t* src0 = t.data + static_cast<int64_t>(kb) * t.plane_pitch + xs - lead;
 
-    uint32_t prev[kBinsPerWarp][4];
+    if (lane == 0)
+        for (int st = 0; st < kStages; ++st) mbar_init(&bars[st * kWarps + warp], 1);
+    if (xs == 0)  // nothing left of the first strip: those words stay 0 in every stage
+        for (int i = threadIdx.x; i < kStages * kWarps * kBinsPerWarp; i += blockDim.x) {
+            uint32_t* r = ring + static_cast<int64_t>(i) * kRowWords;
+            r[0] = r[1] = r[2] = r[3] = 0;
+        }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    __syncthreads();
+
+    auto issue = [&](int y) {  // lane 0: the warp's planes of row y into stage (y - y0) % kStages
+        if (lane != 0 || y >= y1 || nk == 0) return;
+        const int st = (y - y0) % kStages;
+        uint64_t* bar = &bars[st * kWarps + warp];
+        uint32_t* dst = ring + (static_cast<int64_t>(st) * kWarps + warp) * kBinsPerWarp * kRowWords + (4 - lead);
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        mbar_expect_tx(bar, row_bytes * nk);
+        for (int k = 0; k < nk; ++k)
+            bulk_g2s(dst + k * kRowWords, src0 + static_cast<int64_t>(k) * t.plane_pitch +
+                                              static_cast<int64_t>(y) * t.row_pitch, row_bytes, bar);
+    };
+    for (int i = 0; i < kStages; ++i) issue(y0 + i);
+
+    uint32_t prev[kBinsPerWarp][4], prevL[kBinsPerWarp];
 #pragma unroll
     for (int i = 0; i < kBinsPerWarp; ++i) {
         uint4 v = make_uint4(0, 0, 0, 0);
-        if (y0 > 0 && i < nk && lane_live)
-            v = *reinterpret_cast<const uint4*>(base + static_cast<int64_t>(i) * t.plane_pitch +
-                                                static_cast<int64_t>(y0 - 1) * t.row_pitch);
-        prev[i][0] = v.x, prev[i][1] = v.y, prev[i][2] = v.z, prev[i][3] = v.w;
-    }
-    const bool left_live = lane == 0 && xs > 0;  // lane 0 reads the column left of the strip
-
-    for (int y = y0; y < y1; ++y) {
-        const int64_t roff = static_cast<int64_t>(y) * t.row_pitch;
-        uint32_t msum[4] = {0, 0, 0, 0}, nsum[4] = {0, 0, 0, 0}, bad = 0;
-        uint32_t mL = 0, nL = 0;  // the same moments of the column left of the lane (lane 0: x0 - 1)
-#pragma unroll
-        for (int b0 = 0; b0 < kBinsPerWarp; b0 += kBatch) {
-            uint4 cur[kBatch];
-            uint32_t curL[kBatch], prvL[kBatch];
-#pragma unroll
-            for (int i = 0; i < kBatch; ++i) {
-                const int k = b0 + i;
-                const int64_t off = static_cast<int64_t>(k) * t.plane_pitch + roff;
-                cur[i] = (k < nk && lane_live) ? __ldg(reinterpret_cast<const uint4*>(base + off)) : make_uint4(0, 0, 0, 0);
-                curL[i] = (k < nk && left_live) ? __ldg(lbase + off) : 0u;
-                prvL[i] = (k < nk && left_live && y > 0) ? __ldg(lbase + off - t.row_pitch) : 0u;
-            }
-#pragma unroll
-            for (int i = 0; i < kBatch; ++i) {
-                const int k = b0 + i;
-                const uint32_t kk = static_cast<uint32_t>(kb + k);
-                const uint32_t c4[4] = {cur[i].x, cur[i].y, cur[i].z, cur[i].w};
-                uint32_t dv[4];
-#pragma unroll
-                for (int j = 0; j < 4; ++j) {
-                    dv[j] = c4[j] - prev[k][j];
-                    prev[k][j] = c4[j];
-                }
-                // the left neighbour's dv of this plane: lane l - 1's column 3, lane 0's own load
-                const uint32_t dl = curL[i] - prvL[i];
-                uint32_t left = __shfl_up_sync(0xffffffffu, dv[3], 1);
-                if (lane == 0) left = dl;
-#pragma unroll
-                for (int j = 0; j < 4; ++j) {
-                    const uint32_t p = dv[j] - (j ? dv[j - 1] : left);  // the pixel's count of bin kk
-                    bad |= p & ~1u;
-                    msum[j] += kk * dv[j];
-                    nsum[j] += dv[j];
-                }
-                mL += kk * left;
-                nL += left;
-            }
+        uint32_t l = 0;
+        if (y0 > 0 && i < nk) {
+            const int64_t off = static_cast<int64_t>(i) * t.plane_pitch + static_cast<int64_t>(y0 - 1) * t.row_pitch;
+            if (lane_live) v = *reinterpret_cast<const uint4*>(src0 + lead + 4 * lane + off);
+            if (lane == 0 && lead) l = src0[off + 3];
         }
-        // bin = M(x) - M(x - 1), count = N(x) - N(x - 1); a p_k outside {0, 1} flags the tensor
+        prev[i][0] = v.x, prev[i][1] = v.y, prev[i][2] = v.z, prev[i][3] = v.w;
+        prevL[i] = l;
+    }
+
+    const uint32_t kbase = static_cast<uint32_t>(warp * kBinsPerWarp);  // bin relative to the group
+    for (int y = y0; y < y1; ++y) {
+        const int st = (y - y0) % kStages;
+        if (nk) mbar_wait(&bars[st * kWarps + warp], static_cast<uint32_t>(((y - y0) / kStages) & 1));
+        const uint32_t* rows = ring + (static_cast<int64_t>(st) * kWarps + warp) * kBinsPerWarp * kRowWords;
+        uint32_t msum[4] = {0, 0, 0, 0}, nsum[4] = {0, 0, 0, 0}, bad = 0, mL = 0, nL = 0;
+#pragma unroll
+        for (int k = 0; k < kBinsPerWarp; ++k) {
+            if (k >= nk) break;
+            const uint4 c = *reinterpret_cast<const uint4*>(rows + k * kRowWords + 4 + 4 * lane);
+            const uint32_t cl = rows[k * kRowWords + 3];
+            const uint32_t c4[4] = {c.x, c.y, c.z, c.w};
+            uint32_t dv[4];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                dv[j] = c4[j] - prev[k][j];
+                prev[k][j] = c4[j];
+            }
+            const uint32_t dl = cl - prevL[k];  // lane 0: the column left of the strip
+            prevL[k] = cl;
+            uint32_t left = __shfl_up_sync(0xffffffffu, dv[3], 1);
+            if (lane == 0) left = dl;
+            const uint32_t kk = kbase + static_cast<uint32_t>(k);
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                const uint32_t p = dv[j] - (j ? dv[j - 1] : left);  // the pixel's count of bin kk
+                if (j < ncols) bad |= p & ~1u;
+                msum[j] += kk * dv[j];
+                nsum[j] += dv[j];
+            }
+            mL += kk * left;
+            nL += left;
+        }
+        __syncwarp();
+        issue(y + kStages);  // this stage is consumed: refill it with row y + 3
         if (__any_sync(0xffffffffu, bad != 0) && lane == 0) atomicOr(flag, 1u);
-        uint32_t* pi = &part[y & 1][0][warp][4 * lane];
-        uint32_t* pc = &part[y & 1][1][warp][4 * lane];
+        // with every p_k in {0, 1} the warp's bin partial is < 8 * 128 and its count <= 8
         const uint32_t mprev[4] = {mL, msum[0], msum[1], msum[2]}, nprev[4] = {nL, nsum[0], nsum[1], nsum[2]};
-        uint4 wi, wc;
-        wi.x = msum[0] - mprev[0], wi.y = msum[1] - mprev[1], wi.z = msum[2] - mprev[2], wi.w = msum[3] - mprev[3];
-        wc.x = nsum[0] - nprev[0], wc.y = nsum[1] - nprev[1], wc.z = nsum[2] - nprev[2], wc.w = nsum[3] - nprev[3];
-        *reinterpret_cast<uint4*>(pi) = wi;
-        *reinterpret_cast<uint4*>(pc) = wc;
+        uint4 w;
+        w.x = ((msum[0] - mprev[0]) & 0xFFFFu) | ((nsum[0] - nprev[0]) << 16);
+        w.y = ((msum[1] - mprev[1]) & 0xFFFFu) | ((nsum[1] - nprev[1]) << 16);
+        w.z = ((msum[2] - mprev[2]) & 0xFFFFu) | ((nsum[2] - nprev[2]) << 16);
+        w.w = ((msum[3] - mprev[3]) & 0xFFFFu) | ((nsum[3] - nprev[3]) << 16);
+        *reinterpret_cast<uint4*>(part + ((y & 1) * kWarps + warp) * kStrip + 4 * lane) = w;
         __syncthreads();
         if (threadIdx.x < kStrip) {
             const int c = threadIdx.x, x = xs + c;
-            uint32_t si = 0, sc = 0;
+            uint32_t s = 0;
 #pragma unroll
-            for (int w = 0; w < kWarps; ++w) {
-                si += part[y & 1][0][w][c];
-                sc += part[y & 1][1][w][c];
-            }
+            for (int w2 = 0; w2 < kWarps; ++w2) s += part[((y & 1) * kWarps + w2) * kStrip + c];
+            const uint32_t si = (s & 0xFFFFu) + static_cast<uint32_t>(g0), sc = s >> 16;
             if (x < t.width) {
                 if (gridDim.z == 1) {
                     const bool ok = sc == 1u && si < static_cast<uint32_t>(t.bins);
                     bins[static_cast<int64_t>(y) * bins_pitch + x] = ok ? static_cast<uint16_t>(si) : 0;
                     if (!ok) atomicOr(flag, 1u);
-                } else {
+                } else if (sc) {
                     uint32_t* g = gsum + 2 * (static_cast<int64_t>(y) * t.width + x);
                     atomicAdd(g, si);
                     atomicAdd(g + 1, sc);
@@ -181,7 +239,8 @@ spct_status ih_recover_bins(const spct_ih& t, uint16_t* bins, int64_t bins_pitch
     const int band_rows = static_cast<int>(std::max<int64_t>(16, ceil_div(t.height, want)));
     dim3 grid(nstrips, static_cast<unsigned>(ceil_div(t.height, band_rows)), ngroups);
     const int prof = prof_begin("ih_recover_bins", s);
-    ih_bins_kernel<<<grid, 32 * kWarps, 0, s>>>(t, band_rows, bins, bins_pitch, gsum, flag);
+    ensure_smem(ih_bins_kernel, kSmemBytes);
+    ih_bins_kernel<<<grid, 32 * kWarps, kSmemBytes, s>>>(t, band_rows, bins, bins_pitch, gsum, flag);
     prof_end(prof, s);
     if (auto st = launch_status("ih_bins_kernel")) return st;
     if (ngroups > 1) {

@@ -47,7 +47,7 @@ int main(int argc, char** argv) {
         std::uint64_t s = 0;
         for (int i = 0; i < 100; ++i) s += region_histogram(t, Rect{(i * 7) % (n - 64), (i * 5) % (n - 64), 64, 64})[0];
         auto e = clk::now();
-        auto mf = likelihood_from_frame(img, bins, tmpl, 64, 64, 1.0);
+        auto mf = likelihood_from_frame(img, bins, tmpl, 64, 64, 1.0, nullptr, ~0ull);
         auto g = clk::now();
         checksum += m.values[std::size_t(n / 2) * n + n / 2] + mf.values[7] + double(s);
         if (f == 0) continue;  // warm-up
