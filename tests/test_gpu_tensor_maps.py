@@ -220,3 +220,16 @@ def test_tensor_matcher_detects_non_one_hot_pixels(P, tmp_path):
         assert t.min() >= 0
         got, want = _loaded_map_case(P, tmp_path, counts, 13, 11, 1.0, 4)
         assert np.array_equal(got, want), case
+
+
+def test_tensor_matcher_ignores_row_pitch_padding(P, tmp_path):
+    """Cells between width and the 128-byte row pitch carry no pixels: garbage there must
+    not change the map (nor the bin check)."""
+    img = oracle.smooth_image(1000, 150, 8)
+    bins = 12
+    t = _roundtrip(P, tmp_path, P.build_integral_histogram(img, bins))
+    assert t.row_pitch > t.width
+    t.planes()[:, :, t.width:] = 12345
+    tm = _template(bins, 3)
+    want = oracle.hist_distance_map(oracle.build_ih(oracle.quantize(img, bins), bins), tm, 33, 17, 1.0)
+    assert _close(P.hist_distance_map(t, tm, 33, 17, 1.0).cpu().numpy(), want)
