@@ -11,7 +11,7 @@ NVFLAGS   ?= -O3 -lineinfo -std=c++17 $(ARCH) -Xcompiler -fPIC -Xptxas -warn-spi
 PKG        = paper_1711_01656_b200
 CSRC       = $(PKG)/csrc
 LIB        = $(PKG)/libspct_b200.so
-CU_SRCS    = $(CSRC)/ih_build.cu $(CSRC)/carries.cu $(CSRC)/hist_match.cu $(CSRC)/fused.cu $(wildcard $(CSRC)/fused_kw*_nw*.cu) $(CSRC)/orientation.cu $(CSRC)/iht1.cu $(CSRC)/consumers.cu $(CSRC)/swih.cu $(CSRC)/swlh_fused.cu $(CSRC)/motion.cu $(CSRC)/peer.cu $(CSRC)/profile.cu $(CSRC)/tensor_match.cu
+CU_SRCS    = $(CSRC)/ih_build.cu $(CSRC)/carries.cu $(CSRC)/hist_match.cu $(CSRC)/fused.cu $(wildcard $(CSRC)/fused_kw*_s*.cu) $(CSRC)/orientation.cu $(CSRC)/iht1.cu $(CSRC)/consumers.cu $(CSRC)/swih.cu $(CSRC)/swlh_fused.cu $(CSRC)/motion.cu $(CSRC)/peer.cu $(CSRC)/profile.cu $(CSRC)/tensor_match.cu
 HOST_SRCS  = $(CSRC)/host/spct_host.cpp
 HDRS       = include/spct_cuda.h $(CSRC)/spct_device.cuh $(CSRC)/spct_internal.h $(CSRC)/sweep_common.cuh $(CSRC)/fused_kernel.cuh $(wildcard include/spct/*.hpp)
 OBJDIR     = build/obj

@@ -84,12 +84,13 @@ spct_status build_match(const spct_source* src, const spct_ih* out, const double
     }
     const BuildPlan bp = plan_fused_sweep(out->width, out->height, out->bins);
     // Band tops start their running column counts from the carry tables when that takes
-    // fewer load rounds than re-reading the kh - 1 rows above (few bins per CTA); with a
-    // full 128-bin group the row pre-roll costs the same and needs no extra table.
-    const int nw_plan = fused_nw(out->bins), nt_plan = 32 * nw_plan;
-    const int64_t table_rounds = ceil_div(static_cast<int64_t>(std::min(out->bins, kGroupBins)) * kVcWords, 8 * nt_plan);
-    const int64_t preroll_rounds = ceil_div(static_cast<int64_t>(kExt / nt_plan) * (kh - 1), 8);
-    const int win_kh = (kh > 1 && nw_plan < 8 && table_rounds < preroll_rounds) ? kh : 0;
+    // fewer load rounds than re-reading the kh - 1 rows above (narrow histograms, several
+    // strips per CTA); with a full 128-bin group the row pre-roll costs the same and needs
+    // no extra table (the kernel reads the tables only for groups under 128 bins).
+    const int S = fused_strips(out->bins), ext = kStrip * (S + 1), nt = 256;
+    const int64_t table_rounds = ceil_div(static_cast<int64_t>(std::min(out->bins, kGroupBins)) * (ext / 2), 8 * nt);
+    const int64_t preroll_rounds = ceil_div(ceil_div(ext, nt) * (kh - 1), 8);
+    const int win_kh = (kh > 1 && out->bins < kGroupBins && table_rounds < preroll_rounds) ? kh : 0;
     const size_t carry_bytes = out->data ? fused_carry_layout(bp, out->height, win_kh > 1).total : 0;
     const size_t need = carry_bytes + fused_prep_bytes(out->bins);
     if (!workspace || workspace_bytes < need) return contract("ih_build_match: workspace too small");
@@ -138,16 +139,16 @@ spct_status build_match(const spct_source* src, const spct_ih* out, const double
     for (int g = 0; g < ngroups; ++g) {
         f.group0 = g * kGroupBins;
         f.accumulate = g > 0;
-        dim3 grid(bp.nstrips, bp.nbands, 1);
+        dim3 grid(static_cast<unsigned>(ceil_div(bp.nstrips, S)), bp.nbands, 1);
         const int prof = prof_begin(out->data ? "ih_sweep_match" : "sweep_match_nostore", s);
         // the group is the whole histogram: window totals over its bins are kw * kh
         const bool allb = out->bin0 == 0 && out->bins == out->nbins_total && ngroups == 1;
         const int sk = (q.kind == SPCT_SRC_GRAY_U8 && q.fast_u8) ? 1 : (q.kind == SPCT_SRC_BINS_U16 ? 2 : 0);
-        const int nw = fused_nw(out->bins);
 #define SPCT_LAUNCH(KW)                                                                                     \
-    if (nw == 8) launch_##KW##_nw8(allb, sk, grid, s, q, pm, *out, bp, fc, f);                                  \
-    else if (nw == 4) launch_##KW##_nw4(allb, sk, grid, s, q, pm, *out, bp, fc, f);                             \
-    else launch_##KW##_nw2(allb, sk, grid, s, q, pm, *out, bp, fc, f);
+    if (S == 1) launch_##KW##_s1(allb, sk, grid, s, q, pm, *out, bp, fc, f);                                    \
+    else if (S == 2) launch_##KW##_s2(allb, sk, grid, s, q, pm, *out, bp, fc, f);                               \
+    else if (S == 4) launch_##KW##_s4(allb, sk, grid, s, q, pm, *out, bp, fc, f);                               \
+    else launch_##KW##_s8(allb, sk, grid, s, q, pm, *out, bp, fc, f);
         if (kw == 64) {
             SPCT_LAUNCH(kw64)
         } else if (kw == 128) {

@@ -269,49 +269,67 @@ __device__ __forceinline__ void quarter_reduce(uint32_t (&v)[8], int q) {
     }
 }
 
+// Geometry of a CTA with S strips side by side (S * 128 columns of windows) and NWB =
+// 8 / S warps per strip (16 NWB bins).  Narrow histograms (16 NWB bins <= 64) use several
+// strips per CTA, so every CTA has 8 warps and the 128-column halo of staged columns (the
+// kw - 1 columns left of the first window) is shared by S strips instead of one.
+template <int S>
+struct Geo {
+    static constexpr int NW = 8;                      // warps per CTA
+    static constexpr int NWB = NW / S;                // warps (16-bin slabs) per strip
+    static constexpr int NB = NWB * kB;               // bins per CTA
+    static constexpr int NT = 32 * NW;                // threads per CTA
+    static constexpr int E = kStrip * (S + 1);        // staged ("extended") columns
+    static constexpr int VW = E / 2;                  // u16-pair words per bin row of vc
+    static constexpr int VS = VW + VW / 8;            // padded row stride (4 words per 32)
+    static constexpr int CPT = (E + NT - 1) / NT;     // staged columns per thread
+    static constexpr int WOFF = kVcWords / 2 + kVcWords / 16;  // padded vc words per strip (72)
+};
+
 // ALLB (integer path only): the CTA's bin group is the whole histogram, so the window
 // total over the group's bins is kw * kh and need not be accumulated.
 // SK (source kind of the staging loads): 1 = 8-bit gray with the default range
 // (bin = v * nbins >> 8), 2 = a uint16 BinMap (bin = v), 0 = the generic per-kind dispatch.
-// NW: warps per CTA (16 NW bins of the group): 8 for >= 65 bins, fewer for small
-// histograms so that every warp of a CTA has bins (configs 2 and 5 use 32 bins).
-template <int NW>
-constexpr size_t smem_bytes_nw() {
-    return (size_t(NW * kB) * kVcStride + size_t(NW) * 4 * kVcWords) * 4 + size_t(2) * NW * kStrip * 8 +
-           size_t(NW * kB) * 4 * 3 + size_t(2) * kStrip * 2 + 64 * 4;
+// S: strips per CTA (Geo<S>); 1 for >= 65 bins, 2 / 4 / 8 for <= 64 / 32 / 16 bins.
+template <int S>
+constexpr size_t smem_bytes_s() {
+    using G = Geo<S>;
+    return (size_t(G::NB) * G::VS + size_t(G::NW) * 4 * kVcWords + G::NB + 2 * S * G::NB + 64) * 4 +
+           size_t(2) * G::NW * kStrip * 8 + size_t(2) * kStrip * S * 2;
 }
 
-template <bool STORE, bool FAST, int KWM, bool ALLB, int SK, int NW>
-__global__ void __launch_bounds__(32 * NW, 16 / NW) sweep_match_kernel(QuantParams q, PixelMode pm, spct_ih out, int Lb,
-                                                                       int Wp, int band_rows, FusedCarries fc,
-                                                                       FusedParams f) {
-    constexpr int NB = NW * kB;              // bins per CTA
-    constexpr int NT = 32 * NW;              // threads per CTA
-    constexpr int CPT = kExt / NT;           // staged extended columns per thread
+template <bool STORE, bool FAST, int KWM, bool ALLB, int SK, int S>
+__global__ void __launch_bounds__(256, 2) sweep_match_kernel(QuantParams q, PixelMode pm, spct_ih out, int Lb, int Wp,
+                                                             int band_rows, int nstrips, FusedCarries fc,
+                                                             FusedParams f) {
+    using G = Geo<S>;
+    constexpr int NW = G::NW, NWB = G::NWB, NB = G::NB, NT = G::NT, E = G::E, VS = G::VS, CPT = G::CPT;
     extern __shared__ uint4 smem_raw[];
-    uint32_t* vc = reinterpret_cast<uint32_t*>(smem_raw);                 // [NB bins][144 words], padded
-    uint32_t* gbuf = vc + NB * kVcStride;                                   // [NW warps][4][128 words] (general path)
+    uint32_t* vc = reinterpret_cast<uint32_t*>(smem_raw);                 // [NB bins][VS words], padded
+    uint32_t* gbuf = vc + NB * VS;                                          // [NW warps][4][128 words] (general kw)
     double* red = reinterpret_cast<double*>(gbuf + NW * 4 * kVcWords);      // [2 rows][NW warps][128]
     uint32_t* srep_s = reinterpret_cast<uint32_t*>(red + 2 * NW * kStrip);  // [NB]
-    uint32_t* lrow = srep_s + NB;                                           // [2 rows][NB] row carries
-    uint16_t* rowbins = reinterpret_cast<uint16_t*>(lrow + 2 * NB);         // [2 rows][128] strip bins
-    uint32_t* amask = reinterpret_cast<uint32_t*>(rowbins + 2 * kStrip);    // [8 lanes][8 words] anchor masks
-    // integer path: per row parity and window pair, the packed sums over the warps (atomic
-    // adds), I at [parity][64] and C at 128 + [parity][64]
+    uint32_t* lrow = srep_s + NB;                                           // [2 rows][S strips][NB] row carries
+    uint16_t* rowbins = reinterpret_cast<uint16_t*>(lrow + 2 * S * NB);     // [2 rows][S * 128] strip bins
+    uint32_t* amask = reinterpret_cast<uint32_t*>(rowbins + 2 * kStrip * S);  // [8 lanes][8 words] anchor masks
+    // integer path: per row parity, strip and window pair, the packed sums over the warps
+    // (shared atomics), I at [parity][strip][64] and C at 128 S + [parity][strip][64]
     uint32_t* red32 = reinterpret_cast<uint32_t*>(red);
 
     // Both variants are launched; the one that does not match the template prep exits.
     if ((__ldg(f.prep) != 0) != FAST) return;
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int strip = blockIdx.x, band = blockIdx.y;
+    const int sc = warp / NWB, wb = warp % NWB;            // the warp's strip in the CTA, bin slab
+    const int strip = blockIdx.x * S + sc, band = blockIdx.y;
     const int g0 = f.group0;                               // slab-local first bin of the CTA
     const int nb_cta = min(NB, out.bins - g0);
-    const int nwarps_live = (nb_cta + kB - 1) / kB;
-    const int kl0 = g0 + warp * kB;                        // warp's first slab-local bin
-    const bool warp_live = warp < nwarps_live;
+    const int nwarps_live = (nb_cta + kB - 1) / kB;        // live bin slabs per strip
+    const int kl0 = g0 + wb * kB;                          // warp's first slab-local bin
+    const int xc = blockIdx.x * S * kStrip;                // CTA's first column
+    const int xs = strip * kStrip;                         // warp's strip's first column
+    const bool warp_live = wb < nwarps_live && strip < nstrips;
     const int k_live = min(kB, out.bins - kl0);
-    const int xs = strip * kStrip;                         // strip's first column
     const int xl = xs + 4 * lane;                          // lane's first strip column
     const int H = out.height, W = out.width;
     const int y0 = band * band_rows, y1 = min(H, y0 + band_rows);
@@ -330,9 +348,9 @@ __global__ void __launch_bounds__(32 * NW, 16 / NW) sweep_match_kernel(QuantPara
         return bin_of_raw(r, q);
     };
 
-    for (int i = tid; i < NB * kVcStride; i += NT) vc[i] = 0;
+    for (int i = tid; i < NB * VS; i += NT) vc[i] = 0;
     if (FAST)
-        for (int i = tid; i < 256; i += NT) red32[i] = 0;  // row accumulators {I} [2][64] and {C} [2][64]
+        for (int i = tid; i < 4 * 64 * S; i += NT) red32[i] = 0;  // row accumulators {I} [2][S][64], {C} [2][S][64]
     if (tid < NB) srep_s[tid] = (FAST && tid < nb_cta) ? __ldg(f.prep + 1 + g0 + tid) : 0u;
     if (FAST && KWM == 0)
         for (int i = tid; i < 64; i += NT) {
@@ -343,27 +361,27 @@ __global__ void __launch_bounds__(32 * NW, 16 / NW) sweep_match_kernel(QuantPara
 
     uint32_t V[4][kB];
     if (STORE && warp_live)
-        vpart_init_ca<kB>(V, fc.C, fc.A, band, strip, gridDim.y, gridDim.x, Lb, Wp, kl0, xl);
+        vpart_init_ca<kB>(V, fc.C, fc.A, band, strip, gridDim.y, nstrips, Lb, Wp, kl0, xl);
     uint32_t* base_ptr = STORE ? out.data + static_cast<int64_t>(kl0) * out.plane_pitch + xl : nullptr;
     const bool lane_live = xl < out.row_pitch;
-    const uint32_t store_mask = lane_live ? (k_live >= 32 ? 0xFFFFFFFFu : (1u << max(k_live, 0)) - 1u) : 0u;
-    const long long S = FAST ? f.S_group[g0 / kGroupBins] : 0;
+    const uint32_t store_mask = (lane_live && warp_live) ? (k_live >= 32 ? 0xFFFFFFFFu : (1u << max(k_live, 0)) - 1u) : 0u;
+    const long long Sg = FAST ? f.S_group[g0 / kGroupBins] : 0;
+    // the warp's view of vc: ext columns [128 sc, 128 sc + 256) = padded words from 72 sc
+    const uint32_t* vwarp = vc + wb * kB * VS + G::WOFF * sc;
     // general path: G(e - kw) as a word and a bit shift
     const int idx = kStrip + 4 * lane - f.kw;
     const int pw = idx >> 1, psh = (idx & 1) * 16;
     uint32_t* gb = gbuf + warp * 4 * kVcWords;
-    const uint32_t* vwarp = vc + warp * kB * kVcStride;
     // integer path: quarter qq of the warp takes bin 4g + qq; lane mq owns windows 16mq ..
     const int qq = lane >> 3, mq = lane & 7;
     const int ca0 = kStrip + 16 * mq - f.kw;  // extended column of vc(e - kw) for the lane's first window
     const int aw0 = ca0 >> 1, apsh = (ca0 & 1) * 16;
-    const uint32_t* vq = vwarp + qq * kVcStride;  // the quarter's bin row for g = 0
+    const uint32_t* vq = vwarp + qq * VS;  // the quarter's bin row for g = 0
     const uint32_t* pb = vq + vcw(64 + 8 * mq);
 
-    // staging: thread tid owns extended columns tid + c NT (c < CPT); with one column per
-    // thread (NW = 8) its raw pixels are prefetched one row ahead
-    // (narrow CTAs, several columns per thread: prefetched as 32-bit raw values for the
-    // 8/16-bit sources; the generic source keeps the in-row loads)
+    // staging: thread tid owns extended columns tid + c NT (c < CPT, col < E); their raw
+    // pixels are prefetched one row ahead (32-bit raw values for the 8/16-bit sources; the
+    // generic source with several columns per thread keeps the in-row loads)
     constexpr bool PREFETCH = CPT == 1 || SK != 0;
     using RawT = std::conditional_t<CPT == 1 || SK == 0, uint64_t, uint32_t>;
     int xt[CPT], vcol_w[CPT];
@@ -372,13 +390,16 @@ __global__ void __launch_bounds__(32 * NW, 16 / NW) sweep_match_kernel(QuantPara
 #pragma unroll
     for (int c = 0; c < CPT; ++c) {
         const int col = tid + c * NT;
-        xt[c] = xs - kStrip + col;
-        xt_live[c] = xt[c] >= 0 && xt[c] < W;
+        xt[c] = xc - kStrip + col;
+        xt_live[c] = col < E && xt[c] >= 0 && xt[c] < W;
         vcol_w[c] = vcw(col >> 1);  // the column's (padded) vc word
         vinc[c] = 1u << (16 * (col & 1));
     }
-    const uint16_t* lt_cta = (STORE && fc.Lt && strip > 0 && tid < NB && g0 + tid < Lb)
-                                 ? fc.Lt + static_cast<int64_t>(strip) * H * Lb + g0 + tid
+    // row carries: thread tid < S NB loads those of bin tid % NB of strip tid / NB
+    const int lt_strip = blockIdx.x * S + tid / NB;
+    const uint16_t* lt_cta = (STORE && fc.Lt && tid < S * NB && lt_strip > 0 && lt_strip < nstrips &&
+                              g0 + tid % NB < Lb)
+                                 ? fc.Lt + static_cast<int64_t>(lt_strip) * H * Lb + g0 + tid % NB
                                  : nullptr;
     // raw pixel values of the staging column, quantised one row after the load
     RawT rn[CPT], ro[CPT];
@@ -391,9 +412,9 @@ __global__ void __launch_bounds__(32 * NW, 16 / NW) sweep_match_kernel(QuantPara
     uint32_t lpre = lt_cta ? static_cast<uint32_t>(__ldg(lt_cta + static_cast<int64_t>(y0) * Lb)) : 0u;
     __syncthreads();  // vc zeroed
 
-    // (narrow CTAs only: with 8 warps the table loads take as many rounds as the pre-roll,
-    // and the branch alone costs the headline variant ~1.5%)
-    if (NW < 8 && fc.S && band > 0 && f.kh > 1) {
+    // (narrow bin groups only: with 128 bins the table loads take as many rounds as the
+    // pre-roll, and the branch alone costs the headline variant ~1.5%)
+    if (NB < kGroupBins && fc.S && band > 0 && f.kh > 1) {
         // vc over rows [ystart, y0) from the carry tables (carries.cu): rows above y0 minus
         // rows above the band holding ystart, plus that band's suffix from ystart
         // (u16 pairs, every true count >= 0 and < 2^16, so no borrow crosses a half)
@@ -402,15 +423,15 @@ __global__ void __launch_bounds__(32 * NW, 16 / NW) sweep_match_kernel(QuantPara
         const int64_t plane = static_cast<int64_t>(Lb) * Wp / 2;  // words per band
         const int r = y0 - f.kh + 1, ib = r > 0 ? r / band_rows : -1;
         constexpr int U = 8;  // loads in flight per thread
-        const int n = nb_cta * kVcWords;
+        const int n = nb_cta * G::VW;
         for (int i0 = tid; i0 < n; i0 += U * NT) {
             uint32_t pj[U], sf[U], pi[U];
 #pragma unroll
             for (int u = 0; u < U; ++u) {
                 const int i = i0 + u * NT;
-                const int k = i / kVcWords, w = i % kVcWords;  // bin, extended-column word (columns 2w, 2w + 1)
-                const int x = xs - kStrip + 2 * w;
-                const bool live = i < n && x >= 0;
+                const int k = i / G::VW, w = i % G::VW;  // bin, extended-column word (columns 2w, 2w + 1)
+                const int x = xc - kStrip + 2 * w;
+                const bool live = i < n && x >= 0 && x < Wp;
                 const int64_t off = ((static_cast<int64_t>(g0 + k) * Wp) + x) >> 1;
                 pj[u] = live ? __ldg(C32 + (band - 1) * plane + off) : 0u;
                 sf[u] = (live && ib >= 0) ? __ldg(S32 + ib * plane + off) : 0u;
@@ -419,13 +440,13 @@ __global__ void __launch_bounds__(32 * NW, 16 / NW) sweep_match_kernel(QuantPara
 #pragma unroll
             for (int u = 0; u < U; ++u) {
                 const int i = i0 + u * NT;
-                if (i < n) vc[(i / kVcWords) * kVcStride + vcw(i % kVcWords)] = ib < 0 ? pj[u] : (ib + 1 == band ? sf[u] : sf[u] + pj[u] - pi[u]);
+                if (i < n) vc[(i / G::VW) * VS + vcw(i % G::VW)] = ib < 0 ? pj[u] : (ib + 1 == band ? sf[u] : sf[u] + pj[u] - pi[u]);
             }
         }
     } else {
-        // No tables (tensor not stored): pre-roll rows [ystart, y0) only feed vc, and
-        // nothing leaves the window there: one barrier-free pass with several loads in
-        // flight (a per-row loop would pay the full DRAM latency on every row).
+        // No tables (tensor not stored, or 128 bins): pre-roll rows [ystart, y0) only feed
+        // vc, and nothing leaves the window there: one barrier-free pass with several loads
+        // in flight (a per-row loop would pay the full DRAM latency on every row).
 #pragma unroll
         for (int c = 0; c < CPT; ++c)
             if (xt_live[c]) {
@@ -439,17 +460,17 @@ __global__ void __launch_bounds__(32 * NW, 16 / NW) sweep_match_kernel(QuantPara
                     for (int i = 0; i < 8; ++i) {
                         const int bn = bin_of(r[i]) - nb_lo;
                         if (y + i < y0 && static_cast<unsigned>(bn) < static_cast<unsigned>(nb_cta))
-                            atomicAdd(vcol + bn * kVcStride, vinc[c]);
+                            atomicAdd(vcol + bn * VS, vinc[c]);
                     }
                 }
             }
     }
 
-    // Cross-warp combine of row yy: thread t < 128 finishes the window ending at strip
+    // Cross-warp combine of row yy: thread t < 128 S finishes the window ending at CTA
     // column t.  Integer path with a finished map (ALLB): L = alpha + beta I (one FMA).
     const bool intersect = f.metric == SPCT_METRIC_INTERSECTION;
     const double lin_b = f.invT;
-    const double lin_a = intersect ? 0.0 : 1.0 - static_cast<double>(static_cast<long long>(f.kw) * f.kh + S) * f.invT * 0.5;
+    const double lin_a = intersect ? 0.0 : 1.0 - static_cast<double>(static_cast<long long>(f.kw) * f.kh + Sg) * f.invT * 0.5;
     auto write_map = [&](int u, int v, double L) {
         // spread_valid's border replication (likelihood.cpp:44-58)
         const int x = u + (f.kw - 1) / 2, yc = v + (f.kh - 1) / 2;
@@ -463,18 +484,18 @@ __global__ void __launch_bounds__(32 * NW, 16 / NW) sweep_match_kernel(QuantPara
             for (int xx = xa; xx <= xb; ++xx) f.map[static_cast<int64_t>(yy) * f.W + xx] = L;
     };
     auto combine_one = [&](int yy, int t) {
-        const int e = xs + t;
+        const int e = xc + t;
         const int u = e - f.kw + 1, v = yy - f.kh + 1;
         if (FAST) {
             // the warps' packed window-pair sums, accumulated in shared memory; every
             // sum stays below 2^16 (at most kw * kh).  Read, then clear for row yy + 2.
-            uint32_t* ai = red32 + (yy & 1) * 64 + (t >> 1);
+            uint32_t* ai = red32 + (yy & 1) * 64 * S + (t >> 1);
             const uint32_t xi = *ai;
-            const uint32_t xc = ALLB ? 0u : ai[128];
+            const uint32_t xcn = ALLB ? 0u : ai[128 * S];
             __syncwarp();
             if (!(t & 1)) {
                 *ai = 0;
-                if (!ALLB) ai[128] = 0;
+                if (!ALLB) ai[128 * S] = 0;
             }
             if (u < 0 || e >= W) return;
             const uint32_t I = (xi >> (16 * (t & 1))) & 0xFFFFu;
@@ -483,9 +504,9 @@ __global__ void __launch_bounds__(32 * NW, 16 / NW) sweep_match_kernel(QuantPara
                 write_map(u, v, fmin(fmax(L, 0.0), 1.0));
                 return;
             }
-            const long long C = ALLB ? static_cast<long long>(f.kw) * f.kh : (xc >> (16 * (t & 1))) & 0xFFFFu;
+            const long long C = ALLB ? static_cast<long long>(f.kw) * f.kh : (xcn >> (16 * (t & 1))) & 0xFFFFu;
             const double term = intersect ? static_cast<double>(I) * f.invT
-                                          : static_cast<double>(C + S - 2 * static_cast<long long>(I)) * f.invT;
+                                          : static_cast<double>(C + Sg - 2 * static_cast<long long>(I)) * f.invT;
             if (f.map) {
                 write_map(u, v, finalize_L(term, f));
             } else {
@@ -494,11 +515,11 @@ __global__ void __launch_bounds__(32 * NW, 16 / NW) sweep_match_kernel(QuantPara
             }
         } else {
             if (u < 0 || e >= W) return;
-            const double* rb = red + (yy & 1) * (NW * kStrip);
+            const double* rb = red + (yy & 1) * (NW * kStrip) + (t / kStrip) * NWB * kStrip + (t % kStrip);
             double term = 0.0;
 #pragma unroll
-            for (int w = 0; w < NW; ++w)
-                if (w < nwarps_live) term = __dadd_rn(term, rb[w * kStrip + t]);
+            for (int w = 0; w < NWB; ++w)
+                if (w < nwarps_live) term = __dadd_rn(term, rb[w * kStrip]);
             if (f.map) {
                 write_map(u, v, finalize_L(term, f));
             } else {
@@ -509,7 +530,7 @@ __global__ void __launch_bounds__(32 * NW, 16 / NW) sweep_match_kernel(QuantPara
     };
     auto combine = [&](int yy) {
 #pragma unroll
-        for (int t = tid; t < kStrip; t += NT) combine_one(yy, t);
+        for (int t = tid; t < kStrip * S; t += NT) combine_one(yy, t);
     };
 
     // row yy's partials are in `red` (and must be combined) iff it is a match row
@@ -517,10 +538,10 @@ __global__ void __launch_bounds__(32 * NW, 16 / NW) sweep_match_kernel(QuantPara
     for (int y = y0; y < y1; ++y) {
         __syncthreads();  // A: previous row's vc / staging reads are done, its partials written
         // row y - 1's partials were written before A; its buffer is rewritten only after
-        // the next B.  Warps 0-3 combine while warps 4-7 start staging.
+        // the next B.  Some warps combine while the others start staging.
         if (pending(y - 1)) combine(y - 1);
         {   // stage row y: vertical running histogram (add row y, remove row y - kh),
-            // the strip's bins and row carries for the sweep, then prefetch row y + 1
+            // the strips' bins and row carries for the sweep, then prefetch row y + 1
             const bool old_row = y - f.kh >= ystart;
 #pragma unroll
             for (int c = 0; c < CPT; ++c) {
@@ -532,15 +553,15 @@ __global__ void __launch_bounds__(32 * NW, 16 / NW) sweep_match_kernel(QuantPara
                 if (xt_live[c]) {
                     const int bn = pn - out.bin0 - g0;
                     if (static_cast<unsigned>(bn) < static_cast<unsigned>(nb_cta))
-                        atomicAdd(&vc[bn * kVcStride + vcol_w[c]], vinc[c]);
+                        atomicAdd(&vc[bn * VS + vcol_w[c]], vinc[c]);
                     const int bo = po - out.bin0 - g0;
                     if (po >= 0 && static_cast<unsigned>(bo) < static_cast<unsigned>(nb_cta))
-                        atomicSub(&vc[bo * kVcStride + vcol_w[c]], vinc[c]);
+                        atomicSub(&vc[bo * VS + vcol_w[c]], vinc[c]);
                 }
                 const int col = tid + c * NT;
-                if (col >= kStrip) rowbins[(y & 1) * kStrip + col - kStrip] = static_cast<uint16_t>(pn);
+                if (col >= kStrip && col < E) rowbins[(y & 1) * kStrip * S + col - kStrip] = static_cast<uint16_t>(pn);
             }
-            if (tid < NB) lrow[(y & 1) * NB + tid] = lpre;
+            if (tid < S * NB) lrow[(y & 1) * S * NB + tid] = lpre;
             if (y + 1 < y1) {
                 if (PREFETCH) {
                     const int yo = y + 1 - f.kh;
@@ -561,7 +582,7 @@ __global__ void __launch_bounds__(32 * NW, 16 / NW) sweep_match_kernel(QuantPara
 
         uint32_t t4[4] = {0, 0, 0, 0};
         if (STORE) {
-            const uint2 rb2 = *reinterpret_cast<const uint2*>(rowbins + (y & 1) * kStrip + 4 * lane);
+            const uint2 rb2 = *reinterpret_cast<const uint2*>(rowbins + (y & 1) * kStrip * S + sc * kStrip + 4 * lane);
             uint32_t bins4 = 0;
             if (pm.byte_mode) {
                 bins4 = __byte_perm(rb2.x, rb2.y, 0x6420);
@@ -575,7 +596,7 @@ __global__ void __launch_bounds__(32 * NW, 16 / NW) sweep_match_kernel(QuantPara
             }
             onehot_shifts(bins4 ^ kpat0, t4);
         }
-        const uint4* lr = reinterpret_cast<const uint4*>(lrow + (y & 1) * NB + warp * kB);
+        const uint4* lr = reinterpret_cast<const uint4*>(lrow + (y & 1) * S * NB + sc * NB + wb * kB);
         uint32_t* prow = STORE ? base_ptr + static_cast<int64_t>(y) * out.row_pitch : nullptr;
 
         uint32_t Iw[8] = {0, 0, 0, 0, 0, 0, 0, 0}, Cw[8] = {0, 0, 0, 0, 0, 0, 0, 0};
@@ -589,9 +610,9 @@ __global__ void __launch_bounds__(32 * NW, 16 / NW) sweep_match_kernel(QuantPara
             if (FAST && match_row) {
                 uint32_t w[8];
                 int off;
-                const int go = 4 * g * kVcStride;
+                const int go = 4 * g * VS;
                 window_counts_q<KWM>(pb + go, vq + go, mq, aw0, apsh, amask, w, off);
-                const int sk = static_cast<int>(srep_s[warp * kB + 4 * g + qq] & 0xFFFFu);
+                const int sk = static_cast<int>(srep_s[wb * kB + 4 * g + qq] & 0xFFFFu);
                 // min(w + off, s_k) = min(w, s_k - off) + off in signed 16-bit halves: the
                 // integer path runs only for kw * kh <= 24576, so -32768 <= s_k - off <= 32767
                 const uint32_t thr = static_cast<uint32_t>((sk - off) & 0xFFFF) * 0x10001u;
@@ -616,7 +637,7 @@ __global__ void __launch_bounds__(32 * NW, 16 / NW) sweep_match_kernel(QuantPara
                     uint32_t aw[4][2], bw[4][2];
 #pragma unroll
                     for (int i = 0; i < 4; ++i)
-                        window_prefix<KWM == 0>(vwarp + (4 * g + i) * kVcStride, gb + i * kVcWords, lane, aw[i][0],
+                        window_prefix<KWM == 0>(vwarp + (4 * g + i) * VS, gb + i * kVcWords, lane, aw[i][0],
                                                 aw[i][1], bw[i][0], bw[i][1]);
                     if (KWM == 0) __syncwarp();
 #pragma unroll
@@ -665,13 +686,23 @@ __global__ void __launch_bounds__(32 * NW, 16 / NW) sweep_match_kernel(QuantPara
                 }
                 quarter_reduce(Iw, qq);
                 const int jb = 4 * (qq >> 1) + 2 * (qq & 1);
-                uint32_t* rw = red32 + (y & 1) * 64 + 8 * mq + jb;
-                atomicAdd(rw, Iw[0]);
-                atomicAdd(rw + 1, Iw[1]);
+                uint32_t* rw = red32 + (y & 1) * 64 * S + sc * 64 + 8 * mq + jb;
+                if (NWB == 1) {  // one warp per strip: the row's sums are final
+                    rw[0] = Iw[0];
+                    rw[1] = Iw[1];
+                } else {
+                    atomicAdd(rw, Iw[0]);
+                    atomicAdd(rw + 1, Iw[1]);
+                }
                 if (!ALLB) {
                     quarter_reduce(Cw, qq);
-                    atomicAdd(rw + 128, Cw[0]);
-                    atomicAdd(rw + 129, Cw[1]);
+                    if (NWB == 1) {
+                        rw[128 * S] = Cw[0];
+                        rw[128 * S + 1] = Cw[1];
+                    } else {
+                        atomicAdd(rw + 128 * S, Cw[0]);
+                        atomicAdd(rw + 128 * S + 1, Cw[1]);
+                    }
                 }
             } else {
                 double* rb = red + (y & 1) * (NW * kStrip) + warp * kStrip;
@@ -686,35 +717,35 @@ __global__ void __launch_bounds__(32 * NW, 16 / NW) sweep_match_kernel(QuantPara
     if (y1 > y0 && pending(y1 - 1)) combine(y1 - 1);
 }
 
-constexpr size_t kSmemBytes = smem_bytes_nw<8>();
+constexpr size_t kSmemBytes = smem_bytes_s<1>();
 
 
-template <int KWM, bool ALLB, int SK, int NW>
+template <int KWM, bool ALLB, int SK, int S>
 void launch_variants(dim3 grid, cudaStream_t s, const QuantParams& q, const PixelMode& pm, const spct_ih& out,
                      const BuildPlan& bp, const FusedCarries& fc, const FusedParams& f) {
-    constexpr int NT = 32 * NW;
-    constexpr size_t SM = smem_bytes_nw<NW>();
-    ensure_smem(sweep_match_kernel<true, true, KWM, ALLB, SK, NW>, SM);
-    ensure_smem(sweep_match_kernel<true, false, KWM, false, SK, NW>, SM);
-    ensure_smem(sweep_match_kernel<false, true, KWM, ALLB, SK, NW>, SM);
-    ensure_smem(sweep_match_kernel<false, false, KWM, false, SK, NW>, SM);
+    constexpr int NT = Geo<S>::NT;
+    constexpr size_t SM = smem_bytes_s<S>();
+    ensure_smem(sweep_match_kernel<true, true, KWM, ALLB, SK, S>, SM);
+    ensure_smem(sweep_match_kernel<true, false, KWM, false, SK, S>, SM);
+    ensure_smem(sweep_match_kernel<false, true, KWM, ALLB, SK, S>, SM);
+    ensure_smem(sweep_match_kernel<false, false, KWM, false, SK, S>, SM);
     // integer (template-crop) variant and FP64 variant: the one not selected by the
     // device-side template prep exits on entry
     if (out.data) {
-        sweep_match_kernel<true, true, KWM, ALLB, SK, NW><<<grid, NT, SM, s>>>(q, pm, out, bp.Lb, bp.Wp, bp.band_rows, fc, f);
-        sweep_match_kernel<true, false, KWM, false, SK, NW><<<grid, NT, SM, s>>>(q, pm, out, bp.Lb, bp.Wp, bp.band_rows, fc, f);
+        sweep_match_kernel<true, true, KWM, ALLB, SK, S><<<grid, NT, SM, s>>>(q, pm, out, bp.Lb, bp.Wp, bp.band_rows, bp.nstrips, fc, f);
+        sweep_match_kernel<true, false, KWM, false, SK, S><<<grid, NT, SM, s>>>(q, pm, out, bp.Lb, bp.Wp, bp.band_rows, bp.nstrips, fc, f);
     } else {
-        sweep_match_kernel<false, true, KWM, ALLB, SK, NW><<<grid, NT, SM, s>>>(q, pm, out, bp.Lb, bp.Wp, bp.band_rows, FusedCarries{}, f);
-        sweep_match_kernel<false, false, KWM, false, SK, NW><<<grid, NT, SM, s>>>(q, pm, out, bp.Lb, bp.Wp, bp.band_rows, FusedCarries{}, f);
+        sweep_match_kernel<false, true, KWM, ALLB, SK, S><<<grid, NT, SM, s>>>(q, pm, out, bp.Lb, bp.Wp, bp.band_rows, bp.nstrips, fc, f);
+        sweep_match_kernel<false, false, KWM, false, SK, S><<<grid, NT, SM, s>>>(q, pm, out, bp.Lb, bp.Wp, bp.band_rows, bp.nstrips, fc, f);
     }
 }
 
-template <int KWM, int NW>
+template <int KWM, int S>
 void launch_kw_impl(bool allb, int sk, dim3 grid, cudaStream_t s, const QuantParams& q, const PixelMode& pm,
                     const spct_ih& out, const BuildPlan& bp, const FusedCarries& fc, const FusedParams& f) {
 #define SPCT_SK(SKV)                                                                      \
-    if (allb) launch_variants<KWM, true, SKV, NW>(grid, s, q, pm, out, bp, fc, f);          \
-    else launch_variants<KWM, false, SKV, NW>(grid, s, q, pm, out, bp, fc, f);
+    if (allb) launch_variants<KWM, true, SKV, S>(grid, s, q, pm, out, bp, fc, f);           \
+    else launch_variants<KWM, false, SKV, S>(grid, s, q, pm, out, bp, fc, f);
     if (sk == 1) {
         SPCT_SK(1)
     } else if (sk == 2) {
@@ -728,22 +759,26 @@ void launch_kw_impl(bool allb, int sk, dim3 grid, cudaStream_t s, const QuantPar
 }  // namespace spct_fused
 
 namespace spct_fused {
-// One translation unit per (window-width specialisation, warps per CTA), so the kernel
-// variants compile in parallel: fused_kw{64,128,0}_nw{2,4,8}.cu.
+// One translation unit per (window-width specialisation, strips per CTA), so the kernel
+// variants compile in parallel: fused_kw{64,128,0}_s{1,2,4,8}.cu.
 #define SPCT_FUSED_LAUNCHER(NAME)                                                                              \
     void NAME(bool allb, int sk, dim3 grid, cudaStream_t s, const QuantParams& q, const PixelMode& pm,        \
               const spct_ih& out, const BuildPlan& bp, const FusedCarries& fc, const FusedParams& f);
-SPCT_FUSED_LAUNCHER(launch_kw64_nw8)
-SPCT_FUSED_LAUNCHER(launch_kw64_nw4)
-SPCT_FUSED_LAUNCHER(launch_kw64_nw2)
-SPCT_FUSED_LAUNCHER(launch_kw128_nw8)
-SPCT_FUSED_LAUNCHER(launch_kw128_nw4)
-SPCT_FUSED_LAUNCHER(launch_kw128_nw2)
-SPCT_FUSED_LAUNCHER(launch_kw_any_nw8)
-SPCT_FUSED_LAUNCHER(launch_kw_any_nw4)
-SPCT_FUSED_LAUNCHER(launch_kw_any_nw2)
+SPCT_FUSED_LAUNCHER(launch_kw64_s1)
+SPCT_FUSED_LAUNCHER(launch_kw64_s2)
+SPCT_FUSED_LAUNCHER(launch_kw64_s4)
+SPCT_FUSED_LAUNCHER(launch_kw64_s8)
+SPCT_FUSED_LAUNCHER(launch_kw128_s1)
+SPCT_FUSED_LAUNCHER(launch_kw128_s2)
+SPCT_FUSED_LAUNCHER(launch_kw128_s4)
+SPCT_FUSED_LAUNCHER(launch_kw128_s8)
+SPCT_FUSED_LAUNCHER(launch_kw_any_s1)
+SPCT_FUSED_LAUNCHER(launch_kw_any_s2)
+SPCT_FUSED_LAUNCHER(launch_kw_any_s4)
+SPCT_FUSED_LAUNCHER(launch_kw_any_s8)
 #undef SPCT_FUSED_LAUNCHER
 size_t smem_bytes();
-// Warps per CTA of the fused sweep for a slab of `bins` bins (2, 4 or 8).
-inline int fused_nw(int bins) { return bins > 64 ? 8 : (bins > 32 ? 4 : 2); }
+// Strips per CTA of the fused sweep for a slab of `bins` bins (1, 2, 4 or 8): every CTA has
+// 8 warps of 16 bins.
+inline int fused_strips(int bins) { return bins > 64 ? 1 : (bins > 32 ? 2 : (bins > 16 ? 4 : 8)); }
 }  // namespace spct_fused

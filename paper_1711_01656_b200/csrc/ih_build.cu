@@ -39,8 +39,10 @@ int device_sms() {
     });
 }
 
-BuildPlan plan_build(int width, int height, int bins, int force_B, int ctas_per_sm, int min_band_rows) {
+BuildPlan plan_build(int width, int height, int bins, int force_B, int ctas_per_sm, int min_band_rows,
+                     int strips_per_cta) {
     BuildPlan p{};
+    p.strips_per_cta = std::max(1, strips_per_cta);
     p.B = force_B ? force_B : (bins <= 4 ? 4 : (bins <= 8 ? 8 : 16));
     const int nslabs = static_cast<int>(ceil_div(bins, p.B));
     p.warps = std::min(8, nslabs);
@@ -56,7 +58,7 @@ BuildPlan plan_build(int width, int height, int bins, int force_B, int ctas_per_
         // partial last wave runs at partial occupancy for a full tile time.  Bands are
         // kept >= min_band_rows (carry tables and the matcher's pre-roll scale with
         // 1 / band_rows).
-        const int64_t per_band = static_cast<int64_t>(p.nstrips) * p.slab_groups;
+        const int64_t per_band = ceil_div(p.nstrips, p.strips_per_cta) * p.slab_groups;
         const int64_t slots = static_cast<int64_t>(device_sms()) * std::max(1, ctas_per_sm);
         const int64_t nb_max = std::max<int64_t>(1, height / std::max(1, min_band_rows));
         int64_t best_nb = 1;
@@ -279,11 +281,12 @@ BuildPlan plan_build_sweep(int width, int height, int bins) {
 }
 
 BuildPlan plan_fused_sweep(int width, int height, int bins) {
-    // warps per CTA as in spct_fused::fused_nw (fused_kernel.cuh)
-    // The band floor trades the kh - 1 pre-roll rows of every band against filling the
-    // GPU: narrow CTAs (small histograms) need more bands to reach full occupancy.
-    const int nw = bins > 64 ? 8 : (bins > 32 ? 4 : 2);
-    return plan_build(width, height, bins, 16, fused_ctas_per_sm(nw), 8 * nw);
+    // strips per CTA as in spct_fused::fused_strips (fused_kernel.cuh): 8 warps of 16 bins
+    // each, S = 128 / (16 * ceil(bins / 16)) strips side by side for narrow histograms.
+    // The band floor trades the band-start window state (kh - 1 pre-roll rows, or the
+    // carry tables for narrow CTAs) against filling the GPU.
+    const int S = bins > 64 ? 1 : (bins > 32 ? 2 : (bins > 16 ? 4 : 8));
+    return plan_build(width, height, bins, 16, fused_ctas_per_sm(S), S == 1 ? 64 : 16, S);
 }
 
 }  // namespace spct_impl

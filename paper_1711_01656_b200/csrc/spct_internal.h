@@ -81,13 +81,15 @@ struct BuildPlan {
     int band_rows;  // rows per band
     int nbands;
     int slab_groups;  // CTAs along the bin axis
+    int strips_per_cta;  // fused sweep: strips side by side in one CTA (grid.x = ceil(nstrips / strips_per_cta))
 };
-BuildPlan plan_build(int width, int height, int bins, int force_B = 0, int ctas_per_sm = 2, int min_band_rows = 32);
+BuildPlan plan_build(int width, int height, int bins, int force_B = 0, int ctas_per_sm = 2, int min_band_rows = 32,
+                     int strips_per_cta = 1);
 
 // Resident CTAs per SM of the build sweep (B bins per warp, `threads` per CTA) and of the
 // fused sweep; used to size bands in whole waves.  Fall back to 2 without a device.
 int build_ctas_per_sm(int B, int threads);
-int fused_ctas_per_sm(int nw = 8);
+int fused_ctas_per_sm(int strips = 1);
 int device_sms();
 // The two plans every caller (workspace query included) must agree on.
 BuildPlan plan_build_sweep(int width, int height, int bins);

@@ -134,11 +134,13 @@ __global__ void __launch_bounds__(512, 1) ih_bins_kernel(spct_ih t, int band_row
     }
 
     const uint32_t kbase = static_cast<uint32_t>(warp * kBinsPerWarp);  // bin relative to the group
+#pragma unroll 2
     for (int y = y0; y < y1; ++y) {
         const int st = (y - y0) % kStages;
         if (nk) mbar_wait(&bars[st * kWarps + warp], static_cast<uint32_t>(((y - y0) / kStages) & 1));
         const uint32_t* rows = ring + (static_cast<int64_t>(st) * kWarps + warp) * kBinsPerWarp * kRowWords;
-        uint32_t msum[4] = {0, 0, 0, 0}, nsum[4] = {0, 0, 0, 0}, bad = 0, mL = 0, nL = 0;
+        // pbits: OR of every checked p_k; all in {0, 1} <=> (pbits & ~1) == 0
+        uint32_t msum[4] = {0, 0, 0, 0}, nsum[4] = {0, 0, 0, 0}, pbits = 0, mL = 0, nL = 0;
 #pragma unroll
         for (int k = 0; k < kBinsPerWarp; ++k) {
             if (k >= nk) break;
@@ -156,19 +158,21 @@ __global__ void __launch_bounds__(512, 1) ih_bins_kernel(spct_ih t, int band_row
             uint32_t left = __shfl_up_sync(0xffffffffu, dv[3], 1);
             if (lane == 0) left = dl;
             const uint32_t kk = kbase + static_cast<uint32_t>(k);
+            uint32_t p[4];  // the pixels' counts of bin kk
 #pragma unroll
             for (int j = 0; j < 4; ++j) {
-                const uint32_t p = dv[j] - (j ? dv[j - 1] : left);  // the pixel's count of bin kk
-                if (j < ncols) bad |= p & ~1u;
+                p[j] = dv[j] - (j ? dv[j - 1] : left);
+                if (j >= ncols) p[j] = 0;
                 msum[j] += kk * dv[j];
                 nsum[j] += dv[j];
             }
+            pbits |= (p[0] | p[1]) | (p[2] | p[3]);
             mL += kk * left;
             nL += left;
         }
         __syncwarp();
         issue(y + kStages);  // this stage is consumed: refill it with row y + 3
-        if (__any_sync(0xffffffffu, bad != 0) && lane == 0) atomicOr(flag, 1u);
+        if (__any_sync(0xffffffffu, (pbits & ~1u) != 0) && lane == 0) atomicOr(flag, 1u);
         // with every p_k in {0, 1} the warp's bin partial is < 8 * 128 and its count <= 8
         const uint32_t mprev[4] = {mL, msum[0], msum[1], msum[2]}, nprev[4] = {nL, nsum[0], nsum[1], nsum[2]};
         uint4 w;
