@@ -18,8 +18,8 @@ OBJDIR     = build/obj
 CU_OBJS    = $(patsubst $(CSRC)/%.cu,$(OBJDIR)/%.o,$(CU_SRCS))
 HOST_OBJS  = $(patsubst $(CSRC)/host/%.cpp,$(OBJDIR)/host_%.o,$(HOST_SRCS))
 
-.PHONY: all lib oracle clean sass dropin dropin_bench
-all: lib oracle dropin
+.PHONY: all lib oracle clean sass dropin dropin_bench acceptance
+all: lib oracle dropin acceptance
 
 lib: $(LIB)
 
@@ -58,3 +58,11 @@ dropin_bench: $(DROPIN_BENCH)
 $(DROPIN_BENCH): tests/cpp/dropin_bench.cpp $(LIB) $(wildcard include/spct/*.hpp)
 	@mkdir -p build
 	$(CXX) -O2 -std=c++20 -Iinclude -o $@ tests/cpp/dropin_bench.cpp -L$(PKG) -lspct_b200 -Wl,-rpath,'$$ORIGIN/../$(PKG)'
+
+# the reference's acceptance criteria 1-2 (proj/tests/acceptance.cpp:64-137) at full count,
+# against the drop-in API (run on a GPU box by tests/test_dropin_cpp.py)
+ACCEPT = build/acceptance_test
+acceptance: $(ACCEPT)
+$(ACCEPT): tests/cpp/acceptance_test.cpp $(LIB) $(wildcard include/spct/*.hpp)
+	@mkdir -p build
+	$(CXX) -O2 -std=c++20 -Iinclude -o $@ tests/cpp/acceptance_test.cpp -L$(PKG) -lspct_b200 -Wl,-rpath,'$$ORIGIN/../$(PKG)'
