@@ -64,16 +64,17 @@ spct_status build_match(const spct_source* src, const spct_ih* out, const double
     const int64_t T = static_cast<int64_t>(kw) * kh;
     const bool fusable = spct_cu_fused_window_ok(kw, kh) != 0;
     const int ngroups = static_cast<int>(ceil_div(out->bins, kGroupBins));
+    double* group_part = nullptr;  // > 128 bins with a finished map: the earlier groups' partial sums
     if (fusable && map && ngroups > 1) {
-        // more than one 128-bin group: accumulate the groups' partials, then finalise
-        double* part = nullptr;
         const size_t n = static_cast<size_t>(out->width - kw + 1) * (out->height - kh + 1);
-        if (auto st = cuda_status(malloc_async(&part, n * sizeof(double), s), "ih_build_match_map alloc")) return st;
-        spct_status st = build_match(src, out, tmpl, kw, kh, p, metric, part, nullptr, workspace, workspace_bytes, stream);
-        if (st == SPCT_OK) st = spct_cu_hist_finalize(part, out->width, out->height, kw, kh, p, metric, map, stream);
-        cudaFreeAsync(part, s);
-        return st;
+        if (auto st = cuda_status(malloc_async(&group_part, n * sizeof(double), s), "ih_build_match_map alloc"))
+            return st;
     }
+    struct FreeAsync {
+        double* p;
+        cudaStream_t s;
+        ~FreeAsync() { if (p) cudaFreeAsync(p, s); }
+    } free_part{group_part, s};
     if (!fusable) {
         // two passes: window too large for the 16-bit running-histogram cells, or a
         // finished map over more than one 128-bin group
@@ -131,14 +132,17 @@ spct_status build_match(const spct_source* src, const spct_ih* out, const double
     f.tmpl = tmpl;
     f.prep = prep;
     f.S_group = Sg;
-    f.partial = partial;
-    f.map = map;
+    f.partial = group_part ? group_part : partial;
+    f.map = group_part ? nullptr : map;
     f.W = out->width;
     f.H = out->height;
     const PixelMode pm = make_pixel_mode(q, out->bin0);
     for (int g = 0; g < ngroups; ++g) {
         f.group0 = g * kGroupBins;
         f.accumulate = g > 0;
+        // several groups into a finished map: groups accumulate into group_part, the last
+        // one adds its sums to it and writes the finished map (no finalise pass)
+        if (group_part && g == ngroups - 1) f.map = map;
         dim3 grid(static_cast<unsigned>(ceil_div(bp.nstrips, S)), bp.nbands, 1);
         const int prof = prof_begin(out->data ? "ih_sweep_match" : "sweep_match_nostore", s);
         // the group is the whole histogram: window totals over its bins are kw * kh

@@ -312,6 +312,8 @@ __global__ void __launch_bounds__(256, 2) sweep_match_kernel(QuantParams q, Pixe
     uint32_t* lrow = srep_s + NB;                                           // [2 rows][S strips][NB] row carries
     uint16_t* rowbins = reinterpret_cast<uint16_t*>(lrow + 2 * S * NB);     // [2 rows][S * 128] strip bins
     uint32_t* amask = reinterpret_cast<uint32_t*>(rowbins + 2 * kStrip * S);  // [8 lanes][8 words] anchor masks
+    // integer path: [2 rows][128] earlier groups' sums (the FP64 path's part of `red`)
+    double* accb = red + 2 * kStrip;
     // integer path: per row parity, strip and window pair, the packed sums over the warps
     // (shared atomics), I at [parity][strip][64] and C at 128 S + [parity][strip][64]
     uint32_t* red32 = reinterpret_cast<uint32_t*>(red);
@@ -466,6 +468,9 @@ __global__ void __launch_bounds__(256, 2) sweep_match_kernel(QuantParams q, Pixe
             }
     }
 
+    // row yy's partials are in `red` (and must be combined) iff it is a match row
+    auto pending_row = [&](int yy) { return yy >= y0 && yy >= f.kh - 1; };
+    auto pending = pending_row;
     // Cross-warp combine of row yy: thread t < 128 S finishes the window ending at CTA
     // column t.  Integer path with a finished map (ALLB): L = alpha + beta I (one FMA).
     const bool intersect = f.metric == SPCT_METRIC_INTERSECTION;
@@ -482,6 +487,30 @@ __global__ void __launch_bounds__(256, 2) sweep_match_kernel(QuantParams q, Pixe
         const int ya = v == 0 ? 0 : yc, yb = v == f.nv - 1 ? f.H - 1 : yc;
         for (int yy = ya; yy <= yb; ++yy)
             for (int xx = xa; xx <= xb; ++xx) f.map[static_cast<int64_t>(yy) * f.W + xx] = L;
+    };
+    // accumulate (bin groups after the first): the earlier groups' partial sum of the
+    // window combined next, loaded one row ahead so the combine never waits on DRAM
+    // (S == 1, the only geometry with several groups: thread t < 128 owns window t)
+    // (cp.async into a per-thread shared slot: no register is held across the row)
+    auto load_acc = [&](int yy) {
+        if (FAST && S == 1 && f.accumulate && tid < kStrip && pending_row(yy)) {
+            const int e = xc + tid, u = e - f.kw + 1;
+            if (u >= 0 && e < W) {
+                const double* src = f.partial + static_cast<int64_t>(yy - f.kh + 1) * f.nu + u;
+                asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n\tcp.async.commit_group;" ::"r"(
+                                 static_cast<uint32_t>(__cvta_generic_to_shared(accb + (yy & 1) * kStrip + tid))),
+                             "l"(src)
+                             : "memory");
+            }
+        }
+    };
+    auto add_acc = [&](int yy, int u, int v, double term) {
+        if (!f.accumulate) return term;
+        if (FAST && S == 1) {
+            asm volatile("cp.async.wait_all;" ::: "memory");
+            return __dadd_rn(accb[(yy & 1) * kStrip + tid], term);
+        }
+        return __dadd_rn(f.partial[static_cast<int64_t>(v) * f.nu + u], term);
     };
     auto combine_one = [&](int yy, int t) {
         const int e = xc + t;
@@ -505,14 +534,10 @@ __global__ void __launch_bounds__(256, 2) sweep_match_kernel(QuantParams q, Pixe
                 return;
             }
             const long long C = ALLB ? static_cast<long long>(f.kw) * f.kh : (xcn >> (16 * (t & 1))) & 0xFFFFu;
-            const double term = intersect ? static_cast<double>(I) * f.invT
-                                          : static_cast<double>(C + Sg - 2 * static_cast<long long>(I)) * f.invT;
-            if (f.map) {
-                write_map(u, v, finalize_L(term, f));
-            } else {
-                double* dst = f.partial + static_cast<int64_t>(v) * f.nu + u;
-                *dst = f.accumulate ? __dadd_rn(*dst, term) : term;
-            }
+            const double term = add_acc(yy, u, v, intersect ? static_cast<double>(I) * f.invT
+                                                        : static_cast<double>(C + Sg - 2 * static_cast<long long>(I)) * f.invT);
+            if (f.map) write_map(u, v, finalize_L(term, f));  // the last group finishes the map
+            else f.partial[static_cast<int64_t>(v) * f.nu + u] = term;
         } else {
             if (u < 0 || e >= W) return;
             const double* rb = red + (yy & 1) * (NW * kStrip) + (t / kStrip) * NWB * kStrip + (t % kStrip);
@@ -520,12 +545,9 @@ __global__ void __launch_bounds__(256, 2) sweep_match_kernel(QuantParams q, Pixe
 #pragma unroll
             for (int w = 0; w < NWB; ++w)
                 if (w < nwarps_live) term = __dadd_rn(term, rb[w * kStrip]);
-            if (f.map) {
-                write_map(u, v, finalize_L(term, f));
-            } else {
-                double* dst = f.partial + static_cast<int64_t>(v) * f.nu + u;
-                *dst = f.accumulate ? __dadd_rn(*dst, term) : term;
-            }
+            term = add_acc(yy, u, v, term);
+            if (f.map) write_map(u, v, finalize_L(term, f));
+            else f.partial[static_cast<int64_t>(v) * f.nu + u] = term;
         }
     };
     auto combine = [&](int yy) {
@@ -533,13 +555,13 @@ __global__ void __launch_bounds__(256, 2) sweep_match_kernel(QuantParams q, Pixe
         for (int t = tid; t < kStrip * S; t += NT) combine_one(yy, t);
     };
 
-    // row yy's partials are in `red` (and must be combined) iff it is a match row
-    auto pending = [&](int yy) { return yy >= y0 && yy >= f.kh - 1; };
+
     for (int y = y0; y < y1; ++y) {
         __syncthreads();  // A: previous row's vc / staging reads are done, its partials written
         // row y - 1's partials were written before A; its buffer is rewritten only after
         // the next B.  Some warps combine while the others start staging.
         if (pending(y - 1)) combine(y - 1);
+        load_acc(y);
         {   // stage row y: vertical running histogram (add row y, remove row y - kh),
             // the strips' bins and row carries for the sweep, then prefetch row y + 1
             const bool old_row = y - f.kh >= ystart;
