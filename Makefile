@@ -19,7 +19,7 @@ CU_OBJS    = $(patsubst $(CSRC)/%.cu,$(OBJDIR)/%.o,$(CU_SRCS))
 HOST_OBJS  = $(patsubst $(CSRC)/host/%.cpp,$(OBJDIR)/host_%.o,$(HOST_SRCS))
 
 .PHONY: all lib oracle clean sass dropin dropin_bench acceptance
-all: lib oracle dropin acceptance
+all: lib oracle dropin dropin_bench acceptance
 
 lib: $(LIB)
 

@@ -7,28 +7,54 @@ using namespace spct_impl;
 
 namespace spct_fused {
 
-// Template prep: s_k = T t_k; fast path iff every s_k of the slab is an integer up to
-// FP noise (then the integer formula is exact to ~1e-15) and the metric allows it.
+// Template prep: s_k = T t_k.  Kind 1 (the exact integer path) iff every s_k of the slab
+// is an integer up to FP noise (then the integer formula is exact to ~1e-15) and the metric
+// allows it; otherwise kind 2 (integer path on floor(s_k) plus the fractional parts) when
+// the host allows it (`frac_ok`: p = 1 / intersection, kw kh <= 4096), else kind 0 (FP64).
+// Layout (fused_prep_layout): [0] kind, [1 + k] floor(s_k) replicated in both u16 halves;
+// per 128-bin group sum floor(s_k) (int64) and sum r_k (double); r_k per bin (double).
 __global__ void prep_kernel(const double* __restrict__ tmpl, int bin0, int bins, double T, int fast_metric,
-                            uint32_t* __restrict__ prep, long long* __restrict__ S_group, int ngroups) {
-    __shared__ int ok;
-    if (threadIdx.x == 0) ok = fast_metric;
+                            int frac_ok, uint32_t* __restrict__ prep, long long* __restrict__ S_group,
+                            double* __restrict__ Sr_group, double* __restrict__ rfrac, int ngroups) {
+    __shared__ int all_integral;
+    if (threadIdx.x == 0) all_integral = 1;
     __syncthreads();
     for (int k = threadIdx.x; k < bins; k += blockDim.x) {
         const double s = T * tmpl[bin0 + k];
         const double n = rint(s);
         const bool integral = fabs(s - n) <= 8.0 * 2.220446049250313e-16 * fmax(1.0, fabs(s)) && n >= 0.0 && n <= T;
-        if (!integral) ok = 0;
-        const uint32_t ni = integral ? static_cast<uint32_t>(n) : 0u;
+        if (!integral) all_integral = 0;
+        // s_k >= 0 (template contract); floor clamped to [0, T] (c_k <= T, so min(c, s) = c above)
+        const double fl = integral ? n : fmin(fmax(floor(s), 0.0), T);
+        const uint32_t ni = static_cast<uint32_t>(fl);
         prep[1 + k] = ni | (ni << 16);
+        rfrac[k] = integral ? 0.0 : fmax(s - fl, 0.0);
     }
     __syncthreads();
-    if (threadIdx.x == 0) prep[0] = ok;
+    if (threadIdx.x == 0) prep[0] = fast_metric ? (all_integral ? 1u : (frac_ok ? 2u : 0u)) : 0u;
     for (int g = threadIdx.x; g < ngroups; g += blockDim.x) {
         long long acc = 0;
-        for (int k = g * kGroupBins; k < min(bins, (g + 1) * kGroupBins); ++k) acc += prep[1 + k] & 0xFFFFu;
+        double racc = 0.0;
+        for (int k = g * kGroupBins; k < min(bins, (g + 1) * kGroupBins); ++k) {
+            acc += prep[1 + k] & 0xFFFFu;
+            racc += rfrac[k];
+        }
         S_group[g] = acc;
+        Sr_group[g] = racc;
     }
+}
+
+struct PrepLayout {
+    size_t S, Sr, r, total;
+};
+inline PrepLayout fused_prep_layout(int bins) {
+    const size_t ng = (static_cast<size_t>(bins) + kGroupBins - 1) / kGroupBins;
+    PrepLayout l;
+    l.S = round_up((static_cast<int64_t>(bins) + 1) * 4, 256);
+    l.Sr = l.S + round_up(static_cast<int64_t>(ng) * 8, 256);
+    l.r = l.Sr + round_up(static_cast<int64_t>(ng) * 8, 256);
+    l.total = l.r + round_up(static_cast<int64_t>(bins) * 8, 256);
+    return l;
 }
 
 }  // namespace spct_fused
@@ -36,7 +62,7 @@ __global__ void prep_kernel(const double* __restrict__ tmpl, int bin0, int bins,
 using namespace spct_fused;
 
 namespace spct_impl {
-size_t fused_prep_bytes(int bins) { return (static_cast<size_t>(bins) + 1) * 4 + 256 + ((bins + 127) / 128 + 1) * 8; }
+size_t fused_prep_bytes(int bins) { return fused_prep_layout(bins).total; }
 }  // namespace spct_impl
 
 namespace spct_fused {
@@ -101,12 +127,18 @@ spct_status build_match(const spct_source* src, const spct_ih* out, const double
         if (auto st = build_fused_carries(q, *out, bp, workspace, workspace_bytes, s, &fc, win_kh)) return st;
         ws += carry_bytes;
     }
+    const PrepLayout pl = fused_prep_layout(out->bins);
     uint32_t* prep = reinterpret_cast<uint32_t*>(ws);
-    long long* Sg = reinterpret_cast<long long*>(ws + round_up((static_cast<int64_t>(out->bins) + 1) * 4, 256));
-    // the integer path's signed 16-bit min needs kw * kh <= 24576 (fused_kernel.cuh)
+    long long* Sg = reinterpret_cast<long long*>(ws + pl.S);
+    double* Sr = reinterpret_cast<double*>(ws + pl.Sr);
+    double* rfrac = reinterpret_cast<double*>(ws + pl.r);
+    // integer paths: packed 16-bit window counts (kw * kh <= 24576, fused_kernel.cuh); the
+    // fractional flags need every count <= 4096
     const int fast_metric = ((metric == SPCT_METRIC_MINKOWSKI && p == 1.0) || metric == SPCT_METRIC_INTERSECTION) &&
                             T <= 24576;
-    prep_kernel<<<1, 256, 0, s>>>(tmpl, out->bin0, out->bins, static_cast<double>(T), fast_metric, prep, Sg, ngroups);
+    const int frac_ok = fast_metric && T <= 4096;
+    prep_kernel<<<1, 256, 0, s>>>(tmpl, out->bin0, out->bins, static_cast<double>(T), fast_metric, frac_ok, prep, Sg,
+                                  Sr, rfrac, ngroups);
     if (auto st = launch_status("prep_kernel")) return st;
 
     FusedParams f{};
@@ -132,6 +164,9 @@ spct_status build_match(const spct_source* src, const spct_ih* out, const double
     f.tmpl = tmpl;
     f.prep = prep;
     f.S_group = Sg;
+    f.Sr_group = Sr;
+    f.rfrac = rfrac;
+    f.frac = frac_ok;
     f.partial = group_part ? group_part : partial;
     f.map = group_part ? nullptr : map;
     f.W = out->width;

@@ -48,12 +48,15 @@ struct FusedParams {
     double p, T, invT;
     int group0;                  // first slab-local bin of this launch's bin group
     const double* tmpl;          // full template, indexed by global bin
-    const uint32_t* prep;        // [0] fast flag, [1..] srep (slab-local), then S per group (int64)
-    const long long* S_group;    // sum of integral s_k per 128-bin group
+    const uint32_t* prep;        // [0] path kind (0 FP64, 1 integral template, 2 fractional), [1..] srep (slab-local)
+    const long long* S_group;    // sum of floor(s_k) per 128-bin group
+    const double* Sr_group;      // sum of the fractional parts r_k = s_k - floor(s_k) per 128-bin group
+    const double* rfrac;         // r_k per slab-local bin (kind 2)
     double* partial;
     double* map;                 // non-null: write the finished likelihood map (one group = every bin)
     double inv_p, dmax, inv_dmax;  // inv_dmax != 0 iff dmax is a power of two (exact product)
     int W, H;
+    int frac;     // host: the fractional variant is launched instead of the FP64 one
     int fp_kind;  // FP64 path term: 0 Minkowski p=1, 1 p=2, 2 general p, 3 intersection, 4 Bhattacharyya, 5 chi-square
 };
 
@@ -298,12 +301,16 @@ constexpr size_t smem_bytes_s() {
            size_t(2) * G::NW * kStrip * 8 + size_t(2) * kStrip * S * 2;
 }
 
-template <bool STORE, bool FAST, int KWM, bool ALLB, int SK, int S>
+// MODE: 0 = the FP64 per-bin path (any metric), 1 = the exact integer path (integral
+// template, p = 1 / intersection), 2 = the integer path on floor(s_k) plus the fractional
+// correction sum_{k: c_k > floor(s_k)} r_k (any template, p = 1 / intersection, kw kh <= 4096).
+template <bool STORE, int MODE, int KWM, bool ALLB, int SK, int S>
 __global__ void __launch_bounds__(256, 2) sweep_match_kernel(QuantParams q, PixelMode pm, spct_ih out, int Lb, int Wp,
                                                              int band_rows, int nstrips, FusedCarries fc,
                                                              FusedParams f) {
     using G = Geo<S>;
     constexpr int NW = G::NW, NWB = G::NWB, NB = G::NB, NT = G::NT, E = G::E, VS = G::VS, CPT = G::CPT;
+    constexpr bool FAST = MODE != 0, FRAC = MODE == 2;
     extern __shared__ uint4 smem_raw[];
     uint32_t* vc = reinterpret_cast<uint32_t*>(smem_raw);                 // [NB bins][VS words], padded
     uint32_t* gbuf = vc + NB * VS;                                          // [NW warps][4][128 words] (general kw)
@@ -317,9 +324,14 @@ __global__ void __launch_bounds__(256, 2) sweep_match_kernel(QuantParams q, Pixe
     // integer path: per row parity, strip and window pair, the packed sums over the warps
     // (shared atomics), I at [parity][strip][64] and C at 128 S + [parity][strip][64]
     uint32_t* red32 = reinterpret_cast<uint32_t*>(red);
+    // fractional path: per warp and row parity the FP32 correction of its 128 windows
+    // [2][NW][128] (after the integer path's 8 KB of `red`), and per bin slab two 256-entry
+    // tables of fractional sums over 8 bins (in gbuf, unused by the integer paths)
+    float* fr = reinterpret_cast<float*>(red) + 2048;
+    float* ftab = reinterpret_cast<float*>(gbuf);
 
-    // Both variants are launched; the one that does not match the template prep exits.
-    if ((__ldg(f.prep) != 0) != FAST) return;
+    // Two variants are launched; the one that does not match the template prep exits.
+    if (__ldg(f.prep) != static_cast<uint32_t>(MODE)) return;
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int sc = warp / NWB, wb = warp % NWB;            // the warp's strip in the CTA, bin slab
@@ -360,6 +372,22 @@ __global__ void __launch_bounds__(256, 2) sweep_match_kernel(QuantParams q, Pixe
             const int n = f.kw - 16 * (i >> 3) - 2 * (i & 7);
             amask[i] = n >= 2 ? 0xFFFFFFFFu : (n == 1 ? 0xFFFFu : 0u);
         }
+    if (FRAC)
+        // table h of slab wbi, index i: sum of r_k over the slab's bins 4 g + qa (bit 4 + g of
+        // i) and 4 g + qb (bit g), {qa, qb} = {0, 2} (h = 0) or {1, 3} (h = 1): the flag
+        // layout after the cross-quarter combine below.  FP64 sums, fixed order.
+        for (int i = tid; i < NWB * 512; i += NT) {
+            const int wbi = i >> 9, h = (i >> 8) & 1, idx = i & 255;
+            const int kb = g0 + wbi * kB, klim = g0 + nb_cta;
+            double acc = 0.0;
+#pragma unroll
+            for (int g = 0; g < 4; ++g) {
+                const int ka = kb + 4 * g + h, kc = kb + 4 * g + 2 + h;
+                if (((idx >> (4 + g)) & 1) && ka < klim) acc += __ldg(f.rfrac + ka);
+                if (((idx >> g) & 1) && kc < klim) acc += __ldg(f.rfrac + kc);
+            }
+            ftab[i] = static_cast<float>(acc);
+        }
 
     uint32_t V[4][kB];
     if (STORE && warp_live)
@@ -368,6 +396,7 @@ __global__ void __launch_bounds__(256, 2) sweep_match_kernel(QuantParams q, Pixe
     const bool lane_live = xl < out.row_pitch;
     const uint32_t store_mask = (lane_live && warp_live) ? (k_live >= 32 ? 0xFFFFFFFFu : (1u << max(k_live, 0)) - 1u) : 0u;
     const long long Sg = FAST ? f.S_group[g0 / kGroupBins] : 0;
+    const double Sd = static_cast<double>(Sg) + (FRAC ? f.Sr_group[g0 / kGroupBins] : 0.0);  // sum of s_k
     // the warp's view of vc: ext columns [128 sc, 128 sc + 256) = padded words from 72 sc
     const uint32_t* vwarp = vc + wb * kB * VS + G::WOFF * sc;
     // general path: G(e - kw) as a word and a bit shift
@@ -475,7 +504,7 @@ __global__ void __launch_bounds__(256, 2) sweep_match_kernel(QuantParams q, Pixe
     // column t.  Integer path with a finished map (ALLB): L = alpha + beta I (one FMA).
     const bool intersect = f.metric == SPCT_METRIC_INTERSECTION;
     const double lin_b = f.invT;
-    const double lin_a = intersect ? 0.0 : 1.0 - static_cast<double>(static_cast<long long>(f.kw) * f.kh + Sg) * f.invT * 0.5;
+    const double lin_a = intersect ? 0.0 : 1.0 - (static_cast<double>(static_cast<long long>(f.kw) * f.kh) + Sd) * f.invT * 0.5;
     auto write_map = [&](int u, int v, double L) {
         // spread_valid's border replication (likelihood.cpp:44-58)
         const int x = u + (f.kw - 1) / 2, yc = v + (f.kh - 1) / 2;
@@ -528,14 +557,26 @@ __global__ void __launch_bounds__(256, 2) sweep_match_kernel(QuantParams q, Pixe
             }
             if (u < 0 || e >= W) return;
             const uint32_t I = (xi >> (16 * (t & 1))) & 0xFFFFu;
+            // sum_k min(c_k, s_k): exact integers, plus the fractional correction (FP32 per
+            // warp, FP64 over the warps in a fixed order)
+            double Id = static_cast<double>(I);
+            if (FRAC) {
+                const float* fb = fr + ((yy & 1) * NW + (t / kStrip) * NWB) * kStrip + (t % kStrip);
+                double corr = 0.0;
+#pragma unroll
+                for (int w = 0; w < NWB; ++w)
+                    if (w < nwarps_live) corr += static_cast<double>(fb[w * kStrip]);
+                Id += corr;
+            }
             if (ALLB && f.map) {
-                const double L = fma(lin_b, static_cast<double>(I), lin_a);
+                const double L = fma(lin_b, Id, lin_a);
                 write_map(u, v, fmin(fmax(L, 0.0), 1.0));
                 return;
             }
             const long long C = ALLB ? static_cast<long long>(f.kw) * f.kh : (xcn >> (16 * (t & 1))) & 0xFFFFu;
-            const double term = add_acc(yy, u, v, intersect ? static_cast<double>(I) * f.invT
-                                                        : static_cast<double>(C + Sg - 2 * static_cast<long long>(I)) * f.invT);
+            const double term = add_acc(yy, u, v, intersect ? Id * f.invT
+                                                        : (FRAC ? (static_cast<double>(C) + Sd - 2.0 * Id) * f.invT
+                                                                : static_cast<double>(C + Sg - 2 * static_cast<long long>(I)) * f.invT));
             if (f.map) write_map(u, v, finalize_L(term, f));  // the last group finishes the map
             else f.partial[static_cast<int64_t>(v) * f.nu + u] = term;
         } else {
@@ -623,6 +664,8 @@ __global__ void __launch_bounds__(256, 2) sweep_match_kernel(QuantParams q, Pixe
 
         uint32_t Iw[8] = {0, 0, 0, 0, 0, 0, 0, 0}, Cw[8] = {0, 0, 0, 0, 0, 0, 0, 0};
         int Ioff = 0, Coff = 0;  // per-lane offsets summed over the lane's bins (integer path)
+        // fractional path: flag of c_k > floor(s_k) for group g at bit 12 + g of each half
+        uint32_t Pf[8] = {0, 0, 0, 0, 0, 0, 0, 0}, pall = 0;
         double acc[4] = {0.0, 0.0, 0.0, 0.0};
 #pragma unroll
         for (int g = 0; g < kB / 4; ++g) {
@@ -635,12 +678,24 @@ __global__ void __launch_bounds__(256, 2) sweep_match_kernel(QuantParams q, Pixe
                 const int go = 4 * g * VS;
                 window_counts_q<KWM>(pb + go, vq + go, mq, aw0, apsh, amask, w, off);
                 const int sk = static_cast<int>(srep_s[wb * kB + 4 * g + qq] & 0xFFFFu);
-                // min(w + off, s_k) = min(w, s_k - off) + off in signed 16-bit halves: the
-                // integer path runs only for kw * kh <= 24576, so -32768 <= s_k - off <= 32767
-                const uint32_t thr = static_cast<uint32_t>((sk - off) & 0xFFFF) * 0x10001u;
+                // min(w + off, s_k) = min(w, s_k - off) + off.  A negative threshold (off > s_k:
+                // e.g. a window inside one bin against a template with < 16 pixels of it) has
+                // min = s_k - off for every w >= 0: it goes to the offset and the packed min
+                // runs on 0, so every half stays a non-negative u16 (exact linear encoding).
+                // 0 <= thr <= s_k + 8160 < 2^16.
+                const int ti = sk - off;
+                const uint32_t thr = static_cast<uint32_t>(max(ti, 0)) * 0x10001u;
+                constexpr uint32_t kFlag = 0x10001u << 12;
 #pragma unroll
-                for (int j = 0; j < 8; ++j) Iw[j] += min_s16x2(w[j], thr);
-                Ioff += off;
+                for (int j = 0; j < 8; ++j) {
+                    const uint32_t mn = min_u16x2(w[j], thr);
+                    Iw[j] += mn;
+                    // d = w - min = max(c - floor(s), 0) <= kw kh <= 4096 per half: bit 12 + g
+                    // of d + 2^(12+g) - 1 is set iff d >= 1 (no carry across the halves)
+                    if (FRAC) Pf[j] |= (w[j] - mn + (kFlag << g) - 0x10001u) & (kFlag << g);
+                }
+                Ioff += off + min(ti, 0);
+                if (FRAC) pall |= ti < 0 ? (kFlag << g) : 0u;  // c > floor(s) in every window
                 if (!ALLB) {
 #pragma unroll
                     for (int j = 0; j < 8; ++j) Cw[j] += w[j];
@@ -708,6 +763,33 @@ __global__ void __launch_bounds__(256, 2) sweep_match_kernel(QuantParams q, Pixe
                 }
                 quarter_reduce(Iw, qq);
                 const int jb = 4 * (qq >> 1) + 2 * (qq & 1);
+                if (FRAC) {
+                    // combine the four quarters' flags of the lane's windows (the words jb, jb + 1
+                    // of quarter_reduce): per half, quarter 0 / 2 / 1 / 3 at bits 12-15 / 8-11 /
+                    // 4-7 / 0-3, then two table lookups (bytes {0 2 | 1 3}) per window
+                    const bool hi2 = qq & 2, hi1 = qq & 1;
+                    uint32_t v[4];
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) {
+                        const uint32_t a = Pf[j] | pall, b = Pf[j + 4] | pall;
+                        const uint32_t r = __shfl_xor_sync(0xffffffffu, hi2 ? a : b, 16);
+                        v[j] = hi2 ? (r | (b >> 4)) : (a | (r >> 4));
+                    }
+                    uint32_t u2[2];
+#pragma unroll
+                    for (int j = 0; j < 2; ++j) {
+                        const uint32_t r = __shfl_xor_sync(0xffffffffu, hi1 ? v[j] : v[j + 2], 8);
+                        u2[j] = hi1 ? (r | (v[j + 2] >> 8)) : (v[j] | (r >> 8));
+                    }
+                    const float* tH = ftab + wb * 512;
+                    const float* tL = tH + 256;
+                    float4 o;
+                    o.x = tH[(u2[0] >> 8) & 255u] + tL[u2[0] & 255u];
+                    o.y = tH[u2[0] >> 24] + tL[(u2[0] >> 16) & 255u];
+                    o.z = tH[(u2[1] >> 8) & 255u] + tL[u2[1] & 255u];
+                    o.w = tH[u2[1] >> 24] + tL[(u2[1] >> 16) & 255u];
+                    *reinterpret_cast<float4*>(fr + ((y & 1) * NW + warp) * kStrip + 16 * mq + 2 * jb) = o;
+                }
                 uint32_t* rw = red32 + (y & 1) * 64 * S + sc * 64 + 8 * mq + jb;
                 if (NWB == 1) {  // one warp per strip: the row's sums are final
                     rw[0] = Iw[0];
@@ -743,31 +825,35 @@ constexpr size_t kSmemBytes = smem_bytes_s<1>();
 
 
 template <int KWM, bool ALLB, int SK, int S>
-void launch_variants(dim3 grid, cudaStream_t s, const QuantParams& q, const PixelMode& pm, const spct_ih& out,
-                     const BuildPlan& bp, const FusedCarries& fc, const FusedParams& f) {
+void launch_variants(bool frac, dim3 grid, cudaStream_t s, const QuantParams& q, const PixelMode& pm,
+                     const spct_ih& out, const BuildPlan& bp, const FusedCarries& fc, const FusedParams& f) {
     constexpr int NT = Geo<S>::NT;
     constexpr size_t SM = smem_bytes_s<S>();
-    ensure_smem(sweep_match_kernel<true, true, KWM, ALLB, SK, S>, SM);
-    ensure_smem(sweep_match_kernel<true, false, KWM, false, SK, S>, SM);
-    ensure_smem(sweep_match_kernel<false, true, KWM, ALLB, SK, S>, SM);
-    ensure_smem(sweep_match_kernel<false, false, KWM, false, SK, S>, SM);
-    // integer (template-crop) variant and FP64 variant: the one not selected by the
-    // device-side template prep exits on entry
-    if (out.data) {
-        sweep_match_kernel<true, true, KWM, ALLB, SK, S><<<grid, NT, SM, s>>>(q, pm, out, bp.Lb, bp.Wp, bp.band_rows, bp.nstrips, fc, f);
-        sweep_match_kernel<true, false, KWM, false, SK, S><<<grid, NT, SM, s>>>(q, pm, out, bp.Lb, bp.Wp, bp.band_rows, bp.nstrips, fc, f);
-    } else {
-        sweep_match_kernel<false, true, KWM, ALLB, SK, S><<<grid, NT, SM, s>>>(q, pm, out, bp.Lb, bp.Wp, bp.band_rows, bp.nstrips, fc, f);
-        sweep_match_kernel<false, false, KWM, false, SK, S><<<grid, NT, SM, s>>>(q, pm, out, bp.Lb, bp.Wp, bp.band_rows, bp.nstrips, fc, f);
+    // the exact integer (template-crop) variant and, for the other templates, the
+    // fractional variant (p = 1 / intersection, kw kh <= 4096) or the FP64 one: the variant
+    // not selected by the device-side template prep exits on entry
+#define SPCT_GO(ST, MD, AB)                                                                                      \
+    {                                                                                                            \
+        ensure_smem(sweep_match_kernel<ST, MD, KWM, AB, SK, S>, SM);                                             \
+        sweep_match_kernel<ST, MD, KWM, AB, SK, S>                                                               \
+            <<<grid, NT, SM, s>>>(q, pm, out, bp.Lb, bp.Wp, bp.band_rows, bp.nstrips, fc, f);                    \
     }
+    if (out.data) {
+        SPCT_GO(true, 1, ALLB)
+        if (frac) SPCT_GO(true, 2, ALLB) else SPCT_GO(true, 0, false)
+    } else {
+        SPCT_GO(false, 1, ALLB)
+        if (frac) SPCT_GO(false, 2, ALLB) else SPCT_GO(false, 0, false)
+    }
+#undef SPCT_GO
 }
 
 template <int KWM, int S>
 void launch_kw_impl(bool allb, int sk, dim3 grid, cudaStream_t s, const QuantParams& q, const PixelMode& pm,
                     const spct_ih& out, const BuildPlan& bp, const FusedCarries& fc, const FusedParams& f) {
 #define SPCT_SK(SKV)                                                                      \
-    if (allb) launch_variants<KWM, true, SKV, S>(grid, s, q, pm, out, bp, fc, f);           \
-    else launch_variants<KWM, false, SKV, S>(grid, s, q, pm, out, bp, fc, f);
+    if (allb) launch_variants<KWM, true, SKV, S>(f.frac, grid, s, q, pm, out, bp, fc, f);   \
+    else launch_variants<KWM, false, SKV, S>(f.frac, grid, s, q, pm, out, bp, fc, f);
     if (sk == 1) {
         SPCT_SK(1)
     } else if (sk == 2) {

@@ -22,7 +22,7 @@ int fused_ctas_per_sm(int strips) {
         cudaError_t e;
 #define SPCT_OCC(SV)                                                                          \
     {                                                                                         \
-        auto k = spct_fused::sweep_match_kernel<true, true, 64, true, 1, SV>;                  \
+        auto k = spct_fused::sweep_match_kernel<true, 1, 64, true, 1, SV>;                  \
         ensure_smem(k, spct_fused::smem_bytes_s<SV>());                                       \
         e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&v, k, 256, spct_fused::smem_bytes_s<SV>()); \
     }

@@ -350,6 +350,41 @@ def test_fused_map_rejects_slabs(P):
         P.build_and_match_map(img, 32, np.full(32, 1 / 32), 16, 16, 1.0, out=t)
 
 
+def _blocky_image(w, h, seed):
+    """Uniform blocks (one bin over whole windows) beside a noisy patch: window counts of
+    kw * kh in one bin against template counts below 16 (negative min thresholds in the
+    integer path)."""
+    rng = np.random.default_rng(seed)
+    img = np.zeros((h, w), np.uint8)
+    img[:, w // 2:] = 255
+    img[h // 3:2 * h // 3, :] = 130
+    y0, x0 = h // 4, w // 4
+    img[y0:y0 + 90, x0:x0 + 90] = rng.integers(20, 120, (90, 90), dtype=np.uint8)  # no block bin
+    return img
+
+
+@pytest.mark.parametrize("bins,kw,kh", [(16, 64, 64), (128, 64, 64), (40, 33, 21), (200, 128, 100)])
+@pytest.mark.parametrize("general", [False, True])
+def test_fused_uniform_regions(P, bins, kw, kh, general):
+    """Windows entirely inside one bin next to templates with few (< 16) pixels of that bin."""
+    w, h = 420, 330
+    img = _blocky_image(w, h, bins)
+    qb = oracle.quantize(img, bins)
+    y0, x0 = h // 4, w // 4
+    th = _crop_template(qb, bins, x0 + 90 - kw + 3, y0 + 90 - kh + 2, kw, kh)  # crop: 3 x 2 pixels of a block
+    if general:
+        th = th * 0.97 + 0.03 / bins
+    for metric in (0, 1):
+        want = oracle.hist_match_map_direct(qb, bins, th, kw, kh, 1.0, metric)
+        for store in (True, False):
+            t = P.IntegralHistogramTensor(w, h, bins)
+            if not store:
+                t.desc.data = None
+            _, lmap = P.build_and_match_map(img, bins, th, kw, kh, 1.0, metric, out=t)
+            got = lmap.cpu().numpy()
+            assert close(got, want), (metric, store, np.abs(got - want).max())
+
+
 @pytest.mark.parametrize("w,h,bins,kw,kh", FUSED_CASES[:6])
 @pytest.mark.parametrize("p,metric", [(1.0, 0), (2.0, 0), (1.7, 0), (1.0, 1), (1.0, 2), (1.0, 3)])
 def test_fused_general_template(P, w, h, bins, kw, kh, p, metric):

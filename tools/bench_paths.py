@@ -19,8 +19,10 @@ integral = bench.template_hist(bench.make_frame(W, H), nb, kw, kh)
 fh = bench.make_frame(W, H)
 crop = (fh[2000:2063, 2000:2064].astype(np.int64) * nb) >> 8  # 63 x 64 crop: non-integral s_k
 nonint = np.bincount(crop.reshape(-1), minlength=nb).astype(np.float64) / crop.size
-cases = {"integer p=1": (integral, 1.0, 0), "fp64 p=1 (non-integral tmpl)": (nonint, 1.0, 0),
-         "fp64 p=2": (integral, 2.0, 0), "fp64 bhattacharyya": (integral, 1.0, 2)}
+gen = bench.general_template(nb)
+cases = {"integer p=1": (integral, 1.0, 0), "frac p=1 (non-integral crop)": (nonint, 1.0, 0),
+         "frac p=1 (random tmpl)": (gen, 1.0, 0), "frac intersection (random)": (gen, 1.0, 1),
+         "fp64 p=2": (gen, 2.0, 0), "fp64 bhattacharyya": (gen, 1.0, 2), "fp64 chi2": (gen, 1.0, 3)}
 res = {}
 for name, (tm, p, metric) in cases.items():
     td = torch.from_numpy(tm).to(dev)
