@@ -11,11 +11,14 @@ namespace spct_fused {
 // is an integer up to FP noise (then the integer formula is exact to ~1e-15) and the metric
 // allows it; otherwise kind 2 (integer path on floor(s_k) plus the fractional parts) when
 // the host allows it (`frac_ok`: p = 1 / intersection, kw kh <= 4096), else kind 0 (FP64).
+// Other metrics: kind `other_kind` (3: integer / FP32 terms, 0: FP64).
 // Layout (fused_prep_layout): [0] kind, [1 + k] floor(s_k) replicated in both u16 halves;
-// per 128-bin group sum floor(s_k) (int64) and sum r_k (double); r_k per bin (double).
+// per 128-bin group sum floor(s_k) (int64) and sum r_k (double); r_k per bin (double);
+// the MODE 3 constants per bin (float4) and per 16-bin slab (double2), FusedParams::c3.
 __global__ void prep_kernel(const double* __restrict__ tmpl, int bin0, int bins, double T, int fast_metric,
-                            int frac_ok, uint32_t* __restrict__ prep, long long* __restrict__ S_group,
-                            double* __restrict__ Sr_group, double* __restrict__ rfrac, int ngroups) {
+                            int frac_ok, int other_kind, uint32_t* __restrict__ prep, long long* __restrict__ S_group,
+                            double* __restrict__ Sr_group, double* __restrict__ rfrac, float4* __restrict__ c3,
+                            double2* __restrict__ c3slab, int ngroups) {
     __shared__ int all_integral;
     if (threadIdx.x == 0) all_integral = 1;
     __syncthreads();
@@ -29,9 +32,24 @@ __global__ void prep_kernel(const double* __restrict__ tmpl, int bin0, int bins,
         const uint32_t ni = static_cast<uint32_t>(fl);
         prep[1 + k] = ni | (ni << 16);
         rfrac[k] = integral ? 0.0 : fmax(s - fl, 0.0);
+        {   // MODE 3 constants (floor and fraction of s_k without the integrality snap)
+            const double f3 = fmin(fmax(floor(s), 0.0), T), r3 = s - f3, R = rint(32.0 * r3);
+            const int K = static_cast<int>(64.0 * f3 + 2.0 * R);
+            c3[k] = make_float4(__int_as_float(K), static_cast<float>(r3 - R / 32.0),
+                                static_cast<float>(sqrt(tmpl[bin0 + k] / T)), static_cast<float>(s));
+        }
     }
     __syncthreads();
-    if (threadIdx.x == 0) prep[0] = fast_metric ? (all_integral ? 1u : (frac_ok ? 2u : 0u)) : 0u;
+    if (threadIdx.x == 0) prep[0] = fast_metric ? (all_integral ? 1u : (frac_ok ? 2u : 0u)) : static_cast<uint32_t>(other_kind);
+    for (int sl = threadIdx.x; sl < (bins + 15) / 16; sl += blockDim.x) {
+        double a = 0.0, b = 0.0;
+        for (int k = 16 * sl; k < min(bins, 16 * sl + 16); ++k) {
+            const double sk = T * tmpl[bin0 + k];
+            a += sk * sk;
+            b += sk;
+        }
+        c3slab[sl] = make_double2(a, b);
+    }
     for (int g = threadIdx.x; g < ngroups; g += blockDim.x) {
         long long acc = 0;
         double racc = 0.0;
@@ -45,7 +63,7 @@ __global__ void prep_kernel(const double* __restrict__ tmpl, int bin0, int bins,
 }
 
 struct PrepLayout {
-    size_t S, Sr, r, total;
+    size_t S, Sr, r, c3, c3slab, total;
 };
 inline PrepLayout fused_prep_layout(int bins) {
     const size_t ng = (static_cast<size_t>(bins) + kGroupBins - 1) / kGroupBins;
@@ -53,7 +71,9 @@ inline PrepLayout fused_prep_layout(int bins) {
     l.S = round_up((static_cast<int64_t>(bins) + 1) * 4, 256);
     l.Sr = l.S + round_up(static_cast<int64_t>(ng) * 8, 256);
     l.r = l.Sr + round_up(static_cast<int64_t>(ng) * 8, 256);
-    l.total = l.r + round_up(static_cast<int64_t>(bins) * 8, 256);
+    l.c3 = l.r + round_up(static_cast<int64_t>(bins) * 8, 256);
+    l.c3slab = l.c3 + round_up(static_cast<int64_t>(bins) * 16, 256);
+    l.total = l.c3slab + round_up(static_cast<int64_t>((bins + 15) / 16) * 16, 256);
     return l;
 }
 
@@ -137,8 +157,14 @@ spct_status build_match(const spct_source* src, const spct_ih* out, const double
     const int fast_metric = ((metric == SPCT_METRIC_MINKOWSKI && p == 1.0) || metric == SPCT_METRIC_INTERSECTION) &&
                             T <= 24576;
     const int frac_ok = fast_metric && T <= 4096;
-    prep_kernel<<<1, 256, 0, s>>>(tmpl, out->bin0, out->bins, static_cast<double>(T), fast_metric, frac_ok, prep, Sg,
-                                  Sr, rfrac, ngroups);
+    // p = 2 (int32 sums need kw kh <= 4096), Bhattacharyya and chi-square: integer / FP32 terms
+    const int f32_ok = (metric == SPCT_METRIC_MINKOWSKI && p == 2.0 && T <= 4096) ||
+                       metric == SPCT_METRIC_BHATTACHARYYA || metric == SPCT_METRIC_CHISQ;
+    const int path = fast_metric ? 1 : (f32_ok ? 3 : 0);
+    float4* c3 = reinterpret_cast<float4*>(ws + pl.c3);
+    double2* c3slab = reinterpret_cast<double2*>(ws + pl.c3slab);
+    prep_kernel<<<1, 256, 0, s>>>(tmpl, out->bin0, out->bins, static_cast<double>(T), fast_metric, frac_ok,
+                                  path == 3 ? 3 : 0, prep, Sg, Sr, rfrac, c3, c3slab, ngroups);
     if (auto st = launch_status("prep_kernel")) return st;
 
     FusedParams f{};
@@ -167,6 +193,9 @@ spct_status build_match(const spct_source* src, const spct_ih* out, const double
     f.Sr_group = Sr;
     f.rfrac = rfrac;
     f.frac = frac_ok;
+    f.path = path;
+    f.c3 = c3;
+    f.c3slab = c3slab;
     f.partial = group_part ? group_part : partial;
     f.map = group_part ? nullptr : map;
     f.W = out->width;

@@ -52,11 +52,15 @@ struct FusedParams {
     const long long* S_group;    // sum of floor(s_k) per 128-bin group
     const double* Sr_group;      // sum of the fractional parts r_k = s_k - floor(s_k) per 128-bin group
     const double* rfrac;         // r_k per slab-local bin (kind 2)
+    const float4* c3;            // kind 3, per slab-local bin: {64 floor(s_k) + 2 R_k (int bits), r_k - R_k / 32,
+                                 //   sqrt(t_k / T), s_k}, R_k = rint(32 r_k)
+    const double2* c3slab;       // kind 3, per 16-bin slab: {sum s_k^2, sum s_k}
     double* partial;
     double* map;                 // non-null: write the finished likelihood map (one group = every bin)
     double inv_p, dmax, inv_dmax;  // inv_dmax != 0 iff dmax is a power of two (exact product)
     int W, H;
     int frac;     // host: the fractional variant is launched instead of the FP64 one
+    int path;     // host: 1 = integer metric (MODE 1 + MODE 2 or 0), 3 = MODE 3 only, 0 = MODE 0 only
     int fp_kind;  // FP64 path term: 0 Minkowski p=1, 1 p=2, 2 general p, 3 intersection, 4 Bhattacharyya, 5 chi-square
 };
 
@@ -140,6 +144,42 @@ __device__ __forceinline__ double fp_term(uint32_t c, double t, double invT, dou
     if (!(den > 0.0)) return 0.0;
     const double df = __dsub_rn(q, t);
     return __ddiv_rn(__dmul_rn(df, df), den);
+}
+
+// u16 count -> float, exactly (c < 2^23): 2^23 + c by bit pattern, minus 2^23.
+__device__ __forceinline__ float count_f32(uint32_t c) { return __int_as_float(0x4B000000u | c) - 8388608.0f; }
+
+__device__ __forceinline__ float sqrt_approx(float x) {
+    float r;
+    asm("sqrt.approx.f32 %0, %1;" : "=f"(r) : "f"(x));
+    return r;
+}
+
+__device__ __forceinline__ float rcp_approx(float x) {
+    float r;
+    asm("rcp.approx.f32 %0, %1;" : "=f"(r) : "f"(x));
+    return r;
+}
+
+// MODE 3 per-bin terms of one window count c (cst = FusedParams::c3 of the bin):
+//   FK 1 (p = 2): T^2 d^2 = sum (c - s)^2 = (1/32) sum c (32 c - 64 f - 2 R) - 2 sum c r_lo + sum s^2
+//     with s = f + R/32 + r_lo: the first sum exact in int32 (|.| < 2^31 for kw kh <= 4096), the
+//     second (|r_lo| <= 1/64) in FP32, so no cancellation is left in FP32 near d = 0;
+//   FK 4 (Bhattacharyya): sum sqrt(q t) = sum sqrt(c) sqrt(t / T), FP32 (non-negative terms);
+//   FK 5 (chi-square): (q - t)^2 / (q + t) = q + t - 4 q t / (q + t): FP32 sum of
+//     Y = sum c s / (c + s) (non-negative terms); the linear part is exact (window counts).
+template <int FK>
+__device__ __forceinline__ void f32_term(uint32_t c, const float4& cst, int& ai, float& af) {
+    const float cf = count_f32(c);
+    if (FK == 1) {
+        const int ci = static_cast<int>(c);
+        ai += ci * (32 * ci - __float_as_int(cst.x));
+        af = fmaf(cf, cst.y, af);
+    } else if (FK == 4) {
+        af = fmaf(sqrt_approx(cf), cst.z, af);
+    } else {
+        af = fmaf(cf * cst.w, rcp_approx(cf + cst.w), af);
+    }
 }
 
 // Window counts (general path), phase 1: for bin row `vrow`, the inclusive prefix G of the
@@ -303,14 +343,16 @@ constexpr size_t smem_bytes_s() {
 
 // MODE: 0 = the FP64 per-bin path (any metric), 1 = the exact integer path (integral
 // template, p = 1 / intersection), 2 = the integer path on floor(s_k) plus the fractional
-// correction sum_{k: c_k > floor(s_k)} r_k (any template, p = 1 / intersection, kw kh <= 4096).
+// correction sum_{k: c_k > floor(s_k)} r_k (any template, p = 1 / intersection, kw kh <= 4096),
+// 3 = the full-warp layout of MODE 0 with integer / FP32 per-bin terms for p = 2 (kw kh <= 4096),
+// Bhattacharyya and chi-square (f32_term below).
 template <bool STORE, int MODE, int KWM, bool ALLB, int SK, int S>
 __global__ void __launch_bounds__(256, 2) sweep_match_kernel(QuantParams q, PixelMode pm, spct_ih out, int Lb, int Wp,
                                                              int band_rows, int nstrips, FusedCarries fc,
                                                              FusedParams f) {
     using G = Geo<S>;
     constexpr int NW = G::NW, NWB = G::NWB, NB = G::NB, NT = G::NT, E = G::E, VS = G::VS, CPT = G::CPT;
-    constexpr bool FAST = MODE != 0, FRAC = MODE == 2;
+    constexpr bool FAST = MODE == 1 || MODE == 2, FRAC = MODE == 2;
     extern __shared__ uint4 smem_raw[];
     uint32_t* vc = reinterpret_cast<uint32_t*>(smem_raw);                 // [NB bins][VS words], padded
     uint32_t* gbuf = vc + NB * VS;                                          // [NW warps][4][128 words] (general kw)
@@ -324,11 +366,13 @@ __global__ void __launch_bounds__(256, 2) sweep_match_kernel(QuantParams q, Pixe
     // integer path: per row parity, strip and window pair, the packed sums over the warps
     // (shared atomics), I at [parity][strip][64] and C at 128 S + [parity][strip][64]
     uint32_t* red32 = reinterpret_cast<uint32_t*>(red);
-    // fractional path: per warp and row parity the FP32 correction of its 128 windows
-    // [2][NW][128] (after the integer path's 8 KB of `red`), and per bin slab two 256-entry
-    // tables of fractional sums over 8 bins (in gbuf, unused by the integer paths)
-    float* fr = reinterpret_cast<float*>(red) + 2048;
-    float* ftab = reinterpret_cast<float*>(gbuf);
+    // fractional path, in 2^-40 fixed point (exact sums in any order): per row parity and
+    // window the correction accumulated over the warps ([2][S][128] pairs of u32 shared
+    // atomics on the low 24 bits and the rest of each warp's u64 value: no 64-bit CAS loop), and
+    // per bin slab four 16-entry tables (one per flag nibble) of sums of r_k over 4 bins.
+    // gbuf (16 KB) is unused by the integer paths; `red` holds red32 (S KB) and accb.
+    uint64_t* acc64 = S == 8 ? reinterpret_cast<uint64_t*>(gbuf) : reinterpret_cast<uint64_t*>(red + 512);
+    uint64_t* tab64 = S == 8 ? reinterpret_cast<uint64_t*>(red + 1024) : reinterpret_cast<uint64_t*>(gbuf);
 
     // Two variants are launched; the one that does not match the template prep exits.
     if (__ldg(f.prep) != static_cast<uint32_t>(MODE)) return;
@@ -372,22 +416,23 @@ __global__ void __launch_bounds__(256, 2) sweep_match_kernel(QuantParams q, Pixe
             const int n = f.kw - 16 * (i >> 3) - 2 * (i & 7);
             amask[i] = n >= 2 ? 0xFFFFFFFFu : (n == 1 ? 0xFFFFu : 0u);
         }
-    if (FRAC)
-        // table h of slab wbi, index i: sum of r_k over the slab's bins 4 g + qa (bit 4 + g of
-        // i) and 4 g + qb (bit g), {qa, qb} = {0, 2} (h = 0) or {1, 3} (h = 1): the flag
-        // layout after the cross-quarter combine below.  FP64 sums, fixed order.
-        for (int i = tid; i < NWB * 512; i += NT) {
-            const int wbi = i >> 9, h = (i >> 8) & 1, idx = i & 255;
-            const int kb = g0 + wbi * kB, klim = g0 + nb_cta;
-            double acc = 0.0;
+    if (FRAC) {
+        // table n of slab wbi, index i: sum of r_k (2^-40 units) over the slab's bins 4 g + q(n)
+        // with bit g of i set, q = {3, 1, 2, 0} for nibbles n = 0..3: the flag layout after the
+        // cross-quarter combine below
+        for (int i = tid; i < NWB * 64; i += NT) {
+            const int wbi = i >> 6, n = (i >> 4) & 3, idx = i & 15;
+            const int q = n == 0 ? 3 : (n == 1 ? 1 : (n == 2 ? 2 : 0));
+            const int kb = g0 + wbi * kB + q, klim = g0 + nb_cta;
+            uint64_t acc = 0;
 #pragma unroll
-            for (int g = 0; g < 4; ++g) {
-                const int ka = kb + 4 * g + h, kc = kb + 4 * g + 2 + h;
-                if (((idx >> (4 + g)) & 1) && ka < klim) acc += __ldg(f.rfrac + ka);
-                if (((idx >> g) & 1) && kc < klim) acc += __ldg(f.rfrac + kc);
-            }
-            ftab[i] = static_cast<float>(acc);
+            for (int g = 0; g < 4; ++g)
+                if (((idx >> g) & 1) && kb + 4 * g < klim)
+                    acc += __double2ull_rn(__ldg(f.rfrac + kb + 4 * g) * 1099511627776.0);  // 2^40
+            tab64[i] = acc;
         }
+        for (int i = tid; i < 2 * kStrip * S; i += NT) acc64[i] = 0;
+    }
 
     uint32_t V[4][kB];
     if (STORE && warp_live)
@@ -557,16 +602,15 @@ __global__ void __launch_bounds__(256, 2) sweep_match_kernel(QuantParams q, Pixe
             }
             if (u < 0 || e >= W) return;
             const uint32_t I = (xi >> (16 * (t & 1))) & 0xFFFFu;
-            // sum_k min(c_k, s_k): exact integers, plus the fractional correction (FP32 per
-            // warp, FP64 over the warps in a fixed order)
+            // sum_k min(c_k, s_k): exact integers, plus the fractional correction (2^-40 fixed
+            // point: within 2^-41 per bin of sum r_k, independent of the summation order)
             double Id = static_cast<double>(I);
             if (FRAC) {
-                const float* fb = fr + ((yy & 1) * NW + (t / kStrip) * NWB) * kStrip + (t % kStrip);
-                double corr = 0.0;
-#pragma unroll
-                for (int w = 0; w < NWB; ++w)
-                    if (w < nwarps_live) corr += static_cast<double>(fb[w * kStrip]);
-                Id += corr;
+                uint64_t* a64 = acc64 + (yy & 1) * kStrip * S + t;
+                const uint2 pr = *reinterpret_cast<const uint2*>(a64);
+                *a64 = 0;  // for row yy + 2
+                const uint64_t corr = (static_cast<uint64_t>(pr.y) << 24) + pr.x;
+                Id += static_cast<double>(corr) * (1.0 / 1099511627776.0);
             }
             if (ALLB && f.map) {
                 const double L = fma(lin_b, Id, lin_a);
@@ -704,11 +748,15 @@ __global__ void __launch_bounds__(256, 2) sweep_match_kernel(QuantParams q, Pixe
             }
         }
         if constexpr (!FAST) if (match_row) {
-            // FP64 path: the window terms in a rolled loop over the bin groups, one loop per
-            // metric (a per-row switch) so the running loop stays small
+            // FP64 path (MODE 0) / integer-FP32 terms (MODE 3): the window terms in a rolled loop
+            // over the bin groups, one loop per metric (a per-row switch) so the running loop
+            // stays small
             auto rows = [&](auto fk_tag) {
                 constexpr int FK = decltype(fk_tag)::value;
                 const double invT = f.invT, pp = f.p;
+                int ai[4] = {0, 0, 0, 0};                   // MODE 3
+                float af[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+                uint32_t cw[2] = {0u, 0u};                  // MODE 3, chi-square: packed window counts
 #pragma unroll 1
                 for (int g = 0; g < kB / 4; ++g) {
                     uint32_t aw[4][2], bw[4][2];
@@ -733,7 +781,21 @@ __global__ void __launch_bounds__(256, 2) sweep_match_kernel(QuantParams q, Pixe
                         } else {
                             window_diff(gb + i * kVcWords, pw, psh, bw[i][0], bw[i][1], c0, c1);
                         }
-                        if (k < k_live) {
+                        if constexpr (MODE == 3) {
+                            if (k < k_live) {
+                                const float4 cst = __ldg(f.c3 + kl0 + k);
+                                if (FK == 5) {
+                                    cw[0] += c0;
+                                    cw[1] += c1;
+                                }
+                                if (FK != 5 || cst.w > 0.0f) {  // chi-square: bins with s = 0 add 0 to Y
+                                    f32_term<FK>(c0 & 0xFFFFu, cst, ai[0], af[0]);
+                                    f32_term<FK>(c0 >> 16, cst, ai[1], af[1]);
+                                    f32_term<FK>(c1 & 0xFFFFu, cst, ai[2], af[2]);
+                                    f32_term<FK>(c1 >> 16, cst, ai[3], af[3]);
+                                }
+                            }
+                        } else if (k < k_live) {
                             const double t = __ldg(f.tmpl + k0 + k);
                             acc[0] = __dadd_rn(acc[0], fp_term<FK>(c0 & 0xFFFFu, t, invT, pp));
                             acc[1] = __dadd_rn(acc[1], fp_term<FK>(c0 >> 16, t, invT, pp));
@@ -743,8 +805,30 @@ __global__ void __launch_bounds__(256, 2) sweep_match_kernel(QuantParams q, Pixe
                     }
                     if (KWM == 0) __syncwarp();
                 }
+                if constexpr (MODE == 3) {
+                    // the warp's partial term per window, in the units of the FP64 path
+                    const double2 sc = f.c3slab[kl0 / kB];  // {sum s^2, sum s} over the warp's bins
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) {
+                        if (FK == 1) {
+                            acc[j] = (static_cast<double>(ai[j]) * (1.0 / 32.0) - 2.0 * static_cast<double>(af[j]) + sc.x) *
+                                     invT * invT;
+                        } else if (FK == 4) {
+                            acc[j] = static_cast<double>(af[j]);
+                        } else {
+                            const uint32_t cj = (cw[j >> 1] >> (16 * (j & 1))) & 0xFFFFu;
+                            acc[j] = (static_cast<double>(cj) + sc.y - 4.0 * static_cast<double>(af[j])) * invT;
+                        }
+                    }
+                }
             };
-            switch (f.fp_kind) {
+            if constexpr (MODE == 3) {
+                switch (f.fp_kind) {
+                    case 1: rows(std::integral_constant<int, 1>{}); break;
+                    case 4: rows(std::integral_constant<int, 4>{}); break;
+                    default: rows(std::integral_constant<int, 5>{}); break;
+                }
+            } else switch (f.fp_kind) {
                 case 0: rows(std::integral_constant<int, 0>{}); break;
                 case 1: rows(std::integral_constant<int, 1>{}); break;
                 case 2: rows(std::integral_constant<int, 2>{}); break;
@@ -766,7 +850,7 @@ __global__ void __launch_bounds__(256, 2) sweep_match_kernel(QuantParams q, Pixe
                 if (FRAC) {
                     // combine the four quarters' flags of the lane's windows (the words jb, jb + 1
                     // of quarter_reduce): per half, quarter 0 / 2 / 1 / 3 at bits 12-15 / 8-11 /
-                    // 4-7 / 0-3, then two table lookups (bytes {0 2 | 1 3}) per window
+                    // 4-7 / 0-3, then one table lookup per nibble and window
                     const bool hi2 = qq & 2, hi1 = qq & 1;
                     uint32_t v[4];
 #pragma unroll
@@ -781,14 +865,18 @@ __global__ void __launch_bounds__(256, 2) sweep_match_kernel(QuantParams q, Pixe
                         const uint32_t r = __shfl_xor_sync(0xffffffffu, hi1 ? v[j] : v[j + 2], 8);
                         u2[j] = hi1 ? (r | (v[j + 2] >> 8)) : (v[j] | (r >> 8));
                     }
-                    const float* tH = ftab + wb * 512;
-                    const float* tL = tH + 256;
-                    float4 o;
-                    o.x = tH[(u2[0] >> 8) & 255u] + tL[u2[0] & 255u];
-                    o.y = tH[u2[0] >> 24] + tL[(u2[0] >> 16) & 255u];
-                    o.z = tH[(u2[1] >> 8) & 255u] + tL[u2[1] & 255u];
-                    o.w = tH[u2[1] >> 24] + tL[(u2[1] >> 16) & 255u];
-                    *reinterpret_cast<float4*>(fr + ((y & 1) * NW + warp) * kStrip + 16 * mq + 2 * jb) = o;
+                    const uint64_t* tb = tab64 + wb * 64;
+                    uint64_t* a64 = acc64 + ((y & 1) * S + sc) * kStrip + 16 * mq + 2 * jb;
+#pragma unroll
+                    for (int h = 0; h < 4; ++h) {  // window 16 mq + 2 jb + h: half h & 1 of word h >> 1
+                        const uint32_t x = u2[h >> 1] >> (16 * (h & 1));
+                        const uint64_t v = tb[x & 15u] + tb[16 + ((x >> 4) & 15u)] + tb[32 + ((x >> 8) & 15u)] +
+                                           tb[48 + ((x >> 12) & 15u)];
+                        // v < 16 * 2^40: the low 24 bits and the high 20 summed over <= 8 warps fit u32
+                        uint32_t* a32 = reinterpret_cast<uint32_t*>(a64 + h);
+                        atomicAdd(a32, static_cast<uint32_t>(v) & 0xFFFFFFu);
+                        atomicAdd(a32 + 1, static_cast<uint32_t>(v >> 24));
+                    }
                 }
                 uint32_t* rw = red32 + (y & 1) * 64 * S + sc * 64 + 8 * mq + jb;
                 if (NWB == 1) {  // one warp per strip: the row's sums are final
@@ -825,7 +913,7 @@ constexpr size_t kSmemBytes = smem_bytes_s<1>();
 
 
 template <int KWM, bool ALLB, int SK, int S>
-void launch_variants(bool frac, dim3 grid, cudaStream_t s, const QuantParams& q, const PixelMode& pm,
+void launch_variants(bool frac, int path, dim3 grid, cudaStream_t s, const QuantParams& q, const PixelMode& pm,
                      const spct_ih& out, const BuildPlan& bp, const FusedCarries& fc, const FusedParams& f) {
     constexpr int NT = Geo<S>::NT;
     constexpr size_t SM = smem_bytes_s<S>();
@@ -838,12 +926,25 @@ void launch_variants(bool frac, dim3 grid, cudaStream_t s, const QuantParams& q,
         sweep_match_kernel<ST, MD, KWM, AB, SK, S>                                                               \
             <<<grid, NT, SM, s>>>(q, pm, out, bp.Lb, bp.Wp, bp.band_rows, bp.nstrips, fc, f);                    \
     }
+    // (a metric without an integer path launches its one variant: FP32 terms or FP64)
     if (out.data) {
-        SPCT_GO(true, 1, ALLB)
-        if (frac) SPCT_GO(true, 2, ALLB) else SPCT_GO(true, 0, false)
+        if (path == 1) {
+            SPCT_GO(true, 1, ALLB)
+            if (frac) SPCT_GO(true, 2, ALLB) else SPCT_GO(true, 0, false)
+        } else if (path == 3) {
+            SPCT_GO(true, 3, false)
+        } else {
+            SPCT_GO(true, 0, false)
+        }
     } else {
-        SPCT_GO(false, 1, ALLB)
-        if (frac) SPCT_GO(false, 2, ALLB) else SPCT_GO(false, 0, false)
+        if (path == 1) {
+            SPCT_GO(false, 1, ALLB)
+            if (frac) SPCT_GO(false, 2, ALLB) else SPCT_GO(false, 0, false)
+        } else if (path == 3) {
+            SPCT_GO(false, 3, false)
+        } else {
+            SPCT_GO(false, 0, false)
+        }
     }
 #undef SPCT_GO
 }
@@ -852,8 +953,8 @@ template <int KWM, int S>
 void launch_kw_impl(bool allb, int sk, dim3 grid, cudaStream_t s, const QuantParams& q, const PixelMode& pm,
                     const spct_ih& out, const BuildPlan& bp, const FusedCarries& fc, const FusedParams& f) {
 #define SPCT_SK(SKV)                                                                      \
-    if (allb) launch_variants<KWM, true, SKV, S>(f.frac, grid, s, q, pm, out, bp, fc, f);   \
-    else launch_variants<KWM, false, SKV, S>(f.frac, grid, s, q, pm, out, bp, fc, f);
+    if (allb) launch_variants<KWM, true, SKV, S>(f.frac, f.path, grid, s, q, pm, out, bp, fc, f);   \
+    else launch_variants<KWM, false, SKV, S>(f.frac, f.path, grid, s, q, pm, out, bp, fc, f);
     if (sk == 1) {
         SPCT_SK(1)
     } else if (sk == 2) {

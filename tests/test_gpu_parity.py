@@ -385,6 +385,31 @@ def test_fused_uniform_regions(P, bins, kw, kh, general):
             assert close(got, want), (metric, store, np.abs(got - want).max())
 
 
+@pytest.mark.parametrize("bins,kw,kh", [(128, 64, 64), (48, 33, 17), (200, 40, 40)])
+@pytest.mark.parametrize("p,metric", [(1.0, 0), (2.0, 0), (1.0, 1), (1.0, 2), (1.0, 3)])
+def test_fused_near_zero_likelihoods(P, bins, kw, kh, p, metric):
+    """Templates whose mass sits on bins most windows lack (likelihoods down to ~1e-6): the
+    fractional (p = 1 / intersection) and integer / FP32 (p = 2, Bhattacharyya, chi-square)
+    paths keep the relative tolerance where the map is near 0."""
+    w, h = 380, 260
+    img = oracle.smooth_image(w, h, bins + kw)
+    qb = oracle.quantize(img, bins)
+    cnt = np.bincount(qb.reshape(-1), minlength=bins).astype(np.float64)
+    rng = np.random.default_rng(bins * kh)
+    th = rng.random(bins) * 1e-6
+    rare = np.argsort(cnt)[: max(2, bins // 8)]  # the least frequent bins carry the mass
+    th[rare] += rng.random(rare.size)
+    th /= th.sum()
+    for store in (True, False):
+        t = P.IntegralHistogramTensor(w, h, bins)
+        if not store:
+            t.desc.data = None
+        _, lmap = P.build_and_match_map(img, bins, th, kw, kh, p, metric, out=t)
+        want = oracle.hist_match_map_direct(qb, bins, th, kw, kh, p, metric)
+        got = lmap.cpu().numpy()
+        assert close(got, want), (store, np.abs(got - want).max(), want.min())
+
+
 @pytest.mark.parametrize("w,h,bins,kw,kh", FUSED_CASES[:6])
 @pytest.mark.parametrize("p,metric", [(1.0, 0), (2.0, 0), (1.7, 0), (1.0, 1), (1.0, 2), (1.0, 3)])
 def test_fused_general_template(P, w, h, bins, kw, kh, p, metric):

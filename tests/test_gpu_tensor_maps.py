@@ -161,7 +161,9 @@ def test_extension_metrics_match_published_implementations(P, name):
         want = d[f"{name}_{key}"]
         fused = P.build_and_match_map(bm, bins, t, kw, kh, 1.0, metric)[1].cpu().numpy()
         tensor = P.hist_match_map(tens, t, kw, kh, 1.0, metric, exact=True).cpu().numpy()
-        assert np.abs(fused - want).max() <= 1e-12, (key, "fused")
+        # the fused sweep sums Bhattacharyya / chi-square terms in FP32 per 16-bin slab (MODE 3):
+        # the north star's 1e-5 relative bar; the tensor path keeps the FP64 operation order
+        assert np.all(np.abs(fused - want) <= 1e-5 * np.abs(want) + 1e-12), (key, "fused")
         assert np.abs(tensor - want).max() <= 1e-12, (key, "tensor")
 
 

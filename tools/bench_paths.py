@@ -22,7 +22,8 @@ nonint = np.bincount(crop.reshape(-1), minlength=nb).astype(np.float64) / crop.s
 gen = bench.general_template(nb)
 cases = {"integer p=1": (integral, 1.0, 0), "frac p=1 (non-integral crop)": (nonint, 1.0, 0),
          "frac p=1 (random tmpl)": (gen, 1.0, 0), "frac intersection (random)": (gen, 1.0, 1),
-         "fp64 p=2": (gen, 2.0, 0), "fp64 bhattacharyya": (gen, 1.0, 2), "fp64 chi2": (gen, 1.0, 3)}
+         "p=2 (random)": (gen, 2.0, 0), "bhattacharyya (random)": (gen, 1.0, 2), "chi2 (random)": (gen, 1.0, 3),
+         "fp64 p=1.5 (random)": (gen, 1.5, 0)}
 res = {}
 for name, (tm, p, metric) in cases.items():
     td = torch.from_numpy(tm).to(dev)
