@@ -788,8 +788,9 @@ def run_paths(P, dev, timer, pk, frame, tmpl, t, args) -> dict:
     gt = general_template(NBINS)
     gdev = torch.from_numpy(gt).to(dev)
     alg_f = NBINS * W_IMG * H_IMG * 4 + W_IMG * H_IMG + W_IMG * H_IMG * 8
-    for key, p, metric in (("general_template_p1", 1.0, 0), ("general_template_p2", 2.0, 0),
-                           ("general_template_bhattacharyya", 1.0, 2)):
+    for key, p, metric in (("general_template_p1", 1.0, 0), ("general_template_intersection", 1.0, 1),
+                           ("general_template_p2", 2.0, 0), ("general_template_bhattacharyya", 1.0, 2),
+                           ("general_template_chisq", 1.0, 3)):
         profiling.reset()
         profiling.enable(True)
         ms_g = timer(lambda: P.build_and_match_map(frame, NBINS, None, KW, KH, p, metric, out=t, lmap=lmap,
