@@ -45,58 +45,142 @@ __global__ void fuse_kernel(FuseArgs a, int64_t n, double* __restrict__ out) {
 
 // ---------------------------------------------------------------- find_peaks
 
-constexpr int kPeakTile = 1024;   // pixels per compaction block (256 threads x 4)
 constexpr int kSortTile = 2048;   // keys per radix block (256 threads x 8)
 
-__global__ void smooth3_kernel(const double* __restrict__ map, int w, int h, double* __restrict__ s) {
-    const int64_t n = static_cast<int64_t>(w) * h;
-    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
-         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-        const int y = static_cast<int>(i / w), x = static_cast<int>(i % w);
-        double acc = 0.0;
-        int cnt = 0;
-        for (int dy = -1; dy <= 1; ++dy)
-            for (int dx = -1; dx <= 1; ++dx) {
-                const int nx = x + dx, ny = y + dy;
-                if (nx < 0 || ny < 0 || nx >= w || ny >= h) continue;
-                acc = __dadd_rn(acc, map[static_cast<int64_t>(ny) * w + nx]);
-                ++cnt;
-            }
-        s[i] = __ddiv_rn(acc, static_cast<double>(cnt));
-    }
+// RN(a / d) for d in {6, 9} (y = RN(1 / d)): q = a y, then one FMA correction with the exact
+// remainder (Markstein) — the correctly rounded quotient for |a| in [2^-1000, 2^1000] (checked
+// on 6e8 samples against IEEE division); zero, tiny, huge and non-finite `a` divide.
+__device__ __forceinline__ double div_small(double a, double d, double y) {
+    const double q = __dmul_rn(a, y);
+    const double aa = fabs(a);
+    if (aa == 0.0) return q;
+    if (!(aa >= 0x1p-1000 && aa <= 0x1p1000)) return __ddiv_rn(a, d);
+    return fma(fma(-q, d, a), y, q);
 }
 
-// likelihood.cpp:312-322 at (x, y): every in-bounds neighbour + 1e-9 below the value.
-__device__ __forceinline__ bool is_peak_xy(const double* s, int w, int h, int x, int y) {
-    const double* c = s + static_cast<int64_t>(y) * w + x;
-    const double v = *c;
-    if (x > 0 && y > 0 && x + 1 < w && y + 1 < h) {  // interior: no bounds checks
-        // the exact negation of the reference's rejection test `n + 1e-9 >= v`
-        // (likelihood.cpp:316), so NaN neighbours / centres behave as on the border
-        const double* up = c - w;
-        const double* dn = c + w;
-        return !(__dadd_rn(up[-1], 1e-9) >= v) && !(__dadd_rn(up[0], 1e-9) >= v) && !(__dadd_rn(up[1], 1e-9) >= v) &&
-               !(__dadd_rn(c[-1], 1e-9) >= v) && !(__dadd_rn(c[1], 1e-9) >= v) && !(__dadd_rn(dn[-1], 1e-9) >= v) &&
-               !(__dadd_rn(dn[0], 1e-9) >= v) && !(__dadd_rn(dn[1], 1e-9) >= v);
-    }
-    for (int dy = -1; dy <= 1; ++dy)
-        for (int dx = -1; dx <= 1; ++dx) {
-            if (dx == 0 && dy == 0) continue;
-            const int nx = x + dx, ny = y + dy;
-            if (nx < 0 || ny < 0 || nx >= w || ny >= h) continue;
-            if (__dadd_rn(s[static_cast<int64_t>(ny) * w + nx], 1e-9) >= v) return false;
-        }
-    return true;
-}
+// Smoothing and peak flags in one pass over the map (find_peaks / score_map front end):
+// per CTA a 64 x 32 tile, its raw map with a 2-cell halo and the smoothed map with a
+// 1-cell halo staged in shared memory; the smoothed tile is stored, and the peak flags
+// leave as one bit per pixel (mask[y][x / 32], bit x % 32, one warp ballot per word).
+// Same arithmetic as the reference (likelihood.cpp:288-322): in-image neighbours only,
+// row-major order, then / count; the exact negation of `n + 1e-9 >= v`.  Tiles whose halo
+// lies inside the map run without bounds checks.
+constexpr int kSmX = 64, kSmY = 32;
 
-__device__ __forceinline__ bool is_peak(const double* s, int w, int h, int64_t i) {
-    return is_peak_xy(s, w, h, static_cast<int>(i % w), static_cast<int>(i / w));
-}
-
-// Block-wide exclusive scan of one value per thread (256 threads); returns the total too.
-__device__ __forceinline__ uint32_t block_excl_scan(uint32_t v, uint32_t* total, uint32_t* wsum) {
+__global__ void __launch_bounds__(256) smooth_peaks_kernel(const double* __restrict__ map, int w, int h,
+                                                           double* __restrict__ s, uint32_t* __restrict__ mask,
+                                                           int mw) {
+    __shared__ double raw[kSmY + 4][kSmX + 4];
+    __shared__ double sm[kSmY + 2][kSmX + 2];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    uint32_t inc = v;
+    const int x0 = blockIdx.x * kSmX, y0 = blockIdx.y * kSmY;
+    const bool inner = x0 >= 2 && y0 >= 2 && x0 + kSmX + 2 <= w && y0 + kSmY + 2 <= h;
+    {   // warp = row, lane = column; every load of the thread in flight before the stores
+        constexpr int RR = (kSmY + 4 + 7) / 8, CC = (kSmX + 4 + 31) / 32;
+        double v[RR][CC];
+#pragma unroll
+        for (int k = 0; k < RR; ++k) {
+            const int r = warp + 8 * k, gy = y0 - 2 + r;
+            const double* row = map + static_cast<int64_t>(gy) * w;
+#pragma unroll
+            for (int j = 0; j < CC; ++j) {
+                const int c = lane + 32 * j, gx = x0 - 2 + c;
+                v[k][j] = (r < kSmY + 4 && c < kSmX + 4 && (inner || (gx >= 0 && gy >= 0 && gx < w && gy < h)))
+                              ? __ldg(row + gx)
+                              : 0.0;
+            }
+        }
+#pragma unroll
+        for (int k = 0; k < RR; ++k)
+#pragma unroll
+            for (int j = 0; j < CC; ++j)
+                if (warp + 8 * k < kSmY + 4 && lane + 32 * j < kSmX + 4) raw[warp + 8 * k][lane + 32 * j] = v[k][j];
+    }
+    __syncthreads();
+    constexpr double kInv9 = 1.0 / 9.0, kInv6 = 1.0 / 6.0;
+    for (int r = warp; r < kSmY + 2; r += 8)
+        for (int c = lane; c < kSmX + 2; c += 32) {
+            const int gy = y0 - 1 + r, gx = x0 - 1 + c;
+            double v = 0.0;
+            if (inner) {
+                double acc = raw[r][c];
+                acc = __dadd_rn(acc, raw[r][c + 1]);
+                acc = __dadd_rn(acc, raw[r][c + 2]);
+                acc = __dadd_rn(acc, raw[r + 1][c]);
+                acc = __dadd_rn(acc, raw[r + 1][c + 1]);
+                acc = __dadd_rn(acc, raw[r + 1][c + 2]);
+                acc = __dadd_rn(acc, raw[r + 2][c]);
+                acc = __dadd_rn(acc, raw[r + 2][c + 1]);
+                acc = __dadd_rn(acc, raw[r + 2][c + 2]);
+                v = div_small(acc, 9.0, kInv9);
+            } else if (gx >= 0 && gy >= 0 && gx < w && gy < h) {
+                double acc = 0.0;
+                int cnt = 0;
+#pragma unroll
+                for (int dy = -1; dy <= 1; ++dy)
+#pragma unroll
+                    for (int dx = -1; dx <= 1; ++dx) {
+                        const int nx = gx + dx, ny = gy + dy;
+                        if (nx < 0 || ny < 0 || nx >= w || ny >= h) continue;
+                        acc = __dadd_rn(acc, raw[r + 1 + dy][c + 1 + dx]);
+                        ++cnt;
+                    }
+                v = cnt == 9 ? div_small(acc, 9.0, kInv9)
+                             : (cnt == 6 ? div_small(acc, 6.0, kInv6) : __ddiv_rn(acc, static_cast<double>(cnt)));
+            }
+            sm[r][c] = v;
+        }
+    __syncthreads();
+    for (int r = warp; r < kSmY; r += 8) {
+        const int gy = y0 + r;
+#pragma unroll
+        for (int hw = 0; hw < kSmX / 32; ++hw) {  // a warp: one 32-column mask word
+            const int c = 32 * hw + lane, gx = x0 + c;
+            const bool in = inner || (gx < w && gy < h);
+            bool peak = false;
+            if (in) {
+                const double v = sm[r + 1][c + 1];
+                s[static_cast<int64_t>(gy) * w + gx] = v;
+                if (inner) {
+                    const double* u = &sm[r][c];
+                    const double* m = &sm[r + 1][c];
+                    const double* d = &sm[r + 2][c];
+                    peak = !(__dadd_rn(u[0], 1e-9) >= v) & !(__dadd_rn(u[1], 1e-9) >= v) &
+                           !(__dadd_rn(u[2], 1e-9) >= v) & !(__dadd_rn(m[0], 1e-9) >= v) &
+                           !(__dadd_rn(m[2], 1e-9) >= v) & !(__dadd_rn(d[0], 1e-9) >= v) &
+                           !(__dadd_rn(d[1], 1e-9) >= v) & !(__dadd_rn(d[2], 1e-9) >= v);
+                } else {
+                    peak = true;
+#pragma unroll
+                    for (int dy = -1; dy <= 1; ++dy)
+#pragma unroll
+                        for (int dx = -1; dx <= 1; ++dx) {
+                            if (dx == 0 && dy == 0) continue;
+                            const int nx = gx + dx, ny = gy + dy;
+                            if (nx < 0 || ny < 0 || nx >= w || ny >= h) continue;
+                            if (__dadd_rn(sm[r + 1 + dy][c + 1 + dx], 1e-9) >= v) peak = false;
+                        }
+                }
+            }
+            const uint32_t b = __ballot_sync(0xffffffffu, peak);
+            if (lane == 0 && gy < h && x0 + 32 * hw < w) mask[static_cast<int64_t>(gy) * mw + ((x0 >> 5) + hw)] = b;
+        }
+    }
+}
+
+__device__ __forceinline__ bool mask_bit(const uint32_t* mask, int mw, int x, int y) {
+    return (mask[static_cast<int64_t>(y) * mw + (x >> 5)] >> (x & 31)) & 1u;
+}
+
+// Exclusive prefix of the mask words' popcounts within runs of 1024 words (woff) and the
+// runs' totals (runtot; scanned afterwards by excl_scan_kernel).
+__global__ void __launch_bounds__(1024) mask_scan_kernel(const uint32_t* __restrict__ mask, int64_t nwords,
+                                                         uint32_t* __restrict__ woff, uint32_t* __restrict__ runtot) {
+    __shared__ uint32_t wsum[32];
+    const int64_t i = static_cast<int64_t>(blockIdx.x) * 1024 + threadIdx.x;
+    const uint32_t x = i < nwords ? static_cast<uint32_t>(__popc(mask[i])) : 0u;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    uint32_t inc = x;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
         const uint32_t t = __shfl_up_sync(0xffffffffu, inc, o);
@@ -104,33 +188,19 @@ __device__ __forceinline__ uint32_t block_excl_scan(uint32_t v, uint32_t* total,
     }
     if (lane == 31) wsum[warp] = inc;
     __syncthreads();
-    uint32_t off = 0, tot = 0;
-    for (int k = 0; k < 8; ++k) {
-        if (k < warp) off += wsum[k];
-        tot += wsum[k];
+    if (warp == 0) {
+        const uint32_t ws = wsum[lane];
+        uint32_t wi = ws;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t t = __shfl_up_sync(0xffffffffu, wi, o);
+            if (lane >= o) wi += t;
+        }
+        wsum[lane] = wi - ws;
+        if (lane == 31) runtot[blockIdx.x] = wi;
     }
     __syncthreads();
-    *total = tot;
-    return off + inc - v;
-}
-
-__global__ void __launch_bounds__(256) peak_count_kernel(const double* __restrict__ s, int w, int h,
-                                                         uint32_t* __restrict__ bcount) {
-    __shared__ uint32_t wsum[8];
-    const int64_t n = static_cast<int64_t>(w) * h;
-    const int64_t base = static_cast<int64_t>(blockIdx.x) * kPeakTile + 4 * threadIdx.x;
-    uint32_t c = 0;
-    int x = static_cast<int>(base % w), y = static_cast<int>(base / w);
-    for (int j = 0; j < 4; ++j) {
-        if (base + j < n && is_peak_xy(s, w, h, x, y)) ++c;
-        if (++x == w) {
-            x = 0;
-            ++y;
-        }
-    }
-    uint32_t tot;
-    block_excl_scan(c, &tot, wsum);
-    if (threadIdx.x == 0) bcount[blockIdx.x] = tot;
+    if (i < nwords) woff[i] = wsum[warp] + inc - x;
 }
 
 // Exclusive scan of n values in place (1024 threads, sequential chunks); CTA b scans the
@@ -181,40 +251,33 @@ __device__ __forceinline__ uint64_t desc_key(double h) {
     return ~asc;
 }
 
-// kminmax[0..1]: the smallest and largest key (atomics; the sort skips the digit passes
-// above the highest bit in which any two keys differ).
-__global__ void __launch_bounds__(256) peak_compact_kernel(const double* __restrict__ s, int w, int h,
-                                                           const uint32_t* __restrict__ boff,
-                                                           uint64_t* __restrict__ keys, uint32_t* __restrict__ idx,
-                                                           unsigned long long* __restrict__ kminmax, int64_t cap) {
-    __shared__ uint32_t wsum[8];
-    const int64_t n = static_cast<int64_t>(w) * h;
-    const int64_t base = static_cast<int64_t>(blockIdx.x) * kPeakTile + 4 * threadIdx.x;
-    bool f[4];
-    uint32_t c = 0;
-    int x = static_cast<int>(base % w), y = static_cast<int>(base / w);
-    for (int j = 0; j < 4; ++j) {
-        f[j] = base + j < n && is_peak_xy(s, w, h, x, y);
-        c += f[j];
-        if (++x == w) {
-            x = 0;
-            ++y;
-        }
-    }
-    uint32_t tot;
-    uint32_t pos = boff[blockIdx.x] + block_excl_scan(c, &tot, wsum);
+// Row-major compaction of the flagged peaks (thread per mask word), with the key range.
+__global__ void __launch_bounds__(256) peak_compact_mask_kernel(const double* __restrict__ s, int w, int mw,
+                                                                int64_t nwords, const uint32_t* __restrict__ mask,
+                                                                const uint32_t* __restrict__ woff,
+                                                                const uint32_t* __restrict__ runoff,
+                                                                uint64_t* __restrict__ keys, uint32_t* __restrict__ idx,
+                                                                unsigned long long* __restrict__ kminmax, int64_t cap) {
+    const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
     unsigned long long kmin = ~0ull, kmax = 0ull;
-    for (int j = 0; j < 4; ++j)
-        if (f[j]) {
-            const unsigned long long k = desc_key(s[base + j]);
+    if (i < nwords) {
+        uint32_t bits = mask[i];
+        uint32_t pos = woff[i] + runoff[i >> 10];
+        const int64_t y = i / mw, xb = (i % mw) * 32;
+        while (bits) {
+            const int b = __ffs(bits) - 1;
+            bits &= bits - 1;
+            const int64_t p = y * w + xb + b;
+            const unsigned long long k = desc_key(s[p]);
             if (pos < cap) {  // NaN maps can hold more peaks than the n / 4 + 2 of strict maxima
                 keys[pos] = k;
-                idx[pos] = static_cast<uint32_t>(base + j);
+                idx[pos] = static_cast<uint32_t>(p);
             }
             ++pos;
             kmin = k < kmin ? k : kmin;
             kmax = k > kmax ? k : kmax;
         }
+    }
 #pragma unroll
     for (int o = 16; o; o >>= 1) {
         const unsigned long long a = __shfl_xor_sync(0xffffffffu, kmin, o), b = __shfl_xor_sync(0xffffffffu, kmax, o);
@@ -296,29 +359,34 @@ __global__ void peak_gather_kernel(const uint32_t* __restrict__ idx, const doubl
 // peak with the smallest (descending-height key, index) — stable_sort keeps row-major
 // order among equal heights — and its rank is 1 + the number of peaks before it in that
 // order (or, with no peak in the rect, the peak count + 1).
-__global__ void rect_best_key_kernel(const double* __restrict__ s, int w, int h, int gx, int gy, int gw, int gh,
-                                     unsigned long long* __restrict__ best_key) {
+__global__ void rect_best_key_kernel(const double* __restrict__ s, const uint32_t* __restrict__ mask, int mw, int w,
+                                     int gx, int gy, int gw, int gh, unsigned long long* __restrict__ best_key) {
     const int64_t n = static_cast<int64_t>(gw) * gh;
     for (int64_t j = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; j < n;
          j += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-        const int64_t i = static_cast<int64_t>(gy + j / gw) * w + gx + j % gw;
-        if (is_peak(s, w, h, i)) atomicMin(best_key, static_cast<unsigned long long>(desc_key(s[i])));
+        const int x = gx + static_cast<int>(j % gw), y = gy + static_cast<int>(j / gw);
+        if (mask_bit(mask, mw, x, y))
+            atomicMin(best_key, static_cast<unsigned long long>(desc_key(s[static_cast<int64_t>(y) * w + x])));
     }
 }
 
-__global__ void rect_best_idx_kernel(const double* __restrict__ s, int w, int h, int gx, int gy, int gw, int gh,
-                                     const unsigned long long* __restrict__ best_key, unsigned* __restrict__ best_idx) {
+__global__ void rect_best_idx_kernel(const double* __restrict__ s, const uint32_t* __restrict__ mask, int mw, int w,
+                                     int gx, int gy, int gw, int gh, const unsigned long long* __restrict__ best_key,
+                                     unsigned* __restrict__ best_idx) {
     const int64_t n = static_cast<int64_t>(gw) * gh;
     const unsigned long long bk = *best_key;
     for (int64_t j = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; j < n;
          j += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-        const int64_t i = static_cast<int64_t>(gy + j / gw) * w + gx + j % gw;
-        if (desc_key(s[i]) == bk && is_peak(s, w, h, i)) atomicMin(best_idx, static_cast<unsigned>(i));
+        const int x = gx + static_cast<int>(j % gw), y = gy + static_cast<int>(j / gw);
+        const int64_t i = static_cast<int64_t>(y) * w + x;
+        if (mask_bit(mask, mw, x, y) && desc_key(s[i]) == bk) atomicMin(best_idx, static_cast<unsigned>(i));
     }
 }
 
-// found: count the peaks ordered before (best_key, best_idx); else count every peak.
-__global__ void __launch_bounds__(256) rank_count_kernel(const double* __restrict__ s, int w, int h,
+// found: count the peaks ordered before (best_key, best_idx); else count every peak
+// (thread per mask word: only the flagged pixels' heights are read).
+__global__ void __launch_bounds__(256) rank_count_kernel(const double* __restrict__ s, int w, int mw, int64_t nwords,
+                                                         const uint32_t* __restrict__ mask,
                                                          const unsigned* __restrict__ best_idx,
                                                          const unsigned long long* __restrict__ best_key,
                                                          unsigned long long* __restrict__ count) {
@@ -326,13 +394,22 @@ __global__ void __launch_bounds__(256) rank_count_kernel(const double* __restric
     const bool found = bi != 0xFFFFFFFFu;
     const unsigned long long bk = *best_key;
     unsigned c = 0;
-    for (int y = blockIdx.y; y < h; y += gridDim.y)
-        for (int x = blockIdx.x * blockDim.x + threadIdx.x; x < w; x += gridDim.x * blockDim.x) {
-            if (!is_peak_xy(s, w, h, x, y)) continue;
-            const int64_t i = static_cast<int64_t>(y) * w + x;
-            const unsigned long long k = desc_key(s[i]);
-            c += !found || k < bk || (k == bk && static_cast<unsigned>(i) < bi);
+    for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < nwords;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        uint32_t bits = mask[i];
+        if (!found) {
+            c += __popc(bits);
+            continue;
         }
+        const int64_t y = i / mw, xb = (i % mw) * 32;
+        while (bits) {
+            const int b = __ffs(bits) - 1;
+            bits &= bits - 1;
+            const int64_t p = y * w + xb + b;
+            const unsigned long long k = desc_key(s[p]);
+            c += k < bk || (k == bk && static_cast<unsigned>(p) < bi);
+        }
+    }
 #pragma unroll
     for (int o = 16; o; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
     if ((threadIdx.x & 31) == 0 && c) atomicAdd(count, static_cast<unsigned long long>(c));
@@ -419,7 +496,9 @@ int grid1(int64_t n) { return static_cast<int>(std::min<int64_t>(std::max<int64_
 
 struct PeakWs {
     double* s;
-    uint32_t* bcount;
+    uint32_t* mask;    // [h][mw] peak flags, mw = ceil(w / 32)
+    uint32_t* woff;    // per mask word: exclusive popcount prefix within its run of 1024 words
+    uint32_t* runoff;  // per run: exclusive prefix over the runs
     uint64_t* k[2];
     uint32_t* v[2];
     uint32_t* counts;
@@ -427,13 +506,17 @@ struct PeakWs {
     void* extra;        // stream-ordered overflow buffers (freed by the caller after use), or null
 };
 
+int64_t mask_words(int w, int h) { return static_cast<int64_t>(h) * ceil_div(w, 32); }
+
+// nblk_peak: runs of 1024 mask words
 size_t peak_ws_bytes(int w, int h, int64_t* nblk_peak, int64_t* nblk_sort) {
-    const int64_t n = static_cast<int64_t>(w) * h;
+    const int64_t n = static_cast<int64_t>(w) * h, nw = mask_words(w, h);
     const int64_t cap = n / 4 + 2;  // strict 8-neighbour maxima: at most one per 2 x 2 cell
-    *nblk_peak = ceil_div(n, kPeakTile);
+    *nblk_peak = ceil_div(nw, 1024);
     *nblk_sort = std::max<int64_t>(1, ceil_div(cap, kSortTile));
     auto r = [](int64_t b) { return static_cast<size_t>(round_up(b, 256)); };
-    return r(n * 8) + r(*nblk_peak * 4) + 2 * r(cap * 8) + 2 * r(cap * 4) + r(256 * *nblk_sort * 4) + r(16 + 1024 + 16);
+    return r(n * 8) + 2 * r(nw * 4) + r(*nblk_peak * 4) + 2 * r(cap * 8) + 2 * r(cap * 4) + r(256 * *nblk_sort * 4) +
+           r(16 + 1024 + 16);
 }
 
 PeakWs carve(void* ws, int w, int h) {
@@ -448,7 +531,9 @@ PeakWs carve(void* ws, int w, int h) {
     };
     PeakWs s;
     s.s = reinterpret_cast<double*>(take(n * 8));
-    s.bcount = reinterpret_cast<uint32_t*>(take(nbp * 4));
+    s.mask = reinterpret_cast<uint32_t*>(take(mask_words(w, h) * 4));
+    s.woff = reinterpret_cast<uint32_t*>(take(mask_words(w, h) * 4));
+    s.runoff = reinterpret_cast<uint32_t*>(take(nbp * 4));
     s.k[0] = reinterpret_cast<uint64_t*>(take(cap * 8));
     s.k[1] = reinterpret_cast<uint64_t*>(take(cap * 8));
     s.v[0] = reinterpret_cast<uint32_t*>(take(cap * 4));
@@ -466,15 +551,19 @@ spct_status sorted_peaks(const double* map, int w, int h, void* ws, size_t ws_by
     int64_t nbp, nbs;
     if (!ws || ws_bytes < peak_ws_bytes(w, h, &nbp, &nbs)) return contract("find_peaks: workspace too small");
     PeakWs P = carve(ws, w, h);
-    const int64_t n = static_cast<int64_t>(w) * h;
-    smooth3_kernel<<<grid1(n), 256, 0, st>>>(map, w, h, P.s);
-    peak_count_kernel<<<static_cast<unsigned>(nbp), 256, 0, st>>>(P.s, w, h, P.bcount);
-    excl_scan_kernel<<<1, 1024, 0, st>>>(P.bcount, nbp, P.scalars);
+    const int64_t n = static_cast<int64_t>(w) * h, nw = mask_words(w, h);
+    const int mw = static_cast<int>(ceil_div(w, 32));
+    smooth_peaks_kernel<<<dim3(static_cast<unsigned>(ceil_div(w, kSmX)), static_cast<unsigned>(ceil_div(h, kSmY))), 256,
+                          0, st>>>(map, w, h, P.s, P.mask, mw);
+    mask_scan_kernel<<<static_cast<unsigned>(nbp), 1024, 0, st>>>(P.mask, nw, P.woff, P.runoff);
+    excl_scan_kernel<<<1, 1024, 0, st>>>(P.runoff, nbp, P.scalars);
     unsigned long long* kminmax = reinterpret_cast<unsigned long long*>(P.scalars + 260);
     const unsigned long long init[2] = {~0ull, 0ull};
     cudaMemcpyAsync(kminmax, init, 16, cudaMemcpyHostToDevice, st);
     const int64_t cap = n / 4 + 2;
-    peak_compact_kernel<<<static_cast<unsigned>(nbp), 256, 0, st>>>(P.s, w, h, P.bcount, P.k[0], P.v[0], kminmax, cap);
+    const unsigned ncb = static_cast<unsigned>(ceil_div(nw, 256));  // one thread per mask word
+    peak_compact_mask_kernel<<<ncb, 256, 0, st>>>(P.s, w, mw, nw, P.mask, P.woff, P.runoff, P.k[0], P.v[0], kminmax,
+                                                  cap);
     if (auto e = launch_status("find_peaks compaction")) return e;
     uint32_t hdr[264];
     if (auto e = cuda_status(cudaMemcpyAsync(hdr, P.scalars, sizeof(hdr), cudaMemcpyDeviceToHost, st), "find_peaks count"))
@@ -495,7 +584,8 @@ spct_status sorted_peaks(const double* map, int w, int h, void* ws, size_t ws_by
         P.counts = reinterpret_cast<uint32_t*>(x + 2 * kb + 2 * vb);
         P.extra = x;
         cudaMemcpyAsync(kminmax, init, 16, cudaMemcpyHostToDevice, st);
-        peak_compact_kernel<<<static_cast<unsigned>(nbp), 256, 0, st>>>(P.s, w, h, P.bcount, P.k[0], P.v[0], kminmax, m);
+        peak_compact_mask_kernel<<<ncb, 256, 0, st>>>(P.s, w, mw, nw, P.mask, P.woff, P.runoff, P.k[0], P.v[0],
+                                                      kminmax, m);
         if (auto e = launch_status("find_peaks compaction")) return e;
         if (auto e = cuda_status(cudaMemcpyAsync(hdr, P.scalars, sizeof(hdr), cudaMemcpyDeviceToHost, st), "find_peaks"))
             return e;
@@ -612,13 +702,14 @@ extern "C" spct_status spct_cu_score_map(const double* map, int w, int h, int gx
     unsigned long long* cnt = reinterpret_cast<unsigned long long*>(P.scalars + 4);
     cudaMemsetAsync(P.scalars, 0xFF, 12, s);  // key and index: "none"
     cudaMemsetAsync(cnt, 0, 8, s);
-    smooth3_kernel<<<grid1(n), 256, 0, s>>>(map, w, h, P.s);
+    const int mw = static_cast<int>(ceil_div(w, 32));
+    const int64_t nw = mask_words(w, h);
+    smooth_peaks_kernel<<<dim3(static_cast<unsigned>(ceil_div(w, kSmX)), static_cast<unsigned>(ceil_div(h, kSmY))), 256,
+                          0, s>>>(map, w, h, P.s, P.mask, mw);
     const int64_t nr = static_cast<int64_t>(gw) * gh;
-    rect_best_key_kernel<<<grid1(nr), 256, 0, s>>>(P.s, w, h, gx, gy, gw, gh, bk);
-    rect_best_idx_kernel<<<grid1(nr), 256, 0, s>>>(P.s, w, h, gx, gy, gw, gh, bk, bi);
-    {
-        rank_count_kernel<<<grid2d(w, h), 256, 0, s>>>(P.s, w, h, bi, bk, cnt);
-    }
+    rect_best_key_kernel<<<grid1(nr), 256, 0, s>>>(P.s, P.mask, mw, w, gx, gy, gw, gh, bk);
+    rect_best_idx_kernel<<<grid1(nr), 256, 0, s>>>(P.s, P.mask, mw, w, gx, gy, gw, gh, bk, bi);
+    rank_count_kernel<<<grid1(nw), 256, 0, s>>>(P.s, w, mw, nw, P.mask, bi, bk, cnt);
     if (auto st = launch_status("score_map")) return st;
     unsigned long long c = 0;
     if (auto st = cuda_status(cudaMemcpyAsync(&c, cnt, 8, cudaMemcpyDeviceToHost, s), "score")) return st;
