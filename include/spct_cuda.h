@@ -299,6 +299,18 @@ spct_status spct_cu_ih_build_match_map(const spct_source* src, const spct_ih* ou
                                        int kw, int kh, double p, int metric, double* map,
                                        void* workspace, size_t workspace_bytes, void* stream);
 
+/* spct_cu_ih_build_match_map for n (1..8) sources of one shape — the feature channels of a
+ * tracking batch (reference: track_loop.cpp's per-channel likelihood fan-out, each channel
+ * build_integral_histogram + hist_distance_map): the carry tables and template preps of all
+ * channels are computed in one launch per kernel, then one sweep per channel.  outs[c]
+ * share width / height / bins and either all store their tensor or none; tmpls[c] and
+ * maps[c] are per-channel device pointers; each channel has its own workspace of
+ * workspace_bytes (spct_cu_ih_build_workspace of one channel). */
+spct_status spct_cu_ih_build_match_map_multi(int n, const spct_source* srcs, const spct_ih* outs,
+                                             const double* const* tmpls, int kw, int kh, double p, int metric,
+                                             double* const* maps, void* const* workspaces,
+                                             size_t workspace_bytes, void* stream);
+
 /* ----------------------------------------------------------------- bin-slab reduce over peer memory
  * (peer.cu).  The multi-GPU form of hist_distance_map (likelihood.cpp:193-225)
  * with the bins sharded across ranks: rank r passes a slot of the root's slot buffer

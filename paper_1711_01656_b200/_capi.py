@@ -77,6 +77,8 @@ SIGNATURES = {
     "spct_cu_fused_window_ok": (_i, [_i, _i]),
     "spct_cu_ih_build_match": (_i, [_src_p, _ih_p, _vp, _i, _i, _d, _i, _vp, _vp, _sz, _vp]),
     "spct_cu_ih_build_match_map": (_i, [_src_p, _ih_p, _vp, _i, _i, _d, _i, _vp, _vp, _sz, _vp]),
+    "spct_cu_ih_build_match_map_multi": (_i, [_i, _src_p, _ih_p, C.POINTER(_vp), _i, _i, _d, _i, C.POINTER(_vp),
+                                              C.POINTER(_vp), _sz, _vp]),
     "spct_cu_orientation_workspace": (_i, [_i, _i, C.POINTER(_sz)]),
     "spct_cu_orientation_bins": (_i, [_vp, _i64, _i, _i, _d, _i, _vp, _i64, _vp, _sz, _vp]),
     "spct_cu_ih_dump": (_i, [_ih_p, C.c_char_p, _i, _vp]),

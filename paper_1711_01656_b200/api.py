@@ -435,6 +435,31 @@ def build_and_match(frame, nbins: int, tmpl, kw: int, kh: int, p: float = 1.0, m
     return t, partial
 
 
+def build_and_match_map_multi(frames, nbins: int, tmpl_devs, kw: int, kh: int, p: float = 1.0,
+                              metric: int = A.METRIC_MINKOWSKI, *, outs, lmaps, stream=None):
+    """build_and_match_map for several same-shape sources (the channels of a tracking batch)
+    in one call: the carry tables and template preps of all of them in one launch per
+    kernel, then one sweep each (spct_cu_ih_build_match_map_multi).  ``tmpl_devs``,
+    ``outs`` and ``lmaps`` are per-source device templates, tensors and maps."""
+    n = len(frames)
+    srcs, keeps, need = (A.spct_source * n)(), [], 0
+    for i, f in enumerate(frames):
+        src, keep = frame_source(f, nbins)
+        srcs[i] = src
+        keeps.append(keep)
+        ws = C.c_size_t()
+        check(A.lib().spct_cu_ih_build_workspace(C.byref(src), outs[i].bin0, outs[i].bins, C.byref(ws)))
+        need = max(need, (ws.value + 255) // 256 * 256)
+    ihs = (A.spct_ih * n)(*[o.desc for o in outs])
+    wbuf = _WS.get(need * n, keeps[0][0].device, stream)
+    base = wbuf.data_ptr()
+    vp = C.c_void_p * n
+    check(A.lib().spct_cu_ih_build_match_map_multi(n, srcs, ihs, vp(*[t.data_ptr() for t in tmpl_devs]), kw, kh, p,
+                                                   metric, vp(*[m.data_ptr() for m in lmaps]),
+                                                   vp(*[base + i * need for i in range(n)]), need, _stream(stream)))
+    return outs, lmaps
+
+
 def build_and_match_map(frame, nbins: int, tmpl, kw: int, kh: int, p: float = 1.0,
                         metric: int = A.METRIC_MINKOWSKI, *, lo: float = 0.0, hi: float = 256.0,
                         out: IntegralHistogramTensor | None = None, lmap: torch.Tensor | None = None,

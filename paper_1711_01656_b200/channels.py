@@ -35,14 +35,15 @@ def likelihood_channels(r, g, b, nbins: int, templates: dict, kw: int, kh: int, 
     each channel to its normalised template histogram (nbins values); ``tensors`` /
     ``maps`` / ``tmpl_dev`` may hold preallocated per-channel outputs for a batch."""
     srcs = channel_sources(r, g, b, nbins, sigma, stream)
-    out = {}
-    for c in CHANNELS:
-        t = tensors.get(c) if tensors else None
-        m = maps.get(c) if maps else None
-        td = tmpl_dev.get(c) if tmpl_dev else None
-        _, out[c] = _api.build_and_match_map(srcs[c], nbins, None if td is not None else templates[c], kw, kh, p,
-                                             metric, out=t, lmap=m, tmpl_dev=td, stream=stream)
-    return out
+    dev = srcs["intensity"].device
+    h, w = srcs["intensity"].shape
+    ts = [tensors[c] if tensors else _api.IntegralHistogramTensor(w, h, nbins, device=dev) for c in CHANNELS]
+    ms = [maps[c] if maps else torch.empty((h, w), dtype=torch.float64, device=dev) for c in CHANNELS]
+    tds = [tmpl_dev[c] if tmpl_dev else _api._tmpl(templates[c], nbins, w, h, kw, kh, p) for c in CHANNELS]
+    # all five channels share one launch of each carry kernel and of the template prep
+    _api.build_and_match_map_multi([srcs[c] for c in CHANNELS], nbins, tds, kw, kh, p, metric, outs=ts, lmaps=ms,
+                                   stream=stream)
+    return dict(zip(CHANNELS, ms))
 
 
 class ChannelGraph:

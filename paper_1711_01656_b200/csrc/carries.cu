@@ -20,12 +20,30 @@ using namespace spct_dev;
 namespace spct_carry {
 
 constexpr int kTileBins = 128;
+using spct_impl::kMaxCarryCh;
+
+// The carry tables of up to kMaxCarryCh same-shape sources (the channels of a tracking
+// batch) in one launch of each kernel: grid.z (tiles) / grid.y (prefix) selects the source.
+struct CarryBatch {
+    QuantParams q[kMaxCarryCh];
+    uint8_t* R8[kMaxCarryCh];
+    uint16_t* C16[kMaxCarryCh];
+    uint32_t* T1[kMaxCarryCh];
+    uint16_t* S16[kMaxCarryCh];
+    uint16_t* Lt16[kMaxCarryCh];
+    int nchunk;  // 128-bin chunks per source (grid.z = sources x chunks)
+};
 
 template <bool G8>
-__global__ void __launch_bounds__(256) fcarry_tiles_kernel(QuantParams q, int bin0, int bins, int Lb, int nstrips,
-                                                           int nbands, int band_rows, int tb, int suf_row0,
-                                                           uint8_t* __restrict__ R8, uint16_t* __restrict__ C16,
-                                                           uint32_t* __restrict__ T1, uint16_t* __restrict__ S16) {
+__global__ void __launch_bounds__(256) fcarry_tiles_kernel(const __grid_constant__ CarryBatch cb, int bin0, int bins,
+                                                           int Lb, int nstrips, int nbands, int band_rows, int tb,
+                                                           int suf_row0) {
+    const int ch = blockIdx.z / cb.nchunk;
+    const QuantParams& q = cb.q[ch];
+    uint8_t* __restrict__ R8 = cb.R8[ch];
+    uint16_t* __restrict__ C16 = cb.C16[ch];
+    uint32_t* __restrict__ T1 = cb.T1[ch];
+    uint16_t* __restrict__ S16 = cb.S16[ch];
     // column counts as u16 pairs (a column's count within a band is < 2^16, as in C16):
     // word h * 32 + lane of a bin row holds strip columns 4 lane + 2h (low) and + 2h + 1
     // (high), i.e. already the C16 layout; half the shared memory of u32 counters, so a
@@ -34,7 +52,7 @@ __global__ void __launch_bounds__(256) fcarry_tiles_kernel(QuantParams q, int bi
     uint32_t* cnt = fsm;                     // [tb bins][64 words]
     uint32_t* rh = fsm + tb * kStrip / 2;    // [8 warps][128 bins]
     uint32_t* cs = rh + 8 * kTileBins;       // [tb bins][64 words]: window-start suffix counts
-    const int s = blockIdx.x, j = blockIdx.y, kc0 = blockIdx.z * kTileBins;
+    const int s = blockIdx.x, j = blockIdx.y, kc0 = (blockIdx.z % cb.nchunk) * kTileBins;
     const int kcn = min(kTileBins, Lb - kc0);
     const bool need_r = s + 1 < nstrips, need_c = j + 1 < nbands;
     const bool need_s = need_c && S16;
@@ -53,7 +71,9 @@ __global__ void __launch_bounds__(256) fcarry_tiles_kernel(QuantParams q, int bi
     uint32_t* rw = rh + warp * kTileBins;
     // column 4 lane + c of the strip is counted in word (c >> 1) * 32 + lane, half c & 1
     // (conflict-free atomics)
-    const bool wide = G8 && x + 3 < q.width &&
+    // 8-bit gray with the default range: four pixels per 32-bit load (per source: a batch
+    // may mix them with BinMaps)
+    const bool wide = G8 && q.kind == SPCT_SRC_GRAY_U8 && q.fast_u8 && x + 3 < q.width &&
                       ((reinterpret_cast<uintptr_t>(q.p0) + x) & 3) == 0 && (q.pitch & 3) == 0;
     auto bins4 = [&](int y, uint32_t w, int (&b)[4]) {
         if (wide) {
@@ -137,11 +157,13 @@ __global__ void __launch_bounds__(256) fcarry_tiles_kernel(QuantParams q, int bi
 // ... and blocks [nb_lt + nb_c, + Lb): the corner sums of one bin each (corner_block).
 __device__ void corner_block(int kl, int nstrips, int nbands, uint32_t* __restrict__ T1, uint32_t* tsm);
 
-__global__ void __launch_bounds__(256) fcarry_prefix_kernel(int H, int Lb, int Wp, int nstrips, int nbands, int nb_lt,
-                                                            int nb_c, const uint8_t* __restrict__ R8,
-                                                            uint16_t* __restrict__ Lt16, uint16_t* __restrict__ C16,
-                                                            uint32_t* __restrict__ A32) {
+__global__ void __launch_bounds__(256) fcarry_prefix_kernel(const __grid_constant__ CarryBatch cb, int H, int Lb, int Wp,
+                                                            int nstrips, int nbands, int nb_lt, int nb_c) {
     extern __shared__ uint32_t corner_sm[];
+    const uint8_t* __restrict__ R8 = cb.R8[blockIdx.y];
+    uint16_t* __restrict__ Lt16 = cb.Lt16[blockIdx.y];
+    uint16_t* __restrict__ C16 = cb.C16[blockIdx.y];
+    uint32_t* __restrict__ A32 = cb.T1[blockIdx.y];
     if (static_cast<int>(blockIdx.x) >= nb_lt + nb_c) {
         corner_block(static_cast<int>(blockIdx.x) - nb_lt - nb_c, nstrips, nbands, A32, corner_sm);
         return;
@@ -244,49 +266,66 @@ FusedCarryLayout fused_carry_layout(const BuildPlan& p, int height, bool window)
     return L;
 }
 
-spct_status build_fused_carries(const QuantParams& q, const spct_ih& out, const BuildPlan& p, void* workspace,
-                                size_t ws_bytes, cudaStream_t s, FusedCarries* fc, int kh) {
-    *fc = FusedCarries{};
+spct_status build_fused_carries_multi(int n, const QuantParams* qs, const spct_ih& out, const BuildPlan& p,
+                                      void* const* workspaces, size_t ws_bytes, cudaStream_t s, FusedCarries* fcs,
+                                      int kh) {
+    if (n < 1 || n > kMaxCarryCh) return contract("ih_build_match: 1 .. 8 sources per batch");
     const FusedCarryLayout L = fused_carry_layout(p, out.height, kh > 1);
-    if (L.total > 0 && (!workspace || ws_bytes < L.total))
-        return contract("ih_build_match: workspace too small (query spct_cu_ih_build_workspace)");
+    for (int c = 0; c < n; ++c) fcs[c] = FusedCarries{};
     if (L.total == 0) return SPCT_OK;
-    char* ws = static_cast<char*>(workspace);
-    uint8_t* R8 = L.r_bytes ? reinterpret_cast<uint8_t*>(ws + L.r_off) : nullptr;
-    uint16_t* Lt16 = L.lt_bytes ? reinterpret_cast<uint16_t*>(ws + L.lt_off) : nullptr;
-    uint16_t* C16 = L.c_bytes ? reinterpret_cast<uint16_t*>(ws + L.c_off) : nullptr;
-    uint32_t* A32 = L.a_bytes ? reinterpret_cast<uint32_t*>(ws + L.a_off) : nullptr;
-    uint16_t* S16 = L.s_bytes ? reinterpret_cast<uint16_t*>(ws + L.s_off) : nullptr;
+    CarryBatch cb{};
+    cb.nchunk = static_cast<int>(ceil_div(p.Lb, kTileBins));
+    bool g8 = false;  // some source is 8-bit gray: the kernel variant with the 4-pixel loads
+    for (int c = 0; c < n; ++c) {
+        if (!workspaces[c] || ws_bytes < L.total)
+            return contract("ih_build_match: workspace too small (query spct_cu_ih_build_workspace)");
+        char* ws = static_cast<char*>(workspaces[c]);
+        cb.q[c] = qs[c];
+        cb.R8[c] = L.r_bytes ? reinterpret_cast<uint8_t*>(ws + L.r_off) : nullptr;
+        cb.Lt16[c] = L.lt_bytes ? reinterpret_cast<uint16_t*>(ws + L.lt_off) : nullptr;
+        cb.C16[c] = L.c_bytes ? reinterpret_cast<uint16_t*>(ws + L.c_off) : nullptr;
+        cb.T1[c] = L.a_bytes ? reinterpret_cast<uint32_t*>(ws + L.a_off) : nullptr;
+        cb.S16[c] = L.s_bytes ? reinterpret_cast<uint16_t*>(ws + L.s_off) : nullptr;
+        g8 = g8 || (qs[c].kind == SPCT_SRC_GRAY_U8 && qs[c].fast_u8);
+    }
     // window-start rows in every band: [y0 + o, y1), o = (-(kh - 1)) mod band_rows
     const int suf_row0 = kh > 1 ? (p.band_rows - (kh - 1) % p.band_rows) % p.band_rows : 0;
     const int tb = std::min(p.Lb, kTileBins);
-    const size_t smem = (static_cast<size_t>(tb) * (kStrip / 2) * (S16 ? 2 : 1) + 8 * kTileBins) * 4;
+    const size_t smem = (static_cast<size_t>(tb) * (kStrip / 2) * (L.s_bytes ? 2 : 1) + 8 * kTileBins) * 4;
     ensure_smem(fcarry_tiles_kernel<true>, smem);
     ensure_smem(fcarry_tiles_kernel<false>, smem);
-    dim3 g(p.nstrips, p.nbands, static_cast<unsigned>(ceil_div(p.Lb, kTileBins)));
-    if (q.kind == SPCT_SRC_GRAY_U8 && q.fast_u8)
-        fcarry_tiles_kernel<true><<<g, 256, smem, s>>>(q, out.bin0, out.bins, p.Lb, p.nstrips, p.nbands, p.band_rows, tb,
-                                                        suf_row0, R8, C16, A32, S16);
+    dim3 g(p.nstrips, p.nbands, static_cast<unsigned>(cb.nchunk * n));
+    if (g8)
+        fcarry_tiles_kernel<true><<<g, 256, smem, s>>>(cb, out.bin0, out.bins, p.Lb, p.nstrips, p.nbands, p.band_rows, tb,
+                                                        suf_row0);
     else
-        fcarry_tiles_kernel<false><<<g, 256, smem, s>>>(q, out.bin0, out.bins, p.Lb, p.nstrips, p.nbands, p.band_rows,
-                                                         tb, suf_row0, R8, C16, A32, S16);
+        fcarry_tiles_kernel<false><<<g, 256, smem, s>>>(cb, out.bin0, out.bins, p.Lb, p.nstrips, p.nbands, p.band_rows,
+                                                         tb, suf_row0);
     if (auto st = launch_status("fcarry_tiles_kernel")) return st;
-    const int nb_lt = Lt16 ? static_cast<int>(ceil_div(static_cast<int64_t>(out.height) * (p.Lb / 4), 256)) : 0;
-    const int nb_c = C16 ? static_cast<int>(ceil_div(static_cast<int64_t>(p.Lb) * p.Wp / 4, 256)) : 0;
-    const int nb_a = A32 ? p.Lb : 0;
-    const size_t tsm = A32 ? static_cast<size_t>(p.nbands - 1) * p.nstrips * 4 : 0;
+    const int nb_lt = L.lt_bytes ? static_cast<int>(ceil_div(static_cast<int64_t>(out.height) * (p.Lb / 4), 256)) : 0;
+    const int nb_c = L.c_bytes ? static_cast<int>(ceil_div(static_cast<int64_t>(p.Lb) * p.Wp / 4, 256)) : 0;
+    const int nb_a = L.a_bytes ? p.Lb : 0;
+    const size_t tsm = L.a_bytes ? static_cast<size_t>(p.nbands - 1) * p.nstrips * 4 : 0;
     if (tsm > 200 * 1024) return contract("ih_build_match: image too large for the fused carry tables");
     if (nb_lt + nb_c + nb_a > 0) {
         ensure_smem(fcarry_prefix_kernel, tsm);
-        fcarry_prefix_kernel<<<nb_lt + nb_c + nb_a, 256, tsm, s>>>(out.height, p.Lb, p.Wp, p.nstrips, p.nbands, nb_lt,
-                                                                   nb_c, R8, Lt16, C16, A32);
+        fcarry_prefix_kernel<<<dim3(nb_lt + nb_c + nb_a, n), 256, tsm, s>>>(cb, out.height, p.Lb, p.Wp, p.nstrips,
+                                                                          p.nbands, nb_lt, nb_c);
         if (auto st = launch_status("fcarry_prefix_kernel")) return st;
     }
-    fc->Lt = Lt16;
-    fc->C = C16;
-    fc->A = A32;
-    fc->S = S16;
+    for (int c = 0; c < n; ++c) {
+        fcs[c].Lt = cb.Lt16[c];
+        fcs[c].C = cb.C16[c];
+        fcs[c].A = cb.T1[c];
+        fcs[c].S = cb.S16[c];
+    }
     return SPCT_OK;
+}
+
+spct_status build_fused_carries(const QuantParams& q, const spct_ih& out, const BuildPlan& p, void* workspace,
+                                size_t ws_bytes, cudaStream_t s, FusedCarries* fc, int kh) {
+    void* ws[1] = {workspace};
+    return build_fused_carries_multi(1, &q, out, p, ws, ws_bytes, s, fc, kh);
 }
 
 }  // namespace spct_impl

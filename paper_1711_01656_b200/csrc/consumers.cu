@@ -695,7 +695,6 @@ extern "C" spct_status spct_cu_score_map(const double* map, int w, int h, int gx
     if (!workspace || workspace_bytes < peak_ws_bytes(w, h, &nbp, &nbs)) return contract("find_peaks: workspace too small");
     cudaStream_t s = as_stream(stream);
     PeakWs P = carve(workspace, w, h);
-    const int64_t n = static_cast<int64_t>(w) * h;
     // scalars: [0..1] best key (u64), [2] best index, [4..5] count (u64)
     unsigned long long* bk = reinterpret_cast<unsigned long long*>(P.scalars);
     unsigned* bi = P.scalars + 2;

@@ -15,10 +15,26 @@ namespace spct_fused {
 // Layout (fused_prep_layout): [0] kind, [1 + k] floor(s_k) replicated in both u16 halves;
 // per 128-bin group sum floor(s_k) (int64) and sum r_k (double); r_k per bin (double);
 // the MODE 3 constants per bin (float4) and per 16-bin slab (double2), FusedParams::c3.
-__global__ void prep_kernel(const double* __restrict__ tmpl, int bin0, int bins, double T, int fast_metric,
-                            int frac_ok, int other_kind, uint32_t* __restrict__ prep, long long* __restrict__ S_group,
-                            double* __restrict__ Sr_group, double* __restrict__ rfrac, float4* __restrict__ c3,
-                            double2* __restrict__ c3slab, int ngroups) {
+// One CTA per source of a batch (PrepBatch, blockIdx.x).
+struct PrepBatch {
+    const double* tmpl[kMaxCarryCh];
+    uint32_t* prep[kMaxCarryCh];
+    long long* S_group[kMaxCarryCh];
+    double* Sr_group[kMaxCarryCh];
+    double* rfrac[kMaxCarryCh];
+    float4* c3[kMaxCarryCh];
+    double2* c3slab[kMaxCarryCh];
+};
+
+__global__ void prep_kernel(const __grid_constant__ PrepBatch pb, int bin0, int bins, double T, int fast_metric,
+                            int frac_ok, int other_kind, int ngroups) {
+    const double* __restrict__ tmpl = pb.tmpl[blockIdx.x];
+    uint32_t* __restrict__ prep = pb.prep[blockIdx.x];
+    long long* __restrict__ S_group = pb.S_group[blockIdx.x];
+    double* __restrict__ Sr_group = pb.Sr_group[blockIdx.x];
+    double* __restrict__ rfrac = pb.rfrac[blockIdx.x];
+    float4* __restrict__ c3 = pb.c3[blockIdx.x];
+    double2* __restrict__ c3slab = pb.c3slab[blockIdx.x];
     __shared__ int all_integral;
     if (threadIdx.x == 0) all_integral = 1;
     __syncthreads();
@@ -87,33 +103,58 @@ size_t fused_prep_bytes(int bins) { return fused_prep_layout(bins).total; }
 
 namespace spct_fused {
 
-// Shared body of spct_cu_ih_build_match (partial != null) and spct_cu_ih_build_match_map (map != null).
-spct_status build_match(const spct_source* src, const spct_ih* out, const double* tmpl, int kw, int kh, double p,
-                        int metric, double* partial, double* map, void* workspace, size_t workspace_bytes,
-                        void* stream) {
-    QuantParams q;
-    if (auto st = make_quant(src, &q)) return st;
-    if (auto st = check_ih(out)) return st;
-    if (out->width != src->width || out->height != src->height || out->nbins_total != src->nbins)
-        return contract("ih_build_match: tensor dims do not match the source");
-    if (auto st = check_carry_dims(out->width, out->height)) return st;
-    if (out->data && reinterpret_cast<uintptr_t>(out->data) % 16 != 0)
-        return contract("ih_build_match: tensor data must be 16-byte aligned");
-    if (!(p >= 1.0)) return contract("hist_distance_map: Minkowski order must be >= 1");
-    if (!(kw >= 1 && kh >= 1 && kw <= src->width && kh <= src->height))
-        return contract("hist_distance_map: kernel exceeds image");
-    if (metric < SPCT_METRIC_MINKOWSKI || metric > SPCT_METRIC_CHISQ) return contract("hist_match: unknown metric");
-    if (!tmpl || !(partial || map)) return contract("ih_build_match: null template or output");
-    if (map && (out->bin0 != 0 || out->bins != out->nbins_total))
-        return contract("ih_build_match_map: the slab must hold every bin (use the partial form for slabs)");
+// Shared body of spct_cu_ih_build_match (partial != null), spct_cu_ih_build_match_map (map
+// != null) and the batched spct_cu_ih_build_match_map_multi: n same-shape sources (one
+// tensor, template, output and workspace each) share one launch of each carry kernel and of
+// the template prep; the sweeps run per source.
+spct_status build_match(int n, const spct_source* srcs, const spct_ih* outs, const double* const* tmpls, int kw,
+                        int kh, double p, int metric, double* const* partials, double* const* maps,
+                        void* const* workspaces, size_t workspace_bytes, void* stream) {
+    if (n < 1 || n > kMaxCarryCh) return contract("ih_build_match_map_multi: 1 .. 8 sources");
+    QuantParams qs[kMaxCarryCh];
+    for (int c = 0; c < n; ++c) {
+        const spct_source* src = &srcs[c];
+        const spct_ih* out = &outs[c];
+        if (auto st = make_quant(src, &qs[c])) return st;
+        if (auto st = check_ih(out)) return st;
+        if (out->width != src->width || out->height != src->height || out->nbins_total != src->nbins)
+            return contract("ih_build_match: tensor dims do not match the source");
+        if (auto st = check_carry_dims(out->width, out->height)) return st;
+        if (out->data && reinterpret_cast<uintptr_t>(out->data) % 16 != 0)
+            return contract("ih_build_match: tensor data must be 16-byte aligned");
+        if (!(p >= 1.0)) return contract("hist_distance_map: Minkowski order must be >= 1");
+        if (!(kw >= 1 && kh >= 1 && kw <= src->width && kh <= src->height))
+            return contract("hist_distance_map: kernel exceeds image");
+        if (metric < SPCT_METRIC_MINKOWSKI || metric > SPCT_METRIC_CHISQ) return contract("hist_match: unknown metric");
+        if (!tmpls[c] || !((partials && partials[c]) || (maps && maps[c])))
+            return contract("ih_build_match: null template or output");
+        if (maps && (out->bin0 != 0 || out->bins != out->nbins_total))
+            return contract("ih_build_match_map: the slab must hold every bin (use the partial form for slabs)");
+        if (c > 0 && (out->width != outs[0].width || out->height != outs[0].height || out->bins != outs[0].bins ||
+                      out->bin0 != outs[0].bin0 || out->nbins_total != outs[0].nbins_total ||
+                      (out->data != nullptr) != (outs[0].data != nullptr)))
+            return contract("ih_build_match_map_multi: the sources must share one shape (and all store or none)");
+    }
+    const spct_ih* out = &outs[0];
     cudaStream_t s = as_stream(stream);
     const int64_t T = static_cast<int64_t>(kw) * kh;
     const bool fusable = spct_cu_fused_window_ok(kw, kh) != 0;
     const int ngroups = static_cast<int>(ceil_div(out->bins, kGroupBins));
-    double* group_part = nullptr;  // > 128 bins with a finished map: the earlier groups' partial sums
-    if (fusable && map && ngroups > 1) {
-        const size_t n = static_cast<size_t>(out->width - kw + 1) * (out->height - kh + 1);
-        if (auto st = cuda_status(malloc_async(&group_part, n * sizeof(double), s), "ih_build_match_map alloc"))
+    if (n > 1 && (!fusable || (maps && ngroups > 1))) {  // one source at a time
+        for (int c = 0; c < n; ++c) {
+            double* pc = partials ? partials[c] : nullptr;
+            double* mc = maps ? maps[c] : nullptr;
+            if (auto st = build_match(1, &srcs[c], &outs[c], &tmpls[c], kw, kh, p, metric, partials ? &pc : nullptr,
+                                      maps ? &mc : nullptr, &workspaces[c], workspace_bytes, stream))
+                return st;
+        }
+        return SPCT_OK;
+    }
+    double* const map0 = maps ? maps[0] : nullptr;
+    double* group_part = nullptr;  // > 128 bins with a finished map: the earlier groups' partial sums (n == 1)
+    if (fusable && map0 && ngroups > 1) {
+        const size_t nw = static_cast<size_t>(out->width - kw + 1) * (out->height - kh + 1);
+        if (auto st = cuda_status(malloc_async(&group_part, nw * sizeof(double), s), "ih_build_match_map alloc"))
             return st;
     }
     struct FreeAsync {
@@ -122,12 +163,11 @@ spct_status build_match(const spct_source* src, const spct_ih* out, const double
         ~FreeAsync() { if (p) cudaFreeAsync(p, s); }
     } free_part{group_part, s};
     if (!fusable) {
-        // two passes: window too large for the 16-bit running-histogram cells, or a
-        // finished map over more than one 128-bin group
+        // two passes: window too large for the 16-bit running-histogram cells (n == 1 here)
         if (!out->data) return contract("ih_build_match: this shape needs tensor storage (two-pass schedule)");
-        if (auto st = spct_cu_ih_build(src, out, workspace, workspace_bytes, stream)) return st;
-        if (map) return spct_cu_hist_match(out, tmpl, kw, kh, p, metric, map, stream);
-        return spct_cu_hist_partial(out, tmpl, kw, kh, p, metric, partial, 0, stream);
+        if (auto st = spct_cu_ih_build(&srcs[0], out, workspaces[0], workspace_bytes, stream)) return st;
+        if (map0) return spct_cu_hist_match(out, tmpls[0], kw, kh, p, metric, map0, stream);
+        return spct_cu_hist_partial(out, tmpls[0], kw, kh, p, metric, partials[0], 0, stream);
     }
     const BuildPlan bp = plan_fused_sweep(out->width, out->height, out->bins);
     // Band tops start their running column counts from the carry tables when that takes
@@ -140,18 +180,11 @@ spct_status build_match(const spct_source* src, const spct_ih* out, const double
     const int win_kh = (kh > 1 && out->bins < kGroupBins && table_rounds < preroll_rounds) ? kh : 0;
     const size_t carry_bytes = out->data ? fused_carry_layout(bp, out->height, win_kh > 1).total : 0;
     const size_t need = carry_bytes + fused_prep_bytes(out->bins);
-    if (!workspace || workspace_bytes < need) return contract("ih_build_match: workspace too small");
-    FusedCarries fc{};
-    char* ws = static_cast<char*>(workspace);
-    if (out->data) {
-        if (auto st = build_fused_carries(q, *out, bp, workspace, workspace_bytes, s, &fc, win_kh)) return st;
-        ws += carry_bytes;
-    }
-    const PrepLayout pl = fused_prep_layout(out->bins);
-    uint32_t* prep = reinterpret_cast<uint32_t*>(ws);
-    long long* Sg = reinterpret_cast<long long*>(ws + pl.S);
-    double* Sr = reinterpret_cast<double*>(ws + pl.Sr);
-    double* rfrac = reinterpret_cast<double*>(ws + pl.r);
+    for (int c = 0; c < n; ++c)
+        if (!workspaces[c] || workspace_bytes < need) return contract("ih_build_match: workspace too small");
+    FusedCarries fcs[kMaxCarryCh] = {};
+    if (out->data)
+        if (auto st = build_fused_carries_multi(n, qs, *out, bp, workspaces, workspace_bytes, s, fcs, win_kh)) return st;
     // integer paths: packed 16-bit window counts (kw * kh <= 24576, fused_kernel.cuh); the
     // fractional flags need every count <= 4096
     const int fast_metric = ((metric == SPCT_METRIC_MINKOWSKI && p == 1.0) || metric == SPCT_METRIC_INTERSECTION) &&
@@ -161,73 +194,89 @@ spct_status build_match(const spct_source* src, const spct_ih* out, const double
     const int f32_ok = (metric == SPCT_METRIC_MINKOWSKI && p == 2.0 && T <= 4096) ||
                        metric == SPCT_METRIC_BHATTACHARYYA || metric == SPCT_METRIC_CHISQ;
     const int path = fast_metric ? 1 : (f32_ok ? 3 : 0);
-    float4* c3 = reinterpret_cast<float4*>(ws + pl.c3);
-    double2* c3slab = reinterpret_cast<double2*>(ws + pl.c3slab);
-    prep_kernel<<<1, 256, 0, s>>>(tmpl, out->bin0, out->bins, static_cast<double>(T), fast_metric, frac_ok,
-                                  path == 3 ? 3 : 0, prep, Sg, Sr, rfrac, c3, c3slab, ngroups);
+    const PrepLayout pl = fused_prep_layout(out->bins);
+    PrepBatch pbt{};
+    for (int c = 0; c < n; ++c) {
+        char* ws = static_cast<char*>(workspaces[c]) + carry_bytes;
+        pbt.tmpl[c] = tmpls[c];
+        pbt.prep[c] = reinterpret_cast<uint32_t*>(ws);
+        pbt.S_group[c] = reinterpret_cast<long long*>(ws + pl.S);
+        pbt.Sr_group[c] = reinterpret_cast<double*>(ws + pl.Sr);
+        pbt.rfrac[c] = reinterpret_cast<double*>(ws + pl.r);
+        pbt.c3[c] = reinterpret_cast<float4*>(ws + pl.c3);
+        pbt.c3slab[c] = reinterpret_cast<double2*>(ws + pl.c3slab);
+    }
+    prep_kernel<<<n, 256, 0, s>>>(pbt, out->bin0, out->bins, static_cast<double>(T), fast_metric, frac_ok,
+                                  path == 3 ? 3 : 0, ngroups);
     if (auto st = launch_status("prep_kernel")) return st;
 
-    FusedParams f{};
-    f.kw = kw;
-    f.kh = kh;
-    f.nu = out->width - kw + 1;
-    f.nv = out->height - kh + 1;
-    f.metric = metric;
-    f.p = p;
-    f.inv_p = 1.0 / p;
-    f.dmax = std::pow(2.0, 1.0 / p);  // likelihood.cpp:208
-    {   // d / dmax == d * (1 / dmax) bit for bit when dmax is a power of two (p = 1: dmax = 2)
-        int e = 0;
-        f.inv_dmax = std::frexp(f.dmax, &e) == 0.5 ? 1.0 / f.dmax : 0.0;
-    }
-    f.p_kind = p == 1.0 ? 1 : (p == 2.0 ? 2 : 0);
-    f.fp_kind = metric == SPCT_METRIC_MINKOWSKI ? (f.p_kind == 1 ? 0 : (f.p_kind == 2 ? 1 : 2))
-                                                : (metric == SPCT_METRIC_INTERSECTION ? 3
-                                                   : (metric == SPCT_METRIC_BHATTACHARYYA ? 4 : 5));
-    f.T = static_cast<double>(T);
-    f.invT = 1.0 / f.T;
-    f.T_pow2 = (T & (T - 1)) == 0;
-    f.tmpl = tmpl;
-    f.prep = prep;
-    f.S_group = Sg;
-    f.Sr_group = Sr;
-    f.rfrac = rfrac;
-    f.frac = frac_ok;
-    f.path = path;
-    f.c3 = c3;
-    f.c3slab = c3slab;
-    f.partial = group_part ? group_part : partial;
-    f.map = group_part ? nullptr : map;
-    f.W = out->width;
-    f.H = out->height;
-    const PixelMode pm = make_pixel_mode(q, out->bin0);
-    for (int g = 0; g < ngroups; ++g) {
-        f.group0 = g * kGroupBins;
-        f.accumulate = g > 0;
-        // several groups into a finished map: groups accumulate into group_part, the last
-        // one adds its sums to it and writes the finished map (no finalise pass)
-        if (group_part && g == ngroups - 1) f.map = map;
-        dim3 grid(static_cast<unsigned>(ceil_div(bp.nstrips, S)), bp.nbands, 1);
-        const int prof = prof_begin(out->data ? "ih_sweep_match" : "sweep_match_nostore", s);
-        // the group is the whole histogram: window totals over its bins are kw * kh
-        const bool allb = out->bin0 == 0 && out->bins == out->nbins_total && ngroups == 1;
-        const int sk = (q.kind == SPCT_SRC_GRAY_U8 && q.fast_u8) ? 1 : (q.kind == SPCT_SRC_BINS_U16 ? 2 : 0);
-#define SPCT_LAUNCH(KW)                                                                                     \
-    if (S == 1) launch_##KW##_s1(allb, sk, grid, s, q, pm, *out, bp, fc, f);                                    \
-    else if (S == 2) launch_##KW##_s2(allb, sk, grid, s, q, pm, *out, bp, fc, f);                               \
-    else if (S == 4) launch_##KW##_s4(allb, sk, grid, s, q, pm, *out, bp, fc, f);                               \
-    else launch_##KW##_s8(allb, sk, grid, s, q, pm, *out, bp, fc, f);
-        if (kw == 64) {
-            SPCT_LAUNCH(kw64)
-        } else if (kw == 128) {
-            SPCT_LAUNCH(kw128)
-        } else {
-            SPCT_LAUNCH(kw_any)
+    for (int c = 0; c < n; ++c) {
+        FusedParams f{};
+        f.kw = kw;
+        f.kh = kh;
+        f.nu = out->width - kw + 1;
+        f.nv = out->height - kh + 1;
+        f.metric = metric;
+        f.p = p;
+        f.inv_p = 1.0 / p;
+        f.dmax = std::pow(2.0, 1.0 / p);  // likelihood.cpp:208
+        {   // d / dmax == d * (1 / dmax) bit for bit when dmax is a power of two (p = 1: dmax = 2)
+            int e = 0;
+            f.inv_dmax = std::frexp(f.dmax, &e) == 0.5 ? 1.0 / f.dmax : 0.0;
         }
+        f.p_kind = p == 1.0 ? 1 : (p == 2.0 ? 2 : 0);
+        f.fp_kind = metric == SPCT_METRIC_MINKOWSKI ? (f.p_kind == 1 ? 0 : (f.p_kind == 2 ? 1 : 2))
+                                                    : (metric == SPCT_METRIC_INTERSECTION ? 3
+                                                       : (metric == SPCT_METRIC_BHATTACHARYYA ? 4 : 5));
+        f.T = static_cast<double>(T);
+        f.invT = 1.0 / f.T;
+        f.T_pow2 = (T & (T - 1)) == 0;
+        f.tmpl = tmpls[c];
+        f.prep = pbt.prep[c];
+        f.S_group = pbt.S_group[c];
+        f.Sr_group = pbt.Sr_group[c];
+        f.rfrac = pbt.rfrac[c];
+        f.frac = frac_ok;
+        f.path = path;
+        f.c3 = pbt.c3[c];
+        f.c3slab = pbt.c3slab[c];
+        double* const mapc = maps ? maps[c] : nullptr;
+        f.partial = group_part ? group_part : (partials ? partials[c] : nullptr);
+        f.map = group_part ? nullptr : mapc;
+        f.W = out->width;
+        f.H = out->height;
+        const QuantParams& q = qs[c];
+        const FusedCarries& fc = fcs[c];
+        const spct_ih& oc = outs[c];
+        const PixelMode pm = make_pixel_mode(q, oc.bin0);
+        for (int g = 0; g < ngroups; ++g) {
+            f.group0 = g * kGroupBins;
+            f.accumulate = g > 0;
+            // several groups into a finished map: groups accumulate into group_part, the last
+            // one adds its sums to it and writes the finished map (no finalise pass)
+            if (group_part && g == ngroups - 1) f.map = mapc;
+            dim3 grid(static_cast<unsigned>(ceil_div(bp.nstrips, S)), bp.nbands, 1);
+            const int prof = prof_begin(oc.data ? "ih_sweep_match" : "sweep_match_nostore", s);
+            // the group is the whole histogram: window totals over its bins are kw * kh
+            const bool allb = oc.bin0 == 0 && oc.bins == oc.nbins_total && ngroups == 1;
+            const int sk = (q.kind == SPCT_SRC_GRAY_U8 && q.fast_u8) ? 1 : (q.kind == SPCT_SRC_BINS_U16 ? 2 : 0);
+#define SPCT_LAUNCH(KW)                                                                                     \
+    if (S == 1) launch_##KW##_s1(allb, sk, grid, s, q, pm, oc, bp, fc, f);                                      \
+    else if (S == 2) launch_##KW##_s2(allb, sk, grid, s, q, pm, oc, bp, fc, f);                                 \
+    else if (S == 4) launch_##KW##_s4(allb, sk, grid, s, q, pm, oc, bp, fc, f);                                 \
+    else launch_##KW##_s8(allb, sk, grid, s, q, pm, oc, bp, fc, f);
+            if (kw == 64) {
+                SPCT_LAUNCH(kw64)
+            } else if (kw == 128) {
+                SPCT_LAUNCH(kw128)
+            } else {
+                SPCT_LAUNCH(kw_any)
+            }
 #undef SPCT_LAUNCH
-        prof_end(prof, s);
-        note_launch();
-        if (auto st = launch_status("sweep_match_kernel")) return st;
+            prof_end(prof, s);
+            note_launch();
+            if (auto st = launch_status("sweep_match_kernel")) return st;
+        }
     }
     return SPCT_OK;
 }
@@ -243,13 +292,25 @@ extern "C" spct_status spct_cu_ih_build_match(const spct_source* src, const spct
                                               int kh, double p, int metric, double* partial, void* workspace,
                                               size_t workspace_bytes, void* stream) {
     if (!partial) return contract("ih_build_match: null partial");
-    return spct_fused::build_match(src, out, tmpl, kw, kh, p, metric, partial, nullptr, workspace, workspace_bytes,
-                                   stream);
+    if (!src || !out) return contract("ih_build_match: null argument");
+    return spct_fused::build_match(1, src, out, &tmpl, kw, kh, p, metric, &partial, nullptr, &workspace,
+                                   workspace_bytes, stream);
 }
 
 extern "C" spct_status spct_cu_ih_build_match_map(const spct_source* src, const spct_ih* out, const double* tmpl, int kw,
                                                   int kh, double p, int metric, double* map, void* workspace,
                                                   size_t workspace_bytes, void* stream) {
     if (!map) return contract("ih_build_match_map: null map");
-    return spct_fused::build_match(src, out, tmpl, kw, kh, p, metric, nullptr, map, workspace, workspace_bytes, stream);
+    if (!src || !out) return contract("ih_build_match_map: null argument");
+    return spct_fused::build_match(1, src, out, &tmpl, kw, kh, p, metric, nullptr, &map, &workspace, workspace_bytes,
+                                   stream);
+}
+
+extern "C" spct_status spct_cu_ih_build_match_map_multi(int n, const spct_source* srcs, const spct_ih* outs,
+                                                        const double* const* tmpls, int kw, int kh, double p, int metric,
+                                                        double* const* maps, void* const* workspaces,
+                                                        size_t workspace_bytes, void* stream) {
+    if (!srcs || !outs || !tmpls || !maps || !workspaces) return contract("ih_build_match_map_multi: null argument");
+    return spct_fused::build_match(n, srcs, outs, tmpls, kw, kh, p, metric, nullptr, maps, workspaces, workspace_bytes,
+                                   stream);
 }

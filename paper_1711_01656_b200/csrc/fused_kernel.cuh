@@ -753,10 +753,10 @@ __global__ void __launch_bounds__(256, 2) sweep_match_kernel(QuantParams q, Pixe
             // stays small
             auto rows = [&](auto fk_tag) {
                 constexpr int FK = decltype(fk_tag)::value;
-                const double invT = f.invT, pp = f.p;
-                int ai[4] = {0, 0, 0, 0};                   // MODE 3
-                float af[4] = {0.0f, 0.0f, 0.0f, 0.0f};
-                uint32_t cw[2] = {0u, 0u};                  // MODE 3, chi-square: packed window counts
+                [[maybe_unused]] const double invT = f.invT, pp = f.p;
+                [[maybe_unused]] int ai[4] = {0, 0, 0, 0};  // MODE 3
+                [[maybe_unused]] float af[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+                [[maybe_unused]] uint32_t cw[2] = {0u, 0u};  // MODE 3, chi-square: packed window counts
 #pragma unroll 1
                 for (int g = 0; g < kB / 4; ++g) {
                     uint32_t aw[4][2], bw[4][2];

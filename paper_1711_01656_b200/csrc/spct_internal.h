@@ -120,5 +120,10 @@ struct FusedCarryLayout {
 FusedCarryLayout fused_carry_layout(const BuildPlan& p, int height, bool window = false);
 spct_status build_fused_carries(const spct_dev::QuantParams& q, const spct_ih& out, const BuildPlan& p,
                                 void* workspace, size_t ws_bytes, cudaStream_t s, FusedCarries* fc, int kh = 0);
+// The same for n <= kMaxCarryCh same-shape sources (one workspace each) in one launch per kernel.
+constexpr int kMaxCarryCh = 8;
+spct_status build_fused_carries_multi(int n, const spct_dev::QuantParams* qs, const spct_ih& out, const BuildPlan& p,
+                                      void* const* workspaces, size_t ws_bytes, cudaStream_t s, FusedCarries* fcs,
+                                      int kh);
 
 }  // namespace spct_impl
