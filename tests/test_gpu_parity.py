@@ -795,3 +795,35 @@ def test_channel_graph_replays_exactly(P):
         want = P.likelihood_channels(r, gg, b, nbins, None, kw, kh, 1.0, tmpl_dev=tdev)
         for c in P.CHANNELS:
             assert torch.equal(got[c], want[c]), c
+
+
+@pytest.mark.parametrize("bins,p,metric,store", [(32, 1.0, 0, True), (48, 2.0, 0, False), (32, 1.0, 2, True),
+                                                  (200, 1.0, 0, True)])
+def test_build_match_map_multi_matches_single(P, bins, p, metric, store):
+    """spct_cu_ih_build_match_map_multi (batched carries / preps, per-source sweeps) equals
+    one spct_cu_ih_build_match_map per source: 8-bit frames beside a uint16 BinMap, a crop
+    template and a random one; above 128 bins the batch runs source by source."""
+    w, h, kw, kh = 300, 190, 64, 48
+    imgs = [oracle.smooth_image(w, h, 30 + i) for i in range(3)]
+    bm = oracle.random_binmap(w, h, bins, 77)
+    srcs = [torch.from_numpy(x).cuda() for x in imgs] + [torch.from_numpy(bm.astype(np.int16)).cuda()]
+    rng = np.random.default_rng(bins)
+    tm = [_crop_template(oracle.quantize(imgs[0], bins), bins, 40, 30, kw, kh), rng.random(bins) + 0.05,
+          _crop_template(oracle.quantize(imgs[2], bins), bins, 100, 60, kw, kh), rng.random(bins) + 0.05]
+    tm = [t / t.sum() for t in tm]
+    tds = [torch.from_numpy(t).cuda() for t in tm]
+    outs = [P.IntegralHistogramTensor(w, h, bins) for _ in srcs]
+    if not store:
+        for t in outs:
+            t.desc.data = None
+    maps = [torch.empty((h, w), dtype=torch.float64, device="cuda") for _ in srcs]
+    P.api.build_and_match_map_multi(srcs, bins, tds, kw, kh, p, metric, outs=outs, lmaps=maps)
+    for i, s in enumerate(srcs):
+        t1 = P.IntegralHistogramTensor(w, h, bins)
+        if not store:
+            t1.desc.data = None
+        _, m1 = P.build_and_match_map(s, bins, None, kw, kh, p, metric, out=t1, tmpl_dev=tds[i])
+        assert torch.equal(maps[i], m1), i
+        if store:
+            assert np.array_equal(outs[i].padded_u64(), t1.padded_u64()), i
+    assert close(maps[3].cpu().numpy(), oracle.hist_match_map_direct(bm, bins, tm[3], kw, kh, p, metric))
