@@ -68,7 +68,7 @@ def _ih_mismatches(t, qb, nbins, group=4):
         return sum(ex.map(one, range(0, nbins, group)))
 
 
-def _valid_grid(qb, nbins, tmpl, kw, kh, p):
+def _valid_grid(qb, nbins, tmpl, kw, kh, p, metric=0):
     """The reference's per-window values (the valid grid, nv x nu), computed by the oracle
     in window-row bands: band [v0, v1) needs bin-map rows [v0, v1 + kh - 1)."""
     h, w = qb.shape
@@ -79,7 +79,7 @@ def _valid_grid(qb, nbins, tmpl, kw, kh, p):
 
     def band(v0):
         v1 = min(nv, v0 + step)
-        m = oracle.hist_match_map_direct(qb[v0:v1 + kh - 1], nbins, tmpl, kw, kh, p)
+        m = oracle.hist_match_map_direct(qb[v0:v1 + kh - 1], nbins, tmpl, kw, kh, p, metric)
         grid[v0:v1] = m[cy:cy + v1 - v0, cx:cx + nu]
 
     with ThreadPoolExecutor(THREADS) as ex:
@@ -125,6 +125,20 @@ def test_c3_general_template_p2_every_window(P):
     tmpl = r / r.sum()
     _, lmap = P.build_and_match_map(torch.from_numpy(img).cuda(), nbins, tmpl, kw, kh, 2.0)
     want = _spread(_valid_grid(qb, nbins, tmpl, kw, kh, 2.0), side, side, kw, kh)
+    _compare_map(lmap.cpu().numpy(), want, exact=False)
+
+
+@pytest.mark.parametrize("p,metric", [(1.0, 0), (1.0, 1), (1.0, 2), (1.0, 3)])
+def test_c3_general_template_every_window(P, p, metric):
+    """A random normalised template at C3: the fractional-template integer path (p = 1,
+    intersection) and the integer / FP32 terms (Bhattacharyya, chi-square), every window."""
+    side, nbins, kw, kh = 4096, 128, 64, 64
+    img = _frame(side, 1)
+    qb = oracle.quantize(img, nbins)
+    r = np.random.default_rng(3).random(nbins) + 0.1
+    tmpl = r / r.sum()
+    _, lmap = P.build_and_match_map(torch.from_numpy(img).cuda(), nbins, tmpl, kw, kh, p, metric)
+    want = _spread(_valid_grid(qb, nbins, tmpl, kw, kh, p, metric), side, side, kw, kh)
     _compare_map(lmap.cpu().numpy(), want, exact=False)
 
 
