@@ -180,8 +180,26 @@ spct_status build_match(int n, const spct_source* srcs, const spct_ih* outs, con
     const int win_kh = (kh > 1 && out->bins < kGroupBins && table_rounds < preroll_rounds) ? kh : 0;
     const size_t carry_bytes = out->data ? fused_carry_layout(bp, out->height, win_kh > 1).total : 0;
     const size_t need = carry_bytes + fused_prep_bytes(out->bins);
-    for (int c = 0; c < n; ++c)
-        if (!workspaces[c] || workspace_bytes < need) return contract("ih_build_match: workspace too small");
+    for (int c = 0; c < n; ++c) {
+        const size_t gray = srcs[c].kind == SPCT_SRC_RGB_U8 ? fused_gray_bytes(&srcs[c]) : 0;
+        if (!workspaces[c] || workspace_bytes < need + gray) return contract("ih_build_match: workspace too small");
+        if (gray) {
+            // planar RGB: to_grayscale (imagecore.cpp:17-24) once into the workspace, then the
+            // 8-bit source path (prefetched staging, 4-pixel carry loads) — the same bins as
+            // the per-pixel conversion in the load stage, for 4 extra bytes per pixel
+            uint8_t* g = static_cast<uint8_t*>(workspaces[c]) + need;
+            const int64_t np = srcs[c].pitch * static_cast<int64_t>(srcs[c].height);
+            if (auto st = spct_cu_to_grayscale(static_cast<const uint8_t*>(srcs[c].plane[0]),
+                                               static_cast<const uint8_t*>(srcs[c].plane[1]),
+                                               static_cast<const uint8_t*>(srcs[c].plane[2]), np, g, stream))
+                return st;
+            spct_source gs = srcs[c];
+            gs.kind = SPCT_SRC_GRAY_U8;
+            gs.plane[0] = g;
+            gs.plane[1] = gs.plane[2] = nullptr;
+            if (auto st = make_quant(&gs, &qs[c])) return st;
+        }
+    }
     FusedCarries fcs[kMaxCarryCh] = {};
     if (out->data)
         if (auto st = build_fused_carries_multi(n, qs, *out, bp, workspaces, workspace_bytes, s, fcs, win_kh)) return st;

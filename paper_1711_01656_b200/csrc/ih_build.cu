@@ -351,7 +351,7 @@ extern "C" spct_status spct_cu_ih_build_workspace(const spct_source* src, int bi
     const BuildPlan p = plan_build_sweep(src->width, src->height, bins);
     const BuildPlan pf = plan_fused_sweep(src->width, src->height, bins);  // fused sweep: 16 bins per warp
     *bytes = std::max(fused_carry_layout(p, src->height).total, fused_carry_layout(pf, src->height, true).total) +
-             fused_prep_bytes(bins) + 256;
+             fused_prep_bytes(bins) + 256 + (src->kind == SPCT_SRC_RGB_U8 ? fused_gray_bytes(src) : 0);
     return SPCT_OK;
 }
 

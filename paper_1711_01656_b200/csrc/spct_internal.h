@@ -101,6 +101,10 @@ spct_status ih_recover_bins(const spct_ih& t, uint16_t* bins, int64_t bins_pitch
 
 // Workspace of the fused path's template prep (fused.cu).
 size_t fused_prep_bytes(int bins);
+// ... and of the gray frame an RGB source is converted to first (pitch x height bytes).
+inline size_t fused_gray_bytes(const spct_source* src) {
+    return static_cast<size_t>(round_up(src->pitch * static_cast<int64_t>(src->height), 256));
+}
 
 
 // Carry tables of the fused build+match sweep (carries.cu): row carries (u16), column
