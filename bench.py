@@ -469,8 +469,9 @@ def run_next_rows(P, dev, pk_gbs: float) -> dict:
     mb = P.motion.MedianBackgroundIH(fr[:5], 16, 7, 7)
     it = iter(range(10 ** 9))
     ms_sl = timed(lambda: mb.slide(fr[5 + next(it) % 3]))
-    out["median_slide"] = line(f"{n}x{n}, 16 bins, 5 frames: joint tensor += IH(new), -= IH(old)", ms_sl,
-                               2 * 2 * 16 * n * n * 4 + 2 * n * n)
+    out["median_slide"] = line(f"{n}x{n}, 16 bins, 5 frames: joint tensor += IH(new) - IH(old), one read-modify-"
+                               "write pass (algorithmic bytes: the joint tensor read + written once, two frames)", ms_sl,
+                               2 * 16 * n * n * 4 + 2 * n * n)
     ms_bg = timed(lambda: mb.background())
     out["median_background"] = line("7x7 windows, per-pixel CDF walk over 16 bins", ms_bg, 16 * n * n * 4 + n * n)
     return out

@@ -216,6 +216,15 @@ spct_status spct_cu_swlh_map_direct(const uint16_t* bins, int64_t pitch, int wid
  * median_background_sort (motion.cpp:103-118), frames a host array of nf device planes. */
 spct_status spct_cu_ih_accumulate(const spct_source* src, const spct_ih* acc, int sign, void* workspace,
                                   size_t workspace_bytes, void* stream);
+
+/* One slide of a joint integral histogram (reference motion.cpp:62-69, MedianBackgroundIH::
+ * slide): acc += IH(src_new) - IH(src_old) in ONE read-modify-write pass of acc (the two
+ * frames' carry tables in one launch each, their rows scanned side by side), instead of two
+ * spct_cu_ih_accumulate passes.  acc holds every bin of both sources.  Workspace:
+ * spct_cu_ih_slide_workspace. */
+spct_status spct_cu_ih_slide_workspace(int width, int height, int bins, size_t* bytes);
+spct_status spct_cu_ih_slide(const spct_source* src_new, const spct_source* src_old, const spct_ih* acc,
+                             void* workspace, size_t workspace_bytes, void* stream);
 spct_status spct_cu_median_background(const spct_ih* joint, int nframes, int m, int n, uint8_t* out, int64_t out_pitch,
                                       void* stream);
 spct_status spct_cu_median_sort(const uint8_t* const* frames, int nf, int width, int height, int64_t pitch,

@@ -98,6 +98,8 @@ SIGNATURES = {
     "spct_cu_swlh_brute": (_i, [_vp, _i64, _i, _i, _i, _i, _i, C.POINTER(C.c_int32), _i, _vp, _vp]),
     "spct_cu_swlh_map": (_i, [C.POINTER(spct_wih), _i, _i, _vp, _vp, _vp]),
     "spct_cu_ih_accumulate": (_i, [_src_p, _ih_p, _i, _vp, _sz, _vp]),
+    "spct_cu_ih_slide_workspace": (_i, [_i, _i, _i, C.POINTER(_sz)]),
+    "spct_cu_ih_slide": (_i, [_src_p, _src_p, _ih_p, _vp, _sz, _vp]),
     "spct_cu_median_background": (_i, [_ih_p, _i, _i, _i, _vp, _i64, _vp]),
     "spct_cu_median_sort": (_i, [C.POINTER(_vp), _i, _i, _i, _i64, _vp, _i64, _vp]),
     "spct_cu_peer_alloc": (_i, [_sz, C.POINTER(_vp), _vp]),

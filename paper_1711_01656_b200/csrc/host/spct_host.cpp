@@ -1047,8 +1047,8 @@ void FrameWindow::validate() const {  // motion.cpp:12-19
 
 struct MedianBackgroundIH::State {
     spct_ih joint{};
-    std::unique_ptr<DevBuf> mem, frame, ws;
-    std::size_t ws_bytes = 0;
+    std::unique_ptr<DevBuf> mem, frame, frame_old, ws, slide_ws;
+    std::size_t ws_bytes = 0, slide_ws_bytes = 0;
 };
 
 MedianBackgroundIH::~MedianBackgroundIH() = default;
@@ -1086,6 +1086,9 @@ MedianBackgroundIH::MedianBackgroundIH(const FrameWindow& window, int bins, int 
     s.nbins = bins_;
     check(spct_cu_ih_build_workspace(&s, 0, bins_, &st_->ws_bytes));
     st_->ws = std::make_unique<DevBuf>(st_->ws_bytes);
+    st_->frame_old = std::make_unique<DevBuf>(std::size_t(width_) * height_ * 2);
+    check(spct_cu_ih_slide_workspace(width_, height_, bins_, &st_->slide_ws_bytes));
+    st_->slide_ws = std::make_unique<DevBuf>(st_->slide_ws_bytes);
     for (const auto& f : window.frames) {
         add_frame(f, +1);
         frames_.push_back(f);
@@ -1109,8 +1112,23 @@ void MedianBackgroundIH::add_frame(const GrayImage& f, int sign) {  // motion.cp
 
 void MedianBackgroundIH::slide(const GrayImage& next) {  // motion.cpp:62-69
     require(next.width == width_ && next.height == height_, "median_background_ih: slide frame dimensions differ");
-    add_frame(next, +1);
-    add_frame(frames_.front(), -1);
+    for (auto v : next.data) require(v < bins_, "median_background_ih: frame value exceeds bin count");
+    // both frames' bins on the device, then J += IH(next) - IH(front) in one pass
+    // (the outgoing frame passed the same check when it entered)
+    upload(*st_->frame, std::vector<std::uint16_t>(next.data.begin(), next.data.end()));
+    const GrayImage& old = frames_.front();
+    upload(*st_->frame_old, std::vector<std::uint16_t>(old.data.begin(), old.data.end()));
+    spct_source sn{};
+    sn.kind = SPCT_SRC_BINS_U16;
+    sn.plane[0] = st_->frame->p;
+    sn.pitch = width_;
+    sn.width = width_;
+    sn.height = height_;
+    sn.nbins = bins_;
+    spct_source so = sn;
+    so.plane[0] = st_->frame_old->p;
+    check(spct_cu_ih_slide(&sn, &so, &st_->joint, st_->slide_ws->p, st_->slide_ws_bytes, nullptr));
+    cuda(cudaDeviceSynchronize(), "median_background_ih");  // the staging buffers are reused
     frames_.pop_front();
     frames_.push_back(next);
 }

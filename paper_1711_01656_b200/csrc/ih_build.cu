@@ -136,9 +136,52 @@ namespace spct_build {
 
 // ------------------------------------------------------------------ main sweep
 
+// MODE 3 (slide of a joint tensor, motion.cpp:62-69): one group of four planes of
+// J += IH(new) - IH(old) in one read-modify-write — V holds the difference of the two
+// frames' integral histograms (uint32 wrap arithmetic: J itself stays exact), the two
+// frames' rows scanned side by side (two independent shuffle chains).
+template <int B>
+__device__ __forceinline__ void vpart_group_slide(uint32_t (&V)[4][B], int g, const uint32_t (&tn)[4],
+                                                  const uint32_t (&to)[4], uint4 Ln, uint4 Lo, uint32_t* p,
+                                                  int64_t plane_pitch, uint32_t store_mask, const uint4* pre) {
+    uint32_t Qn[4], Qo[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+        const uint32_t mn = shl_clamp(1u, tn[j] - 32u * g), mo = shl_clamp(1u, to[j] - 32u * g);
+        Qn[j] = j ? Qn[j - 1] + mn : mn;
+        Qo[j] = j ? Qo[j - 1] + mo : mo;
+    }
+    uint32_t in = Qn[3], io = Qo[3];
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        in = scan_add(in, o);
+        io = scan_add(io, o);
+    }
+    const uint32_t en = in - Qn[3], eo = io - Qo[3];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+        Qn[j] += en;
+        Qo[j] += eo;
+    }
+    const uint32_t Ld[4] = {Ln.x - Lo.x, Ln.y - Lo.y, Ln.z - Lo.z, Ln.w - Lo.w};
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        const int k = 4 * g + i;
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+            V[j][k] += Ld[i] + __byte_perm(Qn[j], 0, 0x4440 + i) - __byte_perm(Qo[j], 0, 0x4440 + i);
+        if (store_mask & (1u << k)) {
+            const uint4 o = pre[i];
+            *reinterpret_cast<uint4*>(p) = make_uint4(o.x + V[0][k], o.y + V[1][k], o.z + V[2][k], o.w + V[3][k]);
+        }
+        p += plane_pitch;
+    }
+}
+
 template <int B, bool GUARD, int MODE>
 __global__ void __launch_bounds__(256) ih_sweep_kernel(QuantParams q, PixelMode pm, spct_ih out, int Lb, int Wp,
-                                                       int band_rows, int warps_per_cta, FusedCarries fc) {
+                                                       int band_rows, int warps_per_cta, FusedCarries fc,
+                                                       QuantParams q2 = {}, PixelMode pm2 = {}, FusedCarries fc2 = {}) {
     const int lane = lane_id();
     const int warp = threadIdx.x >> 5;
     const int strip = blockIdx.x;
@@ -157,10 +200,23 @@ __global__ void __launch_bounds__(256) ih_sweep_kernel(QuantParams q, PixelMode 
 
     uint32_t V[4][B];
     vpart_init_ca<B>(V, fc.C, fc.A, band, strip, gridDim.y, gridDim.x, Lb, Wp, kl0, x0);
+    if (MODE == 3) {  // the difference of the two frames' band-top rows
+        uint32_t Vo[4][B];
+        vpart_init_ca<B>(Vo, fc2.C, fc2.A, band, strip, gridDim.y, gridDim.x, Lb, Wp, kl0, x0);
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+#pragma unroll
+            for (int k = 0; k < B; ++k) V[j][k] -= Vo[j][k];
+    }
     uint32_t* base_ptr = out.data + static_cast<int64_t>(kl0) * out.plane_pitch + x0;
     LtRows<B> lt{(fc.Lt && strip > 0) ? fc.Lt + (static_cast<int64_t>(strip) * out.height + y0) * Lb + kl0 : nullptr,
                  Lb, y1 - y0};
     lt.start();
+    LtRows<B> lt2{(MODE == 3 && fc2.Lt && strip > 0) ? fc2.Lt + (static_cast<int64_t>(strip) * out.height + y0) * Lb + kl0
+                                                    : nullptr,
+                  Lb, y1 - y0};
+    if (MODE == 3) lt2.start();
+    const uint32_t kpat2 = (MODE == 3 && pm2.byte_mode) ? 0x01010101u * static_cast<uint32_t>(k0) : 0u;
 
     // accumulate modes read-modify-write the tensor: its cells of row y + 1 are loaded
     // during row y (B x 16 bytes per lane; only the B <= 8 plans use these modes cheaply)
@@ -176,9 +232,15 @@ __global__ void __launch_bounds__(256) ih_sweep_kernel(QuantParams q, PixelMode 
     if (MODE != 0 && y0 < y1) load_row(y0, pnx);
 
     uint32_t nxt = load_bins4_raw(q, pm, x0, y0, k0, B);
+    uint32_t nxt2 = MODE == 3 ? load_bins4_raw(q2, pm2, x0, y0, k0, B) : 0u;
     for (int y = y0; y < y1; ++y) {
         const uint32_t cur = decode_bins4(pm, nxt);
         if (y + 1 < y1) nxt = load_bins4_raw(q, pm, x0, y + 1, k0, B);
+        uint32_t cur2 = 0;
+        if (MODE == 3) {
+            cur2 = decode_bins4(pm2, nxt2);
+            if (y + 1 < y1) nxt2 = load_bins4_raw(q2, pm2, x0, y + 1, k0, B);
+        }
         if (MODE != 0) {
 #pragma unroll
             for (int k = 0; k < NPRE; ++k) pre[k] = pnx[k];
@@ -188,10 +250,21 @@ __global__ void __launch_bounds__(256) ih_sweep_kernel(QuantParams q, PixelMode 
         onehot_shifts(cur ^ kpat0, t4);
         lt.row(y - y0);
         uint32_t* prow = base_ptr + static_cast<int64_t>(y) * out.row_pitch;
+        if constexpr (MODE == 3) {
+            uint32_t t4o[4];
+            onehot_shifts(cur2 ^ kpat2, t4o);
+            lt2.row(y - y0);
 #pragma unroll
-        for (int g = 0; g < B / 4; ++g)
-            vpart_group_q<B, MODE>(V, g, t4, lt.group(y - y0, g), prow + static_cast<int64_t>(4 * g) * out.plane_pitch,
-                                   out.plane_pitch, store_mask, MODE != 0 ? pre + 4 * g : nullptr);
+            for (int g = 0; g < B / 4; ++g)
+                vpart_group_slide<B>(V, g, t4, t4o, lt.group(y - y0, g), lt2.group(y - y0, g),
+                                     prow + static_cast<int64_t>(4 * g) * out.plane_pitch, out.plane_pitch, store_mask,
+                                     pre + 4 * g);
+        } else {
+#pragma unroll
+            for (int g = 0; g < B / 4; ++g)
+                vpart_group_q<B, MODE>(V, g, t4, lt.group(y - y0, g), prow + static_cast<int64_t>(4 * g) * out.plane_pitch,
+                                       out.plane_pitch, store_mask, MODE != 0 ? pre + 4 * g : nullptr);
+        }
     }
 }
 
@@ -360,12 +433,14 @@ namespace {
 
 template <int MODE>
 void launch_sweep(const BuildPlan& p, dim3 grid, int threads, cudaStream_t s, const QuantParams& q, const PixelMode& pm,
-                  const spct_ih& out, const FusedCarries& fc) {
+                  const spct_ih& out, const FusedCarries& fc, const QuantParams& q2 = {}, const PixelMode& pm2 = {},
+                  const FusedCarries& fc2 = {}) {
     switch (p.B) {
 #define SPCT_SWEEP(BB)                                                                                               \
-    ih_sweep_kernel<BB, false, MODE><<<grid, threads, 0, s>>>(q, pm, out, p.Lb, p.Wp, p.band_rows, p.warps, fc);     \
+    ih_sweep_kernel<BB, false, MODE><<<grid, threads, 0, s>>>(q, pm, out, p.Lb, p.Wp, p.band_rows, p.warps, fc, q2,  \
+                                                              pm2, fc2);                                             \
     if (out.bins % BB) ih_sweep_kernel<BB, true, MODE><<<grid, threads, 0, s>>>(q, pm, out, p.Lb, p.Wp, p.band_rows, \
-                                                                                p.warps, fc);
+                                                                                p.warps, fc, q2, pm2, fc2);
         case 4: SPCT_SWEEP(4) break;
         case 8: SPCT_SWEEP(8) break;
         default: SPCT_SWEEP(16) break;
@@ -403,6 +478,51 @@ spct_status build_mode(const spct_source* src, const spct_ih* out, void* workspa
 extern "C" spct_status spct_cu_ih_build(const spct_source* src, const spct_ih* out, void* workspace,
                                         size_t workspace_bytes, void* stream) {
     return build_mode(src, out, workspace, workspace_bytes, stream, 0);
+}
+
+namespace {
+// slide plans keep B <= 8 bins per warp (V and the read-ahead tensor row cost 8 B registers)
+BuildPlan plan_slide(int width, int height, int bins) {
+    return plan_build(width, height, bins, bins >= 32 ? 8 : 4, 2, 32);
+}
+size_t slide_half_bytes(const BuildPlan& p, int height) {
+    return static_cast<size_t>(round_up(static_cast<int64_t>(fused_carry_layout(p, height).total), 256));
+}
+}  // namespace
+
+extern "C" spct_status spct_cu_ih_slide_workspace(int width, int height, int bins, size_t* bytes) {
+    if (!bytes) return contract("ih_slide_workspace: null argument");
+    if (!(width > 0 && height > 0 && bins >= 1)) return contract("build: empty bin map");
+    *bytes = 2 * slide_half_bytes(plan_slide(width, height, bins), height) + 256;
+    return SPCT_OK;
+}
+
+extern "C" spct_status spct_cu_ih_slide(const spct_source* src_new, const spct_source* src_old, const spct_ih* acc,
+                                        void* workspace, size_t workspace_bytes, void* stream) {
+    QuantParams q[2];
+    if (!src_new || !src_old) return contract("ih_slide: null source");
+    if (auto st = make_quant(src_new, &q[0])) return st;
+    if (auto st = make_quant(src_old, &q[1])) return st;
+    if (auto st = check_ih(acc)) return st;
+    if (!acc->data) return contract("ih_build: null tensor data");
+    if (auto st = check_carry_dims(acc->width, acc->height)) return st;
+    for (const spct_source* src : {src_new, src_old})
+        if (acc->width != src->width || acc->height != src->height || acc->nbins_total != src->nbins)
+            return contract("ih_build: tensor dims do not match the source");
+    if (reinterpret_cast<uintptr_t>(acc->data) % 16 != 0) return contract("ih_build: tensor data must be 16-byte aligned");
+    const BuildPlan p = plan_slide(acc->width, acc->height, acc->bins);
+    const size_t half = slide_half_bytes(p, acc->height);
+    if (!workspace || workspace_bytes < 2 * half) return contract("ih_slide: workspace too small (spct_cu_ih_slide_workspace)");
+    cudaStream_t s = as_stream(stream);
+    void* ws[2] = {workspace, static_cast<char*>(workspace) + half};
+    FusedCarries fc[2] = {};
+    if (auto st = build_fused_carries_multi(2, q, *acc, p, ws, half, s, fc, 0)) return st;
+    dim3 grid(p.nstrips, p.nbands, p.slab_groups);
+    const int prof = prof_begin("ih_slide", s);
+    const PixelMode pm0 = make_pixel_mode(q[0], acc->bin0), pm1 = make_pixel_mode(q[1], acc->bin0);
+    launch_sweep<3>(p, grid, 32 * p.warps, s, q[0], pm0, *acc, fc[0], q[1], pm1, fc[1]);
+    prof_end(prof, s);
+    return launch_status("ih_sweep_kernel");
 }
 
 extern "C" spct_status spct_cu_ih_accumulate(const spct_source* src, const spct_ih* acc, int sign, void* workspace,

@@ -70,12 +70,23 @@ class MedianBackgroundIH:
                                             _stream(self.stream)))
 
     def slide(self, nxt) -> None:
+        """motion.cpp:62-69: J += IH(next) - IH(oldest) in one read-modify-write pass of J
+        (spct_cu_ih_slide) instead of an add and a subtract pass."""
         f = _dev(nxt, torch.uint8)
         if tuple(f.shape) != (self.height, self.width):
             raise ContractError(A.SPCT_ERR_CONTRACT, "median_background_ih: slide frame dimensions differ")
-        self._add(f, +1)
+        if int(f.max().item()) >= self.bins:  # motion.cpp:23-26
+            raise ContractError(A.SPCT_ERR_CONTRACT, "median_background_ih: frame value exceeds bin count")
         # the outgoing frame passed the same check when it entered (motion.cpp:64-65 repeats it)
-        self._add(self.frames.popleft(), -1, validate=False)
+        old = self.frames.popleft()
+        bn, bo = f.to(torch.int16), old.to(torch.int16)  # the frames' values are their bins (motion.cpp:53-54)
+        sn = _source(A.SRC_BINS_U16, [bn], self.width, self.height, self.bins)
+        so = _source(A.SRC_BINS_U16, [bo], self.width, self.height, self.bins)
+        ws = C.c_size_t()
+        check(A.lib().spct_cu_ih_slide_workspace(self.width, self.height, self.bins, C.byref(ws)))
+        wb = _WS.get(ws.value, bn.device, self.stream)
+        check(A.lib().spct_cu_ih_slide(C.byref(sn), C.byref(so), C.byref(self.joint.desc), _ptr(wb), wb.numel(),
+                                       _stream(self.stream)))
         self.frames.append(f)
 
     def background(self) -> torch.Tensor:
