@@ -277,6 +277,51 @@ __global__ void gray_kernel(const uint8_t* __restrict__ r, const uint8_t* __rest
         out[i] = static_cast<uint8_t>(gray_of(r[i], g[i], b[i]));
 }
 
+// 16 pixels per thread (every plane and the output 16-byte aligned): 16-byte loads and
+// stores, the division by 3 as a multiply-shift (exact for sums <= 766).
+__device__ __forceinline__ uint32_t gray4(uint32_t r, uint32_t g, uint32_t b) {
+    uint32_t o = 0;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+        const uint32_t s = ((r >> (8 * j)) & 0xFFu) + ((g >> (8 * j)) & 0xFFu) + ((b >> (8 * j)) & 0xFFu) + 1u;
+        o |= ((s * 0xAAABu) >> 17) << (8 * j);  // s / 3 for s < 2^15
+    }
+    return o;
+}
+
+__global__ void gray16_kernel(const uint4* __restrict__ r, const uint4* __restrict__ g, const uint4* __restrict__ b,
+                              int64_t n16, uint4* __restrict__ out) {
+    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n16;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const uint4 x = __ldg(r + i), y = __ldg(g + i), z = __ldg(b + i);
+        out[i] = make_uint4(gray4(x.x, y.x, z.x), gray4(x.y, y.y, z.y), gray4(x.z, y.z, z.z), gray4(x.w, y.w, z.w));
+    }
+}
+
+// quantize of an 8-bit gray frame with the default range (bin = v * nbins >> 8), 16 pixels
+// per thread on 16-byte aligned rows: one 16-byte load, two 16-byte stores.
+__global__ void quantize16_kernel(const uint8_t* __restrict__ src, int64_t pitch, int w, int h, uint32_t nbins,
+                                  uint16_t* __restrict__ out) {
+    const int per_row = w / 16;
+    const int64_t n = static_cast<int64_t>(per_row) * h;
+    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int y = static_cast<int>(i / per_row), c = static_cast<int>(i % per_row);
+        const uint4 v = __ldg(reinterpret_cast<const uint4*>(src + static_cast<int64_t>(y) * pitch) + c);
+        const uint32_t wv[4] = {v.x, v.y, v.z, v.w};
+        uint32_t o[8];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const uint32_t a = wv[j];
+            o[2 * j] = (((a & 0xFFu) * nbins) >> 8) | ((((a >> 8) & 0xFFu) * nbins) >> 8) << 16;
+            o[2 * j + 1] = ((((a >> 16) & 0xFFu) * nbins) >> 8) | (((a >> 24) * nbins) >> 8) << 16;
+        }
+        uint4* d = reinterpret_cast<uint4*>(out + static_cast<int64_t>(y) * w) + 2 * c;
+        d[0] = make_uint4(o[0], o[1], o[2], o[3]);
+        d[1] = make_uint4(o[4], o[5], o[6], o[7]);
+    }
+}
+
 __global__ void quantize_kernel(QuantParams q, uint16_t* __restrict__ out) {
     const int64_t n = static_cast<int64_t>(q.width) * q.height;
     for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
@@ -371,7 +416,16 @@ extern "C" spct_status spct_cu_to_grayscale(const uint8_t* r, const uint8_t* g, 
     if (n < 0) return contract("to_grayscale: negative size");
     if (n == 0) return SPCT_OK;
     if (!r || !g || !b || !out) return contract("to_grayscale: null plane");
-    gray_kernel<<<grid_for(n, 256), 256, 0, as_stream(stream)>>>(r, g, b, n, out);
+    cudaStream_t s = as_stream(stream);
+    const bool vec = ((reinterpret_cast<uintptr_t>(r) | reinterpret_cast<uintptr_t>(g) | reinterpret_cast<uintptr_t>(b) |
+                       reinterpret_cast<uintptr_t>(out)) & 15) == 0;
+    const int64_t n16 = vec ? n / 16 : 0;
+    if (n16 > 0)
+        gray16_kernel<<<grid_for(n16, 256), 256, 0, s>>>(reinterpret_cast<const uint4*>(r), reinterpret_cast<const uint4*>(g),
+                                                         reinterpret_cast<const uint4*>(b), n16, reinterpret_cast<uint4*>(out));
+    if (n > 16 * n16)
+        gray_kernel<<<grid_for(n - 16 * n16, 256), 256, 0, s>>>(r + 16 * n16, g + 16 * n16, b + 16 * n16, n - 16 * n16,
+                                                                out + 16 * n16);
     return launch_status("to_grayscale");
 }
 
@@ -382,6 +436,12 @@ extern "C" spct_status spct_cu_quantize(const spct_source* src, uint16_t* out, v
     if (auto st = make_quant(src, &q)) return st;
     if (!out) return contract("quantize: null output");
     const int64_t n = static_cast<int64_t>(q.width) * q.height;
+    if (q.kind == SPCT_SRC_GRAY_U8 && q.fast_u8 && q.width % 16 == 0 && q.pitch % 16 == 0 &&
+        reinterpret_cast<uintptr_t>(q.p0) % 16 == 0 && reinterpret_cast<uintptr_t>(out) % 16 == 0) {
+        quantize16_kernel<<<grid_for(n / 16, 256), 256, 0, as_stream(stream)>>>(
+            static_cast<const uint8_t*>(q.p0), q.pitch, q.width, q.height, static_cast<uint32_t>(q.nbins), out);
+        return launch_status("quantize");
+    }
     quantize_kernel<<<grid_for(n, 256), 256, 0, as_stream(stream)>>>(q, out);
     return launch_status("quantize");
 }
