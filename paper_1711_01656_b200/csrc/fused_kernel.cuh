@@ -337,7 +337,7 @@ struct Geo {
 template <int S>
 constexpr size_t smem_bytes_s() {
     using G = Geo<S>;
-    return (size_t(G::NB) * G::VS + size_t(G::NW) * 4 * kVcWords + G::NB + 2 * S * G::NB + 64) * 4 +
+    return (size_t(G::NB + 1) * G::VS + size_t(G::NW) * 4 * kVcWords + G::NB + 2 * S * G::NB + 64) * 4 +
            size_t(2) * G::NW * kStrip * 8 + size_t(2) * kStrip * S * 2;
 }
 
@@ -355,7 +355,10 @@ __global__ void __launch_bounds__(256, 2) sweep_match_kernel(QuantParams q, Pixe
     constexpr bool FAST = MODE == 1 || MODE == 2, FRAC = MODE == 2;
     extern __shared__ uint4 smem_raw[];
     uint32_t* vc = reinterpret_cast<uint32_t*>(smem_raw);                 // [NB bins][VS words], padded
-    uint32_t* gbuf = vc + NB * VS;                                          // [NW warps][4][128 words] (general kw)
+    // integer paths over part of the histogram (!ALLB): running column counts of the group's
+    // bins together, the window totals C of the group from one window-count pass per strip
+    uint32_t* vcind = vc + NB * VS;                                         // [VS words]
+    uint32_t* gbuf = vcind + VS;                                            // [NW warps][4][128 words] (general kw)
     double* red = reinterpret_cast<double*>(gbuf + NW * 4 * kVcWords);      // [2 rows][NW warps][128]
     uint32_t* srep_s = reinterpret_cast<uint32_t*>(red + 2 * NW * kStrip);  // [NB]
     uint32_t* lrow = srep_s + NB;                                           // [2 rows][S strips][NB] row carries
@@ -406,7 +409,7 @@ __global__ void __launch_bounds__(256, 2) sweep_match_kernel(QuantParams q, Pixe
         return bin_of_raw(r, q);
     };
 
-    for (int i = tid; i < NB * VS; i += NT) vc[i] = 0;
+    for (int i = tid; i < (NB + 1) * VS; i += NT) vc[i] = 0;
     if (FAST)
         for (int i = tid; i < 4 * 64 * S; i += NT) red32[i] = 0;  // row accumulators {I} [2][S][64], {C} [2][S][64]
     if (tid < NB) srep_s[tid] = (FAST && tid < nb_cta) ? __ldg(f.prep + 1 + g0 + tid) : 0u;
@@ -541,6 +544,15 @@ __global__ void __launch_bounds__(256, 2) sweep_match_kernel(QuantParams q, Pixe
                 }
             }
     }
+    constexpr bool IND = FAST && !ALLB;  // the group indicator row is kept
+    if (IND) {  // band start: the indicator's column counts are the sum of the bins' (u16 pairs <= kh)
+        __syncthreads();
+        for (int i = tid; i < VS; i += NT) {
+            uint32_t acc = 0;
+            for (int k = 0; k < nb_cta; ++k) acc += vc[k * VS + i];
+            vcind[i] = acc;
+        }
+    }
 
     // row yy's partials are in `red` (and must be combined) iff it is a match row
     auto pending_row = [&](int yy) { return yy >= y0 && yy >= f.kh - 1; };
@@ -659,11 +671,12 @@ __global__ void __launch_bounds__(256, 2) sweep_match_kernel(QuantParams q, Pixe
                 const int po = (xt_live[c] && ho) ? bin_of(roc) : -1;
                 if (xt_live[c]) {
                     const int bn = pn - out.bin0 - g0;
-                    if (static_cast<unsigned>(bn) < static_cast<unsigned>(nb_cta))
-                        atomicAdd(&vc[bn * VS + vcol_w[c]], vinc[c]);
+                    const bool in_n = static_cast<unsigned>(bn) < static_cast<unsigned>(nb_cta);
+                    if (in_n) atomicAdd(&vc[bn * VS + vcol_w[c]], vinc[c]);
                     const int bo = po - out.bin0 - g0;
-                    if (po >= 0 && static_cast<unsigned>(bo) < static_cast<unsigned>(nb_cta))
-                        atomicSub(&vc[bo * VS + vcol_w[c]], vinc[c]);
+                    const bool in_o = po >= 0 && static_cast<unsigned>(bo) < static_cast<unsigned>(nb_cta);
+                    if (in_o) atomicSub(&vc[bo * VS + vcol_w[c]], vinc[c]);
+                    if (IND && in_n != in_o) atomicAdd(&vcind[vcol_w[c]], in_n ? vinc[c] : 0u - vinc[c]);
                 }
                 const int col = tid + c * NT;
                 if (col >= kStrip && col < E) rowbins[(y & 1) * kStrip * S + col - kStrip] = static_cast<uint16_t>(pn);
@@ -706,8 +719,8 @@ __global__ void __launch_bounds__(256, 2) sweep_match_kernel(QuantParams q, Pixe
         const uint4* lr = reinterpret_cast<const uint4*>(lrow + (y & 1) * S * NB + sc * NB + wb * kB);
         uint32_t* prow = STORE ? base_ptr + static_cast<int64_t>(y) * out.row_pitch : nullptr;
 
-        uint32_t Iw[8] = {0, 0, 0, 0, 0, 0, 0, 0}, Cw[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-        int Ioff = 0, Coff = 0;  // per-lane offsets summed over the lane's bins (integer path)
+        uint32_t Iw[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+        int Ioff = 0;  // per-lane offset summed over the lane's bins (integer path)
         // fractional path: flag of c_k > floor(s_k) for group g at bit 12 + g of each half
         uint32_t Pf[8] = {0, 0, 0, 0, 0, 0, 0, 0}, pall = 0;
         double acc[4] = {0.0, 0.0, 0.0, 0.0};
@@ -740,11 +753,7 @@ __global__ void __launch_bounds__(256, 2) sweep_match_kernel(QuantParams q, Pixe
                 }
                 Ioff += off + min(ti, 0);
                 if (FRAC) pall |= ti < 0 ? (kFlag << g) : 0u;  // c > floor(s) in every window
-                if (!ALLB) {
-#pragma unroll
-                    for (int j = 0; j < 8; ++j) Cw[j] += w[j];
-                    Coff += off;
-                }
+
             }
         }
         if constexpr (!FAST) if (match_row) {
@@ -841,10 +850,7 @@ __global__ void __launch_bounds__(256, 2) sweep_match_kernel(QuantParams q, Pixe
             if (FAST) {
                 // the quarters hold the same 16 windows per lane for different bins
 #pragma unroll
-                for (int j = 0; j < 8; ++j) {
-                    Iw[j] += static_cast<uint32_t>(Ioff) * 0x10001u;
-                    if (!ALLB) Cw[j] += static_cast<uint32_t>(Coff) * 0x10001u;
-                }
+                for (int j = 0; j < 8; ++j) Iw[j] += static_cast<uint32_t>(Ioff) * 0x10001u;
                 quarter_reduce(Iw, qq);
                 const int jb = 4 * (qq >> 1) + 2 * (qq & 1);
                 if (FRAC) {
@@ -886,14 +892,17 @@ __global__ void __launch_bounds__(256, 2) sweep_match_kernel(QuantParams q, Pixe
                     atomicAdd(rw, Iw[0]);
                     atomicAdd(rw + 1, Iw[1]);
                 }
-                if (!ALLB) {
-                    quarter_reduce(Cw, qq);
-                    if (NWB == 1) {
-                        rw[128 * S] = Cw[0];
-                        rw[128 * S + 1] = Cw[1];
-                    } else {
-                        atomicAdd(rw + 128 * S, Cw[0]);
-                        atomicAdd(rw + 128 * S + 1, Cw[1]);
+                if (IND && wb == 0) {
+                    // the strip's window totals over the group's bins: one window-count pass over
+                    // the indicator row (every quarter computes it; quarter 0 stores the 128)
+                    const uint32_t* vwi = vcind + G::WOFF * sc;
+                    uint32_t cw[8];
+                    int coff;
+                    window_counts_q<KWM>(vwi + vcw(64 + 8 * mq), vwi, mq, aw0, apsh, amask, cw, coff);
+                    if (qq == 0) {
+                        uint32_t* cr = red32 + 128 * S + (y & 1) * 64 * S + sc * 64 + 8 * mq;
+#pragma unroll
+                        for (int j = 0; j < 8; ++j) cr[j] = cw[j] + static_cast<uint32_t>(coff) * 0x10001u;
                     }
                 }
             } else {
