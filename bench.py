@@ -449,7 +449,8 @@ def run_next_rows(P, dev, pk_gbs: float) -> dict:
                                     4 * nb * n * n * 8 + n * n * 2)
     ms_m = timed(lambda: P.swih.swlh_distance_map(bm, nb, model, k, k))
     out["swih_distance_map"] = line("swlh-distance map (float64) in one sweep over the BinMap (no tensors; "
-                                    "bound by the FP64 division per window and bin)", ms_m, n * n * 2 + n * n * 8)
+                                    "W / mass from a table of every window sum; compute-bound by the FP64 "
+                                    "per-bin terms |q - model| summed in bin order)", ms_m, n * n * 2 + n * n * 8)
     ms_q = timed(lambda: P.swih.swlh_distance_map(bm, nb, model, k, k, method="quadrant"))
     out["swih_distance_map_quadrant"] = line("the same map through the quadrant tensors (reference construction)",
                                              ms_q, 4 * nb * n * n * 8 + n * n * 2 + n * n * 8)
