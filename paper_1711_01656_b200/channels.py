@@ -39,7 +39,7 @@ def likelihood_channels(r, g, b, nbins: int, templates: dict, kw: int, kh: int, 
     h, w = srcs["intensity"].shape
     ts = [tensors[c] if tensors else _api.IntegralHistogramTensor(w, h, nbins, device=dev) for c in CHANNELS]
     ms = [maps[c] if maps else torch.empty((h, w), dtype=torch.float64, device=dev) for c in CHANNELS]
-    tds = [tmpl_dev[c] if tmpl_dev else _api._tmpl(templates[c], nbins, w, h, kw, kh, p) for c in CHANNELS]
+    tds = [tmpl_dev[c] if tmpl_dev else _api._tmpl(templates[c], nbins, w, h, kw, kh, p).to(dev) for c in CHANNELS]
     # all five channels share one launch of each carry kernel and of the template prep
     _api.build_and_match_map_multi([srcs[c] for c in CHANNELS], nbins, tds, kw, kh, p, metric, outs=ts, lmaps=ms,
                                    stream=stream)
