@@ -827,3 +827,18 @@ def test_build_match_map_multi_matches_single(P, bins, p, metric, store):
         if store:
             assert np.array_equal(outs[i].padded_u64(), t1.padded_u64()), i
     assert close(maps[3].cpu().numpy(), oracle.hist_match_map_direct(bm, bins, tm[3], kw, kh, p, metric))
+
+
+@pytest.mark.parametrize("w,h,bins", [(520, 300, 64), (700, 130, 16), (129, 517, 40)])
+def test_joint_tensor_after_slides_bit_exact(P, w, h, bins, band_rows):
+    """The one-pass slide (J += IH(new) - IH(old), spct_cu_ih_slide) keeps the joint tensor
+    equal to the sum of the window frames' integral histograms, cell by cell, across
+    strips and (forced short) bands."""
+    band_rows(37)
+    rng = np.random.default_rng(w + bins)
+    frames = [rng.integers(0, bins, (h, w), dtype=np.uint8) for _ in range(7)]
+    bg = P.motion.MedianBackgroundIH(frames[:3], bins, 3, 3)
+    for i in range(3, 7):
+        bg.slide(frames[i])
+        want = sum(oracle.build_ih(f.astype(np.uint16), bins) for f in frames[i - 2:i + 1])
+        assert np.array_equal(bg.joint.padded_u64(), want), i
