@@ -211,7 +211,8 @@ spct_status build_match(int n, const spct_source* srcs, const spct_ih* outs, con
     // p = 2 (int32 sums need kw kh <= 4096), Bhattacharyya and chi-square: integer / FP32 terms
     const int f32_ok = (metric == SPCT_METRIC_MINKOWSKI && p == 2.0 && T <= 4096) ||
                        metric == SPCT_METRIC_BHATTACHARYYA || metric == SPCT_METRIC_CHISQ;
-    const int path = fast_metric ? 1 : (f32_ok ? 3 : 0);
+    // Bhattacharyya in the quarter layout (MODE 4, packed 16-bit window counts: kw kh <= 24576)
+    const int path = fast_metric ? 1 : (metric == SPCT_METRIC_BHATTACHARYYA && T <= 24576 ? 4 : (f32_ok ? 3 : 0));
     const PrepLayout pl = fused_prep_layout(out->bins);
     PrepBatch pbt{};
     for (int c = 0; c < n; ++c) {
@@ -225,7 +226,7 @@ spct_status build_match(int n, const spct_source* srcs, const spct_ih* outs, con
         pbt.c3slab[c] = reinterpret_cast<double2*>(ws + pl.c3slab);
     }
     prep_kernel<<<n, 256, 0, s>>>(pbt, out->bin0, out->bins, static_cast<double>(T), fast_metric, frac_ok,
-                                  path == 3 ? 3 : 0, ngroups);
+                                  path == 1 ? 0 : path, ngroups);
     if (auto st = launch_status("prep_kernel")) return st;
 
     for (int c = 0; c < n; ++c) {

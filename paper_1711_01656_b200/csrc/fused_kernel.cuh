@@ -60,7 +60,7 @@ struct FusedParams {
     double inv_p, dmax, inv_dmax;  // inv_dmax != 0 iff dmax is a power of two (exact product)
     int W, H;
     int frac;     // host: the fractional variant is launched instead of the FP64 one
-    int path;     // host: 1 = integer metric (MODE 1 + MODE 2 or 0), 3 = MODE 3 only, 0 = MODE 0 only
+    int path;     // host: 1 = integer metric (MODE 1 + MODE 2 or 0), 3 / 4 / 0 = that MODE only
     int fp_kind;  // FP64 path term: 0 Minkowski p=1, 1 p=2, 2 general p, 3 intersection, 4 Bhattacharyya, 5 chi-square
 };
 
@@ -344,15 +344,17 @@ constexpr size_t smem_bytes_s() {
 // MODE: 0 = the FP64 per-bin path (any metric), 1 = the exact integer path (integral
 // template, p = 1 / intersection), 2 = the integer path on floor(s_k) plus the fractional
 // correction sum_{k: c_k > floor(s_k)} r_k (any template, p = 1 / intersection, kw kh <= 4096),
-// 3 = the full-warp layout of MODE 0 with integer / FP32 per-bin terms for p = 2 (kw kh <= 4096),
-// Bhattacharyya and chi-square (f32_term below).
+// 3 = the full-warp layout of MODE 0 with integer / FP32 per-bin terms for p = 2 (kw kh <= 4096)
+// and chi-square (f32_term below), 4 = Bhattacharyya in the quarter layout of the integer
+// paths: per window and bin sqrt(c) sqrt(t / T) in FP32 (16 windows per lane, four bins per
+// lane, the quarters summed in a fixed order), the warps' partials combined in FP64.
 template <bool STORE, int MODE, int KWM, bool ALLB, int SK, int S>
 __global__ void __launch_bounds__(256, 2) sweep_match_kernel(QuantParams q, PixelMode pm, spct_ih out, int Lb, int Wp,
                                                              int band_rows, int nstrips, FusedCarries fc,
                                                              FusedParams f) {
     using G = Geo<S>;
     constexpr int NW = G::NW, NWB = G::NWB, NB = G::NB, NT = G::NT, E = G::E, VS = G::VS, CPT = G::CPT;
-    constexpr bool FAST = MODE == 1 || MODE == 2, FRAC = MODE == 2;
+    constexpr bool FAST = MODE == 1 || MODE == 2, FRAC = MODE == 2, QF = MODE == 4;
     extern __shared__ uint4 smem_raw[];
     uint32_t* vc = reinterpret_cast<uint32_t*>(smem_raw);                 // [NB bins][VS words], padded
     // integer paths over part of the histogram (!ALLB): running column counts of the group's
@@ -413,7 +415,7 @@ __global__ void __launch_bounds__(256, 2) sweep_match_kernel(QuantParams q, Pixe
     if (FAST)
         for (int i = tid; i < 4 * 64 * S; i += NT) red32[i] = 0;  // row accumulators {I} [2][S][64], {C} [2][S][64]
     if (tid < NB) srep_s[tid] = (FAST && tid < nb_cta) ? __ldg(f.prep + 1 + g0 + tid) : 0u;
-    if (FAST && KWM == 0)
+    if ((FAST || QF) && KWM == 0)
         for (int i = tid; i < 64; i += NT) {
             // anchor masks: u16 i of lane m's word j is valid iff 16m + 2j + i < kw
             const int n = f.kw - 16 * (i >> 3) - 2 * (i & 7);
@@ -723,12 +725,34 @@ __global__ void __launch_bounds__(256, 2) sweep_match_kernel(QuantParams q, Pixe
         int Ioff = 0;  // per-lane offset summed over the lane's bins (integer path)
         // fractional path: flag of c_k > floor(s_k) for group g at bit 12 + g of each half
         uint32_t Pf[8] = {0, 0, 0, 0, 0, 0, 0, 0}, pall = 0;
+        // MODE 4: the lane's 16 windows' FP32 sums over its four bins
+        [[maybe_unused]] float qf[16];
+        if (QF)
+#pragma unroll
+            for (int i = 0; i < 16; ++i) qf[i] = 0.0f;
         double acc[4] = {0.0, 0.0, 0.0, 0.0};
 #pragma unroll
         for (int g = 0; g < kB / 4; ++g) {
             if (STORE)
                 vpart_group_q<kB>(V, g, t4, lr[g], prow + static_cast<int64_t>(4 * g) * out.plane_pitch, out.plane_pitch,
                                   store_mask);
+            if (QF && match_row) {
+                uint32_t w[8];
+                int off;
+                const int go = 4 * g * VS;
+                window_counts_q<KWM>(pb + go, vq + go, mq, aw0, apsh, amask, w, off);
+                const int kq = kl0 + 4 * g + qq;  // the quarter's bin (slab-local)
+                const float wk = kq < out.bins ? __ldg(f.c3 + kq).z : 0.0f;  // sqrt(t / T)
+                // c = half + off exactly in FP32: 2^23 + half by bit pattern, plus off - 2^23
+                const float cfo = static_cast<float>(off) - 8388608.0f;
+#pragma unroll
+                for (int j = 0; j < 8; ++j) {
+                    const float c0 = __int_as_float(0x4B000000u | (w[j] & 0xFFFFu)) + cfo;
+                    const float c1 = __int_as_float(0x4B000000u | (w[j] >> 16)) + cfo;
+                    qf[2 * j] = fmaf(sqrt_approx(c0), wk, qf[2 * j]);
+                    qf[2 * j + 1] = fmaf(sqrt_approx(c1), wk, qf[2 * j + 1]);
+                }
+            }
             if (FAST && match_row) {
                 uint32_t w[8];
                 int off;
@@ -756,7 +780,7 @@ __global__ void __launch_bounds__(256, 2) sweep_match_kernel(QuantParams q, Pixe
 
             }
         }
-        if constexpr (!FAST) if (match_row) {
+        if constexpr (!FAST && !QF) if (match_row) {
             // FP64 path (MODE 0) / integer-FP32 terms (MODE 3): the window terms in a rolled loop
             // over the bin groups, one loop per metric (a per-row switch) so the running loop
             // stays small
@@ -905,6 +929,23 @@ __global__ void __launch_bounds__(256, 2) sweep_match_kernel(QuantParams q, Pixe
                         for (int j = 0; j < 8; ++j) cr[j] = cw[j] + static_cast<uint32_t>(coff) * 0x10001u;
                     }
                 }
+            } else if (QF) {
+                // the four quarters' sums of the same windows (reduce-scatter as quarter_reduce:
+                // the lane keeps windows 16 mq + 8 hi2 + 4 hi1 + 0..3), then the warp's partial
+                const bool hi2 = qq & 2, hi1 = qq & 1;
+#pragma unroll
+                for (int i = 0; i < 8; ++i) {
+                    const float snd = hi2 ? qf[i] : qf[i + 8], kp = hi2 ? qf[i + 8] : qf[i];
+                    qf[i] = kp + __shfl_xor_sync(0xffffffffu, snd, 16);
+                }
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                    const float snd = hi1 ? qf[i] : qf[i + 4], kp = hi1 ? qf[i + 4] : qf[i];
+                    qf[i] = kp + __shfl_xor_sync(0xffffffffu, snd, 8);
+                }
+                double* rb = red + (y & 1) * (NW * kStrip) + warp * kStrip + 16 * mq + 8 * (qq >> 1) + 4 * (qq & 1);
+#pragma unroll
+                for (int i = 0; i < 4; ++i) rb[i] = static_cast<double>(qf[i]);
             } else {
                 double* rb = red + (y & 1) * (NW * kStrip) + warp * kStrip;
                 rb[4 * lane + 0] = acc[0];
@@ -942,6 +983,8 @@ void launch_variants(bool frac, int path, dim3 grid, cudaStream_t s, const Quant
             if (frac) SPCT_GO(true, 2, ALLB) else SPCT_GO(true, 0, false)
         } else if (path == 3) {
             SPCT_GO(true, 3, false)
+        } else if (path == 4) {
+            SPCT_GO(true, 4, false)
         } else {
             SPCT_GO(true, 0, false)
         }
@@ -951,6 +994,8 @@ void launch_variants(bool frac, int path, dim3 grid, cudaStream_t s, const Quant
             if (frac) SPCT_GO(false, 2, ALLB) else SPCT_GO(false, 0, false)
         } else if (path == 3) {
             SPCT_GO(false, 3, false)
+        } else if (path == 4) {
+            SPCT_GO(false, 4, false)
         } else {
             SPCT_GO(false, 0, false)
         }
