@@ -211,8 +211,9 @@ spct_status build_match(int n, const spct_source* srcs, const spct_ih* outs, con
     // p = 2 (int32 sums need kw kh <= 4096), Bhattacharyya and chi-square: integer / FP32 terms
     const int f32_ok = (metric == SPCT_METRIC_MINKOWSKI && p == 2.0 && T <= 4096) ||
                        metric == SPCT_METRIC_BHATTACHARYYA || metric == SPCT_METRIC_CHISQ;
-    // Bhattacharyya in the quarter layout (MODE 4, packed 16-bit window counts: kw kh <= 24576)
-    const int path = fast_metric ? 1 : (metric == SPCT_METRIC_BHATTACHARYYA && T <= 24576 ? 4 : (f32_ok ? 3 : 0));
+    // Bhattacharyya / chi-square in the quarter layout (MODE 4 / 5, packed 16-bit window counts)
+    const int quarter = T <= 24576 ? (metric == SPCT_METRIC_BHATTACHARYYA ? 4 : (metric == SPCT_METRIC_CHISQ ? 5 : 0)) : 0;
+    const int path = fast_metric ? 1 : (quarter ? quarter : (f32_ok ? 3 : 0));
     const PrepLayout pl = fused_prep_layout(out->bins);
     PrepBatch pbt{};
     for (int c = 0; c < n; ++c) {

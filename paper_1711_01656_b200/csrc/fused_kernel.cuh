@@ -345,8 +345,9 @@ constexpr size_t smem_bytes_s() {
 // template, p = 1 / intersection), 2 = the integer path on floor(s_k) plus the fractional
 // correction sum_{k: c_k > floor(s_k)} r_k (any template, p = 1 / intersection, kw kh <= 4096),
 // 3 = the full-warp layout of MODE 0 with integer / FP32 per-bin terms for p = 2 (kw kh <= 4096)
-// and chi-square (f32_term below), 4 = Bhattacharyya in the quarter layout of the integer
-// paths: per window and bin sqrt(c) sqrt(t / T) in FP32 (16 windows per lane, four bins per
+// (f32_term below), 4 / 5 = Bhattacharyya / chi-square in the quarter layout of the integer
+// paths: per window and bin sqrt(c) sqrt(t / T), resp. c s / (c + s) (chi-square through
+// (q - t)^2 / (q + t) = q + t - 4 q t / (q + t)), in FP32 (16 windows per lane, four bins per
 // lane, the quarters summed in a fixed order), the warps' partials combined in FP64.
 template <bool STORE, int MODE, int KWM, bool ALLB, int SK, int S>
 __global__ void __launch_bounds__(256, 2) sweep_match_kernel(QuantParams q, PixelMode pm, spct_ih out, int Lb, int Wp,
@@ -354,13 +355,15 @@ __global__ void __launch_bounds__(256, 2) sweep_match_kernel(QuantParams q, Pixe
                                                              FusedParams f) {
     using G = Geo<S>;
     constexpr int NW = G::NW, NWB = G::NWB, NB = G::NB, NT = G::NT, E = G::E, VS = G::VS, CPT = G::CPT;
-    constexpr bool FAST = MODE == 1 || MODE == 2, FRAC = MODE == 2, QF = MODE == 4;
+    constexpr bool FAST = MODE == 1 || MODE == 2, FRAC = MODE == 2, QF = MODE == 4 || MODE == 5, CHI = MODE == 5;
     extern __shared__ uint4 smem_raw[];
     uint32_t* vc = reinterpret_cast<uint32_t*>(smem_raw);                 // [NB bins][VS words], padded
     // integer paths over part of the histogram (!ALLB): running column counts of the group's
     // bins together, the window totals C of the group from one window-count pass per strip
     uint32_t* vcind = vc + NB * VS;                                         // [VS words]
     uint32_t* gbuf = vcind + VS;                                            // [NW warps][4][128 words] (general kw)
+    // the group's window totals C per row parity, strip and window pair (packed): red32 for
+    // the integer paths, gbuf for the quarter-layout FP32 paths (whose partials fill `red`)
     double* red = reinterpret_cast<double*>(gbuf + NW * 4 * kVcWords);      // [2 rows][NW warps][128]
     uint32_t* srep_s = reinterpret_cast<uint32_t*>(red + 2 * NW * kStrip);  // [NB]
     uint32_t* lrow = srep_s + NB;                                           // [2 rows][S strips][NB] row carries
@@ -371,6 +374,7 @@ __global__ void __launch_bounds__(256, 2) sweep_match_kernel(QuantParams q, Pixe
     // integer path: per row parity, strip and window pair, the packed sums over the warps
     // (shared atomics), I at [parity][strip][64] and C at 128 S + [parity][strip][64]
     uint32_t* red32 = reinterpret_cast<uint32_t*>(red);
+    uint32_t* carea = (MODE == 4 || MODE == 5) ? gbuf : red32 + 128 * S;
     // fractional path, in 2^-40 fixed point (exact sums in any order): per row parity and
     // window the correction accumulated over the warps ([2][S][128] pairs of u32 shared
     // atomics on the low 24 bits and the rest of each warp's u64 value: no 64-bit CAS loop), and
@@ -546,7 +550,7 @@ __global__ void __launch_bounds__(256, 2) sweep_match_kernel(QuantParams q, Pixe
                 }
             }
     }
-    constexpr bool IND = FAST && !ALLB;  // the group indicator row is kept
+    constexpr bool IND = (FAST || CHI) && !ALLB;  // the group indicator row is kept
     if (IND) {  // band start: the indicator's column counts are the sum of the bins' (u16 pairs <= kh)
         __syncthreads();
         for (int i = tid; i < VS; i += NT) {
@@ -608,12 +612,9 @@ __global__ void __launch_bounds__(256, 2) sweep_match_kernel(QuantParams q, Pixe
             // sum stays below 2^16 (at most kw * kh).  Read, then clear for row yy + 2.
             uint32_t* ai = red32 + (yy & 1) * 64 * S + (t >> 1);
             const uint32_t xi = *ai;
-            const uint32_t xcn = ALLB ? 0u : ai[128 * S];
+            const uint32_t xcn = ALLB ? 0u : carea[(yy & 1) * 64 * S + (t >> 1)];  // rewritten every row
             __syncwarp();
-            if (!(t & 1)) {
-                *ai = 0;
-                if (!ALLB) ai[128 * S] = 0;
-            }
+            if (!(t & 1)) *ai = 0;
             if (u < 0 || e >= W) return;
             const uint32_t I = (xi >> (16 * (t & 1))) & 0xFFFFu;
             // sum_k min(c_k, s_k): exact integers, plus the fractional correction (2^-40 fixed
@@ -644,6 +645,11 @@ __global__ void __launch_bounds__(256, 2) sweep_match_kernel(QuantParams q, Pixe
 #pragma unroll
             for (int w = 0; w < NWB; ++w)
                 if (w < nwarps_live) term = __dadd_rn(term, rb[w * kStrip]);
+            if (CHI) {  // + C / T, C the window's count over the group's bins
+                const uint32_t cn = ALLB ? 0u : carea[(yy & 1) * 64 * S + (t >> 1)];
+                const double C = ALLB ? static_cast<double>(f.kw) * f.kh : static_cast<double>((cn >> (16 * (t & 1))) & 0xFFFFu);
+                term = __dadd_rn(term, C * f.invT);
+            }
             term = add_acc(yy, u, v, term);
             if (f.map) write_map(u, v, finalize_L(term, f));
             else f.partial[static_cast<int64_t>(v) * f.nu + u] = term;
@@ -654,6 +660,23 @@ __global__ void __launch_bounds__(256, 2) sweep_match_kernel(QuantParams q, Pixe
         for (int t = tid; t < kStrip * S; t += NT) combine_one(yy, t);
     };
 
+
+    // The strip's window totals over the group's bins (paths that need C and do not hold
+    // the whole histogram): one window-count pass over the indicator row per strip and row
+    // (every quarter of the strip's first warp computes it; quarter 0 stores the 128)
+    auto ind_pass = [&](int y) {
+        if (IND && wb == 0) {
+            const uint32_t* vwi = vcind + G::WOFF * sc;
+            uint32_t cw[8];
+            int coff;
+            window_counts_q<KWM>(vwi + vcw(64 + 8 * mq), vwi, mq, aw0, apsh, amask, cw, coff);
+            if (qq == 0) {
+                uint32_t* cr = carea + (y & 1) * 64 * S + sc * 64 + 8 * mq;
+#pragma unroll
+                for (int j = 0; j < 8; ++j) cr[j] = cw[j] + static_cast<uint32_t>(coff) * 0x10001u;
+            }
+        }
+    };
 
     for (int y = y0; y < y1; ++y) {
         __syncthreads();  // A: previous row's vc / staging reads are done, its partials written
@@ -742,15 +765,20 @@ __global__ void __launch_bounds__(256, 2) sweep_match_kernel(QuantParams q, Pixe
                 const int go = 4 * g * VS;
                 window_counts_q<KWM>(pb + go, vq + go, mq, aw0, apsh, amask, w, off);
                 const int kq = kl0 + 4 * g + qq;  // the quarter's bin (slab-local)
-                const float wk = kq < out.bins ? __ldg(f.c3 + kq).z : 0.0f;  // sqrt(t / T)
+                const float4 cst = kq < out.bins ? __ldg(f.c3 + kq) : make_float4(0.0f, 0.0f, 0.0f, 0.0f);
                 // c = half + off exactly in FP32: 2^23 + half by bit pattern, plus off - 2^23
                 const float cfo = static_cast<float>(off) - 8388608.0f;
 #pragma unroll
                 for (int j = 0; j < 8; ++j) {
                     const float c0 = __int_as_float(0x4B000000u | (w[j] & 0xFFFFu)) + cfo;
                     const float c1 = __int_as_float(0x4B000000u | (w[j] >> 16)) + cfo;
-                    qf[2 * j] = fmaf(sqrt_approx(c0), wk, qf[2 * j]);
-                    qf[2 * j + 1] = fmaf(sqrt_approx(c1), wk, qf[2 * j + 1]);
+                    if (CHI) {  // c s / (c + s); c = s = 0 gives 0 (the reference skips q + t = 0)
+                        qf[2 * j] = fmaf(c0 * cst.w, rcp_approx(c0 + cst.w + 1e-30f), qf[2 * j]);
+                        qf[2 * j + 1] = fmaf(c1 * cst.w, rcp_approx(c1 + cst.w + 1e-30f), qf[2 * j + 1]);
+                    } else {    // sqrt(c) sqrt(t / T)
+                        qf[2 * j] = fmaf(sqrt_approx(c0), cst.z, qf[2 * j]);
+                        qf[2 * j + 1] = fmaf(sqrt_approx(c1), cst.z, qf[2 * j + 1]);
+                    }
                 }
             }
             if (FAST && match_row) {
@@ -916,20 +944,9 @@ __global__ void __launch_bounds__(256, 2) sweep_match_kernel(QuantParams q, Pixe
                     atomicAdd(rw, Iw[0]);
                     atomicAdd(rw + 1, Iw[1]);
                 }
-                if (IND && wb == 0) {
-                    // the strip's window totals over the group's bins: one window-count pass over
-                    // the indicator row (every quarter computes it; quarter 0 stores the 128)
-                    const uint32_t* vwi = vcind + G::WOFF * sc;
-                    uint32_t cw[8];
-                    int coff;
-                    window_counts_q<KWM>(vwi + vcw(64 + 8 * mq), vwi, mq, aw0, apsh, amask, cw, coff);
-                    if (qq == 0) {
-                        uint32_t* cr = red32 + 128 * S + (y & 1) * 64 * S + sc * 64 + 8 * mq;
-#pragma unroll
-                        for (int j = 0; j < 8; ++j) cr[j] = cw[j] + static_cast<uint32_t>(coff) * 0x10001u;
-                    }
-                }
+                ind_pass(y);
             } else if (QF) {
+                ind_pass(y);
                 // the four quarters' sums of the same windows (reduce-scatter as quarter_reduce:
                 // the lane keeps windows 16 mq + 8 hi2 + 4 hi1 + 0..3), then the warp's partial
                 const bool hi2 = qq & 2, hi1 = qq & 1;
@@ -944,8 +961,14 @@ __global__ void __launch_bounds__(256, 2) sweep_match_kernel(QuantParams q, Pixe
                     qf[i] = kp + __shfl_xor_sync(0xffffffffu, snd, 8);
                 }
                 double* rb = red + (y & 1) * (NW * kStrip) + warp * kStrip + 16 * mq + 8 * (qq >> 1) + 4 * (qq & 1);
+                if (CHI) {  // the warp's (S_w - 4 Y_w) / T, S_w = sum of s_k over its bins
+                    const double sw = f.c3slab[kl0 / kB].y;
 #pragma unroll
-                for (int i = 0; i < 4; ++i) rb[i] = static_cast<double>(qf[i]);
+                    for (int i = 0; i < 4; ++i) rb[i] = (sw - 4.0 * static_cast<double>(qf[i])) * f.invT;
+                } else {
+#pragma unroll
+                    for (int i = 0; i < 4; ++i) rb[i] = static_cast<double>(qf[i]);
+                }
             } else {
                 double* rb = red + (y & 1) * (NW * kStrip) + warp * kStrip;
                 rb[4 * lane + 0] = acc[0];
@@ -985,6 +1008,8 @@ void launch_variants(bool frac, int path, dim3 grid, cudaStream_t s, const Quant
             SPCT_GO(true, 3, false)
         } else if (path == 4) {
             SPCT_GO(true, 4, false)
+        } else if (path == 5) {
+            SPCT_GO(true, 5, false)
         } else {
             SPCT_GO(true, 0, false)
         }
@@ -996,6 +1021,8 @@ void launch_variants(bool frac, int path, dim3 grid, cudaStream_t s, const Quant
             SPCT_GO(false, 3, false)
         } else if (path == 4) {
             SPCT_GO(false, 4, false)
+        } else if (path == 5) {
+            SPCT_GO(false, 5, false)
         } else {
             SPCT_GO(false, 0, false)
         }
