@@ -595,6 +595,21 @@ def run_ours(args) -> None:
         weak.close()
         del weak
 
+    # ---- N > 1: the north star's collective (one NCCL reduce of the partial maps + finalise
+    # on the root) beside the default peer-memory band reduce, same configuration
+    if world > 1 and args.reduce != "nccl":
+        try:
+            alt = ShardedMapStep(W_IMG, H_IMG, NBINS, tmpl, KW, KH, P_ORDER, reduce="nccl", device=dev)
+            ms_n = timer(lambda: alt.step(frame), args.steps, warmup=args.warmup)
+            extras["reduce_nccl"] = {"workload": "the headline step with one dist.reduce (NCCL) of the partial maps "
+                                                 "and hist_finalize on rank 0", "ms_per_step": round(ms_n, 4),
+                                     "value": round(NBINS * W_IMG * H_IMG / (ms_n * 1e-3) / 1e9, 2), "unit": UNIT,
+                                     "reduce": alt.note, "backend": dist.get_backend()}
+            alt.close()
+            del alt
+        except Exception as e:  # e.g. the shared-GPU functional mode runs gloo
+            extras["reduce_nccl"] = {"unavailable": f"{type(e).__name__}: {str(e)[:160]}"}
+
     # ---- single-GPU extras
     if world == 1:
         t = main.tensor
