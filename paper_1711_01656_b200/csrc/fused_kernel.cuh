@@ -467,7 +467,10 @@ __global__ void __launch_bounds__(256, 2) sweep_match_kernel(QuantParams q, Pixe
     // staging: thread tid owns extended columns tid + c NT (c < CPT, col < E); their raw
     // pixels are prefetched one row ahead (32-bit raw values for the 8/16-bit sources; the
     // generic source with several columns per thread keeps the in-row loads)
-    constexpr bool PREFETCH = CPT == 1 || SK != 0;
+    // (not for the slab variants of 4- and 8-strip CTAs: with the indicator row their
+    // prefetch registers spill, which turns every prefetch into a stall; measured on the
+    // 32 / 16-bin slabs of C3: 0.816 -> 0.770 / 0.554 -> 0.536 ms, tools/slab_time.py)
+    constexpr bool PREFETCH = CPT == 1 || (SK != 0 && (ALLB || S < 4));
     using RawT = std::conditional_t<CPT == 1 || SK == 0, uint64_t, uint32_t>;
     int xt[CPT], vcol_w[CPT];
     bool xt_live[CPT];
