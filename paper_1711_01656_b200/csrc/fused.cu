@@ -1,11 +1,47 @@
 // Fused integral histogram + sliding-window matcher: host side (C-ABI, template prep,
 // dispatch).  The kernel is in fused_kernel.cuh.
+#include <mutex>
+
 #include "fused_kernel.cuh"
 
 using namespace spct_dev;
 using namespace spct_impl;
 
 namespace spct_fused {
+
+// Side streams of a batched call (per device, created once): the sweeps of a batch's
+// sources are independent, so sources 1.. run on their own streams, forked from and joined
+// back into the caller's stream by events (captured as parallel branches inside a CUDA
+// graph).  Each sweep is about one wave of CTAs; side by side, one source's pre-roll and
+// tail overlap another's steady state.  The mutex keeps a fork / join sequence's event
+// records and waits together when several host threads share the pool.
+struct SidePool {
+    std::mutex mu;
+    cudaStream_t side[kMaxCarryCh] = {};
+    cudaEvent_t fork = nullptr, join[kMaxCarryCh] = {};
+    bool ok = false;
+};
+
+static SidePool* side_pool() {
+    static SidePool pools[64];
+    static std::mutex init_mu;
+    const int dev = current_device();
+    if (dev < 0 || dev >= 64) return nullptr;
+    SidePool& P = pools[dev];
+    std::lock_guard<std::mutex> lk(init_mu);
+    if (!P.ok) {
+        bool good = cudaEventCreateWithFlags(&P.fork, cudaEventDisableTiming) == cudaSuccess;
+        for (int i = 0; good && i < kMaxCarryCh; ++i)
+            good = cudaStreamCreateWithFlags(&P.side[i], cudaStreamNonBlocking) == cudaSuccess &&
+                   cudaEventCreateWithFlags(&P.join[i], cudaEventDisableTiming) == cudaSuccess;
+        if (!good) {
+            cudaGetLastError();
+            return nullptr;
+        }
+        P.ok = true;
+    }
+    return &P;
+}
 
 // Template prep: s_k = T t_k.  Kind 1 (the exact integer path) iff every s_k of the slab
 // is an integer up to FP noise (then the integer formula is exact to ~1e-15) and the metric
@@ -230,7 +266,19 @@ spct_status build_match(int n, const spct_source* srcs, const spct_ih* outs, con
                                   path == 1 ? 0 : path, ngroups);
     if (auto st = launch_status("prep_kernel")) return st;
 
+    // sources 1.. on side streams (sweeps only: carries and prep above are batched launches)
+    SidePool* pool = n > 1 && !std::getenv("SPCT_NO_SIDE_STREAMS") ? side_pool() : nullptr;
+    std::unique_lock<std::mutex> side_lk;
+    if (pool) {
+        side_lk = std::unique_lock<std::mutex>(pool->mu);
+        if (auto st = cuda_status(cudaEventRecord(pool->fork, s), "ih_build_match fork")) return st;
+    }
     for (int c = 0; c < n; ++c) {
+        cudaStream_t sc = s;
+        if (pool && c > 0) {
+            sc = pool->side[c];
+            if (auto st = cuda_status(cudaStreamWaitEvent(sc, pool->fork, 0), "ih_build_match fork")) return st;
+        }
         FusedParams f{};
         f.kw = kw;
         f.kh = kh;
@@ -276,15 +324,15 @@ spct_status build_match(int n, const spct_source* srcs, const spct_ih* outs, con
             // one adds its sums to it and writes the finished map (no finalise pass)
             if (group_part && g == ngroups - 1) f.map = mapc;
             dim3 grid(static_cast<unsigned>(ceil_div(bp.nstrips, S)), bp.nbands, 1);
-            const int prof = prof_begin(oc.data ? "ih_sweep_match" : "sweep_match_nostore", s);
+            const int prof = prof_begin(oc.data ? "ih_sweep_match" : "sweep_match_nostore", sc);
             // the group is the whole histogram: window totals over its bins are kw * kh
             const bool allb = oc.bin0 == 0 && oc.bins == oc.nbins_total && ngroups == 1;
             const int sk = (q.kind == SPCT_SRC_GRAY_U8 && q.fast_u8) ? 1 : (q.kind == SPCT_SRC_BINS_U16 ? 2 : 0);
 #define SPCT_LAUNCH(KW)                                                                                     \
-    if (S == 1) launch_##KW##_s1(allb, sk, grid, s, q, pm, oc, bp, fc, f);                                      \
-    else if (S == 2) launch_##KW##_s2(allb, sk, grid, s, q, pm, oc, bp, fc, f);                                 \
-    else if (S == 4) launch_##KW##_s4(allb, sk, grid, s, q, pm, oc, bp, fc, f);                                 \
-    else launch_##KW##_s8(allb, sk, grid, s, q, pm, oc, bp, fc, f);
+    if (S == 1) launch_##KW##_s1(allb, sk, grid, sc, q, pm, oc, bp, fc, f);                                      \
+    else if (S == 2) launch_##KW##_s2(allb, sk, grid, sc, q, pm, oc, bp, fc, f);                                 \
+    else if (S == 4) launch_##KW##_s4(allb, sk, grid, sc, q, pm, oc, bp, fc, f);                                 \
+    else launch_##KW##_s8(allb, sk, grid, sc, q, pm, oc, bp, fc, f);
             if (kw == 64) {
                 SPCT_LAUNCH(kw64)
             } else if (kw == 128) {
@@ -293,9 +341,13 @@ spct_status build_match(int n, const spct_source* srcs, const spct_ih* outs, con
                 SPCT_LAUNCH(kw_any)
             }
 #undef SPCT_LAUNCH
-            prof_end(prof, s);
+            prof_end(prof, sc);
             note_launch();
             if (auto st = launch_status("sweep_match_kernel")) return st;
+        }
+        if (sc != s) {
+            if (auto st = cuda_status(cudaEventRecord(pool->join[c], sc), "ih_build_match join")) return st;
+            if (auto st = cuda_status(cudaStreamWaitEvent(s, pool->join[c], 0), "ih_build_match join")) return st;
         }
     }
     return SPCT_OK;
