@@ -658,7 +658,33 @@ __global__ void __launch_bounds__(256, 2) sweep_match_kernel(QuantParams q, Pixe
             else f.partial[static_cast<int64_t>(v) * f.nu + u] = term;
         }
     };
+    // exact integer path into a finished map with several strips per CTA: thread t finishes
+    // the window pair (2 t, 2 t + 1), whose packed sums share one word: one read and clear
+    // (no other thread touches the word) and one 16-byte store for an interior pair
+    constexpr bool PAIRS = MODE == 1 && ALLB && S >= 2;
+    const bool map_even = PAIRS && f.map && (reinterpret_cast<uintptr_t>(f.map) & 15) == 0 && (f.W & 1) == 0;
+    auto combine_pair = [&](int yy, int t2) {
+        uint32_t* ai = red32 + (yy & 1) * 64 * S + t2;
+        const uint32_t xi = *ai;
+        *ai = 0;  // for row yy + 2
+        const int e = xc + 2 * t2;
+        const int u = e - f.kw + 1, v = yy - f.kh + 1;
+        const double L0 = fmin(fmax(fma(lin_b, static_cast<double>(xi & 0xFFFFu), lin_a), 0.0), 1.0);
+        const double L1 = fmin(fmax(fma(lin_b, static_cast<double>(xi >> 16), lin_a), 0.0), 1.0);
+        const int x = u + (f.kw - 1) / 2, yc = v + (f.kh - 1) / 2;
+        if (map_even && u > 0 && u + 1 < f.nu - 1 && v > 0 && v < f.nv - 1 && !(x & 1)) {
+            *reinterpret_cast<double2*>(f.map + static_cast<int64_t>(yc) * f.W + x) = make_double2(L0, L1);
+            return;
+        }
+        if (u >= 0 && e < W) write_map(u, v, L0);
+        if (u + 1 >= 0 && e + 1 < W) write_map(u + 1, v, L1);
+    };
     auto combine = [&](int yy) {
+        if (PAIRS && f.map) {
+#pragma unroll
+            for (int t2 = tid; t2 < 64 * S; t2 += NT) combine_pair(yy, t2);
+            return;
+        }
 #pragma unroll
         for (int t = tid; t < kStrip * S; t += NT) combine_one(yy, t);
     };
