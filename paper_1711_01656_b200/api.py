@@ -260,6 +260,7 @@ class Workspace:
 
 _WS = Workspace()
 _WS_ORIENT = Workspace()
+_WS_SIDE = Workspace()  # the orientation branch of a tracking-batch frame (channels.py)
 
 
 def frame_source(frame, nbins: int, lo: float = 0.0, hi: float = 256.0):
@@ -463,10 +464,11 @@ def build_and_match_map_multi(frames, nbins: int, tmpl_devs, kw: int, kh: int, p
 def build_and_match_map(frame, nbins: int, tmpl, kw: int, kh: int, p: float = 1.0,
                         metric: int = A.METRIC_MINKOWSKI, *, lo: float = 0.0, hi: float = 256.0,
                         out: IntegralHistogramTensor | None = None, lmap: torch.Tensor | None = None,
-                        tmpl_dev: torch.Tensor | None = None, stream=None):
+                        tmpl_dev: torch.Tensor | None = None, stream=None, workspace: "Workspace | None" = None):
     """Fused quantise -> build -> finished likelihood map (every bin on this device):
     build_integral_histogram + hist_distance_map (spct_main.cpp:332-333) in one pass.
-    Returns (tensor, map).  ``out.desc.data = None`` skips storing the tensor."""
+    Returns (tensor, map).  ``out.desc.data = None`` skips storing the tensor.  Calls that
+    may run concurrently on different streams need different ``workspace`` caches."""
     src, keep = frame_source(frame, nbins, lo, hi)
     if tmpl_dev is None:
         tmpl_dev = _tmpl(tmpl, nbins, src.width, src.height, kw, kh, p)
@@ -475,7 +477,7 @@ def build_and_match_map(frame, nbins: int, tmpl, kw: int, kh: int, p: float = 1.
         lmap = torch.empty((src.height, src.width), dtype=torch.float64, device=keep[0].device)
     ws = C.c_size_t()
     check(A.lib().spct_cu_ih_build_workspace(C.byref(src), t.bin0, t.bins, C.byref(ws)))
-    wbuf = _WS.get(ws.value, keep[0].device, stream)
+    wbuf = (workspace or _WS).get(ws.value, keep[0].device, stream)
     check(A.lib().spct_cu_ih_build_match_map(C.byref(src), C.byref(t.desc), _ptr(tmpl_dev), kw, kh, p, metric,
                                              _ptr(lmap), _ptr(wbuf), wbuf.numel(), _stream(stream)))
     return t, lmap

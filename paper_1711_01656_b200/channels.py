@@ -34,16 +34,44 @@ def likelihood_channels(r, g, b, nbins: int, templates: dict, kw: int, kh: int, 
     """{channel: (height, width) float64 device map} for one RGB frame.  ``templates`` maps
     each channel to its normalised template histogram (nbins values); ``tensors`` /
     ``maps`` / ``tmpl_dev`` may hold preallocated per-channel outputs for a batch."""
-    srcs = channel_sources(r, g, b, nbins, sigma, stream)
-    dev = srcs["intensity"].device
-    h, w = srcs["intensity"].shape
-    ts = [tensors[c] if tensors else _api.IntegralHistogramTensor(w, h, nbins, device=dev) for c in CHANNELS]
-    ms = [maps[c] if maps else torch.empty((h, w), dtype=torch.float64, device=dev) for c in CHANNELS]
-    tds = [tmpl_dev[c] if tmpl_dev else _api._tmpl(templates[c], nbins, w, h, kw, kh, p).to(dev) for c in CHANNELS]
-    # all five channels share one launch of each carry kernel and of the template prep
-    _api.build_and_match_map_multi([srcs[c] for c in CHANNELS], nbins, tds, kw, kh, p, metric, outs=ts, lmaps=ms,
-                                   stream=stream)
-    return dict(zip(CHANNELS, ms))
+    rd, gd, bd = (_api._dev(x, torch.uint8) for x in (r, g, b))
+    dev = rd.device
+    h, w = rd.shape
+    main = stream if stream is not None else torch.cuda.current_stream(dev)
+    ts = {c: tensors[c] if tensors else _api.IntegralHistogramTensor(w, h, nbins, device=dev) for c in CHANNELS}
+    ms = {c: maps[c] if maps else torch.empty((h, w), dtype=torch.float64, device=dev) for c in CHANNELS}
+    tds = {c: tmpl_dev[c] if tmpl_dev else _api._tmpl(templates[c], nbins, w, h, kw, kh, p).to(dev) for c in CHANNELS}
+    gray = _api.to_grayscale(rd, gd, bd, stream=main)
+    # the orientation channel (gradient + bins, then its map) branches off on a side stream
+    # and overlaps the four plane channels, which share one launch of each carry kernel,
+    # of the template prep and of the sweep per source kind (build_and_match_map_multi)
+    side = _side_stream(dev)
+    fork = torch.cuda.Event()
+    fork.record(main)
+    side.wait_event(fork)
+    gray.record_stream(side)
+    with torch.cuda.stream(side):
+        ob = _api.orientation_bins(gray, nbins, sigma, stream=side)
+        _api.build_and_match_map(ob, nbins, None, kw, kh, p, metric, out=ts["orientation"], lmap=ms["orientation"],
+                                 tmpl_dev=tds["orientation"], stream=side, workspace=_api._WS_SIDE)
+    planes = {"intensity": gray, "red": rd, "green": gd, "blue": bd}
+    pc = [c for c in CHANNELS if c != "orientation"]
+    _api.build_and_match_map_multi([planes[c] for c in pc], nbins, [tds[c] for c in pc], kw, kh, p, metric,
+                                   outs=[ts[c] for c in pc], lmaps=[ms[c] for c in pc], stream=main)
+    join = torch.cuda.Event()
+    join.record(side)
+    main.wait_event(join)
+    return {c: ms[c] for c in CHANNELS}
+
+
+_SIDE: dict = {}
+
+
+def _side_stream(dev) -> torch.cuda.Stream:
+    idx = dev.index if dev.index is not None else torch.cuda.current_device()
+    if idx not in _SIDE:
+        _SIDE[idx] = torch.cuda.Stream(torch.device("cuda", idx))
+    return _SIDE[idx]
 
 
 class ChannelGraph:
