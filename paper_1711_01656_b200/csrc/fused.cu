@@ -327,7 +327,9 @@ spct_status build_match(int n, const spct_source* srcs, const spct_ih* outs, con
             const int prof = prof_begin(oc.data ? "ih_sweep_match" : "sweep_match_nostore", sc);
             // the group is the whole histogram: window totals over its bins are kw * kh
             const bool allb = oc.bin0 == 0 && oc.bins == oc.nbins_total && ngroups == 1;
-            const int sk = (q.kind == SPCT_SRC_GRAY_U8 && q.fast_u8) ? 1 : (q.kind == SPCT_SRC_BINS_U16 ? 2 : 0);
+            const bool al4 = ((reinterpret_cast<uintptr_t>(q.p0) | static_cast<uintptr_t>(q.pitch)) & 3) == 0;
+            const int sk = (q.kind == SPCT_SRC_GRAY_U8 && q.fast_u8) ? (S >= 4 && al4 && !std::getenv("SPCT_NO_WIDE") ? 3 : 1)
+                                                                     : (q.kind == SPCT_SRC_BINS_U16 ? 2 : 0);
 #define SPCT_LAUNCH(KW)                                                                                     \
     if (S == 1) launch_##KW##_s1(allb, sk, grid, sc, q, pm, oc, bp, fc, f);                                      \
     else if (S == 2) launch_##KW##_s2(allb, sk, grid, sc, q, pm, oc, bp, fc, f);                                 \

@@ -332,7 +332,8 @@ struct Geo {
 // ALLB (integer path only): the CTA's bin group is the whole histogram, so the window
 // total over the group's bins is kw * kh and need not be accumulated.
 // SK (source kind of the staging loads): 1 = 8-bit gray with the default range
-// (bin = v * nbins >> 8), 2 = a uint16 BinMap (bin = v), 0 = the generic per-kind dispatch.
+// (bin = v * nbins >> 8), 2 = a uint16 BinMap (bin = v), 0 = the generic per-kind dispatch,
+// 3 = SK 1 with 4-byte aligned rows, staged four columns per thread (4- and 8-strip CTAs).
 // S: strips per CTA (Geo<S>); 1 for >= 65 bins, 2 / 4 / 8 for <= 64 / 32 / 16 bins.
 template <int S>
 constexpr size_t smem_bytes_s() {
@@ -405,12 +406,12 @@ __global__ void __launch_bounds__(256, 2) sweep_match_kernel(QuantParams q, Pixe
     const uint32_t kpat0 = pm.byte_mode ? 0x01010101u * static_cast<uint32_t>(k0) : 0u;
     const uint8_t* g8p = static_cast<const uint8_t*>(q.p0);
     auto raw_at = [&](int x, int y) -> uint64_t {
-        if (SK == 1) return static_cast<uint64_t>(__ldg(g8p + static_cast<int64_t>(y) * q.pitch + x));
+        if (SK == 1 || SK == 3) return static_cast<uint64_t>(__ldg(g8p + static_cast<int64_t>(y) * q.pitch + x));
         if (SK == 2) return static_cast<uint64_t>(__ldg(static_cast<const uint16_t*>(q.p0) + static_cast<int64_t>(y) * q.pitch + x));
         return pixel_raw(q, x, y);
     };
     auto bin_of = [&](uint64_t r) -> int {
-        if (SK == 1) return static_cast<int>((static_cast<uint32_t>(r) * static_cast<uint32_t>(q.nbins)) >> 8);
+        if (SK == 1 || SK == 3) return static_cast<int>((static_cast<uint32_t>(r) * static_cast<uint32_t>(q.nbins)) >> 8);
         if (SK == 2) return static_cast<int>(r);
         return bin_of_raw(r, q);
     };
@@ -470,7 +471,8 @@ __global__ void __launch_bounds__(256, 2) sweep_match_kernel(QuantParams q, Pixe
     // (not for the slab variants of 4- and 8-strip CTAs: with the indicator row their
     // prefetch registers spill, which turns every prefetch into a stall; measured on the
     // 32 / 16-bin slabs of C3: 0.816 -> 0.770 / 0.554 -> 0.536 ms, tools/slab_time.py)
-    constexpr bool PREFETCH = CPT == 1 || (SK != 0 && (ALLB || S < 4));
+    constexpr bool WIDE = SK == 3;  // below
+    constexpr bool PREFETCH = !WIDE && (CPT == 1 || (SK != 0 && (ALLB || S < 4)));
     using RawT = std::conditional_t<CPT == 1 || SK == 0, uint64_t, uint32_t>;
     int xt[CPT], vcol_w[CPT];
     bool xt_live[CPT];
@@ -495,6 +497,21 @@ __global__ void __launch_bounds__(256, 2) sweep_match_kernel(QuantParams q, Pixe
     for (int c = 0; c < CPT; ++c) {
         rn[c] = (PREFETCH && xt_live[c]) ? static_cast<RawT>(raw_at(xt[c], y0)) : 0;
         ro[c] = 0;
+    }
+    // WIDE (SK 3: 8-bit gray, 4-byte aligned rows; 4- and 8-strip CTAs): thread tid stages
+    // the 4-column words tid + w NT of the extended row instead — one 32-bit load per word
+    // and row for the entering and one for the leaving pixels, one 8-byte store of the
+    // strip bins — a third of the per-column staging instructions, which weigh 4x more per
+    // output byte at 32 bins than at 128
+    constexpr int EW = E / 4, WPT = WIDE ? (EW + NT - 1) / NT : 1;
+    bool xw_live[WPT];
+    uint32_t rnw[WPT], row_[WPT];
+#pragma unroll
+    for (int w = 0; w < WPT; ++w) {
+        const int wi = tid + w * NT, xw = xc - kStrip + 4 * wi;
+        xw_live[w] = WIDE && wi < EW && xw >= 0 && xw < W;
+        rnw[w] = xw_live[w] ? __ldg(reinterpret_cast<const uint32_t*>(g8p + static_cast<int64_t>(y0) * q.pitch + xw)) : 0u;
+        row_[w] = 0;
     }
     bool have_o = false;  // y0 - kh < ystart: nothing to remove on the first row
     uint32_t lpre = lt_cta ? static_cast<uint32_t>(__ldg(lt_cta + static_cast<int64_t>(y0) * Lb)) : 0u;
@@ -716,8 +733,37 @@ __global__ void __launch_bounds__(256, 2) sweep_match_kernel(QuantParams q, Pixe
         {   // stage row y: vertical running histogram (add row y, remove row y - kh),
             // the strips' bins and row carries for the sweep, then prefetch row y + 1
             const bool old_row = y - f.kh >= ystart;
+            if (WIDE) {
 #pragma unroll
-            for (int c = 0; c < CPT; ++c) {
+                for (int w = 0; w < WPT; ++w) {
+                    const int wi = tid + w * NT;
+                    const int xw = xc - kStrip + 4 * wi;
+                    uint32_t* vw = vc + vcw(2 * wi);  // columns 4 wi, +1 (word 2 wi) and +2, +3 (the next)
+                    uint32_t pk[2] = {0xFFFFFFFFu, 0xFFFFFFFFu};  // strip bins, 0xFFFF past the image
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) {
+                        if (!xw_live[w] || xw + j >= W) break;
+                        const uint32_t inc = 1u << (16 * (j & 1));
+                        const int pn = static_cast<int>((((rnw[w] >> (8 * j)) & 0xFFu) * static_cast<uint32_t>(q.nbins)) >> 8);
+                        const int bn = pn - out.bin0 - g0;
+                        const bool in_n = static_cast<unsigned>(bn) < static_cast<unsigned>(nb_cta);
+                        if (in_n) atomicAdd(vw + bn * VS + (j >> 1), inc);
+                        bool in_o = false;
+                        if (have_o) {
+                            const int po = static_cast<int>((((row_[w] >> (8 * j)) & 0xFFu) * static_cast<uint32_t>(q.nbins)) >> 8);
+                            const int bo = po - out.bin0 - g0;
+                            in_o = static_cast<unsigned>(bo) < static_cast<unsigned>(nb_cta);
+                            if (in_o) atomicSub(vw + bo * VS + (j >> 1), inc);
+                        }
+                        if (IND && in_n != in_o) atomicAdd(vcind + vcw(2 * wi) + (j >> 1), in_n ? inc : 0u - inc);
+                        pk[j >> 1] = (pk[j >> 1] & ~(0xFFFFu << (16 * (j & 1)))) | (static_cast<uint32_t>(pn) << (16 * (j & 1)));
+                    }
+                    if (4 * wi >= kStrip && wi < EW)
+                        *reinterpret_cast<uint2*>(rowbins + (y & 1) * kStrip * S + 4 * wi - kStrip) = make_uint2(pk[0], pk[1]);
+                }
+            }
+#pragma unroll
+            for (int c = 0; c < (WIDE ? 0 : CPT); ++c) {
                 const uint64_t rnc = PREFETCH ? rn[c] : (xt_live[c] ? raw_at(xt[c], y) : 0);
                 const uint64_t roc = PREFETCH ? ro[c] : ((xt_live[c] && old_row) ? raw_at(xt[c], y - f.kh) : 0);
                 const bool ho = PREFETCH ? have_o : old_row;
@@ -737,7 +783,17 @@ __global__ void __launch_bounds__(256, 2) sweep_match_kernel(QuantParams q, Pixe
             }
             if (tid < S * NB) lrow[(y & 1) * S * NB + tid] = lpre;
             if (y + 1 < y1) {
-                if (PREFETCH) {
+                if (WIDE) {
+                    const int yo = y + 1 - f.kh;
+                    have_o = yo >= ystart;
+#pragma unroll
+                    for (int w = 0; w < WPT; ++w)
+                        if (xw_live[w]) {
+                            const uint8_t* cp = g8p + xc - kStrip + 4 * (tid + w * NT);
+                            rnw[w] = __ldg(reinterpret_cast<const uint32_t*>(cp + static_cast<int64_t>(y + 1) * q.pitch));
+                            if (have_o) row_[w] = __ldg(reinterpret_cast<const uint32_t*>(cp + static_cast<int64_t>(yo) * q.pitch));
+                        }
+                } else if (PREFETCH) {
                     const int yo = y + 1 - f.kh;
                     have_o = yo >= ystart;
 #pragma unroll
@@ -1065,7 +1121,13 @@ void launch_kw_impl(bool allb, int sk, dim3 grid, cudaStream_t s, const QuantPar
 #define SPCT_SK(SKV)                                                                      \
     if (allb) launch_variants<KWM, true, SKV, S>(f.frac, f.path, grid, s, q, pm, out, bp, fc, f);   \
     else launch_variants<KWM, false, SKV, S>(f.frac, f.path, grid, s, q, pm, out, bp, fc, f);
-    if (sk == 1) {
+    if (sk == 3) {
+        if constexpr (S >= 4) {
+            SPCT_SK(3)
+        } else {
+            SPCT_SK(1)
+        }
+    } else if (sk == 1) {
         SPCT_SK(1)
     } else if (sk == 2) {
         SPCT_SK(2)

@@ -842,3 +842,37 @@ def test_joint_tensor_after_slides_bit_exact(P, w, h, bins, band_rows):
         bg.slide(frames[i])
         want = sum(oracle.build_ih(f.astype(np.uint16), bins) for f in frames[i - 2:i + 1])
         assert np.array_equal(bg.joint.padded_u64(), want), i
+
+
+@pytest.mark.parametrize("w,bins,pitch", [(1001, 32, 1008), (1003, 16, 1004), (998, 32, 1000), (1022, 20, 1024)])
+def test_fused_wide_staging_pitched_edges(P, w, bins, pitch):
+    """4- and 8-strip CTAs stage four 8-bit columns per thread from 4-byte aligned rows (SK 3):
+    a pitched frame whose last word straddles the image edge (garbage in the pitch padding)
+    keeps the reference bins, tensor and map."""
+    import ctypes as C
+
+    import torch
+
+    from paper_1711_01656_b200 import _capi as A
+    from paper_1711_01656_b200 import api
+
+    h, kw, kh = 150, 64, 40
+    img = oracle.smooth_image(w, h, 77 + w)
+    buf = np.full((h, pitch), 255, np.uint8)
+    buf[:, :w] = img
+    dev = torch.from_numpy(buf).cuda()
+    qb = oracle.quantize(img, bins)
+    th = _crop_template(qb, bins, (w - kw) // 2, (h - kh) // 3, kw, kh)
+    t = P.IntegralHistogramTensor(w, h, bins)
+    lmap = torch.empty((h, w), dtype=torch.float64, device="cuda")
+    tdev = api._tmpl(th, bins, w, h, kw, kh, 1.0).cuda()
+    src = api._source(A.SRC_GRAY_U8, [dev], w, h, bins, pitch=pitch)
+    ws = C.c_size_t()
+    api.check(A.lib().spct_cu_ih_build_workspace(C.byref(src), t.bin0, t.bins, C.byref(ws)))
+    wbuf = torch.empty(max(ws.value, 256), dtype=torch.uint8, device="cuda")
+    api.check(A.lib().spct_cu_ih_build_match_map(C.byref(src), C.byref(t.desc), api._ptr(tdev), kw, kh, 1.0,
+                                                 A.METRIC_MINKOWSKI, api._ptr(lmap), api._ptr(wbuf), wbuf.numel(),
+                                                 api._stream(None)))
+    torch.cuda.synchronize()
+    assert close(lmap.cpu().numpy(), oracle.hist_match_map_direct(qb, bins, th, kw, kh, 1.0))
+    assert np.array_equal(t.padded_u64(), oracle.build_ih(qb, bins))
