@@ -1122,8 +1122,8 @@ void launch_kw_impl(bool allb, int sk, dim3 grid, cudaStream_t s, const QuantPar
     if (allb) launch_variants<KWM, true, SKV, S>(f.frac, f.path, grid, s, q, pm, out, bp, fc, f);   \
     else launch_variants<KWM, false, SKV, S>(f.frac, f.path, grid, s, q, pm, out, bp, fc, f);
     if (sk == 3) {
-        if constexpr (S >= 4) {
-            SPCT_SK(3)
+        if constexpr (S >= 4) {  // (2- and 1-strip CTAs: 0.97 -> 1.19 / 1.83 -> 1.93 ms measured, the
+            SPCT_SK(3)               // per-thread atomics of four columns lengthen their row)
         } else {
             SPCT_SK(1)
         }
