@@ -58,11 +58,13 @@ __global__ void __launch_bounds__(256) fcarry_tiles_kernel(const __grid_constant
     const bool need_s = need_c && S16;
     if (!need_r && !need_c) return;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    // (16-byte clears: every region is a multiple of 4 words and 16-byte aligned)
+    const uint4 z4 = make_uint4(0, 0, 0, 0);
     if (need_c)
-        for (int i = tid; i < tb * kStrip / 2; i += 256) cnt[i] = 0;
+        for (int i = tid; i < tb * kStrip / 8; i += 256) reinterpret_cast<uint4*>(cnt)[i] = z4;
     if (need_s)
-        for (int i = tid; i < tb * kStrip / 2; i += 256) cs[i] = 0;
-    for (int i = tid; i < 8 * kTileBins; i += 256) rh[i] = 0;
+        for (int i = tid; i < tb * kStrip / 8; i += 256) reinterpret_cast<uint4*>(cs)[i] = z4;
+    for (int i = tid; i < 2 * kTileBins; i += 256) reinterpret_cast<uint4*>(rh)[i] = z4;
     __syncthreads();
     const int y0 = j * band_rows, y1 = min(q.height, y0 + band_rows);
     const int ys = y0 + suf_row0;  // the suffix rows [ys, y1)
@@ -131,23 +133,19 @@ __global__ void __launch_bounds__(256) fcarry_tiles_kernel(const __grid_constant
     if (!need_c) return;
     __syncthreads();
     const int Wp = nstrips * kStrip;
-    for (int i = tid; i < kcn * (kStrip / 4); i += 256) {
-        const int k = i / (kStrip / 4), l = i % (kStrip / 4);  // columns 4 l .. 4 l + 3
-        const uint32_t* ck = cnt + k * (kStrip / 2) + l;
-        const int64_t o = (static_cast<int64_t>(j) * Lb + kc0 + k) * Wp + s * kStrip + 4 * l;
-        *reinterpret_cast<uint2*>(C16 + o) = make_uint2(ck[0], ck[32]);
-        if (need_s) {
-            const uint32_t* cq = cs + k * (kStrip / 2) + l;
-            *reinterpret_cast<uint2*>(S16 + o) = make_uint2(cq[0], cq[32]);
-        }
-    }
-    // band x strip totals, [kl][j][s]
+    // warp w dumps bins w, w + 8, ...: lane l the columns 4 l .. 4 l + 3 of the C16 (and S16)
+    // rows, and the warp's sum of the bin's column counts is its band x strip total,
+    // [kl][j][s] (one REDUX)
     for (int k = warp; k < kcn; k += 8) {
         const uint32_t* ck = cnt + k * (kStrip / 2) + lane;
         const uint32_t p0 = ck[0], p1 = ck[32];
-        uint32_t t = (p0 & 0xFFFFu) + (p0 >> 16) + (p1 & 0xFFFFu) + (p1 >> 16);
-#pragma unroll
-        for (int o = 16; o; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+        const int64_t o = (static_cast<int64_t>(j) * Lb + kc0 + k) * Wp + s * kStrip + 4 * lane;
+        *reinterpret_cast<uint2*>(C16 + o) = make_uint2(p0, p1);
+        if (need_s) {
+            const uint32_t* cq = cs + k * (kStrip / 2) + lane;
+            *reinterpret_cast<uint2*>(S16 + o) = make_uint2(cq[0], cq[32]);
+        }
+        const uint32_t t = __reduce_add_sync(0xffffffffu, (p0 & 0xFFFFu) + (p0 >> 16) + (p1 & 0xFFFFu) + (p1 >> 16));
         if (lane == 0) T1[(static_cast<int64_t>(kc0 + k) * (nbands - 1) + j) * nstrips + s] = t;
     }
 }
