@@ -269,6 +269,17 @@ spct_status build_match(int n, const spct_source* srcs, const spct_ih* outs, con
     // sources 1.. on side streams (sweeps only: carries and prep above are batched launches)
     SidePool* pool = n > 1 && !std::getenv("SPCT_NO_SIDE_STREAMS") ? side_pool() : nullptr;
     std::unique_lock<std::mutex> side_lk;
+    // a side stream forked and not yet joined (an error return in between) is joined on
+    // the way out, so the caller's stream (or graph capture) never leaves one dangling
+    struct JoinOnExit {
+        SidePool* pool = nullptr;
+        cudaStream_t s = nullptr;
+        int open = -1;
+        ~JoinOnExit() {
+            if (open > 0 && cudaEventRecord(pool->join[open], pool->side[open]) == cudaSuccess)
+                cudaStreamWaitEvent(s, pool->join[open], 0);
+        }
+    } joiner{pool, s};
     if (pool) {
         side_lk = std::unique_lock<std::mutex>(pool->mu);
         if (auto st = cuda_status(cudaEventRecord(pool->fork, s), "ih_build_match fork")) return st;
@@ -278,6 +289,7 @@ spct_status build_match(int n, const spct_source* srcs, const spct_ih* outs, con
         if (pool && c > 0) {
             sc = pool->side[c];
             if (auto st = cuda_status(cudaStreamWaitEvent(sc, pool->fork, 0), "ih_build_match fork")) return st;
+            joiner.open = c;
         }
         FusedParams f{};
         f.kw = kw;
@@ -350,6 +362,7 @@ spct_status build_match(int n, const spct_source* srcs, const spct_ih* outs, con
         if (sc != s) {
             if (auto st = cuda_status(cudaEventRecord(pool->join[c], sc), "ih_build_match join")) return st;
             if (auto st = cuda_status(cudaStreamWaitEvent(s, pool->join[c], 0), "ih_build_match join")) return st;
+            joiner.open = -1;
         }
     }
     return SPCT_OK;
