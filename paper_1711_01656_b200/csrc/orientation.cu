@@ -121,6 +121,27 @@ __global__ void __launch_bounds__(kThreads) orientation_tile_kernel(const uint8_
     }
     __syncthreads();
     // hblur (features.cpp:35-41): acc += k_i * in(clamp(x + i), y), i ascending
+    if constexpr (R >= 0) {
+        // lane l takes the consecutive columns 3 l .. 3 l + 2: the 3 + 2R gray values it
+        // needs are converted to double once (not once per tap); same products and sums
+        // in the same order per output
+        constexpr int NV = 3 + 2 * R;
+        for (int ry = warp; ry < nhy; ry += kWarps) {
+            const uint8_t* g = G + ry * gs;
+            const int cb = 3 * lane;
+            if (cb >= nbx) continue;
+            double v[NV];
+#pragma unroll
+            for (int i = 0; i < NV; ++i) v[i] = static_cast<double>(g[min(cb + i, ngx - 1)]);
+#pragma unroll
+            for (int j = 0; j < 3; ++j) {
+                double acc = 0.0;
+#pragma unroll
+                for (int k = 0; k <= 2 * R; ++k) acc = __dadd_rn(acc, __dmul_rn(tap[k], v[j + k]));
+                if (cb + j < nbx) H[ry * kBS + cb + j] = acc;
+            }
+        }
+    } else
     for (int ry = warp; ry < nhy; ry += kWarps) {
         const uint8_t* g = G + ry * gs;
         double acc[3] = {0.0, 0.0, 0.0};
@@ -139,6 +160,28 @@ __global__ void __launch_bounds__(kThreads) orientation_tile_kernel(const uint8_
     }
     __syncthreads();
     // vblur (:43-49): acc += k_i * tmp(x, clamp(y + i)), i ascending
+    if constexpr (R >= 0) {
+        // warp w takes the consecutive output rows [r0, r0 + nr): per column the lane loads
+        // the nr + 2R rows of H it needs once (not 2R + 1 per output row)
+        constexpr int MR = (kTY + 2 + kWarps - 1) / kWarps;  // rows per warp (5 for 34)
+        const int r0 = warp * MR, nr = min(MR, nby - r0);
+        if (nr > 0)
+            for (int j = 0; j < 3; ++j) {
+                const int c = lane + 32 * j;
+                if (c >= nbx) break;
+                double hv[MR + 2 * R];
+#pragma unroll
+                for (int i = 0; i < MR + 2 * R; ++i) hv[i] = i < nr + 2 * R ? H[(r0 + i) * kBS + c] : 0.0;
+#pragma unroll
+                for (int q = 0; q < MR; ++q) {
+                    if (q >= nr) break;
+                    double acc = 0.0;
+#pragma unroll
+                    for (int k = 0; k <= 2 * R; ++k) acc = __dadd_rn(acc, __dmul_rn(tap[k], hv[q + k]));
+                    B[(r0 + q) * kBS + c] = acc;
+                }
+            }
+    } else
     for (int by = warp; by < nby; by += kWarps) {
         double acc[3] = {0.0, 0.0, 0.0};
         int c[3];
