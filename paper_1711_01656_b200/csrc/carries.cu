@@ -1,3 +1,5 @@
+#include <type_traits>
+
 #include "spct_internal.h"
 
 using namespace spct_dev;
@@ -86,11 +88,16 @@ __global__ void __launch_bounds__(256) fcarry_tiles_kernel(const __grid_constant
             for (int c = 0; c < 4; ++c) b[c] = x + c < q.width ? pixel_bin(q, x + c, y) : -1;
         }
     };
-    auto count_row = [&](int y, const int (&b)[4]) {
+    // every bin of the source lands in this chunk (one chunk, the whole histogram): no
+    // per-pixel range check
+    const bool full_range = wide && klo == 0 && khi >= q.nbins;
+    uint8_t* const r8col = R8 + static_cast<int64_t>(s) * q.height * Lb + kc0 + 4 * lane;
+    auto count_row = [&](int y, const int (&b)[4], auto full_tag) {
+        constexpr bool FULL = decltype(full_tag)::value;
 #pragma unroll
         for (int c = 0; c < 4; ++c) {
             const int k = b[c] - klo;
-            if (b[c] >= 0 && static_cast<unsigned>(k) < static_cast<unsigned>(khi)) {
+            if (FULL || (b[c] >= 0 && static_cast<unsigned>(k) < static_cast<unsigned>(khi))) {
                 if (need_c) atomicAdd(&cnt[k * (kStrip / 2) + (c >> 1) * 32 + lane], 1u << (16 * (c & 1)));
                 if (need_s && y >= ys) atomicAdd(&cs[k * (kStrip / 2) + (c >> 1) * 32 + lane], 1u << (16 * (c & 1)));
                 if (need_r) atomicAdd(&rw[k], 1u);
@@ -102,51 +109,60 @@ __global__ void __launch_bounds__(256) fcarry_tiles_kernel(const __grid_constant
                 const uint4 h = *reinterpret_cast<const uint4*>(rw + 4 * lane);
                 *reinterpret_cast<uint4*>(rw + 4 * lane) = make_uint4(0, 0, 0, 0);
                 const uint32_t packed = h.x | (h.y << 8) | (h.z << 16) | (h.w << 24);
-                *reinterpret_cast<uint32_t*>(R8 + (static_cast<int64_t>(s) * q.height + y) * Lb + kc0 + 4 * lane) = packed;
+                *reinterpret_cast<uint32_t*>(r8col + static_cast<int64_t>(y) * Lb) = packed;
             }
             __syncwarp();
         }
     };
     // rows y0 + warp + 8 i; the 8-bit gray words of four rows are loaded before any is counted
     const uint8_t* colp = static_cast<const uint8_t*>(q.p0) + x;
-    int y = y0 + warp;
-    for (; y + 24 < y1; y += 32) {
-        uint32_t w[4] = {0, 0, 0, 0};
-        if (wide) {
+    auto rows = [&](auto full_tag) {
+        int y = y0 + warp;
+        for (; y + 24 < y1; y += 32) {
+            uint32_t w[4] = {0, 0, 0, 0};
+            if (wide) {
 #pragma unroll
-            for (int u = 0; u < 4; ++u)
-                w[u] = __ldg(reinterpret_cast<const uint32_t*>(colp + static_cast<int64_t>(y + 8 * u) * q.pitch));
+                for (int u = 0; u < 4; ++u)
+                    w[u] = __ldg(reinterpret_cast<const uint32_t*>(colp + static_cast<int64_t>(y + 8 * u) * q.pitch));
+            }
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                int b[4];
+                bins4(y + 8 * u, w[u], b);
+                count_row(y + 8 * u, b, full_tag);
+            }
         }
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
+        for (; y < y1; y += 8) {
+            const uint32_t w = wide ? __ldg(reinterpret_cast<const uint32_t*>(colp + static_cast<int64_t>(y) * q.pitch)) : 0u;
             int b[4];
-            bins4(y + 8 * u, w[u], b);
-            count_row(y + 8 * u, b);
+            bins4(y, w, b);
+            count_row(y, b, full_tag);
         }
-    }
-    for (; y < y1; y += 8) {
-        const uint32_t w = wide ? __ldg(reinterpret_cast<const uint32_t*>(colp + static_cast<int64_t>(y) * q.pitch)) : 0u;
-        int b[4];
-        bins4(y, w, b);
-        count_row(y, b);
-    }
+    };
+    if (full_range)
+        rows(std::true_type{});
+    else
+        rows(std::false_type{});
     if (!need_c) return;
     __syncthreads();
     const int Wp = nstrips * kStrip;
     // warp w dumps bins w, w + 8, ...: lane l the columns 4 l .. 4 l + 3 of the C16 (and S16)
     // rows, and the warp's sum of the bin's column counts is its band x strip total,
     // [kl][j][s] (one REDUX)
-    for (int k = warp; k < kcn; k += 8) {
+    const int64_t o0 = (static_cast<int64_t>(j) * Lb + kc0 + warp) * Wp + s * kStrip + 4 * lane, ostep = 8 * static_cast<int64_t>(Wp);
+    uint32_t* t1 = T1 + (static_cast<int64_t>(kc0 + warp) * (nbands - 1) + j) * nstrips + s;
+    const int64_t tstep = 8 * static_cast<int64_t>(nbands - 1) * nstrips;
+    for (int k = warp, i = 0; k < kcn; k += 8, ++i) {
         const uint32_t* ck = cnt + k * (kStrip / 2) + lane;
         const uint32_t p0 = ck[0], p1 = ck[32];
-        const int64_t o = (static_cast<int64_t>(j) * Lb + kc0 + k) * Wp + s * kStrip + 4 * lane;
+        const int64_t o = o0 + i * ostep;
         *reinterpret_cast<uint2*>(C16 + o) = make_uint2(p0, p1);
         if (need_s) {
             const uint32_t* cq = cs + k * (kStrip / 2) + lane;
             *reinterpret_cast<uint2*>(S16 + o) = make_uint2(cq[0], cq[32]);
         }
         const uint32_t t = __reduce_add_sync(0xffffffffu, (p0 & 0xFFFFu) + (p0 >> 16) + (p1 & 0xFFFFu) + (p1 >> 16));
-        if (lane == 0) T1[(static_cast<int64_t>(kc0 + k) * (nbands - 1) + j) * nstrips + s] = t;
+        if (lane == 0) t1[i * tstep] = t;
     }
 }
 
