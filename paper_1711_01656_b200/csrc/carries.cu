@@ -79,10 +79,16 @@ __global__ void __launch_bounds__(256) fcarry_tiles_kernel(const __grid_constant
     // may mix them with BinMaps)
     const bool wide = G8 && q.kind == SPCT_SRC_GRAY_U8 && q.fast_u8 && x + 3 < q.width &&
                       ((reinterpret_cast<uintptr_t>(q.p0) + x) & 3) == 0 && (q.pitch & 3) == 0;
-    auto bins4 = [&](int y, uint32_t w, int (&b)[4]) {
+    // a uint16 BinMap (the orientation channel): four bins per 8-byte load
+    const bool wide16 = !G8 && q.kind == SPCT_SRC_BINS_U16 && x + 3 < q.width &&
+                        ((reinterpret_cast<uintptr_t>(q.p0) + 2 * static_cast<uintptr_t>(x)) & 7) == 0 && (q.pitch & 3) == 0;
+    auto bins4 = [&](int y, uint2 w, int (&b)[4]) {
         if (wide) {
 #pragma unroll
-            for (int c = 0; c < 4; ++c) b[c] = static_cast<int>((((w >> (8 * c)) & 0xFFu) * q.nbins) >> 8);
+            for (int c = 0; c < 4; ++c) b[c] = static_cast<int>((((w.x >> (8 * c)) & 0xFFu) * q.nbins) >> 8);
+        } else if (wide16) {
+#pragma unroll
+            for (int c = 0; c < 4; ++c) b[c] = static_cast<int>(((c < 2 ? w.x : w.y) >> (16 * (c & 1))) & 0xFFFFu);
         } else {
 #pragma unroll
             for (int c = 0; c < 4; ++c) b[c] = x + c < q.width ? pixel_bin(q, x + c, y) : -1;
@@ -116,14 +122,18 @@ __global__ void __launch_bounds__(256) fcarry_tiles_kernel(const __grid_constant
     };
     // rows y0 + warp + 8 i; the 8-bit gray words of four rows are loaded before any is counted
     const uint8_t* colp = static_cast<const uint8_t*>(q.p0) + x;
+    const uint16_t* colp16 = static_cast<const uint16_t*>(q.p0) + x;
     auto rows = [&](auto full_tag) {
         int y = y0 + warp;
         for (; y + 24 < y1; y += 32) {
-            uint32_t w[4] = {0, 0, 0, 0};
+            uint2 w[4] = {};
             if (wide) {
 #pragma unroll
                 for (int u = 0; u < 4; ++u)
-                    w[u] = __ldg(reinterpret_cast<const uint32_t*>(colp + static_cast<int64_t>(y + 8 * u) * q.pitch));
+                    w[u].x = __ldg(reinterpret_cast<const uint32_t*>(colp + static_cast<int64_t>(y + 8 * u) * q.pitch));
+            } else if (wide16) {
+#pragma unroll
+                for (int u = 0; u < 4; ++u) w[u] = __ldg(reinterpret_cast<const uint2*>(colp16 + static_cast<int64_t>(y + 8 * u) * q.pitch));
             }
 #pragma unroll
             for (int u = 0; u < 4; ++u) {
@@ -133,7 +143,9 @@ __global__ void __launch_bounds__(256) fcarry_tiles_kernel(const __grid_constant
             }
         }
         for (; y < y1; y += 8) {
-            const uint32_t w = wide ? __ldg(reinterpret_cast<const uint32_t*>(colp + static_cast<int64_t>(y) * q.pitch)) : 0u;
+            uint2 w = {};
+            if (wide) w.x = __ldg(reinterpret_cast<const uint32_t*>(colp + static_cast<int64_t>(y) * q.pitch));
+            else if (wide16) w = __ldg(reinterpret_cast<const uint2*>(colp16 + static_cast<int64_t>(y) * q.pitch));
             int b[4];
             bins4(y, w, b);
             count_row(y, b, full_tag);
