@@ -84,7 +84,7 @@ struct BuildPlan {
     int strips_per_cta;  // fused sweep: strips side by side in one CTA (grid.x = ceil(nstrips / strips_per_cta))
 };
 BuildPlan plan_build(int width, int height, int bins, int force_B = 0, int ctas_per_sm = 2, int min_band_rows = 32,
-                     int strips_per_cta = 1);
+                     int strips_per_cta = 1, int max_waves = 8, bool prefer_more_bands = false);
 
 // Resident CTAs per SM of the build sweep (B bins per warp, `threads` per CTA) and of the
 // fused sweep; used to size bands in whole waves.  Fall back to 2 without a device.
