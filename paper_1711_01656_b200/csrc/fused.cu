@@ -249,7 +249,9 @@ spct_status build_match(int n, const spct_source* srcs, const spct_ih* outs, con
                        metric == SPCT_METRIC_BHATTACHARYYA || metric == SPCT_METRIC_CHISQ;
     // Bhattacharyya / chi-square in the quarter layout (MODE 4 / 5, packed 16-bit window counts)
     const int quarter = T <= 24576 ? (metric == SPCT_METRIC_BHATTACHARYYA ? 4 : (metric == SPCT_METRIC_CHISQ ? 5 : 0)) : 0;
-    const int path = fast_metric ? 1 : (quarter ? quarter : (f32_ok ? 3 : 0));
+    // p = 2 (kw kh <= 4096): MODE 3's exact integer + FP32 split in the quarter layout (MODE 6)
+    const int p2q = metric == SPCT_METRIC_MINKOWSKI && p == 2.0 && T <= 4096 && !std::getenv("SPCT_P2_MODE3") ? 6 : 0;
+    const int path = fast_metric ? 1 : (quarter ? quarter : (p2q ? p2q : (f32_ok ? 3 : 0)));
     const PrepLayout pl = fused_prep_layout(out->bins);
     PrepBatch pbt{};
     for (int c = 0; c < n; ++c) {

@@ -349,14 +349,17 @@ constexpr size_t smem_bytes_s() {
 // (f32_term below), 4 / 5 = Bhattacharyya / chi-square in the quarter layout of the integer
 // paths: per window and bin sqrt(c) sqrt(t / T), resp. c s / (c + s) (chi-square through
 // (q - t)^2 / (q + t) = q + t - 4 q t / (q + t)), in FP32 (16 windows per lane, four bins per
-// lane, the quarters summed in a fixed order), the warps' partials combined in FP64.
+// lane, the quarters summed in a fixed order), the warps' partials combined in FP64;
+// 6 = p = 2 in the quarter layout: MODE 3's exact int32 part c (32 c - X) and FP32 part c Y
+// per window and bin (kw kh <= 4096).
 template <bool STORE, int MODE, int KWM, bool ALLB, int SK, int S>
 __global__ void __launch_bounds__(256, 2) sweep_match_kernel(QuantParams q, PixelMode pm, spct_ih out, int Lb, int Wp,
                                                              int band_rows, int nstrips, FusedCarries fc,
                                                              FusedParams f) {
     using G = Geo<S>;
     constexpr int NW = G::NW, NWB = G::NWB, NB = G::NB, NT = G::NT, E = G::E, VS = G::VS, CPT = G::CPT;
-    constexpr bool FAST = MODE == 1 || MODE == 2, FRAC = MODE == 2, QF = MODE == 4 || MODE == 5, CHI = MODE == 5;
+    constexpr bool FAST = MODE == 1 || MODE == 2, FRAC = MODE == 2, QF = MODE == 4 || MODE == 5 || MODE == 6, CHI = MODE == 5,
+                   P2Q = MODE == 6;
     extern __shared__ uint4 smem_raw[];
     uint32_t* vc = reinterpret_cast<uint32_t*>(smem_raw);                 // [NB bins][VS words], padded
     // integer paths over part of the histogram (!ALLB): running column counts of the group's
@@ -835,9 +838,13 @@ __global__ void __launch_bounds__(256, 2) sweep_match_kernel(QuantParams q, Pixe
         uint32_t Pf[8] = {0, 0, 0, 0, 0, 0, 0, 0}, pall = 0;
         // MODE 4: the lane's 16 windows' FP32 sums over its four bins
         [[maybe_unused]] float qf[16];
+        [[maybe_unused]] int qi[16];  // MODE 6: the exact integer part of the p = 2 terms
         if (QF)
 #pragma unroll
             for (int i = 0; i < 16; ++i) qf[i] = 0.0f;
+        if (P2Q)
+#pragma unroll
+            for (int i = 0; i < 16; ++i) qi[i] = 0;
         double acc[4] = {0.0, 0.0, 0.0, 0.0};
 #pragma unroll
         for (int g = 0; g < kB / 4; ++g) {
@@ -857,7 +864,13 @@ __global__ void __launch_bounds__(256, 2) sweep_match_kernel(QuantParams q, Pixe
                 for (int j = 0; j < 8; ++j) {
                     const float c0 = __int_as_float(0x4B000000u | (w[j] & 0xFFFFu)) + cfo;
                     const float c1 = __int_as_float(0x4B000000u | (w[j] >> 16)) + cfo;
-                    if (CHI) {  // c s / (c + s); c = s = 0 gives 0 (the reference skips q + t = 0)
+                    if (P2Q) {  // (c - s)^2 as MODE 3: c (32 c - X) exact in int32, c Y in FP32
+                        const int i0 = static_cast<int>(w[j] & 0xFFFFu) + off, i1 = static_cast<int>(w[j] >> 16) + off;
+                        qi[2 * j] += i0 * (32 * i0 - __float_as_int(cst.x));
+                        qi[2 * j + 1] += i1 * (32 * i1 - __float_as_int(cst.x));
+                        qf[2 * j] = fmaf(c0, cst.y, qf[2 * j]);
+                        qf[2 * j + 1] = fmaf(c1, cst.y, qf[2 * j + 1]);
+                    } else if (CHI) {  // c s / (c + s); c = s = 0 gives 0 (the reference skips q + t = 0)
                         qf[2 * j] = fmaf(c0 * cst.w, rcp_approx(c0 + cst.w + 1e-30f), qf[2 * j]);
                         qf[2 * j + 1] = fmaf(c1 * cst.w, rcp_approx(c1 + cst.w + 1e-30f), qf[2 * j + 1]);
                     } else {    // sqrt(c) sqrt(t / T)
@@ -1039,14 +1052,28 @@ __global__ void __launch_bounds__(256, 2) sweep_match_kernel(QuantParams q, Pixe
                 for (int i = 0; i < 8; ++i) {
                     const float snd = hi2 ? qf[i] : qf[i + 8], kp = hi2 ? qf[i + 8] : qf[i];
                     qf[i] = kp + __shfl_xor_sync(0xffffffffu, snd, 16);
+                    if (P2Q) {
+                        const int sn = hi2 ? qi[i] : qi[i + 8], kq = hi2 ? qi[i + 8] : qi[i];
+                        qi[i] = kq + __shfl_xor_sync(0xffffffffu, sn, 16);
+                    }
                 }
 #pragma unroll
                 for (int i = 0; i < 4; ++i) {
                     const float snd = hi1 ? qf[i] : qf[i + 4], kp = hi1 ? qf[i + 4] : qf[i];
                     qf[i] = kp + __shfl_xor_sync(0xffffffffu, snd, 8);
+                    if (P2Q) {
+                        const int sn = hi1 ? qi[i] : qi[i + 4], kq = hi1 ? qi[i + 4] : qi[i];
+                        qi[i] = kq + __shfl_xor_sync(0xffffffffu, sn, 8);
+                    }
                 }
                 double* rb = red + (y & 1) * (NW * kStrip) + warp * kStrip + 16 * mq + 8 * (qq >> 1) + 4 * (qq & 1);
-                if (CHI) {  // the warp's (S_w - 4 Y_w) / T, S_w = sum of s_k over its bins
+                if (P2Q) {  // the warp's (sum c^2 - 2 sum c s + sum s^2) / T^2 (MODE 3's units)
+                    const double s2 = f.c3slab[kl0 / kB].x;
+#pragma unroll
+                    for (int i = 0; i < 4; ++i)
+                        rb[i] = (static_cast<double>(qi[i]) * (1.0 / 32.0) - 2.0 * static_cast<double>(qf[i]) + s2) * f.invT *
+                                f.invT;
+                } else if (CHI) {  // the warp's (S_w - 4 Y_w) / T, S_w = sum of s_k over its bins
                     const double sw = f.c3slab[kl0 / kB].y;
 #pragma unroll
                     for (int i = 0; i < 4; ++i) rb[i] = (sw - 4.0 * static_cast<double>(qf[i])) * f.invT;
@@ -1095,6 +1122,8 @@ void launch_variants(bool frac, int path, dim3 grid, cudaStream_t s, const Quant
             SPCT_GO(true, 4, false)
         } else if (path == 5) {
             SPCT_GO(true, 5, false)
+        } else if (path == 6) {
+            SPCT_GO(true, 6, false)
         } else {
             SPCT_GO(true, 0, false)
         }
@@ -1108,6 +1137,8 @@ void launch_variants(bool frac, int path, dim3 grid, cudaStream_t s, const Quant
             SPCT_GO(false, 4, false)
         } else if (path == 5) {
             SPCT_GO(false, 5, false)
+        } else if (path == 6) {
+            SPCT_GO(false, 6, false)
         } else {
             SPCT_GO(false, 0, false)
         }
